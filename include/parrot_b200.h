@@ -1,0 +1,134 @@
+/*
+ * parrot_b200.h -- C ABI of libparrot_b200.so, the B200 (sm_100a) device-side
+ * hot path of FedML Parrot's simulator.
+ *
+ * The reference (FedML Parrot, `fedsim` 0.1.0, pure Python/NumPy) has no FFI:
+ * its "plugin" boundary is the in-process Python API.  Each
+ * entry point below names the reference function it replaces; the Python
+ * package `paper_2303_01778_b200` binds them through ctypes and presents the
+ * reference's own API (client_execute / local_fold / global_fold /
+ * server_update / StateStore / schedule / DeviceWorker.execute_clients).
+ *
+ * Conventions
+ *  - All buffers are caller-owned device pointers (unless marked HOST); the
+ *    library never allocates on the hot path.  `stream` is a cudaStream_t
+ *    passed as void*; every kernel is asynchronous on it.
+ *  - Return 0 on success, a PB_ERR_* code otherwise; pb_last_error() returns
+ *    the thread-local message of the last failure.
+ *  - Parameter vectors are flat fp32 in the model's canonical order.  A
+ *    "group" is G clients laid out as rows of a [G, stride] matrix.
+ */
+#ifndef PARROT_B200_H
+#define PARROT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_OK 0
+#define PB_ERR_INVALID 1   /* bad argument / unsupported shape  */
+#define PB_ERR_CUDA 2      /* CUDA runtime error                */
+
+const char* pb_last_error(void);
+int pb_version(void);
+int pb_device_sm_count(int device);
+
+/* ---------------------------------------------------------------------------
+ * Host-side scheduling / RNG (native runtime around the kernels)
+ * ------------------------------------------------------------------------- */
+
+/* Greedy min-makespan assignment.  Replaces fedsim/schedule.py:88-126
+ * (_greedy_jit, the numba kernel) and :48-85 (_greedy_core).  sizes_desc are
+ * task sizes already sorted largest-first; assign[i] receives the device of
+ * task i, loads[k] the predicted load of device k.  HOST pointers.  Compiled
+ * with -ffp-contract=off: bit-identical to the reference. */
+int pb_greedy_assign(const double* sizes_desc, int64_t n, const double* t, const double* b,
+                     int64_t k, int64_t* assign, double* loads);
+
+/* Per-client minibatch orders.  Replaces the per-epoch
+ * `default_rng([seed, 6, client, round]).permutation(n)` of
+ * fedsim/trainer.py:445,452-453 (NumPy PCG64 + SeedSequence + Fisher-Yates
+ * with masked rejection, restated bit-exactly).  For client i the output
+ * out[offset[i] + e*n[i] + j] = row_base[i] + perm_e[j], e < epochs.
+ * keys is [g][4] = (seed, stream, client_id, round).  HOST pointers. */
+int pb_minibatch_rows(const uint64_t* keys, const int64_t* n, const int64_t* offset,
+                      const int64_t* row_base, int64_t g, int epochs, int32_t* out,
+                      int threads);
+
+/* ---------------------------------------------------------------------------
+ * (b) fused weighted fold  -- fedsim/aggregate.py:76-102 (local_fold) and
+ *     :130-142 (global_fold's device-order sum)
+ * ------------------------------------------------------------------------- */
+
+/* acc[i] = fma(w, x[i], acc[i]) -- one client folded into a running sum. */
+int pb_fold_f32(float* acc, const float* x, float w, int64_t n, void* stream);
+
+/* acc[i] += sum_{j<g} w[j] * xs[order[j]*x_stride + i], j ascending (plan
+ * order), one pass over acc.  order may be NULL (identity), w may be NULL
+ * (all ones).  The sum is sequential per element, so the result equals g
+ * successive pb_fold_f32 calls bit for bit. */
+int pb_fold_group_f32(float* acc, const float* xs, int64_t x_stride, const int32_t* order,
+                      const float* w, int64_t g, int64_t n, void* stream);
+
+/* out[i] = a*x[i] + b*y[i] + c*z[i]; NULL inputs contribute nothing.  Used by
+ * global_fold's final divide and the plugin server rules
+ * (fedsim/trainer.py:232-234, :280-285, :340-348, :397-407). */
+int pb_lincomb_f32(float* out, const float* x, float a, const float* y, float b,
+                   const float* z, float c, int64_t n, void* stream);
+
+/* Plugin finalize (fedsim/trainer.py:268-278, :325-338, :388-395) for a group:
+ * out[j,i] = s[j]*(a[j,i] - base[i]) + c*cvec[i] + d*dmat[j,i].
+ * cvec/dmat may be NULL. */
+int pb_delta_affine_group(float* out, int64_t out_stride, const float* a, int64_t a_stride,
+                          const float* base, const float* s, const float* cvec, float c,
+                          const float* dmat, int64_t d_stride, float d, int64_t g, int64_t n,
+                          void* stream);
+
+/* ---------------------------------------------------------------------------
+ * (c) client-state gather / scatter -- fedsim/statestore.py:147-210
+ *     (StateStore.load/save) + default_state (fedsim/trainer.py:315-317,
+ *     :376-378): slot < 0 gathers the all-zero default state.
+ * ------------------------------------------------------------------------- */
+int pb_state_gather(float* work, int64_t work_stride, const float* store, int64_t store_stride,
+                    const int32_t* slot, int64_t g, int64_t width, void* stream);
+int pb_state_scatter(float* store, int64_t store_stride, const float* work, int64_t work_stride,
+                     const int32_t* slot, int64_t g, int64_t width, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * (a) batched client training, multinomial logistic regression
+ *     -- fedsim/trainer.py:427-477 (client_execute) with the plugin
+ *     local_gradient hooks (:223, :249-257, :319-323, :380-386) fused in:
+ *     grad = CE grad + mu*(w - w0) + cg*ctrl_g + cc*ctrl_c[client]
+ * One CTA per client; the whole local run (E epochs x ceil(n/bs) steps) stays
+ * on chip.  w layout: W[C][F] row-major then b[C].
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const float* X;          /* [rows, F] fp32, all clients packed           */
+  const int32_t* Y;        /* [rows] labels                                 */
+  const int32_t* order;    /* packed minibatch row ids (pb_minibatch_rows)  */
+  const int64_t* order_off;/* [g] offset of client j's rows in `order`      */
+  const int32_t* n;        /* [g] samples per client                        */
+  const float* w0;         /* [P] start model (the global bundle)           */
+  float* w_out;            /* [g, P] end model per client                   */
+  const float* ctrl_g;     /* [P] shared correction or NULL                 */
+  const float* ctrl_c;     /* [g, ctrl_stride] per-client correction / NULL */
+  int64_t ctrl_stride;
+  double* loss_sum;        /* [g] sum of per-step losses                    */
+  int32_t* steps;          /* [g] steps taken                               */
+  int32_t* nonfinite;      /* [g] first step whose loss was not finite, -1  */
+  int64_t g;
+  int32_t F, C, epochs, batch_size;
+  float lr, mu, prox_loss, cg, cc;
+} pb_lr_train_args;
+int pb_lr_train_group(const pb_lr_train_args* args, void* stream);
+
+/* evaluate (fedsim/trainer.py:148-158): out2[0] += #correct, out2[1] += sum CE */
+int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F, int C, const float* w,
+               double* out2, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARROT_B200_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of libparrot_b200.so (declared in include/parrot_b200.h).
+
+There is no fallback: if the library is missing the import fails loudly, and
+every non-zero return code becomes ``NativeError`` carrying pb_last_error().
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint64, c_void_p
+from pathlib import Path
+
+_PATH = Path(__file__).resolve().parent / "libparrot_b200.so"
+
+
+class NativeError(RuntimeError):
+    """A libparrot_b200 entry point returned an error code."""
+
+
+class LrTrainArgs(ctypes.Structure):
+    _fields_ = [
+        ("X", c_void_p), ("Y", c_void_p), ("order", c_void_p), ("order_off", c_void_p),
+        ("n", c_void_p), ("w0", c_void_p), ("w_out", c_void_p), ("ctrl_g", c_void_p),
+        ("ctrl_c", c_void_p), ("ctrl_stride", c_int64), ("loss_sum", c_void_p),
+        ("steps", c_void_p), ("nonfinite", c_void_p), ("g", c_int64),
+        ("F", c_int32), ("C", c_int32), ("epochs", c_int32), ("batch_size", c_int32),
+        ("lr", c_float), ("mu", c_float), ("prox_loss", c_float), ("cg", c_float),
+        ("cc", c_float),
+    ]
+
+
+_SIGS = {
+    "pb_last_error": (ctypes.c_char_p, []),
+    "pb_version": (c_int, []),
+    "pb_device_sm_count": (c_int, [c_int]),
+    "pb_greedy_assign": (c_int, [POINTER(c_double), c_int64, POINTER(c_double), POINTER(c_double),
+                                 c_int64, POINTER(c_int64), POINTER(c_double)]),
+    "pb_minibatch_rows": (c_int, [POINTER(c_uint64), POINTER(c_int64), POINTER(c_int64),
+                                  POINTER(c_int64), c_int64, c_int, POINTER(c_int32), c_int]),
+    "pb_fold_f32": (c_int, [c_void_p, c_void_p, c_float, c_int64, c_void_p]),
+    "pb_fold_group_f32": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                  c_int64, c_void_p]),
+    "pb_lincomb_f32": (c_int, [c_void_p, c_void_p, c_float, c_void_p, c_float, c_void_p, c_float,
+                               c_int64, c_void_p]),
+    "pb_delta_affine_group": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                                      c_void_p, c_float, c_void_p, c_int64, c_float, c_int64,
+                                      c_int64, c_void_p]),
+    "pb_state_gather": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+                                c_void_p]),
+    "pb_state_scatter": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                 c_int64, c_void_p]),
+    "pb_lr_train_group": (c_int, [POINTER(LrTrainArgs), c_void_p]),
+    "pb_lr_eval": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p,
+                           c_void_p]),
+}
+
+
+class _Lib:
+    def __init__(self, path: Path):
+        if not path.exists():
+            raise ImportError(
+                f"{path} is missing: build it with `python -m paper_2303_01778_b200.build` "
+                "(there is no CPU fallback for the device path)")
+        self._dll = ctypes.CDLL(str(path))
+        self.path = path
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(self._dll, name)
+            fn.restype = res
+            fn.argtypes = args
+            setattr(self, name, fn)
+
+    def exported(self) -> list[str]:
+        return sorted(_SIGS)
+
+    def check(self, rc: int) -> None:
+        if rc != 0:
+            raise NativeError(self.pb_last_error().decode("utf-8", "replace"))
+
+
+lib = _Lib(_PATH)
+
+
+def ptr(t) -> int | None:
+    """Raw device/host address of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_of(t=None) -> int:
+    """The current CUDA stream handle of the tensor's device, as void*."""
+    import torch
+    dev = t.device if t is not None else torch.device("cuda")
+    return torch.cuda.current_stream(dev).cuda_stream

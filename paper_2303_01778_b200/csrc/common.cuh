@@ -1,0 +1,40 @@
+// Shared helpers for libparrot_b200: error plumbing and launch utilities.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "parrot_b200.h"
+
+namespace pb {
+
+void set_error(const std::string& msg);
+
+inline int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(PB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return PB_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Grid size for grid-stride elementwise kernels: enough CTAs to cover n
+// items, capped at a whole number of waves over the SMs.
+int sm_count();
+inline unsigned grid_for(int64_t items, int threads, int waves = 8) {
+  int64_t need = (items + threads - 1) / threads;
+  int64_t cap = int64_t(sm_count()) * waves * (2048 / threads);
+  if (need < 1) need = 1;
+  return unsigned(need < cap ? need : cap);
+}
+
+}  // namespace pb

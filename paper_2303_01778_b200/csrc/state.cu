@@ -1,0 +1,91 @@
+// (c) Client-state gather/scatter between the HBM-resident per-client store
+// [M, width] and a group's working rows [G, width].
+//
+// Reference: StateStore.load/save (fedsim/statestore.py:147-210).  Loading a
+// never-saved client yields default_state(), which for both stateful plugins
+// is all zeros (fedsim/trainer.py:315-317, :376-378): slot < 0 encodes that.
+// The disjoint-client contract of the reference (no client on two devices in
+// one round, fedsim/statestore.py:112-118) is asserted by the host before a
+// scatter, so rows never race.
+//
+// Algorithmic traffic: gather reads store + writes work, scatter reads work +
+// writes store = 16 B per state element per client.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <bool kGather>
+__global__ void __launch_bounds__(kThreads)
+move_rows_vec(float4* __restrict__ dst, int64_t dst_stride4, const float4* __restrict__ src,
+              int64_t src_stride4, const int32_t* __restrict__ slot, int64_t width4) {
+  const int64_t j = blockIdx.y;
+  const int32_t s = slot[j];
+  if (!kGather && s < 0) return;
+  float4* d = kGather ? dst + j * dst_stride4 : dst + int64_t(s) * dst_stride4;
+  const float4* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride4 : nullptr)
+                               : src + j * src_stride4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < width4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = srow ? __ldcs(srow + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __stcs(d + i, v);
+  }
+}
+
+template <bool kGather>
+__global__ void move_rows_scalar(float* __restrict__ dst, int64_t dst_stride,
+                                 const float* __restrict__ src, int64_t src_stride,
+                                 const int32_t* __restrict__ slot, int64_t width) {
+  const int64_t j = blockIdx.y;
+  const int32_t s = slot[j];
+  if (!kGather && s < 0) return;
+  float* d = kGather ? dst + j * dst_stride : dst + int64_t(s) * dst_stride;
+  const float* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride : nullptr)
+                              : src + j * src_stride;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < width;
+       i += int64_t(gridDim.x) * blockDim.x)
+    d[i] = srow ? srow[i] : 0.0f;
+}
+
+template <bool kGather>
+int move_rows(float* dst, int64_t dst_stride, const float* src, int64_t src_stride,
+              const int32_t* slot, int64_t g, int64_t width, void* stream, const char* name) {
+  if (g < 0 || g > 65535 || width < 0 || (g > 0 && width > 0 && (!dst || !src || !slot)))
+    return pb::fail(PB_ERR_INVALID, std::string(name) + ": bad arguments");
+  if (g == 0 || width == 0) return PB_OK;
+  cudaStream_t s = pb::as_stream(stream);
+  // spread each row over enough CTAs that g*gx fills the machine
+  int64_t per_row = (int64_t(pb::sm_count()) * 8 + g - 1) / g;
+  if (width % 4 == 0 && dst_stride % 4 == 0 && src_stride % 4 == 0 && pb::aligned16(dst) &&
+      pb::aligned16(src)) {
+    const int64_t w4 = width / 4;
+    int64_t gx = std::min<int64_t>(per_row, (w4 + kThreads - 1) / kThreads);
+    dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
+    move_rows_vec<kGather><<<grid, kThreads, 0, s>>>(
+        reinterpret_cast<float4*>(dst), dst_stride / 4, reinterpret_cast<const float4*>(src),
+        src_stride / 4, slot, w4);
+  } else {
+    int64_t gx = std::min<int64_t>(per_row, (width + kThreads - 1) / kThreads);
+    dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
+    move_rows_scalar<kGather><<<grid, kThreads, 0, s>>>(dst, dst_stride, src, src_stride, slot,
+                                                         width);
+  }
+  return pb::check_launch(name);
+}
+
+}  // namespace
+
+extern "C" int pb_state_gather(float* work, int64_t work_stride, const float* store,
+                               int64_t store_stride, const int32_t* slot, int64_t g,
+                               int64_t width, void* stream) {
+  return move_rows<true>(work, work_stride, store, store_stride, slot, g, width, stream,
+                         "pb_state_gather");
+}
+
+extern "C" int pb_state_scatter(float* store, int64_t store_stride, const float* work,
+                                int64_t work_stride, const int32_t* slot, int64_t g,
+                                int64_t width, void* stream) {
+  return move_rows<false>(store, store_stride, work, work_stride, slot, g, width, stream,
+                          "pb_state_scatter");
+}

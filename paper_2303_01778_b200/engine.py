@@ -1,0 +1,531 @@
+"""Round driver: select -> fit -> schedule (host, bit-exact) -> batched device
+execution -> hierarchical fold -> server rule -> evaluate.
+
+Reference: ``fedsim/engine.py`` (PARROT branch of ``SimulationEngine.run_round``
+at :748-812 and ``DeviceWorker.execute_clients`` at :470-503, the device seam).
+What changes is the device side:
+
+* the K simulated devices of a process share the GPU; all their clients of a
+  round train in ONE batched launch (``train_group``), then each device's
+  clients are folded into that device's partial in plan order
+  (``fold_group``), which is exactly the reference's sequential
+  load-train-save-fold loop reordered -- legal because a round never places
+  a client on two devices and minibatch order depends only on
+  (seed, client, round);
+* stateful algorithms gather/scatter client state through the HBM store;
+* with ``torch.distributed`` initialised (one process per GPU, NCCL), rank r
+  executes the devices k with k % world == r and the per-device partials are
+  combined with ONE all-reduce of the packed partial (kernel (d)); every rank
+  then applies the same server rule, so the global model stays replicated.
+
+Timing under the virtual clock (default) is the reference's synthetic model
+(``virtual_task_seconds`` + ``report_time``), so fits, plans and device loads
+are bit-identical to the reference's.  The in-process byte channel and wire
+codec of the reference are not rebuilt (NCCL replaces them).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from .aggregate import (DevicePartial, PartialEntry, fold_group, global_fold, partial_byte_roles,
+                        server_update)
+from .core import (STREAM_NOISE, ClientProfile, ConfigError, SimConfig, select_clients,
+                   stream_rng)
+from .estimate import (InsufficientDataError, TimingHistory, TimingRecord, WorkloadFit,
+                       estimation_error, fit_device, record)
+from .metrics import CostLedger, ReplicaGauge
+from .models import ModelSpec, cnn_init, spec_for
+from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
+from .statestore import StateStore
+from .trainer import (AggOp, AlgorithmPlugin, ClientData, ModelParams, NamedParams, ParamBundle,
+                      device, evaluate, finalize_results, spec_of_bundle, train_group)
+
+RESULTS_HEADER = ("round\tscheme\tscheduling\tsim_seconds\twall_seconds\t"
+                  "device_loads\ttrips_up\ttrips_down\tbytes_avg\tbytes_special\t"
+                  "accuracy\tloss\test_error")
+
+
+class DeviceFailureError(RuntimeError):
+    """A device's client execution raised; the round aborts with the cause."""
+
+
+@dataclass(frozen=True)
+class DeviceModel:
+    """fedsim/engine.py:380-403: identity plus injected timing behaviour."""
+
+    device_id: int
+    hetero_ratio: float = 0.0
+    dynamic: bool = False
+    t_true: float = 1e-4
+    b_true: float = 0.0
+    noise: float = 0.0
+
+    def __post_init__(self) -> None:
+        if self.device_id < 0:
+            raise ConfigError("device_id must be >= 0")
+        if self.hetero_ratio < 0:
+            raise ConfigError(f"device {self.device_id}: hetero_ratio must be >= 0")
+        if self.t_true <= 0 or self.b_true < 0 or self.noise < 0:
+            raise ConfigError(f"device {self.device_id}: bad ground-truth timing")
+
+
+def make_device_models(k: int, hetero=0.0, dynamic: bool = False, t_true=1e-4, b_true=0.0,
+                       noise: float = 0.0) -> list[DeviceModel]:
+    def per_device(v, label):
+        if np.isscalar(v):
+            return [float(v)] * k
+        vals = [float(x) for x in v]
+        if len(vals) != k:
+            raise ConfigError(f"{label} needs {k} values, got {len(vals)}")
+        return vals
+
+    het, ts, bs = per_device(hetero, "hetero"), per_device(t_true, "t_true"), per_device(b_true, "b_true")
+    return [DeviceModel(i, het[i], dynamic, ts[i], bs[i], noise) for i in range(k)]
+
+
+def report_time(measured_seconds: float, device: DeviceModel, round_num: int,
+                total_rounds: int) -> float:
+    """measured*(1+eta_k), times (1+cos(3.14 r/R + k)) for dynamic devices, floor 1e-9."""
+    if measured_seconds <= 0:
+        raise ValueError("measured_seconds must be > 0")
+    out = measured_seconds * (1.0 + device.hetero_ratio)
+    if device.dynamic:
+        out *= 1.0 + math.cos(3.14 * round_num / total_rounds + device.device_id)
+    return max(out, 1e-9)
+
+
+def virtual_task_seconds(device: DeviceModel, sample_count: int, seed: int, round_num: int,
+                         client_id: int) -> float:
+    """N*t_true + b_true with optional relative noise from stream 4."""
+    base = sample_count * device.t_true + device.b_true
+    if device.noise > 0:
+        eps = stream_rng(seed, STREAM_NOISE, round_num, device.device_id, client_id).standard_normal()
+        base *= 1.0 + device.noise * eps
+    return max(base, 1e-9)
+
+
+@dataclass
+class RoundOutcome:
+    round: int
+    scheme: str
+    scheduling_mode: str
+    simulated_round_seconds: float
+    wall_seconds: float
+    device_loads: dict
+    costs: CostLedger
+    accuracy: float
+    loss: float
+    estimation_error: float
+    fit_seconds: float
+    schedule_seconds: float
+    new_global: ParamBundle
+    device_seconds: float = 0.0     # GPU time of the round's training launch(es)
+
+
+def append_results(path: str | Path, outcome: RoundOutcome) -> None:
+    path = Path(path)
+    fresh = not path.exists() or path.stat().st_size == 0
+    loads = ",".join(f"{outcome.device_loads[k]:.9g}" for k in sorted(outcome.device_loads))
+    row = "\t".join([str(outcome.round), outcome.scheme, outcome.scheduling_mode,
+                     f"{outcome.simulated_round_seconds:.9g}", f"{outcome.wall_seconds:.9g}",
+                     loads, str(outcome.costs.trips_up), str(outcome.costs.trips_down),
+                     str(outcome.costs.bytes_avg_params), str(outcome.costs.bytes_special_params),
+                     f"{outcome.accuracy:.9g}", f"{outcome.loss:.9g}",
+                     f"{outcome.estimation_error:.9g}"])
+    with open(path, "a", encoding="utf-8") as fh:
+        if fresh:
+            fh.write(RESULTS_HEADER + "\n")
+        fh.write(row + "\n")
+
+
+# ---------------------------------------------------------------------------
+# device runtime (the GPU-resident side of a process)
+# ---------------------------------------------------------------------------
+
+class DeviceRuntime:
+    """Client data, state store and model layout shared by the local devices."""
+
+    def __init__(self, cfg: SimConfig, plugin: AlgorithmPlugin, spec: ModelSpec, data: ClientData,
+                 store: StateStore | None, gauge: ReplicaGauge):
+        self.cfg, self.plugin, self.spec, self.data = cfg, plugin, spec, data
+        self.store, self.gauge = store, gauge
+        self.last_device_seconds = 0.0
+
+    def execute(self, assignments: dict[int, list[int]], bundle: ParamBundle,
+                round_num: int) -> dict[int, DevicePartial]:
+        """Train every assigned client of the local devices in one batched
+        launch, then fold each device's clients in its plan order."""
+        order = [(dev, m) for dev in sorted(assignments) for m in assignments[dev]]
+        partials = {dev: DevicePartial(device_id=dev) for dev in assignments}
+        self.last_device_seconds = 0.0
+        if not order:
+            return partials
+        clients = [m for _, m in order]
+        if len(set(clients)) != len(clients):
+            raise ValueError(f"round {round_num}: a client is assigned twice")
+        plugin, spec = self.plugin, self.spec
+        w0 = bundle.flat(spec)
+        work = None
+        if plugin.is_stateful:
+            if self.store is None:
+                raise ConfigError(f"{plugin.name} is stateful and needs a state store")
+            work = torch.empty(len(clients), spec.numel, device=w0.device)
+            self.store.gather(clients, work)
+        self.gauge.acquire(len(clients))
+        try:
+            go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
+                             self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
+                             round_num)
+        finally:
+            self.gauge.release(len(clients))
+        self.last_device_seconds = go.seconds
+        groups, new_state = finalize_results(plugin, spec, go, w0, bundle, work)
+        if plugin.is_stateful and new_state is not None:
+            self.store.scatter(clients, round_num, new_state)
+        pos = 0
+        for dev in sorted(assignments):
+            k = len(assignments[dev])
+            fold_group(partials[dev], groups, list(range(pos, pos + k)), assignments[dev])
+            pos += k
+        return partials
+
+
+class DeviceWorker:
+    """One simulated device (fedsim/engine.py:453-503): ``execute_clients``
+    trains its clients (batched on the GPU) and folds them in order."""
+
+    def __init__(self, device_model: DeviceModel, cfg: SimConfig, plugin: AlgorithmPlugin,
+                 profiles: Sequence[ClientProfile], store: StateStore | None,
+                 gauge: ReplicaGauge, channel=None, *, runtime: DeviceRuntime | None = None):
+        self.device = device_model
+        self.cfg, self.plugin, self.profiles, self.store, self.gauge = cfg, plugin, profiles, store, gauge
+        self.channel = channel
+        self._runtime = runtime
+
+    def _rt(self, bundle: ParamBundle) -> DeviceRuntime:
+        if self._runtime is None:
+            spec = spec_of_bundle(bundle, self.plugin)
+            data = ClientData.from_profiles(self.profiles, n_classes=spec.n_classes)
+            self._runtime = DeviceRuntime(self.cfg, self.plugin, spec, data, self.store, self.gauge)
+        return self._runtime
+
+    def execute_clients(self, bundle: ParamBundle, clients: Sequence[int],
+                        round_num: int) -> tuple[DevicePartial, list[TimingRecord]]:
+        rt = self._rt(bundle)
+        partial = rt.execute({self.device.device_id: list(clients)}, bundle, round_num)[
+            self.device.device_id]
+        timings = [TimingRecord(self.device.device_id, m, round_num,
+                                int(rt.data.sizes[m]),
+                                self._reported(rt, m, round_num, len(clients)))
+                   for m in clients]
+        return partial, timings
+
+    def _reported(self, rt: DeviceRuntime, m: int, round_num: int, g: int) -> float:
+        if self.cfg.clock == "virtual":
+            measured = virtual_task_seconds(self.device, int(rt.data.sizes[m]), self.cfg.seed,
+                                            round_num, m)
+        else:
+            measured = max(rt.last_device_seconds / max(g, 1), 1e-9)
+        return report_time(measured, self.device, round_num, self.cfg.total_rounds)
+
+
+# ---------------------------------------------------------------------------
+# server loop
+# ---------------------------------------------------------------------------
+
+def result_schema(plugin: AlgorithmPlugin, spec: ModelSpec) -> list[tuple[str, AggOp, tuple]]:
+    """The (name, op, shape) entries every client result carries."""
+    cols = [(n, sh) for n, _, _, sh in spec.columns()]
+    name = plugin.name
+    if name in ("fedavg", "fedprox"):
+        out = [(n, AggOp.WEIGHTED_AVERAGE, sh) for n, sh in cols]
+    elif name == "fednova":
+        out = [("direction_" + n, AggOp.WEIGHTED_AVERAGE, sh) for n, sh in cols]
+        out.append(("step_scale", AggOp.SUM, (1,)))
+    elif name == "scaffold":
+        out = [("delta_" + n, AggOp.WEIGHTED_AVERAGE, sh) for n, sh in cols]
+        out += [("ctrl_delta_" + n, AggOp.SIMPLE_AVERAGE, sh) for n, sh in cols]
+    elif name == "feddyn":
+        out = [(n, AggOp.SIMPLE_AVERAGE, sh) for n, sh in cols]
+    else:
+        raise ValueError(f"no result schema for plugin {name!r}")
+    if plugin.collect_local_loss:
+        out.append(("local_loss", AggOp.COLLECT, (1,)))
+    return out
+
+
+class SimulationEngine:
+    """Server loop with the reference's constructor and outputs
+    (fedsim/engine.py:563-828), executing on the GPU.
+
+    Extra keyword arguments: ``model`` ("lr" default, or "cnn"),
+    ``client_data`` (a prebuilt device ClientData), ``init_seed`` (CNN init),
+    ``eval_batch`` (unused for LR)."""
+
+    def __init__(self, cfg: SimConfig, plugin: AlgorithmPlugin, profiles: Sequence[ClientProfile],
+                 device_models: Sequence[DeviceModel], store: StateStore | None = None,
+                 eval_data=None, results_path: str | Path | None = None, start_round: int = 0,
+                 initial_global: ParamBundle | None = None, history: TimingHistory | None = None,
+                 eval_every: int = 1, *, model: str | None = None,
+                 client_data: ClientData | None = None, init_seed: int = 0):
+        if len(profiles) != cfg.total_clients:
+            raise ConfigError(f"need {cfg.total_clients} client profiles, got {len(profiles)}")
+        if len(device_models) != cfg.num_devices:
+            raise ConfigError(f"scheme {cfg.scheme} with K={cfg.num_devices} needs "
+                              f"{cfg.num_devices} device models, got {len(device_models)}")
+        if [d.device_id for d in device_models] != list(range(cfg.num_devices)):
+            raise ConfigError("device ids must be 0..K-1 in order")
+        if plugin.is_stateful and store is None:
+            raise ConfigError(f"{plugin.name} is stateful and needs a state store")
+        if not 0 <= start_round <= cfg.total_rounds:
+            raise ConfigError(f"start_round {start_round} outside [0, {cfg.total_rounds}]")
+        if cfg.scheme == "FA_DIST" and cfg.clock == "real":
+            raise ConfigError("FA_DIST under the real clock is not supported on the device path")
+        self.cfg, self.plugin = cfg, plugin
+        self.profiles = list(profiles)
+        self.devices = list(device_models)
+        self.store, self.eval_data, self.results_path = store, eval_data, results_path
+        self.eval_every = max(1, eval_every)
+        self.history = history if history is not None else TimingHistory()
+        self.gauge = ReplicaGauge()
+        self.next_round = start_round
+        self.sizes = np.array([p.sample_count for p in self.profiles], dtype=np.int64)
+        self.data = client_data if client_data is not None else ClientData.from_profiles(self.profiles)
+        if initial_global is not None:
+            self.global_bundle = initial_global
+            self.spec = spec_of_bundle(initial_global, plugin if plugin.spec else None)
+            plugin.spec = self.spec
+        else:
+            self.spec = spec_for(model or "lr", self.data.n_features, self.data.n_classes)
+            if self.spec.kind == "lr":
+                start = ModelParams.zeros(self.spec.n_classes, self.spec.n_features)
+            else:
+                start = NamedParams.from_flat(self.spec, cnn_init(self.spec, init_seed))
+            self.global_bundle = plugin.init_global(start)
+        if plugin.is_stateful:
+            names = plugin.state_names(self.spec)
+            store.configure(names, [sh for _, _, _, sh in self.spec.columns()])
+        self._world, self._rank = 1, 0
+        if torch.distributed.is_available() and torch.distributed.is_initialized():
+            self._world = torch.distributed.get_world_size()
+            self._rank = torch.distributed.get_rank()
+            if cfg.clock == "real":
+                raise ConfigError("multi-process runs need the virtual clock (shared histories)")
+        self.local_devices = [k for k in range(cfg.num_devices) if k % self._world == self._rank]
+        self.runtime = DeviceRuntime(cfg, plugin, self.spec, self.data, store, self.gauge)
+        if cfg.scheme == "PARROT" and cfg.scheduling in ("full-history", "time-window"):
+            warm_jit()
+
+    # -- per-round pieces -------------------------------------------------------
+    def _fit_all(self, round_num: int):
+        if self.cfg.scheduling not in ("full-history", "time-window") \
+                or round_num <= self.cfg.warmup_rounds:
+            return None, 0.0
+        window = self.cfg.time_window if self.cfg.scheduling == "time-window" else "all-history"
+        t0 = time.perf_counter()
+        fits: dict[int, WorkloadFit | None] = {}
+        for k in range(self.cfg.num_devices):
+            try:
+                fits[k] = fit_device(self.history, k, window, round_num)
+            except InsufficientDataError:
+                fits[k] = None
+        return fits, time.perf_counter() - t0
+
+    def _reported(self, dev: int, m: int, round_num: int, measured: float | None = None) -> float:
+        d = self.devices[dev]
+        if measured is None:
+            measured = virtual_task_seconds(d, int(self.sizes[m]), self.cfg.seed, round_num, m)
+        return report_time(measured, d, round_num, self.cfg.total_rounds)
+
+    def _fa_tasks(self, round_num: int, selected: Sequence[int]):
+        """FA_DIST work pulling under the virtual clock (fedsim/engine.py:699-746):
+        returns [(device, client)] in completion (= fold) order."""
+        k = self.cfg.num_devices
+        pending = list(selected)
+        clocks = {d: 0.0 for d in range(k)}
+        busy: dict[int, tuple[float, int]] = {}
+        done = []
+        idx = 0
+        for d in range(min(k, len(pending))):
+            busy[d] = (clocks[d] + self._reported(d, pending[idx], round_num), pending[idx])
+            idx += 1
+        while busy:
+            d = min(busy, key=lambda x: (busy[x][0], x))
+            t_end, m = busy.pop(d)
+            clocks[d] = t_end
+            done.append((d, m))
+            if idx < len(pending):
+                busy[d] = (clocks[d] + self._reported(d, pending[idx], round_num), pending[idx])
+                idx += 1
+        return done
+
+    def _reduce_partials(self, partials: list[DevicePartial], schema) -> list[DevicePartial]:
+        """Multi-process: sum this rank's partials (device order) and all-reduce
+        the packed buffer over NCCL; returns one combined partial."""
+        dist = torch.distributed
+        d = device()
+        local = DevicePartial(device_id=self._rank)
+        live = [p for p in partials if p.entries]
+        accs, meta = [], []
+        for name, op, shape in schema:
+            if op is AggOp.COLLECT:
+                continue
+            acc = torch.zeros(shape, device=d)
+            wsum, cnt = 0.0, 0
+            for p in live:
+                pe = p.entries.get(name)
+                if pe is not None:
+                    from . import _kernels as K
+                    K.fold(acc.view(-1), pe.acc.view(-1), 1.0)
+                    wsum += pe.weight_sum
+                    cnt += pe.count
+            accs.append(acc.view(-1))
+            meta += [wsum, float(cnt)]
+        packed = torch.cat(accs) if accs else torch.zeros(0, device=d)
+        meta_t = torch.tensor(meta, dtype=torch.float64, device=d)
+        dist.all_reduce(packed)
+        dist.all_reduce(meta_t)
+        meta_h = meta_t.cpu().numpy()
+        pos, mi = 0, 0
+        for name, op, shape in schema:
+            if op is AggOp.COLLECT:
+                continue
+            size = int(np.prod(shape))
+            local.entries[name] = PartialEntry(op=op, acc=packed[pos:pos + size].view(shape),
+                                               weight_sum=float(meta_h[mi]),
+                                               count=int(round(meta_h[mi + 1])))
+            pos += size
+            mi += 2
+        collects = [(name, [it for p in live for it in p.entries[name].collected])
+                    for name, op, _ in schema if op is AggOp.COLLECT and any(name in p.entries for p in live)]
+        host_collects = {n: [(c, t.detach().cpu()) for c, t in items] for n, items in collects}
+        gathered = [None] * self._world
+        dist.all_gather_object(gathered, (host_collects, [c for p in live for c in p.clients_folded]))
+        for name, op, _ in schema:
+            if op is not AggOp.COLLECT:
+                continue
+            items = [(c, t.to(d)) for g in gathered for c, t in g[0].get(name, [])]
+            local.entries[name] = PartialEntry(op=op, collected=items, count=len(items))
+        local.clients_folded = [c for g in gathered for c in g[1]]
+        return [local]
+
+    # -- the round ----------------------------------------------------------------
+    def run_round(self, round_num: int) -> RoundOutcome:
+        wall0 = time.perf_counter()
+        cfg = self.cfg
+        selection = select_clients(cfg, round_num)
+        sizes = {m: int(self.sizes[m]) for m in selection.selected}
+        fits, fit_seconds = self._fit_all(round_num)
+        t0 = time.perf_counter()
+        fa_tasks = None
+        if cfg.scheme in ("SP", "SD_DIST"):
+            plan = uniform_division(round_num, selection, cfg.num_devices)
+        elif cfg.scheme == "PARROT":
+            plan = schedule(round_num, selection, fits, sizes, cfg)
+        else:
+            plan = RoundPlan(round=round_num, assignments={}, predicted_loads={},
+                             mode="work-pulling")
+            fa_tasks = self._fa_tasks(round_num, selection.selected)
+        schedule_seconds = time.perf_counter() - t0
+
+        ledger = CostLedger(round=round_num, scheme=cfg.scheme)
+        schema = result_schema(self.plugin, self.spec)
+        try:
+            if fa_tasks is not None:
+                # one task per partial, folded in completion order
+                mine = [(i, dev, m) for i, (dev, m) in enumerate(fa_tasks)
+                        if dev % self._world == self._rank]
+                assign = {i: [m] for i, _, m in mine}
+                got = self.runtime.execute(assign, self.global_bundle, round_num)
+                partials = [got[i] for i, _, _ in mine]
+                task_devs = [dev for dev, _ in fa_tasks]
+            else:
+                assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
+                got = self.runtime.execute(assign, self.global_bundle, round_num)
+                partials = [got[k] for k in self.local_devices]
+                task_devs = list(range(cfg.num_devices))
+        except Exception as exc:
+            raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
+
+        # timing records: device order, plan order (fedsim/engine.py:689-697)
+        if fa_tasks is not None:
+            for dev, m in fa_tasks:
+                record(self.history, TimingRecord(dev, m, round_num, sizes[m],
+                                                  self._reported(dev, m, round_num)))
+        else:
+            for dev in range(cfg.num_devices):
+                for m in plan.assignments.get(dev, []):
+                    measured = None
+                    if cfg.clock == "real":
+                        g = max(len(selection.selected), 1)
+                        measured = max(self.runtime.last_device_seconds / g, 1e-9)
+                    record(self.history, TimingRecord(dev, m, round_num, sizes[m],
+                                                      self._reported(dev, m, round_num, measured)))
+
+        if self._world > 1:
+            partials = self._reduce_partials(partials, schema)
+        agg = global_fold(partials)
+        new_global = server_update(self.plugin, self.global_bundle, agg)
+        self.global_bundle = new_global
+
+        # communication ledger at the reference's 8 B/element convention
+        if cfg.scheme != "SP":
+            avg_elems = sum(int(np.prod(sh)) for _, op, sh in schema if op is not AggOp.COLLECT)
+            coll_elems = sum(int(np.prod(sh)) for _, op, sh in schema if op is AggOp.COLLECT)
+            if fa_tasks is not None:
+                uploads = [[m] for _, m in fa_tasks]
+            else:
+                uploads = [plan.assignments.get(k, []) for k in range(cfg.num_devices)]
+            for clients in uploads:
+                ledger.add_downlink()
+                ledger.add_uplink(8 * avg_elems if clients else 0, 8 * coll_elems * len(clients))
+
+        loads = {dev: 0.0 for dev in range(cfg.num_devices)}
+        for rec in self.history.round_records(round_num):
+            loads[rec.device_id] += rec.reported_seconds
+        sim_seconds = max(loads.values()) + cfg.trip_overhead_seconds * (
+            ledger.trips_up + ledger.trips_down)
+        est_err = float("nan")
+        if fits is not None and plan.mode == MODE_GREEDY:
+            est_err = estimation_error(self.history, fits, round_num)
+        accuracy = loss = float("nan")
+        if self.eval_data is not None and (round_num % self.eval_every == 0
+                                           or round_num == cfg.total_rounds - 1):
+            accuracy, loss = evaluate(self.global_model(), self.eval_data)
+        ledger.peak_live_model_replicas = self.gauge.peak
+        if self.store is not None:
+            ledger.state_bytes_disk = self.store.stats().bytes_on_disk
+        outcome = RoundOutcome(round=round_num, scheme=cfg.scheme, scheduling_mode=plan.mode,
+                               simulated_round_seconds=sim_seconds,
+                               wall_seconds=time.perf_counter() - wall0, device_loads=loads,
+                               costs=ledger, accuracy=accuracy, loss=loss,
+                               estimation_error=est_err, fit_seconds=fit_seconds,
+                               schedule_seconds=schedule_seconds, new_global=new_global,
+                               device_seconds=self.runtime.last_device_seconds)
+        if self.results_path is not None and self._rank == 0:
+            append_results(self.results_path, outcome)
+        return outcome
+
+    def global_model(self):
+        if self.spec.kind == "lr":
+            return self.global_bundle.model()
+        return NamedParams(self.spec, self.global_bundle.named_model(self.spec))
+
+    def run(self, rounds: int | None = None) -> list[RoundOutcome]:
+        remaining = self.cfg.total_rounds - self.next_round
+        count = remaining if rounds is None else min(rounds, remaining)
+        out = []
+        for _ in range(count):
+            out.append(self.run_round(self.next_round))
+            self.next_round += 1
+        if self.store is not None:
+            self.store.flush()
+        return out

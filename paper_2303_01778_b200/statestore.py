@@ -1,0 +1,397 @@
+"""Client state manager: an HBM-resident per-client store with an optional
+FSST on-disk tier.
+
+Reference: ``fedsim/statestore.py`` (one fsynced file per client, loaded
+before and saved after each task).  Here the primary copy of every client's
+state is a row of a device matrix ``[slots, width]`` (fp32), moved to and
+from a group's working rows by the gather/scatter kernels
+(``pb_state_gather`` / ``pb_state_scatter``, csrc/state.cu) -- kernel (c) of
+the north star.  The disk tier keeps the reference's byte format
+(``client_%08d.state``: 28-byte little-endian header, magic ``FSST``,
+version 1, client, round, payload length, CRC-32; tensor-map payload of
+float64 data), so stores written by either implementation are readable by
+the other.  Semantics kept: never-saved clients load the default (all-zero)
+state at round -1, saves must strictly increase the round (StaleWriteError),
+CRC/magic failures raise CorruptRecordError, peak checked-out states are
+tracked.
+
+persist="sync"  -- every save also writes + fsyncs the file (reference
+                   durability; slow: one file per client per round);
+persist="async" -- files are written by a background thread, ``flush()``
+                   waits for them;
+persist="none"  -- HBM only (the bench's mode); ``flush_to_disk()`` can still
+                   spill everything on demand.
+"""
+
+from __future__ import annotations
+
+import os
+import queue
+import struct
+import threading
+import zlib
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Callable, Mapping, Sequence
+
+import numpy as np
+import torch
+
+MAGIC = b"FSST"
+VERSION = 1
+_HEADER = struct.Struct("<4sHHIIQI")
+
+
+class StaleWriteError(RuntimeError):
+    """A save went backwards (or sideways) in rounds."""
+
+
+class CorruptRecordError(RuntimeError):
+    """Magic/version/checksum mismatch on a state file."""
+
+
+@dataclass(frozen=True)
+class ClientState:
+    client_id: int
+    round_written: int
+    payload: dict
+
+
+@dataclass(frozen=True)
+class StateStoreStats:
+    bytes_on_disk: int
+    live_cache_entries: int
+    loads: int
+    saves: int
+    peak_live_entries: int
+
+
+def encode_tensor_map(payload: Mapping[str, object]) -> bytes:
+    """u32 count; per entry u16 name len, name, u8 ndim, u64 dims, f64 data."""
+    out = bytearray(struct.pack("<I", len(payload)))
+    for name, t in payload.items():
+        arr = _host_f64(t)
+        raw = name.encode("utf-8")
+        out += struct.pack("<H", len(raw)) + raw + struct.pack("<B", arr.ndim)
+        out += struct.pack(f"<{arr.ndim}Q", *arr.shape) + arr.tobytes()
+    return bytes(out)
+
+
+def decode_tensor_map(blob: bytes, offset: int = 0) -> tuple[dict[str, np.ndarray], int]:
+    (count,) = struct.unpack_from("<I", blob, offset)
+    pos = offset + 4
+    out: dict[str, np.ndarray] = {}
+    for _ in range(count):
+        (ln,) = struct.unpack_from("<H", blob, pos)
+        name = blob[pos + 2: pos + 2 + ln].decode("utf-8")
+        pos += 2 + ln
+        ndim = blob[pos]
+        pos += 1
+        shape = struct.unpack_from(f"<{ndim}Q", blob, pos)
+        pos += 8 * ndim
+        size = int(np.prod(shape, dtype=np.int64)) if ndim else 1
+        out[name] = np.frombuffer(blob, dtype="<f8", count=size, offset=pos).reshape(shape).copy()
+        pos += 8 * size
+    return out, pos
+
+
+def tensor_map_data_bytes(payload: Mapping[str, object]) -> int:
+    return sum(8 * int(np.asarray(_host_f64(t)).size) for t in payload.values())
+
+
+def _host_f64(t) -> np.ndarray:
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().double().numpy()
+    return np.asarray(t, dtype="<f8")
+
+
+class StateStore:
+    """Per-client state, HBM-resident, optionally mirrored to FSST files."""
+
+    def __init__(self, root: str | Path | None = None, persist: str | None = None,
+                 device: torch.device | None = None):
+        if persist is None:
+            persist = "sync" if root is not None else "none"
+        if persist not in ("sync", "async", "none"):
+            raise ValueError(f"persist must be sync|async|none, got {persist!r}")
+        if persist != "none" and root is None:
+            raise ValueError("a persisting store needs a root directory")
+        self.root = Path(root) if root is not None else None
+        self.persist = persist
+        self._device = device
+        self._lock = threading.Lock()
+        self._last_round: dict[int, int] = {}
+        self._loads = 0
+        self._saves = 0
+        self._live: set[int] = set()
+        self._peak_live = 0
+        self._slot: dict[int, int] = {}
+        self._rows: torch.Tensor | None = None
+        self._schema: list[tuple[str, tuple[int, ...]]] | None = None
+        self._width = 0
+        self._queue: "queue.Queue | None" = None
+        self._writer: threading.Thread | None = None
+        self._writer_error: BaseException | None = None
+        if self.root is not None:
+            self.root.mkdir(parents=True, exist_ok=True)
+            for path in self.root.glob("client_*.state"):
+                cid, rnd, _, _ = self._read_header(path)
+                self._last_round[cid] = rnd
+
+    # -- helpers --------------------------------------------------------------
+    def _dev(self) -> torch.device:
+        if self._device is None:
+            self._device = torch.device("cuda", torch.cuda.current_device())
+        return self._device
+
+    def _path(self, client_id: int) -> Path:
+        return self.root / f"client_{client_id:08d}.state"
+
+    @staticmethod
+    def _read_header(path: Path) -> tuple[int, int, int, int]:
+        with open(path, "rb") as fh:
+            head = fh.read(_HEADER.size)
+        if len(head) != _HEADER.size:
+            raise CorruptRecordError(f"{path}: truncated header")
+        magic, version, _, cid, rnd, length, crc = _HEADER.unpack(head)
+        if magic != MAGIC or version != VERSION:
+            raise CorruptRecordError(f"{path}: bad magic or version")
+        return cid, rnd, length, crc
+
+    def _read_file(self, client_id: int) -> tuple[int, dict[str, np.ndarray]]:
+        path = self._path(client_id)
+        cid, rnd, length, crc = self._read_header(path)
+        if cid != client_id:
+            raise CorruptRecordError(f"{path}: header claims client {cid}")
+        with open(path, "rb") as fh:
+            fh.seek(_HEADER.size)
+            blob = fh.read(length)
+        if len(blob) != length or zlib.crc32(blob) != crc:
+            raise CorruptRecordError(f"{path}: payload checksum mismatch")
+        return rnd, decode_tensor_map(blob)[0]
+
+    def _has_file(self, client_id: int) -> bool:
+        return self.root is not None and self._path(client_id).exists()
+
+    def _set_schema(self, payload: Mapping[str, object]) -> None:
+        schema = [(n, tuple(np.shape(t) if not isinstance(t, torch.Tensor) else t.shape))
+                  for n, t in payload.items()]
+        if self._schema is None:
+            self._schema = schema
+            self._width = int(sum(int(np.prod(s, dtype=np.int64)) if s else 1 for _, s in schema))
+        elif [n for n, _ in schema] != [n for n, _ in self._schema]:
+            raise ValueError("state payload schema changed between saves")
+
+    def configure(self, names: Sequence[str], shapes: Sequence[tuple[int, ...]]) -> None:
+        """Declare the payload layout up front (the engine does this)."""
+        self._set_schema({n: np.zeros(s, dtype=np.float32) for n, s in zip(names, shapes)})
+
+    def _ensure_rows(self, need: int) -> None:
+        cap = 0 if self._rows is None else self._rows.shape[0]
+        if need <= cap:
+            return
+        new_cap = max(need, 2 * cap, 64)
+        rows = torch.zeros(new_cap, self._width, device=self._dev())
+        if self._rows is not None:
+            rows[:cap].copy_(self._rows)
+        self._rows = rows
+
+    def _slot_for(self, client_id: int) -> int:
+        s = self._slot.get(client_id)
+        if s is None:
+            s = len(self._slot)
+            self._slot[client_id] = s
+            self._ensure_rows(s + 1)
+        return s
+
+    def _flat(self, payload: Mapping[str, object]) -> torch.Tensor:
+        parts = []
+        for n, shape in self._schema:
+            t = payload[n]
+            t = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.asarray(t, np.float32))
+            parts.append(t.to(self._dev(), torch.float32).reshape(-1))
+        return torch.cat(parts)
+
+    def _unflat(self, row: torch.Tensor) -> dict[str, torch.Tensor]:
+        out, pos = {}, 0
+        for n, shape in self._schema:
+            size = int(np.prod(shape, dtype=np.int64)) if shape else 1
+            out[n] = row[pos:pos + size].view(shape)
+            pos += size
+        return out
+
+    def _track_checkout(self, client_id: int) -> None:
+        self._live.add(client_id)
+        self._peak_live = max(self._peak_live, len(self._live))
+
+    def _page_in(self, client_id: int) -> None:
+        """Disk tier -> HBM row (CRC-checked)."""
+        _, payload = self._read_file(client_id)
+        self._set_schema(payload)
+        s = self._slot_for(client_id)
+        self._rows[s].copy_(self._flat(payload))
+
+    # -- reference API ----------------------------------------------------------
+    def load(self, client_id: int,
+             default_factory: Callable[[], Mapping[str, object]] | None = None) -> ClientState | None:
+        if client_id not in self._slot and self._has_file(client_id):
+            self._page_in(client_id)
+        if client_id not in self._slot:
+            if default_factory is None:
+                return None
+            with self._lock:
+                self._track_checkout(client_id)
+            return ClientState(client_id, -1, dict(default_factory()))
+        row = self._rows[self._slot[client_id]].clone()
+        with self._lock:
+            self._loads += 1
+            self._track_checkout(client_id)
+        return ClientState(client_id, self._last_round[client_id], self._unflat(row))
+
+    def save(self, client_id: int, round_num: int, payload: Mapping[str, object]) -> None:
+        self._check_rounds([client_id], round_num)
+        self._set_schema(payload)
+        s = self._slot_for(client_id)
+        self._rows[s].copy_(self._flat(payload))
+        self._commit([client_id], round_num, rows=self._rows[s:s + 1])
+
+    def stats(self) -> StateStoreStats:
+        self.flush()
+        with self._lock:
+            disk = sum(p.stat().st_size for p in self.root.glob("client_*.state")) \
+                if self.root is not None else 0
+            return StateStoreStats(bytes_on_disk=disk, live_cache_entries=len(self._live),
+                                   loads=self._loads, saves=self._saves,
+                                   peak_live_entries=self._peak_live)
+
+    # -- device fast path -------------------------------------------------------
+    def gather(self, client_ids: Sequence[int], work: torch.Tensor) -> None:
+        """Load the listed clients' states into work rows [G, width] (zeros for
+        never-saved clients) with one gather kernel."""
+        from . import _kernels as K
+        for c in client_ids:
+            if c not in self._slot and self._has_file(c):
+                self._page_in(c)
+        slots = np.array([self._slot.get(int(c), -1) for c in client_ids], dtype=np.int32)
+        with self._lock:
+            self._loads += int((slots >= 0).sum())
+            for c in client_ids:
+                self._track_checkout(int(c))
+        if self._rows is None:
+            work.zero_()
+            return
+        slot_d = torch.from_numpy(slots).to(work.device)
+        K.state_gather(work, self._rows, slot_d)
+
+    def scatter(self, client_ids: Sequence[int], round_num: int, work: torch.Tensor) -> None:
+        """Persist the group's new states (rows of ``work``) for ``round_num``."""
+        from . import _kernels as K
+        ids = [int(c) for c in client_ids]
+        if len(set(ids)) != len(ids):
+            raise ValueError("a client appears twice in one scatter (disjoint-client contract)")
+        self._check_rounds(ids, round_num)
+        if self._schema is None:
+            raise ValueError("state store schema unknown; call configure() first")
+        slots = np.array([self._slot_for(c) for c in ids], dtype=np.int32)
+        K.state_scatter(self._rows, work, torch.from_numpy(slots).to(work.device))
+        self._commit(ids, round_num, rows=work)
+
+    # -- commit / persistence -----------------------------------------------------
+    def _check_rounds(self, ids: Sequence[int], round_num: int) -> None:
+        with self._lock:
+            for c in ids:
+                prev = self._last_round.get(c, -1)
+                if round_num <= prev:
+                    raise StaleWriteError(
+                        f"client {c}: save at round {round_num} after round {prev}")
+
+    def _commit(self, ids: Sequence[int], round_num: int, rows: torch.Tensor) -> None:
+        if self.persist != "none":
+            host = rows.detach().to("cpu", torch.float64).numpy()
+            jobs = [(c, round_num, host[j]) for j, c in enumerate(ids)]
+            if self.persist == "sync":
+                for job in jobs:
+                    self._write_file(*job)
+            else:
+                self._start_writer()
+                for job in jobs:
+                    self._queue.put(job)
+        with self._lock:
+            for c in ids:
+                self._last_round[c] = round_num
+                self._live.discard(c)
+            self._saves += len(ids)
+
+    def _write_file(self, client_id: int, round_num: int, row: np.ndarray) -> None:
+        payload, pos = {}, 0
+        for n, shape in self._schema:
+            size = int(np.prod(shape, dtype=np.int64)) if shape else 1
+            payload[n] = row[pos:pos + size].reshape(shape)
+            pos += size
+        blob = encode_tensor_map(payload)
+        head = _HEADER.pack(MAGIC, VERSION, 0, client_id, round_num, len(blob), zlib.crc32(blob))
+        path = self._path(client_id)
+        tmp = path.with_suffix(".tmp")
+        fd = os.open(tmp, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+        try:
+            os.write(fd, head + blob)
+            os.fsync(fd)
+        finally:
+            os.close(fd)
+        os.replace(tmp, path)
+        dfd = os.open(self.root, os.O_RDONLY)
+        try:
+            os.fsync(dfd)
+        finally:
+            os.close(dfd)
+
+    def _start_writer(self) -> None:
+        if self._writer is not None:
+            return
+        self._queue = queue.Queue()
+
+        def run():
+            while True:
+                job = self._queue.get()
+                try:
+                    if job is None:
+                        return
+                    self._write_file(*job)
+                except BaseException as exc:  # surfaced by flush()
+                    self._writer_error = exc
+                finally:
+                    self._queue.task_done()
+
+        self._writer = threading.Thread(target=run, name="fsst-writer", daemon=True)
+        self._writer.start()
+
+    def flush(self) -> None:
+        """Wait for write-behind files (persist='async')."""
+        if self._queue is not None:
+            self._queue.join()
+        if self._writer_error is not None:
+            err, self._writer_error = self._writer_error, None
+            raise err
+
+    def flush_to_disk(self, root: str | Path | None = None) -> None:
+        """Spill every HBM-resident state to FSST files (any persist mode)."""
+        if root is not None:
+            self.root = Path(root)
+            self.root.mkdir(parents=True, exist_ok=True)
+        if self.root is None:
+            raise ValueError("no root directory to flush to")
+        if self._rows is None:
+            return
+        host = self._rows.detach().to("cpu", torch.float64).numpy()
+        for c, s in self._slot.items():
+            self._write_file(c, self._last_round[c], host[s])
+
+    def hbm_bytes(self) -> int:
+        return 0 if self._rows is None else self._rows.numel() * 4
+
+    def close(self) -> None:
+        self.flush()
+        if self._writer is not None:
+            self._queue.put(None)
+            self._writer.join()
+            self._writer = None
