@@ -621,17 +621,20 @@ def client_execute(plugin: AlgorithmPlugin, client: ClientProfile, global_bundle
 # evaluation
 # ---------------------------------------------------------------------------
 
-_EVAL_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_EVAL_CACHE: dict = {}
 
 
 def _eval_tensors(ds):
-    hit = _EVAL_CACHE.get(ds)
-    if hit is None:
+    """Device copy of an eval set, uploaded once per dataset object."""
+    hit = _EVAL_CACHE.get(id(ds))
+    if hit is None or hit[0]() is not ds:
         d = device()
-        hit = (torch.from_numpy(np.asarray(ds.features, dtype=np.float32)).to(d),
+        hit = (weakref.ref(ds),
+               torch.from_numpy(np.asarray(ds.features, dtype=np.float32)).to(d),
                torch.from_numpy(np.asarray(ds.labels, dtype=np.int32)).to(d))
-        _EVAL_CACHE[ds] = hit
-    return hit
+        _EVAL_CACHE[id(ds)] = hit
+        weakref.finalize(ds, _EVAL_CACHE.pop, id(ds), None)
+    return hit[1], hit[2]
 
 
 def evaluate(model, ds) -> tuple[float, float]:

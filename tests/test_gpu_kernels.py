@@ -29,7 +29,7 @@ def test_fold_matches_numpy_fma(K, n):
     x = rng.standard_normal(n).astype(np.float32)
     acc = dev(acc0)
     K.fold(acc, dev(x), 3.0)
-    want = (np.float64(acc0) + 3.0 * np.float64(x)).astype(np.float32)  # single rounding == fma
+    want = (acc0.astype(np.float64) + 3.0 * x.astype(np.float64)).astype(np.float32)  # one rounding == fma
     assert np.array_equal(host(acc), want)
 
 
@@ -47,8 +47,9 @@ def test_fold_group_equals_sequential_folds(K, g, n):
     for j in range(g):
         K.fold(ref, X[int(order[j])].contiguous(), float(w[j]))
     assert np.array_equal(host(acc), host(ref))
-    want = (w[:, None].astype(np.float64) * xs[order].astype(np.float64)).sum(0)
-    assert np.allclose(host(acc), want, rtol=1e-5, atol=1e-3)
+    terms = w[:, None].astype(np.float64) * xs[order].astype(np.float64)
+    bound = 1e-6 * g * np.abs(terms).sum(0)  # fp32 sequential-sum error bound (loose)
+    assert np.all(np.abs(host(acc) - terms.sum(0)) <= bound + 1e-6)
 
 
 def test_fold_group_column_slice(K):
