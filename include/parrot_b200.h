@@ -128,6 +128,67 @@ int pb_lr_train_group(const pb_lr_train_args* args, void* stream);
 int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F, int C, const float* w,
                double* out2, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * (a) batched client training, 2-layer FEMNIST CNN (BASELINE config 2; the
+ *     reference has no CNN -- semantics follow client_execute,
+ *     fedsim/trainer.py:427-477).  Parameters: flat fp32 per client in the
+ *     layout of models.py:cnn_spec.  All active clients advance one SGD step
+ *     per sweep; conv2 forward/dgrad/wgrad run on tcgen05 (bf16 operands,
+ *     fp32 TMEM accumulation), the rest in fp32.  Workspace buffers are
+ *     caller-allocated, sized per slot (= client) for BS samples:
+ *       ws_slots 16 B, ws_p1 BS*21504 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
+ *       ws_am2 BS*3136 B, ws_h/ws_dh BS*512 f32, ws_dp2 BS*3136 f32,
+ *       ws_dz BS*43008 B, ws_dp1 BS*6272 f32.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const float* X;           /* [rows, 784] fp32 images                        */
+  const int32_t* Y;         /* [rows] labels                                  */
+  const int32_t* order;     /* packed minibatch row ids                       */
+  const int64_t* order_off; /* [g] per client                                 */
+  const int32_t* n;         /* [g] samples per client                         */
+  const int32_t* rank;      /* [g] slot -> client row, by step count desc     */
+  const int32_t* active;    /* HOST [sweeps]: clients still stepping per sweep*/
+  int32_t sweeps;
+  float* w;                 /* [g, P] params (start = w0), updated in place   */
+  const float* w0;          /* [P]                                            */
+  const float* ctrl_g;      /* [P] or NULL                                    */
+  const float* ctrl_c;      /* [g, ctrl_stride] or NULL                       */
+  int64_t ctrl_stride;
+  double* loss_sum;         /* [g] (zero-initialised by the caller)           */
+  int32_t* steps;           /* [g] (zero-initialised)                         */
+  int32_t* bad;             /* [g] (-1 initialised): step of a non-finite loss*/
+  void* ws_slots;
+  uint8_t* ws_p1;
+  uint8_t* ws_am1;
+  float* ws_p2;
+  uint8_t* ws_am2;
+  float* ws_h;
+  float* ws_dh;
+  float* ws_dp2;
+  uint8_t* ws_dz;
+  float* ws_dp1;
+  int64_t g;
+  int32_t C, BS, batch_size, epochs, samples_per_cta;
+  float lr, mu, cg, cc;
+} pb_cnn_train_args;
+int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
+
+/* Forward-only evaluation of parameter row 0 of args->w on `rows` samples
+ * (order = row ids); out2[0] += #correct, out2[1] += sum CE.  args->g is the
+ * workspace capacity in slots of BS samples. */
+int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------- */
+/* One M x N x K bf16 tcgen05 GEMM D = A * B^T (A [M,K], B [N,K] row-major
+ * bf16; D [128,N] fp32 receives all 128 TMEM lanes) through the canonical
+ * SWIZZLE_NONE shared-memory layouts; *_mode: 0 K-major, 1 MN-major,
+ * 2 K-major "planes" starting `shift` rows in.  Pins the descriptor
+ * conventions the conv kernels use (tests only). */
+int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K, int a_mode,
+                     int b_mode, int shift, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

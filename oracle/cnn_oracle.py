@@ -1,0 +1,136 @@
+"""TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+torch-CPU restatement of ``client_execute`` (fedsim/trainer.py:427-477) for
+the 2-layer FEMNIST CNN of BASELINE config 2.  The reference has no CNN, so
+this oracle is restatement-pinned: it reuses the LR oracle's bit-exact
+minibatch orders (fedsim_oracle.minibatch_orders, pinned to the reference's
+own permutations) and follows the loop exactly -- per-epoch permutation,
+partial last batch kept, mean cross-entropy per batch, ``w -= lr * g`` with
+the plain gradient (FedAvg), steps = E * ceil(n / bs), result weight = N_m.
+The flat parameter layout is the product's (models.py cnn_spec, NHWC
+conv weights and NHWC flatten order for fc1); this module converts.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from .fedsim_oracle import minibatch_orders
+
+NAMES = ("conv1_w", "conv1_b", "conv2_w", "conv2_b", "fc1_w", "fc1_b", "fc2_w", "fc2_b")
+
+
+def shapes(n_classes: int):
+    return ((32, 5, 5, 1), (32,), (64, 5, 5, 32), (64,), (512, 3136), (512,), (n_classes, 512),
+            (n_classes,))
+
+
+def unflatten(flat, n_classes: int, dtype=torch.float64) -> list[torch.Tensor]:
+    flat = torch.as_tensor(np.asarray(flat), dtype=dtype)
+    out, pos = [], 0
+    for shp in shapes(n_classes):
+        size = int(np.prod(shp))
+        out.append(flat[pos:pos + size].reshape(shp).clone())
+        pos += size
+    return out
+
+
+def flatten(params) -> np.ndarray:
+    return torch.cat([p.detach().reshape(-1) for p in params]).numpy()
+
+
+class _RoundValue(torch.autograd.Function):
+    """bf16-round the value, pass the gradient through (device operand staging)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.to(torch.bfloat16).to(x.dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+class _RoundGrad(torch.autograd.Function):
+    """Identity forward; bf16-round the incoming gradient (the device stages
+    dL/dz2 as bf16 for the conv2 dgrad and wgrad tensor-core GEMMs)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.to(torch.bfloat16).to(g.dtype)
+
+
+def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor:
+    """x [B, 784] -> logits; conv weights are NHWC ([co, ky, kx, ci]).
+
+    emulate_bf16=True rounds exactly the operands the device feeds to its
+    tcgen05 conv2 GEMMs (p1 and W2 in the forward, dL/dz2 in both backward
+    GEMMs); everything else stays in the oracle's precision.  Used to check the
+    kernels' arithmetic separately from bf16's effect on the trajectory."""
+    c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
+    h = x.reshape(-1, 1, 28, 28)
+    h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
+    if emulate_bf16:
+        z = F.conv2d(_RoundValue.apply(h), _RoundValue.apply(c2w).permute(0, 3, 1, 2), padding=2)
+        h = F.max_pool2d(F.relu(_RoundGrad.apply(z) + c2b.view(1, -1, 1, 1)), 2)
+    else:
+        h = F.max_pool2d(F.relu(F.conv2d(h, c2w.permute(0, 3, 1, 2), c2b, padding=2)), 2)
+    h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)  # NHWC flatten
+    h = F.relu(h @ f1w.t() + f1b)
+    return h @ f2w.t() + f2b
+
+
+def client_train(flat_w0, X: np.ndarray, y: np.ndarray, client_id: int, seed: int, rnd: int,
+                 epochs: int, batch_size: int, lr: float, n_classes: int,
+                 dtype=torch.float64, emulate_bf16: bool = False):
+    """Returns (flat end parameters, steps, mean per-step loss)."""
+    params = [p.requires_grad_(True) for p in unflatten(flat_w0, n_classes, dtype)]
+    Xt = torch.as_tensor(np.asarray(X), dtype=dtype)
+    yt = torch.as_tensor(np.asarray(y), dtype=torch.long)
+    n = len(y)
+    bs = n if batch_size <= 0 else min(batch_size, n)
+    steps, loss_sum = 0, 0.0
+    for order in minibatch_orders(seed, client_id, rnd, n, epochs):
+        for lo in range(0, n, bs):
+            idx = torch.as_tensor(order[lo:lo + bs])
+            loss = F.cross_entropy(forward(params, Xt[idx], emulate_bf16), yt[idx])
+            grads = torch.autograd.grad(loss, params)
+            with torch.no_grad():
+                for p, g in zip(params, grads):
+                    p -= lr * g
+            loss_sum += float(loss.detach())
+            steps += 1
+    return flatten(params), steps, loss_sum / steps
+
+
+def evaluate(flat, X: np.ndarray, y: np.ndarray, n_classes: int, dtype=torch.float64):
+    params = unflatten(flat, n_classes, dtype)
+    with torch.no_grad():
+        z = forward(params, torch.as_tensor(np.asarray(X), dtype=dtype))
+        yt = torch.as_tensor(np.asarray(y), dtype=torch.long)
+        acc = float((z.argmax(1) == yt).double().mean())
+        loss = float(F.cross_entropy(z, yt))
+    return acc, loss
+
+
+def fedavg_round(flat_global, data: dict, selected, seed: int, rnd: int, epochs: int,
+                 batch_size: int, lr: float, n_classes: int, dtype=torch.float64,
+                 emulate_bf16: bool = False):
+    """One SP FedAvg round (fedsim/engine.py:748-812 semantics): every selected
+    client trains from the global model, the server adopts the
+    sample-weighted average."""
+    acc = np.zeros_like(np.asarray(flat_global, dtype=np.float64))
+    wsum = 0.0
+    for m in selected:
+        X, y = data[m]
+        w, _, _ = client_train(flat_global, X, y, m, seed, rnd, epochs, batch_size, lr, n_classes,
+                               dtype, emulate_bf16)
+        acc += len(y) * np.asarray(w, dtype=np.float64)
+        wsum += len(y)
+    return acc / wsum

@@ -1,0 +1,122 @@
+"""Host side of the CNN path: workspace management and argument marshalling
+for ``pb_cnn_train_group`` / ``pb_cnn_eval`` (csrc/cnn.cu)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from ._lib import CnnTrainArgs, lib, ptr, stream_of
+from .models import ModelSpec
+
+# bytes per sample of each workspace buffer (include/parrot_b200.h)
+_PER_SAMPLE = {"p1": 21504, "am1": 6272, "p2": 3136 * 4, "am2": 3136, "h": 512 * 4, "dh": 512 * 4,
+               "dp2": 3136 * 4, "dz": 43008, "dp1": 6272 * 4}
+MAX_BATCH = 32
+
+
+class _Workspace:
+    def __init__(self):
+        self.slots = 0
+        self.bs = 0
+        self.buf: dict[str, torch.Tensor] = {}
+
+    def get(self, slots: int, bs: int, device) -> dict[str, torch.Tensor]:
+        if slots > self.slots or bs > self.bs or (self.buf and self.buf["slots"].device != device):
+            self.buf = {}
+            torch.cuda.empty_cache()
+            self.slots, self.bs = max(slots, self.slots), max(bs, self.bs)
+            n = self.slots * self.bs
+            self.buf = {k: torch.empty(n * v, dtype=torch.uint8, device=device)
+                        for k, v in _PER_SAMPLE.items()}
+            self.buf["slots"] = torch.empty(self.slots * 16, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = _Workspace()
+
+
+def _samples_per_cta() -> int:
+    return int(os.environ.get("PB_CNN_SPB", "10"))
+
+
+def _fill(args: CnnTrainArgs, ws: dict, slots: int, BS: int) -> None:
+    args.ws_slots = ptr(ws["slots"])
+    for k in ("p1", "am1", "p2", "am2", "h", "dh", "dp2", "dz", "dp1"):
+        setattr(args, "ws_" + k, ptr(ws[k]))
+    args.g = slots
+    args.BS = BS
+    args.samples_per_cta = _samples_per_cta()
+
+
+def sweep_plan(n: np.ndarray, batch_size: int, epochs: int):
+    """Per-client step counts, slot order (most steps first) and the number
+    of clients still stepping in each sweep."""
+    bs = n.copy() if batch_size <= 0 else np.minimum(batch_size, n)
+    total = epochs * ((n + bs - 1) // bs)
+    rank = np.argsort(-total, kind="stable").astype(np.int32)
+    sweeps = int(total.max()) if len(total) else 0
+    active = np.array([(total > s).sum() for s in range(sweeps)], dtype=np.int32)
+    return int(bs.max()) if len(bs) else 0, total, rank, active
+
+
+def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, bad, *,
+                    spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
+                    state_work) -> None:
+    G = len(n)
+    BS, _, rank, active = sweep_plan(n, batch_size, epochs)
+    if BS > MAX_BATCH:
+        raise ValueError(f"the CNN path supports minibatches of up to {MAX_BATCH} samples, got {BS}")
+    d = w_out.device
+    w_out.copy_(w0.view(1, -1).expand(G, -1))
+    loss.zero_()
+    steps.zero_()
+    bad.fill_(-1)
+    rank_d = torch.from_numpy(rank).to(d)
+    n_d = torch.from_numpy(n.astype(np.int32)).to(d)
+    ws = _WS.get(G, BS, d)
+    a = CnnTrainArgs()
+    a.X, a.Y, a.order, a.order_off, a.n, a.rank = (ptr(data.X), ptr(data.Y), ptr(rows_d),
+                                                    ptr(off_d), ptr(n_d), ptr(rank_d))
+    a.active = active.ctypes.data
+    a.sweeps = len(active)
+    a.w, a.w0 = ptr(w_out), ptr(w0)
+    a.ctrl_g = ptr(terms.get("ctrl_g"))
+    ctrl_c = state_work if terms.get("ctrl_c") else None
+    a.ctrl_c = ptr(ctrl_c)
+    a.ctrl_stride = ctrl_c.stride(0) if ctrl_c is not None else 0
+    a.loss_sum, a.steps, a.bad = ptr(loss), ptr(steps), ptr(bad)
+    _fill(a, ws, G, BS)
+    a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
+    a.lr, a.mu = lr, terms.get("mu", 0.0)
+    a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)
+    lib.check(lib.pb_cnn_train_group(ctypes.byref(a), stream_of(w_out)))
+
+
+_EVAL_ORDER: dict = {}
+
+
+def cnn_evaluate(model, X: torch.Tensor, Y: torch.Tensor) -> tuple[float, float]:
+    spec = model.spec
+    rows = int(Y.numel())
+    w = torch.cat([model.tensors[n].reshape(-1) for n in spec.names]).contiguous()
+    key = (rows, X.device)
+    order = _EVAL_ORDER.get(key)
+    if order is None:
+        order = torch.arange(rows, dtype=torch.int32, device=X.device)
+        _EVAL_ORDER[key] = order
+    BS = MAX_BATCH
+    slots = min((rows + BS - 1) // BS, 1024)
+    ws = _WS.get(slots, BS, X.device)
+    a = CnnTrainArgs()
+    a.X, a.Y, a.order = ptr(X), ptr(Y), ptr(order)
+    a.w = a.w0 = ptr(w)
+    _fill(a, ws, slots, BS)
+    a.C, a.batch_size, a.epochs = spec.n_classes, BS, 1
+    out = torch.zeros(2, dtype=torch.float64, device=X.device)
+    lib.check(lib.pb_cnn_eval(ctypes.byref(a), rows, ptr(out), stream_of(w)))
+    correct, loss = out.cpu().tolist()
+    return correct / rows, loss / rows

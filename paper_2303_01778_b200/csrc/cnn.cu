@@ -1,0 +1,856 @@
+// (a) Batched client training for the 2-layer FEMNIST CNN (BASELINE config 2):
+//   conv5x5(1->32)+relu+maxpool2 -> conv5x5(32->64)+relu+maxpool2
+//   -> fc(3136->512)+relu -> fc(512->C) -> softmax CE, 'same' padding.
+// The reference has no CNN; the local-training semantics
+// follow client_execute (fedsim/trainer.py:427-477): per-epoch permutation,
+// partial last batch, mean CE per batch, plain SGD w -= lr*g (+ the fused
+// plugin terms mu*(w - w0) + cg*ctrl_g + cc*ctrl_c as in lr_train.cu).
+//
+// Execution: every active client of the group advances one SGD step per
+// "step sweep"; a sweep is 7 launches over the active slots (clients sorted
+// by step count, so the active set is a prefix):
+//   k_slots      minibatch bookkeeping for the sweep
+//   k_fwd        conv1 (SIMT) + conv2 on tcgen05 (implicit GEMM: the A
+//                operand is the padded p1 image itself, one shifted
+//                descriptor per filter tap; B = the client's bf16 weights) +
+//                bias/relu/maxpool epilogue from TMEM
+//   k_fc1_fwd    fc1 + relu (per-client weights, fp32)
+//   k_head       fc2, softmax-CE loss, dlogits, fc2 grads + update, dH
+//   k_fc1_bwd    fc1 dgrad + wgrad + update in one pass over the weights
+//   k_bwd_conv   pool2/relu backward, conv2 dgrad on tcgen05 (flipped taps,
+//                the same weight tile read MN-major)
+//   k_wgrad      conv2 wgrad on tcgen05 (M=64 x N=32 per tap, K = output
+//                positions) + update; conv1 wgrad/biases (SIMT) + update
+// Operands are bf16 with fp32 accumulation in TMEM; master weights, biases,
+// losses and all non-GEMM math are fp32 (loss reduction in double).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace {
+
+using namespace pb::umma;
+
+// ---- model geometry --------------------------------------------------------
+constexpr int kImg = 28, kC1 = 32, kC2 = 64, kH1 = 512, kFlat = 7 * 7 * kC2;  // 3136
+constexpr int kP1 = 14 * 14 * kC1;   // 6272 pooled conv1 outputs
+constexpr int kG = 18;               // padded 14x14 grid width (2-pixel border)
+constexpr int kRows = 336;           // plane rows (>= 256 + 4*18 + 4 = 332)
+constexpr int kPlane = kRows * 16;   // bytes per plane (8 channels x bf16)
+constexpr int kP1Bytes = 4 * kPlane;   // p1 image, 4 channel planes
+constexpr int kDzBytes = 8 * kPlane;   // dz2 image, 8 channel planes
+constexpr int kW2Bytes = 25 * 4 * 1024;  // conv2 weights in the UMMA B layout
+// flat parameter offsets (models.py cnn_spec)
+constexpr int64_t oC1W = 0, oC1B = 800, oC2W = 832, oC2B = 832 + 51200, oF1W = oC2B + 64,
+                  oF1B = oF1W + int64_t(kH1) * kFlat, oF2W = oF1B + kH1;
+
+struct Slot {
+  int32_t r;        // group row (parameter row / per-client outputs)
+  int32_t cnt;      // samples in this step's batch (0 = inactive)
+  int64_t row_off;  // offset of the batch's row ids in `order`
+};
+
+struct Args {
+  const float* X;
+  const int32_t* Y;
+  const int32_t* order;
+  const int64_t* order_off;
+  const int32_t* n;
+  const int32_t* rank;
+  float* w;               // [G, P] parameters, updated in place
+  const float* w0;        // [P] start model (prox term)
+  const float* ctrl_g;    // [P] or null
+  const float* ctrl_c;    // [G, ctrl_stride] or null
+  int64_t ctrl_stride;
+  double* loss_sum;
+  int32_t* steps;
+  int32_t* bad;
+  // workspace, slot-major with BS samples per slot
+  Slot* slots;
+  uint8_t* p1g;    // [slots*BS, kP1Bytes]  bf16 planes
+  uint8_t* am1;    // [slots*BS, kP1]
+  float* p2;       // [slots*BS, kFlat]
+  uint8_t* am2;    // [slots*BS, kFlat]
+  float* h;        // [slots*BS, kH1]
+  float* dh;       // [slots*BS, kH1]
+  float* dp2;      // [slots*BS, kFlat]
+  uint8_t* dzg;    // [slots*BS, kDzBytes] bf16 planes
+  float* dp1;      // [slots*BS, kP1]
+  double* eval;    // [2] correct, loss (eval mode)
+  int64_t P;
+  int32_t C, BS, bs, epochs, step;
+  float lr, mu, cg, cc;
+};
+
+__device__ __forceinline__ float sgd(const Args& a, int r, int64_t idx, float w, float g) {
+  if (a.mu != 0.0f) g = fmaf(a.mu, w - a.w0[idx], g);
+  if (a.ctrl_g) g = fmaf(a.cg, a.ctrl_g[idx], g);
+  if (a.ctrl_c) g = fmaf(a.cc, a.ctrl_c[int64_t(r) * a.ctrl_stride + idx], g);
+  return fmaf(-a.lr, g, w);
+}
+
+__device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j) * BS + i; }
+
+// NaN-propagating relu / max (torch semantics; fmaxf would drop a NaN and
+// hide a diverged client from the non-finite check)
+__device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
+__device__ __forceinline__ bool takes_max(float z, float best) { return z > best || z != z; }
+
+__device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
+  // UMMA B layout, K-major over (tap, ci): core matrix = 8 co x 8 ci
+  return uint32_t((tap * 4 + (ci >> 3)) * 1024 + (co >> 3) * 128 + (co & 7) * 16 + (ci & 7) * 2);
+}
+
+__device__ void stage_w2(uint8_t* sW2, const float* W, int tid, int nthreads) {
+  const float* w2 = W + oC2W;
+  for (int e = tid; e < 64 * 800; e += nthreads) {
+    const int co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
+    *reinterpret_cast<__nv_bfloat16*>(sW2 + w2_off(co, tap, ci)) = __float2bfloat16(w2[e]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_slots: one thread per active slot -> (row, batch size, row-id offset)
+// ---------------------------------------------------------------------------
+__global__ void k_slots(Args a, int active) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= active) return;
+  const int r = a.rank[j];
+  const int n = a.n[r];
+  const int bs = a.bs <= 0 ? n : min(a.bs, n);
+  const int nb = (n + bs - 1) / bs;
+  const int e = a.step / nb, b = a.step - e * nb;
+  Slot s;
+  s.r = r;
+  s.cnt = (e < a.epochs && a.bad[r] < 0) ? min(bs, n - b * bs) : 0;
+  s.row_off = a.order_off[r] + int64_t(e) * n + int64_t(b) * bs;
+  a.slots[j] = s;
+}
+
+// ---------------------------------------------------------------------------
+// k_fwd: conv1 (SIMT) -> p1 planes -> conv2 (tcgen05) -> relu/pool epilogue
+// grid (active, ceil(BS/spb)), 256 threads
+// ---------------------------------------------------------------------------
+constexpr int kFwdThreads = 256;
+constexpr int kZStride = 65;  // padded fp32 row of the conv2 output tile
+constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + (1024 + 832 + 64) * 4;
+
+__global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
+  const Slot sl = a.slots[blockIdx.x];
+  const int i0 = blockIdx.y * spb, i1 = min(sl.cnt, i0 + spb);
+  if (i0 >= i1) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  uint8_t* sW2 = smem;
+  uint8_t* sPl = sW2 + kW2Bytes;
+  float* sZ = reinterpret_cast<float*>(sPl + kP1Bytes);
+  float* sX = sZ + 256 * kZStride;
+  float* sW1 = sX + 1024;
+  float* sB2 = sW1 + 832;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const float* W = a.w + int64_t(sl.r) * a.P;
+
+  stage_w2(sW2, W, tid, kFwdThreads);
+  for (int e = tid; e < 832; e += kFwdThreads) sW1[e] = W[oC1W + e];
+  for (int e = tid; e < 64; e += kFwdThreads) sB2[e] = W[oC2B + e];
+  for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads)
+    reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<128>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = idesc_bf16(128, 64);
+  uint32_t phase = 0;
+
+  // conv1 weights of this thread's output channel live in registers
+  const int c1 = lane;
+  float wr[25];
+#pragma unroll
+  for (int t = 0; t < 25; ++t) wr[t] = sW1[c1 * 25 + t];
+  const float b1 = sW1[800 + c1];
+
+  for (int i = i0; i < i1; ++i) {
+    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+    for (int e = tid; e < 1024; e += kFwdThreads) {
+      const int yy = e >> 5, xx = e & 31;
+      sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+    }
+    __syncthreads();
+    // conv1 + relu + maxpool2 (warp = pooled position, lane = channel)
+    uint8_t* am1 = a.am1 + sid * kP1;
+    for (int pp = warp; pp < 196; pp += kFwdThreads / 32) {
+      const int py = pp / 14, px = pp - py * 14;
+      float win[6][6];
+#pragma unroll
+      for (int u = 0; u < 6; ++u)
+#pragma unroll
+        for (int v = 0; v < 6; ++v) win[u][v] = sX[(2 * py + u) * 32 + 2 * px + v];
+      float best = -INFINITY;
+      int arg = 0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const int dy = d >> 1, dx = d & 1;
+        float z = b1;
+#pragma unroll
+        for (int ky = 0; ky < 5; ++ky)
+#pragma unroll
+          for (int kx = 0; kx < 5; ++kx) z = fmaf(win[dy + ky][dx + kx], wr[ky * 5 + kx], z);
+        if (takes_max(z, best) && best == best) {
+          best = z;
+          arg = d;
+        }
+      }
+      const float v = relu_nan(best);
+      *reinterpret_cast<__nv_bfloat16*>(sPl + (c1 >> 3) * kPlane +
+                                        ((py + 2) * kG + px + 2) * 16 + (c1 & 7) * 2) =
+          __float2bfloat16(v);
+      am1[pp * kC1 + c1] = uint8_t(arg);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const uint32_t pa = smem_u32(sPl), pw = smem_u32(sW2);
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t)
+#pragma unroll 1
+        for (int tap = 0; tap < 25; ++tap) {
+          const int ky = tap / 5, kx = tap - ky * 5;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint64_t ad = desc(pa + (t * 128 + ky * kG + kx) * 16 + 2 * hh * kPlane, kPlane, 128);
+            const uint64_t bd = desc(pw + (tap * 4 + 2 * hh) * 1024, 1024, 128);
+            mma_bf16(tmem + t * 64, ad, bd, idesc, tap > 0 || hh > 0);
+          }
+        }
+      commit(&mbar);
+    }
+    // p1 image to global for the backward kernels (overlaps the MMAs)
+    {
+      uint4* dst = reinterpret_cast<uint4*>(a.p1g + sid * kP1Bytes);
+      const uint4* src = reinterpret_cast<const uint4*>(sPl);
+      for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) dst[e] = src[e];
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    fence_after_sync();
+    {
+      const int q = warp & 3, half = warp >> 2;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int row = t * 128 + q * 32 + lane;
+        float v[16];
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + half * 32 + c16 * 16), v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int co = half * 32 + c16 * 16 + k;
+            sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
+          }
+        }
+      }
+    }
+    fence_before_sync();
+    __syncthreads();
+    float* p2 = a.p2 + sid * kFlat;
+    uint8_t* am2 = a.am2 + sid * kFlat;
+    for (int o = tid; o < kFlat; o += kFwdThreads) {
+      const int pp = o >> 6, co = o & 63;
+      const int py = pp / 7, px = pp - py * 7;
+      const int r0 = (2 * py) * kG + 2 * px;
+      const int rows[4] = {r0, r0 + 1, r0 + kG, r0 + kG + 1};
+      float best = -INFINITY;
+      int arg = 0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const float z = sZ[rows[d] * kZStride + co];
+        if (takes_max(z, best) && best == best) {
+          best = z;
+          arg = d;
+        }
+      }
+      p2[o] = best;
+      am2[o] = uint8_t(arg);
+    }
+    __syncthreads();
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<128>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// k_fc1_fwd: h = relu(p2 W1^T + b1); grid (active, 512/64), 256 threads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fc1_fwd(Args a) {
+  const Slot sl = a.slots[blockIdx.x];
+  if (sl.cnt == 0) return;
+  __shared__ float sW[64][33];
+  __shared__ float sA[32][33];
+  const int tid = threadIdx.x;
+  const int o0 = blockIdx.y * 64;
+  const float* W1 = a.w + int64_t(sl.r) * a.P + oF1W;
+  const float* p2 = a.p2 + sidx(blockIdx.x, 0, a.BS) * kFlat;
+  const int ol = tid & 63, ig = tid >> 6;  // 4 sample groups
+  const int nper = (sl.cnt + 3) / 4;
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+  for (int k0 = 0; k0 < kFlat; k0 += 32) {
+    for (int e = tid; e < 64 * 32; e += 256) {
+      const int r = e >> 5, c = e & 31;
+      sW[r][c] = W1[int64_t(o0 + r) * kFlat + k0 + c];
+    }
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int r = e >> 5, c = e & 31;
+      sA[r][c] = r < sl.cnt ? p2[int64_t(r) * kFlat + k0 + c] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 32; ++kk) {
+      const float w = sW[ol][kk];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < nper) acc[k] = fmaf(sA[ig + 4 * k][kk], w, acc[k]);
+    }
+    __syncthreads();
+  }
+  const float b = a.w[int64_t(sl.r) * a.P + oF1B + o0 + ol];
+  for (int k = 0; k < nper; ++k) {
+    const int i = ig + 4 * k;
+    if (i < sl.cnt) a.h[sidx(blockIdx.x, i, a.BS) * kH1 + o0 + ol] = relu_nan(acc[k] + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_head: fc2 + softmax CE + fc2 backward/update + dH; grid (active), 256 thr
+// (also the eval head when a.eval != null)
+// ---------------------------------------------------------------------------
+constexpr int kHeadThreads = 256;
+
+__device__ double block_sum_d(double v, double* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) t += scratch[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
+  const Slot sl = a.slots[blockIdx.x];
+  if (sl.cnt == 0) return;
+  extern __shared__ float hs[];
+  const int C = a.C, cnt = sl.cnt, tid = threadIdx.x;
+  float* sW = hs;                      // [C][512] fc2 weights
+  float* sH = sW + C * kH1;            // [cnt][512]
+  float* sL = sH + cnt * kH1;          // [cnt][C] logits -> dlogits
+  __shared__ double scratch[kHeadThreads / 32];
+  __shared__ int s_bad;
+  float* W = a.w + int64_t(sl.r) * a.P;
+  for (int e = tid; e < C * kH1; e += kHeadThreads) sW[e] = W[oF2W + e];
+  const float* hrow = a.h + sidx(blockIdx.x, 0, a.BS) * kH1;
+  for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
+  __syncthreads();
+  const float* b2 = W + oF2W + int64_t(C) * kH1;
+  for (int p = tid; p < cnt * C; p += kHeadThreads) {
+    const int i = p / C, c = p - i * C;
+    const float* hr = sH + i * kH1;
+    const float* wc = sW + c * kH1;
+    float s = 0.0f;
+    // rotate the start by c so lanes (consecutive c) hit different banks
+    for (int oo = 0; oo < kH1; ++oo) {
+      const int o = (oo + c) & (kH1 - 1);
+      s = fmaf(hr[o], wc[o], s);
+    }
+    sL[p] = s + b2[c];
+  }
+  __syncthreads();
+  double lpart = 0.0, cpart = 0.0;
+  const float inv = 1.0f / float(cnt);
+  if (tid < cnt) {
+    float* z = sL + tid * C;
+    const int y = a.Y[a.order[sl.row_off + tid]];
+    float m = z[0];
+    int best = 0;
+    for (int c = 1; c < C; ++c)
+      if (z[c] > m) {
+        m = z[c];
+        best = c;
+      }
+    float se = 0.0f;
+    for (int c = 0; c < C; ++c) se += expf(z[c] - m);
+    const float lse = logf(se);
+    lpart = double(lse) - double(z[y] - m);
+    cpart = best == y ? 1.0 : 0.0;
+    if (!a.eval)
+      for (int c = 0; c < C; ++c) z[c] = (expf(z[c] - m - lse) - (c == y ? 1.0f : 0.0f)) * inv;
+  }
+  const double lsum = block_sum_d(lpart, scratch);
+  if (a.eval) {
+    const double csum = block_sum_d(cpart, scratch);
+    if (tid == 0) {
+      atomicAdd(a.eval, csum);
+      atomicAdd(a.eval + 1, lsum);
+    }
+    return;
+  }
+  if (tid == 0) {
+    const double loss = lsum / double(cnt);
+    s_bad = !isfinite(loss);
+    if (s_bad) {
+      a.bad[sl.r] = a.steps[sl.r];
+    } else {
+      a.loss_sum[sl.r] += loss;
+      a.steps[sl.r] += 1;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    a.slots[blockIdx.x].cnt = 0;  // later kernels of this sweep skip the client
+    return;
+  }
+  // dH = dlogits W2 (old weights) masked by relu'
+  float* dh = a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
+  for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
+    const int i = p >> 9, o = p & (kH1 - 1);
+    float s = 0.0f;
+    for (int c = 0; c < C; ++c) s = fmaf(sL[i * C + c], sW[c * kH1 + o], s);
+    dh[p] = sH[p] > 0.0f ? s : 0.0f;
+  }
+  // fc2 weight / bias update
+  for (int p = tid; p < C * kH1; p += kHeadThreads) {
+    const int c = p >> 9, o = p & (kH1 - 1);
+    float g = 0.0f;
+    for (int i = 0; i < cnt; ++i) g = fmaf(sL[i * C + c], sH[i * kH1 + o], g);
+    const int64_t idx = oF2W + p;
+    W[idx] = sgd(a, sl.r, idx, sW[p], g);
+  }
+  for (int c = tid; c < C; c += kHeadThreads) {
+    float g = 0.0f;
+    for (int i = 0; i < cnt; ++i) g += sL[i * C + c];
+    const int64_t idx = oF2W + int64_t(C) * kH1 + c;
+    W[idx] = sgd(a, sl.r, idx, W[idx], g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_fc1_bwd: dP2 = dH W1, dW1 = dH^T p2, W1 -= lr dW1 (one pass over W1)
+// grid (active, 3136/32), 256 threads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fc1_bwd(Args a) {
+  const Slot sl = a.slots[blockIdx.x];
+  if (sl.cnt == 0) return;
+  extern __shared__ float fs[];
+  float* sW = fs;                   // [512][33]
+  float* sDH = sW + kH1 * 33;       // [cnt][512]
+  float* sA = sDH + sl.cnt * kH1;   // [cnt][33]
+  const int tid = threadIdx.x, cnt = sl.cnt;
+  const int k0 = blockIdx.y * 32;
+  float* W = a.w + int64_t(sl.r) * a.P;
+  float* W1 = W + oF1W;
+  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
+  for (int e = tid; e < kH1 * 32; e += 256) {
+    const int o = e >> 5, c = e & 31;
+    sW[o * 33 + c] = W1[int64_t(o) * kFlat + k0 + c];
+  }
+  for (int e = tid; e < cnt * kH1; e += 256) sDH[e] = a.dh[s0 * kH1 + e];
+  for (int e = tid; e < cnt * 32; e += 256) {
+    const int i = e >> 5, c = e & 31;
+    sA[i * 33 + c] = a.p2[(s0 + i) * kFlat + k0 + c];
+  }
+  __syncthreads();
+  for (int p = tid; p < cnt * 32; p += 256) {
+    const int i = p >> 5, c = p & 31;
+    float s = 0.0f;
+    for (int o = 0; o < kH1; ++o) s = fmaf(sDH[i * kH1 + o], sW[o * 33 + c], s);
+    a.dp2[(s0 + i) * kFlat + k0 + c] = s;
+  }
+  const int c = tid & 31;
+  for (int o = tid >> 5; o < kH1; o += 8) {
+    float g = 0.0f;
+    for (int i = 0; i < cnt; ++i) g = fmaf(sDH[i * kH1 + o], sA[i * 33 + c], g);
+    const int64_t idx = oF1W + int64_t(o) * kFlat + k0 + c;
+    W[idx] = sgd(a, sl.r, idx, sW[o * 33 + c], g);
+  }
+  if (blockIdx.y == 0) {
+    for (int o = tid; o < kH1; o += 256) {
+      float g = 0.0f;
+      for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
+      const int64_t idx = oF1B + o;
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_bwd_conv: dz2 planes (pool2/relu backward) -> conv2 dgrad on tcgen05 -> dp1
+// grid (active, ceil(BS/spb)), 256 threads
+// ---------------------------------------------------------------------------
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes;
+
+__global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
+  const Slot sl = a.slots[blockIdx.x];
+  const int i0 = blockIdx.y * spb, i1 = min(sl.cnt, i0 + spb);
+  if (i0 >= i1) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  uint8_t* sW2 = smem;
+  uint8_t* sDz = sW2 + kW2Bytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, 256);
+  if (warp == 0) tmem_alloc<64>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = idesc_bf16(128, 32, false, true);
+  uint32_t phase = 0;
+  for (int i = i0; i < i1; ++i) {
+    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    for (int e = tid; e < kDzBytes / 16; e += 256)
+      reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const float* dp2 = a.dp2 + sid * kFlat;
+    const float* p2 = a.p2 + sid * kFlat;
+    const uint8_t* am2 = a.am2 + sid * kFlat;
+    for (int o = tid; o < kFlat; o += 256) {
+      const int pp = o >> 6, co = o & 63;
+      const int py = pp / 7, px = pp - py * 7;
+      const int d = am2[o];
+      const float g = p2[o] > 0.0f ? dp2[o] : 0.0f;
+      const int row = (2 * py + (d >> 1) + 2) * kG + 2 * px + (d & 1) + 2;
+      *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) =
+          __float2bfloat16(g);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const uint32_t pa = smem_u32(sDz), pw = smem_u32(sW2);
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t)
+#pragma unroll 1
+        for (int tap = 0; tap < 25; ++tap) {
+          const int ky = tap / 5, kx = tap - ky * 5;       // flipped tap
+          const int wt = (4 - ky) * 5 + (4 - kx);
+#pragma unroll
+          for (int kq = 0; kq < 4; ++kq) {
+            const uint64_t ad = desc(pa + (t * 128 + ky * kG + kx) * 16 + 2 * kq * kPlane, kPlane, 128);
+            const uint64_t bd = desc(pw + wt * 4 * 1024 + kq * 256, 128, 1024);
+            mma_bf16(tmem + t * 32, ad, bd, idesc, tap > 0 || kq > 0);
+          }
+        }
+      commit(&mbar);
+    }
+    {
+      uint4* dst = reinterpret_cast<uint4*>(a.dzg + sid * kDzBytes);
+      const uint4* src = reinterpret_cast<const uint4*>(sDz);
+      for (int e = tid; e < kDzBytes / 16; e += 256) dst[e] = src[e];
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    fence_after_sync();
+    if (warp < 4) {
+      float* dp1 = a.dp1 + sid * kP1;
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        const int row = t * 128 + warp * 32 + lane;
+        const int y = row / kG, x = row - y * kG;
+        float v[16];
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(t * 32 + c16 * 16), v);
+          if (y < 14 && x < 14) {
+            float4* d4 = reinterpret_cast<float4*>(dp1 + (y * 14 + x) * kC1 + c16 * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          }
+        }
+      }
+    }
+    fence_before_sync();
+    __syncthreads();
+  }
+  if (warp == 0) tmem_free<64>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// k_wgrad: y<2: conv2 wgrad for taps [13y, 13y+13) on tcgen05 + update;
+//          y==2: conv1 wgrad + conv1/conv2 bias grads (SIMT) + update
+// grid (active, 3), 256 threads
+// ---------------------------------------------------------------------------
+constexpr size_t kWgSmem = kP1Bytes + kDzBytes;
+
+__global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
+  const Slot sl = a.slots[blockIdx.x];
+  if (sl.cnt == 0) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cnt = sl.cnt;
+  float* W = a.w + int64_t(sl.r) * a.P;
+  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
+  if (blockIdx.y == 2) {
+    // ---- conv1 wgrad + biases (SIMT) ----
+    float* sX = reinterpret_cast<float*>(smem);   // [32*32] padded image
+    float* sG = sX + 1024;                        // [196][32] gated dp1
+    uint8_t* sAm = reinterpret_cast<uint8_t*>(sG + 196 * 32);
+    const int co = tid & 31;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float bacc = 0.0f;
+    for (int i = 0; i < cnt; ++i) {
+      const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+      for (int e = tid; e < 1024; e += 256) {
+        const int yy = e >> 5, xx = e & 31;
+        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+      }
+      const uint8_t* p1 = a.p1g + (s0 + i) * kP1Bytes;
+      for (int e = tid; e < kP1; e += 256) {
+        const int pp = e >> 5, c = e & 31;
+        const int py = pp / 14, px = pp - py * 14;
+        const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+            p1 + (c >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (c & 7) * 2));
+        sG[e] = pv > 0.0f ? a.dp1[(s0 + i) * kP1 + e] : 0.0f;
+        sAm[e] = a.am1[(s0 + i) * kP1 + e];
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int pp = 0; pp < 196; ++pp) {
+        const float g = sG[pp * 32 + co];
+        if (tid < 32) bacc += g;
+        const int d = sAm[pp * 32 + co];
+        const int py = pp / 14, px = pp - py * 14;
+        const int y = 2 * py + (d >> 1), xq = 2 * px + (d & 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int tap = (tid >> 5) + 8 * k;
+          if (tap < 25) {
+            const int ky = tap / 5, kx = tap - ky * 5;
+            acc[k] = fmaf(g, sX[(y + ky) * 32 + xq + kx], acc[k]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int tap = (tid >> 5) + 8 * k;
+      if (tap < 25) {
+        const int64_t idx = oC1W + co * 25 + tap;
+        W[idx] = sgd(a, sl.r, idx, W[idx], acc[k]);
+      }
+    }
+    if (tid < 32) {
+      const int64_t idx = oC1B + co;
+      W[idx] = sgd(a, sl.r, idx, W[idx], bacc);
+    }
+    // conv2 bias: sum of gated pooled gradients
+    for (int c2 = tid; c2 < 64; c2 += 256) {
+      float g = 0.0f;
+      for (int i = 0; i < cnt; ++i) {
+        const float* dp2 = a.dp2 + (s0 + i) * kFlat;
+        const float* p2 = a.p2 + (s0 + i) * kFlat;
+        for (int pp = 0; pp < 49; ++pp) {
+          const int o = pp * 64 + c2;
+          if (p2[o] > 0.0f) g += dp2[o];
+        }
+      }
+      const int64_t idx = oC2B + c2;
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+    }
+    return;
+  }
+  // ---- conv2 wgrad on tcgen05: D[co][tap_l*32 + ci] over output positions ----
+  const int tap0 = blockIdx.y * 13, ntap = min(13, 25 - tap0);
+  uint8_t* sP1 = smem;
+  uint8_t* sDz = smem + kP1Bytes;
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = idesc_bf16(64, 32, true, true);
+  uint32_t phase = 0;
+  for (int i = 0; i < cnt; ++i) {
+    {
+      const uint4* s1 = reinterpret_cast<const uint4*>(a.p1g + (s0 + i) * kP1Bytes);
+      const uint4* s2 = reinterpret_cast<const uint4*>(a.dzg + (s0 + i) * kDzBytes);
+      for (int e = tid; e < kP1Bytes / 16; e += 256) reinterpret_cast<uint4*>(sP1)[e] = s1[e];
+      for (int e = tid; e < kDzBytes / 16; e += 256) reinterpret_cast<uint4*>(sDz)[e] = s2[e];
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const uint32_t pz = smem_u32(sDz), pp1 = smem_u32(sP1);
+#pragma unroll 1
+      for (int tl = 0; tl < ntap; ++tl) {
+        const int tap = tap0 + tl, ky = tap / 5, kx = tap - ky * 5;
+#pragma unroll 4
+        for (int ks = 0; ks < 16; ++ks) {
+          // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[ci][p] = p1 row p + ky*18 + kx
+          const uint64_t ad = desc(pz + (2 * kG + 2 + ks * 16) * 16, 128, kPlane);
+          const uint64_t bd = desc(pp1 + (ky * kG + kx + ks * 16) * 16, 128, kPlane);
+          mma_bf16(tmem + tl * 32, ad, bd, idesc, i > 0 || ks > 0);
+        }
+      }
+      commit(&mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    fence_after_sync();
+    __syncthreads();
+  }
+  // epilogue: M=64 rows live in lanes 32q + [0,16) of each quarter q
+  {
+    const int q = warp & 3, part = warp >> 2;
+    const int co = q * 16 + lane;
+#pragma unroll 1
+    for (int tl = part; tl < ntap; tl += 2) {
+      float v[16];
+#pragma unroll
+      for (int c16 = 0; c16 < 2; ++c16) {
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(tl * 32 + c16 * 16), v);
+        if (lane < 16) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int64_t idx = oC2W + int64_t(co) * 800 + (tap0 + tl) * 32 + c16 * 16 + k;
+            W[idx] = sgd(a, sl.r, idx, W[idx], v[k]);
+          }
+        }
+      }
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(tmem);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host entry points
+// ---------------------------------------------------------------------------
+static int set_smem(const void* fn, size_t bytes, const char* name) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+  return PB_OK;
+}
+
+static int cnn_setup() {
+  static int done = 0;
+  if (done) return PB_OK;
+  int rc;
+  if ((rc = set_smem((const void*)k_fwd, kFwdSmem, "k_fwd"))) return rc;
+  if ((rc = set_smem((const void*)k_bwd_conv, kBwdSmem, "k_bwd_conv"))) return rc;
+  if ((rc = set_smem((const void*)k_wgrad, kWgSmem, "k_wgrad"))) return rc;
+  if ((rc = set_smem((const void*)k_head, 200 * 1024, "k_head"))) return rc;
+  if ((rc = set_smem((const void*)k_fc1_bwd, 200 * 1024, "k_fc1_bwd"))) return rc;
+  done = 1;
+  return PB_OK;
+}
+
+static Args to_args(const pb_cnn_train_args& t) {
+  Args a{};
+  a.X = t.X; a.Y = t.Y; a.order = t.order; a.order_off = t.order_off; a.n = t.n;
+  a.rank = t.rank; a.w = t.w; a.w0 = t.w0; a.ctrl_g = t.ctrl_g; a.ctrl_c = t.ctrl_c;
+  a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
+  a.slots = reinterpret_cast<Slot*>(t.ws_slots);
+  a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
+  a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.dp1 = t.ws_dp1; a.eval = nullptr;
+  a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
+  a.P = oF2W + int64_t(t.C) * kH1 + t.C;
+  a.lr = t.lr; a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;
+  return a;
+}
+
+static size_t head_smem(int C, int BS) { return size_t(C * kH1 + BS * kH1 + BS * C) * 4; }
+static size_t fc1b_smem(int BS) { return size_t(kH1 * 33 + BS * kH1 + BS * 33) * 4; }
+
+static int launch_sweep(Args& a, int active, bool train, int spb, cudaStream_t s) {
+  const int BSpb = (a.BS + spb - 1) / spb;
+  k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
+  k_fc1_fwd<<<dim3(active, kH1 / 64), 256, 0, s>>>(a);
+  k_head<<<active, kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+  if (!train) return pb::check_launch("cnn eval sweep");
+  k_fc1_bwd<<<dim3(active, kFlat / 32), 256, fc1b_smem(a.BS), s>>>(a);
+  k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
+  k_wgrad<<<dim3(active, 3), 256, kWgSmem, s>>>(a);
+  return pb::check_launch("cnn train sweep");
+}
+
+extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
+  if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: null args");
+  const pb_cnn_train_args& t = *args;
+  if (t.g < 0 || t.C < 2 || t.C > 128 || t.BS < 1 || t.BS > 32 || t.epochs < 1 || !t.w ||
+      !t.active || t.sweeps < 0)
+    return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad arguments");
+  if (t.g == 0 || t.sweeps == 0) return PB_OK;
+  if (head_smem(t.C, t.BS) > 200 * 1024) return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: C too large");
+  int rc = cnn_setup();
+  if (rc) return rc;
+  Args a = to_args(t);
+  cudaStream_t s = pb::as_stream(stream);
+  const int spb = t.samples_per_cta > 0 ? t.samples_per_cta : 10;
+  for (int step = 0; step < t.sweeps; ++step) {
+    const int active = t.active[step];
+    if (active <= 0) break;
+    a.step = step;
+    k_slots<<<(active + 127) / 128, 128, 0, s>>>(a, active);
+    if ((rc = launch_sweep(a, active, true, spb, s))) return rc;
+  }
+  return PB_OK;
+}
+
+extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2,
+                           void* stream) {
+  if (!args || !out2 || rows < 0) return pb::fail(PB_ERR_INVALID, "pb_cnn_eval: bad arguments");
+  const pb_cnn_train_args& t = *args;
+  if (rows == 0) return PB_OK;
+  int rc = cnn_setup();
+  if (rc) return rc;
+  Args a = to_args(t);
+  a.eval = out2;
+  cudaStream_t s = pb::as_stream(stream);
+  // slots: batches of BS consecutive rows of `order`, all on parameter row 0
+  const int64_t nslots = (rows + t.BS - 1) / t.BS;
+  const int64_t cap = t.g;  // workspace capacity in slots
+  for (int64_t s0 = 0; s0 < nslots; s0 += cap) {
+    const int active = int(std::min<int64_t>(cap, nslots - s0));
+    std::vector<Slot> host(static_cast<size_t>(active));
+    for (int j = 0; j < active; ++j) {
+      const int64_t first = (s0 + j) * t.BS;
+      host[size_t(j)] = Slot{0, int32_t(std::min<int64_t>(t.BS, rows - first)), first};
+    }
+    cudaMemcpyAsync(a.slots, host.data(), sizeof(Slot) * size_t(active), cudaMemcpyHostToDevice, s);
+    if ((rc = launch_sweep(a, active, false, t.samples_per_cta > 0 ? t.samples_per_cta : 10, s)))
+      return rc;
+    cudaStreamSynchronize(s);  // host slot table is reused
+  }
+  return pb::check_launch("pb_cnn_eval");
+}

@@ -1,0 +1,105 @@
+// Diagnostic: one M x N x K bf16 tcgen05 GEMM through canonical SWIZZLE_NONE
+// layouts.  Used by the GPU tests to pin the descriptor conventions (operand
+// majorness, 16-byte-shifted "plane" operands, M=64 accumulator lanes) that
+// the CNN kernels rely on.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace {
+
+using namespace pb::umma;
+
+// staging modes
+//   0: K-major compact   (core (r/8,k/8); K-adjacent cores 128 B apart)
+//   1: MN-major compact  (core (k/8,r/8); MN-adjacent cores 128 B apart)
+//   2: K-major "planes"  (plane q = k/8 holds rows at 16 B stride, R+8 rows per
+//      plane); the descriptor starts `shift` rows into the plane.
+__device__ __forceinline__ uint32_t stage_off(int mode, int r, int k, int R, int K, int shift) {
+  if (mode == 0) return uint32_t((r >> 3) * (K / 8) * 128 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+  if (mode == 1) return uint32_t((k >> 3) * (R / 8) * 128 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2);
+  return uint32_t((k >> 3) * (R + 8) * 16 + (r + shift) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ void mode_desc(int mode, int R, int K, uint32_t& lbo, uint32_t& sbo,
+                                          uint32_t& kstep) {
+  if (mode == 0) { lbo = 128; sbo = uint32_t(K / 8 * 128); kstep = 256; }
+  else if (mode == 1) { lbo = uint32_t(R / 8 * 128); sbo = 128; kstep = 2 * lbo; }
+  else { lbo = uint32_t((R + 8) * 16); sbo = 128; kstep = 2 * lbo; }
+}
+
+__global__ void __launch_bounds__(128) umma_selftest_kernel(const __nv_bfloat16* A,
+                                                            const __nv_bfloat16* B, float* D,
+                                                            int M, int N, int K, int a_mode,
+                                                            int b_mode, int shift) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int a_bytes = (M + 8) * K * 2;
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + a_bytes;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (M + 8) * K + (N + 8) * K; i += blockDim.x) {
+    if (i < (M + 8) * K) reinterpret_cast<__nv_bfloat16*>(sa)[i] = __float2bfloat16(0.f);
+    else reinterpret_cast<__nv_bfloat16*>(sb)[i - (M + 8) * K] = __float2bfloat16(0.f);
+  }
+  __syncthreads();
+  for (int i = tid; i < M * K; i += blockDim.x) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sa + stage_off(a_mode, r, k, M, K, shift)) = A[i];
+  }
+  for (int i = tid; i < N * K; i += blockDim.x) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<__nv_bfloat16*>(sb + stage_off(b_mode, r, k, N, K, shift)) = B[i];
+  }
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    uint32_t al, as, ak, bl, bs, bk;
+    mode_desc(a_mode, M, K, al, as, ak);
+    mode_desc(b_mode, N, K, bl, bs, bk);
+    const uint32_t a0 = smem_u32(sa) + (a_mode == 2 ? shift * 16 : 0);
+    const uint32_t b0 = smem_u32(sb) + (b_mode == 2 ? shift * 16 : 0);
+    const uint32_t idesc = idesc_bf16(M, N, a_mode == 1, b_mode == 1);
+    for (int ks = 0; ks < K / 16; ++ks)
+      mma_bf16(tbase, desc(a0 + ks * ak, al, as), desc(b0 + ks * bk, bl, bs), idesc, ks > 0);
+    commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after_sync();
+  const int row = warp * 32 + (tid & 31);  // every TMEM lane, whatever M is
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tbase + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tbase);
+}
+
+}  // namespace
+
+extern "C" int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K,
+                                int a_mode, int b_mode, int shift, void* stream) {
+  if (!A || !B || !D || (M != 64 && M != 128) || N < 16 || N > 256 || N % 16 || K < 16 ||
+      K % 16 || a_mode < 0 || a_mode > 2 || b_mode < 0 || b_mode > 2 || shift < 0 || shift > 7)
+    return pb::fail(PB_ERR_INVALID, "pb_umma_selftest: bad arguments");
+  const size_t smem = size_t(M + 8 + N + 8) * K * 2;
+  if (smem > 200 * 1024) return pb::fail(PB_ERR_INVALID, "pb_umma_selftest: too large");
+  cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  umma_selftest_kernel<<<1, 128, smem, pb::as_stream(stream)>>>(
+      static_cast<const __nv_bfloat16*>(A), static_cast<const __nv_bfloat16*>(B), D, M, N, K,
+      a_mode, b_mode, shift);
+  return pb::check_launch("pb_umma_selftest");
+}

@@ -67,16 +67,16 @@ def cnn_spec(n_classes: int = 62) -> ModelSpec:
 
 
 def cnn_init(spec: ModelSpec, seed: int = 0) -> np.ndarray:
-    """Deterministic He-uniform initialisation (float32 flat vector); the
-    reference has no CNN, so this is the builder's choice, documented in
-    DESIGN.md."""
+    """Deterministic initialisation with PyTorch's default Conv2d/Linear rule
+    (weights and biases ~ U(-1/sqrt(fan_in), 1/sqrt(fan_in))), as the FedML
+    FEMNIST CNN uses; float32 flat vector.  The reference has no CNN, so the
+    init is the builder's choice."""
     g = np.random.default_rng([seed, 97])
     out = np.zeros(spec.numel, dtype=np.float32)
-    fan_in = {"conv1_w": 25, "conv2_w": 800, "fc1_w": 3136, "fc2_w": 512}
+    fan_in = {"conv1": 25, "conv2": 800, "fc1": 3136, "fc2": 512}
     for name, off, size, _ in spec.columns():
-        if name in fan_in:
-            bound = np.sqrt(6.0 / fan_in[name])
-            out[off:off + size] = g.uniform(-bound, bound, size).astype(np.float32)
+        bound = 1.0 / np.sqrt(fan_in[name.split("_")[0]])
+        out[off:off + size] = g.uniform(-bound, bound, size).astype(np.float32)
     return out
 
 

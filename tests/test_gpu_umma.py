@@ -1,0 +1,35 @@
+"""Pin the tcgen05 operand-layout conventions (SWIZZLE_NONE canonical layouts,
+K-major, MN-major and 16-byte-shifted "plane" operands; M=64 accumulator lane
+mapping) that the CNN kernels are built on."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(M, n, k, a_mode, b_mode, shift):
+    import torch
+    from paper_2303_01778_b200._lib import lib
+    g = torch.Generator().manual_seed(M * n * k + a_mode * 3 + b_mode + shift)
+    A = torch.randn(M, k, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn(n, k, generator=g).to(torch.bfloat16).cuda()
+    want = (A.float() @ B.float().t()).cpu().numpy()
+    D = torch.zeros(128, n, device="cuda")
+    lib.check(lib.pb_umma_selftest(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, n, k, a_mode,
+                                   b_mode, shift, torch.cuda.current_stream().cuda_stream))
+    return D.cpu().numpy(), want
+
+
+@pytest.mark.parametrize("n,k", [(64, 128), (16, 32), (32, 512)])
+@pytest.mark.parametrize("a_mode,b_mode", [(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (2, 1), (2, 2)])
+@pytest.mark.parametrize("shift", [0, 5])
+def test_umma_m128_layouts(n, k, a_mode, b_mode, shift):
+    got, want = _run(128, n, k, a_mode, b_mode, shift)
+    assert np.allclose(got, want, rtol=1e-3, atol=1e-2), np.abs(got - want).max()
+
+
+def test_umma_m64_accumulator_lanes():
+    got, want = _run(64, 32, 64, 1, 1, 0)
+    lanes = [(r // 16) * 32 + r % 16 for r in range(64)]
+    assert np.allclose(got[lanes], want, rtol=1e-3, atol=1e-2)
