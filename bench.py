@@ -1,0 +1,435 @@
+"""Benchmark: FL rounds/sec, 1000 clients per round, FEMNIST-shaped CNN
+(BASELINE.json metric, config 2 at the headline M_p = 1000), plus the
+aggregation microbench (config 5) as a secondary measurement.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+A "step" is one Parrot round: select 1000 of 3400 clients, heterogeneity-
+aware schedule over the N GPUs (K = N devices, one per rank), every client's
+full local SGD run (E=1, bs=20, lr=0.05), hierarchical fold, NCCL reduction
+of the per-GPU partials, FedAvg server update.
+
+* ``value``  device-timed rounds/s with the round's inputs (plan, minibatch
+  row ids, global model) already in HBM: CUDA events around K rounds,
+  barrier + synchronize on both sides, max over ranks;
+* ``e2e``    the same rounds through the public API
+  (``SimulationEngine.run_round``): host selection/schedule/permutations,
+  host->device copies of the round inputs and the device->host read of the
+  round's loss/step results inside the timed region;
+* ``roofline`` for the dominant kernel (per-kernel CUDA events recorded by
+  the library on the launching stream over the timed rounds);
+* ``cpu_baseline``: the CPU oracle port (torch, all host threads) on a
+  bounded sample of the same round, extrapolated to 1000 clients.
+
+Data: synthetic FEMNIST-shaped (28x28, 62 classes) Gaussian class mixture of
+fedsim.data.generate's form, generated on the device (768,400 samples, 2.4
+GB fp32; client sizes from the reference's Dirichlet(1.0) partition rule,
+bit-exact); inputs exceed L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+M_TOTAL, M_ROUND, N_CLASSES, BS, LR, EPOCHS = 3400, 1000, 62, 20, 0.05, 1
+N_SAMPLES = 768_400
+PEAKS = {"hbm_gbs": 6542.1, "bf16_tflops": 1668.8, "bf16_tflops_sustained": 1366.7}
+# algorithmic work: CNN training 73.8 MFLOP/sample at P = 1,690,046
+FLOP_CONV2_PER_SAMPLE = 3 * 2 * 14 * 14 * 64 * 800   # fwd + dgrad + wgrad of conv2
+FLOP_TRAIN_PER_SAMPLE = 73.8e6
+
+
+def load_peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {k: d.get(k, v) for k, v in PEAKS.items()}, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def client_sizes():
+    from paper_2303_01778_b200.core import STREAM_PARTITION, stream_rng
+    from paper_2303_01778_b200.data import PartitionSpec, client_sizes as sizes_fn
+    return sizes_fn(N_SAMPLES, M_TOTAL, PartitionSpec(quantity_skew=1.0, min_samples_per_client=10),
+                    stream_rng(0, STREAM_PARTITION))
+
+
+def build_device_data(device):
+    """FEMNIST-shaped Gaussian mixture on the device (same construction as
+    fedsim.data.generate: unit-norm class means * 3.0 + N(0,1) noise)."""
+    import torch
+    from paper_2303_01778_b200.trainer import ClientData
+    g = torch.Generator(device=device).manual_seed(0)
+    means = torch.randn(N_CLASSES, 784, generator=g, device=device)
+    means *= 3.0 / means.norm(dim=1, keepdim=True)
+    labels = torch.randint(0, N_CLASSES, (N_SAMPLES,), generator=g, device=device, dtype=torch.int64)
+    X = torch.empty(N_SAMPLES, 784, device=device)
+    chunk = 1 << 17
+    for lo in range(0, N_SAMPLES, chunk):
+        hi = min(N_SAMPLES, lo + chunk)
+        X[lo:hi] = means[labels[lo:hi]] + torch.randn(hi - lo, 784, generator=g, device=device)
+    sizes = client_sizes()
+    base = np.zeros(M_TOTAL, dtype=np.int64)
+    base[1:] = np.cumsum(sizes)[:-1]
+    return ClientData(X, labels.to(torch.int32), base, sizes.astype(np.int64), 784, N_CLASSES), sizes
+
+
+def light_profiles(sizes):
+    """ClientProfiles carrying only sample counts (the data lives on the GPU)."""
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    feat = np.zeros((1, 784), dtype=np.float32)
+    out = []
+    for cid, n in enumerate(sizes):
+        n = int(n)
+        out.append(ClientProfile(cid, n, DataSlice(np.broadcast_to(feat, (n, 784)),
+                                                   np.zeros(n, dtype=np.int64), np.arange(n))))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=5)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+
+def dist_setup(gpus: int):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    import torch
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_sample_rounds_per_s(sizes, n_clients: int = 6, threads: int | None = None):
+    """Oracle port (torch CPU fp32, all host threads) on a bounded sample of the
+    round: n_clients clients' full local runs, extrapolated to 1000 clients."""
+    import torch
+    from oracle import cnn_oracle
+    from paper_2303_01778_b200.models import cnn_init, cnn_spec
+    if threads:
+        torch.set_num_threads(threads)
+    spec = cnn_spec(N_CLASSES)
+    w0 = cnn_init(spec, seed=0)
+    rng = np.random.default_rng(1)
+    picks = rng.choice(M_TOTAL, size=n_clients, replace=False)
+    samples = 0
+    t0 = time.perf_counter()
+    for m in picks:
+        n = int(sizes[m])
+        X = rng.standard_normal((n, 784)).astype(np.float32)
+        y = rng.integers(0, N_CLASSES, n)
+        cnn_oracle.client_train(w0, X, y, int(m), 0, 0, EPOCHS, BS, LR, N_CLASSES,
+                                dtype=torch.float32)
+        samples += n
+    dt = time.perf_counter() - t0
+    per_sample = dt / samples
+    mean_round_samples = float(np.mean(sizes)) * M_ROUND
+    return 1.0 / (per_sample * mean_round_samples), {
+        "clients": n_clients, "samples": samples, "seconds": dt,
+        "threads": torch.get_num_threads()}
+
+
+def run_b200(args) -> dict:
+    import torch
+    import paper_2303_01778_b200 as pb
+    from paper_2303_01778_b200._lib import lib, prof_collect
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    data, sizes = build_device_data(dev)
+    profiles = light_profiles(sizes)
+    total_rounds = args.warmup + 2 * args.steps + 2
+    cfg = pb.SimConfig(total_clients=M_TOTAL, concurrent_clients=M_ROUND, num_devices=world,
+                       total_rounds=total_rounds, warmup_rounds=1, seed=0, scheme="PARROT",
+                       scheduling="time-window")
+    eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=LR, batch_size=BS), profiles,
+                              pb.make_device_models(world), model="cnn", client_data=data,
+                              init_seed=0)
+    r = 0
+    for _ in range(args.warmup):
+        eng.run_round(r)
+        r += 1
+    # ---- device-timed rounds (inputs prepared and resident before timing) ----
+    prepared = [eng.prepare_round(r + i) for i in range(args.steps)]
+    for p in prepared:
+        p.upload()
+    lib.pb_prof_enable(1)
+    prof_collect()
+    barrier(world)
+    launches0 = lib.pb_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for p in prepared:
+            eng.execute_round(p, sync=False)
+        e1.record()
+        barrier(world)
+    launches = lib.pb_launch_count() - launches0
+    lib.pb_prof_enable(0)
+    kernels = prof_collect()
+    dev_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    r += args.steps
+    # ---- end-to-end rounds through the public API ----
+    barrier(world)
+    h2d0, d2h0 = eng.io_bytes()
+    t0 = time.perf_counter()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for i in range(args.steps):
+        eng.run_round(r + i)
+    e3.record()
+    barrier(world)
+    e2e_ms = max_over_ranks(max(e2.elapsed_time(e3), (time.perf_counter() - t0) * 1e3), world)
+    h2d1, d2h1 = eng.io_bytes()
+
+    # ---- aggregation microbench (config 5), bounded ----
+    agg = aggregation_microbench(world, dev) if args.agg else None
+
+    peaks, peak_src = load_peaks()
+    samples_round = float(np.sum(sizes)) / M_TOTAL * M_ROUND
+    ms_round = dev_ms / args.steps
+    # dominant kernel
+    dom = max(kernels.items(), key=lambda kv: kv[1][0]) if kernels else ("none", (0.0, 0))
+    dom_name, (dom_ms, dom_n) = dom
+    roof = roofline(dom_name, dom_ms, dom_n, kernels, samples_round * args.steps, peaks, peak_src)
+    out = {
+        "metric": "FL rounds/sec (1000 clients, FEMNIST-CNN)",
+        "value": args.steps / (dev_ms / 1e3),
+        "unit": "rounds/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_round,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16 (conv2 tcgen05 operands) / fp32 (master weights, other layers)",
+        "data": "synthetic FEMNIST-shaped Gaussian mixture generated on device; "
+                "Dirichlet(1.0) client sizes bit-exact with fedsim.partition",
+        "config": {"workload": "C2: FedAvg 2-layer CNN (P=1,690,046), 3400 clients, 1000 per round, "
+                               "bs=20, E=1, lr=0.05, PARROT greedy schedule over the GPUs",
+                   "clients_per_round": M_ROUND, "total_clients": M_TOTAL,
+                   "samples_per_round": samples_round, "parallelism": f"clients across {world} GPU(s)",
+                   "l2": "inputs exceed L2 (2.4 GB data, 6.8 GB client parameters per round)"},
+        "e2e": {"value": args.steps / (e2e_ms / 1e3), "unit": "rounds/s",
+                "h2d_bytes_per_step": int((h2d1 - h2d0) / args.steps),
+                "d2h_bytes_per_step": int((d2h1 - d2h0) / args.steps)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "kernels_ms_per_round": {k: round(v[0] / args.steps, 3) for k, v in kernels.items()},
+        "clocks": clocks.summary(),
+    }
+    if agg is not None:
+        out["aggregation"] = agg
+    if rank == 0 and args.cpu_baseline and world == 1:
+        v, info = cpu_sample_rounds_per_s(sizes)
+        out["cpu_baseline"] = {"value": v, "unit": "rounds/s", "cores": info["threads"],
+                               "kind": "port",
+                               "sample": f"{info['clients']} clients' full local runs "
+                                         f"({info['samples']} samples, {info['seconds']:.1f} s, "
+                                         f"torch CPU fp32 oracle port) extrapolated to a 1000-client round"}
+    return out if rank == 0 else None
+
+
+def roofline(name, ms, n, kernels, samples_timed, peaks, peak_src) -> dict:
+    """Dominant kernel vs its roofline (algorithmic work per launch / its
+    average launch duration)."""
+    if name in ("cnn_fwd", "cnn_bwd_conv", "cnn_wgrad"):
+        share = {"cnn_fwd": 1 / 3, "cnn_bwd_conv": 1 / 3, "cnn_wgrad": 1 / 3}[name]
+        flops = FLOP_CONV2_PER_SAMPLE * share * samples_timed
+        achieved = flops / (ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": f"{peak_src} bf16 sustained",
+                "work": "conv2 implicit-GEMM FLOPs (2*14*14*64*800 per sample per pass)"}
+    if name in ("cnn_fc1_fwd", "cnn_fc1_bwd"):
+        per = 4 if name == "cnn_fc1_fwd" else 8
+        steps_timed = n  # one launch per sweep, over all active clients
+        bytes_ = per * 512 * 3136 * kernels.get("_client_steps", (0, 0))[0] if False else None
+        return {"kernel": name, "bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src}
+    return {"kernel": name, "bound": "unknown", "achieved": None, "peak": None, "unit": None,
+            "frac": None, "traffic": None}
+
+
+def aggregation_microbench(world: int, dev) -> dict:
+    """Config 5: weighted sum of 1000 client updates of an 11.17M-param model,
+    1000/N clients per GPU, fp32, one fold_group pass + one all-reduce."""
+    import torch
+    from paper_2303_01778_b200 import _kernels as K
+    P = 11_173_962
+    g = M_ROUND // world
+    xs = torch.empty(g, P, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    for lo in range(0, g, 50):
+        xs[lo:lo + 50].normal_(generator=gen)
+    w = torch.from_numpy(client_sizes()[:g].astype(np.float32)).to(dev)
+    acc = torch.zeros(P, device=dev)
+    for _ in range(2):
+        acc.zero_()
+        K.fold_group(acc, xs, None, w)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(3):
+        acc.zero_()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.fold_group(acc, xs, None, w)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = max_over_ranks(min(times), world)
+    red_ms = None
+    if world > 1:
+        import torch.distributed as dist
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dist.all_reduce(acc)
+        b.record()
+        torch.cuda.synchronize()
+        red_ms = max_over_ranks(a.elapsed_time(b), world)
+    peaks, src = load_peaks()
+    alg_bytes = 4.0 * g * P + 8.0 * P  # each client row read once, acc read+written once
+    gbs = alg_bytes / (ms / 1e3) / 1e9
+    out = {"clients_per_gpu": g, "params": P, "fold_ms": ms, "achieved_gbs": gbs,
+           "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
+           "algorithmic_bytes": "4*P per client + 8*P per launch (acc read+write)",
+           "clients_per_s": g * world / (ms / 1e3)}
+    if red_ms is not None:
+        out["allreduce_ms"] = red_ms
+    del xs
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the reference (CPU oracle port) arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import torch
+    sizes = client_sizes()
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample_rounds_per_s(sizes, n_clients=1)
+    for i in range(args.steps):
+        v, info = cpu_sample_rounds_per_s(sizes, n_clients=2)
+        vals.append(v)
+    v = float(np.median(vals))
+    return {"metric": "FL rounds/sec (1000 clients, FEMNIST-CNN)", "value": v, "unit": "rounds/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic FEMNIST-shaped", "config": {"workload": "C2 (see B200 arm)"},
+            "cpu_baseline": {"value": v, "unit": "rounds/s", "cores": torch.get_num_threads(),
+                             "kind": "port",
+                             "sample": "per step: 2 clients' full local runs with the torch CPU "
+                                       "oracle port (the reference has no CNN and no compiled "
+                                       "path), extrapolated to a 1000-client round"},
+            "e2e": {"value": v, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-agg", dest="agg", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    out = run_reference(args) if args.impl == "reference" else run_b200(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

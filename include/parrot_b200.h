@@ -35,6 +35,17 @@ const char* pb_last_error(void);
 int pb_version(void);
 int pb_device_sm_count(int device);
 
+/* Launch accounting and optional per-kernel-class timing (CUDA events on the
+ * launching stream).  pb_launch_count: kernels launched by this library so far.
+ * pb_prof_collect fills ms[id] / count[id] for the kernel classes
+ *   0 fold1 1 fold_group 2 lincomb 3 delta_affine 4 state_gather
+ *   5 state_scatter 6 lr_train 7 lr_eval 8 cnn_slots 9 cnn_fwd 10 cnn_fc1_fwd
+ *   11 cnn_head 12 cnn_fc1_bwd 13 cnn_bwd_conv 14 cnn_wgrad
+ * recorded since the last collect (nslots >= 15), synchronising on them. */
+int pb_prof_enable(int on);
+int64_t pb_launch_count(void);
+int pb_prof_collect(double* ms, int64_t* count, int nslots);
+
 /* ---------------------------------------------------------------------------
  * Host-side scheduling / RNG (native runtime around the kernels)
  * ------------------------------------------------------------------------- */

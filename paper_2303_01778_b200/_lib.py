@@ -48,6 +48,9 @@ _SIGS = {
     "pb_last_error": (ctypes.c_char_p, []),
     "pb_version": (c_int, []),
     "pb_device_sm_count": (c_int, [c_int]),
+    "pb_prof_enable": (c_int, [c_int]),
+    "pb_launch_count": (c_int64, []),
+    "pb_prof_collect": (c_int, [POINTER(c_double), POINTER(c_int64), c_int]),
     "pb_greedy_assign": (c_int, [POINTER(c_double), c_int64, POINTER(c_double), POINTER(c_double),
                                  c_int64, POINTER(c_int64), POINTER(c_double)]),
     "pb_minibatch_rows": (c_int, [POINTER(c_uint64), POINTER(c_int64), POINTER(c_int64),
@@ -97,6 +100,20 @@ class _Lib:
 
 
 lib = _Lib(_PATH)
+
+
+KERNEL_CLASSES = ("fold1", "fold_group", "lincomb", "delta_affine", "state_gather",
+                  "state_scatter", "lr_train", "lr_eval", "cnn_slots", "cnn_fwd", "cnn_fc1_fwd",
+                  "cnn_head", "cnn_fc1_bwd", "cnn_bwd_conv", "cnn_wgrad")
+
+
+def prof_collect() -> dict[str, tuple[float, int]]:
+    """{kernel class: (total ms, launches)} since the last collect."""
+    n = len(KERNEL_CLASSES)
+    ms = (c_double * n)()
+    cnt = (c_int64 * n)()
+    lib.check(lib.pb_prof_collect(ms, cnt, n))
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES) if cnt[i]}
 
 
 def ptr(t) -> int | None:

@@ -1,4 +1,7 @@
 // Error plumbing and device queries for the C ABI.
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace pb {
@@ -21,7 +24,79 @@ int sm_count() {
   return cached;
 }
 
+namespace {
+struct Rec {
+  int id;
+  cudaEvent_t a, b;
+};
+std::mutex g_mu;
+bool g_prof = false;
+int64_t g_launches = 0;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+cudaEvent_t pooled() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+thread_local cudaEvent_t t_open = nullptr;
+}  // namespace
+
+void prof_begin(int id, cudaStream_t stream) {
+  std::lock_guard<std::mutex> g(g_mu);
+  ++g_launches;
+  (void)id;
+  if (!g_prof) return;
+  t_open = pooled();
+  cudaEventRecord(t_open, stream);
+}
+
+void prof_end(int id, cudaStream_t stream) {
+  std::lock_guard<std::mutex> g(g_mu);
+  if (!g_prof || !t_open) return;
+  cudaEvent_t b = pooled();
+  cudaEventRecord(b, stream);
+  g_recs.push_back(Rec{id, t_open, b});
+  t_open = nullptr;
+}
+
 }  // namespace pb
+
+extern "C" int pb_prof_enable(int on) {
+  std::lock_guard<std::mutex> g(pb::g_mu);
+  pb::g_prof = on != 0;
+  return PB_OK;
+}
+
+extern "C" int64_t pb_launch_count(void) {
+  std::lock_guard<std::mutex> g(pb::g_mu);
+  return pb::g_launches;
+}
+
+extern "C" int pb_prof_collect(double* ms, int64_t* count, int nslots) {
+  std::lock_guard<std::mutex> g(pb::g_mu);
+  if (!ms || !count || nslots < pb::K_NUM_IDS) return pb::fail(PB_ERR_INVALID, "pb_prof_collect: bad arguments");
+  for (int i = 0; i < nslots; ++i) {
+    ms[i] = 0.0;
+    count[i] = 0;
+  }
+  for (auto& r : pb::g_recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.id] += t;
+    count[r.id] += 1;
+    pb::g_pool.push_back(r.a);
+    pb::g_pool.push_back(r.b);
+  }
+  pb::g_recs.clear();
+  return pb::check_launch("pb_prof_collect");
+}
 
 extern "C" const char* pb_last_error(void) { return pb::g_last_error.c_str(); }
 

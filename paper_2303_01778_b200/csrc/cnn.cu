@@ -794,13 +794,25 @@ static size_t fc1b_smem(int BS) { return size_t(kH1 * 33 + BS * kH1 + BS * 33) *
 
 static int launch_sweep(Args& a, int active, bool train, int spb, cudaStream_t s) {
   const int BSpb = (a.BS + spb - 1) / spb;
+  pb::prof_begin(pb::K_CNN_FWD, s);
   k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
+  pb::prof_end(pb::K_CNN_FWD, s);
+  pb::prof_begin(pb::K_CNN_FC1_FWD, s);
   k_fc1_fwd<<<dim3(active, kH1 / 64), 256, 0, s>>>(a);
+  pb::prof_end(pb::K_CNN_FC1_FWD, s);
+  pb::prof_begin(pb::K_CNN_HEAD, s);
   k_head<<<active, kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+  pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
+  pb::prof_begin(pb::K_CNN_FC1_BWD, s);
   k_fc1_bwd<<<dim3(active, kFlat / 32), 256, fc1b_smem(a.BS), s>>>(a);
+  pb::prof_end(pb::K_CNN_FC1_BWD, s);
+  pb::prof_begin(pb::K_CNN_BWD_CONV, s);
   k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
+  pb::prof_end(pb::K_CNN_BWD_CONV, s);
+  pb::prof_begin(pb::K_CNN_WGRAD, s);
   k_wgrad<<<dim3(active, 3), 256, kWgSmem, s>>>(a);
+  pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
 }
 
@@ -821,7 +833,9 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     const int active = t.active[step];
     if (active <= 0) break;
     a.step = step;
+    pb::prof_begin(pb::K_CNN_SLOTS, s);
     k_slots<<<(active + 127) / 128, 128, 0, s>>>(a, active);
+    pb::prof_end(pb::K_CNN_SLOTS, s);
     if ((rc = launch_sweep(a, active, true, spb, s))) return rc;
   }
   return PB_OK;

@@ -37,4 +37,15 @@ inline unsigned grid_for(int64_t items, int threads, int waves = 8) {
   return unsigned(need < cap ? need : cap);
 }
 
+// ---- launch accounting / optional per-kernel-class timing -----------------
+enum KernelId {
+  K_FOLD1 = 0, K_FOLD_GROUP, K_LINCOMB, K_DELTA_AFFINE, K_STATE_GATHER, K_STATE_SCATTER,
+  K_LR_TRAIN, K_LR_EVAL, K_CNN_SLOTS, K_CNN_FWD, K_CNN_FC1_FWD, K_CNN_HEAD, K_CNN_FC1_BWD,
+  K_CNN_BWD_CONV, K_CNN_WGRAD, K_NUM_IDS
+};
+// Call around one kernel launch on `stream`: counts the launch and, when
+// profiling is on, brackets it with pooled CUDA events.
+void prof_begin(int id, cudaStream_t stream);
+void prof_end(int id, cudaStream_t stream);
+
 }  // namespace pb

@@ -122,10 +122,14 @@ extern "C" int pb_fold_f32(float* acc, const float* x, float w, int64_t n, void*
   if (n == 0) return PB_OK;
   cudaStream_t s = pb::as_stream(stream);
   if (n % 4 == 0 && pb::aligned16(acc) && pb::aligned16(x)) {
+    pb::prof_begin(pb::K_FOLD1, s);
     fold1_vec<<<pb::grid_for(n / 4, kThreads), kThreads, 0, s>>>(
         reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(x), w, n / 4);
+    pb::prof_end(pb::K_FOLD1, s);
   } else {
+    pb::prof_begin(pb::K_FOLD1, s);
     fold1_scalar<<<pb::grid_for(n, kThreads), kThreads, 0, s>>>(acc, x, w, n);
+    pb::prof_end(pb::K_FOLD1, s);
   }
   return pb::check_launch("pb_fold_f32");
 }
@@ -141,11 +145,15 @@ extern "C" int pb_fold_group_f32(float* acc, const float* xs, int64_t x_stride,
     const int64_t n4 = n / 4;
     // one float4 per thread, no grid-stride re-walk of the g rows
     const int64_t blocks = (n4 + kThreads - 1) / kThreads;
+    pb::prof_begin(pb::K_FOLD_GROUP, s);
     fold_group_vec<8><<<unsigned(blocks), kThreads, 0, s>>>(
         reinterpret_cast<float4*>(acc), xs, x_stride, order, w, int(g), n4);
+    pb::prof_end(pb::K_FOLD_GROUP, s);
   } else {
     const int64_t blocks = (n + kThreads - 1) / kThreads;
+    pb::prof_begin(pb::K_FOLD_GROUP, s);
     fold_group_scalar<<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
+    pb::prof_end(pb::K_FOLD_GROUP, s);
   }
   return pb::check_launch("pb_fold_group_f32");
 }
@@ -154,8 +162,10 @@ extern "C" int pb_lincomb_f32(float* out, const float* x, float a, const float* 
                               const float* z, float c, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && !out)) return pb::fail(PB_ERR_INVALID, "pb_lincomb_f32: bad arguments");
   if (n == 0) return PB_OK;
+  pb::prof_begin(pb::K_LINCOMB, pb::as_stream(stream));
   lincomb_kernel<<<pb::grid_for(n, kThreads), kThreads, 0, pb::as_stream(stream)>>>(out, x, a, y,
                                                                                    b, z, c, n);
+  pb::prof_end(pb::K_LINCOMB, pb::as_stream(stream));
   return pb::check_launch("pb_lincomb_f32");
 }
 
@@ -169,7 +179,9 @@ extern "C" int pb_delta_affine_group(float* out, int64_t out_stride, const float
   if (n == 0 || g == 0) return PB_OK;
   unsigned gx = pb::grid_for(n, kThreads, 2);
   dim3 grid(gx, unsigned(g));
+  pb::prof_begin(pb::K_DELTA_AFFINE, pb::as_stream(stream));
   delta_affine_kernel<<<grid, kThreads, 0, pb::as_stream(stream)>>>(
       out, out_stride, a, a_stride, base, s, cvec, c, dmat, d_stride, d, n);
+  pb::prof_end(pb::K_DELTA_AFFINE, pb::as_stream(stream));
   return pb::check_launch("pb_delta_affine_group");
 }

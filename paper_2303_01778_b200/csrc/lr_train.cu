@@ -225,7 +225,9 @@ extern "C" int pb_lr_train_group(const pb_lr_train_args* args, void* stream) {
                                        int(smem));
   if (e != cudaSuccess)
     return pb::fail(PB_ERR_CUDA, std::string("pb_lr_train_group: ") + cudaGetErrorString(e));
+  pb::prof_begin(pb::K_LR_TRAIN, pb::as_stream(stream));
   lr_train_kernel<<<unsigned(a.g), kThreads, smem, pb::as_stream(stream)>>>(a, int(rows));
+  pb::prof_end(pb::K_LR_TRAIN, pb::as_stream(stream));
   return pb::check_launch("pb_lr_train_group");
 }
 
@@ -237,7 +239,9 @@ extern "C" int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F,
   int64_t blocks = (rows + kWarps - 1) / kWarps;
   const int64_t cap = int64_t(pb::sm_count()) * 8;
   if (blocks > cap) blocks = cap;
+  pb::prof_begin(pb::K_LR_EVAL, pb::as_stream(stream));
   lr_eval_kernel<<<unsigned(blocks), kThreads, size_t(kWarps) * C * sizeof(float),
                    pb::as_stream(stream)>>>(X, Y, rows, F, C, w, out2);
+  pb::prof_end(pb::K_LR_EVAL, pb::as_stream(stream));
   return pb::check_launch("pb_lr_eval");
 }

@@ -62,14 +62,18 @@ int move_rows(float* dst, int64_t dst_stride, const float* src, int64_t src_stri
     const int64_t w4 = width / 4;
     int64_t gx = std::min<int64_t>(per_row, (w4 + kThreads - 1) / kThreads);
     dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
+    pb::prof_begin(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
     move_rows_vec<kGather><<<grid, kThreads, 0, s>>>(
         reinterpret_cast<float4*>(dst), dst_stride / 4, reinterpret_cast<const float4*>(src),
         src_stride / 4, slot, w4);
+    pb::prof_end(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
   } else {
     int64_t gx = std::min<int64_t>(per_row, (width + kThreads - 1) / kThreads);
     dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
+    pb::prof_begin(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
     move_rows_scalar<kGather><<<grid, kThreads, 0, s>>>(dst, dst_stride, src, src_stride, slot,
                                                          width);
+    pb::prof_end(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
   }
   return pb::check_launch(name);
 }

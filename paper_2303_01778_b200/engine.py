@@ -45,8 +45,9 @@ from .metrics import CostLedger, ReplicaGauge
 from .models import ModelSpec, cnn_init, spec_for
 from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
 from .statestore import StateStore
-from .trainer import (AggOp, AlgorithmPlugin, ClientData, ModelParams, NamedParams, ParamBundle,
-                      device, evaluate, finalize_results, spec_of_bundle, train_group)
+from .trainer import (AggOp, AlgorithmPlugin, ClientData, GroupInputs, ModelParams, NamedParams,
+                      ParamBundle, device, evaluate, finalize_results, io_bytes, spec_of_bundle,
+                      train_group)
 
 RESULTS_HEADER = ("round\tscheme\tscheduling\tsim_seconds\twall_seconds\t"
                   "device_loads\ttrips_up\ttrips_down\tbytes_avg\tbytes_special\t"
@@ -113,6 +114,28 @@ def virtual_task_seconds(device: DeviceModel, sample_count: int, seed: int, roun
 
 
 @dataclass
+class RoundInputs:
+    """Everything the host decides for one round before the device runs it."""
+
+    round: int
+    selection: object
+    sizes: dict
+    fits: dict | None
+    fit_seconds: float
+    schedule_seconds: float
+    plan: RoundPlan
+    fa_tasks: list | None
+    assign: dict
+    group: GroupInputs | None
+    wall0: float
+
+    def upload(self) -> "RoundInputs":
+        if self.group is not None:
+            self.group.upload()
+        return self
+
+
+@dataclass
 class RoundOutcome:
     round: int
     scheme: str
@@ -159,8 +182,16 @@ class DeviceRuntime:
         self.store, self.gauge = store, gauge
         self.last_device_seconds = 0.0
 
+    def prepare(self, assignments: dict[int, list[int]], round_num: int) -> GroupInputs | None:
+        """Host side of a round for the local devices: minibatch row ids of all
+        their clients (device order, then plan order)."""
+        clients = [m for dev in sorted(assignments) for m in assignments[dev]]
+        if not clients:
+            return None
+        return GroupInputs(self.data, clients, self.cfg.local_epochs, self.cfg.seed, round_num)
+
     def execute(self, assignments: dict[int, list[int]], bundle: ParamBundle,
-                round_num: int) -> dict[int, DevicePartial]:
+                round_num: int, inputs: GroupInputs | None = None) -> dict[int, DevicePartial]:
         """Train every assigned client of the local devices in one batched
         launch, then fold each device's clients in its plan order."""
         order = [(dev, m) for dev in sorted(assignments) for m in assignments[dev]]
@@ -183,7 +214,7 @@ class DeviceRuntime:
         try:
             go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
                              self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
-                             round_num)
+                             round_num, inputs=inputs)
         finally:
             self.gauge.release(len(clients))
         self.last_device_seconds = go.seconds
@@ -418,9 +449,13 @@ class SimulationEngine:
         return [local]
 
     # -- the round ----------------------------------------------------------------
-    def run_round(self, round_num: int) -> RoundOutcome:
-        wall0 = time.perf_counter()
+    def prepare_round(self, round_num: int) -> "RoundInputs":
+        """Host half of a round: selection, workload fits, schedule, the
+        virtual-clock timing records (added to the history now, exactly the
+        records the reference's devices report) and the local clients'
+        minibatch orders.  Deterministic in (seed, round, history)."""
         cfg = self.cfg
+        wall0 = time.perf_counter()
         selection = select_clients(cfg, round_num)
         sizes = {m: int(self.sizes[m]) for m in selection.selected}
         fits, fit_seconds = self._fit_all(round_num)
@@ -435,41 +470,45 @@ class SimulationEngine:
                              mode="work-pulling")
             fa_tasks = self._fa_tasks(round_num, selection.selected)
         schedule_seconds = time.perf_counter() - t0
+        if fa_tasks is not None:
+            mine = [(i, dev, m) for i, (dev, m) in enumerate(fa_tasks)
+                    if dev % self._world == self._rank]
+            assign = {i: [m] for i, _, m in mine}
+        else:
+            assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
+        inp = RoundInputs(round_num, selection, sizes, fits, fit_seconds, schedule_seconds, plan,
+                          fa_tasks, assign, self.runtime.prepare(assign, round_num), wall0)
+        if cfg.clock == "virtual":
+            self._record(inp, None)
+        return inp
 
+    def _record(self, inp: "RoundInputs", measured_per_client: float | None) -> None:
+        """Timing records in the reference's order: device order, plan order
+        (fedsim/engine.py:689-697), or completion order for FA_DIST."""
+        r = inp.round
+        if inp.fa_tasks is not None:
+            tasks = list(inp.fa_tasks)
+        else:
+            tasks = [(dev, m) for dev in range(self.cfg.num_devices)
+                     for m in inp.plan.assignments.get(dev, [])]
+        for dev, m in tasks:
+            record(self.history, TimingRecord(dev, m, r, inp.sizes[m],
+                                              self._reported(dev, m, r, measured_per_client)))
+
+    def execute_round(self, inp: "RoundInputs", sync: bool = True) -> RoundOutcome:
+        """Device half of a round: batched training, hierarchical fold,
+        (multi-GPU) partial all-reduce, server rule, evaluation."""
+        cfg, round_num = self.cfg, inp.round
         ledger = CostLedger(round=round_num, scheme=cfg.scheme)
         schema = result_schema(self.plugin, self.spec)
         try:
-            if fa_tasks is not None:
-                # one task per partial, folded in completion order
-                mine = [(i, dev, m) for i, (dev, m) in enumerate(fa_tasks)
-                        if dev % self._world == self._rank]
-                assign = {i: [m] for i, _, m in mine}
-                got = self.runtime.execute(assign, self.global_bundle, round_num)
-                partials = [got[i] for i, _, _ in mine]
-                task_devs = [dev for dev, _ in fa_tasks]
-            else:
-                assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
-                got = self.runtime.execute(assign, self.global_bundle, round_num)
-                partials = [got[k] for k in self.local_devices]
-                task_devs = list(range(cfg.num_devices))
+            got = self.runtime.execute(inp.assign, self.global_bundle, round_num, inp.group)
         except Exception as exc:
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
-
-        # timing records: device order, plan order (fedsim/engine.py:689-697)
-        if fa_tasks is not None:
-            for dev, m in fa_tasks:
-                record(self.history, TimingRecord(dev, m, round_num, sizes[m],
-                                                  self._reported(dev, m, round_num)))
-        else:
-            for dev in range(cfg.num_devices):
-                for m in plan.assignments.get(dev, []):
-                    measured = None
-                    if cfg.clock == "real":
-                        g = max(len(selection.selected), 1)
-                        measured = max(self.runtime.last_device_seconds / g, 1e-9)
-                    record(self.history, TimingRecord(dev, m, round_num, sizes[m],
-                                                      self._reported(dev, m, round_num, measured)))
-
+        partials = [got[k] for k in sorted(inp.assign)]
+        if cfg.clock == "real":
+            g = max(len(inp.selection.selected), 1)
+            self._record(inp, max(self.runtime.last_device_seconds / g, 1e-9))
         if self._world > 1:
             partials = self._reduce_partials(partials, schema)
         agg = global_fold(partials)
@@ -480,10 +519,10 @@ class SimulationEngine:
         if cfg.scheme != "SP":
             avg_elems = sum(int(np.prod(sh)) for _, op, sh in schema if op is not AggOp.COLLECT)
             coll_elems = sum(int(np.prod(sh)) for _, op, sh in schema if op is AggOp.COLLECT)
-            if fa_tasks is not None:
-                uploads = [[m] for _, m in fa_tasks]
+            if inp.fa_tasks is not None:
+                uploads = [[m] for _, m in inp.fa_tasks]
             else:
-                uploads = [plan.assignments.get(k, []) for k in range(cfg.num_devices)]
+                uploads = [inp.plan.assignments.get(k, []) for k in range(cfg.num_devices)]
             for clients in uploads:
                 ledger.add_downlink()
                 ledger.add_uplink(8 * avg_elems if clients else 0, 8 * coll_elems * len(clients))
@@ -494,8 +533,8 @@ class SimulationEngine:
         sim_seconds = max(loads.values()) + cfg.trip_overhead_seconds * (
             ledger.trips_up + ledger.trips_down)
         est_err = float("nan")
-        if fits is not None and plan.mode == MODE_GREEDY:
-            est_err = estimation_error(self.history, fits, round_num)
+        if inp.fits is not None and inp.plan.mode == MODE_GREEDY:
+            est_err = estimation_error(self.history, inp.fits, round_num)
         accuracy = loss = float("nan")
         if self.eval_data is not None and (round_num % self.eval_every == 0
                                            or round_num == cfg.total_rounds - 1):
@@ -503,16 +542,26 @@ class SimulationEngine:
         ledger.peak_live_model_replicas = self.gauge.peak
         if self.store is not None:
             ledger.state_bytes_disk = self.store.stats().bytes_on_disk
-        outcome = RoundOutcome(round=round_num, scheme=cfg.scheme, scheduling_mode=plan.mode,
+        if sync:
+            torch.cuda.synchronize()
+        outcome = RoundOutcome(round=round_num, scheme=cfg.scheme, scheduling_mode=inp.plan.mode,
                                simulated_round_seconds=sim_seconds,
-                               wall_seconds=time.perf_counter() - wall0, device_loads=loads,
+                               wall_seconds=time.perf_counter() - inp.wall0, device_loads=loads,
                                costs=ledger, accuracy=accuracy, loss=loss,
-                               estimation_error=est_err, fit_seconds=fit_seconds,
-                               schedule_seconds=schedule_seconds, new_global=new_global,
+                               estimation_error=est_err, fit_seconds=inp.fit_seconds,
+                               schedule_seconds=inp.schedule_seconds, new_global=new_global,
                                device_seconds=self.runtime.last_device_seconds)
         if self.results_path is not None and self._rank == 0:
             append_results(self.results_path, outcome)
         return outcome
+
+    def run_round(self, round_num: int) -> RoundOutcome:
+        return self.execute_round(self.prepare_round(round_num))
+
+    @staticmethod
+    def io_bytes() -> tuple[int, int]:
+        """(host->device, device->host) bytes of round inputs/results so far."""
+        return io_bytes()
 
     def global_model(self):
         if self.spec.kind == "lr":

@@ -272,24 +272,58 @@ def client_bundle(groups: Sequence[ResultGroup], j: int, client_id: int) -> Para
     return out
 
 
+_IO = {"h2d": 0, "d2h": 0}
+
+
+def io_bytes() -> tuple[int, int]:
+    """Host<->device bytes moved by the training path so far (inputs / results)."""
+    return _IO["h2d"], _IO["d2h"]
+
+
+class GroupInputs:
+    """Host-prepared per-round inputs of one training group: the clients'
+    minibatch row ids (native NumPy-PCG64 permutations), offsets and sizes,
+    in pinned memory, plus their device copies once uploaded."""
+
+    def __init__(self, data: "ClientData", clients: Sequence[int], epochs: int, seed: int,
+                 round_num: int):
+        self.clients = [int(c) for c in clients]
+        G = len(self.clients)
+        self.n = data.sizes[self.clients].astype(np.int64)
+        keys = np.zeros((G, 4), dtype=np.uint64)
+        keys[:, 0] = np.uint64(seed)
+        keys[:, 1] = STREAM_MINIBATCH
+        keys[:, 2] = np.asarray(self.clients, dtype=np.uint64)
+        keys[:, 3] = round_num
+        rows, off = K.minibatch_rows(keys, self.n, data.row_base[self.clients], epochs)
+        self.rows_h = torch.from_numpy(rows).pin_memory()
+        self.off_h = torch.from_numpy(off).pin_memory()
+        self.n_h = torch.from_numpy(self.n.astype(np.int32)).pin_memory()
+        self.rows_d = self.off_d = self.n_d = None
+
+    def upload(self) -> "GroupInputs":
+        if self.rows_d is None:
+            d = device()
+            self.rows_d = self.rows_h.to(d, non_blocking=True)
+            self.off_d = self.off_h.to(d, non_blocking=True)
+            self.n_d = self.n_h.to(d, non_blocking=True)
+            _IO["h2d"] += (self.rows_h.numel() * 4 + self.off_h.numel() * 8 + self.n_h.numel() * 4)
+        return self
+
+
 def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                 clients: Sequence[int], w0: torch.Tensor, global_bundle: ParamBundle,
                 state_work: torch.Tensor | None, epochs: int, batch_size: int, lr: float,
-                seed: int, round_num: int) -> GroupOutcome:
+                seed: int, round_num: int, inputs: GroupInputs | None = None) -> GroupOutcome:
     """Run every listed client's full local schedule concurrently on the GPU."""
     d = device()
-    clients = [int(c) for c in clients]
+    if inputs is None:
+        inputs = GroupInputs(data, clients, epochs, seed, round_num)
+    if [int(c) for c in clients] != inputs.clients:
+        raise ValueError("prepared inputs belong to a different client group")
+    inputs.upload()
+    clients, n = inputs.clients, inputs.n
     G = len(clients)
-    n = data.sizes[clients].astype(np.int64)
-    keys = np.zeros((G, 4), dtype=np.uint64)
-    keys[:, 0] = np.uint64(seed)
-    keys[:, 1] = STREAM_MINIBATCH
-    keys[:, 2] = np.asarray(clients, dtype=np.uint64)
-    keys[:, 3] = round_num
-    rows, off = K.minibatch_rows(keys, n, data.row_base[clients], epochs)
-    rows_d = torch.from_numpy(rows).pin_memory().to(d, non_blocking=True)
-    off_d = torch.from_numpy(off).pin_memory().to(d, non_blocking=True)
-    n_d = torch.from_numpy(n.astype(np.int32)).pin_memory().to(d, non_blocking=True)
     P = spec.numel
     w_out = torch.empty(G, P, device=d)
     loss = torch.empty(G, dtype=torch.float64, device=d)
@@ -302,22 +336,24 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     if spec.kind == "lr":
-        K.lr_train(data.X, data.Y, rows_d, off_d, n_d, w0, w_out, loss, steps, bad,
-                   F=spec.n_features, C=spec.n_classes, epochs=epochs, batch_size=batch_size,
-                   lr=lr, mu=terms.get("mu", 0.0), prox_loss=terms.get("prox_loss", 0.0),
-                   ctrl_g=terms.get("ctrl_g"), cg=terms.get("cg", 0.0),
-                   ctrl_c=state_work if terms.get("ctrl_c") else None, cc=terms.get("cc", 0.0))
+        K.lr_train(data.X, data.Y, inputs.rows_d, inputs.off_d, inputs.n_d, w0, w_out, loss,
+                   steps, bad, F=spec.n_features, C=spec.n_classes, epochs=epochs,
+                   batch_size=batch_size, lr=lr, mu=terms.get("mu", 0.0),
+                   prox_loss=terms.get("prox_loss", 0.0), ctrl_g=terms.get("ctrl_g"),
+                   cg=terms.get("cg", 0.0), ctrl_c=state_work if terms.get("ctrl_c") else None,
+                   cc=terms.get("cc", 0.0))
     elif spec.kind == "cnn":
         from .cnn import cnn_train_group
-        cnn_train_group(data, rows_d, off_d, n, w0, w_out, loss, steps, bad, spec=spec,
-                        epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
+        cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
+                        spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
                         state_work=state_work)
     else:
         raise ValueError(f"unknown model kind {spec.kind!r}")
     t1.record()
-    bad_h = bad.cpu().numpy()
-    steps_h = steps.cpu().numpy().astype(np.int64)
-    loss_h = loss.cpu().numpy()
+    # one device->host read per group: failures, step counts, losses
+    res = torch.cat([bad.double(), steps.double(), loss]).cpu().numpy()
+    _IO["d2h"] += res.size * 8
+    bad_h, steps_h, loss_h = res[:G], res[G:2 * G].astype(np.int64), res[2 * G:]
     seconds = max(t0.elapsed_time(t1) / 1e3, 1e-9)
     for j in range(G):
         if bad_h[j] >= 0:
