@@ -81,6 +81,9 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     a = CnnTrainArgs()
     a.X, a.Y, a.order, a.order_off, a.n, a.rank = (ptr(data.X), ptr(data.Y), ptr(rows_d),
                                                     ptr(off_d), ptr(n_d), ptr(rank_d))
+    limit = int(os.environ.get("PB_CNN_MAX_SWEEPS", "0"))  # debugging aid
+    if limit > 0:
+        active = active[:limit].copy()
     a.active = active.ctypes.data
     a.sweeps = len(active)
     a.w, a.w0 = ptr(w_out), ptr(w0)

@@ -355,29 +355,27 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
   extern __shared__ float hs[];
-  const int C = a.C, cnt = sl.cnt, tid = threadIdx.x;
-  float* sW = hs;                      // [C][512] fc2 weights
-  float* sH = sW + C * kH1;            // [cnt][512]
+  const int C = a.C, cnt = sl.cnt, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* sH = hs;                      // [cnt][512]
   float* sL = sH + cnt * kH1;          // [cnt][C] logits -> dlogits
   __shared__ double scratch[kHeadThreads / 32];
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
-  for (int e = tid; e < C * kH1; e += kHeadThreads) sW[e] = W[oF2W + e];
+  const float* W2 = W + oF2W;          // [C][512], read from L2 (coalesced rows)
   const float* hrow = a.h + sidx(blockIdx.x, 0, a.BS) * kH1;
   for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
   __syncthreads();
-  const float* b2 = W + oF2W + int64_t(C) * kH1;
-  for (int p = tid; p < cnt * C; p += kHeadThreads) {
+  const float* b2 = W2 + int64_t(C) * kH1;
+  // logits: one warp per (sample, class), lanes split the 512-long dot product
+  for (int p = warp; p < cnt * C; p += kHeadThreads / 32) {
     const int i = p / C, c = p - i * C;
     const float* hr = sH + i * kH1;
-    const float* wc = sW + c * kH1;
+    const float* wc = W2 + int64_t(c) * kH1;
     float s = 0.0f;
-    // rotate the start by c so lanes (consecutive c) hit different banks
-    for (int oo = 0; oo < kH1; ++oo) {
-      const int o = (oo + c) & (kH1 - 1);
-      s = fmaf(hr[o], wc[o], s);
-    }
-    sL[p] = s + b2[c];
+#pragma unroll 4
+    for (int o = lane; o < kH1; o += 32) s = fmaf(hr[o], wc[o], s);
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) sL[p] = s + b2[c];
   }
   __syncthreads();
   double lpart = 0.0, cpart = 0.0;
@@ -388,7 +386,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
     float m = z[0];
     int best = 0;
     for (int c = 1; c < C; ++c)
-      if (z[c] > m) {
+      if (takes_max(z[c], m) && m == m) {
         m = z[c];
         best = c;
       }
@@ -429,16 +427,16 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
     const int i = p >> 9, o = p & (kH1 - 1);
     float s = 0.0f;
-    for (int c = 0; c < C; ++c) s = fmaf(sL[i * C + c], sW[c * kH1 + o], s);
+    for (int c = 0; c < C; ++c) s = fmaf(sL[i * C + c], W2[int64_t(c) * kH1 + o], s);
     dh[p] = sH[p] > 0.0f ? s : 0.0f;
   }
-  // fc2 weight / bias update
+  __syncthreads();  // every read of the old W2 is done before the update
   for (int p = tid; p < C * kH1; p += kHeadThreads) {
     const int c = p >> 9, o = p & (kH1 - 1);
     float g = 0.0f;
     for (int i = 0; i < cnt; ++i) g = fmaf(sL[i * C + c], sH[i * kH1 + o], g);
     const int64_t idx = oF2W + p;
-    W[idx] = sgd(a, sl.r, idx, sW[p], g);
+    W[idx] = sgd(a, sl.r, idx, W[idx], g);
   }
   for (int c = tid; c < C; c += kHeadThreads) {
     float g = 0.0f;
@@ -600,92 +598,106 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
 // grid (active, 3), 256 threads
 // ---------------------------------------------------------------------------
 constexpr size_t kWgSmem = kP1Bytes + kDzBytes;
+constexpr int kWgSplit = 4;  // conv2 taps split over 4 CTAs: 7,6,6,6 taps -> <=224 TMEM cols
 
-__global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
+__device__ void conv1_wgrad_and_biases(const Args& a, const Slot& sl, uint8_t* smem) {
+  const int tid = threadIdx.x, cnt = sl.cnt;
+  float* W = a.w + int64_t(sl.r) * a.P;
+  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
+  float* sX = reinterpret_cast<float*>(smem);   // [32*32] padded image
+  float* sG = sX + 1024;                        // [196][32] gated dp1
+  float* sRed = sG + 196 * 32;                  // [4][64] conv2-bias partials
+  uint8_t* sAm = reinterpret_cast<uint8_t*>(sRed + 4 * 64);
+  const int co = tid & 31;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float bacc = 0.0f;
+  // conv2 bias: sum over samples and pooled positions of the gated dp2
+  const int c2 = tid & 63, grp = tid >> 6;
+  float b2acc = 0.0f;
+  for (int i = 0; i < cnt; ++i) {
+    const float* dp2 = a.dp2 + (s0 + i) * kFlat;
+    const float* p2 = a.p2 + (s0 + i) * kFlat;
+    for (int pp = grp; pp < 49; pp += 4) {
+      const int o = pp * 64 + c2;
+      if (p2[o] > 0.0f) b2acc += dp2[o];
+    }
+  }
+  sRed[grp * 64 + c2] = b2acc;
+  for (int i = 0; i < cnt; ++i) {
+    const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+    for (int e = tid; e < 1024; e += 256) {
+      const int yy = e >> 5, xx = e & 31;
+      sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+    }
+    const uint8_t* p1 = a.p1g + (s0 + i) * kP1Bytes;
+    for (int e = tid; e < kP1; e += 256) {
+      const int pp = e >> 5, c = e & 31;
+      const int py = pp / 14, px = pp - py * 14;
+      const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+          p1 + (c >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (c & 7) * 2));
+      sG[e] = pv > 0.0f ? a.dp1[(s0 + i) * kP1 + e] : 0.0f;
+      sAm[e] = a.am1[(s0 + i) * kP1 + e];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int pp = 0; pp < 196; ++pp) {
+      const float g = sG[pp * 32 + co];
+      if (tid < 32) bacc += g;
+      const int d = sAm[pp * 32 + co];
+      const int py = pp / 14, px = pp - py * 14;
+      const int y = 2 * py + (d >> 1), xq = 2 * px + (d & 1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int tap = (tid >> 5) + 8 * k;
+        if (tap < 25) {
+          const int ky = tap / 5, kx = tap - ky * 5;
+          acc[k] = fmaf(g, sX[(y + ky) * 32 + xq + kx], acc[k]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int tap = (tid >> 5) + 8 * k;
+    if (tap < 25) {
+      const int64_t idx = oC1W + co * 25 + tap;
+      W[idx] = sgd(a, sl.r, idx, W[idx], acc[k]);
+    }
+  }
+  if (tid < 32) {
+    const int64_t idx = oC1B + co;
+    W[idx] = sgd(a, sl.r, idx, W[idx], bacc);
+  }
+  if (tid < 64) {
+    const float g = ((sRed[tid] + sRed[64 + tid]) + sRed[128 + tid]) + sRed[192 + tid];
+    const int64_t idx = oC2B + tid;
+    W[idx] = sgd(a, sl.r, idx, W[idx], g);
+  }
+}
+
+// k_wgrad: y < 4: conv2 wgrad for a quarter of the taps on tcgen05 + update;
+//          y == 4: conv1 wgrad + conv1/conv2 bias gradients (SIMT) + update
+// grid (active, 5), 256 threads, 2 CTAs per SM
+__global__ void __launch_bounds__(256, 2) k_wgrad(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
+  if (blockIdx.y == kWgSplit) {
+    conv1_wgrad_and_biases(a, sl, smem);
+    return;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = sl.cnt;
   float* W = a.w + int64_t(sl.r) * a.P;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  if (blockIdx.y == 2) {
-    // ---- conv1 wgrad + biases (SIMT) ----
-    float* sX = reinterpret_cast<float*>(smem);   // [32*32] padded image
-    float* sG = sX + 1024;                        // [196][32] gated dp1
-    uint8_t* sAm = reinterpret_cast<uint8_t*>(sG + 196 * 32);
-    const int co = tid & 31;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float bacc = 0.0f;
-    for (int i = 0; i < cnt; ++i) {
-      const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
-      for (int e = tid; e < 1024; e += 256) {
-        const int yy = e >> 5, xx = e & 31;
-        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
-      }
-      const uint8_t* p1 = a.p1g + (s0 + i) * kP1Bytes;
-      for (int e = tid; e < kP1; e += 256) {
-        const int pp = e >> 5, c = e & 31;
-        const int py = pp / 14, px = pp - py * 14;
-        const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-            p1 + (c >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (c & 7) * 2));
-        sG[e] = pv > 0.0f ? a.dp1[(s0 + i) * kP1 + e] : 0.0f;
-        sAm[e] = a.am1[(s0 + i) * kP1 + e];
-      }
-      __syncthreads();
-#pragma unroll 1
-      for (int pp = 0; pp < 196; ++pp) {
-        const float g = sG[pp * 32 + co];
-        if (tid < 32) bacc += g;
-        const int d = sAm[pp * 32 + co];
-        const int py = pp / 14, px = pp - py * 14;
-        const int y = 2 * py + (d >> 1), xq = 2 * px + (d & 1);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int tap = (tid >> 5) + 8 * k;
-          if (tap < 25) {
-            const int ky = tap / 5, kx = tap - ky * 5;
-            acc[k] = fmaf(g, sX[(y + ky) * 32 + xq + kx], acc[k]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int tap = (tid >> 5) + 8 * k;
-      if (tap < 25) {
-        const int64_t idx = oC1W + co * 25 + tap;
-        W[idx] = sgd(a, sl.r, idx, W[idx], acc[k]);
-      }
-    }
-    if (tid < 32) {
-      const int64_t idx = oC1B + co;
-      W[idx] = sgd(a, sl.r, idx, W[idx], bacc);
-    }
-    // conv2 bias: sum of gated pooled gradients
-    for (int c2 = tid; c2 < 64; c2 += 256) {
-      float g = 0.0f;
-      for (int i = 0; i < cnt; ++i) {
-        const float* dp2 = a.dp2 + (s0 + i) * kFlat;
-        const float* p2 = a.p2 + (s0 + i) * kFlat;
-        for (int pp = 0; pp < 49; ++pp) {
-          const int o = pp * 64 + c2;
-          if (p2[o] > 0.0f) g += dp2[o];
-        }
-      }
-      const int64_t idx = oC2B + c2;
-      W[idx] = sgd(a, sl.r, idx, W[idx], g);
-    }
-    return;
-  }
-  // ---- conv2 wgrad on tcgen05: D[co][tap_l*32 + ci] over output positions ----
-  const int tap0 = blockIdx.y * 13, ntap = min(13, 25 - tap0);
+  const int tap0 = blockIdx.y == 0 ? 0 : 7 + (blockIdx.y - 1) * 6;
+  const int ntap = blockIdx.y == 0 ? 7 : 6;
   uint8_t* sP1 = smem;
   uint8_t* sDz = smem + kP1Bytes;
-  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
   if (tid == 0) {
     mbar_init(&mbar, 1);
     fence_init();
@@ -748,7 +760,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<512>(tmem);
+  if (warp == 0) tmem_free<256>(tmem);
 }
 
 }  // namespace
@@ -789,10 +801,16 @@ static Args to_args(const pb_cnn_train_args& t) {
   return a;
 }
 
-static size_t head_smem(int C, int BS) { return size_t(C * kH1 + BS * kH1 + BS * C) * 4; }
+static size_t head_smem(int C, int BS) { return size_t(BS * kH1 + BS * C) * 4; }
 static size_t fc1b_smem(int BS) { return size_t(kH1 * 33 + BS * kH1 + BS * 33) * 4; }
 
-static int launch_sweep(Args& a, int active, bool train, int spb, cudaStream_t s) {
+static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream_t s) {
+  // samples per CTA of the per-sample conv kernels: enough CTAs to fill the
+  // machine in the sparse tail sweeps, amortised weight staging otherwise
+  const int sms = pb::sm_count();
+  int spb = int((int64_t(active) * a.BS + 2 * sms - 1) / (2 * sms));
+  spb = spb < 1 ? 1 : (spb > max_spb ? max_spb : spb);
+  if (max_spb < 0) spb = -max_spb;  // forced (tests)
   const int BSpb = (a.BS + spb - 1) / spb;
   pb::prof_begin(pb::K_CNN_FWD, s);
   k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
@@ -811,7 +829,7 @@ static int launch_sweep(Args& a, int active, bool train, int spb, cudaStream_t s
   k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
-  k_wgrad<<<dim3(active, 3), 256, kWgSmem, s>>>(a);
+  k_wgrad<<<dim3(active, kWgSplit + 1), 256, kWgSmem, s>>>(a);
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
 }
@@ -828,7 +846,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   if (rc) return rc;
   Args a = to_args(t);
   cudaStream_t s = pb::as_stream(stream);
-  const int spb = t.samples_per_cta > 0 ? t.samples_per_cta : 10;
+  const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
   for (int step = 0; step < t.sweeps; ++step) {
     const int active = t.active[step];
     if (active <= 0) break;
