@@ -200,6 +200,13 @@ int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2, void*
 int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K, int a_mode,
                      int b_mode, int shift, void* stream);
 
+/* Issue `iters` back-to-back M x N x 16 bf16 tcgen05 MMAs from smem operands
+ * staged in *_mode layouts (as above), round-robin over `naccum` independent
+ * TMEM accumulators, and store the elapsed cycles (one CTA, device pointer).
+ * Diagnostic for the UMMA throughput table in DESIGN.md. */
+int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, int naccum, long long* cycles,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

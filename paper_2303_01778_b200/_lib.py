@@ -70,6 +70,7 @@ _SIGS = {
     "pb_lr_train_group": (c_int, [POINTER(LrTrainArgs), c_void_p]),
     "pb_lr_eval": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p,
                            c_void_p]),
+    "pb_umma_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
     "pb_cnn_eval": (c_int, [POINTER(CnnTrainArgs), c_int64, c_void_p, c_void_p]),
     "pb_umma_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,

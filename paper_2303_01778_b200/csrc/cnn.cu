@@ -44,6 +44,7 @@ constexpr int kPlane = kRows * 16;   // bytes per plane (8 channels x bf16)
 constexpr int kP1Bytes = 4 * kPlane;   // p1 image, 4 channel planes
 constexpr int kDzBytes = 8 * kPlane;   // dz2 image, 8 channel planes
 constexpr int kW2Bytes = 25 * 4 * 1024;  // conv2 weights in the UMMA B layout
+constexpr int kPg = 800 + 32 + 64;        // per-sample partials: conv1 w, conv1 b, conv2 b
 // flat parameter offsets (models.py cnn_spec)
 constexpr int64_t oC1W = 0, oC1B = 800, oC2W = 832, oC2B = 832 + 51200, oF1W = oC2B + 64,
                   oF1B = oF1W + int64_t(kH1) * kFlat, oF2W = oF1B + kH1;
@@ -79,7 +80,7 @@ struct Args {
   float* dh;       // [slots*BS, kH1]
   float* dp2;      // [slots*BS, kFlat]
   uint8_t* dzg;    // [slots*BS, kDzBytes] bf16 planes
-  float* dp1;      // [slots*BS, kP1]
+  float* pg;       // [slots*BS, kPg] per-sample conv1-w/conv1-b/conv2-b gradient partials
   double* eval;    // [2] correct, loss (eval mode)
   int64_t P;
   int32_t C, BS, bs, epochs, step;
@@ -222,19 +223,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
     __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      const uint32_t pa = smem_u32(sPl), pw = smem_u32(sW2);
-#pragma unroll 1
-      for (int t = 0; t < 2; ++t)
-#pragma unroll 1
-        for (int tap = 0; tap < 25; ++tap) {
-          const int ky = tap / 5, kx = tap - ky * 5;
+      // precomputed descriptors; per MMA only the 14-bit address field moves
+      const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
+      const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint64_t ad = desc(pa + (t * 128 + ky * kG + kx) * 16 + 2 * hh * kPlane, kPlane, 128);
-            const uint64_t bd = desc(pw + (tap * 4 + 2 * hh) * 1024, 1024, 128);
-            mma_bf16(tmem + t * 64, ad, bd, idesc, tap > 0 || hh > 0);
-          }
-        }
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int tap = 0; tap < 25; ++tap)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            mma_bf16(tmem + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
+                     b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc, tap > 0 || hh > 0);
       commit(&mbar);
     }
     // p1 image to global for the backward kernels (overlaps the MMAs)
@@ -496,7 +495,10 @@ __global__ void __launch_bounds__(256) k_fc1_bwd(Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_bwd_conv: dz2 planes (pool2/relu backward) -> conv2 dgrad on tcgen05 -> dp1
+// k_bwd_conv: per sample, dz2 planes (pool2/relu backward) -> conv2 dgrad on
+// tcgen05 -> dp1 (TMEM -> smem) -> pool1/relu backward fused with the conv1
+// weight gradient and the conv1/conv2 bias gradients of this sample
+// (per-sample partials, summed in sample order by k_wgrad: deterministic).
 // grid (active, ceil(BS/spb)), 256 threads
 // ---------------------------------------------------------------------------
 constexpr size_t kBwdSmem = kW2Bytes + kDzBytes;
@@ -508,8 +510,14 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
+  __shared__ float sB2[4][64];
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
+  // after the dgrad MMAs the dz2 region is reused:
+  float* sDp1 = reinterpret_cast<float*>(sDz);           // [196][32] dp1 (25,088 B)
+  float* sX = sDp1 + 196 * 32;                           // [32][32] padded image
+  uint8_t* sAm = reinterpret_cast<uint8_t*>(sX + 1024);  // [196][32] conv1 argmax
+  float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp partials (after sync)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, 256);
   if (warp == 0) tmem_alloc<64>(&tmem_base);
@@ -531,33 +539,32 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     const float* dp2 = a.dp2 + sid * kFlat;
     const float* p2 = a.p2 + sid * kFlat;
     const uint8_t* am2 = a.am2 + sid * kFlat;
+    float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
     for (int o = tid; o < kFlat; o += 256) {
       const int pp = o >> 6, co = o & 63;
       const int py = pp / 7, px = pp - py * 7;
       const int d = am2[o];
       const float g = p2[o] > 0.0f ? dp2[o] : 0.0f;
+      b2part += g;
       const int row = (2 * py + (d >> 1) + 2) * kG + 2 * px + (d & 1) + 2;
       *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) =
           __float2bfloat16(g);
     }
+    sB2[tid >> 6][tid & 63] = b2part;
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      const uint32_t pa = smem_u32(sDz), pw = smem_u32(sW2);
-#pragma unroll 1
-      for (int t = 0; t < 2; ++t)
-#pragma unroll 1
-        for (int tap = 0; tap < 25; ++tap) {
-          const int ky = tap / 5, kx = tap - ky * 5;       // flipped tap
-          const int wt = (4 - ky) * 5 + (4 - kx);
+      const uint64_t a0 = desc(smem_u32(sDz), kPlane, 128);
+      const uint64_t b0 = desc(smem_u32(sW2), 128, 1024);
 #pragma unroll
-          for (int kq = 0; kq < 4; ++kq) {
-            const uint64_t ad = desc(pa + (t * 128 + ky * kG + kx) * 16 + 2 * kq * kPlane, kPlane, 128);
-            const uint64_t bd = desc(pw + wt * 4 * 1024 + kq * 256, 128, 1024);
-            mma_bf16(tmem + t * 32, ad, bd, idesc, tap > 0 || kq > 0);
-          }
-        }
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int tap = 0; tap < 25; ++tap)   // flipped tap: weights (4-ky, 4-kx)
+#pragma unroll
+          for (int kq = 0; kq < 4; ++kq)
+            mma_bf16(tmem + t * 32, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + kq * (2 * kPlane / 16)),
+                     b0 + uint64_t((24 - tap) * 256 + kq * 16), idesc, tap > 0 || kq > 0);
       commit(&mbar);
     }
     {
@@ -568,8 +575,8 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     mbar_wait(&mbar, phase);
     phase ^= 1;
     fence_after_sync();
+    __syncthreads();  // the dz2 copy-out is done: the region can be reused
     if (warp < 4) {
-      float* dp1 = a.dp1 + sid * kP1;
 #pragma unroll 1
       for (int t = 0; t < 2; ++t) {
         const int row = t * 128 + warp * 32 + lane;
@@ -579,14 +586,61 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
         for (int c16 = 0; c16 < 2; ++c16) {
           tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(t * 32 + c16 * 16), v);
           if (y < 14 && x < 14) {
-            float4* d4 = reinterpret_cast<float4*>(dp1 + (y * 14 + x) * kC1 + c16 * 16);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) d4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kC1 + c16 * 16 + k] = v[k];
           }
         }
       }
+    } else {
+      const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+      for (int e = tid - 128; e < 1024; e += 128) {
+        const int yy = e >> 5, xx = e & 31;
+        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+      }
+      const uint8_t* am1 = a.am1 + sid * kP1;
+      for (int e = tid - 128; e < kP1 / 16; e += 128)
+        reinterpret_cast<uint4*>(sAm)[e] = reinterpret_cast<const uint4*>(am1)[e];
     }
     fence_before_sync();
+    __syncthreads();
+    // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
+    // warp w takes pooled positions w, w+8, ...; 26 accumulators per thread
+    {
+      const uint8_t* p1 = a.p1g + sid * kP1Bytes;
+      float acc[25];
+#pragma unroll
+      for (int t = 0; t < 25; ++t) acc[t] = 0.0f;
+      float bacc = 0.0f;
+      const int co = lane;
+      for (int pp = warp; pp < 196; pp += 8) {
+        const int py = pp / 14, px = pp - py * 14;
+        const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+            p1 + (co >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (co & 7) * 2));
+        const float g = pv > 0.0f ? sDp1[pp * kC1 + co] : 0.0f;
+        bacc += g;
+        const int d = sAm[pp * kC1 + co];
+        const float* xw = sX + (2 * py + (d >> 1)) * 32 + 2 * px + (d & 1);
+#pragma unroll
+        for (int ky = 0; ky < 5; ++ky)
+#pragma unroll
+          for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * 32 + kx], acc[ky * 5 + kx]);
+      }
+      __syncthreads();  // all reads of sDp1/sX/sAm done; reuse as reduction scratch
+#pragma unroll
+      for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] = acc[t];
+      sRed[warp * 832 + 800 + co] = bacc;
+    }
+    __syncthreads();
+    {
+      float* pg = a.pg + sid * kPg;
+      for (int k = tid; k < 832; k += 256) {
+        float s8 = 0.0f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s8 += sRed[w * 832 + k];
+        pg[k] = s8;
+      }
+      if (tid < 64) pg[832 + tid] = ((sB2[0][tid] + sB2[1][tid]) + sB2[2][tid]) + sB2[3][tid];
+    }
     __syncthreads();
   }
   if (warp == 0) tmem_free<64>(tmem);
@@ -597,107 +651,53 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
 //          y==2: conv1 wgrad + conv1/conv2 bias grads (SIMT) + update
 // grid (active, 3), 256 threads
 // ---------------------------------------------------------------------------
-constexpr size_t kWgSmem = kP1Bytes + kDzBytes;
-constexpr int kWgSplit = 4;  // conv2 taps split over 4 CTAs: 7,6,6,6 taps -> <=224 TMEM cols
+constexpr int kWgBuf = kP1Bytes + kDzBytes;   // one staged sample (p1 + dz2 planes)
+constexpr size_t kWgSmem = 2 * kWgBuf;         // double-buffered
+constexpr int kWgSplit = 2;                    // conv2 taps split over 2 CTAs: 13 + 12
 
-__device__ void conv1_wgrad_and_biases(const Args& a, const Slot& sl, uint8_t* smem) {
-  const int tid = threadIdx.x, cnt = sl.cnt;
-  float* W = a.w + int64_t(sl.r) * a.P;
-  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  float* sX = reinterpret_cast<float*>(smem);   // [32*32] padded image
-  float* sG = sX + 1024;                        // [196][32] gated dp1
-  float* sRed = sG + 196 * 32;                  // [4][64] conv2-bias partials
-  uint8_t* sAm = reinterpret_cast<uint8_t*>(sRed + 4 * 64);
-  const int co = tid & 31;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  float bacc = 0.0f;
-  // conv2 bias: sum over samples and pooled positions of the gated dp2
-  const int c2 = tid & 63, grp = tid >> 6;
-  float b2acc = 0.0f;
-  for (int i = 0; i < cnt; ++i) {
-    const float* dp2 = a.dp2 + (s0 + i) * kFlat;
-    const float* p2 = a.p2 + (s0 + i) * kFlat;
-    for (int pp = grp; pp < 49; pp += 4) {
-      const int o = pp * 64 + c2;
-      if (p2[o] > 0.0f) b2acc += dp2[o];
-    }
-  }
-  sRed[grp * 64 + c2] = b2acc;
-  for (int i = 0; i < cnt; ++i) {
-    const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
-    for (int e = tid; e < 1024; e += 256) {
-      const int yy = e >> 5, xx = e & 31;
-      sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
-    }
-    const uint8_t* p1 = a.p1g + (s0 + i) * kP1Bytes;
-    for (int e = tid; e < kP1; e += 256) {
-      const int pp = e >> 5, c = e & 31;
-      const int py = pp / 14, px = pp - py * 14;
-      const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-          p1 + (c >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (c & 7) * 2));
-      sG[e] = pv > 0.0f ? a.dp1[(s0 + i) * kP1 + e] : 0.0f;
-      sAm[e] = a.am1[(s0 + i) * kP1 + e];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int pp = 0; pp < 196; ++pp) {
-      const float g = sG[pp * 32 + co];
-      if (tid < 32) bacc += g;
-      const int d = sAm[pp * 32 + co];
-      const int py = pp / 14, px = pp - py * 14;
-      const int y = 2 * py + (d >> 1), xq = 2 * px + (d & 1);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int tap = (tid >> 5) + 8 * k;
-        if (tap < 25) {
-          const int ky = tap / 5, kx = tap - ky * 5;
-          acc[k] = fmaf(g, sX[(y + ky) * 32 + xq + kx], acc[k]);
-        }
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int tap = (tid >> 5) + 8 * k;
-    if (tap < 25) {
-      const int64_t idx = oC1W + co * 25 + tap;
-      W[idx] = sgd(a, sl.r, idx, W[idx], acc[k]);
-    }
-  }
-  if (tid < 32) {
-    const int64_t idx = oC1B + co;
-    W[idx] = sgd(a, sl.r, idx, W[idx], bacc);
-  }
-  if (tid < 64) {
-    const float g = ((sRed[tid] + sRed[64 + tid]) + sRed[128 + tid]) + sRed[192 + tid];
-    const int64_t idx = oC2B + tid;
-    W[idx] = sgd(a, sl.r, idx, W[idx], g);
-  }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// k_wgrad: y < 4: conv2 wgrad for a quarter of the taps on tcgen05 + update;
-//          y == 4: conv1 wgrad + conv1/conv2 bias gradients (SIMT) + update
-// grid (active, 5), 256 threads, 2 CTAs per SM
-__global__ void __launch_bounds__(256, 2) k_wgrad(Args a) {
+__device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* buf, int tid) {
+  const uint8_t* s1 = a.p1g + sid * kP1Bytes;
+  const uint8_t* s2 = a.dzg + sid * kDzBytes;
+  for (int e = tid; e < kP1Bytes / 16; e += 256) cp_async16(buf + e * 16, s1 + e * 16);
+  for (int e = tid; e < kDzBytes / 16; e += 256) cp_async16(buf + kP1Bytes + e * 16, s2 + e * 16);
+  cp_async_commit();
+}
+
+// k_wgrad: y < 2: conv2 wgrad for half of the taps on tcgen05 (double-buffered
+//          sample staging overlaps the MMAs) + update;
+//          y == 2: sum the per-sample conv1/bias partials (sample order) + update
+// grid (active, 3), 256 threads
+__global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
-  if (blockIdx.y == kWgSplit) {
-    conv1_wgrad_and_biases(a, sl, smem);
-    return;
-  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = sl.cnt;
   float* W = a.w + int64_t(sl.r) * a.P;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  const int tap0 = blockIdx.y == 0 ? 0 : 7 + (blockIdx.y - 1) * 6;
-  const int ntap = blockIdx.y == 0 ? 7 : 6;
-  uint8_t* sP1 = smem;
-  uint8_t* sDz = smem + kP1Bytes;
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (blockIdx.y == kWgSplit) {
+    for (int k = tid; k < kPg; k += 256) {
+      float g = 0.0f;
+      for (int i = 0; i < cnt; ++i) g += a.pg[(s0 + i) * kPg + k];
+      const int64_t idx = k < 800 ? oC1W + k : (k < 832 ? oC1B + (k - 800) : oC2B + (k - 832));
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+    }
+    return;
+  }
+  const int tap0 = blockIdx.y * 13, ntap = blockIdx.y == 0 ? 13 : 12;
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     mbar_init(&mbar, 1);
     fence_init();
@@ -707,38 +707,41 @@ __global__ void __launch_bounds__(256, 2) k_wgrad(Args a) {
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = idesc_bf16(64, 32, true, true);
-  uint32_t phase = 0;
+  wg_stage(a, s0, smem, tid);
   for (int i = 0; i < cnt; ++i) {
-    {
-      const uint4* s1 = reinterpret_cast<const uint4*>(a.p1g + (s0 + i) * kP1Bytes);
-      const uint4* s2 = reinterpret_cast<const uint4*>(a.dzg + (s0 + i) * kDzBytes);
-      for (int e = tid; e < kP1Bytes / 16; e += 256) reinterpret_cast<uint4*>(sP1)[e] = s1[e];
-      for (int e = tid; e < kDzBytes / 16; e += 256) reinterpret_cast<uint4*>(sDz)[e] = s2[e];
+    uint8_t* buf = smem + (i & 1) * kWgBuf;
+    if (i + 1 < cnt) {
+      if (i >= 1) mbar_wait(&mbar, (i - 1) & 1);  // MMAs of sample i-1 read the other buffer
+      wg_stage(a, s0 + i + 1, smem + ((i + 1) & 1) * kWgBuf, tid);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      const uint32_t pz = smem_u32(sDz), pp1 = smem_u32(sP1);
+      // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[ci][p] = p1 row p + ky*18 + kx
+      const uint64_t a0 = desc(smem_u32(buf) + kP1Bytes, 128, kPlane) + uint64_t(2 * kG + 2);
+      const uint64_t b00 = desc(smem_u32(buf), 128, kPlane);
 #pragma unroll 1
       for (int tl = 0; tl < ntap; ++tl) {
-        const int tap = tap0 + tl, ky = tap / 5, kx = tap - ky * 5;
-#pragma unroll 4
-        for (int ks = 0; ks < 16; ++ks) {
-          // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[ci][p] = p1 row p + ky*18 + kx
-          const uint64_t ad = desc(pz + (2 * kG + 2 + ks * 16) * 16, 128, kPlane);
-          const uint64_t bd = desc(pp1 + (ky * kG + kx + ks * 16) * 16, 128, kPlane);
-          mma_bf16(tmem + tl * 32, ad, bd, idesc, i > 0 || ks > 0);
-        }
+        const int tap = tap0 + tl;
+        const uint64_t b0 = b00 + uint64_t((tap / 5) * kG + tap % 5);
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks)
+          mma_bf16(tmem + tl * 32, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), idesc,
+                   i > 0 || ks > 0);
       }
       commit(&mbar);
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    fence_after_sync();
-    __syncthreads();
   }
-  // epilogue: M=64 rows live in lanes 32q + [0,16) of each quarter q
+  mbar_wait(&mbar, (cnt - 1) & 1);
+  fence_after_sync();
+  // epilogue: TMEM (M=64 rows in lanes 32q + [0,16)) -> smem tile [64][ntap*32]
+  // -> coalesced SGD update of the contiguous W2[co][tap0*32 ...] row segments
+  float* sG = reinterpret_cast<float*>(smem);  // 64 x 416 fp32 = 106 KB (buffers are free)
+  const int width = ntap * 32;
   {
     const int q = warp & 3, part = warp >> 2;
     const int co = q * 16 + lane;
@@ -750,17 +753,21 @@ __global__ void __launch_bounds__(256, 2) k_wgrad(Args a) {
         tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(tl * 32 + c16 * 16), v);
         if (lane < 16) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int64_t idx = oC2W + int64_t(co) * 800 + (tap0 + tl) * 32 + c16 * 16 + k;
-            W[idx] = sgd(a, sl.r, idx, W[idx], v[k]);
-          }
+          for (int k = 0; k < 16; ++k) sG[co * (13 * 32 + 1) + tl * 32 + c16 * 16 + k] = v[k];
         }
       }
     }
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  for (int e = tid; e < 64 * width; e += 256) {
+    const int co = e / width, c = e - co * width;
+    const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
+    W[idx] = sgd(a, sl.r, idx, W[idx], sG[co * (13 * 32 + 1) + c]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(tmem);
 }
 
 }  // namespace
@@ -794,7 +801,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
-  a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.dp1 = t.ws_dp1; a.eval = nullptr;
+  a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
   a.P = oF2W + int64_t(t.C) * kH1 + t.C;
   a.lr = t.lr; a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;

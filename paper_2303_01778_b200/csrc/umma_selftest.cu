@@ -103,3 +103,75 @@ extern "C" int pb_umma_selftest(const void* A, const void* B, float* D, int M, i
       a_mode, b_mode, shift);
   return pb::check_launch("pb_umma_selftest");
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: tcgen05 issue throughput for a given shape/layout.  One CTA
+// issues `iters` MMAs (K=16 each, operands resident in smem) back to back and
+// reports the cycles from first issue to completion.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128) umma_bench_kernel(int M, int N, int a_mode, int b_mode,
+                                                         int iters, int naccum, long long* cycles) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int K = 64;  // operands hold 4 k-steps; we cycle over them
+  for (int i = tid; i < (M + 8 + N + 8) * K / 8; i += 128)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0x3f803f80u);
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    uint32_t al, as, ak, bl, bs, bk;
+    mode_desc(a_mode, M, K, al, as, ak);
+    mode_desc(b_mode, N, K, bl, bs, bk);
+    const uint32_t a0 = smem_u32(smem), b0 = a0 + (M + 8) * K * 2;
+    const uint32_t idesc = idesc_bf16(M, N, a_mode == 1, b_mode == 1);
+    // precomputed descriptors; the k-step advances only the 14-bit address field
+    const uint64_t ad0 = desc(a0, al, as), bd0 = desc(b0, bl, bs);
+    const uint64_t da = ak >> 4, db = bk >> 4;
+    const long long t0 = clock64();
+    if (naccum == 1) {
+      mma_bf16(tbase, ad0, bd0, idesc, false);
+#pragma unroll 1
+      for (int it = 1; it < iters; it += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mma_bf16(tbase, ad0 + u * da, bd0 + u * db, idesc, true);
+      }
+    } else {
+#pragma unroll 1
+      for (int it = 0; it < iters; it += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          mma_bf16(tbase + (u % naccum) * N, ad0 + u * da, bd0 + u * db, idesc, it > 0);
+      }
+    }
+    commit(&mbar);
+    mbar_wait(&mbar, 0);
+    cycles[0] = clock64() - t0;
+  }
+  __syncthreads();
+  if (tid != 0) mbar_wait(&mbar, 0);
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tbase);
+}
+}  // namespace
+
+extern "C" int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, int naccum,
+                             long long* cycles, void* stream) {
+  if (naccum < 1 || naccum * N > 256) return pb::fail(PB_ERR_INVALID, "pb_umma_bench: accumulators");
+  const size_t smem = size_t(M + 8 + N + 8) * 64 * 2;
+  cudaFuncSetAttribute(umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  umma_bench_kernel<<<1, 128, smem, pb::as_stream(stream)>>>(M, N, a_mode, b_mode, iters, naccum,
+                                                             cycles);
+  return pb::check_launch("pb_umma_bench");
+}
