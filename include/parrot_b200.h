@@ -149,7 +149,8 @@ int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F, int C, con
  *     caller-allocated, sized per slot (= client) for BS samples:
  *       ws_slots 16 B, ws_p1 BS*21504 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
  *       ws_am2 BS*3136 B, ws_h/ws_dh BS*512 f32, ws_dp2 BS*3136 f32,
- *       ws_dz BS*43008 B, ws_dp1 BS*6272 f32.
+ *       ws_dz BS*43008 B, ws_dp1 BS*6272 f32 (per-sample conv1/bias gradient
+ *       partials, 896 used), ws_dht 16384 f32 per slot.
  * ------------------------------------------------------------------------- */
 typedef struct {
   const float* X;           /* [rows, 784] fp32 images                        */
@@ -160,7 +161,8 @@ typedef struct {
   const int32_t* rank;      /* [g] slot -> client row, by step count desc     */
   const int32_t* active;    /* HOST [sweeps]: clients still stepping per sweep*/
   int32_t sweeps;
-  float* w;                 /* [g, P] params (start = w0), updated in place   */
+  float* w;                 /* [g, w_stride] params (start = w0), in place    */
+  int64_t w_stride;         /* row stride of w in floats, multiple of 4       */
   const float* w0;          /* [P]                                            */
   const float* ctrl_g;      /* [P] or NULL                                    */
   const float* ctrl_c;      /* [g, ctrl_stride] or NULL                       */
@@ -178,6 +180,7 @@ typedef struct {
   float* ws_dp2;
   uint8_t* ws_dz;
   float* ws_dp1;
+  float* ws_dht;            /* per slot: 512*32 f32 (dH transposed, zero-padded) */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;
@@ -199,6 +202,11 @@ int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2, void*
  * conventions the conv kernels use (tests only). */
 int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K, int a_mode,
                      int b_mode, int shift, void* stream);
+
+/* 128 x N x K tf32 tcgen05 GEMM D = A * B^T from fp32 row-major A [128,K],
+ * B [N,K]; a_mn/b_mn select MN-major smem staging (tests only). */
+int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,
+                          int b_mn, void* stream);
 
 /* Issue `iters` back-to-back M x N x 16 bf16 tcgen05 MMAs from smem operands
  * staged in *_mode layouts (as above), round-robin over `naccum` independent

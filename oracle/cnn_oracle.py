@@ -66,13 +66,42 @@ class _RoundGrad(torch.autograd.Function):
         return g.to(torch.bfloat16).to(g.dtype)
 
 
+def _tf32(x: torch.Tensor) -> torch.Tensor:
+    """fp32 -> tf32 by truncation (how tcgen05 kind::tf32 reads fp32 operands,
+    measured in tests/test_gpu_umma.py)."""
+    f = x.to(torch.float32).contiguous()
+    return (f.view(torch.int32) & -8192).view(torch.float32).to(x.dtype)
+
+
+class _TruncValue(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return _tf32(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+class _TruncGrad(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return _tf32(g)
+
+
 def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor:
     """x [B, 784] -> logits; conv weights are NHWC ([co, ky, kx, ci]).
 
     emulate_bf16=True rounds exactly the operands the device feeds to its
-    tcgen05 conv2 GEMMs (p1 and W2 in the forward, dL/dz2 in both backward
-    GEMMs); everything else stays in the oracle's precision.  Used to check the
-    kernels' arithmetic separately from bf16's effect on the trajectory."""
+    tensor cores -- bf16 for conv2 (p1 and W2 in the forward, dL/dz2 in both
+    backward GEMMs) and tf32 truncation for fc1 (X and W1 in the forward, dL/dz1
+    in both backward GEMMs); everything else stays in the oracle's precision.
+    Used to check the kernels' arithmetic separately from the effect of the
+    reduced-precision operands on the trajectory."""
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
     h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
@@ -82,7 +111,10 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor
     else:
         h = F.max_pool2d(F.relu(F.conv2d(h, c2w.permute(0, 3, 1, 2), c2b, padding=2)), 2)
     h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)  # NHWC flatten
-    h = F.relu(h @ f1w.t() + f1b)
+    if emulate_bf16:
+        h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ _TruncValue.apply(f1w).t()) + f1b)
+    else:
+        h = F.relu(h @ f1w.t() + f1b)
     return h @ f2w.t() + f2b
 
 

@@ -33,11 +33,12 @@ class CnnTrainArgs(ctypes.Structure):
     _fields_ = [
         ("X", c_void_p), ("Y", c_void_p), ("order", c_void_p), ("order_off", c_void_p),
         ("n", c_void_p), ("rank", c_void_p), ("active", c_void_p), ("sweeps", c_int32),
-        ("w", c_void_p), ("w0", c_void_p), ("ctrl_g", c_void_p), ("ctrl_c", c_void_p),
+        ("w", c_void_p), ("w_stride", c_int64), ("w0", c_void_p), ("ctrl_g", c_void_p),
+        ("ctrl_c", c_void_p),
         ("ctrl_stride", c_int64), ("loss_sum", c_void_p), ("steps", c_void_p), ("bad", c_void_p),
         ("ws_slots", c_void_p), ("ws_p1", c_void_p), ("ws_am1", c_void_p), ("ws_p2", c_void_p),
         ("ws_am2", c_void_p), ("ws_h", c_void_p), ("ws_dh", c_void_p), ("ws_dp2", c_void_p),
-        ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("g", c_int64),
+        ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("ws_dht", c_void_p), ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),
@@ -70,6 +71,8 @@ _SIGS = {
     "pb_lr_train_group": (c_int, [POINTER(LrTrainArgs), c_void_p]),
     "pb_lr_eval": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p,
                            c_void_p]),
+    "pb_umma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                      c_void_p]),
     "pb_umma_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
     "pb_cnn_eval": (c_int, [POINTER(CnnTrainArgs), c_int64, c_void_p, c_void_p]),

@@ -33,6 +33,7 @@ class _Workspace:
             self.buf = {k: torch.empty(n * v, dtype=torch.uint8, device=device)
                         for k, v in _PER_SAMPLE.items()}
             self.buf["slots"] = torch.empty(self.slots * 16, dtype=torch.uint8, device=device)
+            self.buf["dht"] = torch.empty(self.slots * 512 * 32 * 4, dtype=torch.uint8, device=device)
         return self.buf
 
 
@@ -45,7 +46,7 @@ def _samples_per_cta() -> int:
 
 def _fill(args: CnnTrainArgs, ws: dict, slots: int, BS: int) -> None:
     args.ws_slots = ptr(ws["slots"])
-    for k in ("p1", "am1", "p2", "am2", "h", "dh", "dp2", "dz", "dp1"):
+    for k in ("p1", "am1", "p2", "am2", "h", "dh", "dp2", "dz", "dp1", "dht"):
         setattr(args, "ws_" + k, ptr(ws[k]))
     args.g = slots
     args.BS = BS
@@ -87,6 +88,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     a.active = active.ctypes.data
     a.sweeps = len(active)
     a.w, a.w0 = ptr(w_out), ptr(w0)
+    a.w_stride = w_out.stride(0)
     a.ctrl_g = ptr(terms.get("ctrl_g"))
     ctrl_c = state_work if terms.get("ctrl_c") else None
     a.ctrl_c = ptr(ctrl_c)
@@ -117,6 +119,7 @@ def cnn_evaluate(model, X: torch.Tensor, Y: torch.Tensor) -> tuple[float, float]
     a = CnnTrainArgs()
     a.X, a.Y, a.order = ptr(X), ptr(Y), ptr(order)
     a.w = a.w0 = ptr(w)
+    a.w_stride = (w.numel() + 3) // 4 * 4
     _fill(a, ws, slots, BS)
     a.C, a.batch_size, a.epochs = spec.n_classes, BS, 1
     out = torch.zeros(2, dtype=torch.float64, device=X.device)

@@ -78,6 +78,7 @@ struct Args {
   uint8_t* am2;    // [slots*BS, kFlat]
   float* h;        // [slots*BS, kH1]
   float* dh;       // [slots*BS, kH1]
+  float* dht;      // [slots, kH1, 32] dH transposed, samples zero-padded to 32
   float* dp2;      // [slots*BS, kFlat]
   uint8_t* dzg;    // [slots*BS, kDzBytes] bf16 planes
   float* pg;       // [slots*BS, kPg] per-sample conv1-w/conv1-b/conv2-b gradient partials
@@ -100,6 +101,22 @@ __device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j
 // hide a diverged client from the non-finite check)
 __device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
 __device__ __forceinline__ bool takes_max(float z, float best) { return z > best || z != z; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// zero-fills the 16 bytes when !valid (src is not read)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
   // UMMA B layout, K-major over (tap, ci): core matrix = 8 co x 8 ci
@@ -292,46 +309,102 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fc1_fwd: h = relu(p2 W1^T + b1); grid (active, 512/64), 256 threads
+// fc1 on tensor cores (kind::tf32: the fp32 master weights feed the MMA
+// straight from smem).  fc1 holds 95% of the client's parameters and every
+// client has its own copy, so the layer is HBM-bound: the forward streams W1
+// once (4 B/param), the backward once more plus one write-back (8 B/param).
+// fp32 K-major operand tiles: core matrix = 8 rows x 16 B (4 elements).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_fc1_fwd(Args a) {
+constexpr int kF1KC = 64;                        // K (fp32 elements) per pipeline stage
+constexpr int kF1SBO = (kF1KC / 4) * 128;        // row-group stride of a [rows x 64] tile
+constexpr int kF1ABytes = 128 * kF1KC * 4;       // 32 KB
+constexpr int kF1BBytes = 32 * kF1KC * 4;        // 8 KB
+constexpr size_t kF1FwdSmem = 2 * (kF1ABytes + kF1BBytes);
+
+__device__ __forceinline__ uint32_t kmaj_f32(int r, int k4, int sbo) {
+  return uint32_t((r >> 3) * sbo + k4 * 128 + (r & 7) * 16);
+}
+
+// k_fc1_fwd: h = relu(p2 W1^T + b1); CTA = (client, 128 output rows)
+// D[o][i] (M=128, N=32, K=3136 in 49 stages of 64); grid (active, 4), 128 thr
+__global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
-  __shared__ float sW[64][33];
-  __shared__ float sA[32][33];
-  const int tid = threadIdx.x;
-  const int o0 = blockIdx.y * 64;
-  const float* W1 = a.w + int64_t(sl.r) * a.P + oF1W;
-  const float* p2 = a.p2 + sidx(blockIdx.x, 0, a.BS) * kFlat;
-  const int ol = tid & 63, ig = tid >> 6;  // 4 sample groups
-  const int nper = (sl.cnt + 3) / 4;
-  float acc[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
-  for (int k0 = 0; k0 < kFlat; k0 += 32) {
-    for (int e = tid; e < 64 * 32; e += 256) {
-      const int r = e >> 5, c = e & 31;
-      sW[r][c] = W1[int64_t(o0 + r) * kFlat + k0 + c];
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cnt = sl.cnt;
+  const int o0 = blockIdx.y * 128;
+  const float* W = a.w + int64_t(sl.r) * a.P;
+  const float* W1 = W + oF1W + int64_t(o0) * kFlat;
+  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
+  const float* X = a.p2 + s0 * kFlat;
+  auto stage = [&](int c, int buf) {
+    uint8_t* sa = smem + buf * (kF1ABytes + kF1BBytes);
+    uint8_t* sb = sa + kF1ABytes;
+    const int k0 = c * kF1KC;
+    for (int e = tid; e < 128 * (kF1KC / 4); e += 128) {
+      const int r = e >> 4, k4 = e & 15;
+      cp_async16(sa + kmaj_f32(r, k4, kF1SBO), W1 + int64_t(r) * kFlat + k0 + k4 * 4);
     }
-    for (int e = tid; e < 32 * 32; e += 256) {
-      const int r = e >> 5, c = e & 31;
-      sA[r][c] = r < sl.cnt ? p2[int64_t(r) * kFlat + k0 + c] : 0.0f;
+    for (int e = tid; e < 32 * (kF1KC / 4); e += 128) {
+      const int r = e >> 4, k4 = e & 15;
+      cp_async16_zfill(sb + kmaj_f32(r, k4, kF1SBO), X + int64_t(r < cnt ? r : 0) * kFlat + k0 + k4 * 4,
+                       r < cnt);
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < 32; ++kk) {
-      const float w = sW[ol][kk];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (k < nper) acc[k] = fmaf(sA[ig + 4 * k][kk], w, acc[k]);
-    }
-    __syncthreads();
+    cp_async_commit();
+  };
+  if (warp == 0) tmem_alloc<32>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
   }
-  const float b = a.w[int64_t(sl.r) * a.P + oF1B + o0 + ol];
-  for (int k = 0; k < nper; ++k) {
-    const int i = ig + 4 * k;
-    if (i < sl.cnt) a.h[sidx(blockIdx.x, i, a.BS) * kH1 + o0 + ol] = relu_nan(acc[k] + b);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = idesc_tf32(128, 32);
+  constexpr int kChunks = kFlat / kF1KC;  // 49
+  stage(0, 0);
+  for (int c = 0; c < kChunks; ++c) {
+    if (c + 1 < kChunks) {
+      if (c >= 1) mbar_wait(&mbar, (c - 1) & 1);  // MMAs reading the other buffer are done
+      stage(c + 1, (c + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const uint32_t sa = smem_u32(smem + (c & 1) * (kF1ABytes + kF1BBytes));
+      const uint64_t a0 = desc(sa, 128, kF1SBO), b0 = desc(sa + kF1ABytes, 128, kF1SBO);
+#pragma unroll
+      for (int kk = 0; kk < kF1KC / 8; ++kk)
+        mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
+      commit(&mbar);
+    }
   }
+  mbar_wait(&mbar, (kChunks - 1) & 1);
+  fence_after_sync();
+  {
+    const int o = o0 + warp * 32 + lane;
+    const float b = W[oF1B + o];
+    float v[16];
+#pragma unroll
+    for (int c16 = 0; c16 < 2; ++c16) {
+      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c16 * 16), v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = c16 * 16 + k;
+        if (i < cnt) a.h[(s0 + i) * kH1 + o] = relu_nan(v[k] + b);
+      }
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<32>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -357,6 +430,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   const int C = a.C, cnt = sl.cnt, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* sH = hs;                      // [cnt][512]
   float* sL = sH + cnt * kH1;          // [cnt][C] logits -> dlogits
+  float* sDH = sL + cnt * a.C;         // [cnt][512] dH
   __shared__ double scratch[kHeadThreads / 32];
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
@@ -421,15 +495,24 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
     a.slots[blockIdx.x].cnt = 0;  // later kernels of this sweep skip the client
     return;
   }
-  // dH = dlogits W2 (old weights) masked by relu'
+  // dH = dlogits W2 (old weights) masked by relu'; stored [i][o] and [o][i<32]
   float* dh = a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
   for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
     const int i = p >> 9, o = p & (kH1 - 1);
     float s = 0.0f;
     for (int c = 0; c < C; ++c) s = fmaf(sL[i * C + c], W2[int64_t(c) * kH1 + o], s);
-    dh[p] = sH[p] > 0.0f ? s : 0.0f;
+    const float g = sH[p] > 0.0f ? s : 0.0f;
+    dh[p] = g;
+    sDH[p] = g;
   }
   __syncthreads();  // every read of the old W2 is done before the update
+  {
+    float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
+    for (int p = tid; p < kH1 * 32; p += kHeadThreads) {
+      const int o = p >> 5, i = p & 31;
+      dht[p] = i < cnt ? sDH[i * kH1 + o] : 0.0f;
+    }
+  }
   for (int p = tid; p < C * kH1; p += kHeadThreads) {
     const int c = p >> 9, o = p & (kH1 - 1);
     float g = 0.0f;
@@ -446,52 +529,166 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fc1_bwd: dP2 = dH W1, dW1 = dH^T p2, W1 -= lr dW1 (one pass over W1)
-// grid (active, 3136/32), 256 threads
+// k_fc1_bwd: one pass over a 64-column slice of W1 per CTA (tf32 UMMA):
+//   dgrad  D1[k][i] = sum_o W1[o][k] dH[i][o]   (M=64, N=32, K=512, 8 stages)
+//   wgrad  D2[o][k] = sum_i dHt[o][i] X[i][k]   (4 x M=128, N=64, K=32)
+//   update W1[o][k] -= lr * (D2 + plugin terms); b1 by the k0 == 0 CTA
+// W1 is staged transposed (SIMT) so every operand is K-major.
+// grid (active, 3136/64), 128 threads, 1 CTA/SM
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_fc1_bwd(Args a) {
+constexpr int kB1A = 64 * 64 * 4;            // dgrad A stage: W1^T [64 k x 64 o]
+constexpr int kB1B = 32 * 64 * 4;            // dgrad B stage: dH [32 i x 64 o]
+constexpr int kB2A = kH1 * 32 * 4;           // wgrad A: dHt [512 o x 32 i]
+constexpr int kB2B = 64 * 32 * 4;            // wgrad B: X^T [64 k x 32 i]
+constexpr size_t kF1BwdSmem = 2 * (kB1A + kB1B) + kB2A + kB2B;   // 120 KB
+
+__global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
-  extern __shared__ float fs[];
-  float* sW = fs;                   // [512][33]
-  float* sDH = sW + kH1 * 33;       // [cnt][512]
-  float* sA = sDH + sl.cnt * kH1;   // [cnt][33]
-  const int tid = threadIdx.x, cnt = sl.cnt;
-  const int k0 = blockIdx.y * 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar[3];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cnt = sl.cnt;
+  const int k0 = blockIdx.y * 64;
   float* W = a.w + int64_t(sl.r) * a.P;
   float* W1 = W + oF1W;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  for (int e = tid; e < kH1 * 32; e += 256) {
-    const int o = e >> 5, c = e & 31;
-    sW[o * 33 + c] = W1[int64_t(o) * kFlat + k0 + c];
+  const float* dh = a.dh + s0 * kH1;
+  const float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
+  const float* X = a.p2 + s0 * kFlat;
+  uint8_t* sA2 = smem + 2 * (kB1A + kB1B);
+  uint8_t* sB2 = sA2 + kB2A;
+  // wgrad operands: dHt rows (cp.async, K-major (o/8, i/4)), X^T (SIMT transpose)
+  for (int e = tid; e < kH1 * 8; e += 256) {
+    const int o = e >> 3, i4 = e & 7;
+    cp_async16(sA2 + (o >> 3) * 1024 + i4 * 128 + (o & 7) * 16, dht + o * 32 + i4 * 4);
   }
-  for (int e = tid; e < cnt * kH1; e += 256) sDH[e] = a.dh[s0 * kH1 + e];
-  for (int e = tid; e < cnt * 32; e += 256) {
-    const int i = e >> 5, c = e & 31;
-    sA[i * 33 + c] = a.p2[(s0 + i) * kFlat + k0 + c];
+  cp_async_commit();
+  for (int e = tid; e < 32 * 64; e += 256) {
+    const int i = e >> 6, kk = e & 63;
+    const float v = i < cnt ? X[int64_t(i) * kFlat + k0 + kk] : 0.0f;
+    *reinterpret_cast<float*>(sB2 + (kk >> 3) * 1024 + (i >> 2) * 128 + (kk & 7) * 16 + (i & 3) * 4) = v;
   }
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], 1);
+    fence_init();
+  }
+  fence_before_sync();
   __syncthreads();
-  for (int p = tid; p < cnt * 32; p += 256) {
-    const int i = p >> 5, c = p & 31;
-    float s = 0.0f;
-    for (int o = 0; o < kH1; ++o) s = fmaf(sDH[i * kH1 + o], sW[o * 33 + c], s);
-    a.dp2[(s0 + i) * kFlat + k0 + c] = s;
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  // W1[oc + o][k0 .. k0+63] for one o-chunk: 1024 float4, 4 per thread, kept in
+  // registers one chunk ahead of the MMAs
+  float4 pre[4];
+  auto load_chunk = [&](int c) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
+      pre[j] = *reinterpret_cast<const float4*>(W1 + int64_t(c * 64 + o) * kFlat + k0 + k4 * 4);
+    }
+  };
+  load_chunk(0);
+  for (int c = 0; c < kH1 / 64; ++c) {
+    const int buf = c & 1;
+    uint8_t* sA = smem + buf * (kB1A + kB1B);
+    uint8_t* sB = sA + kB1A;
+    if (c >= 2) mbar_wait(&mbar[buf], ((c - 2) >> 1) & 1);
+    const int oc = c * 64;
+    for (int e = tid; e < 32 * 16; e += 256) {  // dH rows i, 64 o: 16 chunks each
+      const int i = e >> 4, o4 = e & 15;
+      cp_async16_zfill(sB + (i >> 3) * 2048 + o4 * 128 + (i & 7) * 16,
+                       dh + int64_t(i < cnt ? i : 0) * kH1 + oc + o4 * 4, i < cnt);
+    }
+    cp_async_commit();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // transpose into A[k][o] (K-major over o)
+      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
+      const float vv[4] = {pre[j].x, pre[j].y, pre[j].z, pre[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kk = k4 * 4 + q;
+        *reinterpret_cast<float*>(sA + (kk >> 3) * 2048 + (o >> 2) * 128 + (kk & 7) * 16 + (o & 3) * 4) = vv[q];
+      }
+    }
+    if (c + 1 < kH1 / 64) load_chunk(c + 1);  // in flight during the sync + MMAs
+    cp_async_wait<0>();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const uint64_t a0 = desc(smem_u32(sA), 128, 2048), b0 = desc(smem_u32(sB), 128, 2048);
+      const uint32_t idesc = idesc_tf32(64, 32);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
+      commit(&mbar[buf]);
+    }
   }
-  const int c = tid & 31;
-  for (int o = tid >> 5; o < kH1; o += 8) {
-    float g = 0.0f;
-    for (int i = 0; i < cnt; ++i) g = fmaf(sDH[i * kH1 + o], sA[i * 33 + c], g);
-    const int64_t idx = oF1W + int64_t(o) * kFlat + k0 + c;
-    W[idx] = sgd(a, sl.r, idx, sW[o * 33 + c], g);
+  if (tid == 0) {
+    fence_after_sync();
+    const uint32_t idesc = idesc_tf32(128, 64);
+    const uint64_t a0 = desc(smem_u32(sA2), 128, 1024), b0 = desc(smem_u32(sB2), 128, 1024);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_tf32(tmem + 64 + t * 64, a0 + uint64_t(t * 1024 + kk * 16), b0 + uint64_t(kk * 16), idesc,
+                 kk > 0);
+    commit(&mbar[2]);
+  }
+  mbar_wait(&mbar[0], 1);  // chunks 6 and 7 (buffers 0/1, 4th completion each)
+  mbar_wait(&mbar[1], 1);
+  mbar_wait(&mbar[2], 0);
+  fence_after_sync();
+  const int q = warp & 3, half = warp >> 2;
+  // dgrad epilogue (M=64: rows k in lanes 32q + [0,16)): dp2[i][k0+k]
+  {
+    const int k = q * 16 + lane;
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 16), v);
+    if (lane < 16) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int i = half * 16 + j;
+        if (i < cnt) a.dp2[(s0 + i) * kFlat + k0 + k] = v[j];
+      }
+    }
+  }
+  // wgrad epilogue: row o of each tile, 32 of the 64 columns per warp half
+#pragma unroll 1
+  for (int t = 0; t < 4; ++t) {
+    const int o = t * 128 + q * 32 + lane;
+    float* wrow = W1 + int64_t(o) * kFlat + k0 + half * 32;
+    const int64_t base = oF1W + int64_t(o) * kFlat + k0 + half * 32;
+    float4 w4[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w4[j] = reinterpret_cast<const float4*>(wrow)[j];
+    float v[32];
+    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32), *reinterpret_cast<float(*)[16]>(v));
+    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32 + 16),
+              *reinterpret_cast<float(*)[16]>(v + 16));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t id = base + j * 4;
+      w4[j].x = sgd(a, sl.r, id + 0, w4[j].x, v[j * 4 + 0]);
+      w4[j].y = sgd(a, sl.r, id + 1, w4[j].y, v[j * 4 + 1]);
+      w4[j].z = sgd(a, sl.r, id + 2, w4[j].z, v[j * 4 + 2]);
+      w4[j].w = sgd(a, sl.r, id + 3, w4[j].w, v[j * 4 + 3]);
+      reinterpret_cast<float4*>(wrow)[j] = w4[j];
+    }
   }
   if (blockIdx.y == 0) {
     for (int o = tid; o < kH1; o += 256) {
       float g = 0.0f;
-      for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
+      for (int i = 0; i < 32; ++i) g += dht[o * 32 + i];
       const int64_t idx = oF1B + o;
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
   }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -655,16 +852,6 @@ constexpr int kWgBuf = kP1Bytes + kDzBytes;   // one staged sample (p1 + dz2 pla
 constexpr size_t kWgSmem = 2 * kWgBuf;         // double-buffered
 constexpr int kWgSplit = 2;                    // conv2 taps split over 2 CTAs: 13 + 12
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* buf, int tid) {
   const uint8_t* s1 = a.p1g + sid * kP1Bytes;
   const uint8_t* s2 = a.dzg + sid * kDzBytes;
@@ -789,7 +976,8 @@ static int cnn_setup() {
   if ((rc = set_smem((const void*)k_bwd_conv, kBwdSmem, "k_bwd_conv"))) return rc;
   if ((rc = set_smem((const void*)k_wgrad, kWgSmem, "k_wgrad"))) return rc;
   if ((rc = set_smem((const void*)k_head, 200 * 1024, "k_head"))) return rc;
-  if ((rc = set_smem((const void*)k_fc1_bwd, 200 * 1024, "k_fc1_bwd"))) return rc;
+  if ((rc = set_smem((const void*)k_fc1_bwd, kF1BwdSmem, "k_fc1_bwd"))) return rc;
+  if ((rc = set_smem((const void*)k_fc1_fwd, kF1FwdSmem, "k_fc1_fwd"))) return rc;
   done = 1;
   return PB_OK;
 }
@@ -801,15 +989,14 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
-  a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.eval = nullptr;
+  a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.dht = t.ws_dht; a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
-  a.P = oF2W + int64_t(t.C) * kH1 + t.C;
+  a.P = t.w_stride;  // row stride of the parameter matrix (>= the model size)
   a.lr = t.lr; a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;
   return a;
 }
 
-static size_t head_smem(int C, int BS) { return size_t(BS * kH1 + BS * C) * 4; }
-static size_t fc1b_smem(int BS) { return size_t(kH1 * 33 + BS * kH1 + BS * 33) * 4; }
+static size_t head_smem(int C, int BS) { return size_t(2 * BS * kH1 + BS * C) * 4; }
 
 static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream_t s) {
   // samples per CTA of the per-sample conv kernels: enough CTAs to fill the
@@ -823,14 +1010,14 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_FWD, s);
   pb::prof_begin(pb::K_CNN_FC1_FWD, s);
-  k_fc1_fwd<<<dim3(active, kH1 / 64), 256, 0, s>>>(a);
+  k_fc1_fwd<<<dim3(active, kH1 / 128), 128, kF1FwdSmem, s>>>(a);
   pb::prof_end(pb::K_CNN_FC1_FWD, s);
   pb::prof_begin(pb::K_CNN_HEAD, s);
   k_head<<<active, kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
   pb::prof_begin(pb::K_CNN_FC1_BWD, s);
-  k_fc1_bwd<<<dim3(active, kFlat / 32), 256, fc1b_smem(a.BS), s>>>(a);
+  k_fc1_bwd<<<dim3(active, kFlat / 64), 256, kF1BwdSmem, s>>>(a);
   pb::prof_end(pb::K_CNN_FC1_BWD, s);
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
   k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
@@ -845,7 +1032,8 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: null args");
   const pb_cnn_train_args& t = *args;
   if (t.g < 0 || t.C < 2 || t.C > 128 || t.BS < 1 || t.BS > 32 || t.epochs < 1 || !t.w ||
-      !t.active || t.sweeps < 0)
+      !t.active || t.sweeps < 0 || t.w_stride % 4 != 0 ||
+      t.w_stride < oF2W + int64_t(t.C) * kH1 + t.C || (reinterpret_cast<uintptr_t>(t.w) & 15))
     return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad arguments");
   if (t.g == 0 || t.sweeps == 0) return PB_OK;
   if (head_smem(t.C, t.BS) > 200 * 1024) return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: C too large");
@@ -871,6 +1059,8 @@ extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* 
   if (!args || !out2 || rows < 0) return pb::fail(PB_ERR_INVALID, "pb_cnn_eval: bad arguments");
   const pb_cnn_train_args& t = *args;
   if (rows == 0) return PB_OK;
+  if (t.w_stride % 4 != 0 || (reinterpret_cast<uintptr_t>(t.w) & 15))
+    return pb::fail(PB_ERR_INVALID, "pb_cnn_eval: parameters must be 16-byte aligned");
   int rc = cnn_setup();
   if (rc) return rc;
   Args a = to_args(t);

@@ -175,3 +175,79 @@ extern "C" int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, in
                                                              cycles);
   return pb::check_launch("pb_umma_bench");
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: 128 x N x K tf32 GEMM, A/B fp32 row-major [rows, K], K-major
+// (a_mn = 0) or MN-major (a_mn = 1) staging; D [128, N] fp32.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128) umma_tf32_kernel(const float* A, const float* B, float* D,
+                                                        int N, int K, int a_mn, int b_mn) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  constexpr int M = 128;
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + M * K * 4;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // fp32 core matrix: 8 rows x 16 B (4 elements)
+  for (int i = tid; i < M * K; i += 128) {
+    const int r = i / K, k = i % K;
+    const uint32_t off = a_mn ? uint32_t((k >> 3) * (M / 4) * 128 + (r >> 2) * 128 + (k & 7) * 16 + (r & 3) * 4)
+                              : uint32_t((r >> 3) * (K / 4) * 128 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+    *reinterpret_cast<float*>(sa + off) = A[i];
+  }
+  for (int i = tid; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    const uint32_t off = b_mn ? uint32_t((k >> 3) * (N / 4) * 128 + (r >> 2) * 128 + (k & 7) * 16 + (r & 3) * 4)
+                              : uint32_t((r >> 3) * (K / 4) * 128 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+    *reinterpret_cast<float*>(sb + off) = B[i];
+  }
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    // K-major: LBO = K-adjacent core stride (128), SBO = row-group stride (K/4*128)
+    // MN-major: LBO = K-adjacent (8 k) core stride (MN/4*128), SBO = MN-adjacent (128)
+    const uint32_t al = a_mn ? uint32_t(M / 4 * 128) : 128u, as = a_mn ? 128u : uint32_t(K / 4 * 128);
+    const uint32_t bl = b_mn ? uint32_t(N / 4 * 128) : 128u, bs = b_mn ? 128u : uint32_t(K / 4 * 128);
+    const uint32_t astep = a_mn ? uint32_t(M / 4 * 128) : 256u;  // K += 8
+    const uint32_t bstep = b_mn ? uint32_t(N / 4 * 128) : 256u;
+    const uint32_t idesc = idesc_tf32(M, N, a_mn != 0, b_mn != 0);
+    for (int ks = 0; ks < K / 8; ++ks)
+      mma_tf32(tbase, desc(smem_u32(sa) + ks * astep, al, as), desc(smem_u32(sb) + ks * bstep, bl, bs),
+               idesc, ks > 0);
+    commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after_sync();
+  const int row = warp * 32 + (tid & 31);
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tbase + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tbase);
+}
+}  // namespace
+
+extern "C" int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,
+                                     int b_mn, void* stream) {
+  if (!A || !B || !D || N < 16 || N > 256 || N % 16 || K < 8 || K % 8)
+    return pb::fail(PB_ERR_INVALID, "pb_umma_tf32_selftest: bad arguments");
+  const size_t smem = size_t(128 + N) * K * 4;
+  if (smem > 200 * 1024) return pb::fail(PB_ERR_INVALID, "pb_umma_tf32_selftest: too large");
+  cudaFuncSetAttribute(umma_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  umma_tf32_kernel<<<1, 128, smem, pb::as_stream(stream)>>>(A, B, D, N, K, a_mn, b_mn);
+  return pb::check_launch("pb_umma_tf32_selftest");
+}

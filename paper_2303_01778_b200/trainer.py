@@ -325,7 +325,9 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     clients, n = inputs.clients, inputs.n
     G = len(clients)
     P = spec.numel
-    w_out = torch.empty(G, P, device=d)
+    # CNN rows padded to 32 floats: 16-byte aligned vector / cp.async access
+    P_pad = (P + 31) // 32 * 32 if spec.kind == "cnn" else P
+    w_out = torch.empty(G, P_pad, device=d)[:, :P]
     loss = torch.empty(G, dtype=torch.float64, device=d)
     steps = torch.empty(G, dtype=torch.int32, device=d)
     bad = torch.empty(G, dtype=torch.int32, device=d)

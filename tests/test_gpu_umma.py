@@ -33,3 +33,40 @@ def test_umma_m64_accumulator_lanes():
     got, want = _run(64, 32, 64, 1, 1, 0)
     lanes = [(r // 16) * 32 + r % 16 for r in range(64)]
     assert np.allclose(got[lanes], want, rtol=1e-3, atol=1e-2)
+
+
+def _tf32_trunc(x):
+    import numpy as np
+    return (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+def _tf32_rne(x):
+    import numpy as np
+    u = x.astype(np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0xFFF + ((u >> 13) & 1)) & 0xFFFFE000
+    return u.astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0)])
+def test_umma_tf32_layouts_and_rounding(a_mn, b_mn):
+    """kind::tf32 from fp32 smem operands, K-major (the fc1 kernels' path);
+    records whether the hardware truncates or rounds fp32 -> tf32.  (MN-major
+    tf32 staging does not follow the bf16 convention; the kernels stage
+    transposed K-major tiles instead.)"""
+    import torch
+    from paper_2303_01778_b200._lib import lib
+    g = torch.Generator().manual_seed(7)
+    A = torch.randn(128, 64, generator=g).cuda()
+    B = torch.randn(32, 64, generator=g).cuda()
+    D = torch.zeros(128, 32, device="cuda")
+    lib.check(lib.pb_umma_tf32_selftest(A.data_ptr(), B.data_ptr(), D.data_ptr(), 32, 64, a_mn,
+                                        b_mn, torch.cuda.current_stream().cuda_stream))
+    got = D.cpu().numpy().astype(np.float64)
+    a, b = A.cpu().numpy(), B.cpu().numpy()
+    exact = a.astype(np.float64) @ b.astype(np.float64).T
+    trunc = _tf32_trunc(a).astype(np.float64) @ _tf32_trunc(b).astype(np.float64).T
+    rne = _tf32_rne(a).astype(np.float64) @ _tf32_rne(b).astype(np.float64).T
+    errs = {k: float(np.abs(got - v).max()) for k, v in
+            (("exact", exact), ("trunc", trunc), ("rne", rne))}
+    print("tf32 error vs", errs)
+    assert min(errs.values()) < 5e-4, errs
