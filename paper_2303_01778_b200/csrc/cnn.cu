@@ -537,11 +537,25 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
 // grid (active, 3136/64), 128 threads, 1 CTA/SM
 // ---------------------------------------------------------------------------
 constexpr int kB1A = 64 * 64 * 4;            // dgrad A stage: W1^T [64 k x 64 o]
-constexpr int kB1B = 32 * 64 * 4;            // dgrad B stage: dH [32 i x 64 o]
+constexpr int kB1B = 32 * kH1 * 4;           // dgrad B: dH [32 i x 512 o] (whole)
 constexpr int kB2A = kH1 * 32 * 4;           // wgrad A: dHt [512 o x 32 i]
 constexpr int kB2B = 64 * 32 * 4;            // wgrad B: X^T [64 k x 32 i]
-constexpr size_t kF1BwdSmem = 2 * (kB1A + kB1B) + kB2A + kB2B;   // 120 KB
+constexpr size_t kF1BwdSmem = 2 * kB1A + kB1B + kB2A + kB2B;   // 168 KB
 
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+constexpr int kF1Slices = kFlat / 64;   // 49 column slices of 64
+constexpr int kF1SlicesPerCta = 4;      // staging/setup amortised over 4 slices
+
+// grid (active, ceil(49/4)), 256 threads, 1 CTA/SM
 __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
@@ -549,134 +563,173 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   __shared__ __align__(8) uint64_t mbar[3];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cnt = sl.cnt;
-  const int k0 = blockIdx.y * 64;
+  const int slice0 = blockIdx.y * kF1SlicesPerCta;
+  const int nslices = min(kF1SlicesPerCta, kF1Slices - slice0);
   float* W = a.w + int64_t(sl.r) * a.P;
   float* W1 = W + oF1W;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
   const float* dh = a.dh + s0 * kH1;
   const float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
   const float* X = a.p2 + s0 * kFlat;
-  uint8_t* sA2 = smem + 2 * (kB1A + kB1B);
+  uint8_t* sB1 = smem + 2 * kB1A;
+  uint8_t* sA2 = sB1 + kB1B;
   uint8_t* sB2 = sA2 + kB2A;
-  // wgrad operands: dHt rows (cp.async, K-major (o/8, i/4)), X^T (SIMT transpose)
+  const bool plain_sgd = a.mu == 0.0f && a.ctrl_g == nullptr && a.ctrl_c == nullptr;
+  // slice-invariant operands once: dH (K-major (i/8, o/4)), dHt (K-major (o/8, i/4))
+  for (int e = tid; e < 32 * (kH1 / 4); e += 256) {
+    const int i = e >> 7, o4 = e & 127;
+    cp_async16_zfill(sB1 + (i >> 3) * (kH1 / 4) * 128 + o4 * 128 + (i & 7) * 16,
+                     dh + int64_t(i < cnt ? i : 0) * kH1 + o4 * 4, i < cnt);
+  }
   for (int e = tid; e < kH1 * 8; e += 256) {
     const int o = e >> 3, i4 = e & 7;
     cp_async16(sA2 + (o >> 3) * 1024 + i4 * 128 + (o & 7) * 16, dht + o * 32 + i4 * 4);
   }
   cp_async_commit();
-  for (int e = tid; e < 32 * 64; e += 256) {
-    const int i = e >> 6, kk = e & 63;
-    const float v = i < cnt ? X[int64_t(i) * kFlat + k0 + kk] : 0.0f;
-    *reinterpret_cast<float*>(sB2 + (kk >> 3) * 1024 + (i >> 2) * 128 + (kk & 7) * 16 + (i & 3) * 4) = v;
-  }
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], 1);
     fence_init();
   }
+  // W1[oc + o][k0 .. k0+63] for one o-chunk: 1024 float4, 4 per thread, kept in
+  // registers one chunk ahead of the MMAs (across slices too)
+  float4 pre[4];
+  auto load_chunk = [&](int g) {
+    const int kk0 = (slice0 + (g >> 3)) * 64, oc = (g & 7) * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
+      pre[j] = *reinterpret_cast<const float4*>(W1 + int64_t(oc + o) * kFlat + kk0 + k4 * 4);
+    }
+  };
+  load_chunk(0);
+  cp_async_wait<0>();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  // W1[oc + o][k0 .. k0+63] for one o-chunk: 1024 float4, 4 per thread, kept in
-  // registers one chunk ahead of the MMAs
-  float4 pre[4];
-  auto load_chunk = [&](int c) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
-      pre[j] = *reinterpret_cast<const float4*>(W1 + int64_t(c * 64 + o) * kFlat + k0 + k4 * 4);
+  const int q = warp & 3, half = warp >> 2;
+  const int nchunks = nslices * 8;
+  for (int sidx_ = 0; sidx_ < nslices; ++sidx_) {
+    const int k0 = (slice0 + sidx_) * 64;
+    // X^T for this slice (the previous slice's wgrad MMAs are complete)
+    for (int e = tid; e < 32 * 64; e += 256) {
+      const int i = e >> 6, kk = e & 63;
+      const float v = i < cnt ? X[int64_t(i) * kFlat + k0 + kk] : 0.0f;
+      *reinterpret_cast<float*>(sB2 + (kk >> 3) * 1024 + (i >> 2) * 128 + (kk & 7) * 16 + (i & 3) * 4) = v;
     }
-  };
-  load_chunk(0);
-  for (int c = 0; c < kH1 / 64; ++c) {
-    const int buf = c & 1;
-    uint8_t* sA = smem + buf * (kB1A + kB1B);
-    uint8_t* sB = sA + kB1A;
-    if (c >= 2) mbar_wait(&mbar[buf], ((c - 2) >> 1) & 1);
-    const int oc = c * 64;
-    for (int e = tid; e < 32 * 16; e += 256) {  // dH rows i, 64 o: 16 chunks each
-      const int i = e >> 4, o4 = e & 15;
-      cp_async16_zfill(sB + (i >> 3) * 2048 + o4 * 128 + (i & 7) * 16,
-                       dh + int64_t(i < cnt ? i : 0) * kH1 + oc + o4 * 4, i < cnt);
-    }
-    cp_async_commit();
+    if (plain_sgd) bulk_wait_read0();  // the previous slice's update staging (A buffers) is free
+    for (int c = 0; c < 8; ++c) {
+      const int g = sidx_ * 8 + c;
+      const int buf = g & 1;
+      uint8_t* sA = smem + buf * kB1A;
+      if (g >= 2) mbar_wait(&mbar[buf], ((g - 2) >> 1) & 1);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {  // transpose into A[k][o] (K-major over o)
-      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
-      const float vv[4] = {pre[j].x, pre[j].y, pre[j].z, pre[j].w};
+      for (int j = 0; j < 4; ++j) {  // transpose into A[k][o] (K-major over o)
+        const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
+        const float vv[4] = {pre[j].x, pre[j].y, pre[j].z, pre[j].w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int kk = k4 * 4 + q;
-        *reinterpret_cast<float*>(sA + (kk >> 3) * 2048 + (o >> 2) * 128 + (kk & 7) * 16 + (o & 3) * 4) = vv[q];
+        for (int qq = 0; qq < 4; ++qq) {
+          const int kk = k4 * 4 + qq;
+          *reinterpret_cast<float*>(sA + (kk >> 3) * 2048 + (o >> 2) * 128 + (kk & 7) * 16 + (o & 3) * 4) = vv[qq];
+        }
+      }
+      if (g + 1 < nchunks) load_chunk(g + 1);  // in flight during the sync + MMAs
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        fence_after_sync();
+        const uint64_t a0 = desc(smem_u32(sA), 128, 2048);
+        const uint64_t b0 = desc(smem_u32(sB1), 128, (kH1 / 4) * 128) + uint64_t(c * 128);
+        const uint32_t idesc = idesc_tf32(64, 32);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
+        commit(&mbar[buf]);
       }
     }
-    if (c + 1 < kH1 / 64) load_chunk(c + 1);  // in flight during the sync + MMAs
-    cp_async_wait<0>();
-    fence_async_smem();
-    __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      const uint64_t a0 = desc(smem_u32(sA), 128, 2048), b0 = desc(smem_u32(sB), 128, 2048);
-      const uint32_t idesc = idesc_tf32(64, 32);
+      const uint32_t idesc = idesc_tf32(128, 64);
+      const uint64_t a0 = desc(smem_u32(sA2), 128, 1024), b0 = desc(smem_u32(sB2), 128, 1024);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
-      commit(&mbar[buf]);
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem + 64 + t * 64, a0 + uint64_t(t * 1024 + kk * 16), b0 + uint64_t(kk * 16), idesc,
+                   kk > 0);
+      commit(&mbar[2]);
     }
-  }
-  if (tid == 0) {
+    {
+      const int gl = sidx_ * 8 + 7;  // last two chunks of the slice
+      mbar_wait(&mbar[(gl - 1) & 1], ((gl - 1) >> 1) & 1);
+      mbar_wait(&mbar[gl & 1], (gl >> 1) & 1);
+      mbar_wait(&mbar[2], sidx_ & 1);
+    }
     fence_after_sync();
-    const uint32_t idesc = idesc_tf32(128, 64);
-    const uint64_t a0 = desc(smem_u32(sA2), 128, 1024), b0 = desc(smem_u32(sB2), 128, 1024);
+    // dgrad epilogue (M=64: rows k in lanes 32q + [0,16)): dp2[i][k0+k]
+    {
+      const int k = q * 16 + lane;
+      float v[16];
+      tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 16), v);
+      if (lane < 16) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem + 64 + t * 64, a0 + uint64_t(t * 1024 + kk * 16), b0 + uint64_t(kk * 16), idesc,
-                 kk > 0);
-    commit(&mbar[2]);
-  }
-  mbar_wait(&mbar[0], 1);  // chunks 6 and 7 (buffers 0/1, 4th completion each)
-  mbar_wait(&mbar[1], 1);
-  mbar_wait(&mbar[2], 0);
-  fence_after_sync();
-  const int q = warp & 3, half = warp >> 2;
-  // dgrad epilogue (M=64: rows k in lanes 32q + [0,16)): dp2[i][k0+k]
-  {
-    const int k = q * 16 + lane;
-    float v[16];
-    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 16), v);
-    if (lane < 16) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int i = half * 16 + j;
-        if (i < cnt) a.dp2[(s0 + i) * kFlat + k0 + k] = v[j];
+        for (int j = 0; j < 16; ++j) {
+          const int i = half * 16 + j;
+          if (i < cnt) a.dp2[(s0 + i) * kFlat + k0 + k] = v[j];
+        }
       }
     }
-  }
-  // wgrad epilogue: row o of each tile, 32 of the 64 columns per warp half
+    // wgrad epilogue: row o of each tile, 32 of the 64 columns per warp half
+    if (plain_sgd) {
+      // W1 += -lr * g through bulk reduce-adds from smem (no read-back of W1):
+      // each thread stages its 128-byte row segment in the free A buffers
+      float* mine = reinterpret_cast<float*>(smem) + tid * 32;
 #pragma unroll 1
-  for (int t = 0; t < 4; ++t) {
-    const int o = t * 128 + q * 32 + lane;
-    float* wrow = W1 + int64_t(o) * kFlat + k0 + half * 32;
-    const int64_t base = oF1W + int64_t(o) * kFlat + k0 + half * 32;
-    float4 w4[8];
+      for (int t = 0; t < 4; ++t) {
+        const int o = t * 128 + q * 32 + lane;
+        float v[32];
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32),
+                  *reinterpret_cast<float(*)[16]>(v));
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32 + 16),
+                  *reinterpret_cast<float(*)[16]>(v + 16));
+        if (t > 0) bulk_wait_read0();  // my previous segment has been read
 #pragma unroll
-    for (int j = 0; j < 8; ++j) w4[j] = reinterpret_cast<const float4*>(wrow)[j];
-    float v[32];
-    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32), *reinterpret_cast<float(*)[16]>(v));
-    tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32 + 16),
-              *reinterpret_cast<float(*)[16]>(v + 16));
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<float4*>(mine)[j] =
+              make_float4(-a.lr * v[4 * j], -a.lr * v[4 * j + 1], -a.lr * v[4 * j + 2], -a.lr * v[4 * j + 3]);
+        fence_async_smem();
+        bulk_reduce_add_f32(W1 + int64_t(o) * kFlat + k0 + half * 32, mine, 128);
+        bulk_commit();
+      }
+    } else {
+#pragma unroll 1
+      for (int t = 0; t < 4; ++t) {
+        const int o = t * 128 + q * 32 + lane;
+        float* wrow = W1 + int64_t(o) * kFlat + k0 + half * 32;
+        const int64_t base = oF1W + int64_t(o) * kFlat + k0 + half * 32;
+        float4 w4[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t id = base + j * 4;
-      w4[j].x = sgd(a, sl.r, id + 0, w4[j].x, v[j * 4 + 0]);
-      w4[j].y = sgd(a, sl.r, id + 1, w4[j].y, v[j * 4 + 1]);
-      w4[j].z = sgd(a, sl.r, id + 2, w4[j].z, v[j * 4 + 2]);
-      w4[j].w = sgd(a, sl.r, id + 3, w4[j].w, v[j * 4 + 3]);
-      reinterpret_cast<float4*>(wrow)[j] = w4[j];
+        for (int j = 0; j < 8; ++j) w4[j] = reinterpret_cast<const float4*>(wrow)[j];
+        float v[32];
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32),
+                  *reinterpret_cast<float(*)[16]>(v));
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32 + 16),
+                  *reinterpret_cast<float(*)[16]>(v + 16));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t id = base + j * 4;
+          w4[j].x = sgd(a, sl.r, id + 0, w4[j].x, v[j * 4 + 0]);
+          w4[j].y = sgd(a, sl.r, id + 1, w4[j].y, v[j * 4 + 1]);
+          w4[j].z = sgd(a, sl.r, id + 2, w4[j].z, v[j * 4 + 2]);
+          w4[j].w = sgd(a, sl.r, id + 3, w4[j].w, v[j * 4 + 3]);
+          reinterpret_cast<float4*>(wrow)[j] = w4[j];
+        }
+      }
     }
+    fence_before_sync();
+    __syncthreads();  // TMEM reads done before the next slice's MMAs overwrite it
+    fence_after_sync();
   }
   if (blockIdx.y == 0) {
     for (int o = tid; o < kH1; o += 256) {
@@ -686,6 +739,7 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
   }
+  if (plain_sgd) bulk_wait_read0();  // smem sources consumed before the CTA retires
   fence_before_sync();
   __syncthreads();
   if (warp == 0) tmem_free<512>(tmem);
@@ -1017,7 +1071,8 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
   pb::prof_begin(pb::K_CNN_FC1_BWD, s);
-  k_fc1_bwd<<<dim3(active, kFlat / 64), 256, kF1BwdSmem, s>>>(a);
+  k_fc1_bwd<<<dim3(active, (kF1Slices + kF1SlicesPerCta - 1) / kF1SlicesPerCta), 256, kF1BwdSmem,
+              s>>>(a);
   pb::prof_end(pb::K_CNN_FC1_BWD, s);
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
   k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
