@@ -208,6 +208,11 @@ int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K
 int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,
                           int b_mn, void* stream);
 
+/* 128 x 32 x 32 tf32 GEMM with the A operand staged by the layout formula in
+ * params[0..9] (device int array; see csrc/umma_selftest.cu) -- probes the
+ * MN-major tf32 operand convention (tests only). */
+int pb_umma_tf32_probe(const float* A, const float* B, float* D, const int* params, void* stream);
+
 /* Issue `iters` back-to-back M x N x 16 bf16 tcgen05 MMAs from smem operands
  * staged in *_mode layouts (as above), round-robin over `naccum` independent
  * TMEM accumulators, and store the elapsed cycles (one CTA, device pointer).

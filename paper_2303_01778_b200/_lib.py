@@ -73,6 +73,7 @@ _SIGS = {
                            c_void_p]),
     "pb_umma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                                       c_void_p]),
+    "pb_umma_tf32_probe": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pb_umma_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
     "pb_cnn_eval": (c_int, [POINTER(CnnTrainArgs), c_int64, c_void_p, c_void_p]),

@@ -536,15 +536,22 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
 // W1 is staged transposed (SIMT) so every operand is K-major.
 // grid (active, 3136/64), 128 threads, 1 CTA/SM
 // ---------------------------------------------------------------------------
-constexpr int kB1A = 64 * 64 * 4;            // dgrad A stage: W1^T [64 k x 64 o]
-constexpr int kB1B = 32 * kH1 * 4;           // dgrad B: dH [32 i x 512 o] (whole)
+constexpr int kB1A = 64 * 64 * 4;            // dgrad A: W1^T [64 k x 64 o] (K-major, transposed)
+constexpr int kRawW = 64 * 64 * 4;           // raw W1 chunk [64 o x 64 k] row-major
+constexpr int kRawH = 32 * 64 * 4;           // dH chunk [32 i x 64 o] (dgrad B, K-major)
+constexpr int kRing = 4;                     // cp.async ring depth
 constexpr int kB2A = kH1 * 32 * 4;           // wgrad A: dHt [512 o x 32 i]
 constexpr int kB2B = 64 * 32 * 4;            // wgrad B: X^T [64 k x 32 i]
-constexpr size_t kF1BwdSmem = 2 * kB1A + kB1B + kB2A + kB2B;   // 168 KB
+constexpr size_t kF1BwdSmem = kRing * (kRawW + kRawH) + 2 * kB1A + kB2A + kB2B;   // 200 KB
 
 __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
                "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* gaddr, float x, float y, float z, float w) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(gaddr), "f"(x), "f"(y), "f"(z),
+               "f"(w)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
@@ -553,9 +560,11 @@ __device__ __forceinline__ void bulk_wait_read0() {
 }
 
 constexpr int kF1Slices = kFlat / 64;   // 49 column slices of 64
-constexpr int kF1SlicesPerCta = 4;      // staging/setup amortised over 4 slices
+constexpr int kF1SlicesPerCta = 4;      // setup amortised over 4 slices
 
-// grid (active, ceil(49/4)), 256 threads, 1 CTA/SM
+// grid (active, ceil(49/4)), 256 threads, 1 CTA/SM.  Per slice: 8 o-chunks
+// stream through a 4-deep cp.async ring (raw W1 rows + dH columns); each chunk
+// is transposed smem->smem into the K-major dgrad operand.
 __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
@@ -565,82 +574,91 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cnt = sl.cnt;
   const int slice0 = blockIdx.y * kF1SlicesPerCta;
   const int nslices = min(kF1SlicesPerCta, kF1Slices - slice0);
+  const int nchunks = nslices * 8;
   float* W = a.w + int64_t(sl.r) * a.P;
   float* W1 = W + oF1W;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
   const float* dh = a.dh + s0 * kH1;
   const float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
   const float* X = a.p2 + s0 * kFlat;
-  uint8_t* sB1 = smem + 2 * kB1A;
-  uint8_t* sA2 = sB1 + kB1B;
+  uint8_t* sRing = smem;
+  uint8_t* sA = sRing + kRing * (kRawW + kRawH);  // 2 transposed buffers
+  uint8_t* sA2 = sA + 2 * kB1A;
   uint8_t* sB2 = sA2 + kB2A;
   const bool plain_sgd = a.mu == 0.0f && a.ctrl_g == nullptr && a.ctrl_c == nullptr;
-  // slice-invariant operands once: dH (K-major (i/8, o/4)), dHt (K-major (o/8, i/4))
-  for (int e = tid; e < 32 * (kH1 / 4); e += 256) {
-    const int i = e >> 7, o4 = e & 127;
-    cp_async16_zfill(sB1 + (i >> 3) * (kH1 / 4) * 128 + o4 * 128 + (i & 7) * 16,
-                     dh + int64_t(i < cnt ? i : 0) * kH1 + o4 * 4, i < cnt);
-  }
-  for (int e = tid; e < kH1 * 8; e += 256) {
+  auto issue = [&](int g) {  // chunk g -> ring slot g % kRing (one commit group)
+    uint8_t* raw = sRing + (g % kRing) * (kRawW + kRawH);
+    const int kk0 = (slice0 + (g >> 3)) * 64, oc = (g & 7) * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
+      cp_async16(raw + o * 256 + k4 * 16, W1 + int64_t(oc + o) * kFlat + kk0 + k4 * 4);
+    }
+    for (int e = tid; e < 32 * 16; e += 256) {  // dH rows i, 64 o -> K-major (i/8, o/4)
+      const int i = e >> 4, o4 = e & 15;
+      cp_async16_zfill(raw + kRawW + (i >> 3) * 2048 + o4 * 128 + (i & 7) * 16,
+                       dh + int64_t(i < cnt ? i : 0) * kH1 + oc + o4 * 4, i < cnt);
+    }
+    cp_async_commit();
+  };
+  for (int e = tid; e < kH1 * 8; e += 256) {  // dHt: K-major (o/8, i/4)
     const int o = e >> 3, i4 = e & 7;
     cp_async16(sA2 + (o >> 3) * 1024 + i4 * 128 + (o & 7) * 16, dht + o * 32 + i4 * 4);
   }
   cp_async_commit();
+  for (int g = 0; g < kRing - 1 && g < nchunks; ++g) issue(g);
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], 1);
     fence_init();
   }
-  // W1[oc + o][k0 .. k0+63] for one o-chunk: 1024 float4, 4 per thread, kept in
-  // registers one chunk ahead of the MMAs (across slices too)
-  float4 pre[4];
-  auto load_chunk = [&](int g) {
-    const int kk0 = (slice0 + (g >> 3)) * 64, oc = (g & 7) * 64;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
-      pre[j] = *reinterpret_cast<const float4*>(W1 + int64_t(oc + o) * kFlat + kk0 + k4 * 4);
-    }
-  };
-  load_chunk(0);
-  cp_async_wait<0>();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const int q = warp & 3, half = warp >> 2;
-  const int nchunks = nslices * 8;
   for (int sidx_ = 0; sidx_ < nslices; ++sidx_) {
     const int k0 = (slice0 + sidx_) * 64;
-    // X^T for this slice (the previous slice's wgrad MMAs are complete)
-    for (int e = tid; e < 32 * 64; e += 256) {
+    for (int e = tid; e < 32 * 64; e += 256) {  // X^T for this slice
       const int i = e >> 6, kk = e & 63;
       const float v = i < cnt ? X[int64_t(i) * kFlat + k0 + kk] : 0.0f;
       *reinterpret_cast<float*>(sB2 + (kk >> 3) * 1024 + (i >> 2) * 128 + (kk & 7) * 16 + (i & 3) * 4) = v;
     }
-    if (plain_sgd) bulk_wait_read0();  // the previous slice's update staging (A buffers) is free
     for (int c = 0; c < 8; ++c) {
       const int g = sidx_ * 8 + c;
       const int buf = g & 1;
-      uint8_t* sA = smem + buf * kB1A;
-      if (g >= 2) mbar_wait(&mbar[buf], ((g - 2) >> 1) & 1);
+      uint8_t* raw = sRing + (g % kRing) * (kRawW + kRawH);
+      uint8_t* sAb = sA + buf * kB1A;
+      // keep kRing-1 chunks in flight: the slot of chunk g+kRing-1 held chunk g-1,
+      // whose MMAs (reading its dH part) must be complete
+      if (g + kRing - 1 < nchunks) {
+        if (g >= 1) mbar_wait(&mbar[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        issue(g + kRing - 1);
+        cp_async_wait<kRing - 1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();  // chunk g landed for every thread
+      // MMAs of chunk g-2 read sAb: done once chunk g-1's completion was observed
+      // (commits complete in order), or wait explicitly at the tail
+      if (!(g + kRing - 1 < nchunks) && g >= 2) mbar_wait(&mbar[buf], ((g - 2) >> 1) & 1);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // transpose into A[k][o] (K-major over o)
+      for (int j = 0; j < 4; ++j) {  // raw [o][k] -> A[k][o] (K-major over o)
         const int e = tid + j * 256, o = e >> 4, k4 = e & 15;
-        const float vv[4] = {pre[j].x, pre[j].y, pre[j].z, pre[j].w};
+        const float4 v = *reinterpret_cast<const float4*>(raw + o * 256 + k4 * 16);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           const int kk = k4 * 4 + qq;
-          *reinterpret_cast<float*>(sA + (kk >> 3) * 2048 + (o >> 2) * 128 + (kk & 7) * 16 + (o & 3) * 4) = vv[qq];
+          *reinterpret_cast<float*>(sAb + (kk >> 3) * 2048 + (o >> 2) * 128 + (kk & 7) * 16 + (o & 3) * 4) = vv[qq];
         }
       }
-      if (g + 1 < nchunks) load_chunk(g + 1);  // in flight during the sync + MMAs
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
         fence_after_sync();
-        const uint64_t a0 = desc(smem_u32(sA), 128, 2048);
-        const uint64_t b0 = desc(smem_u32(sB1), 128, (kH1 / 4) * 128) + uint64_t(c * 128);
+        const uint64_t a0 = desc(smem_u32(sAb), 128, 2048);
+        const uint64_t b0 = desc(smem_u32(raw + kRawW), 128, 2048);
         const uint32_t idesc = idesc_tf32(64, 32);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -682,9 +700,8 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
     }
     // wgrad epilogue: row o of each tile, 32 of the 64 columns per warp half
     if (plain_sgd) {
-      // W1 += -lr * g through bulk reduce-adds from smem (no read-back of W1):
-      // each thread stages its 128-byte row segment in the free A buffers
-      float* mine = reinterpret_cast<float*>(smem) + tid * 32;
+      // W1 += -lr * g with vector reductions performed at L2 (no read-back of W1
+      // into the SM; every lane issues its own, nothing serialises)
 #pragma unroll 1
       for (int t = 0; t < 4; ++t) {
         const int o = t * 128 + q * 32 + lane;
@@ -693,14 +710,11 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
                   *reinterpret_cast<float(*)[16]>(v));
         tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(64 + t * 64 + half * 32 + 16),
                   *reinterpret_cast<float(*)[16]>(v + 16));
-        if (t > 0) bulk_wait_read0();  // my previous segment has been read
+        float* wrow = W1 + int64_t(o) * kFlat + k0 + half * 32;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          reinterpret_cast<float4*>(mine)[j] =
-              make_float4(-a.lr * v[4 * j], -a.lr * v[4 * j + 1], -a.lr * v[4 * j + 2], -a.lr * v[4 * j + 3]);
-        fence_async_smem();
-        bulk_reduce_add_f32(W1 + int64_t(o) * kFlat + k0 + half * 32, mine, 128);
-        bulk_commit();
+          red_add_v4(wrow + 4 * j, -a.lr * v[4 * j], -a.lr * v[4 * j + 1], -a.lr * v[4 * j + 2],
+                     -a.lr * v[4 * j + 3]);
       }
     } else {
 #pragma unroll 1
@@ -739,7 +753,6 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
   }
-  if (plain_sgd) bulk_wait_read0();  // smem sources consumed before the CTA retires
   fence_before_sync();
   __syncthreads();
   if (warp == 0) tmem_free<512>(tmem);

@@ -251,3 +251,76 @@ extern "C" int pb_umma_tf32_selftest(const float* A, const float* B, float* D, i
   umma_tf32_kernel<<<1, 128, smem, pb::as_stream(stream)>>>(A, B, D, N, K, a_mn, b_mn);
   return pb::check_launch("pb_umma_tf32_selftest");
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: 128 x 32 x 32 tf32 GEMM with the A operand staged by an explicit
+// layout formula (p: kr, sk, sk_in, mr, sm, sm_in, lbo, sbo, kstep, mn) to probe
+// MN-major conventions; B is K-major.  D [128, 32].
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128) umma_tf32_probe_kernel(const float* A, const float* B, float* D,
+                                                              const int* p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  constexpr int M = 128, N = 32, K = 32;
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + 65536;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 65536 / 4; i += 128) reinterpret_cast<float*>(sa)[i] = 0.f;
+  __syncthreads();
+  const int kr = p[0], sk = p[1], sk_in = p[2], mr = p[3], sm = p[4], sm_in = p[5];
+  const int swz = p[10];  // 0: none; 1: 128B swizzle of MN-major atoms (8 k-rows x 128 B)
+  for (int i = tid; i < M * K; i += 128) {
+    const int r = i / K, k = i % K;
+    int off;
+    if (swz) {
+      // atom (r/32, k/8): 8 rows (k) of 128 B (32 mn); 16B chunk index XOR row
+      off = (r / 32) * sm + (k / 8) * sk + (k % 8) * 128 + ((((r % 32) / 4) ^ (k % 8)) * 16) + (r % 4) * 4;
+    } else {
+      off = (k / kr) * sk + (r / mr) * sm + (k % kr) * sk_in + (r % mr) * sm_in;
+    }
+    if (off >= 0 && off < 65536) *reinterpret_cast<float*>(sa + off) = A[i];
+  }
+  for (int i = tid; i < N * K; i += 128) {
+    const int r = i / K, k = i % K;
+    *reinterpret_cast<float*>(sb + (r >> 3) * (K / 4) * 128 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4) = B[i];
+  }
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<32>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_tf32(M, N, p[9] != 0, false);
+    for (int ks = 0; ks < K / 8; ++ks)
+      mma_tf32(tbase, desc(smem_u32(sa) + ks * p[8], p[6], p[7]) | (uint64_t(p[11]) << 61),
+               desc(smem_u32(sb) + ks * 256, 128, (K / 4) * 128), idesc, ks > 0);
+    commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after_sync();
+  const int row = warp * 32 + (tid & 31);
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    float v[16];
+    tmem_ld16(tbase + (uint32_t(warp * 32) << 16) + uint32_t(c0), v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) D[row * N + c0 + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<32>(tbase);
+}
+}  // namespace
+
+extern "C" int pb_umma_tf32_probe(const float* A, const float* B, float* D, const int* params,
+                                  void* stream) {
+  cudaFuncSetAttribute(umma_tf32_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 8192);
+  umma_tf32_probe_kernel<<<1, 128, 65536 + 8192, pb::as_stream(stream)>>>(A, B, D, params);
+  return pb::check_launch("pb_umma_tf32_probe");
+}

@@ -350,7 +350,8 @@ class SimulationEngine:
             self._rank = torch.distributed.get_rank()
             if cfg.clock == "real":
                 raise ConfigError("multi-process runs need the virtual clock (shared histories)")
-        self.local_devices = [k for k in range(cfg.num_devices) if k % self._world == self._rank]
+        from .distributed import local_devices
+        self.local_devices = local_devices(cfg.num_devices, self._world, self._rank)
         self.runtime = DeviceRuntime(cfg, plugin, self.spec, self.data, store, self.gauge)
         if cfg.scheme == "PARROT" and cfg.scheduling in ("full-history", "time-window"):
             warm_jit()
@@ -399,54 +400,11 @@ class SimulationEngine:
         return done
 
     def _reduce_partials(self, partials: list[DevicePartial], schema) -> list[DevicePartial]:
-        """Multi-process: sum this rank's partials (device order) and all-reduce
-        the packed buffer over NCCL; returns one combined partial."""
-        dist = torch.distributed
-        d = device()
-        local = DevicePartial(device_id=self._rank)
-        live = [p for p in partials if p.entries]
-        accs, meta = [], []
-        for name, op, shape in schema:
-            if op is AggOp.COLLECT:
-                continue
-            acc = torch.zeros(shape, device=d)
-            wsum, cnt = 0.0, 0
-            for p in live:
-                pe = p.entries.get(name)
-                if pe is not None:
-                    from . import _kernels as K
-                    K.fold(acc.view(-1), pe.acc.view(-1), 1.0)
-                    wsum += pe.weight_sum
-                    cnt += pe.count
-            accs.append(acc.view(-1))
-            meta += [wsum, float(cnt)]
-        packed = torch.cat(accs) if accs else torch.zeros(0, device=d)
-        meta_t = torch.tensor(meta, dtype=torch.float64, device=d)
-        dist.all_reduce(packed)
-        dist.all_reduce(meta_t)
-        meta_h = meta_t.cpu().numpy()
-        pos, mi = 0, 0
-        for name, op, shape in schema:
-            if op is AggOp.COLLECT:
-                continue
-            size = int(np.prod(shape))
-            local.entries[name] = PartialEntry(op=op, acc=packed[pos:pos + size].view(shape),
-                                               weight_sum=float(meta_h[mi]),
-                                               count=int(round(meta_h[mi + 1])))
-            pos += size
-            mi += 2
-        collects = [(name, [it for p in live for it in p.entries[name].collected])
-                    for name, op, _ in schema if op is AggOp.COLLECT and any(name in p.entries for p in live)]
-        host_collects = {n: [(c, t.detach().cpu()) for c, t in items] for n, items in collects}
-        gathered = [None] * self._world
-        dist.all_gather_object(gathered, (host_collects, [c for p in live for c in p.clients_folded]))
-        for name, op, _ in schema:
-            if op is not AggOp.COLLECT:
-                continue
-            items = [(c, t.to(d)) for g in gathered for c, t in g[0].get(name, [])]
-            local.entries[name] = PartialEntry(op=op, collected=items, count=len(items))
-        local.clients_folded = [c for g in gathered for c in g[1]]
-        return [local]
+        """Multi-process: one all-reduce of this rank's packed partials (NCCL)."""
+        from . import _kernels as K
+        from .distributed import allreduce_partials
+        return [allreduce_partials(partials, schema, device=device(),
+                                   fold=lambda acc, x: K.fold(acc, x, 1.0))]
 
     # -- the round ----------------------------------------------------------------
     def prepare_round(self, round_num: int) -> "RoundInputs":
