@@ -233,6 +233,9 @@ def run_b200(args) -> dict:
         r += 1
     # ---- device-timed rounds (inputs prepared and resident before timing) ----
     prepared = [eng.prepare_round(r + i) for i in range(args.steps)]
+    # algorithmic work of the timed rounds: client-steps (fc1 streams) and samples
+    client_steps = sum(int(np.sum((p.group.n + BS - 1) // BS)) for p in prepared if p.group)
+    samples_timed = sum(int(np.sum(p.group.n)) for p in prepared if p.group)
     for p in prepared:
         p.upload()
     lib.pb_prof_enable(1)
@@ -274,7 +277,9 @@ def run_b200(args) -> dict:
     # dominant kernel
     dom = max(kernels.items(), key=lambda kv: kv[1][0]) if kernels else ("none", (0.0, 0))
     dom_name, (dom_ms, dom_n) = dom
-    roof = roofline(dom_name, dom_ms, dom_n, kernels, samples_round * args.steps, peaks, peak_src)
+    roof = roofline(dom_name, dom_ms, kernels, samples_timed, client_steps, peaks, peak_src)
+    all_roofs = {k: roofline(k, v[0], kernels, samples_timed, client_steps, peaks, peak_src)
+                 for k, v in kernels.items() if k.startswith("cnn_") and k != "cnn_slots"}
     out = {
         "metric": "FL rounds/sec (1000 clients, FEMNIST-CNN)",
         "value": args.steps / (dev_ms / 1e3),
@@ -300,6 +305,8 @@ def run_b200(args) -> dict:
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernels_ms_per_round": {k: round(v[0] / args.steps, 3) for k, v in kernels.items()},
+        "kernels_roofline_frac": {k: (round(v["frac"], 4) if v.get("frac") is not None else None)
+                                  for k, v in all_roofs.items()},
         "clocks": clocks.summary(),
     }
     if agg is not None:
@@ -314,25 +321,36 @@ def run_b200(args) -> dict:
     return out if rank == 0 else None
 
 
-def roofline(name, ms, n, kernels, samples_timed, peaks, peak_src) -> dict:
-    """Dominant kernel vs its roofline (algorithmic work per launch / its
-    average launch duration)."""
+# fc1 (per-client weights, 512 x 3136 fp32): the forward streams W1 once,
+# the fused backward reads it once and writes it once (SGD update).
+FC1_BYTES = {"cnn_fc1_fwd": 4 * 512 * 3136, "cnn_fc1_bwd": 8 * 512 * 3136}
+# conv2 implicit-GEMM FLOPs per sample and pass (fwd, dgrad, wgrad)
+CONV2_FLOP = 2 * 14 * 14 * 64 * 800
+
+
+def roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src) -> dict:
+    """A kernel vs its roofline: ALGORITHMIC work of the timed rounds divided by
+    the kernel's total device time over those rounds (CUDA events recorded by
+    the library around each launch, on the launching stream)."""
+    if ms <= 0:
+        return {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None,
+                "frac": None, "traffic": None}
+    if name in FC1_BYTES:
+        gbs = FC1_BYTES[name] * client_steps / (ms / 1e3) / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": f"{peak_src} HBM copy bandwidth",
+                "work": f"{FC1_BYTES[name]} B per client-step x {client_steps} client-steps"}
     if name in ("cnn_fwd", "cnn_bwd_conv", "cnn_wgrad"):
-        share = {"cnn_fwd": 1 / 3, "cnn_bwd_conv": 1 / 3, "cnn_wgrad": 1 / 3}[name]
-        flops = FLOP_CONV2_PER_SAMPLE * share * samples_timed
-        achieved = flops / (ms / 1e3) / 1e12
+        tf = CONV2_FLOP * samples_timed / (ms / 1e3) / 1e12
         peak = peaks["bf16_tflops_sustained"]
-        return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                "peak_source": f"{peak_src} bf16 sustained",
-                "work": "conv2 implicit-GEMM FLOPs (2*14*14*64*800 per sample per pass)"}
-    if name in ("cnn_fc1_fwd", "cnn_fc1_bwd"):
-        per = 4 if name == "cnn_fc1_fwd" else 8
-        steps_timed = n  # one launch per sweep, over all active clients
-        bytes_ = per * 512 * 3136 * kernels.get("_client_steps", (0, 0))[0] if False else None
-        return {"kernel": name, "bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_src}
-    return {"kernel": name, "bound": "unknown", "achieved": None, "peak": None, "unit": None,
+        return {"kernel": name, "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": tf / peak, "traffic": None, "peak_source": f"{peak_src} bf16 sustained",
+                "work": f"conv2 implicit GEMM {CONV2_FLOP} FLOP/sample x {samples_timed} samples"}
+    if name == "cnn_head":
+        return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
+                "frac": None, "traffic": None}
+    return {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None,
             "frac": None, "traffic": None}
 
 
