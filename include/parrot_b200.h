@@ -40,8 +40,9 @@ int pb_device_sm_count(int device);
  * pb_prof_collect fills ms[id] / count[id] for the kernel classes
  *   0 fold1 1 fold_group 2 lincomb 3 delta_affine 4 state_gather
  *   5 state_scatter 6 lr_train 7 lr_eval 8 cnn_slots 9 cnn_fwd 10 cnn_fc1_fwd
- *   11 cnn_head 12 cnn_fc1_bwd 13 cnn_bwd_conv 14 cnn_wgrad
- * recorded since the last collect (nslots >= 15), synchronising on them. */
+ *   11 cnn_head 12 cnn_fc1_bwd 13 cnn_bwd_conv 14 cnn_wgrad 15 cnn_lz_xt
+ *   16 cnn_lz_gram_fwd 17 cnn_lz_fwd 18 cnn_lz_gram_bwd 19 cnn_lz_bwd 20 cnn_lz_mat
+ * recorded since the last collect (nslots >= 21), synchronising on them. */
 int pb_prof_enable(int on);
 int64_t pb_launch_count(void);
 int pb_prof_collect(double* ms, int64_t* count, int nslots);
@@ -147,7 +148,7 @@ int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F, int C, con
  *     per sweep; conv2 forward/dgrad/wgrad run on tcgen05 (bf16 operands,
  *     fp32 TMEM accumulation), the rest in fp32.  Workspace buffers are
  *     caller-allocated, sized per slot (= client) for BS samples:
- *       ws_slots 16 B, ws_p1 BS*21504 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
+ *       ws_slots 32 B, ws_p1 BS*21504 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
  *       ws_am2 BS*3136 B, ws_h/ws_dh BS*512 f32, ws_dp2 BS*3136 f32,
  *       ws_dz BS*43008 B, ws_dp1 BS*6272 f32 (per-sample conv1/bias gradient
  *       partials, 896 used), ws_dht 16384 f32 per slot.
@@ -181,6 +182,22 @@ typedef struct {
   uint8_t* ws_dz;
   float* ws_dp1;
   float* ws_dht;            /* per slot: 512*32 f32 (dH transposed, zero-padded) */
+  /* Low-rank fc1 for plain SGD (mu = 0, no control variates); all NULL for
+   * the direct per-client fc1.  Client row r owns history rows
+   * [lz_hoff[r], lz_hoff[r] + lz_hlen[r]), lz_hlen[r] = round_up(steps_r*BS, 4);
+   * step t's sample i is row t*BS + i.  Every client's fc1 weights stay
+   * W0 - lr * sum_t dH_t^T X_t during the round (never materialised per
+   * step); they are written to w once, after the last sweep.  The four
+   * history buffers must be zeroed by the caller before the call. */
+  float* lz_hx;             /* [rows, 3136] f32                               */
+  float* lz_hxt;            /* per client [3136][hlen] f32                    */
+  float* lz_hd;             /* [rows, 512] f32                                */
+  float* lz_hdt;            /* per client [512][hlen] f32                     */
+  const int64_t* lz_hoff;   /* [g]                                            */
+  const int32_t* lz_hlen;   /* [g]                                            */
+  float* lz_w0t;            /* [3136*512] f32 scratch (W1 of w0 transposed)   */
+  float* lz_zp;             /* max_t active_t*njt_t * 512*32 f32, njt_t = ceil(t*BS/128) */
+  float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;

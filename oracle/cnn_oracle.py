@@ -93,7 +93,8 @@ class _TruncGrad(torch.autograd.Function):
         return _tf32(g)
 
 
-def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor:
+def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
+            fc1_base: torch.Tensor | None = None) -> torch.Tensor:
     """x [B, 784] -> logits; conv weights are NHWC ([co, ky, kx, ci]).
 
     emulate_bf16=True rounds exactly the operands the device feeds to its
@@ -101,7 +102,12 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor
     backward GEMMs) and tf32 truncation for fc1 (X and W1 in the forward, dL/dz1
     in both backward GEMMs); everything else stays in the oracle's precision.
     Used to check the kernels' arithmetic separately from the effect of the
-    reduced-precision operands on the trajectory."""
+    reduced-precision operands on the trajectory.
+
+    fc1_base (with emulate_bf16): the round-start fc1 weights W0 of a device
+    run that used the low-rank fc1 (csrc/cnn_lazy.cu), whose tensor cores see
+    tf32(W0) plus the client's accumulated update in (near) full precision
+    instead of tf32(W_t): the emulated weight is tf32(W0) + (W_t - W0)."""
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
     h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
@@ -112,7 +118,8 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False) -> torch.Tensor
         h = F.max_pool2d(F.relu(F.conv2d(h, c2w.permute(0, 3, 1, 2), c2b, padding=2)), 2)
     h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)  # NHWC flatten
     if emulate_bf16:
-        h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ _TruncValue.apply(f1w).t()) + f1b)
+        w1 = _TruncValue.apply(f1w) if fc1_base is None else f1w - fc1_base + _tf32(fc1_base)
+        h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ w1.t()) + f1b)
     else:
         h = F.relu(h @ f1w.t() + f1b)
     return h @ f2w.t() + f2b

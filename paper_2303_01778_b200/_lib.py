@@ -38,7 +38,10 @@ class CnnTrainArgs(ctypes.Structure):
         ("ctrl_stride", c_int64), ("loss_sum", c_void_p), ("steps", c_void_p), ("bad", c_void_p),
         ("ws_slots", c_void_p), ("ws_p1", c_void_p), ("ws_am1", c_void_p), ("ws_p2", c_void_p),
         ("ws_am2", c_void_p), ("ws_h", c_void_p), ("ws_dh", c_void_p), ("ws_dp2", c_void_p),
-        ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("ws_dht", c_void_p), ("g", c_int64),
+        ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("ws_dht", c_void_p),
+        ("lz_hx", c_void_p), ("lz_hxt", c_void_p), ("lz_hd", c_void_p), ("lz_hdt", c_void_p),
+        ("lz_hoff", c_void_p), ("lz_hlen", c_void_p), ("lz_w0t", c_void_p), ("lz_zp", c_void_p),
+        ("lz_gdt", c_void_p), ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),
@@ -109,7 +112,8 @@ lib = _Lib(_PATH)
 
 KERNEL_CLASSES = ("fold1", "fold_group", "lincomb", "delta_affine", "state_gather",
                   "state_scatter", "lr_train", "lr_eval", "cnn_slots", "cnn_fwd", "cnn_fc1_fwd",
-                  "cnn_head", "cnn_fc1_bwd", "cnn_bwd_conv", "cnn_wgrad")
+                  "cnn_head", "cnn_fc1_bwd", "cnn_bwd_conv", "cnn_wgrad", "cnn_lz_xt",
+                  "cnn_lz_gram_fwd", "cnn_lz_fwd", "cnn_lz_gram_bwd", "cnn_lz_bwd", "cnn_lz_mat")
 
 
 def prof_collect() -> dict[str, tuple[float, int]]:

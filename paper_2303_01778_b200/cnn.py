@@ -32,12 +32,60 @@ class _Workspace:
             n = self.slots * self.bs
             self.buf = {k: torch.empty(n * v, dtype=torch.uint8, device=device)
                         for k, v in _PER_SAMPLE.items()}
-            self.buf["slots"] = torch.empty(self.slots * 16, dtype=torch.uint8, device=device)
+            self.buf["slots"] = torch.empty(self.slots * 32, dtype=torch.uint8, device=device)
             self.buf["dht"] = torch.empty(self.slots * 512 * 32 * 4, dtype=torch.uint8, device=device)
         return self.buf
 
 
 _WS = _Workspace()
+
+
+class _LazyWorkspace:
+    """Grow-only buffers of the low-rank fc1 (csrc/cnn_lazy.cu): the round's
+    (X, dH) history per client plus the per-sweep partials."""
+
+    def __init__(self):
+        self.buf: dict[str, torch.Tensor] = {}
+
+    def _get(self, name: str, numel: int, device) -> torch.Tensor:
+        t = self.buf.get(name)
+        if t is None or t.numel() < numel or t.device != device:
+            self.buf.pop(name, None)
+            t = torch.empty(max(numel, 4), dtype=torch.float32, device=device)
+            self.buf[name] = t
+        return t
+
+    def get(self, rows: int, zp: int, gdt: int, device) -> dict[str, torch.Tensor]:
+        out = {"hx": self._get("hx", rows * 3136, device), "hxt": self._get("hxt", rows * 3136, device),
+               "hd": self._get("hd", rows * 512, device), "hdt": self._get("hdt", rows * 512, device),
+               "w0t": self._get("w0t", 3136 * 512, device), "zp": self._get("zp", zp, device),
+               "gdt": self._get("gdt", gdt, device)}
+        for k, width in (("hx", 3136), ("hxt", 3136), ("hd", 512), ("hdt", 512)):
+            out[k][:rows * width].zero_()
+        return out
+
+
+_LZ = _LazyWorkspace()
+
+
+def lazy_enabled(terms: dict) -> bool:
+    """The low-rank fc1 applies to plain SGD (FedAvg): no proximal or
+    control-variate term in the local gradient.  PB_CNN_LAZY=0 forces the
+    direct per-client fc1 (A/B testing)."""
+    plain = not terms.get("mu") and terms.get("ctrl_g") is None and not terms.get("ctrl_c")
+    return plain and os.environ.get("PB_CNN_LAZY", "1") != "0"
+
+
+def lazy_plan(total: np.ndarray, active: np.ndarray, BS: int):
+    """History layout: client row r owns hlen[r] = round_up(steps_r * BS, 4)
+    rows from hoff[r]; partial-buffer capacities over the sweeps."""
+    hlen = ((total * BS + 3) // 4 * 4).astype(np.int32)
+    hoff = np.zeros(len(total), dtype=np.int64)
+    if len(total) > 1:
+        hoff[1:] = np.cumsum(hlen[:-1], dtype=np.int64)
+    njt = (np.arange(len(active)) * BS + 127) // 128
+    cap = int((active.astype(np.int64) * njt).max()) if len(active) else 0
+    return hlen, hoff, int(hlen.sum()), cap * 512 * 32, cap * 32 * 128
 
 
 def _samples_per_cta() -> int:
@@ -68,7 +116,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
                     spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
                     state_work) -> None:
     G = len(n)
-    BS, _, rank, active = sweep_plan(n, batch_size, epochs)
+    BS, total, rank, active = sweep_plan(n, batch_size, epochs)
     if BS > MAX_BATCH:
         raise ValueError(f"the CNN path supports minibatches of up to {MAX_BATCH} samples, got {BS}")
     d = w_out.device
@@ -95,6 +143,15 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     a.ctrl_stride = ctrl_c.stride(0) if ctrl_c is not None else 0
     a.loss_sum, a.steps, a.bad = ptr(loss), ptr(steps), ptr(bad)
     _fill(a, ws, G, BS)
+    if lazy_enabled(terms):
+        hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
+        lz = _LZ.get(rows, zp, gdt, d)
+        hlen_d = torch.from_numpy(hlen).to(d)
+        hoff_d = torch.from_numpy(hoff).to(d)
+        a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),
+                                                ptr(lz["hdt"]))
+        a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
+        a.lz_zp, a.lz_gdt = ptr(lz["zp"]), ptr(lz["gdt"])
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)

@@ -23,113 +23,12 @@
 //                positions) + update; conv1 wgrad/biases (SIMT) + update
 // Operands are bf16 with fp32 accumulation in TMEM; master weights, biases,
 // losses and all non-GEMM math are fp32 (loss reduction in double).
-#include <cuda_bf16.h>
-
-#include <algorithm>
-#include <vector>
-
-#include "common.cuh"
-#include "umma.cuh"
+#include "cnn_common.cuh"
 
 namespace {
 
 using namespace pb::umma;
-
-// ---- model geometry --------------------------------------------------------
-constexpr int kImg = 28, kC1 = 32, kC2 = 64, kH1 = 512, kFlat = 7 * 7 * kC2;  // 3136
-constexpr int kP1 = 14 * 14 * kC1;   // 6272 pooled conv1 outputs
-constexpr int kG = 18;               // padded 14x14 grid width (2-pixel border)
-constexpr int kRows = 336;           // plane rows (>= 256 + 4*18 + 4 = 332)
-constexpr int kPlane = kRows * 16;   // bytes per plane (8 channels x bf16)
-constexpr int kP1Bytes = 4 * kPlane;   // p1 image, 4 channel planes
-constexpr int kDzBytes = 8 * kPlane;   // dz2 image, 8 channel planes
-constexpr int kW2Bytes = 25 * 4 * 1024;  // conv2 weights in the UMMA B layout
-constexpr int kPg = 800 + 32 + 64;        // per-sample partials: conv1 w, conv1 b, conv2 b
-// flat parameter offsets (models.py cnn_spec)
-constexpr int64_t oC1W = 0, oC1B = 800, oC2W = 832, oC2B = 832 + 51200, oF1W = oC2B + 64,
-                  oF1B = oF1W + int64_t(kH1) * kFlat, oF2W = oF1B + kH1;
-
-struct Slot {
-  int32_t r;        // group row (parameter row / per-client outputs)
-  int32_t cnt;      // samples in this step's batch (0 = inactive)
-  int64_t row_off;  // offset of the batch's row ids in `order`
-};
-
-struct Args {
-  const float* X;
-  const int32_t* Y;
-  const int32_t* order;
-  const int64_t* order_off;
-  const int32_t* n;
-  const int32_t* rank;
-  float* w;               // [G, P] parameters, updated in place
-  const float* w0;        // [P] start model (prox term)
-  const float* ctrl_g;    // [P] or null
-  const float* ctrl_c;    // [G, ctrl_stride] or null
-  int64_t ctrl_stride;
-  double* loss_sum;
-  int32_t* steps;
-  int32_t* bad;
-  // workspace, slot-major with BS samples per slot
-  Slot* slots;
-  uint8_t* p1g;    // [slots*BS, kP1Bytes]  bf16 planes
-  uint8_t* am1;    // [slots*BS, kP1]
-  float* p2;       // [slots*BS, kFlat]
-  uint8_t* am2;    // [slots*BS, kFlat]
-  float* h;        // [slots*BS, kH1]
-  float* dh;       // [slots*BS, kH1]
-  float* dht;      // [slots, kH1, 32] dH transposed, samples zero-padded to 32
-  float* dp2;      // [slots*BS, kFlat]
-  uint8_t* dzg;    // [slots*BS, kDzBytes] bf16 planes
-  float* pg;       // [slots*BS, kPg] per-sample conv1-w/conv1-b/conv2-b gradient partials
-  double* eval;    // [2] correct, loss (eval mode)
-  int64_t P;
-  int32_t C, BS, bs, epochs, step;
-  float lr, mu, cg, cc;
-};
-
-__device__ __forceinline__ float sgd(const Args& a, int r, int64_t idx, float w, float g) {
-  if (a.mu != 0.0f) g = fmaf(a.mu, w - a.w0[idx], g);
-  if (a.ctrl_g) g = fmaf(a.cg, a.ctrl_g[idx], g);
-  if (a.ctrl_c) g = fmaf(a.cc, a.ctrl_c[int64_t(r) * a.ctrl_stride + idx], g);
-  return fmaf(-a.lr, g, w);
-}
-
-__device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j) * BS + i; }
-
-// NaN-propagating relu / max (torch semantics; fmaxf would drop a NaN and
-// hide a diverged client from the non-finite check)
-__device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
-__device__ __forceinline__ bool takes_max(float z, float best) { return z > best || z != z; }
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
-// zero-fills the 16 bytes when !valid (src is not read)
-__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
-  // UMMA B layout, K-major over (tap, ci): core matrix = 8 co x 8 ci
-  return uint32_t((tap * 4 + (ci >> 3)) * 1024 + (co >> 3) * 128 + (co & 7) * 16 + (ci & 7) * 2);
-}
-
-__device__ void stage_w2(uint8_t* sW2, const float* W, int tid, int nthreads) {
-  const float* w2 = W + oC2W;
-  for (int e = tid; e < 64 * 800; e += nthreads) {
-    const int co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
-    *reinterpret_cast<__nv_bfloat16*>(sW2 + w2_off(co, tap, ci)) = __float2bfloat16(w2[e]);
-  }
-}
+using namespace pb::cnn;
 
 // ---------------------------------------------------------------------------
 // k_slots: one thread per active slot -> (row, batch size, row-id offset)
@@ -146,6 +45,8 @@ __global__ void k_slots(Args a, int active) {
   s.r = r;
   s.cnt = (e < a.epochs && a.bad[r] < 0) ? min(bs, n - b * bs) : 0;
   s.row_off = a.order_off[r] + int64_t(e) * n + int64_t(b) * bs;
+  s.hist = a.hoff ? a.hoff[r] : 0;
+  s.pad_ = 0;
   a.slots[j] = s;
 }
 
@@ -281,7 +182,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
     }
     fence_before_sync();
     __syncthreads();
-    float* p2 = a.p2 + sid * kFlat;
+    float* p2 = p2_row(a, sl, blockIdx.x, i);
     uint8_t* am2 = a.am2 + sid * kFlat;
     for (int o = tid; o < kFlat; o += kFwdThreads) {
       const int pp = o >> 6, co = o & 63;
@@ -321,9 +222,6 @@ constexpr int kF1ABytes = 128 * kF1KC * 4;       // 32 KB
 constexpr int kF1BBytes = 32 * kF1KC * 4;        // 8 KB
 constexpr size_t kF1FwdSmem = 2 * (kF1ABytes + kF1BBytes);
 
-__device__ __forceinline__ uint32_t kmaj_f32(int r, int k4, int sbo) {
-  return uint32_t((r >> 3) * sbo + k4 * 128 + (r & 7) * 16);
-}
 
 // k_fc1_fwd: h = relu(p2 W1^T + b1); CTA = (client, 128 output rows)
 // D[o][i] (M=128, N=32, K=3136 in 49 stages of 64); grid (active, 4), 128 thr
@@ -338,7 +236,7 @@ __global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
   const float* W = a.w + int64_t(sl.r) * a.P;
   const float* W1 = W + oF1W + int64_t(o0) * kFlat;
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  const float* X = a.p2 + s0 * kFlat;
+  const float* X = p2_row(a, sl, blockIdx.x, 0);
   auto stage = [&](int c, int buf) {
     uint8_t* sa = smem + buf * (kF1ABytes + kF1BBytes);
     uint8_t* sb = sa + kF1ABytes;
@@ -496,7 +394,9 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
     return;
   }
   // dH = dlogits W2 (old weights) masked by relu'; stored [i][o] and [o][i<32]
-  float* dh = a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
+  // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
+  const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
+  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
   for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
     const int i = p >> 9, o = p & (kH1 - 1);
     float s = 0.0f;
@@ -506,7 +406,20 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
     sDH[p] = g;
   }
   __syncthreads();  // every read of the old W2 is done before the update
-  {
+  if (a.hx) {
+    const int L = a.hlen[sl.r];
+    float* hdt = a.hdt + sl.hist * kH1 + int64_t(a.step) * a.BS;
+    for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
+      const int o = p / cnt, i = p - o * cnt;
+      hdt[int64_t(o) * L + i] = sDH[i * kH1 + o];
+    }
+    for (int o = tid; o < kH1; o += kHeadThreads) {  // fc1 bias (sample order)
+      float g = 0.0f;
+      for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
+      const int64_t idx = oF1B + o;
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+    }
+  } else {
     float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
     for (int p = tid; p < kH1 * 32; p += kHeadThreads) {
       const int o = p >> 5, i = p & 31;
@@ -580,7 +493,7 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
   const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
   const float* dh = a.dh + s0 * kH1;
   const float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
-  const float* X = a.p2 + s0 * kFlat;
+  const float* X = p2_row(a, sl, blockIdx.x, 0);
   uint8_t* sRing = smem;
   uint8_t* sA = sRing + kRing * (kRawW + kRawH);  // 2 transposed buffers
   uint8_t* sA2 = sA + 2 * kB1A;
@@ -801,7 +714,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
       reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     const float* dp2 = a.dp2 + sid * kFlat;
-    const float* p2 = a.p2 + sid * kFlat;
+    const float* p2 = p2_row(a, sl, blockIdx.x, i);
     const uint8_t* am2 = a.am2 + sid * kFlat;
     float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
     for (int o = tid; o < kFlat; o += 256) {
@@ -1055,6 +968,8 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.rank = t.rank; a.w = t.w; a.w0 = t.w0; a.ctrl_g = t.ctrl_g; a.ctrl_c = t.ctrl_c;
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
+  a.hx = t.lz_hx; a.hxt = t.lz_hxt; a.hd = t.lz_hd; a.hdt = t.lz_hdt; a.hoff = t.lz_hoff;
+  a.hlen = t.lz_hlen; a.w0t = t.lz_w0t; a.zp = t.lz_zp; a.gdt = t.lz_gdt;
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
   a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.dht = t.ws_dht; a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
@@ -1076,17 +991,27 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   pb::prof_begin(pb::K_CNN_FWD, s);
   k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_FWD, s);
-  pb::prof_begin(pb::K_CNN_FC1_FWD, s);
-  k_fc1_fwd<<<dim3(active, kH1 / 128), 128, kF1FwdSmem, s>>>(a);
-  pb::prof_end(pb::K_CNN_FC1_FWD, s);
+  if (a.hx) {
+    int rc = lazy_fc1_sweep(a, active, 0, s);
+    if (rc) return rc;
+  } else {
+    pb::prof_begin(pb::K_CNN_FC1_FWD, s);
+    k_fc1_fwd<<<dim3(active, kH1 / 128), 128, kF1FwdSmem, s>>>(a);
+    pb::prof_end(pb::K_CNN_FC1_FWD, s);
+  }
   pb::prof_begin(pb::K_CNN_HEAD, s);
   k_head<<<active, kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
-  pb::prof_begin(pb::K_CNN_FC1_BWD, s);
-  k_fc1_bwd<<<dim3(active, (kF1Slices + kF1SlicesPerCta - 1) / kF1SlicesPerCta), 256, kF1BwdSmem,
-              s>>>(a);
-  pb::prof_end(pb::K_CNN_FC1_BWD, s);
+  if (a.hx) {
+    int rc = lazy_fc1_sweep(a, active, 1, s);
+    if (rc) return rc;
+  } else {
+    pb::prof_begin(pb::K_CNN_FC1_BWD, s);
+    k_fc1_bwd<<<dim3(active, (kF1Slices + kF1SlicesPerCta - 1) / kF1SlicesPerCta), 256, kF1BwdSmem,
+                s>>>(a);
+    pb::prof_end(pb::K_CNN_FC1_BWD, s);
+  }
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
   k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
@@ -1110,6 +1035,14 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   Args a = to_args(t);
   cudaStream_t s = pb::as_stream(stream);
   const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
+  if (a.hx) {
+    // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
+    if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hxt || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
+        !a.w0t || !a.zp || !a.gdt || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
+        !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
+      return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
+    if ((rc = lazy_fc1_prepare(a, s))) return rc;
+  }
   for (int step = 0; step < t.sweeps; ++step) {
     const int active = t.active[step];
     if (active <= 0) break;
@@ -1119,6 +1052,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     pb::prof_end(pb::K_CNN_SLOTS, s);
     if ((rc = launch_sweep(a, active, true, spb, s))) return rc;
   }
+  if (a.hx) return lazy_fc1_materialize(a, int(t.g), s);
   return PB_OK;
 }
 
@@ -1133,6 +1067,7 @@ extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* 
   if (rc) return rc;
   Args a = to_args(t);
   a.eval = out2;
+  a.hx = nullptr;  // evaluation reads the materialised weights
   cudaStream_t s = pb::as_stream(stream);
   // slots: batches of BS consecutive rows of `order`, all on parameter row 0
   const int64_t nslots = (rows + t.BS - 1) / t.BS;

@@ -1,0 +1,151 @@
+// Shared definitions of the FEMNIST-CNN training kernels (cnn.cu: conv
+// layers, head, direct fc1; cnn_lazy.cu: the low-rank fc1 of plain-SGD runs).
+#pragma once
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace pb {
+namespace cnn {
+
+using namespace pb::umma;
+
+// ---- model geometry --------------------------------------------------------
+constexpr int kImg = 28, kC1 = 32, kC2 = 64, kH1 = 512, kFlat = 7 * 7 * kC2;  // 3136
+constexpr int kP1 = 14 * 14 * kC1;   // 6272 pooled conv1 outputs
+constexpr int kG = 18;               // padded 14x14 grid width (2-pixel border)
+constexpr int kRows = 336;           // plane rows (>= 256 + 4*18 + 4 = 332)
+constexpr int kPlane = kRows * 16;   // bytes per plane (8 channels x bf16)
+constexpr int kP1Bytes = 4 * kPlane;   // p1 image, 4 channel planes
+constexpr int kDzBytes = 8 * kPlane;   // dz2 image, 8 channel planes
+constexpr int kW2Bytes = 25 * 4 * 1024;  // conv2 weights in the UMMA B layout
+constexpr int kPg = 800 + 32 + 64;        // per-sample partials: conv1 w, conv1 b, conv2 b
+// flat parameter offsets (models.py cnn_spec)
+constexpr int64_t oC1W = 0, oC1B = 800, oC2W = 832, oC2B = 832 + 51200, oF1W = oC2B + 64,
+                  oF1B = oF1W + int64_t(kH1) * kFlat, oF2W = oF1B + kH1;
+
+struct Slot {
+  int32_t r;        // group row (parameter row / per-client outputs)
+  int32_t cnt;      // samples in this step's batch (0 = inactive)
+  int64_t row_off;  // offset of the batch's row ids in `order`
+  int64_t hist;     // lazy fc1: first history row of this client (hist_off[r])
+  int64_t pad_;
+};
+static_assert(sizeof(Slot) == 32, "Slot is 32 bytes (ws_slots in parrot_b200.h)");
+
+struct Args {
+  const float* X;
+  const int32_t* Y;
+  const int32_t* order;
+  const int64_t* order_off;
+  const int32_t* n;
+  const int32_t* rank;
+  float* w;               // [G, P] parameters, updated in place
+  const float* w0;        // [P] start model (prox term)
+  const float* ctrl_g;    // [P] or null
+  const float* ctrl_c;    // [G, ctrl_stride] or null
+  int64_t ctrl_stride;
+  double* loss_sum;
+  int32_t* steps;
+  int32_t* bad;
+  // workspace, slot-major with BS samples per slot
+  Slot* slots;
+  uint8_t* p1g;    // [slots*BS, kP1Bytes]  bf16 planes
+  uint8_t* am1;    // [slots*BS, kP1]
+  float* p2;       // [slots*BS, kFlat]   (lazy runs: p2 rows live in hx instead)
+  uint8_t* am2;    // [slots*BS, kFlat]
+  float* h;        // [slots*BS, kH1]
+  float* dh;       // [slots*BS, kH1]
+  float* dht;      // [slots, kH1, 32] dH transposed, samples zero-padded to 32
+  float* dp2;      // [slots*BS, kFlat]
+  uint8_t* dzg;    // [slots*BS, kDzBytes] bf16 planes
+  float* pg;       // [slots*BS, kPg] per-sample conv1-w/conv1-b/conv2-b gradient partials
+  double* eval;    // [2] correct, loss (eval mode)
+  // ---- lazy fc1 (plain SGD): the round's (X, dH) history, see cnn_lazy.cu --
+  // Client row r owns history rows [hist_off[r], hist_off[r] + L_r); step t's
+  // sample i is row t*BS + i.  All four buffers are zeroed before the round.
+  float* hx;              // [rows, kFlat]  X_t (the p2 activations)
+  float* hxt;             // client block [kFlat][L_r]  X transposed
+  float* hd;              // [rows, kH1]    dH_t = dL/dz1
+  float* hdt;             // client block [kH1][L_r]    dH transposed
+  const int64_t* hoff;    // [G] first history row of client row r
+  const int32_t* hlen;    // [G] L_r (multiple of 4)
+  const float* w0t;       // [kFlat][kH1] fc1 block of w0, transposed
+  float* zp;              // [slots * njt][kH1][32] forward correction partials
+  float* gdt;             // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
+  int64_t P;
+  int32_t C, BS, bs, epochs, step;
+  float lr, mu, cg, cc;
+};
+
+__device__ __forceinline__ float sgd(const Args& a, int r, int64_t idx, float w, float g) {
+  if (a.mu != 0.0f) g = fmaf(a.mu, w - a.w0[idx], g);
+  if (a.ctrl_g) g = fmaf(a.cg, a.ctrl_g[idx], g);
+  if (a.ctrl_c) g = fmaf(a.cc, a.ctrl_c[int64_t(r) * a.ctrl_stride + idx], g);
+  return fmaf(-a.lr, g, w);
+}
+
+__device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j) * BS + i; }
+
+// Row i of slot j's p2 activations (the fc1 input X_t).  Lazy runs write it
+// straight into the history, where step t of the client is row t*BS + i.
+__device__ __forceinline__ float* p2_row(const Args& a, const Slot& sl, int j, int i) {
+  return a.hx ? a.hx + (sl.hist + int64_t(a.step) * a.BS + i) * kFlat
+              : a.p2 + sidx(j, i, a.BS) * kFlat;
+}
+
+// NaN-propagating relu / max (torch semantics; fmaxf would drop a NaN and
+// hide a diverged client from the non-finite check)
+__device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
+__device__ __forceinline__ bool takes_max(float z, float best) { return z > best || z != z; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// zero-fills the 16 bytes when !valid (src is not read)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
+  // UMMA B layout, K-major over (tap, ci): core matrix = 8 co x 8 ci
+  return uint32_t((tap * 4 + (ci >> 3)) * 1024 + (co >> 3) * 128 + (co & 7) * 16 + (ci & 7) * 2);
+}
+
+__device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthreads) {
+  const float* w2 = W + oC2W;
+  for (int e = tid; e < 64 * 800; e += nthreads) {
+    const int co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
+    *reinterpret_cast<__nv_bfloat16*>(sW2 + w2_off(co, tap, ci)) = __float2bfloat16(w2[e]);
+  }
+}
+
+// fp32 K-major UMMA operand tile (kind::tf32): core matrix = 8 rows x 16 B
+// (4 elements); row groups `sbo` bytes apart, K groups 128 B apart.
+__device__ __forceinline__ uint32_t kmaj_f32(int r, int k4, int sbo) {
+  return uint32_t((r >> 3) * sbo + k4 * 128 + (r & 7) * 16);
+}
+
+// Launch the lazy-fc1 kernels of one sweep (cnn_lazy.cu).  phase 0: before
+// the head (forward correction + shared forward), phase 1: after it
+// (backward Gram rows + shared/corrected dgrad).
+int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s);
+// Write each client's end fc1 weights W0 - lr * dH^T X (cnn_lazy.cu).
+int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s);
+// Transpose the fc1 block of w0 into a.w0t (cnn_lazy.cu).
+int lazy_fc1_prepare(const Args& a, cudaStream_t s);
+
+}  // namespace cnn
+}  // namespace pb

@@ -51,19 +51,30 @@ def _device_after(spec, w0, X, y, bs, epochs, sweeps, monkeypatch):
             float(rep.client_result.numpy("local_loss")[0]))
 
 
+@pytest.mark.parametrize("lazy", [True, False], ids=["lowrank_fc1", "direct_fc1"])
 @pytest.mark.parametrize("n,bs,epochs", [(100, 20, 1), (45, 16, 1), (7, 20, 1), (20, 20, 3)])
-def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, monkeypatch):
+def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, lazy, monkeypatch):
     """Every local step k is replayed in the bf16-emulating oracle from the
     DEVICE's own weights after step k-1, so errors cannot compound.  A step
     whose batch has a pre-activation within rounding noise of a ReLU/max-pool
     decision boundary legitimately flips (fp32 device vs f64 oracle) and
-    perturbs dH by ~1e-2; hence: median step error <= 1e-3, every step <= 5e-2."""
+    perturbs dH by ~1e-2; hence: median step error <= 1e-3, every step <= 5e-2.
+    FedAvg runs the low-rank fc1 by default (csrc/cnn_lazy.cu); PB_CNN_LAZY=0
+    forces the direct per-client fc1 -- both are checked.  The low-rank path
+    is replayed with tf32(W0) + (W_t - W0) as the fc1 weight (what its tensor
+    cores see); its correction term goes through tf32 Gram products of the
+    client's history, which the replay cannot reproduce (it would need the
+    device's past activations), leaving ~1e-3 relative noise in dH and more
+    boundary flips: its median bound is 2e-3."""
     import torch
     import torch.nn.functional as F
     from oracle import cnn_oracle, fedsim_oracle
     from paper_2303_01778_b200.models import cnn_init
+    monkeypatch.setenv("PB_CNN_LAZY", "1" if lazy else "0")
     X, y = femnist_like.features[100:100 + n], femnist_like.labels[100:100 + n]
     w0 = cnn_init(spec, seed=3)
+    o1, s1 = [(o, s) for nm, o, s, _ in spec.columns() if nm == "fc1_w"][0]
+    base = torch.as_tensor(w0.reshape(-1)[o1:o1 + s1].astype(np.float64)).view(512, 3136) if lazy else None
     bs_eff = min(bs, n)
     nb = -(-n // bs_eff)
     orders = fedsim_oracle.minibatch_orders(4, 11, 2, n, epochs)
@@ -75,7 +86,7 @@ def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, monke
         e, b = divmod(k, nb)
         idx = torch.as_tensor(orders[e][b * bs_eff:(b + 1) * bs_eff])
         params = [p.requires_grad_(True) for p in cnn_oracle.unflatten(prev, 62)]
-        loss = F.cross_entropy(cnn_oracle.forward(params, Xt[idx], True), yt[idx])
+        loss = F.cross_entropy(cnn_oracle.forward(params, Xt[idx], True, base), yt[idx])
         grads = torch.autograd.grad(loss, params)
         ref = np.concatenate([(p - 0.05 * g).detach().reshape(-1).numpy()
                               for p, g in zip(params, grads)])
@@ -84,7 +95,7 @@ def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, monke
         step_errs.append(err)
         losses.append(float(loss.detach()))
         prev = cur.astype(np.float64)
-    assert float(np.median(step_errs)) <= 1e-3, step_errs
+    assert float(np.median(step_errs)) <= (2e-3 if lazy else 1e-3), step_errs
     assert max(step_errs) <= 5e-2, step_errs
     # the device's mean local loss over the whole run vs the replayed step losses
     _, mean_loss = _device_after(spec, w0, X, y, bs, epochs, 0, monkeypatch)
