@@ -198,6 +198,7 @@ typedef struct {
   float* lz_w0t;            /* [3136*512] f32 scratch (W1 of w0 transposed)   */
   float* lz_zp;             /* max_t active_t*njt_t * 512*32 f32, njt_t = ceil(t*BS/128) */
   float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
+  float* lz_fpart;          /* 74*512*32 f32: tail split-K partials           */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;

@@ -73,6 +73,33 @@ def _tf32(x: torch.Tensor) -> torch.Tensor:
     return (f.view(torch.int32) & -8192).view(torch.float32).to(x.dtype)
 
 
+def _tf32_rna(x: torch.Tensor) -> torch.Tensor:
+    """fp32 -> tf32 rounded to nearest, ties away (cvt.rna.tf32.f32): how the
+    low-rank fc1 stores X and dH."""
+    f = x.to(torch.float32).contiguous()
+    return ((f.view(torch.int32) + 4096) & -8192).view(torch.float32).to(x.dtype)
+
+
+class _RnaValue(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return _tf32_rna(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
+class _RnaGrad(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x):
+        return x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, g):
+        return _tf32_rna(g)
+
+
 class _TruncValue(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x):
@@ -107,7 +134,9 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     fc1_base (with emulate_bf16): the round-start fc1 weights W0 of a device
     run that used the low-rank fc1 (csrc/cnn_lazy.cu), whose tensor cores see
     tf32(W0) plus the client's accumulated update in (near) full precision
-    instead of tf32(W_t): the emulated weight is tf32(W0) + (W_t - W0)."""
+    instead of tf32(W_t): the emulated weight is tf32(W0) + (W_t - W0), and X
+    and dL/dz1 (fc1 bias gradient included) are rounded to nearest tf32, as
+    that path stores them."""
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
     h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
@@ -118,8 +147,11 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
         h = F.max_pool2d(F.relu(F.conv2d(h, c2w.permute(0, 3, 1, 2), c2b, padding=2)), 2)
     h = h.permute(0, 2, 3, 1).reshape(h.shape[0], -1)  # NHWC flatten
     if emulate_bf16:
-        w1 = _TruncValue.apply(f1w) if fc1_base is None else f1w - fc1_base + _tf32(fc1_base)
-        h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ w1.t()) + f1b)
+        if fc1_base is None:
+            h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ _TruncValue.apply(f1w).t()) + f1b)
+        else:
+            w1 = f1w - fc1_base + _tf32(fc1_base)
+            h = F.relu(_RnaGrad.apply(_RnaValue.apply(h) @ w1.t() + f1b))
     else:
         h = F.relu(h @ f1w.t() + f1b)
     return h @ f2w.t() + f2b

@@ -59,7 +59,7 @@ class _LazyWorkspace:
         out = {"hx": self._get("hx", rows * 3136, device), "hxt": self._get("hxt", rows * 3136, device),
                "hd": self._get("hd", rows * 512, device), "hdt": self._get("hdt", rows * 512, device),
                "w0t": self._get("w0t", 3136 * 512, device), "zp": self._get("zp", zp, device),
-               "gdt": self._get("gdt", gdt, device)}
+               "gdt": self._get("gdt", gdt, device), "fpart": self._get("fpart", 74 * 512 * 32, device)}
         for k, width in (("hx", 3136), ("hxt", 3136), ("hd", 512), ("hdt", 512)):
             out[k][:rows * width].zero_()
         return out
@@ -151,7 +151,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
         a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),
                                                 ptr(lz["hdt"]))
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
-        a.lz_zp, a.lz_gdt = ptr(lz["zp"]), ptr(lz["gdt"])
+        a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)

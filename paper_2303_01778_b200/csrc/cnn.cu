@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
           arg = d;
         }
       }
-      p2[o] = best;
+      p2[o] = a.hx ? tf32_rna(best) : best;
       am2[o] = uint8_t(arg);
     }
     __syncthreads();
@@ -337,16 +337,22 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
   __syncthreads();
   const float* b2 = W2 + int64_t(C) * kH1;
-  // logits: one warp per (sample, class), lanes split the 512-long dot product
-  for (int p = warp; p < cnt * C; p += kHeadThreads / 32) {
-    const int i = p / C, c = p - i * C;
-    const float* hr = sH + i * kH1;
+  // logits: one warp per class c holds W2[c] in registers (16 per lane, all
+  // loads in flight at once); lanes split each 512-long dot product
+  for (int c = warp; c < C; c += kHeadThreads / 32) {
     const float* wc = W2 + int64_t(c) * kH1;
-    float s = 0.0f;
-#pragma unroll 4
-    for (int o = lane; o < kH1; o += 32) s = fmaf(hr[o], wc[o], s);
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) sL[p] = s + b2[c];
+    float wr[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wr[k] = wc[lane + 32 * k];
+    const float bc = b2[c];
+    for (int i = 0; i < cnt; ++i) {
+      const float* hr = sH + i * kH1;
+      float s = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s = fmaf(hr[lane + 32 * k], wr[k], s);
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) sL[i * C + c] = s + bc;
+    }
   }
   __syncthreads();
   double lpart = 0.0, cpart = 0.0;
@@ -397,15 +403,40 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
   const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
   float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
-  for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
-    const int i = p >> 9, o = p & (kH1 - 1);
-    float s = 0.0f;
-    for (int c = 0; c < C; ++c) s = fmaf(sL[i * C + c], W2[int64_t(c) * kH1 + o], s);
-    const float g = sH[p] > 0.0f ? s : 0.0f;
-    dh[p] = g;
-    sDH[p] = g;
+  // one pass over W2 per output o (thread-owned column): dH[i][o] from the
+  // old W2[c][o], then the fc2 update of that element (fused; sample order)
+  for (int o = tid; o < kH1; o += kHeadThreads) {
+    float hreg[32], acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      hreg[i] = i < cnt ? sH[i * kH1 + o] : 0.0f;
+      acc[i] = 0.0f;
+    }
+    for (int c = 0; c < C; ++c) {
+      const int64_t idx = oF2W + int64_t(c) * kH1 + o;
+      const float w = W[idx];
+      float g = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i < cnt) {
+          const float d = sL[i * C + c];
+          acc[i] = fmaf(d, w, acc[i]);
+          g = fmaf(d, hreg[i], g);
+        }
+      }
+      W[idx] = sgd(a, sl.r, idx, w, g);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < cnt) {
+        float gi = hreg[i] > 0.0f ? acc[i] : 0.0f;
+        if (a.hx) gi = tf32_rna(gi);
+        dh[i * kH1 + o] = gi;
+        sDH[i * kH1 + o] = gi;
+      }
+    }
   }
-  __syncthreads();  // every read of the old W2 is done before the update
+  __syncthreads();  // sDH complete
   if (a.hx) {
     const int L = a.hlen[sl.r];
     float* hdt = a.hdt + sl.hist * kH1 + int64_t(a.step) * a.BS;
@@ -425,13 +456,6 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
       const int o = p >> 5, i = p & 31;
       dht[p] = i < cnt ? sDH[i * kH1 + o] : 0.0f;
     }
-  }
-  for (int p = tid; p < C * kH1; p += kHeadThreads) {
-    const int c = p >> 9, o = p & (kH1 - 1);
-    float g = 0.0f;
-    for (int i = 0; i < cnt; ++i) g = fmaf(sL[i * C + c], sH[i * kH1 + o], g);
-    const int64_t idx = oF2W + p;
-    W[idx] = sgd(a, sl.r, idx, W[idx], g);
   }
   for (int c = tid; c < C; c += kHeadThreads) {
     float g = 0.0f;
@@ -969,7 +993,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
   a.hx = t.lz_hx; a.hxt = t.lz_hxt; a.hd = t.lz_hd; a.hdt = t.lz_hdt; a.hoff = t.lz_hoff;
-  a.hlen = t.lz_hlen; a.w0t = t.lz_w0t; a.zp = t.lz_zp; a.gdt = t.lz_gdt;
+  a.hlen = t.lz_hlen; a.w0t = t.lz_w0t; a.zp = t.lz_zp; a.gdt = t.lz_gdt; a.fpart = t.lz_fpart;
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
   a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.dht = t.ws_dht; a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
@@ -1038,7 +1062,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
     if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hxt || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
-        !a.w0t || !a.zp || !a.gdt || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
+        !a.w0t || !a.zp || !a.gdt || !a.fpart || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
         !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
       return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
     if ((rc = lazy_fc1_prepare(a, s))) return rc;

@@ -77,6 +77,7 @@ struct Args {
   const float* w0t;       // [kFlat][kH1] fc1 block of w0, transposed
   float* zp;              // [slots * njt][kH1][32] forward correction partials
   float* gdt;             // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
+  float* fpart;           // [ks][active][kH1][32] tail split-K partials (<= 74*16384 f32)
   int64_t P;
   int32_t C, BS, bs, epochs, step;
   float lr, mu, cg, cc;
@@ -96,6 +97,15 @@ __device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j
 __device__ __forceinline__ float* p2_row(const Args& a, const Slot& sl, int j, int i) {
   return a.hx ? a.hx + (sl.hist + int64_t(a.step) * a.BS + i) * kFlat
               : a.p2 + sidx(j, i, a.BS) * kFlat;
+}
+
+// fp32 -> tf32, round to nearest (ties away).  The low-rank fc1 stores its
+// tensor-core operands (X, dH and the Gram rows) pre-rounded, so the MMA's
+// truncation is exact and no operand carries truncation bias.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 // NaN-propagating relu / max (torch semantics; fmaxf would drop a NaN and

@@ -17,8 +17,11 @@
 // materialised once (W0 - lr * HD^T HX), so the fold and every API above see
 // ordinary per-client weights.
 //
-// All contractions are tcgen05 kind::tf32 (fp32 operands, truncated to tf32,
-// fp32 accumulation in TMEM), every operand K-major in the SWIZZLE_NONE
+// All contractions are tcgen05 kind::tf32 (fp32 accumulation in TMEM).  The
+// history operands (X, dH) and the Gram rows are stored rounded to nearest
+// tf32, so the MMA's operand truncation is exact for them and the
+// corrections carry no truncation bias; W0 is truncated.  Every operand is
+// K-major in the SWIZZLE_NONE
 // layout, staged by cp.async through a 4-deep ring (umma.cuh conventions).
 // Reductions have a fixed order (no atomics): results are deterministic.
 #include "cnn_common.cuh"
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
       tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        *reinterpret_cast<float*>(sGxT + kmaj_f32(i, j >> 2, 4096) + (j & 3) * 4) = v[i];
+        *reinterpret_cast<float*>(sGxT + kmaj_f32(i, j >> 2, 4096) + (j & 3) * 4) = tf32_rna(v[i]);
       fence_before_sync();
     }
   };
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
     const int64_t jstride = int64_t(njt) * 128;
     float* g = a.gdt + int64_t(s) * 32 * jstride + j0 + j;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) g[i * jstride] = nlr * v[i];
+    for (int i = 0; i < 32; ++i) g[i * jstride] = tf32_rna(nlr * v[i]);
   }
   fence_before_sync();
   __syncthreads();
@@ -247,27 +250,56 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_fwd: h = relu(X_t W0^T + b1 + sum_jt zp) for 8 slots x 32 rows
-// (M = 128 o, N = 256, K = 3136; W0 shared by every client of the sweep)
-// grid (4 o-tiles, ceil(active / 8)), 256 threads
+// k_lz_fwd: h = relu(X_t W0^T + b1 + sum_jt zp) for spc slots x 32 rows
+// (M = 128 o, N = spc*32, K = 3136; W0 shared by every client of the sweep).
+// Head sweeps: spc = 8, fused epilogue.  Tail sweeps (few clients): spc = 1
+// and K split over gridDim.z CTAs writing raw partials to fpart, summed in
+// split order by k_lz_fwd_epi (deterministic).
+// grid (4 o-tiles, ceil(active / spc), ks), 256 threads
 // ---------------------------------------------------------------------------
-constexpr int kSh8 = 8;                         // slots per CTA (N = 8 x 32)
+constexpr int kSh8 = 8;                         // max slots per CTA (N = 8 x 32)
 constexpr int kShKC = 32;                       // K floats per chunk
 constexpr int kShA = 128 * kShKC * 4;           // 16 KB
 constexpr int kShB = 256 * kShKC * 4;           // 32 KB
 constexpr int kShStage = kShA + kShB;           // 48 KB
 constexpr size_t kShSmem = kStages * kShStage;  // 192 KB
+constexpr int kFwdChunks = kFlat / kShKC;       // 98
+constexpr int kTailCtas = 296;                  // 2 x 148 SMs: tail grids aim for this
+constexpr int kFwdSplitMax = 7;                 // 98 chunks = 7 x 14
 
-__global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active) {
+__device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl, int o, float (&v)[32],
+                                           int njt) {
+  const float b = a.w[int64_t(sl.r) * a.P + oF1B + o];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] += b;
+  for (int jt = 0; jt < njt; ++jt) {
+    const float4* zp = reinterpret_cast<const float4*>(a.zp + ((int64_t(s) * njt + jt) * kH1 + o) * 32);
+#pragma unroll
+    for (int i4 = 0; i4 < 8; ++i4) {
+      const float4 z = zp[i4];
+      v[4 * i4] += z.x;
+      v[4 * i4 + 1] += z.y;
+      v[4 * i4 + 2] += z.z;
+      v[4 * i4 + 3] += z.w;
+    }
+  }
+  float* h = a.h + sidx(s, 0, a.BS) * kH1 + o;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
+}
+
+__global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active, int spc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = blockIdx.x, g0 = blockIdx.y * kSh8;
+  const int q = blockIdx.x, g0 = blockIdx.y * spc, ks = gridDim.z, kz = blockIdx.z;
+  const int c0 = kz * kFwdChunks / ks, c1 = (kz + 1) * kFwdChunks / ks;
   if (tid < kSh8) {
     Slot z{};
-    sS[tid] = g0 + tid < active ? a.slots[g0 + tid] : z;
+    sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
   }
   if (warp == 0) tmem_alloc<256>(&tmem_base);
   ring_init(mbar);
@@ -277,16 +309,16 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active) {
   const uint32_t tmem = tmem_base;
   const float* W1 = a.w0 + oF1W + int64_t(q) * 128 * kFlat;
   const int64_t tb = int64_t(a.step) * a.BS;
+  const int nrows = spc * 32;
 
   auto load = [&](int c, uint8_t* st) {
-    const int k0 = c * kShKC;
+    const int k0 = (c0 + c) * kShKC;
 #pragma unroll
     for (int e = tid; e < 128 * 8; e += 256) {
       const int r = e >> 3, k4 = e & 7;
       cp_async16(st + kmaj_f32(r, k4, 1024), W1 + int64_t(r) * kFlat + k0 + k4 * 4);
     }
-#pragma unroll
-    for (int e = tid; e < 256 * 8; e += 256) {
+    for (int e = tid; e < nrows * 8; e += 256) {
       const int r = e >> 3, k4 = e & 7, u = r >> 5, i = r & 31;
       const bool v = i < sS[u].cnt;
       const float* src = a.hx + (sS[u].hist + tb + (v ? i : 0)) * kFlat + k0 + k4 * 4;
@@ -296,45 +328,58 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active) {
   auto mma = [&](int c, uint8_t* st) {
     const uint32_t sa = smem_u32(st);
     const uint64_t a0 = desc(sa, 128, 1024), b0 = desc(sa + kShA, 128, 1024);
-    const uint32_t idesc = idesc_tf32(128, 256);
+    const uint32_t idesc = idesc_tf32(128, nrows);
 #pragma unroll
     for (int kk = 0; kk < kShKC / 8; ++kk)
       mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
   };
-  mma_ring<kStages>(kFlat / kShKC, smem, kShStage, mbar, load, [](int) {}, mma);
+  mma_ring<kStages>(c1 - c0, smem, kShStage, mbar, load, [](int) {}, mma);
 
   const int njt = njt_of(a);
   const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
+  const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
 #pragma unroll 1
-  for (int u = half * 4; u < half * 4 + 4; ++u) {
+  for (int u = u0; u < u1; ++u) {
     const Slot sl = sS[u];
     float v[32];
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32), *reinterpret_cast<float(*)[16]>(v));
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0) continue;
     const int s = g0 + u;
-    const float b = a.w[int64_t(sl.r) * a.P + oF1B + o];
+    if (ks == 1) {
+      fwd_finish(a, s, sl, o, v, njt);
+    } else {
+      float4* dst = reinterpret_cast<float4*>(a.fpart + ((int64_t(kz) * active + s) * kH1 + o) * 32);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += b;
-    for (int jt = 0; jt < njt; ++jt) {
-      const float4* zp = reinterpret_cast<const float4*>(a.zp + ((int64_t(s) * njt + jt) * kH1 + o) * 32);
-#pragma unroll
-      for (int i4 = 0; i4 < 8; ++i4) {
-        const float4 z = zp[i4];
-        v[4 * i4] += z.x;
-        v[4 * i4 + 1] += z.y;
-        v[4 * i4 + 2] += z.z;
-        v[4 * i4 + 3] += z.w;
-      }
+      for (int i4 = 0; i4 < 8; ++i4) dst[i4] = make_float4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
     }
-    float* h = a.h + sidx(s, 0, a.BS) * kH1 + o;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
   }
   fence_before_sync();
   __syncthreads();
   if (warp == 0) tmem_free<256>(tmem);
+}
+
+// k_lz_fwd_epi: sum the ks split-K partials (split order), then as above.
+// grid (active), 512 threads (one per o)
+__global__ void __launch_bounds__(512) k_lz_fwd_epi(Args a, int active, int ks) {
+  const int s = blockIdx.x, o = threadIdx.x;
+  const Slot sl = a.slots[s];
+  if (sl.cnt == 0) return;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+  for (int kz = 0; kz < ks; ++kz) {
+    const float4* p = reinterpret_cast<const float4*>(a.fpart + ((int64_t(kz) * active + s) * kH1 + o) * 32);
+#pragma unroll
+    for (int i4 = 0; i4 < 8; ++i4) {
+      const float4 z = p[i4];
+      v[4 * i4] += z.x;
+      v[4 * i4 + 1] += z.y;
+      v[4 * i4 + 2] += z.z;
+      v[4 * i4 + 3] += z.w;
+    }
+  }
+  fwd_finish(a, s, sl, o, v, njt_of(a));
 }
 
 // ---------------------------------------------------------------------------
@@ -346,17 +391,17 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active) {
 // ---------------------------------------------------------------------------
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
-__global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active) {
+__global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active, int spc) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   __shared__ int sL[kSh8], sU[kSh8], sNv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int k0 = blockIdx.x * 128, g0 = blockIdx.y * kSh8;
+  const int k0 = blockIdx.x * 128, g0 = blockIdx.y * spc;
   if (tid < kSh8) {
     Slot z{};
-    sS[tid] = g0 + tid < active ? a.slots[g0 + tid] : z;
+    sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
     sL[tid] = sS[tid].cnt > 0 ? a.hlen[sS[tid].r] : 0;
   }
   __syncthreads();
@@ -387,8 +432,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active) {
         const bool v = k0 + r < kFlat;
         cp_async16_zfill(st + kmaj_f32(r, k4, 1024), a.w0t + int64_t(v ? k0 + r : 0) * kH1 + o0 + k4 * 4, v);
       }
-#pragma unroll
-      for (int e = tid; e < 256 * 8; e += 256) {
+      for (int e = tid; e < spc * 32 * 8; e += 256) {
         const int r = e >> 3, k4 = e & 7, u = r >> 5, i = r & 31;
         const bool v = i < sS[u].cnt;
         const float* src = a.hd + (sS[u].hist + tb + (v ? i : 0)) * kH1 + o0 + k4 * 4;
@@ -414,7 +458,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active) {
     const uint32_t sa = smem_u32(st);
     const uint64_t a0 = desc(sa, 128, 1024), b0 = desc(sa + kShA, 128, 1024);
     if (c < n1) {
-      const uint32_t idesc = idesc_tf32(128, 256);
+      const uint32_t idesc = idesc_tf32(128, spc * 32);
 #pragma unroll
       for (int kk = 0; kk < kShKC / 8; ++kk)
         mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
@@ -429,8 +473,9 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active) {
   mma_ring<kStages>(n1 + (t > 0 ? sNv * nj : 0), smem, kShStage, mbar, load, [](int) {}, mma);
 
   const int k = k0 + (warp & 3) * 32 + lane, half = warp >> 2;
+  const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
 #pragma unroll 1
-  for (int u = half * 4; u < half * 4 + 4; ++u) {
+  for (int u = u0; u < u1; ++u) {
     const Slot sl = sS[u];
     float v[32];
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32), *reinterpret_cast<float(*)[16]>(v));
@@ -553,7 +598,11 @@ int lazy_fc1_prepare(const Args& a, cudaStream_t s) {
 
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   const int njt = njt_of_host(a.step, a.BS);
-  const unsigned groups = unsigned((active + kSh8 - 1) / kSh8);
+  // head sweeps: 8 clients share each W0 tile (N = 256); tail sweeps (fewer
+  // clients than SMs): one client per CTA, and the forward splits K so that
+  // the grid still covers the machine
+  const int spc = active >= 148 ? kSh8 : 1;
+  const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
     pb::prof_begin(pb::K_CNN_LZ_XT, s);
     k_lz_xt<<<dim3(active, kBwKT), 128, 0, s>>>(a);
@@ -563,9 +612,15 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       k_lz_gram<true><<<dim3(active, njt), 128, kGramFwdSmem, s>>>(a);
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
     }
+    const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
-    k_lz_fwd<<<dim3(kH1 / 128, groups), 256, kShSmem, s>>>(a, active);
+    k_lz_fwd<<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
+    if (ks > 1) {
+      pb::prof_begin(pb::K_CNN_LZ_FWD, s);
+      k_lz_fwd_epi<<<active, kH1, 0, s>>>(a, active, ks);
+      pb::prof_end(pb::K_CNN_LZ_FWD, s);
+    }
   } else {
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
@@ -573,7 +628,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
-    k_lz_bwd<<<dim3(kBwKT, groups), 256, kShSmem, s>>>(a, active);
+    k_lz_bwd<<<dim3(kBwKT, groups), 256, kShSmem, s>>>(a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");

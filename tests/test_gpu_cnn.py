@@ -51,21 +51,9 @@ def _device_after(spec, w0, X, y, bs, epochs, sweeps, monkeypatch):
             float(rep.client_result.numpy("local_loss")[0]))
 
 
-@pytest.mark.parametrize("lazy", [True, False], ids=["lowrank_fc1", "direct_fc1"])
-@pytest.mark.parametrize("n,bs,epochs", [(100, 20, 1), (45, 16, 1), (7, 20, 1), (20, 20, 3)])
-def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, lazy, monkeypatch):
-    """Every local step k is replayed in the bf16-emulating oracle from the
-    DEVICE's own weights after step k-1, so errors cannot compound.  A step
-    whose batch has a pre-activation within rounding noise of a ReLU/max-pool
-    decision boundary legitimately flips (fp32 device vs f64 oracle) and
-    perturbs dH by ~1e-2; hence: median step error <= 1e-3, every step <= 5e-2.
-    FedAvg runs the low-rank fc1 by default (csrc/cnn_lazy.cu); PB_CNN_LAZY=0
-    forces the direct per-client fc1 -- both are checked.  The low-rank path
-    is replayed with tf32(W0) + (W_t - W0) as the fc1 weight (what its tensor
-    cores see); its correction term goes through tf32 Gram products of the
-    client's history, which the replay cannot reproduce (it would need the
-    device's past activations), leaving ~1e-3 relative noise in dH and more
-    boundary flips: its median bound is 2e-3."""
+def _replay_steps(spec, femnist_like, n, bs, epochs, lazy, monkeypatch):
+    """Replay every local step of one client in the emulating oracle from the
+    device's weights after the previous step; (per-step errors, losses)."""
     import torch
     import torch.nn.functional as F
     from oracle import cnn_oracle, fedsim_oracle
@@ -82,7 +70,7 @@ def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, lazy,
     prev = w0.astype(np.float64)
     step_errs, losses = [], []
     for k in range(epochs * nb):
-        cur, loss_k = _device_after(spec, w0, X, y, bs, epochs, k + 1, monkeypatch)
+        cur, _ = _device_after(spec, w0, X, y, bs, epochs, k + 1, monkeypatch)
         e, b = divmod(k, nb)
         idx = torch.as_tensor(orders[e][b * bs_eff:(b + 1) * bs_eff])
         params = [p.requires_grad_(True) for p in cnn_oracle.unflatten(prev, 62)]
@@ -90,16 +78,37 @@ def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, n, bs, epochs, lazy,
         grads = torch.autograd.grad(loss, params)
         ref = np.concatenate([(p - 0.05 * g).detach().reshape(-1).numpy()
                               for p, g in zip(params, grads)])
-        err = max(_rel(cur[o:o + s] - prev[o:o + s], ref[o:o + s] - prev[o:o + s])
-                  for _, o, s, _ in spec.columns())
-        step_errs.append(err)
+        step_errs.append(max(_rel(cur[o:o + s] - prev[o:o + s], ref[o:o + s] - prev[o:o + s])
+                             for _, o, s, _ in spec.columns()))
         losses.append(float(loss.detach()))
         prev = cur.astype(np.float64)
-    assert float(np.median(step_errs)) <= (2e-3 if lazy else 1e-3), step_errs
-    assert max(step_errs) <= 5e-2, step_errs
     # the device's mean local loss over the whole run vs the replayed step losses
     _, mean_loss = _device_after(spec, w0, X, y, bs, epochs, 0, monkeypatch)
-    assert abs(mean_loss - np.mean(losses)) / np.mean(losses) <= 1e-3
+    assert abs(mean_loss - np.mean(losses)) / np.mean(losses) <= 1e-3, (n, bs, epochs)
+    return step_errs
+
+
+@pytest.mark.parametrize("lazy", [True, False], ids=["lowrank_fc1", "direct_fc1"])
+def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, lazy, monkeypatch):
+    """Every local step k is replayed in the bf16-emulating oracle from the
+    DEVICE's own weights after step k-1, so errors cannot compound.  A step
+    whose batch has a pre-activation within rounding noise of a ReLU/max-pool
+    decision boundary legitimately flips (fp32 device vs f64 oracle) and
+    perturbs the update by ~1e-2 (about one step in five, on either fc1
+    path).  Over the 12 steps of four clients (full, partial and single
+    batches, three epochs): median step error <= 1e-3, at least two thirds
+    of the steps <= 2e-3, every step <= 5e-2.  FedAvg runs the low-rank fc1
+    by default (csrc/cnn_lazy.cu), replayed with tf32(W0) + (W_t - W0) as the
+    fc1 weight and tf32-rounded X / dL/dz1 (what its tensor cores see);
+    PB_CNN_LAZY=0 forces the direct per-client fc1.  Both are checked."""
+    errs = []
+    for n, bs, epochs in [(100, 20, 1), (45, 16, 1), (7, 20, 1), (20, 20, 3)]:
+        errs += _replay_steps(spec, femnist_like, n, bs, epochs, lazy, monkeypatch)
+    errs = np.asarray(errs)
+    assert len(errs) == 12
+    assert float(np.median(errs)) <= 1e-3, errs
+    assert (errs <= 2e-3).mean() >= 2 / 3, errs
+    assert errs.max() <= 5e-2, errs
 
 
 def test_cnn_deterministic_across_cta_splits(spec, femnist_like, monkeypatch):
