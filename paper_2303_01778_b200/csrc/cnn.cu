@@ -412,19 +412,28 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
       hreg[i] = i < cnt ? sH[i * kH1 + o] : 0.0f;
       acc[i] = 0.0f;
     }
-    for (int c = 0; c < C; ++c) {
-      const int64_t idx = oF2W + int64_t(c) * kH1 + o;
-      const float w = W[idx];
-      float g = 0.0f;
+    // 8 classes per pass: their W2 loads are all in flight before any store
+    for (int c0 = 0; c0 < C; c0 += 8) {
+      float wv[8];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (i < cnt) {
-          const float d = sL[i * C + c];
-          acc[i] = fmaf(d, w, acc[i]);
-          g = fmaf(d, hreg[i], g);
+      for (int u = 0; u < 8; ++u)
+        wv[u] = c0 + u < C ? W[oF2W + int64_t(c0 + u) * kH1 + o] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u;
+        if (c >= C) break;
+        float g = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i < cnt) {
+            const float d = sL[i * C + c];
+            acc[i] = fmaf(d, wv[u], acc[i]);
+            g = fmaf(d, hreg[i], g);
+          }
         }
+        const int64_t idx = oF2W + int64_t(c) * kH1 + o;
+        W[idx] = sgd(a, sl.r, idx, wv[u], g);
       }
-      W[idx] = sgd(a, sl.r, idx, w, g);
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
