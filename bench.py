@@ -270,6 +270,8 @@ def run_b200(args) -> dict:
 
     # ---- aggregation microbench (config 5), bounded ----
     agg = aggregation_microbench(world, dev) if args.agg else None
+    # ---- config 4 (ResNet-18-GN) rounds, 1 GPU, secondary ----
+    c4 = resnet_round_bench(dev) if args.c4 and world == 1 else None
 
     peaks, peak_src = load_peaks()
     samples_round = float(np.sum(sizes)) / M_TOTAL * M_ROUND
@@ -311,6 +313,8 @@ def run_b200(args) -> dict:
     }
     if agg is not None:
         out["aggregation"] = agg
+    if c4 is not None:
+        out["c4_resnet"] = c4
     if rank == 0 and args.cpu_baseline and world == 1:
         v, info = cpu_sample_rounds_per_s(sizes)
         out["cpu_baseline"] = {"value": v, "unit": "rounds/s", "cores": info["threads"],
@@ -407,6 +411,79 @@ def aggregation_microbench(world: int, dev) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# config 4: ResNet-18 (GroupNorm) FedAvg rounds (secondary measurement)
+# ---------------------------------------------------------------------------
+C4_TOTAL, C4_ROUND, C4_SAMPLES, C4_CLASSES = 1000, 100, 50_000, 10
+# ResNet-18 CIFAR training FLOPs per sample: 0.556 GMAC fwd x 2 x 3
+C4_FLOP_PER_SAMPLE = 3.34e9
+
+
+def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
+    """C4: 1000 clients with the reference's Dirichlet size rule (quantity
+    skew 0.1, min 5 samples), 100 per round, bs 20, E 1, lr 0.05 on one GPU;
+    synthetic CIFAR-shaped data generated on the device."""
+    import torch
+    import paper_2303_01778_b200 as pb
+    from paper_2303_01778_b200._lib import lib, prof_collect
+    from paper_2303_01778_b200.core import STREAM_PARTITION, ClientProfile, DataSlice, stream_rng
+    from paper_2303_01778_b200.data import PartitionSpec, client_sizes as sizes_fn
+    from paper_2303_01778_b200.trainer import ClientData
+    sizes = sizes_fn(C4_SAMPLES, C4_TOTAL, PartitionSpec(label_skew=0.5, quantity_skew=0.1,
+                                                         min_samples_per_client=5),
+                     stream_rng(0, STREAM_PARTITION))
+    g = torch.Generator(device=dev).manual_seed(4)
+    means = torch.randn(C4_CLASSES, 3072, generator=g, device=dev)
+    means *= 3.0 / means.norm(dim=1, keepdim=True)
+    labels = torch.randint(0, C4_CLASSES, (C4_SAMPLES,), generator=g, device=dev, dtype=torch.int64)
+    X = means[labels] + torch.randn(C4_SAMPLES, 3072, generator=g, device=dev)
+    base = np.zeros(C4_TOTAL, dtype=np.int64)
+    base[1:] = np.cumsum(sizes)[:-1]
+    data = ClientData(X, labels.to(torch.int32), base, sizes.astype(np.int64), 3072, C4_CLASSES)
+    feat = np.zeros((1, 3072), dtype=np.float32)
+    profiles = [ClientProfile(c, int(n), DataSlice(np.broadcast_to(feat, (int(n), 3072)),
+                                                  np.zeros(int(n), dtype=np.int64), np.arange(int(n))))
+                for c, n in enumerate(sizes)]
+    cfg = pb.SimConfig(total_clients=C4_TOTAL, concurrent_clients=C4_ROUND, num_devices=1,
+                       total_rounds=warmup + steps + 1, warmup_rounds=1, seed=0, scheme="PARROT")
+    eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=LR, batch_size=BS), profiles, pb.make_device_models(1),
+                              model="resnet", client_data=data, init_seed=0)
+    for r in range(warmup):
+        eng.run_round(r)
+    prepared = [eng.prepare_round(warmup + i) for i in range(steps)]
+    samples = sum(int(np.sum(p.group.n)) for p in prepared if p.group)
+    for p in prepared:
+        p.upload()
+    lib.pb_prof_enable(1)
+    prof_collect()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for p in prepared:
+        eng.execute_round(p, sync=False)
+    e1.record()
+    torch.cuda.synchronize()
+    lib.pb_prof_enable(0)
+    kernels = prof_collect()
+    ms = e0.elapsed_time(e1)
+    peaks, src = load_peaks()
+    tf = C4_FLOP_PER_SAMPLE * samples / (ms / 1e3) / 1e12
+    conv_ms = sum(v[0] for k, v in kernels.items() if k.startswith("rn_conv"))
+    conv_tf = C4_FLOP_PER_SAMPLE * samples / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else None
+    del eng, data, X
+    torch.cuda.empty_cache()
+    return {"workload": "C4: FedAvg ResNet-18-GN (P=11,173,962), 1000 clients (Dirichlet sizes, "
+                        "quantity skew 0.1), 100 per round, bs=20, E=1, lr=0.05, 1 GPU",
+            "rounds_per_s": steps / (ms / 1e3), "ms_per_round": ms / steps,
+            "samples_per_round": samples / steps,
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": peaks["bf16_tflops_sustained"],
+                         "unit": "TFLOP/s", "frac": tf / peaks["bf16_tflops_sustained"],
+                         "peak_source": f"{src} bf16 sustained",
+                         "work": f"{C4_FLOP_PER_SAMPLE:.3g} FLOP/sample x {samples} samples, whole round"},
+            "conv_kernels_tflops": conv_tf,
+            "kernels_ms_per_round": {k: round(v[0] / steps, 3) for k, v in kernels.items()}}
+
+
+# ---------------------------------------------------------------------------
 # the reference (CPU oracle port) arm
 # ---------------------------------------------------------------------------
 
@@ -443,6 +520,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-agg", dest="agg", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-c4", dest="c4", action="store_false")
     args = ap.parse_args()
     out = run_reference(args) if args.impl == "reference" else run_b200(args)
     if out is not None:

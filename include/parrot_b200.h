@@ -42,7 +42,8 @@ int pb_device_sm_count(int device);
  *   5 state_scatter 6 lr_train 7 lr_eval 8 cnn_slots 9 cnn_fwd 10 cnn_fc1_fwd
  *   11 cnn_head 12 cnn_fc1_bwd 13 cnn_bwd_conv 14 cnn_wgrad 15 cnn_lz_xt
  *   16 cnn_lz_gram_fwd 17 cnn_lz_fwd 18 cnn_lz_gram_bwd 19 cnn_lz_bwd 20 cnn_lz_mat
- * recorded since the last collect (nslots >= 21), synchronising on them. */
+ *   21 rn_conv_fwd 22 rn_conv_dgrad 23 rn_conv_wgrad 24 rn_norm 25 rn_head 26 rn_sgd
+ * recorded since the last collect (nslots >= 27), synchronising on them. */
 int pb_prof_enable(int on);
 int64_t pb_launch_count(void);
 int pb_prof_collect(double* ms, int64_t* count, int nslots);
@@ -211,6 +212,50 @@ int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
 int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * (a) batched client training, ResNet-18 with GroupNorm (BASELINE config 4;
+ *     the reference has no ResNet -- semantics follow client_execute,
+ *     fedsim/trainer.py:427-477, plain SGD / FedAvg).  Parameters: flat fp32
+ *     per client in the layout of models.py:resnet_layout (P = 11,173,962 at
+ *     C = 10); inputs 3072 fp32 = a 32x32x3 NHWC image.  All active clients
+ *     advance one SGD step per sweep; every convolution (forward, dgrad,
+ *     wgrad) is a tcgen05 implicit GEMM on bf16 operands with fp32 TMEM
+ *     accumulation.  Workspaces are caller-allocated; their per-slot sizes
+ *     come from pb_resnet_workspace(BS, C, out4):
+ *       out4[0] arena bytes per slot, out4[1] P16 (bf16 weight-copy row
+ *       length), out4[2] wgrad-partial floats per slot, out4[3] GroupNorm
+ *       partial floats per slot.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const float* X;           /* [rows, 3072] fp32 images                       */
+  const int32_t* Y;         /* [rows] labels                                  */
+  const int32_t* order;     /* packed minibatch row ids (pb_minibatch_rows)   */
+  const int64_t* order_off; /* [g] per client                                 */
+  const int32_t* n;         /* [g] samples per client                         */
+  const int32_t* rank;      /* [g] slot -> client row, by step count desc     */
+  const int32_t* active;    /* HOST [sweeps]: clients still stepping per sweep*/
+  int32_t sweeps;
+  float* w;                 /* [g, w_stride] params (start = w0), in place    */
+  int64_t w_stride;         /* floats, multiple of 4, >= P                    */
+  double* loss_sum;         /* [g] (zero-initialised by the caller)           */
+  int32_t* steps;           /* [g] (zero-initialised)                         */
+  int32_t* bad;             /* [g] (-1 initialised)                           */
+  void* ws_slots;           /* 16 B per slot                                  */
+  void* ws_w16;             /* [g][P16] bf16                                  */
+  uint8_t* ws_arena;        /* [g][arena bytes]                               */
+  float* ws_part;           /* [g][partial floats]                            */
+  float* ws_gnp;            /* [g][GroupNorm partial floats]                  */
+  int64_t g;
+  int32_t C, BS, batch_size, epochs;
+  float lr;
+} pb_resnet_train_args;
+int pb_resnet_workspace(int BS, int C, int64_t* out4);
+int pb_resnet_train_group(const pb_resnet_train_args* args, void* stream);
+/* Forward-only evaluation of parameter row 0 of args->w on `rows` samples
+ * (order = row ids); out2[0] += #correct, out2[1] += sum CE.  args->g is the
+ * workspace capacity in slots of BS samples. */
+int pb_resnet_eval(const pb_resnet_train_args* args, int64_t rows, double* out2, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics
  * ------------------------------------------------------------------------- */
 /* One M x N x K bf16 tcgen05 GEMM D = A * B^T (A [M,K], B [N,K] row-major
@@ -220,6 +265,12 @@ int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2, void*
  * conventions the conv kernels use (tests only). */
 int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K, int a_mode,
                      int b_mode, int shift, void* stream);
+
+/* One ResNet convolution through k_rn_conv (mode 0 fwd, 1 dgrad, 2 wgrad)
+ * on caller data, single slot of BS samples of which cnt are live (tests
+ * only; allocates scratch).  See csrc/resnet.cu for the layouts. */
+int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout, int H, int R, int stride,
+                        const void* x, const void* w, const void* dz, float* out, void* stream);
 
 /* 128 x N x K tf32 tcgen05 GEMM D = A * B^T from fp32 row-major A [128,K],
  * B [N,K]; a_mn/b_mn select MN-major smem staging (tests only). */

@@ -48,6 +48,18 @@ class CnnTrainArgs(ctypes.Structure):
     ]
 
 
+class ResnetTrainArgs(ctypes.Structure):
+    _fields_ = [
+        ("X", c_void_p), ("Y", c_void_p), ("order", c_void_p), ("order_off", c_void_p),
+        ("n", c_void_p), ("rank", c_void_p), ("active", c_void_p), ("sweeps", c_int32),
+        ("w", c_void_p), ("w_stride", c_int64), ("loss_sum", c_void_p), ("steps", c_void_p),
+        ("bad", c_void_p), ("ws_slots", c_void_p), ("ws_w16", c_void_p), ("ws_arena", c_void_p),
+        ("ws_part", c_void_p), ("ws_gnp", c_void_p), ("g", c_int64),
+        ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
+        ("lr", c_float),
+    ]
+
+
 _SIGS = {
     "pb_last_error": (ctypes.c_char_p, []),
     "pb_version": (c_int, []),
@@ -79,6 +91,11 @@ _SIGS = {
     "pb_umma_tf32_probe": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pb_umma_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
+    "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
+    "pb_rn_conv_selftest": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pb_resnet_train_group": (c_int, [POINTER(ResnetTrainArgs), c_void_p]),
+    "pb_resnet_eval": (c_int, [POINTER(ResnetTrainArgs), c_int64, c_void_p, c_void_p]),
     "pb_cnn_eval": (c_int, [POINTER(CnnTrainArgs), c_int64, c_void_p, c_void_p]),
     "pb_umma_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                                  c_int, c_void_p]),
@@ -113,7 +130,8 @@ lib = _Lib(_PATH)
 KERNEL_CLASSES = ("fold1", "fold_group", "lincomb", "delta_affine", "state_gather",
                   "state_scatter", "lr_train", "lr_eval", "cnn_slots", "cnn_fwd", "cnn_fc1_fwd",
                   "cnn_head", "cnn_fc1_bwd", "cnn_bwd_conv", "cnn_wgrad", "cnn_lz_xt",
-                  "cnn_lz_gram_fwd", "cnn_lz_fwd", "cnn_lz_gram_bwd", "cnn_lz_bwd", "cnn_lz_mat")
+                  "cnn_lz_gram_fwd", "cnn_lz_fwd", "cnn_lz_gram_bwd", "cnn_lz_bwd", "cnn_lz_mat",
+                  "rn_conv_fwd", "rn_conv_dgrad", "rn_conv_wgrad", "rn_norm", "rn_head", "rn_sgd")
 
 
 def prof_collect() -> dict[str, tuple[float, int]]:

@@ -113,22 +113,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
 __device__ __forceinline__ bool takes_max(float z, float best) { return z > best || z != z; }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
-// zero-fills the 16 bytes when !valid (src is not read)
-__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 __device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
   // UMMA B layout, K-major over (tap, ci): core matrix = 8 co x 8 ci
   return uint32_t((tap * 4 + (ci >> 3)) * 1024 + (co >> 3) * 128 + (co & 7) * 16 + (ci & 7) * 2);
@@ -140,12 +124,6 @@ __device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthre
     const int co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
     *reinterpret_cast<__nv_bfloat16*>(sW2 + w2_off(co, tap, ci)) = __float2bfloat16(w2[e]);
   }
-}
-
-// fp32 K-major UMMA operand tile (kind::tf32): core matrix = 8 rows x 16 B
-// (4 elements); row groups `sbo` bytes apart, K groups 128 B apart.
-__device__ __forceinline__ uint32_t kmaj_f32(int r, int k4, int sbo) {
-  return uint32_t((r >> 3) * sbo + k4 * 128 + (r & 7) * 16);
 }
 
 // Launch the lazy-fc1 kernels of one sweep (cnn_lazy.cu).  phase 0: before

@@ -33,50 +33,6 @@ using namespace pb::cnn;
 
 constexpr int kStages = 4;
 
-// The MMA ring: chunk c is loaded into stage c % S, S-2 chunks ahead, and its
-// MMAs are committed to mbar[c & 1] (two barriers, so waiting for chunk c-2
-// can never alias a later phase).  load(c, stage) issues the cp.async of one
-// chunk (all threads); mid(c) runs on all threads after chunk c landed and
-// before the MMAs are issued; mma(c, stage) issues (thread 0 only).
-template <int S, class Load, class Mid, class Mma>
-__device__ __forceinline__ void mma_ring(int n, uint8_t* ring, int stage_bytes, uint64_t* mbar,
-                                         Load load, Mid mid, Mma mma) {
-  static_assert(S >= 3, "ring depth");
-#pragma unroll 1
-  for (int c = 0; c < S - 2; ++c) {
-    if (c < n) load(c, ring + c * stage_bytes);
-    cp_async_commit();
-  }
-#pragma unroll 1
-  for (int c = 0; c < n; ++c) {
-    const int nx = c + S - 2;
-    if (nx < n) {
-      if (c >= 2) mbar_wait(&mbar[c & 1], ((c - 2) >> 1) & 1);  // chunk c-2 left stage nx % S
-      load(nx, ring + (nx % S) * stage_bytes);
-    }
-    cp_async_commit();
-    cp_async_wait<S - 2>();
-    mid(c);
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      fence_after_sync();
-      mma(c, ring + (c % S) * stage_bytes);
-      commit(&mbar[c & 1]);
-    }
-  }
-  mbar_wait(&mbar[(n - 1) & 1], ((n - 1) >> 1) & 1);
-  fence_after_sync();
-}
-
-__device__ __forceinline__ void ring_init(uint64_t* mbar) {
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    fence_init();
-  }
-}
-
 inline int njt_of_host(int step, int BS) { return (step * BS + 127) >> 7; }
 __device__ __forceinline__ int njt_of(const Args& a) { return (a.step * a.BS + 127) >> 7; }
 

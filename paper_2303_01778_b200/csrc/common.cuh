@@ -42,7 +42,8 @@ enum KernelId {
   K_FOLD1 = 0, K_FOLD_GROUP, K_LINCOMB, K_DELTA_AFFINE, K_STATE_GATHER, K_STATE_SCATTER,
   K_LR_TRAIN, K_LR_EVAL, K_CNN_SLOTS, K_CNN_FWD, K_CNN_FC1_FWD, K_CNN_HEAD, K_CNN_FC1_BWD,
   K_CNN_BWD_CONV, K_CNN_WGRAD, K_CNN_LZ_XT, K_CNN_LZ_GRAM_FWD, K_CNN_LZ_FWD,
-  K_CNN_LZ_GRAM_BWD, K_CNN_LZ_BWD, K_CNN_LZ_MAT, K_NUM_IDS
+  K_CNN_LZ_GRAM_BWD, K_CNN_LZ_BWD, K_CNN_LZ_MAT, K_RN_CONV_FWD, K_RN_CONV_DGRAD, K_RN_CONV_WGRAD,
+  K_RN_NORM, K_RN_HEAD, K_RN_SGD, K_NUM_IDS
 };
 // Call around one kernel launch on `stream`: counts the launch and, when
 // profiling is on, brackets it with pooled CUDA events.

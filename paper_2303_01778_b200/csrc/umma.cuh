@@ -149,5 +149,72 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 
+// ---- cp.async staging (16-byte units) ---------------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// zero-fills the 16 bytes when !valid (src is not read)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// fp32 K-major UMMA operand tile (kind::tf32): core matrix = 8 rows x 16 B
+// (4 elements); row groups `sbo` bytes apart, K groups 128 B apart.
+__device__ __forceinline__ uint32_t kmaj_f32(int r, int k4, int sbo) {
+  return uint32_t((r >> 3) * sbo + k4 * 128 + (r & 7) * 16);
+}
+
+// The MMA ring: chunk c is loaded into stage c % S, S-2 chunks ahead, and its
+// MMAs are committed to mbar[c & 1] (two barriers, so waiting for chunk c-2
+// can never alias a later phase).  load(c, stage) issues the cp.async of one
+// chunk (all threads); mid(c) runs on all threads after chunk c landed and
+// before the MMAs are issued; mma(c, stage) issues (thread 0 only).
+template <int S, class Load, class Mid, class Mma>
+__device__ __forceinline__ void mma_ring(int n, uint8_t* ring, int stage_bytes, uint64_t* mbar,
+                                         Load load, Mid mid, Mma mma) {
+  static_assert(S >= 3, "ring depth");
+#pragma unroll 1
+  for (int c = 0; c < S - 2; ++c) {
+    if (c < n) load(c, ring + c * stage_bytes);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int c = 0; c < n; ++c) {
+    const int nx = c + S - 2;
+    if (nx < n) {
+      if (c >= 2) mbar_wait(&mbar[c & 1], ((c - 2) >> 1) & 1);  // chunk c-2 left stage nx % S
+      load(nx, ring + (nx % S) * stage_bytes);
+    }
+    cp_async_commit();
+    cp_async_wait<S - 2>();
+    mid(c);
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_after_sync();
+      mma(c, ring + (c % S) * stage_bytes);
+      commit(&mbar[c & 1]);
+    }
+  }
+  mbar_wait(&mbar[(n - 1) & 1], ((n - 1) >> 1) & 1);
+  fence_after_sync();
+}
+
+__device__ __forceinline__ void ring_init(uint64_t* mbar) {
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_init();
+  }
+}
+
 }  // namespace umma
 }  // namespace pb

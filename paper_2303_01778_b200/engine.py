@@ -42,7 +42,7 @@ from .core import (STREAM_NOISE, ClientProfile, ConfigError, SimConfig, select_c
 from .estimate import (InsufficientDataError, TimingHistory, TimingRecord, WorkloadFit,
                        estimation_error, fit_device, record)
 from .metrics import CostLedger, ReplicaGauge
-from .models import ModelSpec, cnn_init, spec_for
+from .models import ModelSpec, init_params, spec_for
 from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
 from .statestore import StateStore
 from .trainer import (AggOp, AlgorithmPlugin, ClientData, GroupInputs, ModelParams, NamedParams,
@@ -297,8 +297,8 @@ class SimulationEngine:
     """Server loop with the reference's constructor and outputs
     (fedsim/engine.py:563-828), executing on the GPU.
 
-    Extra keyword arguments: ``model`` ("lr" default, or "cnn"),
-    ``client_data`` (a prebuilt device ClientData), ``init_seed`` (CNN init),
+    Extra keyword arguments: ``model`` ("lr" default, "cnn" or "resnet"),
+    ``client_data`` (a prebuilt device ClientData), ``init_seed`` (CNN/ResNet init),
     ``eval_batch`` (unused for LR)."""
 
     def __init__(self, cfg: SimConfig, plugin: AlgorithmPlugin, profiles: Sequence[ClientProfile],
@@ -339,7 +339,7 @@ class SimulationEngine:
             if self.spec.kind == "lr":
                 start = ModelParams.zeros(self.spec.n_classes, self.spec.n_features)
             else:
-                start = NamedParams.from_flat(self.spec, cnn_init(self.spec, init_seed))
+                start = NamedParams.from_flat(self.spec, init_params(self.spec, init_seed))
             self.global_bundle = plugin.init_global(start)
         if plugin.is_stateful:
             names = plugin.state_names(self.spec)

@@ -30,7 +30,7 @@ import torch
 
 from . import _kernels as K
 from .core import STREAM_MINIBATCH, ClientProfile
-from .models import ModelSpec, cnn_spec, lr_spec
+from .models import ModelSpec, cnn_spec, lr_spec, resnet_spec
 from .statestore import ClientState
 
 
@@ -326,7 +326,7 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     G = len(clients)
     P = spec.numel
     # CNN rows padded to 32 floats: 16-byte aligned vector / cp.async access
-    P_pad = (P + 31) // 32 * 32 if spec.kind == "cnn" else P
+    P_pad = (P + 31) // 32 * 32 if spec.kind in ("cnn", "resnet") else P
     w_out = torch.empty(G, P_pad, device=d)[:, :P]
     loss = torch.empty(G, dtype=torch.float64, device=d)
     steps = torch.empty(G, dtype=torch.int32, device=d)
@@ -349,6 +349,10 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
         cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
                         spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
                         state_work=state_work)
+    elif spec.kind == "resnet":
+        from .resnet import resnet_train_group
+        resnet_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
+                           spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms)
     else:
         raise ValueError(f"unknown model kind {spec.kind!r}")
     t1.record()
@@ -615,6 +619,8 @@ def spec_of_bundle(bundle: ParamBundle, plugin: AlgorithmPlugin | None = None) -
         return lr_spec(w.shape[0], w.shape[1])
     if "fc2_w" in bundle.entries:
         return cnn_spec(bundle.tensor("fc2_w").shape[0])
+    if "fc_w" in bundle.entries and "l4.1.conv2_w" in bundle.entries:
+        return resnet_spec(bundle.tensor("fc_w").shape[0])
     raise ValueError("cannot infer the model layout from the bundle")
 
 
@@ -689,4 +695,8 @@ def evaluate(model, ds) -> tuple[float, float]:
         from .cnn import cnn_evaluate
         X, Y = _eval_tensors(ds)
         return cnn_evaluate(model, X, Y)
+    if isinstance(model, NamedParams) and model.spec.kind == "resnet":
+        from .resnet import resnet_evaluate
+        X, Y = _eval_tensors(ds)
+        return resnet_evaluate(model, X, Y)
     raise TypeError(f"cannot evaluate {type(model).__name__}")

@@ -130,3 +130,28 @@ def test_oracle_plugin_rounds_match_reference_engine(name, hyper, golden_engine)
     for r, glob in enumerate(per_round):
         for entry, (tensor, _) in glob.items():
             assert rel_gap(tensor, golden_engine[f"small_{name}/r{r}/{entry}"]) <= 1e-10, (r, entry)
+
+
+def test_resnet_spec_matches_oracle_layout():
+    """ResNet-18-GN (config 4): P = 11,173,962 at 10 classes; the product's
+    flat layout equals the oracle's; the library's workspace planner agrees
+    with the model size (host-only call)."""
+    from oracle import resnet_oracle as R
+    from paper_2303_01778_b200.models import resnet_init, resnet_spec
+    spec = resnet_spec(10)
+    assert spec.numel == 11_173_962
+    assert [(n, tuple(sh)) for n, _, _, sh in spec.columns()] == [(n, tuple(sh)) for n, sh in R.layout(10)]
+    w = resnet_init(spec, 0)
+    for n, o, s, _ in spec.columns():
+        if "gn" in n:
+            assert np.all(w[o:o + s] == (1.0 if n.endswith("_w") else 0.0))
+    p = R.unflatten(w, 10)
+    assert np.array_equal(R.flatten(p, 10), w.astype(np.float64))
+
+
+def test_resnet_workspace_plan_host_only():
+    from paper_2303_01778_b200.resnet import workspace_sizes
+    arena, p16, part, gnp = workspace_sizes(20, 10)
+    # bf16 copies: every conv weight with the stem's 3 input channels padded to 8
+    assert p16 >= 11_173_962 - 5130 - 2 * 4800  # conv weights only (no fc, no GN affine)
+    assert arena > 0 and part > 0 and gnp > 0
