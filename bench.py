@@ -270,6 +270,7 @@ def run_b200(args) -> dict:
 
     # ---- aggregation microbench (config 5), bounded ----
     agg = aggregation_microbench(world, dev) if args.agg else None
+    state = state_microbench(dev) if args.agg and world == 1 else None
     # ---- config 4 (ResNet-18-GN) rounds, 1 GPU, secondary ----
     c4 = resnet_round_bench(dev) if args.c4 and world == 1 else None
 
@@ -313,6 +314,8 @@ def run_b200(args) -> dict:
     }
     if agg is not None:
         out["aggregation"] = agg
+    if state is not None:
+        out["state_store"] = state
     if c4 is not None:
         out["c4_resnet"] = c4
     if rank == 0 and args.cpu_baseline and world == 1:
@@ -408,6 +411,44 @@ def aggregation_microbench(world: int, dev) -> dict:
     del xs
     torch.cuda.empty_cache()
     return out
+
+
+def state_microbench(dev, P: int = 11_173_962, slots: int = 1000, clients: int = 100) -> dict:
+    """Config 3's client-state manager at ResNet size: gather `clients` rows
+    of a [slots, P] fp32 HBM store into the working buffer and scatter them
+    back (pb_state_gather / pb_state_scatter, SCAFFOLD control variates).
+    Algorithmic bytes: 16 per parameter per client (read + write, both ways)."""
+    import torch
+    from paper_2303_01778_b200 import _kernels as K
+    pad = (P + 3) // 4 * 4  # rows 16-byte aligned, as the StateStore lays them out
+    store = torch.empty(slots, pad, device=dev)[:, :P]
+    work = torch.empty(clients, pad, device=dev)[:, :P]
+    gen = torch.Generator(device=dev).manual_seed(9)
+    store.normal_(generator=gen)
+    rows = np.random.default_rng(3).choice(slots, clients, replace=False).astype(np.int32)
+    slot = torch.from_numpy(rows).to(dev)
+    for _ in range(2):
+        K.state_gather(work, store, slot)
+        K.state_scatter(store, work, slot)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.state_gather(work, store, slot)
+        K.state_scatter(store, work, slot)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    ok = bool(torch.equal(store[torch.from_numpy(rows).long().to(dev)], work))
+    peaks, src = load_peaks()
+    gbs = 16.0 * clients * P / (best / 1e3) / 1e9
+    del store, work
+    torch.cuda.empty_cache()
+    return {"params": P, "store_slots": slots, "clients": clients, "gather_scatter_ms": best,
+            "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
+            "algorithmic_bytes": "16 B per parameter per client (gather read+write, scatter read+write)",
+            "round_trip_exact": ok}
 
 
 # ---------------------------------------------------------------------------

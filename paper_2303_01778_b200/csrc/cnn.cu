@@ -711,7 +711,16 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // (per-sample partials, summed in sample order by k_wgrad: deterministic).
 // grid (active, ceil(BS/spb)), 256 threads
 // ---------------------------------------------------------------------------
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes;
+// per-sample inputs of k_bwd_conv, staged by one cp.async burst per sample
+constexpr int kInDp2 = 0, kInP2 = kInDp2 + kFlat * 4, kInAm2 = kInP2 + kFlat * 4,
+              kInAm1 = kInAm2 + kFlat, kInImg = kInAm1 + kP1, kInP1 = kInImg + kImg * kImg * 4,
+              kInBytes = kInP1 + kP1Bytes;   // 59,136 B
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kInBytes;
+
+__device__ __forceinline__ void stage_bytes(uint8_t* dst, const void* src, int bytes, int tid) {
+  const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
+  for (int e = tid * 16; e < bytes; e += 256 * 16) cp_async16(dst + e, s8 + e);
+}
 
 __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   const Slot sl = a.slots[blockIdx.x];
@@ -723,12 +732,29 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   __shared__ float sB2[4][64];
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
-  // after the dgrad MMAs the dz2 region is reused:
+  uint8_t* sIn = sDz + kDzBytes;
+  const float* iDp2 = reinterpret_cast<const float*>(sIn + kInDp2);
+  const float* iP2 = reinterpret_cast<const float*>(sIn + kInP2);
+  const uint8_t* iAm2 = sIn + kInAm2;
+  const uint8_t* iAm1 = sIn + kInAm1;
+  const float* iImg = reinterpret_cast<const float*>(sIn + kInImg);
+  const uint8_t* iP1 = sIn + kInP1;
+  // after the dgrad MMAs the dz region is reused:
   float* sDp1 = reinterpret_cast<float*>(sDz);           // [196][32] dp1 (25,088 B)
   float* sX = sDp1 + 196 * 32;                           // [32][32] padded image
-  uint8_t* sAm = reinterpret_cast<uint8_t*>(sX + 1024);  // [196][32] conv1 argmax
   float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp partials (after sync)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto stage_inputs = [&](int i) {
+    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    stage_bytes(sIn + kInDp2, a.dp2 + sid * kFlat, kFlat * 4, tid);
+    stage_bytes(sIn + kInP2, p2_row(a, sl, blockIdx.x, i), kFlat * 4, tid);
+    stage_bytes(sIn + kInAm2, a.am2 + sid * kFlat, kFlat, tid);
+    stage_bytes(sIn + kInAm1, a.am1 + sid * kP1, kP1, tid);
+    stage_bytes(sIn + kInImg, a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg), kImg * kImg * 4, tid);
+    stage_bytes(sIn + kInP1, a.p1g + sid * kP1Bytes, kP1Bytes, tid);
+    cp_async_commit();
+  };
+  stage_inputs(i0);
   stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, 256);
   if (warp == 0) tmem_alloc<64>(&tmem_base);
   if (tid == 0) {
@@ -745,16 +771,14 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     const int64_t sid = sidx(blockIdx.x, i, a.BS);
     for (int e = tid; e < kDzBytes / 16; e += 256)
       reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
+    cp_async_wait<0>();
     __syncthreads();
-    const float* dp2 = a.dp2 + sid * kFlat;
-    const float* p2 = p2_row(a, sl, blockIdx.x, i);
-    const uint8_t* am2 = a.am2 + sid * kFlat;
     float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
     for (int o = tid; o < kFlat; o += 256) {
       const int pp = o >> 6, co = o & 63;
       const int py = pp / 7, px = pp - py * 7;
-      const int d = am2[o];
-      const float g = p2[o] > 0.0f ? dp2[o] : 0.0f;
+      const int d = iAm2[o];
+      const float g = iP2[o] > 0.0f ? iDp2[o] : 0.0f;
       b2part += g;
       const int row = (2 * py + (d >> 1) + 2) * kG + 2 * px + (d & 1) + 2;
       *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) =
@@ -802,21 +826,16 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
         }
       }
     } else {
-      const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
       for (int e = tid - 128; e < 1024; e += 128) {
         const int yy = e >> 5, xx = e & 31;
-        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? iImg[(yy - 2) * kImg + (xx - 2)] : 0.0f;
       }
-      const uint8_t* am1 = a.am1 + sid * kP1;
-      for (int e = tid - 128; e < kP1 / 16; e += 128)
-        reinterpret_cast<uint4*>(sAm)[e] = reinterpret_cast<const uint4*>(am1)[e];
     }
     fence_before_sync();
     __syncthreads();
     // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
     // warp w takes pooled positions w, w+8, ...; 26 accumulators per thread
     {
-      const uint8_t* p1 = a.p1g + sid * kP1Bytes;
       float acc[25];
 #pragma unroll
       for (int t = 0; t < 25; ++t) acc[t] = 0.0f;
@@ -825,17 +844,18 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
       for (int pp = warp; pp < 196; pp += 8) {
         const int py = pp / 14, px = pp - py * 14;
         const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-            p1 + (co >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (co & 7) * 2));
+            iP1 + (co >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (co & 7) * 2));
         const float g = pv > 0.0f ? sDp1[pp * kC1 + co] : 0.0f;
         bacc += g;
-        const int d = sAm[pp * kC1 + co];
+        const int d = iAm1[pp * kC1 + co];
         const float* xw = sX + (2 * py + (d >> 1)) * 32 + 2 * px + (d & 1);
 #pragma unroll
         for (int ky = 0; ky < 5; ++ky)
 #pragma unroll
           for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * 32 + kx], acc[ky * 5 + kx]);
       }
-      __syncthreads();  // all reads of sDp1/sX/sAm done; reuse as reduction scratch
+      __syncthreads();  // all reads of sDp1/sX and the staged inputs done
+      if (i + 1 < i1) stage_inputs(i + 1);  // next sample's inputs stream in meanwhile
 #pragma unroll
       for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] = acc[t];
       sRed[warp * 832 + 800 + co] = bacc;

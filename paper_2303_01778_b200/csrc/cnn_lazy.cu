@@ -87,8 +87,9 @@ constexpr int kGrA = 128 * kGrKC * 4;          // 32 KB
 constexpr int kGrB = 32 * kGrKC * 4;           // 8 KB
 constexpr int kGrStage = kGrA + kGrB;          // 40 KB
 constexpr int kGxT = 32 * 128 * 4;             // Gx^T [32 i][128 j], 16 KB
-constexpr size_t kGramFwdSmem = kStages * kGrStage + kGxT;
-constexpr size_t kGramBwdSmem = kStages * kGrStage;
+constexpr int kGrStages = 5;                   // 3 chunks in flight
+constexpr size_t kGramFwdSmem = kGrStages * kGrStage + kGxT;   // 216 KB
+constexpr size_t kGramBwdSmem = kGrStages * kGrStage;
 
 template <bool FWD>
 __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
   const float* Brow = hist + (sl.hist + int64_t(t) * a.BS) * KD;               // current rows
   const int L = a.hlen[sl.r];
   const float* hdt = a.hdt + sl.hist * kH1 + j0;                               // [o][L], from column j0
-  uint8_t* sGxT = smem + kStages * kGrStage;
+  uint8_t* sGxT = smem + kGrStages * kGrStage;
   if (warp == 0) tmem_alloc<FWD ? 256 : 32>(&tmem_base);
   ring_init(mbar);
   fence_before_sync();
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
       for (int e = tid; e < 128 * 8; e += 128) {
         const int r = e >> 3, k4 = e & 7;
         const int col = jc * 32 + k4 * 4;
-        const bool v = j0 + col < L;
+        const bool v = j0 + col < jlim;  // columns >= t*BS hold no history yet
         cp_async16_zfill(st + kmaj_f32(r, k4, 1024), hdt + int64_t(q * 128 + r) * L + (v ? col : 0), v);
       }
     }
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
         mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, jc > 0 || kk > 0);
     }
   };
-  mma_ring<kStages>(FWD ? nA + 16 : nA, smem, kGrStage, mbar, load, mid, mma);
+  mma_ring<kGrStages>(FWD ? nA + 16 : nA, smem, kGrStage, mbar, load, mid, mma);
 
   const float nlr = -a.lr;
   if (FWD) {
@@ -449,10 +450,12 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active, int spc) 
 
 // ---------------------------------------------------------------------------
 // k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hxt[k][j]
-// (M = 128 o, N = 256 k, K = steps_r * BS); grid (g, 4, 13), 256 threads
+// (M = 128 o, N = 256 k, K = steps_r * BS); grid (13, 4, g), 256 threads --
+// the client is the slowest grid dimension, so its 52 tiles run together
+// and re-read its history from L2
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 1) k_lz_mat(Args a) {
-  const int r = blockIdx.x, q = blockIdx.y, k0 = blockIdx.z * 256;
+  const int r = blockIdx.z, q = blockIdx.y, k0 = blockIdx.x * 256;
   const int K = a.steps[r] * a.BS;
   if (K == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -593,7 +596,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
 int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s) {
   if (g <= 0) return PB_OK;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
-  k_lz_mat<<<dim3(g, kH1 / 128, (kFlat + 255) / 256), 256, kShSmem, s>>>(a);
+  k_lz_mat<<<dim3((kFlat + 255) / 256, kH1 / 128, g), 256, kShSmem, s>>>(a);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);
   return pb::check_launch("lazy fc1 materialise");
 }

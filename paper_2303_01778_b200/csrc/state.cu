@@ -10,26 +10,40 @@
 //
 // Algorithmic traffic: gather reads store + writes work, scatter reads work +
 // writes store = 16 B per state element per client.
+#include <cstring>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int kThreads = 256;
 
-template <bool kGather>
+template <bool kGather, class V>
 __global__ void __launch_bounds__(kThreads)
-move_rows_vec(float4* __restrict__ dst, int64_t dst_stride4, const float4* __restrict__ src,
-              int64_t src_stride4, const int32_t* __restrict__ slot, int64_t width4) {
+move_rows_vec(V* __restrict__ dst, int64_t dst_stride, const V* __restrict__ src, int64_t src_stride,
+              const int32_t* __restrict__ slot, int64_t width) {
   const int64_t j = blockIdx.y;
   const int32_t s = slot[j];
   if (!kGather && s < 0) return;
-  float4* d = kGather ? dst + j * dst_stride4 : dst + int64_t(s) * dst_stride4;
-  const float4* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride4 : nullptr)
-                               : src + j * src_stride4;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < width4;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const float4 v = srow ? __ldcs(srow + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    __stcs(d + i, v);
+  V* d = kGather ? dst + j * dst_stride : dst + int64_t(s) * dst_stride;
+  const V* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride : nullptr) : src + j * src_stride;
+  // each CTA streams one contiguous 64 KB chunk of the row, kU independent
+  // vector loads in flight per thread before any store
+  constexpr int kU = 64 / sizeof(V);
+  constexpr int64_t kChunk = 65536 / sizeof(V);
+  const int64_t c0 = int64_t(blockIdx.x) * kChunk, c1 = min(c0 + kChunk, width);
+  V zero;
+  memset(&zero, 0, sizeof(V));
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += kU * kThreads) {
+    V v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = i + u * kThreads;
+      v[u] = (srow && k < c1) ? srow[k] : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i + u * kThreads < c1) d[i + u * kThreads] = v[u];
   }
 }
 
@@ -56,25 +70,31 @@ int move_rows(float* dst, int64_t dst_stride, const float* src, int64_t src_stri
   if (g == 0 || width == 0) return PB_OK;
   cudaStream_t s = pb::as_stream(stream);
   // spread each row over enough CTAs that g*gx fills the machine
-  int64_t per_row = (int64_t(pb::sm_count()) * 8 + g - 1) / g;
-  if (width % 4 == 0 && dst_stride % 4 == 0 && src_stride % 4 == 0 && pb::aligned16(dst) &&
-      pb::aligned16(src)) {
-    const int64_t w4 = width / 4;
-    int64_t gx = std::min<int64_t>(per_row, (w4 + kThreads - 1) / kThreads);
-    dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
-    pb::prof_begin(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
-    move_rows_vec<kGather><<<grid, kThreads, 0, s>>>(
+  int64_t per_row = (int64_t(pb::sm_count()) * 16 + g - 1) / g;
+  // vector width: every row start must be aligned (a single row needs only
+  // its base); 16 B when possible, else 8 B (odd-sized state rows of even length)
+  auto fits = [&](int e) {
+    return width % e == 0 && (g == 1 || (dst_stride % e == 0 && src_stride % e == 0)) &&
+           (reinterpret_cast<uintptr_t>(dst) % (4 * e)) == 0 && (reinterpret_cast<uintptr_t>(src) % (4 * e)) == 0;
+  };
+  pb::prof_begin(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
+  if (fits(4)) {
+    dim3 grid(unsigned((width / 4 + 4095) / 4096), unsigned(g));
+    move_rows_vec<kGather, float4><<<grid, kThreads, 0, s>>>(
         reinterpret_cast<float4*>(dst), dst_stride / 4, reinterpret_cast<const float4*>(src),
-        src_stride / 4, slot, w4);
-    pb::prof_end(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
+        src_stride / 4, slot, width / 4);
+  } else if (fits(2)) {
+    dim3 grid(unsigned((width / 2 + 8191) / 8192), unsigned(g));
+    move_rows_vec<kGather, float2><<<grid, kThreads, 0, s>>>(
+        reinterpret_cast<float2*>(dst), dst_stride / 2, reinterpret_cast<const float2*>(src),
+        src_stride / 2, slot, width / 2);
   } else {
     int64_t gx = std::min<int64_t>(per_row, (width + kThreads - 1) / kThreads);
     dim3 grid(unsigned(gx < 1 ? 1 : gx), unsigned(g));
-    pb::prof_begin(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
     move_rows_scalar<kGather><<<grid, kThreads, 0, s>>>(dst, dst_stride, src, src_stride, slot,
                                                          width);
-    pb::prof_end(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
   }
+  pb::prof_end(kGather ? pb::K_STATE_GATHER : pb::K_STATE_SCATTER, s);
   return pb::check_launch(name);
 }
 

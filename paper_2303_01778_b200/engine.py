@@ -208,7 +208,7 @@ class DeviceRuntime:
         if plugin.is_stateful:
             if self.store is None:
                 raise ConfigError(f"{plugin.name} is stateful and needs a state store")
-            work = torch.empty(len(clients), spec.numel, device=w0.device)
+            work = torch.empty(len(clients), (spec.numel + 3) // 4 * 4, device=w0.device)[:, :spec.numel]
             self.store.gather(clients, work)
         self.gauge.acquire(len(clients))
         try:

@@ -191,7 +191,10 @@ class StateStore:
         if need <= cap:
             return
         new_cap = max(need, 2 * cap, 64)
-        rows = torch.zeros(new_cap, self._width, device=self._dev())
+        # row stride padded to 16 bytes: the gather/scatter kernels move rows
+        # with 16-byte vectors
+        pad = (self._width + 3) // 4 * 4
+        rows = torch.zeros(new_cap, pad, device=self._dev())[:, :self._width]
         if self._rows is not None:
             rows[:cap].copy_(self._rows)
         self._rows = rows
