@@ -56,33 +56,47 @@ __global__ void k_slots(Args a, int active) {
 // ---------------------------------------------------------------------------
 constexpr int kFwdThreads = 256;
 constexpr int kZStride = 65;  // padded fp32 row of the conv2 output tile
-constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + (1024 + 832 + 64) * 4;
+constexpr int kRawImg = kImg * kImg * 4;   // 3136 B
+constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg +
+                            (1024 + 832 + 64) * 4;   // 225,920 B
 
+// Software-pipelined over the CTA's samples: iteration i runs conv1 of
+// sample i (SIMT) into p1 buffer i&1, issues its conv2 MMAs into TMEM half
+// i&1, and then -- while those run -- finishes sample i-1 (TMEM -> bias/relu
+// -> maxpool -> p2).  The raw image of sample i+1 streams in by cp.async.
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
   const Slot sl = a.slots[blockIdx.x];
   const int i0 = blockIdx.y * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
-  uint8_t* sPl = sW2 + kW2Bytes;
-  float* sZ = reinterpret_cast<float*>(sPl + kP1Bytes);
-  float* sX = sZ + 256 * kZStride;
+  uint8_t* sPl0 = sW2 + kW2Bytes;                       // 2 p1 buffers
+  float* sZ = reinterpret_cast<float*>(sPl0 + 2 * kP1Bytes);
+  uint8_t* sRaw = reinterpret_cast<uint8_t*>(sZ + 256 * kZStride);   // 2 raw images
+  float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);
   float* sW1 = sX + 1024;
   float* sB2 = sW1 + 832;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float* W = a.w + int64_t(sl.r) * a.P;
-
+  auto fetch_img = [&](int i) {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg));
+    uint8_t* dst = sRaw + (i & 1) * kRawImg;
+    for (int e = tid * 16; e < kRawImg; e += kFwdThreads * 16) cp_async16(dst + e, src + e);
+    cp_async_commit();
+  };
+  fetch_img(i0);
   stage_w2(sW2, W, tid, kFwdThreads);
   for (int e = tid; e < 832; e += kFwdThreads) sW1[e] = W[oC1W + e];
   for (int e = tid; e < 64; e += kFwdThreads) sB2[e] = W[oC2B + e];
-  for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads)
-    reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < 2 * kP1Bytes / 16; e += kFwdThreads)
+    reinterpret_cast<uint4*>(sPl0)[e] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
-  if (warp == 0) tmem_alloc<128>(&tmem_base);
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
   if (tid == 0) {
-    mbar_init(&mbar, 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     fence_init();
   }
   fence_before_sync();
@@ -90,7 +104,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = idesc_bf16(128, 64);
-  uint32_t phase = 0;
 
   // conv1 weights of this thread's output channel live in registers
   const int c1 = lane;
@@ -99,14 +112,68 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
   for (int t = 0; t < 25; ++t) wr[t] = sW1[c1 * 25 + t];
   const float b1 = sW1[800 + c1];
 
+  // finish sample j: TMEM half (j&1) -> relu(z + b2) -> maxpool -> p2, am2
+  auto epilogue = [&](int j) {
+    mbar_wait(&mbar[j & 1], ((j - i0) >> 1) & 1);
+    fence_after_sync();
+    const uint32_t th = tmem + uint32_t((j & 1) * 128);
+    {
+      const int q = warp & 3, half = warp >> 2;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int row = t * 128 + q * 32 + lane;
+        float v[16];
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          tmem_ld16(th + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + half * 32 + c16 * 16), v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int co = half * 32 + c16 * 16 + k;
+            sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
+          }
+        }
+      }
+    }
+    fence_before_sync();
+    __syncthreads();
+    const int64_t sid = sidx(blockIdx.x, j, a.BS);
+    float* p2 = p2_row(a, sl, blockIdx.x, j);
+    uint8_t* am2 = a.am2 + sid * kFlat;
+    for (int o = tid; o < kFlat; o += kFwdThreads) {
+      const int pp = o >> 6, co = o & 63;
+      const int py = pp / 7, px = pp - py * 7;
+      const int r0 = (2 * py) * kG + 2 * px;
+      const int rows[4] = {r0, r0 + 1, r0 + kG, r0 + kG + 1};
+      float best = -INFINITY;
+      int arg = 0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const float z = sZ[rows[d] * kZStride + co];
+        if (takes_max(z, best) && best == best) {
+          best = z;
+          arg = d;
+        }
+      }
+      p2[o] = a.hx ? tf32_rna(best) : best;
+      am2[o] = uint8_t(arg);
+    }
+    __syncthreads();  // sZ is free again
+  };
+
   for (int i = i0; i < i1; ++i) {
     const int64_t sid = sidx(blockIdx.x, i, a.BS);
-    const float* x = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
-    for (int e = tid; e < 1024; e += kFwdThreads) {
-      const int yy = e >> 5, xx = e & 31;
-      sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+    uint8_t* sPl = sPl0 + (i & 1) * kP1Bytes;
+    cp_async_wait<0>();
+    __syncthreads();
+    {
+      const float* x = reinterpret_cast<const float*>(sRaw + (i & 1) * kRawImg);
+      for (int e = tid; e < 1024; e += kFwdThreads) {
+        const int yy = e >> 5, xx = e & 31;
+        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+      }
     }
     __syncthreads();
+    if (i + 1 < i1) fetch_img(i + 1);
     // conv1 + relu + maxpool2 (warp = pooled position, lane = channel)
     uint8_t* am1 = a.am1 + sid * kP1;
     for (int pp = warp; pp < 196; pp += kFwdThreads / 32) {
@@ -132,27 +199,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
         }
       }
       const float v = relu_nan(best);
-      *reinterpret_cast<__nv_bfloat16*>(sPl + (c1 >> 3) * kPlane +
-                                        ((py + 2) * kG + px + 2) * 16 + (c1 & 7) * 2) =
-          __float2bfloat16(v);
+      *reinterpret_cast<__nv_bfloat16*>(sPl + (c1 >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 +
+                                        (c1 & 7) * 2) = __float2bfloat16(v);
       am1[pp * kC1 + c1] = uint8_t(arg);
     }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      // precomputed descriptors; per MMA only the 14-bit address field moves
       const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
       const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
+      const uint32_t th = tmem + uint32_t((i & 1) * 128);
 #pragma unroll
       for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int tap = 0; tap < 25; ++tap)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh)
-            mma_bf16(tmem + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
+            mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
                      b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc, tap > 0 || hh > 0);
-      commit(&mbar);
+      commit(&mbar[i & 1]);
     }
     // p1 image to global for the backward kernels (overlaps the MMAs)
     {
@@ -160,53 +226,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
       const uint4* src = reinterpret_cast<const uint4*>(sPl);
       for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) dst[e] = src[e];
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    fence_after_sync();
-    {
-      const int q = warp & 3, half = warp >> 2;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int row = t * 128 + q * 32 + lane;
-        float v[16];
-#pragma unroll
-        for (int c16 = 0; c16 < 2; ++c16) {
-          tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + half * 32 + c16 * 16), v);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int co = half * 32 + c16 * 16 + k;
-            sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
-          }
-        }
-      }
-    }
-    fence_before_sync();
-    __syncthreads();
-    float* p2 = p2_row(a, sl, blockIdx.x, i);
-    uint8_t* am2 = a.am2 + sid * kFlat;
-    for (int o = tid; o < kFlat; o += kFwdThreads) {
-      const int pp = o >> 6, co = o & 63;
-      const int py = pp / 7, px = pp - py * 7;
-      const int r0 = (2 * py) * kG + 2 * px;
-      const int rows[4] = {r0, r0 + 1, r0 + kG, r0 + kG + 1};
-      float best = -INFINITY;
-      int arg = 0;
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const float z = sZ[rows[d] * kZStride + co];
-        if (takes_max(z, best) && best == best) {
-          best = z;
-          arg = d;
-        }
-      }
-      p2[o] = a.hx ? tf32_rna(best) : best;
-      am2[o] = uint8_t(arg);
-    }
-    __syncthreads();
+    if (i > i0) epilogue(i - 1);
   }
+  epilogue(i1 - 1);
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<128>(tmem);
+  if (warp == 0) tmem_free<256>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -334,6 +359,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   float* W = a.w + int64_t(sl.r) * a.P;
   const float* W2 = W + oF2W;          // [C][512], read from L2 (coalesced rows)
   const float* hrow = a.h + sidx(blockIdx.x, 0, a.BS) * kH1;
+#pragma unroll 8
   for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
   __syncthreads();
   const float* b2 = W2 + int64_t(C) * kH1;
@@ -910,6 +936,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   if (blockIdx.y == kWgSplit) {
     for (int k = tid; k < kPg; k += 256) {
       float g = 0.0f;
+#pragma unroll 8
       for (int i = 0; i < cnt; ++i) g += a.pg[(s0 + i) * kPg + k];
       const int64_t idx = k < 800 ? oC1W + k : (k < 832 ? oC1B + (k - 800) : oC2B + (k - 832));
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
@@ -980,10 +1007,26 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   }
   fence_before_sync();
   __syncthreads();
-  for (int e = tid; e < 64 * width; e += 256) {
-    const int co = e / width, c = e - co * width;
-    const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
-    W[idx] = sgd(a, sl.r, idx, W[idx], sG[co * (13 * 32 + 1) + c]);
+  // SGD on W2[co][tap0*32 ...]: 8 independent loads in flight per thread
+  for (int e0 = tid; e0 < 64 * width; e0 += 8 * 256) {
+    float wv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = e0 + k * 256;
+      if (e < 64 * width) {
+        const int co = e / width, c = e - co * width;
+        wv[k] = W[oC2W + int64_t(co) * 800 + tap0 * 32 + c];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = e0 + k * 256;
+      if (e < 64 * width) {
+        const int co = e / width, c = e - co * width;
+        const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
+        W[idx] = sgd(a, sl.r, idx, wv[k], sG[co * (13 * 32 + 1) + c]);
+      }
+    }
   }
   fence_before_sync();
   __syncthreads();

@@ -118,11 +118,34 @@ __device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
   return uint32_t((tap * 4 + (ci >> 3)) * 1024 + (co >> 3) * 128 + (co & 7) * 16 + (ci & 7) * 2);
 }
 
+// conv2 weights (fp32 [co][tap][ci] in the client row) -> bf16 UMMA layout.
+// 8 consecutive ci per unit (one 16-byte smem store), 5 units per thread in
+// flight: 10 independent float4 loads before the first conversion.
 __device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthreads) {
-  const float* w2 = W + oC2W;
-  for (int e = tid; e < 64 * 800; e += nthreads) {
-    const int co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
-    *reinterpret_cast<__nv_bfloat16*>(sW2 + w2_off(co, tap, ci)) = __float2bfloat16(w2[e]);
+  const float4* w2 = reinterpret_cast<const float4*>(W + oC2W);
+  constexpr int kUnits = 64 * 800 / 8, kU = 5;
+  for (int u0 = tid; u0 < kUnits; u0 += kU * nthreads) {
+    float4 v[kU][2];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int u = u0 + k * nthreads;
+      if (u < kUnits) {
+        v[k][0] = w2[2 * u];
+        v[k][1] = w2[2 * u + 1];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int u = u0 + k * nthreads;
+      if (u >= kUnits) break;
+      const int e = u * 8, co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
+      uint4 o;
+      o.x = pack_bf16(v[k][0].x, v[k][0].y);
+      o.y = pack_bf16(v[k][0].z, v[k][0].w);
+      o.z = pack_bf16(v[k][1].x, v[k][1].y);
+      o.w = pack_bf16(v[k][1].z, v[k][1].w);
+      *reinterpret_cast<uint4*>(sW2 + w2_off(co, tap, ci)) = o;
+    }
   }
 }
 
