@@ -52,7 +52,7 @@ __global__ void k_slots(Args a, int active) {
 
 // ---------------------------------------------------------------------------
 // k_fwd: conv1 (SIMT) -> p1 planes -> conv2 (tcgen05) -> relu/pool epilogue
-// grid (active, ceil(BS/spb)), 256 threads
+// grid (ceil(BS/spb), active), 256 threads
 // ---------------------------------------------------------------------------
 constexpr int kFwdThreads = 256;
 constexpr int kZStride = 65;  // padded fp32 row of the conv2 output tile
@@ -65,8 +65,8 @@ constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * k
 // i&1, and then -- while those run -- finishes sample i-1 (TMEM -> bias/relu
 // -> maxpool -> p2).  The raw image of sample i+1 streams in by cp.async.
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
-  const Slot sl = a.slots[blockIdx.x];
-  const int i0 = blockIdx.y * spb, i1 = min(sl.cnt, i0 + spb);
+  const Slot sl = a.slots[blockIdx.y];
+  const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar[2];
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
     }
     fence_before_sync();
     __syncthreads();
-    const int64_t sid = sidx(blockIdx.x, j, a.BS);
-    float* p2 = p2_row(a, sl, blockIdx.x, j);
+    const int64_t sid = sidx(blockIdx.y, j, a.BS);
+    float* p2 = p2_row(a, sl, blockIdx.y, j);
     uint8_t* am2 = a.am2 + sid * kFlat;
     for (int o = tid; o < kFlat; o += kFwdThreads) {
       const int pp = o >> 6, co = o & 63;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
   };
 
   for (int i = i0; i < i1; ++i) {
-    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    const int64_t sid = sidx(blockIdx.y, i, a.BS);
     uint8_t* sPl = sPl0 + (i & 1) * kP1Bytes;
     cp_async_wait<0>();
     __syncthreads();
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // tcgen05 -> dp1 (TMEM -> smem) -> pool1/relu backward fused with the conv1
 // weight gradient and the conv1/conv2 bias gradients of this sample
 // (per-sample partials, summed in sample order by k_wgrad: deterministic).
-// grid (active, ceil(BS/spb)), 256 threads
+// grid (ceil(BS/spb), active), 256 threads
 // ---------------------------------------------------------------------------
 // per-sample inputs of k_bwd_conv, staged by one cp.async burst per sample
 constexpr int kInDp2 = 0, kInP2 = kInDp2 + kFlat * 4, kInAm2 = kInP2 + kFlat * 4,
@@ -749,8 +749,8 @@ __device__ __forceinline__ void stage_bytes(uint8_t* dst, const void* src, int b
 }
 
 __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
-  const Slot sl = a.slots[blockIdx.x];
-  const int i0 = blockIdx.y * spb, i1 = min(sl.cnt, i0 + spb);
+  const Slot sl = a.slots[blockIdx.y];
+  const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -771,9 +771,9 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp partials (after sync)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto stage_inputs = [&](int i) {
-    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    const int64_t sid = sidx(blockIdx.y, i, a.BS);
     stage_bytes(sIn + kInDp2, a.dp2 + sid * kFlat, kFlat * 4, tid);
-    stage_bytes(sIn + kInP2, p2_row(a, sl, blockIdx.x, i), kFlat * 4, tid);
+    stage_bytes(sIn + kInP2, p2_row(a, sl, blockIdx.y, i), kFlat * 4, tid);
     stage_bytes(sIn + kInAm2, a.am2 + sid * kFlat, kFlat, tid);
     stage_bytes(sIn + kInAm1, a.am1 + sid * kP1, kP1, tid);
     stage_bytes(sIn + kInImg, a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg), kImg * kImg * 4, tid);
@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   const uint32_t idesc = idesc_bf16(128, 32, false, true);
   uint32_t phase = 0;
   for (int i = i0; i < i1; ++i) {
-    const int64_t sid = sidx(blockIdx.x, i, a.BS);
+    const int64_t sid = sidx(blockIdx.y, i, a.BS);
     for (int e = tid; e < kDzBytes / 16; e += 256)
       reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
     cp_async_wait<0>();
@@ -905,26 +905,38 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
 // ---------------------------------------------------------------------------
 // k_wgrad: y<2: conv2 wgrad for taps [13y, 13y+13) on tcgen05 + update;
 //          y==2: conv1 wgrad + conv1/conv2 bias grads (SIMT) + update
-// grid (active, 3), 256 threads
+// grid (3, active), 256 threads
 // ---------------------------------------------------------------------------
-constexpr int kWgBuf = kP1Bytes + kDzBytes;   // one staged sample (p1 + dz2 planes)
-constexpr size_t kWgSmem = 2 * kWgBuf;         // double-buffered
-constexpr int kWgSplit = 2;                    // conv2 taps split over 2 CTAs: 13 + 12
+// One staged sample: the p1 planes, the same planes shifted by one grid row
+// (so that horizontally adjacent taps (ky, kx), (ky, kx+1) form ONE N=64 MMA:
+// N-groups 0-3 read tap kx, N-groups 4-7 tap kx+1 at a uniform plane stride)
+// and the dz2 planes.
+constexpr int kWgP1 = 2 * kP1Bytes;             // 8 planes: shift 0, shift 1
+constexpr int kWgBuf = kWgP1 + kDzBytes;        // 86,016 B
+constexpr size_t kWgSmem = 2 * kWgBuf;          // double-buffered
+constexpr int kWgSplit = 2;                     // CTA 0: ky 0-2 (15 taps), CTA 1: ky 3-4 (10 taps)
+constexpr int kWgStride = 15 * 32 + 1;          // fp32 row of the gradient tile (epilogue)
 
 __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* buf, int tid) {
   const uint8_t* s1 = a.p1g + sid * kP1Bytes;
   const uint8_t* s2 = a.dzg + sid * kDzBytes;
   for (int e = tid; e < kP1Bytes / 16; e += 256) cp_async16(buf + e * 16, s1 + e * 16);
-  for (int e = tid; e < kDzBytes / 16; e += 256) cp_async16(buf + kP1Bytes + e * 16, s2 + e * 16);
+  for (int e = tid; e < kP1Bytes / 16; e += 256) {   // plane c row r <- p1 plane c row r+1
+    const bool v = (e % kRows) + 1 < kRows;
+    cp_async16_zfill(buf + kP1Bytes + e * 16, s1 + (v ? (e + 1) * 16 : 0), v);
+  }
+  for (int e = tid; e < kDzBytes / 16; e += 256) cp_async16(buf + kWgP1 + e * 16, s2 + e * 16);
   cp_async_commit();
 }
 
-// k_wgrad: y < 2: conv2 wgrad for half of the taps on tcgen05 (double-buffered
-//          sample staging overlaps the MMAs) + update;
-//          y == 2: sum the per-sample conv1/bias partials (sample order) + update
-// grid (active, 3), 256 threads
+// k_wgrad: x < 2: conv2 wgrad for the taps of rows ky in [3x, 3x + 3 - x) on
+//          tcgen05 (M=64 co x N=64 (two taps x 32 ci) / N=32 (kx = 4), K =
+//          output positions; double-buffered sample staging overlaps the
+//          MMAs) + update;
+//          x == 2: sum the per-sample conv1/bias partials (sample order) + update
+// grid (3, active), 256 threads
 __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
-  const Slot sl = a.slots[blockIdx.x];
+  const Slot sl = a.slots[blockIdx.y];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -932,8 +944,8 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = sl.cnt;
   float* W = a.w + int64_t(sl.r) * a.P;
-  const int64_t s0 = sidx(blockIdx.x, 0, a.BS);
-  if (blockIdx.y == kWgSplit) {
+  const int64_t s0 = sidx(blockIdx.y, 0, a.BS);
+  if (blockIdx.x == kWgSplit) {
     for (int k = tid; k < kPg; k += 256) {
       float g = 0.0f;
 #pragma unroll 8
@@ -943,7 +955,8 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
     }
     return;
   }
-  const int tap0 = blockIdx.y * 13, ntap = blockIdx.y == 0 ? 13 : 12;
+  const int ky0 = blockIdx.x * 3, nky = blockIdx.x == 0 ? 3 : 2;
+  const int tap0 = ky0 * 5, ntap = nky * 5;
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     mbar_init(&mbar, 1);
@@ -953,7 +966,8 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t idesc = idesc_bf16(64, 32, true, true);
+  const uint32_t idesc64 = idesc_bf16(64, 64, true, true);
+  const uint32_t idesc32 = idesc_bf16(64, 32, true, true);
   wg_stage(a, s0, smem, tid);
   for (int i = 0; i < cnt; ++i) {
     uint8_t* buf = smem + (i & 1) * kWgBuf;
@@ -968,17 +982,22 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
     __syncthreads();
     if (tid == 0) {
       fence_after_sync();
-      // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[ci][p] = p1 row p + ky*18 + kx
-      const uint64_t a0 = desc(smem_u32(buf) + kP1Bytes, 128, kPlane) + uint64_t(2 * kG + 2);
+      // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[(tap, ci)][p] =
+      // p1 (shift-0 / shift-1 copies) row p + ky*18 + kx
+      const uint64_t a0 = desc(smem_u32(buf) + kWgP1, 128, kPlane) + uint64_t(2 * kG + 2);
       const uint64_t b00 = desc(smem_u32(buf), 128, kPlane);
 #pragma unroll 1
-      for (int tl = 0; tl < ntap; ++tl) {
-        const int tap = tap0 + tl;
-        const uint64_t b0 = b00 + uint64_t((tap / 5) * kG + tap % 5);
+      for (int yy = 0; yy < nky; ++yy) {
+        const int ky = ky0 + yy;
 #pragma unroll
-        for (int ks = 0; ks < 16; ++ks)
-          mma_bf16(tmem + tl * 32, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), idesc,
-                   i > 0 || ks > 0);
+        for (int kx = 0; kx < 5; kx += 2) {
+          const int tl = yy * 5 + kx;
+          const uint64_t b0 = b00 + uint64_t(ky * kG + kx);
+#pragma unroll
+          for (int ks = 0; ks < 16; ++ks)
+            mma_bf16(tmem + tl * 32, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), kx < 4 ? idesc64 : idesc32,
+                     i > 0 || ks > 0);
+        }
       }
       commit(&mbar);
     }
@@ -987,7 +1006,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   fence_after_sync();
   // epilogue: TMEM (M=64 rows in lanes 32q + [0,16)) -> smem tile [64][ntap*32]
   // -> coalesced SGD update of the contiguous W2[co][tap0*32 ...] row segments
-  float* sG = reinterpret_cast<float*>(smem);  // 64 x 416 fp32 = 106 KB (buffers are free)
+  float* sG = reinterpret_cast<float*>(smem);  // 64 x 481 fp32 = 123 KB (buffers are free)
   const int width = ntap * 32;
   {
     const int q = warp & 3, part = warp >> 2;
@@ -1000,7 +1019,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
         tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(tl * 32 + c16 * 16), v);
         if (lane < 16) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) sG[co * (13 * 32 + 1) + tl * 32 + c16 * 16 + k] = v[k];
+          for (int k = 0; k < 16; ++k) sG[co * kWgStride + tl * 32 + c16 * 16 + k] = v[k];
         }
       }
     }
@@ -1024,7 +1043,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
       if (e < 64 * width) {
         const int co = e / width, c = e - co * width;
         const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
-        W[idx] = sgd(a, sl.r, idx, wv[k], sG[co * (13 * 32 + 1) + c]);
+        W[idx] = sgd(a, sl.r, idx, wv[k], sG[co * kWgStride + c]);
       }
     }
   }
@@ -1085,7 +1104,9 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   if (max_spb < 0) spb = -max_spb;  // forced (tests)
   const int BSpb = (a.BS + spb - 1) / spb;
   pb::prof_begin(pb::K_CNN_FWD, s);
-  k_fwd<<<dim3(active, BSpb), kFwdThreads, kFwdSmem, s>>>(a, spb);
+  // grids put a client's CTAs next to each other (slot = blockIdx.y), so the
+  // sample-split / tap-split CTAs of one client share its data through L2
+  k_fwd<<<dim3(BSpb, active), kFwdThreads, kFwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_FWD, s);
   if (a.hx) {
     int rc = lazy_fc1_sweep(a, active, 0, s);
@@ -1109,10 +1130,10 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::prof_end(pb::K_CNN_FC1_BWD, s);
   }
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
-  k_bwd_conv<<<dim3(active, BSpb), 256, kBwdSmem, s>>>(a, spb);
+  k_bwd_conv<<<dim3(BSpb, active), 256, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
-  k_wgrad<<<dim3(active, kWgSplit + 1), 256, kWgSmem, s>>>(a);
+  k_wgrad<<<dim3(kWgSplit + 1, active), 256, kWgSmem, s>>>(a);
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
 }

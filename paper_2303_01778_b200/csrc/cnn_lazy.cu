@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 //         (M = 4 x 128 o, N = 32, K = 128; A = hdt columns, B = Gx^T in smem)
 //   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][i][j] = -lr * Gd
 // History rows j >= t*BS are zero-filled (they hold the current step).
-// grid (active, njt), 128 threads
+// grid (njt, active), 128 threads
 // ---------------------------------------------------------------------------
 constexpr int kGrKC = 64;                      // K floats per chunk
 constexpr int kGrA = 128 * kGrKC * 4;          // 32 KB
@@ -93,7 +93,7 @@ constexpr size_t kGramBwdSmem = kGrStages * kGrStage;
 
 template <bool FWD>
 __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
-  const int s = blockIdx.x, jt = blockIdx.y;
+  const int s = blockIdx.y, jt = blockIdx.x;   // a client's history tiles are adjacent
   const Slot sl = a.slots[s];
   const int cnt = sl.cnt;
   if (cnt == 0) return;
@@ -568,7 +568,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     pb::prof_end(pb::K_CNN_LZ_XT, s);
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, s);
-      k_lz_gram<true><<<dim3(active, njt), 128, kGramFwdSmem, s>>>(a);
+      k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(a);
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
@@ -583,7 +583,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   } else {
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
-      k_lz_gram<false><<<dim3(active, njt), 128, kGramBwdSmem, s>>>(a);
+      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(a);
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
