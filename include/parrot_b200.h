@@ -272,6 +272,11 @@ int pb_umma_selftest(const void* A, const void* B, float* D, int M, int N, int K
 int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout, int H, int R, int stride,
                         const void* x, const void* w, const void* dz, float* out, void* stream);
 
+/* 128 x N x K tf32 GEMM D = A * B^T (A [128,K], B [N,K] row-major fp32) with
+ * both operands loaded by TMA into SWIZZLE_128B K-major tiles (tma.cuh
+ * conventions; tests only).  N % 16 == 0, N <= 256, K % 32 == 0. */
+int pb_tma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, void* stream);
+
 /* 128 x N x K tf32 tcgen05 GEMM D = A * B^T from fp32 row-major A [128,K],
  * B [N,K]; a_mn/b_mn select MN-major smem staging (tests only). */
 int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,

@@ -1,0 +1,118 @@
+// TMA tensor-map encoding (host) and a TMA + SWIZZLE_128B tf32 UMMA self-test
+// that pins the conventions of tma.cuh on the hardware (tests only).
+#include "tma.cuh"
+
+#include <string>
+
+#include "common.cuh"
+
+namespace pb {
+namespace tma {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+int make_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+                uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch * 4) % 16 || box_rows < 1 || box_rows > 256)
+    return fail(PB_ERR_INVALID, "make_2d_f32: misaligned tensor or bad box");
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {pitch * 4};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return PB_OK;
+}
+
+}  // namespace tma
+}  // namespace pb
+
+namespace {
+
+using namespace pb::umma;
+
+// D[128][N] = A[128][K] * B[N][K]^T, fp32 operands (tf32 MMA), one CTA
+__global__ void __launch_bounds__(128) k_tma_selftest(const __grid_constant__ CUtensorMap ta,
+                                                      const __grid_constant__ CUtensorMap tb, float* D, int N,
+                                                      int K) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full, done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    pb::tma::prefetch(&ta);
+    pb::tma::prefetch(&tb);
+    mbar_init(&full, 1);
+    mbar_init(&done, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 128 * 128;
+  const int nk = K / 32;
+  for (int c = 0; c < nk; ++c) {
+    if (tid == 0) {
+      pb::tma::expect_tx(&full, uint32_t((128 + N) * 128));
+      pb::tma::load_2d(sA, &ta, c * 32, 0, &full);
+      pb::tma::load_2d(sB, &tb, c * 32, 0, &full);
+      mbar_wait(&full, c & 1);
+      fence_after_sync();
+      const uint64_t a0 = pb::tma::desc_sw128(smem_u32(sA)), b0 = pb::tma::desc_sw128(smem_u32(sB));
+      const uint32_t idesc = idesc_tf32(128, N);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+      commit(&done);
+      mbar_wait(&done, c & 1);  // stage reused next chunk
+    }
+    __syncthreads();
+  }
+  fence_after_sync();
+  const int row = warp * 32 + lane;
+  for (int c16 = 0; c16 < N; c16 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c16), v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) D[row * N + c16 + k] = v[k];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+
+}  // namespace
+
+extern "C" int pb_tma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, void* stream) {
+  if (!A || !B || !D || N < 16 || N > 256 || N % 16 || K < 32 || K % 32)
+    return pb::fail(PB_ERR_INVALID, "pb_tma_tf32_selftest: bad arguments");
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = pb::tma::make_2d_f32(&ta, A, uint64_t(K), 128, uint64_t(K), 128))) return rc;
+  if ((rc = pb::tma::make_2d_f32(&tb, B, uint64_t(K), uint64_t(N), uint64_t(K), uint32_t(N)))) return rc;
+  const size_t smem = 1024 + 128 * 128 + size_t(N) * 128;
+  cudaFuncSetAttribute((const void*)k_tma_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_tma_selftest<<<1, 128, smem, pb::as_stream(stream)>>>(ta, tb, D, N, K);
+  return pb::check_launch("pb_tma_tf32_selftest");
+}

@@ -70,3 +70,19 @@ def test_umma_tf32_layouts_and_rounding(a_mn, b_mn):
             (("exact", exact), ("trunc", trunc), ("rne", rne))}
     print("tf32 error vs", errs)
     assert min(errs.values()) < 5e-4, errs
+
+
+@pytest.mark.parametrize("N,K", [(32, 64), (128, 256), (256, 96)])
+def test_tma_sw128_tf32_gemm(N, K):
+    """TMA-loaded SWIZZLE_128B K-major tf32 tiles (tma.cuh) through tcgen05:
+    D = A B^T against torch on the same tf32-truncated operands."""
+    import torch
+    from paper_2303_01778_b200._lib import lib, ptr
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    A = torch.randn(128, K, device="cuda", generator=g)
+    B = torch.randn(N, K, device="cuda", generator=g)
+    D = torch.empty(128, N, device="cuda")
+    lib.check(lib.pb_tma_tf32_selftest(ptr(A), ptr(B), ptr(D), N, K, torch.cuda.current_stream().cuda_stream))
+    trunc = lambda x: (x.view(torch.int32) & -8192).view(torch.float32).double()  # noqa: E731
+    ref = trunc(A) @ trunc(B).t()
+    assert float((D.double() - ref).norm() / ref.norm()) < 1e-6
