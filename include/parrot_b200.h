@@ -185,21 +185,23 @@ typedef struct {
   float* ws_dht;            /* per slot: 512*32 f32 (dH transposed, zero-padded) */
   /* Low-rank fc1 for plain SGD (mu = 0, no control variates); all NULL for
    * the direct per-client fc1.  Client row r owns history rows
-   * [lz_hoff[r], lz_hoff[r] + lz_hlen[r]), lz_hlen[r] = round_up(steps_r*BS, 4);
+   * [lz_hoff[r], lz_hoff[r] + lz_hlen[r]) of lz_rows, lz_hlen[r] =
+   * round_up(steps_r*BS, 32);
    * step t's sample i is row t*BS + i.  Every client's fc1 weights stay
    * W0 - lr * sum_t dH_t^T X_t during the round (never materialised per
    * step); they are written to w once, after the last sweep.  The four
    * history buffers must be zeroed by the caller before the call. */
-  float* lz_hx;             /* [rows, 3136] f32                               */
-  float* lz_hxt;            /* per client [3136][hlen] f32                    */
-  float* lz_hd;             /* [rows, 512] f32                                */
-  float* lz_hdt;            /* per client [512][hlen] f32                     */
+  float* lz_hx;             /* [lz_rows, 3136] f32                            */
+  float* lz_hxt;            /* [3136, lz_rows] f32                            */
+  float* lz_hd;             /* [lz_rows, 512] f32                             */
+  float* lz_hdt;            /* [512, lz_rows] f32                             */
   const int64_t* lz_hoff;   /* [g]                                            */
   const int32_t* lz_hlen;   /* [g]                                            */
   float* lz_w0t;            /* [3136*512] f32 scratch (W1 of w0 transposed)   */
   float* lz_zp;             /* max_t active_t*njt_t * 512*32 f32, njt_t = ceil(t*BS/128) */
   float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
   float* lz_fpart;          /* 74*512*32 f32: tail split-K partials           */
+  int64_t lz_rows;          /* total history rows (multiple of 32)            */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;

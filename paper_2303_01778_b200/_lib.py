@@ -41,7 +41,7 @@ class CnnTrainArgs(ctypes.Structure):
         ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("ws_dht", c_void_p),
         ("lz_hx", c_void_p), ("lz_hxt", c_void_p), ("lz_hd", c_void_p), ("lz_hdt", c_void_p),
         ("lz_hoff", c_void_p), ("lz_hlen", c_void_p), ("lz_w0t", c_void_p), ("lz_zp", c_void_p),
-        ("lz_gdt", c_void_p), ("lz_fpart", c_void_p), ("g", c_int64),
+        ("lz_gdt", c_void_p), ("lz_fpart", c_void_p), ("lz_rows", c_int64), ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),

@@ -78,9 +78,9 @@ def lazy_enabled(terms: dict) -> bool:
 
 
 def lazy_plan(total: np.ndarray, active: np.ndarray, BS: int):
-    """History layout: client row r owns hlen[r] = round_up(steps_r * BS, 4)
+    """History layout: client row r owns hlen[r] = round_up(steps_r * BS, 32)
     rows from hoff[r]; partial-buffer capacities over the sweeps."""
-    hlen = ((total * BS + 3) // 4 * 4).astype(np.int32)
+    hlen = ((total * BS + 31) // 32 * 32).astype(np.int32)
     hoff = np.zeros(len(total), dtype=np.int64)
     if len(total) > 1:
         hoff[1:] = np.cumsum(hlen[:-1], dtype=np.int64)
@@ -153,6 +153,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
                                                 ptr(lz["hdt"]))
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
         a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
+        a.lz_rows = rows
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)

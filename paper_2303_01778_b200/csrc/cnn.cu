@@ -473,11 +473,11 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   }
   __syncthreads();  // sDH complete
   if (a.hx) {
-    const int L = a.hlen[sl.r];
-    float* hdt = a.hdt + sl.hist * kH1 + int64_t(a.step) * a.BS;
+    // dH^T columns of the global [512][hrows] history (row pitch hrows)
+    float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
     for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
       const int o = p / cnt, i = p - o * cnt;
-      hdt[int64_t(o) * L + i] = sDH[i * kH1 + o];
+      hdt[int64_t(o) * a.hrows + i] = sDH[i * kH1 + o];
     }
     for (int o = tid; o < kH1; o += kHeadThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
@@ -1085,6 +1085,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
   a.hx = t.lz_hx; a.hxt = t.lz_hxt; a.hd = t.lz_hd; a.hdt = t.lz_hdt; a.hoff = t.lz_hoff;
   a.hlen = t.lz_hlen; a.w0t = t.lz_w0t; a.zp = t.lz_zp; a.gdt = t.lz_gdt; a.fpart = t.lz_fpart;
+  a.hrows = t.lz_rows;
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
   a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.dht = t.ws_dht; a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
@@ -1155,10 +1156,13 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
     if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hxt || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
-        !a.w0t || !a.zp || !a.gdt || !a.fpart || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
+        !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 32 || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
         !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
       return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
-    if ((rc = lazy_fc1_prepare(a, s))) return rc;
+    if ((rc = lazy_fc1_prepare(a, s))) {
+      lazy_fc1_release(a);
+      return rc;
+    }
   }
   for (int step = 0; step < t.sweeps; ++step) {
     const int active = t.active[step];
@@ -1167,10 +1171,13 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     pb::prof_begin(pb::K_CNN_SLOTS, s);
     k_slots<<<(active + 127) / 128, 128, 0, s>>>(a, active);
     pb::prof_end(pb::K_CNN_SLOTS, s);
-    if ((rc = launch_sweep(a, active, true, spb, s))) return rc;
+    if ((rc = launch_sweep(a, active, true, spb, s))) break;
   }
-  if (a.hx) return lazy_fc1_materialize(a, int(t.g), s);
-  return PB_OK;
+  if (a.hx) {
+    if (!rc) rc = lazy_fc1_materialize(a, int(t.g), s);
+    lazy_fc1_release(a);  // the maps were copied into the launches' parameters
+  }
+  return rc;
 }
 
 extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* out2,

@@ -66,14 +66,17 @@ struct Args {
   float* pg;       // [slots*BS, kPg] per-sample conv1-w/conv1-b/conv2-b gradient partials
   double* eval;    // [2] correct, loss (eval mode)
   // ---- lazy fc1 (plain SGD): the round's (X, dH) history, see cnn_lazy.cu --
-  // Client row r owns history rows [hist_off[r], hist_off[r] + L_r); step t's
-  // sample i is row t*BS + i.  All four buffers are zeroed before the round.
-  float* hx;              // [rows, kFlat]  X_t (the p2 activations)
-  float* hxt;             // client block [kFlat][L_r]  X transposed
-  float* hd;              // [rows, kH1]    dH_t = dL/dz1
-  float* hdt;             // client block [kH1][L_r]    dH transposed
+  // Client row r owns history rows [hist_off[r], hist_off[r] + L_r) of
+  // hrows (L_r a multiple of 32); step t's sample i is row t*BS + i.  All
+  // four buffers are zeroed before the round.
+  float* hx;              // [hrows, kFlat]  X_t (the p2 activations)
+  float* hxt;             // [kFlat, hrows]  X transposed
+  float* hd;              // [hrows, kH1]    dH_t = dL/dz1
+  float* hdt;             // [kH1, hrows]    dH transposed
   const int64_t* hoff;    // [G] first history row of client row r
-  const int32_t* hlen;    // [G] L_r (multiple of 4)
+  const int32_t* hlen;    // [G] L_r (multiple of 32)
+  int64_t hrows;          // total history rows (multiple of 32)
+  const void* lzmaps;     // host: the round's TMA tensor maps (cnn_lazy.cu)
   const float* w0t;       // [kFlat][kH1] fc1 block of w0, transposed
   float* zp;              // [slots * njt][kH1][32] forward correction partials
   float* gdt;             // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
@@ -155,8 +158,10 @@ __device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthre
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s);
 // Write each client's end fc1 weights W0 - lr * dH^T X (cnn_lazy.cu).
 int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s);
-// Transpose the fc1 block of w0 into a.w0t (cnn_lazy.cu).
-int lazy_fc1_prepare(const Args& a, cudaStream_t s);
+// Transpose the fc1 block of w0 into a.w0t and encode the round's tensor
+// maps (a.lzmaps); lazy_fc1_release frees them (cnn_lazy.cu).
+int lazy_fc1_prepare(Args& a, cudaStream_t s);
+void lazy_fc1_release(Args& a);
 
 }  // namespace cnn
 }  // namespace pb

@@ -20,21 +20,76 @@
 // All contractions are tcgen05 kind::tf32 (fp32 accumulation in TMEM).  The
 // history operands (X, dH) and the Gram rows are stored rounded to nearest
 // tf32, so the MMA's operand truncation is exact for them and the
-// corrections carry no truncation bias; W0 is truncated.  Every operand is
-// K-major in the SWIZZLE_NONE
-// layout, staged by cp.async through a 4-deep ring (umma.cuh conventions).
-// Reductions have a fixed order (no atomics): results are deterministic.
+// corrections carry no truncation bias; W0 is truncated.  Every operand tile
+// is one TMA box (32 fp32 of K x up to 256 rows, SWIZZLE_128B K-major,
+// tma.cuh) -- the history is kept as plain row-major matrices ([rows, K] and
+// the transposed [K, rows]) so each client's block is a box of one tensor
+// map.  One thread drives a TMA -> MMA ring; the CTA's other warps only run
+// the epilogues.  Reductions have a fixed order (no atomics): results are
+// deterministic.
 #include "cnn_common.cuh"
+#include "tma.cuh"
 
 namespace {
 
 using namespace pb::umma;
 using namespace pb::cnn;
+using pb::tma::desc_sw128;
 
 constexpr int kStages = 4;
 
+// tensor maps of the round (host-encoded, passed as __grid_constant__)
+struct LzMaps {
+  CUtensorMap w0;      // W0 fc1 block  [512][3136],  box 128 rows
+  CUtensorMap w0t;     // W0^T          [3136][512],  box 128
+  CUtensorMap hxa;     // HX            [rows][3136], box 128 (history tiles)
+  CUtensorMap hxb;     // HX                          box 32  (current rows)
+  CUtensorMap hda;     // HD            [rows][512],  box 128
+  CUtensorMap hdb;     // HD                          box 32
+  CUtensorMap hdt;     // HD^T          [512][rows],  box 128
+  CUtensorMap hxt128;  // HX^T          [3136][rows], box 128
+  CUtensorMap hxt256;  // HX^T                        box 256
+  CUtensorMap gdt;     // Gram rows     [slots*32][njt*128], box 32 (per sweep)
+};
+
 inline int njt_of_host(int step, int BS) { return (step * BS + 127) >> 7; }
 __device__ __forceinline__ int njt_of(const Args& a) { return (a.step * a.BS + 127) >> 7; }
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Single-thread TMA -> MMA ring over n chunks (call from ONE thread).
+// issue(c, stage, full) issues chunk c's TMA loads and its expect_tx on
+// `full`; mma(c, stage) issues its MMAs, then the ring commits them to
+// empty[stage] and refills the stage of chunk c-1 (S-1 chunks in flight).
+template <int S, class Issue, class Mma>
+__device__ __forceinline__ void tma_ring(int n, uint8_t* ring, int stage_bytes, uint64_t* full, uint64_t* empty,
+                                         Issue issue, Mma mma) {
+  for (int c = 0; c < n && c < S; ++c) issue(c, ring + c * stage_bytes, &full[c]);
+  for (int c = 0; c < n; ++c) {
+    const int st = c % S;
+    mbar_wait(&full[st], (c / S) & 1);
+    fence_after_sync();
+    mma(c, ring + st * stage_bytes);
+    commit(&empty[st]);
+    const int nx = c - 1 + S;
+    if (c >= 1 && nx < n) {
+      const int s2 = (c - 1) % S;
+      mbar_wait(&empty[s2], ((c - 1) / S) & 1);   // chunk c-1's MMAs released the stage
+      issue(nx, ring + s2 * stage_bytes, &full[s2]);
+    }
+  }
+  if (n > 0) mbar_wait(&empty[(n - 1) % S], ((n - 1) / S) & 1);
+}
+
+__device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, int S) {
+  for (int i = 0; i < S; ++i) {
+    mbar_init(&full[i], 1);
+    mbar_init(&empty[i], 1);
+  }
+  fence_init();
+}
 
 // ---------------------------------------------------------------------------
 // k_lz_w0t: w0t[k][o] = w0[fc1][o][k]  (once per round)
@@ -49,7 +104,7 @@ __global__ void k_lz_w0t(const float* __restrict__ w0, float* __restrict__ w0t) 
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_xt: history columns hxt[k][t*BS + i] = X_t[i][k] of this sweep
+// k_lz_xt: history columns hxt[k][hist + t*BS + i] = X_t[i][k] of this sweep
 // grid (active, 25 k-tiles of 128), 128 threads
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
@@ -64,11 +119,10 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
     if (kk < kn) tile[i][kk] = x[int64_t(i) * kFlat + k0 + kk];
   }
   __syncthreads();
-  const int L = a.hlen[sl.r];
-  float* xt = a.hxt + sl.hist * kFlat + int64_t(k0) * L + int64_t(a.step) * a.BS;
+  float* xt = a.hxt + int64_t(k0) * a.hrows + sl.hist + int64_t(a.step) * a.BS;
   for (int e = threadIdx.x; e < cnt * kn; e += 128) {
     const int kk = e / cnt, i = e - kk * cnt;
-    xt[int64_t(kk) * L + i] = tile[i][kk];
+    xt[int64_t(kk) * a.hrows + i] = tile[i][kk];
   }
 }
 
@@ -79,127 +133,113 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 //         partial  zp[s][jt][o][i] = -lr * sum_{j in tile} dH_j[o] Gx[j][i]
 //         (M = 4 x 128 o, N = 32, K = 128; A = hdt columns, B = Gx^T in smem)
 //   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][i][j] = -lr * Gd
-// History rows j >= t*BS are zero-filled (they hold the current step).
+// History rows j >= t*BS (the current step, later steps, other clients) are
+// zeroed when the Gram tile leaves TMEM.
 // grid (njt, active), 128 threads
 // ---------------------------------------------------------------------------
-constexpr int kGrKC = 64;                      // K floats per chunk
-constexpr int kGrA = 128 * kGrKC * 4;          // 32 KB
-constexpr int kGrB = 32 * kGrKC * 4;           // 8 KB
-constexpr int kGrStage = kGrA + kGrB;          // 40 KB
-constexpr int kGxT = 32 * 128 * 4;             // Gx^T [32 i][128 j], 16 KB
-constexpr int kGrStages = 5;                   // 3 chunks in flight
-constexpr size_t kGramFwdSmem = kGrStages * kGrStage + kGxT;   // 216 KB
-constexpr size_t kGramBwdSmem = kGrStages * kGrStage;
+constexpr int kGrA = 128 * 128;                // 16 KB: 128 rows x 32 fp32
+constexpr int kGrB = 32 * 128;                 // 4 KB
+constexpr int kGrStage = kGrA + kGrB;          // 20 KB
+constexpr int kGrStages = 8;
+constexpr int kGxT = 4 * 32 * 128;             // Gx^T: 4 K-atoms of [32 i][32 j], 16 KB
+constexpr size_t kGramFwdSmem = 1024 + kGrStages * kGrStage + kGxT;
+constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
 
 template <bool FWD>
-__global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
+__global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMaps m, Args a) {
   const int s = blockIdx.y, jt = blockIdx.x;   // a client's history tiles are adjacent
   const Slot sl = a.slots[s];
   const int cnt = sl.cnt;
   if (cnt == 0) return;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kGrStages], empty[kGrStages], full2[kStages], empty2[kStages];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = a.step, jlim = t * a.BS, j0 = jt * 128, njt = njt_of(a);
-  constexpr int KD = FWD ? kFlat : kH1;
-  constexpr int nA = KD / kGrKC;               // 49 | 8
-  const float* hist = FWD ? a.hx : a.hd;
-  const float* Arow = hist + (sl.hist + j0) * KD;                              // history rows
-  const float* Brow = hist + (sl.hist + int64_t(t) * a.BS) * KD;               // current rows
-  const int L = a.hlen[sl.r];
-  const float* hdt = a.hdt + sl.hist * kH1 + j0;                               // [o][L], from column j0
+  constexpr int nA = (FWD ? kFlat : kH1) / 32;   // 98 | 16
+  const int hrow = int(sl.hist) + j0, crow = int(sl.hist + int64_t(t) * a.BS);
   uint8_t* sGxT = smem + kGrStages * kGrStage;
   if (warp == 0) tmem_alloc<FWD ? 256 : 32>(&tmem_base);
-  ring_init(mbar);
+  if (tid == 0) {
+    ring_barriers(full, empty, kGrStages);
+    ring_barriers(full2, empty2, kStages);
+  }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-
-  auto load = [&](int c, uint8_t* st) {
-    if (c < nA) {
-      const int k0 = c * kGrKC;
-#pragma unroll 4
-      for (int e = tid; e < 128 * 16; e += 128) {
-        const int r = e >> 4, k4 = e & 15;
-        const bool v = j0 + r < jlim;
-        cp_async16_zfill(st + kmaj_f32(r, k4, 2048), Arow + int64_t(v ? r : 0) * KD + k0 + k4 * 4, v);
-      }
-#pragma unroll
-      for (int e = tid; e < 32 * 16; e += 128) {
-        const int r = e >> 4, k4 = e & 15;
-        const bool v = r < cnt;
-        cp_async16_zfill(st + kGrA + kmaj_f32(r, k4, 2048), Brow + int64_t(v ? r : 0) * KD + k0 + k4 * 4, v);
-      }
-    } else {  // FWD phase B: hdt tile [128 o][32 j], o-tile q, j sub-chunk jc
-      const int q = (c - nA) >> 2, jc = (c - nA) & 3;
-#pragma unroll
-      for (int e = tid; e < 128 * 8; e += 128) {
-        const int r = e >> 3, k4 = e & 7;
-        const int col = jc * 32 + k4 * 4;
-        const bool v = j0 + col < jlim;  // columns >= t*BS hold no history yet
-        cp_async16_zfill(st + kmaj_f32(r, k4, 1024), hdt + int64_t(q * 128 + r) * L + (v ? col : 0), v);
-      }
-    }
-  };
-  auto mid = [&](int c) {
-    if (FWD && c == nA) {  // Gx complete: TMEM -> Gx^T (the phase-B B operand)
-      mbar_wait(&mbar[(nA - 1) & 1], ((nA - 1) >> 1) & 1);
-      fence_after_sync();
-      const int j = warp * 32 + lane;
-      float v[32];
-      tmem_ld16(tmem + (uint32_t(warp * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
-      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        *reinterpret_cast<float*>(sGxT + kmaj_f32(i, j >> 2, 4096) + (j & 3) * 4) = tf32_rna(v[i]);
-      fence_before_sync();
-    }
-  };
-  auto mma = [&](int c, uint8_t* st) {
-    const uint32_t sa = smem_u32(st);
-    if (c < nA) {
-      const uint64_t a0 = desc(sa, 128, 2048), b0 = desc(sa + kGrA, 128, 2048);
-      const uint32_t idesc = idesc_tf32(128, 32);
-#pragma unroll
-      for (int kk = 0; kk < kGrKC / 8; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
-    } else {
-      const int q = (c - nA) >> 2, jc = (c - nA) & 3;
-      const uint64_t a0 = desc(sa, 128, 1024);
-      const uint64_t b0 = desc(smem_u32(sGxT) + jc * 1024, 128, 4096);
+  const CUtensorMap* ta = FWD ? &m.hxa : &m.hda;
+  const CUtensorMap* tb = FWD ? &m.hxb : &m.hdb;
+  if (tid == 0) {
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      pb::tma::expect_tx(f, kGrStage);
+      pb::tma::load_2d(st, ta, c * 32, hrow, f);
+      pb::tma::load_2d(st + kGrA, tb, c * 32, crow, f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kGrA));
       const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, jc > 0 || kk > 0);
-    }
-  };
-  mma_ring<kGrStages>(FWD ? nA + 16 : nA, smem, kGrStage, mbar, load, mid, mma);
-
+        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    tma_ring<kGrStages>(nA, smem, kGrStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
   const float nlr = -a.lr;
+  const int j = warp * 32 + lane;
+  const bool live = j0 + j < jlim;
+  float v[32];
+  tmem_ld16(tmem + (uint32_t(warp * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
+  tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
   if (FWD) {
+    // Gx^T (B operand of phase B, SWIZZLE_128B K-major: atom j/32, row i)
+    uint8_t* atom = sGxT + (j >> 5) * (32 * 128);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      *reinterpret_cast<float*>(atom + pb::tma::sw128_off(i, j & 31)) = live ? tf32_rna(v[i]) : 0.0f;
+    fence_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after_sync();
+      const int hcol = int(sl.hist) + j0;
+      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = q*4 + jc
+        pb::tma::expect_tx(f, kGrA);
+        pb::tma::load_2d(st, &m.hdt, hcol + (c & 3) * 32, (c >> 2) * 128, f);
+      };
+      auto mma = [&](int c, uint8_t* st) {
+        const int q = c >> 2, jc = c & 3;
+        const uint64_t a0 = desc_sw128(smem_u32(st));
+        const uint64_t b0 = desc_sw128(smem_u32(sGxT + jc * 32 * 128));
+        const uint32_t idesc = idesc_tf32(128, 32);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
+      };
+      tma_ring<kStages>(16, smem, kGrA, full2, empty2, issue, mma);
+    }
+    __syncthreads();
+    fence_after_sync();
     float* zp = a.zp + (int64_t(s) * njt + jt) * kH1 * 32;
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
       const int o = q * 128 + warp * 32 + lane;
-      float v[32];
-      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(32 + q * 32), *reinterpret_cast<float(*)[16]>(v));
-      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(48 + q * 32), *reinterpret_cast<float(*)[16]>(v + 16));
+      float w[32];
+      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(32 + q * 32), *reinterpret_cast<float(*)[16]>(w));
+      tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(48 + q * 32), *reinterpret_cast<float(*)[16]>(w + 16));
       float4* dst = reinterpret_cast<float4*>(zp + int64_t(o) * 32);
 #pragma unroll
       for (int i4 = 0; i4 < 8; ++i4)
-        dst[i4] = make_float4(nlr * v[4 * i4], nlr * v[4 * i4 + 1], nlr * v[4 * i4 + 2], nlr * v[4 * i4 + 3]);
+        dst[i4] = make_float4(nlr * w[4 * i4], nlr * w[4 * i4 + 1], nlr * w[4 * i4 + 2], nlr * w[4 * i4 + 3]);
     }
   } else {
-    const int j = warp * 32 + lane;
-    float v[32];
-    tmem_ld16(tmem + (uint32_t(warp * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
-    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     const int64_t jstride = int64_t(njt) * 128;
     float* g = a.gdt + int64_t(s) * 32 * jstride + j0 + j;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) g[i * jstride] = tf32_rna(nlr * v[i]);
+    for (int i = 0; i < 32; ++i) g[i * jstride] = live ? tf32_rna(nlr * v[i]) : 0.0f;
   }
   fence_before_sync();
   __syncthreads();
@@ -215,12 +255,11 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(Args a) {
 // grid (4 o-tiles, ceil(active / spc), ks), 256 threads
 // ---------------------------------------------------------------------------
 constexpr int kSh8 = 8;                         // max slots per CTA (N = 8 x 32)
-constexpr int kShKC = 32;                       // K floats per chunk
-constexpr int kShA = 128 * kShKC * 4;           // 16 KB
-constexpr int kShB = 256 * kShKC * 4;           // 32 KB
+constexpr int kShA = 128 * 128;                 // 16 KB
+constexpr int kShB = 256 * 128;                 // 32 KB
 constexpr int kShStage = kShA + kShB;           // 48 KB
-constexpr size_t kShSmem = kStages * kShStage;  // 192 KB
-constexpr int kFwdChunks = kFlat / kShKC;       // 98
+constexpr size_t kShSmem = 1024 + kStages * kShStage;
+constexpr int kFwdChunks = kFlat / 32;          // 98
 constexpr int kTailCtas = 296;                  // 2 x 148 SMs: tail grids aim for this
 constexpr int kFwdSplitMax = 7;                 // 98 chunks = 7 x 14
 
@@ -246,9 +285,10 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
     if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
 }
 
-__global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active, int spc) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+__global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -259,39 +299,36 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(Args a, int active, int spc) 
     sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
   }
   if (warp == 0) tmem_alloc<256>(&tmem_base);
-  ring_init(mbar);
+  if (tid == 0) ring_barriers(full, empty, kStages);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const float* W1 = a.w0 + oF1W + int64_t(q) * 128 * kFlat;
   const int64_t tb = int64_t(a.step) * a.BS;
-  const int nrows = spc * 32;
-
-  auto load = [&](int c, uint8_t* st) {
-    const int k0 = (c0 + c) * kShKC;
-#pragma unroll
-    for (int e = tid; e < 128 * 8; e += 256) {
-      const int r = e >> 3, k4 = e & 7;
-      cp_async16(st + kmaj_f32(r, k4, 1024), W1 + int64_t(r) * kFlat + k0 + k4 * 4);
+  if (tid == 0) {
+    int rows[kSh8], nv = 0;
+    for (int u = 0; u < spc; ++u) {
+      rows[u] = int(sS[u].hist + tb);
+      nv += sS[u].cnt > 0;
     }
-    for (int e = tid; e < nrows * 8; e += 256) {
-      const int r = e >> 3, k4 = e & 7, u = r >> 5, i = r & 31;
-      const bool v = i < sS[u].cnt;
-      const float* src = a.hx + (sS[u].hist + tb + (v ? i : 0)) * kFlat + k0 + k4 * 4;
-      cp_async16_zfill(st + kShA + kmaj_f32(r, k4, 1024), v ? src : a.hx, v);
-    }
-  };
-  auto mma = [&](int c, uint8_t* st) {
-    const uint32_t sa = smem_u32(st);
-    const uint64_t a0 = desc(sa, 128, 1024), b0 = desc(sa + kShA, 128, 1024);
-    const uint32_t idesc = idesc_tf32(128, nrows);
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int k0 = (c0 + c) * 32;
+      pb::tma::expect_tx(f, uint32_t(kShA + nv * 32 * 128));
+      pb::tma::load_2d(st, &m.w0, k0, q * 128, f);
+      for (int u = 0; u < spc; ++u)
+        if (sS[u].cnt > 0) pb::tma::load_2d(st + kShA + u * 32 * 128, &m.hxb, k0, rows[u], f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
+      const uint32_t idesc = idesc_tf32(128, spc * 32);
 #pragma unroll
-    for (int kk = 0; kk < kShKC / 8; ++kk)
-      mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
-  };
-  mma_ring<kStages>(c1 - c0, smem, kShStage, mbar, load, [](int) {}, mma);
-
+      for (int kk = 0; kk < 4; ++kk)
+        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    tma_ring<kStages>(c1 - c0, smem, kShStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
   const int njt = njt_of(a);
   const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
   const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
@@ -340,95 +377,75 @@ __global__ void __launch_bounds__(512) k_lz_fwd_epi(Args a, int active, int ks) 
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_bwd: dp2 = dH_t W0 + sum_j hxt[k][j] gdt[i][j] for 8 slots x 32 rows
-//   phase 1 (shared): M = 128 k, N = 256, K = 512 (A = w0t, B = dH_t rows)
+// k_lz_bwd: dp2 = dH_t W0 + sum_j hxt[k][j] gdt[i][j] for spc slots x 32 rows
+//   phase 1 (shared): M = 128 k, N = spc*32, K = 512 (A = w0t, B = dH_t rows)
 //   phase 2 (per slot, t > 0): M = 128 k, N = 32, K = t*BS into the slot's
-//   accumulator columns (A = the client's hxt rows, B = its gdt rows)
-// grid (25 k-tiles, ceil(active / 8)), 256 threads
+//   accumulator columns (A = the client's hxt columns, B = its gdt rows)
+// grid (25 k-tiles, ceil(active / spc)), 256 threads
 // ---------------------------------------------------------------------------
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
-__global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active, int spc) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+__global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
-  __shared__ int sL[kSh8], sU[kSh8], sNv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = blockIdx.x * 128, g0 = blockIdx.y * spc;
   if (tid < kSh8) {
     Slot z{};
     sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
-    sL[tid] = sS[tid].cnt > 0 ? a.hlen[sS[tid].r] : 0;
-  }
-  __syncthreads();
-  if (tid == 0) {  // slots with work, in slot order
-    int nv = 0;
-    for (int u = 0; u < kSh8; ++u)
-      if (sS[u].cnt > 0) sU[nv++] = u;
-    sNv = nv;
   }
   if (warp == 0) tmem_alloc<256>(&tmem_base);
-  ring_init(mbar);
+  if (tid == 0) ring_barriers(full, empty, kStages);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const int t = a.step, jlim = t * a.BS, njt = njt_of(a);
+  const int t = a.step, jlim = t * a.BS;
   const int nj = (jlim + 31) >> 5;               // phase-2 chunks per slot
-  const int64_t jstride = int64_t(njt) * 128;
   const int64_t tb = int64_t(t) * a.BS;
-  constexpr int n1 = kH1 / kShKC;                // 16
-
-  auto load = [&](int c, uint8_t* st) {
-    if (c < n1) {
-      const int o0 = c * kShKC;
-#pragma unroll
-      for (int e = tid; e < 128 * 8; e += 256) {
-        const int r = e >> 3, k4 = e & 7;
-        const bool v = k0 + r < kFlat;
-        cp_async16_zfill(st + kmaj_f32(r, k4, 1024), a.w0t + int64_t(v ? k0 + r : 0) * kH1 + o0 + k4 * 4, v);
-      }
-      for (int e = tid; e < spc * 32 * 8; e += 256) {
-        const int r = e >> 3, k4 = e & 7, u = r >> 5, i = r & 31;
-        const bool v = i < sS[u].cnt;
-        const float* src = a.hd + (sS[u].hist + tb + (v ? i : 0)) * kH1 + o0 + k4 * 4;
-        cp_async16_zfill(st + kShA + kmaj_f32(r, k4, 1024), v ? src : a.hd, v);
-      }
-    } else {
-      const int c2 = c - n1, u = sU[c2 / nj], jc = c2 - (c2 / nj) * nj, s = g0 + u;
-      const int j0 = jc * 32, L = sL[u];
-      const float* xt = a.hxt + sS[u].hist * kFlat;
-#pragma unroll
-      for (int e = tid; e < 128 * 8; e += 256) {
-        const int r = e >> 3, k4 = e & 7;
-        const bool v = k0 + r < kFlat && j0 + k4 * 4 < L;
-        cp_async16_zfill(st + kmaj_f32(r, k4, 1024), xt + (v ? int64_t(k0 + r) * L + j0 + k4 * 4 : 0), v);
-      }
-      {
-        const int e = tid, r = e >> 3, k4 = e & 7;  // 32 rows x 8 = 256 = one per thread
-        cp_async16(st + kShA + kmaj_f32(r, k4, 1024), a.gdt + (int64_t(s) * 32 + r) * jstride + j0 + k4 * 4);
-      }
+  constexpr int n1 = kH1 / 32;                   // 16
+  if (tid == 0) {
+    int us[kSh8], rows[kSh8], nv = 0;
+    for (int u = 0; u < spc; ++u) {
+      rows[u] = int(sS[u].hist + tb);
+      if (sS[u].cnt > 0) us[nv++] = u;
     }
-  };
-  auto mma = [&](int c, uint8_t* st) {
-    const uint32_t sa = smem_u32(st);
-    const uint64_t a0 = desc(sa, 128, 1024), b0 = desc(sa + kShA, 128, 1024);
-    if (c < n1) {
-      const uint32_t idesc = idesc_tf32(128, spc * 32);
+    const int n = n1 + (t > 0 ? nv * nj : 0);
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      if (c < n1) {
+        pb::tma::expect_tx(f, uint32_t(kShA + nv * 32 * 128));
+        pb::tma::load_2d(st, &m.w0t, c * 32, k0, f);
+        for (int u = 0; u < spc; ++u)
+          if (sS[u].cnt > 0) pb::tma::load_2d(st + kShA + u * 32 * 128, &m.hdb, c * 32, rows[u], f);
+      } else {
+        const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
+        pb::tma::expect_tx(f, uint32_t(kShA + 32 * 128));
+        pb::tma::load_2d(st, &m.hxt128, int(sS[u].hist) + jc * 32, k0, f);
+        pb::tma::load_2d(st + kShA, &m.gdt, jc * 32, (g0 + u) * 32, f);
+      }
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
+      if (c < n1) {
+        const uint32_t idesc = idesc_tf32(128, spc * 32);
 #pragma unroll
-      for (int kk = 0; kk < kShKC / 8; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
-    } else {
-      const int c2 = c - n1, u = sU[c2 / nj];
-      const uint32_t idesc = idesc_tf32(128, 32);
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+      } else {
+        const int u = us[(c - n1) / nj];
+        const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
-      for (int kk = 0; kk < kShKC / 8; ++kk)
-        mma_tf32(tmem + u * 32, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, true);
-    }
-  };
-  mma_ring<kStages>(n1 + (t > 0 ? sNv * nj : 0), smem, kShStage, mbar, load, [](int) {}, mma);
-
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem + u * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, true);
+      }
+    };
+    tma_ring<kStages>(n, smem, kShStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
   const int k = k0 + (warp & 3) * 32 + lane, half = warp >> 2;
   const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
 #pragma unroll 1
@@ -450,53 +467,43 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(Args a, int active, int spc) 
 
 // ---------------------------------------------------------------------------
 // k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hxt[k][j]
-// (M = 128 o, N = 256 k, K = steps_r * BS); grid (13, 4, g), 256 threads --
-// the client is the slowest grid dimension, so its 52 tiles run together
-// and re-read its history from L2
+// (M = 128 o, N = 256 k, K = steps_r * BS rounded to 32 -- within the
+// client's 32-aligned history); grid (13, 4, g), 256 threads -- the client
+// is the slowest grid dimension, so its 52 tiles re-read its history from L2
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_lz_mat(Args a) {
+__global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMaps m, Args a) {
   const int r = blockIdx.z, q = blockIdx.y, k0 = blockIdx.x * 256;
   const int K = a.steps[r] * a.BS;
   if (K == 0) return;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) tmem_alloc<256>(&tmem_base);
-  ring_init(mbar);
+  if (tid == 0) ring_barriers(full, empty, kStages);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const int L = a.hlen[r];
-  const int64_t hoff = a.hoff[r];
-  const float* dt = a.hdt + hoff * kH1 + int64_t(q) * 128 * L;
-  const float* xt = a.hxt + hoff * kFlat;
-  auto load = [&](int c, uint8_t* st) {
-    const int j0 = c * kShKC;
+  if (tid == 0) {
+    const int hcol = int(a.hoff[r]);
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      pb::tma::expect_tx(f, kShStage);
+      pb::tma::load_2d(st, &m.hdt, hcol + c * 32, q * 128, f);
+      pb::tma::load_2d(st + kShA, &m.hxt256, hcol + c * 32, k0, f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
+      const uint32_t idesc = idesc_tf32(128, 256);
 #pragma unroll
-    for (int e = tid; e < 128 * 8; e += 256) {
-      const int rr = e >> 3, k4 = e & 7;
-      const bool v = j0 + k4 * 4 < L;
-      cp_async16_zfill(st + kmaj_f32(rr, k4, 1024), dt + (v ? int64_t(rr) * L + j0 + k4 * 4 : 0), v);
-    }
-#pragma unroll
-    for (int e = tid; e < 256 * 8; e += 256) {
-      const int rr = e >> 3, k4 = e & 7;
-      const bool v = k0 + rr < kFlat && j0 + k4 * 4 < L;
-      cp_async16_zfill(st + kShA + kmaj_f32(rr, k4, 1024), xt + (v ? int64_t(k0 + rr) * L + j0 + k4 * 4 : 0), v);
-    }
-  };
-  auto mma = [&](int c, uint8_t* st) {
-    const uint32_t sa = smem_u32(st);
-    const uint64_t a0 = desc(sa, 128, 1024), b0 = desc(sa + kShA, 128, 1024);
-    const uint32_t idesc = idesc_tf32(128, 256);
-#pragma unroll
-    for (int kk = 0; kk < kShKC / 8; ++kk)
-      mma_tf32(tmem, a0 + uint64_t(kk * 16), b0 + uint64_t(kk * 16), idesc, c > 0 || kk > 0);
-  };
-  mma_ring<kStages>((K + kShKC - 1) / kShKC, smem, kShStage, mbar, load, [](int) {}, mma);
-
+      for (int kk = 0; kk < 4; ++kk)
+        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    tma_ring<kStages>((K + 31) / 32, smem, kShStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
   const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
   const float* w0row = a.w0 + oF1W + int64_t(o) * kFlat;
   float* wrow = a.w + int64_t(r) * a.P + oF1W + int64_t(o) * kFlat;
@@ -506,12 +513,12 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(Args a) {
     const int col = half * 128 + c16 * 16;
     float v[16];
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col), v);
-    const int k = k0 + col;
-    if (k >= kFlat) continue;
+    const int kk = k0 + col;
+    if (kk >= kFlat) continue;
 #pragma unroll
     for (int i4 = 0; i4 < 4; ++i4) {
-      const float4 w = *reinterpret_cast<const float4*>(w0row + k + 4 * i4);
-      *reinterpret_cast<float4*>(wrow + k + 4 * i4) =
+      const float4 w = *reinterpret_cast<const float4*>(w0row + kk + 4 * i4);
+      *reinterpret_cast<float4*>(wrow + kk + 4 * i4) =
           make_float4(fmaf(nlr, v[4 * i4], w.x), fmaf(nlr, v[4 * i4 + 1], w.y),
                       fmaf(nlr, v[4 * i4 + 2], w.z), fmaf(nlr, v[4 * i4 + 3], w.w));
     }
@@ -541,21 +548,43 @@ int setup() {
   return PB_OK;
 }
 
+LzMaps* maps_of(const Args& a) { return const_cast<LzMaps*>(static_cast<const LzMaps*>(a.lzmaps)); }
+
 }  // namespace
 
 namespace pb {
 namespace cnn {
 
-int lazy_fc1_prepare(const Args& a, cudaStream_t s) {
+int lazy_fc1_prepare(Args& a, cudaStream_t s) {
   int rc = setup();
   if (rc) return rc;
   pb::prof_begin(pb::K_CNN_LZ_XT, s);
   k_lz_w0t<<<dim3(kFlat / 32, kH1 / 32), dim3(32, 8), 0, s>>>(a.w0, const_cast<float*>(a.w0t));
   pb::prof_end(pb::K_CNN_LZ_XT, s);
+  LzMaps* m = new LzMaps();
+  a.lzmaps = m;
+  const uint64_t R = uint64_t(a.hrows);
+  using pb::tma::make_2d_f32;
+  if ((rc = make_2d_f32(&m->w0, a.w0 + oF1W, kFlat, kH1, kFlat, 128)) ||
+      (rc = make_2d_f32(&m->w0t, a.w0t, kH1, kFlat, kH1, 128)) ||
+      (rc = make_2d_f32(&m->hxa, a.hx, kFlat, R, kFlat, 128)) ||
+      (rc = make_2d_f32(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
+      (rc = make_2d_f32(&m->hda, a.hd, kH1, R, kH1, 128)) ||
+      (rc = make_2d_f32(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
+      (rc = make_2d_f32(&m->hdt, a.hdt, R, kH1, R, 128)) ||
+      (rc = make_2d_f32(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
+      (rc = make_2d_f32(&m->hxt256, a.hxt, R, kFlat, R, 256)))
+    return rc;
   return pb::check_launch("lazy fc1 prepare");
 }
 
+void lazy_fc1_release(Args& a) {
+  delete maps_of(a);
+  a.lzmaps = nullptr;
+}
+
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
+  LzMaps& m = *maps_of(a);
   const int njt = njt_of_host(a.step, a.BS);
   // head sweeps: 8 clients share each W0 tile (N = 256); tail sweeps (fewer
   // clients than SMs): one client per CTA, and the forward splits K so that
@@ -568,12 +597,12 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     pb::prof_end(pb::K_CNN_LZ_XT, s);
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, s);
-      k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(a);
+      k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(m, a);
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
-    k_lz_fwd<<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(a, active, spc);
+    k_lz_fwd<<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (ks > 1) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
@@ -582,12 +611,15 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     }
   } else {
     if (njt > 0) {
+      int rc = pb::tma::make_2d_f32(&m.gdt, a.gdt, uint64_t(njt) * 128, uint64_t(active) * 32,
+                                    uint64_t(njt) * 128, 32);
+      if (rc) return rc;
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
-      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(a);
+      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(m, a);
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
-    k_lz_bwd<<<dim3(kBwKT, groups), 256, kShSmem, s>>>(a, active, spc);
+    k_lz_bwd<<<dim3(kBwKT, groups), 256, kShSmem, s>>>(m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");
@@ -596,7 +628,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
 int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s) {
   if (g <= 0) return PB_OK;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
-  k_lz_mat<<<dim3((kFlat + 255) / 256, kH1 / 128, g), 256, kShSmem, s>>>(a);
+  k_lz_mat<<<dim3((kFlat + 255) / 256, kH1 / 128, g), 256, kShSmem, s>>>(*maps_of(a), a);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);
   return pb::check_launch("lazy fc1 materialise");
 }
