@@ -310,6 +310,13 @@ def run_b200(args) -> dict:
         "kernels_ms_per_round": {k: round(v[0] / args.steps, 3) for k, v in kernels.items()},
         "kernels_roofline_frac": {k: (round(v["frac"], 4) if v.get("frac") is not None else None)
                                   for k, v in all_roofs.items()},
+        "round_roofline": {"bound": "tensor",
+                           "achieved": CNN_TRAIN_FLOP * samples_timed / (dev_ms / 1e3) / 1e12,
+                           "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                           "frac": CNN_TRAIN_FLOP * samples_timed / (dev_ms / 1e3) / 1e12
+                           / peaks["bf16_tflops_sustained"],
+                           "work": f"{CNN_TRAIN_FLOP:.3g} FLOP/sample x {samples_timed} samples "
+                                   f"(whole round, all kernels)"},
         "clocks": clocks.summary(),
     }
     if agg is not None:
@@ -333,6 +340,10 @@ def run_b200(args) -> dict:
 FC1_BYTES = {"cnn_fc1_fwd": 4 * 512 * 3136, "cnn_fc1_bwd": 8 * 512 * 3136}
 # conv2 implicit-GEMM FLOPs per sample and pass (fwd, dgrad, wgrad)
 CONV2_FLOP = 2 * 14 * 14 * 64 * 800
+# fc1 FLOPs per sample and pass
+FC1_FLOP = 2 * 512 * 3136
+# whole CNN training step per sample: 73.8 MFLOP
+CNN_TRAIN_FLOP = 73.8e6
 
 
 def roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src) -> dict:
@@ -354,6 +365,15 @@ def roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src) ->
         return {"kernel": name, "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                 "frac": tf / peak, "traffic": None, "peak_source": f"{peak_src} bf16 sustained",
                 "work": f"conv2 implicit GEMM {CONV2_FLOP} FLOP/sample x {samples_timed} samples"}
+    if name in ("cnn_lz_fwd", "cnn_lz_bwd"):
+        # the shared W0 GEMM of the low-rank fc1 (forward / dgrad): 2*512*3136
+        # FLOP per sample on tf32 tensor cores (tf32 peak = half the bf16 peak)
+        tf = FC1_FLOP * samples_timed / (ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"] / 2
+        return {"kernel": name, "bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": tf / peak, "traffic": None,
+                "peak_source": f"{peak_src} bf16 sustained / 2 (tf32)",
+                "work": f"fc1 {FC1_FLOP} FLOP/sample x {samples_timed} samples (history corrections extra)"}
     if name == "cnn_head":
         return {"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
                 "frac": None, "traffic": None}
