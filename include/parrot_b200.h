@@ -202,11 +202,36 @@ typedef struct {
   float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
   float* lz_fpart;          /* 74*512*32 f32: tail split-K partials           */
   int64_t lz_rows;          /* total history rows (multiple of 32)            */
+  int32_t lz_defer;         /* 1: leave the fc1 block of w unmaterialised      */
+                            /*    (fold it with pb_cnn_lazy_fold instead)      */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;
 } pb_cnn_train_args;
 int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
+
+/* Deferred fc1 fold of a low-rank CNN round (local_fold, fedsim/aggregate.py
+ * :76-102, for the fc1_w entry of a FedAvg device partial):
+ *   acc += wsum * W0 - lr * sum_j w_j * HD_j^T HX_j
+ * over the device's clients j, whose history rows are [row_lo, row_hi) of
+ * the round's [lz_rows] history (pb_cnn_train_group with lz_defer = 1).
+ * Scales the clients' hdt columns in place (round scratch).  part: splits *
+ * 512 * 3136 f32 scratch. */
+typedef struct {
+  float* acc;               /* [512*3136] fc1_w accumulator of the partial     */
+  const float* w0;          /* [P] round-start model                           */
+  const float* hxt;         /* [3136, hrows]                                   */
+  float* hdt;               /* [512, hrows] (scaled in place)                  */
+  int64_t hrows, row_lo, row_hi;
+  const int64_t* hoff;      /* [nclients] first history row of each client    */
+  const int32_t* nrows;     /* [nclients] live history rows (steps * BS)       */
+  const float* w;           /* [nclients] fold weights (sample counts)         */
+  int64_t nclients;
+  float* part;
+  int32_t splits;
+  float wsum, lr;
+} pb_cnn_lazy_fold_args;
+int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream);
 
 /* Forward-only evaluation of parameter row 0 of args->w on `rows` samples
  * (order = row ids); out2[0] += #correct, out2[1] += sum CE.  args->g is the

@@ -41,10 +41,20 @@ class CnnTrainArgs(ctypes.Structure):
         ("ws_dz", c_void_p), ("ws_dp1", c_void_p), ("ws_dht", c_void_p),
         ("lz_hx", c_void_p), ("lz_hxt", c_void_p), ("lz_hd", c_void_p), ("lz_hdt", c_void_p),
         ("lz_hoff", c_void_p), ("lz_hlen", c_void_p), ("lz_w0t", c_void_p), ("lz_zp", c_void_p),
-        ("lz_gdt", c_void_p), ("lz_fpart", c_void_p), ("lz_rows", c_int64), ("g", c_int64),
+        ("lz_gdt", c_void_p), ("lz_fpart", c_void_p), ("lz_rows", c_int64), ("lz_defer", c_int32),
+        ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),
+    ]
+
+
+class LazyFoldArgs(ctypes.Structure):
+    _fields_ = [
+        ("acc", c_void_p), ("w0", c_void_p), ("hxt", c_void_p), ("hdt", c_void_p),
+        ("hrows", c_int64), ("row_lo", c_int64), ("row_hi", c_int64), ("hoff", c_void_p),
+        ("nrows", c_void_p), ("w", c_void_p), ("nclients", c_int64), ("part", c_void_p),
+        ("splits", c_int32), ("wsum", c_float), ("lr", c_float),
     ]
 
 
@@ -91,6 +101,7 @@ _SIGS = {
     "pb_umma_tf32_probe": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pb_umma_bench": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
+    "pb_cnn_lazy_fold": (c_int, [POINTER(LazyFoldArgs), c_void_p]),
     "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
     "pb_tma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "pb_rn_conv_selftest": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,

@@ -9,7 +9,7 @@ import os
 import numpy as np
 import torch
 
-from ._lib import CnnTrainArgs, lib, ptr, stream_of
+from ._lib import CnnTrainArgs, LazyFoldArgs, lib, ptr, stream_of
 from .models import ModelSpec
 
 # bytes per sample of each workspace buffer (include/parrot_b200.h)
@@ -89,6 +89,47 @@ def lazy_plan(total: np.ndarray, active: np.ndarray, BS: int):
     return hlen, hoff, int(hlen.sum()), cap * 512 * 32, cap * 32 * 128
 
 
+class LazyFc1:
+    """Deferred fc1 of a low-rank CNN round (csrc/cnn_lazy.cu): the clients'
+    fc1_w end weights W0 - lr * HD_j^T HX_j are never written; a device
+    partial folds them straight from the round's history with
+    pb_cnn_lazy_fold (aggregate.fold_group).  Valid until the next CNN group
+    reuses the history workspace."""
+
+    entry = "fc1_w"
+    SPLITS = 32
+
+    def __init__(self, lz: dict, hoff: np.ndarray, hlen: np.ndarray, rows: int, BS: int, lr: float,
+                 w0: torch.Tensor):
+        self.lz, self.hoff, self.hlen, self.rows, self.BS, self.lr, self.w0 = lz, hoff, hlen, rows, BS, lr, w0
+        self.steps = None
+
+    def set_steps(self, steps: np.ndarray) -> None:
+        self.steps = np.asarray(steps, dtype=np.int64)
+
+    def fold(self, acc: torch.Tensor, rows: list[int], weights: np.ndarray) -> None:
+        """acc += sum_j w_j * fc1_w of client rows `rows` (contiguous)."""
+        if not rows:
+            return
+        if rows != list(range(rows[0], rows[0] + len(rows))):
+            raise ValueError("lazy fc1 fold needs a contiguous run of group rows")
+        d = acc.device
+        r = np.asarray(rows)
+        lo = int(self.hoff[r[0]])
+        hi = int(self.hoff[r[-1]] + self.hlen[r[-1]])
+        hoff = torch.from_numpy(self.hoff[r].astype(np.int64)).to(d)
+        nrows = torch.from_numpy((self.steps[r] * self.BS).astype(np.int32)).to(d)
+        w = torch.from_numpy(np.asarray(weights, dtype=np.float32)).to(d)
+        part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
+        f = LazyFoldArgs()
+        f.acc, f.w0, f.hxt, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hxt"]), ptr(self.lz["hdt"])
+        f.hrows, f.row_lo, f.row_hi = self.rows, lo, hi
+        f.hoff, f.nrows, f.w, f.nclients = ptr(hoff), ptr(nrows), ptr(w), len(rows)
+        f.part, f.splits = ptr(part), self.SPLITS
+        f.wsum, f.lr = float(np.sum(np.asarray(weights, dtype=np.float64))), self.lr
+        lib.check(lib.pb_cnn_lazy_fold(ctypes.byref(f), stream_of(acc)))
+
+
 def _samples_per_cta() -> int:
     return int(os.environ.get("PB_CNN_SPB", "10"))
 
@@ -115,13 +156,20 @@ def sweep_plan(n: np.ndarray, batch_size: int, epochs: int):
 
 def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, bad, *,
                     spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
-                    state_work) -> None:
+                    state_work, defer_fc1: bool = False) -> "LazyFc1 | None":
     G = len(n)
     BS, total, rank, active = sweep_plan(n, batch_size, epochs)
     if BS > MAX_BATCH:
         raise ValueError(f"the CNN path supports minibatches of up to {MAX_BATCH} samples, got {BS}")
     d = w_out.device
-    w_out.copy_(w0.view(1, -1).expand(G, -1))
+    lazy = lazy_enabled(terms)
+    defer = defer_fc1 and lazy
+    if defer:  # the fc1_w columns stay unwritten: the fold reads the history
+        f_off, f_size = [(o, sz) for nm, o, sz, _ in spec.columns() if nm == "fc1_w"][0]
+        w_out[:, :f_off].copy_(w0[:f_off].view(1, -1).expand(G, -1))
+        w_out[:, f_off + f_size:].copy_(w0[f_off + f_size:].view(1, -1).expand(G, -1))
+    else:
+        w_out.copy_(w0.view(1, -1).expand(G, -1))
     loss.zero_()
     steps.zero_()
     bad.fill_(-1)
@@ -144,7 +192,8 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     a.ctrl_stride = ctrl_c.stride(0) if ctrl_c is not None else 0
     a.loss_sum, a.steps, a.bad = ptr(loss), ptr(steps), ptr(bad)
     _fill(a, ws, G, BS)
-    if lazy_enabled(terms):
+    handle = None
+    if lazy:
         hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
         lz = _LZ.get(rows, zp, gdt, d)
         hlen_d = torch.from_numpy(hlen).to(d)
@@ -154,10 +203,14 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
         a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
         a.lz_rows = rows
+        a.lz_defer = 1 if defer else 0
+        if defer:
+            handle = LazyFc1(lz, hoff, hlen, rows, BS, lr, w0)
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)
     lib.check(lib.pb_cnn_train_group(ctypes.byref(a), stream_of(w_out)))
+    return handle
 
 
 _EVAL_ORDER: dict = {}

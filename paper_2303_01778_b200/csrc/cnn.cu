@@ -1174,7 +1174,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     if ((rc = launch_sweep(a, active, true, spb, s))) break;
   }
   if (a.hx) {
-    if (!rc) rc = lazy_fc1_materialize(a, int(t.g), s);
+    if (!rc && !t.lz_defer) rc = lazy_fc1_materialize(a, int(t.g), s);
     lazy_fc1_release(a);  // the maps were copied into the launches' parameters
   }
   return rc;

@@ -528,6 +528,104 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
   if (warp == 0) tmem_free<256>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Deferred fold (engine FedAvg rounds): a device partial needs only
+//   sum_j w_j W1_j = (sum_j w_j) W0 - lr * sum_j w_j HD_j^T HX_j
+// over its clients j (contiguous history rows [row_lo, row_hi)), so the
+// per-client fc1 weights are never materialised.
+//   k_lz_scale   hdt columns of client j *= w_j          (HDT is round scratch)
+//   k_lz_fold    split-K GEMM D[o][k] = sum_rows hdt[o][row] hxt[k][row]
+//                -> part[split][512][3136]   grid (13, 4, splits)
+//   k_lz_fold_reduce  acc += wsum * W0 - lr * sum_split part (split order)
+// ---------------------------------------------------------------------------
+__global__ void k_lz_scale(float* __restrict__ hdt, int64_t hrows, const int64_t* __restrict__ hoff,
+                           const int32_t* __restrict__ nrows, const float* __restrict__ w) {
+  const int j = blockIdx.y;
+  const int64_t c0 = hoff[j], n = nrows[j];
+  const float wj = w[j];
+  for (int o = blockIdx.x; o < kH1; o += gridDim.x) {
+    float* row = hdt + int64_t(o) * hrows + c0;
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) row[c] *= wj;
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMaps m, float* part, int row_lo,
+                                                    int chunks_per_split, int chunks_total) {
+  const int q = blockIdx.y, k0 = blockIdx.x * 256, ks = blockIdx.z;
+  const int c0 = ks * chunks_per_split, c1 = min(chunks_total, c0 + chunks_per_split);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) ring_barriers(full, empty, kStages);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0 && c1 > c0) {
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int col = row_lo + (c0 + c) * 32;
+      pb::tma::expect_tx(f, kShStage);
+      pb::tma::load_2d(st, &m.hdt, col, q * 128, f);
+      pb::tma::load_2d(st + kShA, &m.hxt256, col, k0, f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
+      const uint32_t idesc = idesc_tf32(128, 256);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    tma_ring<kStages>(c1 - c0, smem, kShStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
+  const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
+  float* prow = part + (int64_t(ks) * kH1 + o) * kFlat;
+#pragma unroll 1
+  for (int c16 = 0; c16 < 8; ++c16) {
+    const int col = half * 128 + c16 * 16;
+    float v[16];
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col), v);
+    const int kk = k0 + col;
+    if (kk >= kFlat) continue;
+    if (c1 <= c0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    }
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4)
+      *reinterpret_cast<float4*>(prow + kk + 4 * i4) = make_float4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+
+__global__ void k_lz_fold_reduce(float* __restrict__ acc, const float* __restrict__ w0, const float* __restrict__ part,
+                                 int splits, float wsum, float nlr) {
+  constexpr int64_t n4 = int64_t(kH1) * kFlat / 4;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n4; e += int64_t(gridDim.x) * blockDim.x) {
+    float4 g = reinterpret_cast<const float4*>(part)[e];
+    for (int sp = 1; sp < splits; ++sp) {
+      const float4 h = reinterpret_cast<const float4*>(part)[sp * n4 + e];
+      g.x += h.x;
+      g.y += h.y;
+      g.z += h.z;
+      g.w += h.w;
+    }
+    const float4 w = reinterpret_cast<const float4*>(w0)[e];
+    float4 a = reinterpret_cast<float4*>(acc)[e];
+    a.x += fmaf(wsum, w.x, nlr * g.x);
+    a.y += fmaf(wsum, w.y, nlr * g.y);
+    a.z += fmaf(wsum, w.z, nlr * g.z);
+    a.w += fmaf(wsum, w.w, nlr * g.w);
+    reinterpret_cast<float4*>(acc)[e] = a;
+  }
+}
+
 int setup() {
   static int done = 0;
   if (done) return PB_OK;
@@ -539,7 +637,8 @@ int setup() {
                {(const void*)k_lz_gram<false>, kGramBwdSmem, "k_lz_gram<bwd>"},
                {(const void*)k_lz_fwd, kShSmem, "k_lz_fwd"},
                {(const void*)k_lz_bwd, kShSmem, "k_lz_bwd"},
-               {(const void*)k_lz_mat, kShSmem, "k_lz_mat"}};
+               {(const void*)k_lz_mat, kShSmem, "k_lz_mat"},
+               {(const void*)k_lz_fold, kShSmem, "k_lz_fold"}};
   for (auto& x : attrs) {
     cudaError_t e = cudaFuncSetAttribute(x.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(x.bytes));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string(x.name) + ": " + cudaGetErrorString(e));
@@ -635,3 +734,37 @@ int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s) {
 
 }  // namespace cnn
 }  // namespace pb
+
+extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream) {
+  using namespace pb::cnn;
+  if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: null args");
+  const pb_cnn_lazy_fold_args& f = *args;
+  if (!f.acc || !f.w0 || !f.hxt || !f.hdt || !f.hoff || !f.nrows || !f.w || !f.part || f.hrows <= 0 ||
+      f.hrows % 32 || f.nclients < 0 || f.splits < 1 || f.row_lo < 0 || f.row_hi < f.row_lo ||
+      f.row_lo % 32 || f.row_hi > f.hrows || !pb::aligned16(f.acc) || !pb::aligned16(f.w0) ||
+      !pb::aligned16(f.part))
+    return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: bad arguments");
+  if (f.nclients == 0) return PB_OK;
+  int rc = setup();
+  if (rc) return rc;
+  cudaStream_t s = pb::as_stream(stream);
+  LzMaps m{};
+  using pb::tma::make_2d_f32;
+  const uint64_t R = uint64_t(f.hrows);
+  if ((rc = make_2d_f32(&m.hdt, f.hdt, R, kH1, R, 128)) || (rc = make_2d_f32(&m.hxt256, f.hxt, R, kFlat, R, 256)))
+    return rc;
+  pb::prof_begin(pb::K_CNN_LZ_MAT, s);
+  k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(f.hdt, f.hrows, f.hoff, f.nrows, f.w);
+  pb::prof_end(pb::K_CNN_LZ_MAT, s);
+  const int chunks = int((f.row_hi - f.row_lo + 31) / 32);
+  const int per = (chunks + f.splits - 1) / f.splits;
+  pb::prof_begin(pb::K_CNN_LZ_MAT, s);
+  k_lz_fold<<<dim3((kFlat + 255) / 256, kH1 / 128, unsigned(f.splits)), 256, kShSmem, s>>>(
+      m, f.part, int(f.row_lo), per, chunks);
+  pb::prof_end(pb::K_CNN_LZ_MAT, s);
+  pb::prof_begin(pb::K_FOLD_GROUP, s);
+  k_lz_fold_reduce<<<pb::grid_for(int64_t(kH1) * kFlat / 4, 256), 256, 0, s>>>(f.acc, f.w0 + oF1W, f.part,
+                                                                                f.splits, f.wsum, -f.lr);
+  pb::prof_end(pb::K_FOLD_GROUP, s);
+  return pb::check_launch("pb_cnn_lazy_fold");
+}

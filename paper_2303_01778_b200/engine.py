@@ -45,7 +45,7 @@ from .metrics import CostLedger, ReplicaGauge
 from .models import ModelSpec, init_params, spec_for
 from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
 from .statestore import StateStore
-from .trainer import (AggOp, AlgorithmPlugin, ClientData, GroupInputs, ModelParams, NamedParams,
+from .trainer import (AggOp, AlgorithmPlugin, ClientData, FedAvg, GroupInputs, ModelParams, NamedParams,
                       ParamBundle, device, evaluate, finalize_results, io_bytes, spec_of_bundle,
                       train_group)
 
@@ -212,13 +212,20 @@ class DeviceRuntime:
             self.store.gather(clients, work)
         self.gauge.acquire(len(clients))
         try:
+            # FedAvg folds exactly the end models: the CNN's low-rank fc1 can be
+            # folded from the round's history without materialising them
+            defer = spec.kind == "cnn" and type(plugin) is FedAvg
             go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
                              self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
-                             round_num, inputs=inputs)
+                             round_num, inputs=inputs, defer_fc1=defer)
         finally:
             self.gauge.release(len(clients))
         self.last_device_seconds = go.seconds
         groups, new_state = finalize_results(plugin, spec, go, w0, bundle, work)
+        if go.lazy is not None:
+            for g in groups:
+                if g.op is AggOp.WEIGHTED_AVERAGE:
+                    g.lazy = go.lazy
         if plugin.is_stateful and new_state is not None:
             self.store.scatter(clients, round_num, new_state)
         pos = 0

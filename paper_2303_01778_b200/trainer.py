@@ -242,6 +242,7 @@ class GroupOutcome:
     loss_mean: np.ndarray   # mean per-step loss (Collect local_loss)
     w_out: torch.Tensor     # [G, P] end models
     seconds: float          # device time of the training launch
+    lazy: object | None = None  # deferred low-rank fc1 (cnn.LazyFc1): fc1_w rows unmaterialised
 
 
 @dataclass
@@ -254,6 +255,7 @@ class ResultGroup:
     mat: torch.Tensor
     op: AggOp
     weights: np.ndarray
+    lazy: object | None = None  # cnn.LazyFc1 when the fc1_w columns are deferred
 
 
 def spec_groups(spec: ModelSpec, mat: torch.Tensor, op: AggOp, weights, prefix: str = ""):
@@ -314,9 +316,16 @@ class GroupInputs:
 def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                 clients: Sequence[int], w0: torch.Tensor, global_bundle: ParamBundle,
                 state_work: torch.Tensor | None, epochs: int, batch_size: int, lr: float,
-                seed: int, round_num: int, inputs: GroupInputs | None = None) -> GroupOutcome:
-    """Run every listed client's full local schedule concurrently on the GPU."""
+                seed: int, round_num: int, inputs: GroupInputs | None = None,
+                defer_fc1: bool = False) -> GroupOutcome:
+    """Run every listed client's full local schedule concurrently on the GPU.
+
+    defer_fc1 (CNN, plain SGD): leave the clients' fc1_w columns of w_out
+    unmaterialised and return the round's low-rank history instead
+    (``GroupOutcome.lazy``); only valid when the caller folds the group with
+    aggregate.fold_group and reads no per-client fc1 weights."""
     d = device()
+    lazy = None
     if inputs is None:
         inputs = GroupInputs(data, clients, epochs, seed, round_num)
     if [int(c) for c in clients] != inputs.clients:
@@ -346,9 +355,9 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                    cc=terms.get("cc", 0.0))
     elif spec.kind == "cnn":
         from .cnn import cnn_train_group
-        cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
-                        spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
-                        state_work=state_work)
+        lazy = cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
+                               spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
+                               state_work=state_work, defer_fc1=defer_fc1)
     elif spec.kind == "resnet":
         from .resnet import resnet_train_group
         resnet_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
@@ -364,7 +373,9 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     for j in range(G):
         if bad_h[j] >= 0:
             raise NonFiniteLossError(f"client {clients[j]} round {round_num}: loss diverged")
-    return GroupOutcome(clients, n, steps_h, loss_h / np.maximum(steps_h, 1), w_out, seconds)
+    if lazy is not None:
+        lazy.set_steps(steps_h)
+    return GroupOutcome(clients, n, steps_h, loss_h / np.maximum(steps_h, 1), w_out, seconds, lazy)
 
 
 # ---------------------------------------------------------------------------
