@@ -54,7 +54,7 @@ __global__ void k_slots(Args a, int active) {
 // k_fwd: conv1 (SIMT) -> p1 planes -> conv2 (tcgen05) -> relu/pool epilogue
 // grid (ceil(BS/spb), active), 256 threads
 // ---------------------------------------------------------------------------
-constexpr int kFwdThreads = 256;
+constexpr int kFwdThreads = 512;
 constexpr int kZStride = 65;  // padded fp32 row of the conv2 output tile
 constexpr int kRawImg = kImg * kImg * 4;   // 3136 B
 constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg +
@@ -118,19 +118,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
     fence_after_sync();
     const uint32_t th = tmem + uint32_t((j & 1) * 128);
     {
-      const int q = warp & 3, half = warp >> 2;
+      // 16 warps: lane quarter q = warp & 3, 16-column slice warp >> 2
+      const int q = warp & 3, part = warp >> 2;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int row = t * 128 + q * 32 + lane;
         float v[16];
+        tmem_ld16(th + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + part * 16), v);
 #pragma unroll
-        for (int c16 = 0; c16 < 2; ++c16) {
-          tmem_ld16(th + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + half * 32 + c16 * 16), v);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int co = half * 32 + c16 * 16 + k;
-            sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
-          }
+        for (int k = 0; k < 16; ++k) {
+          const int co = part * 16 + k;
+          sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
         }
       }
     }
