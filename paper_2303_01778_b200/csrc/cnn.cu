@@ -741,19 +741,21 @@ constexpr int kInDp2 = 0, kInP2 = kInDp2 + kFlat * 4, kInAm2 = kInP2 + kFlat * 4
               kInBytes = kInP1 + kP1Bytes;   // 59,136 B
 constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kInBytes;
 
+constexpr int kBwdThreads = 512;
+
 __device__ __forceinline__ void stage_bytes(uint8_t* dst, const void* src, int bytes, int tid) {
   const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
-  for (int e = tid * 16; e < bytes; e += 256 * 16) cp_async16(dst + e, s8 + e);
+  for (int e = tid * 16; e < bytes; e += kBwdThreads * 16) cp_async16(dst + e, s8 + e);
 }
 
-__global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
+__global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const Slot sl = a.slots[blockIdx.y];
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
-  __shared__ float sB2[4][64];
+  __shared__ float sB2[kBwdThreads / 64][64];
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
   uint8_t* sIn = sDz + kDzBytes;
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   // after the dgrad MMAs the dz region is reused:
   float* sDp1 = reinterpret_cast<float*>(sDz);           // [196][32] dp1 (25,088 B)
   float* sX = sDp1 + 196 * 32;                           // [32][32] padded image
-  float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp partials (after sync)
+  float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp-pair partials (after sync)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto stage_inputs = [&](int i) {
     const int64_t sid = sidx(blockIdx.y, i, a.BS);
@@ -779,7 +781,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     cp_async_commit();
   };
   stage_inputs(i0);
-  stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, 256);
+  stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, kBwdThreads);
   if (warp == 0) tmem_alloc<64>(&tmem_base);
   if (tid == 0) {
     mbar_init(&mbar, 1);
@@ -793,12 +795,12 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
   uint32_t phase = 0;
   for (int i = i0; i < i1; ++i) {
     const int64_t sid = sidx(blockIdx.y, i, a.BS);
-    for (int e = tid; e < kDzBytes / 16; e += 256)
+    for (int e = tid; e < kDzBytes / 16; e += kBwdThreads)
       reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
     cp_async_wait<0>();
     __syncthreads();
     float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
-    for (int o = tid; o < kFlat; o += 256) {
+    for (int o = tid; o < kFlat; o += kBwdThreads) {
       const int pp = o >> 6, co = o & 63;
       const int py = pp / 7, px = pp - py * 7;
       const int d = iAm2[o];
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     {
       uint4* dst = reinterpret_cast<uint4*>(a.dzg + sid * kDzBytes);
       const uint4* src = reinterpret_cast<const uint4*>(sDz);
-      for (int e = tid; e < kDzBytes / 16; e += 256) dst[e] = src[e];
+      for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) dst[e] = src[e];
     }
     mbar_wait(&mbar, phase);
     phase ^= 1;
@@ -850,7 +852,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
         }
       }
     } else {
-      for (int e = tid - 128; e < 1024; e += 128) {
+      for (int e = tid - 128; e < 1024; e += kBwdThreads - 128) {
         const int yy = e >> 5, xx = e & 31;
         sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? iImg[(yy - 2) * kImg + (xx - 2)] : 0.0f;
       }
@@ -858,14 +860,14 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
     fence_before_sync();
     __syncthreads();
     // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
-    // warp w takes pooled positions w, w+8, ...; 26 accumulators per thread
+    // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
     {
       float acc[25];
 #pragma unroll
       for (int t = 0; t < 25; ++t) acc[t] = 0.0f;
       float bacc = 0.0f;
       const int co = lane;
-      for (int pp = warp; pp < 196; pp += 8) {
+      for (int pp = warp; pp < 196; pp += kBwdThreads / 32) {
         const int py = pp / 14, px = pp - py * 14;
         const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
             iP1 + (co >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (co & 7) * 2));
@@ -880,20 +882,35 @@ __global__ void __launch_bounds__(256, 1) k_bwd_conv(Args a, int spb) {
       }
       __syncthreads();  // all reads of sDp1/sX and the staged inputs done
       if (i + 1 < i1) stage_inputs(i + 1);  // next sample's inputs stream in meanwhile
+      // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
+      // them to their own, then the 8 pair sums are added in warp order
+      if (warp >= 8) {
 #pragma unroll
-      for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] = acc[t];
-      sRed[warp * 832 + 800 + co] = bacc;
+        for (int t = 0; t < 25; ++t) sRed[(warp - 8) * 832 + co * 25 + t] = acc[t];
+        sRed[(warp - 8) * 832 + 800 + co] = bacc;
+      }
+      __syncthreads();
+      if (warp < 8) {
+#pragma unroll
+        for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] += acc[t];
+        sRed[warp * 832 + 800 + co] += bacc;
+      }
     }
     __syncthreads();
     {
       float* pg = a.pg + sid * kPg;
-      for (int k = tid; k < 832; k += 256) {
+      for (int k = tid; k < 832; k += kBwdThreads) {
         float s8 = 0.0f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s8 += sRed[w * 832 + k];
         pg[k] = s8;
       }
-      if (tid < 64) pg[832 + tid] = ((sB2[0][tid] + sB2[1][tid]) + sB2[2][tid]) + sB2[3][tid];
+      if (tid < 64) {
+        float b = 0.0f;
+#pragma unroll
+        for (int q = 0; q < kBwdThreads / 64; ++q) b += sB2[q][tid];
+        pg[832 + tid] = b;
+      }
     }
     __syncthreads();
   }
@@ -1129,7 +1146,7 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::prof_end(pb::K_CNN_FC1_BWD, s);
   }
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
-  k_bwd_conv<<<dim3(BSpb, active), 256, kBwdSmem, s>>>(a, spb);
+  k_bwd_conv<<<dim3(BSpb, active), kBwdThreads, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
   k_wgrad<<<dim3(kWgSplit + 1, active), 256, kWgSmem, s>>>(a);
