@@ -402,35 +402,54 @@ struct GnF {
 };
 
 constexpr int kGnThreads = 512;
-constexpr size_t kGnSmem = 4 * 1024 * sizeof(double);   // per-thread partials (2 sums x 2 tensors)
+constexpr size_t kGnSmem = 5 * 1024 * sizeof(double);   // per-thread partials + per-channel sums
 
-// per-channel sums of f(p, c) and g(p, c) over positions, combined in part
-// order into r1[c], r2[c] (double); C <= 512
-template <class F, class G>
+// Per-channel sums of two quantities over positions, 4 channels per thread
+// (float4 loads): thread t owns channel group (t % (C/4)) and every
+// (512 / (C/4))-th position, two independent chains; the per-thread partials
+// are combined in part order into r1[c], r2[c] (double).  f(p, c0, u, v)
+// fills u[0..3], v[0..3] for channels c0..c0+3 at position p.  C <= 512.
+template <class F>
 __device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* part2, double* r1,
-                                          double* r2, F f, G g) {
-  const int tid = threadIdx.x, tpc = kGnThreads / C;  // C <= 512 -> tpc >= 1
-  const int c = tid & (C - 1), pt = tid / C;
-  double a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
+                                          double* r2, F f) {
+  const int tid = threadIdx.x, C4 = C >> 2, tpc = kGnThreads / C4;  // C4 <= 128 -> tpc >= 4
+  const int cg = tid & (C4 - 1), pt = tid / C4, c0 = cg * 4;
+  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+  double a2[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
   int p = pt;
-  for (; p + tpc < HW; p += 2 * tpc) {  // two independent chains
-    a1 += f(p, c);
-    a2 += g(p, c);
-    b1 += f(p + tpc, c);
-    b2 += g(p + tpc, c);
+  for (; p + tpc < HW; p += 2 * tpc) {
+    float u[4], v[4], x[4], y[4];
+    f(p, c0, u, v);
+    f(p + tpc, c0, x, y);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[j] += u[j];
+      b[j] += v[j];
+      a2[j] += x[j];
+      b2[j] += y[j];
+    }
   }
   if (p < HW) {
-    a1 += f(p, c);
-    a2 += g(p, c);
+    float u[4], v[4];
+    f(p, c0, u, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[j] += u[j];
+      b[j] += v[j];
+    }
   }
-  part1[tid] = a1 + b1;
-  part2[tid] = a2 + b2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    part1[tid * 4 + j] = a[j] + a2[j];
+    part2[tid * 4 + j] = b[j] + b2[j];
+  }
   __syncthreads();
   for (int cc = tid; cc < C; cc += kGnThreads) {
+    const int g = cc >> 2, j = cc & 3;
     double t1 = 0.0, t2 = 0.0;
     for (int q = 0; q < tpc; ++q) {
-      t1 += part1[q * C + cc];
-      t2 += part2[q * C + cc];
+      t1 += part1[(q * C4 + g) * 4 + j];
+      t2 += part2[(q * C4 + g) * 4 + j];
     }
     r1[cc] = t1;
     r2[cc] = t2;
@@ -464,28 +483,27 @@ __global__ void __launch_bounds__(kGnThreads) k_rn_gn_fwd(Net a, GnF f) {
   if (i >= sl.cnt) return;
   extern __shared__ double dsm[];
   double* p1 = dsm;
-  double* p2 = dsm + kGnThreads;
-  double* r1 = dsm + 2 * kGnThreads;
+  double* p2 = dsm + 4 * kGnThreads;
+  double* r1 = dsm + 8 * kGnThreads;
   double* r2 = r1 + 512;
   const int C = f.C, HW = f.HW, cshift = __ffs(C / kGroups) - 1;
   const int64_t base = int64_t(i) * HW * C;
   const float* z = at<float>(a, s, f.z) + base;
   const float* W = a.w + int64_t(sl.r) * a.P;
   float mean[kGroups], rstd[kGroups], mean2[kGroups], rstd2[kGroups];
-  chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c) { return double(z[p * C + c]); },
-            [&](int p, int c) {
-              const double v = z[p * C + c];
-              return v * v;
-            });
+  auto sq = [&](const float* t) {
+    return [t, C](int p, int c0, float* u, float* v) {
+      const float4 x = *reinterpret_cast<const float4*>(t + p * C + c0);
+      u[0] = x.x, u[1] = x.y, u[2] = x.z, u[3] = x.w;
+      v[0] = x.x * x.x, v[1] = x.y * x.y, v[2] = x.z * x.z, v[3] = x.w * x.w;
+    };
+  };
+  chan_sums(C, HW, p1, p2, r1, r2, sq(z));
   gn_moments(C, HW, r1, r2, mean, rstd);
   __syncthreads();
   const float* z2 = f.z2 >= 0 ? at<float>(a, s, f.z2) + base : nullptr;
   if (z2) {
-    chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c) { return double(z2[p * C + c]); },
-              [&](int p, int c) {
-                const double v = z2[p * C + c];
-                return v * v;
-              });
+    chan_sums(C, HW, p1, p2, r1, r2, sq(z2));
     gn_moments(C, HW, r1, r2, mean2, rstd2);
   }
   if (threadIdx.x == 0) {
@@ -549,8 +567,8 @@ struct GnB {
 __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float* G, int64_t z_off,
                            int64_t st_off, int64_t gam_off, int64_t dz_off, int64_t pg_off, double* dsm) {
   double* p1 = dsm;
-  double* p2 = dsm + kGnThreads;
-  double* r1 = dsm + 2 * kGnThreads;
+  double* p2 = dsm + 4 * kGnThreads;
+  double* r1 = dsm + 8 * kGnThreads;
   double* r2 = r1 + 512;
   const int C = f.C, HW = f.HW, cg = C / kGroups, cshift = __ffs(cg) - 1;
   const int64_t base = int64_t(i) * HW * C;
@@ -564,11 +582,16 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float
     rstd[g] = st[2 * g + 1];
   }
   // per channel: dbeta = sum G, dgamma = sum G * xhat
-  chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c) { return double(G[p * C + c]); },
-            [&](int p, int c) {
-              const int g = c >> cshift;
-              return double(G[p * C + c]) * double((z[p * C + c] - mean[g]) * rstd[g]);
-            });
+  chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c0, float* u, float* v) {
+    const float4 gv = *reinterpret_cast<const float4*>(G + p * C + c0);
+    const float4 zv = *reinterpret_cast<const float4*>(z + p * C + c0);
+    const int g = c0 >> cshift;
+    u[0] = gv.x, u[1] = gv.y, u[2] = gv.z, u[3] = gv.w;
+    v[0] = gv.x * ((zv.x - mean[g]) * rstd[g]);
+    v[1] = gv.y * ((zv.y - mean[g]) * rstd[g]);
+    v[2] = gv.z * ((zv.z - mean[g]) * rstd[g]);
+    v[3] = gv.w * ((zv.w - mean[g]) * rstd[g]);
+  });
   float* pg = a.gnp + int64_t(s) * a.gnp_slot + pg_off + int64_t(i) * 2 * C;
   for (int c = threadIdx.x; c < C; c += kGnThreads) {
     pg[c] = float(r2[c]);      // dgamma partial of sample i
