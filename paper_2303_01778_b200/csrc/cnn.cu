@@ -369,13 +369,22 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) wr[k] = wc[lane + 32 * k];
     const float bc = b2[c];
-    for (int i = 0; i < cnt; ++i) {
-      const float* hr = sH + i * kH1;
-      float s = 0.0f;
+    // 4 samples per pass: independent FMA / shuffle chains (each dot product
+    // keeps its own summation order)
+    for (int i0 = 0; i0 < cnt; i0 += 4) {
+      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int k = 0; k < 16; ++k) s = fmaf(hr[lane + 32 * k], wr[k], s);
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) sL[i * C + c] = s + bc;
+      for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q < cnt) s[q] = fmaf(sH[(i0 + q) * kH1 + lane + 32 * k], wr[k], s[q]);
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], off);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q < cnt) sL[(i0 + q) * C + c] = s[q] + bc;
     }
   }
   __syncthreads();
