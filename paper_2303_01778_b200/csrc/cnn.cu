@@ -344,8 +344,13 @@ __device__ double block_sum_d(double v, double* scratch) {
   return t;
 }
 
+// grid (parts, active): part p owns fc1 outputs [p*512/parts, (p+1)*512/parts)
+// (tail sweeps split a client over 4 CTAs; logits and softmax are recomputed
+// by each part, the bookkeeping and the fc2 bias belong to part 0)
 __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
-  const Slot sl = a.slots[blockIdx.x];
+  const int slot = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
+  const int olo = part * (kH1 / parts), ohi = olo + kH1 / parts;
+  const Slot sl = a.slots[slot];
   if (sl.cnt == 0) return;
   extern __shared__ float hs[];
   const int C = a.C, cnt = sl.cnt, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
   const float* W2 = W + oF2W;          // [C][512], read from L2 (coalesced rows)
-  const float* hrow = a.h + sidx(blockIdx.x, 0, a.BS) * kH1;
+  const float* hrow = a.h + sidx(slot, 0, a.BS) * kH1;
 #pragma unroll 8
   for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
   __syncthreads();
@@ -411,7 +416,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   const double lsum = block_sum_d(lpart, scratch);
   if (a.eval) {
     const double csum = block_sum_d(cpart, scratch);
-    if (tid == 0) {
+    if (tid == 0 && part == 0) {
       atomicAdd(a.eval, csum);
       atomicAdd(a.eval + 1, lsum);
     }
@@ -420,7 +425,8 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   if (tid == 0) {
     const double loss = lsum / double(cnt);
     s_bad = !isfinite(loss);
-    if (s_bad) {
+    if (part != 0) {
+    } else if (s_bad) {
       a.bad[sl.r] = a.steps[sl.r];
     } else {
       a.loss_sum[sl.r] += loss;
@@ -429,16 +435,16 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   }
   __syncthreads();
   if (s_bad) {
-    a.slots[blockIdx.x].cnt = 0;  // later kernels of this sweep skip the client
+    if (part == 0 && tid == 0) a.slots[slot].cnt = 0;  // later kernels of this sweep skip the client
     return;
   }
   // dH = dlogits W2 (old weights) masked by relu'; stored [i][o] and [o][i<32]
   // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
   const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
-  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(blockIdx.x, 0, a.BS) * kH1;
+  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(slot, 0, a.BS) * kH1;
   // one pass over W2 per output o (thread-owned column): dH[i][o] from the
   // old W2[c][o], then the fc2 update of that element (fused; sample order)
-  for (int o = tid; o < kH1; o += kHeadThreads) {
+  for (int o = olo + tid; o < ohi; o += kHeadThreads) {
     float hreg[32], acc[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -482,24 +488,24 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   if (a.hx) {
     // dH^T columns of the global [512][hrows] history (row pitch hrows)
     float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
-    for (int p = tid; p < cnt * kH1; p += kHeadThreads) {
-      const int o = p / cnt, i = p - o * cnt;
+    for (int p = tid; p < cnt * (ohi - olo); p += kHeadThreads) {
+      const int o = olo + p / cnt, i = p - (o - olo) * cnt;
       hdt[int64_t(o) * a.hrows + i] = sDH[i * kH1 + o];
     }
-    for (int o = tid; o < kH1; o += kHeadThreads) {  // fc1 bias (sample order)
+    for (int o = olo + tid; o < ohi; o += kHeadThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
       const int64_t idx = oF1B + o;
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
   } else {
-    float* dht = a.dht + int64_t(blockIdx.x) * kH1 * 32;
-    for (int p = tid; p < kH1 * 32; p += kHeadThreads) {
+    float* dht = a.dht + int64_t(slot) * kH1 * 32;
+    for (int p = olo * 32 + tid; p < ohi * 32; p += kHeadThreads) {
       const int o = p >> 5, i = p & 31;
       dht[p] = i < cnt ? sDH[i * kH1 + o] : 0.0f;
     }
   }
-  for (int c = tid; c < C; c += kHeadThreads) {
+  for (int c = tid; c < (part == 0 ? C : 0); c += kHeadThreads) {
     float g = 0.0f;
     for (int i = 0; i < cnt; ++i) g += sL[i * C + c];
     const int64_t idx = oF2W + int64_t(C) * kH1 + c;
@@ -938,7 +944,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
 constexpr int kWgP1 = 2 * kP1Bytes;             // 8 planes: shift 0, shift 1
 constexpr int kWgBuf = kWgP1 + kDzBytes;        // 86,016 B
 constexpr size_t kWgSmem = 2 * kWgBuf;          // double-buffered
-constexpr int kWgSplit = 2;                     // CTA 0: ky 0-2 (15 taps), CTA 1: ky 3-4 (10 taps)
+// filter rows per CTA: head sweeps 2 CTAs (ky 0-2 | 3-4); tail sweeps (few
+// clients) one CTA per ky row, so each client's MMA chain is 5x shorter
+constexpr int kWgTailActive = 60;
 constexpr int kWgStride = 15 * 32 + 1;          // fp32 row of the gradient tile (epilogue)
 
 __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* buf, int tid) {
@@ -953,13 +961,13 @@ __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* bu
   cp_async_commit();
 }
 
-// k_wgrad: x < 2: conv2 wgrad for the taps of rows ky in [3x, 3x + 3 - x) on
+// k_wgrad: x < nsplit: conv2 wgrad for the taps of its filter rows ky on
 //          tcgen05 (M=64 co x N=64 (two taps x 32 ci) / N=32 (kx = 4), K =
 //          output positions; double-buffered sample staging overlaps the
 //          MMAs) + update;
-//          x == 2: sum the per-sample conv1/bias partials (sample order) + update
-// grid (3, active), 256 threads
-__global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
+//          x == nsplit: sum the per-sample conv1/bias partials (sample order) + update
+// grid (nsplit + 1, active), 256 threads; nsplit = 2 (ky 0-2 | 3-4) or 5
+__global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
   const Slot sl = a.slots[blockIdx.y];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -969,7 +977,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
   const int cnt = sl.cnt;
   float* W = a.w + int64_t(sl.r) * a.P;
   const int64_t s0 = sidx(blockIdx.y, 0, a.BS);
-  if (blockIdx.x == kWgSplit) {
+  if (blockIdx.x == nsplit) {
     for (int k = tid; k < kPg; k += 256) {
       float g = 0.0f;
 #pragma unroll 8
@@ -979,7 +987,8 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a) {
     }
     return;
   }
-  const int ky0 = blockIdx.x * 3, nky = blockIdx.x == 0 ? 3 : 2;
+  const int ky0 = nsplit == 2 ? blockIdx.x * 3 : blockIdx.x;
+  const int nky = nsplit == 2 ? (blockIdx.x == 0 ? 3 : 2) : 1;
   const int tap0 = ky0 * 5, ntap = nky * 5;
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -1142,7 +1151,8 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::prof_end(pb::K_CNN_FC1_FWD, s);
   }
   pb::prof_begin(pb::K_CNN_HEAD, s);
-  k_head<<<active, kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+  const int hparts = active < kWgTailActive ? 4 : 1;
+  k_head<<<dim3(hparts, active), kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
   if (a.hx) {
@@ -1158,7 +1168,8 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   k_bwd_conv<<<dim3(BSpb, active), kBwdThreads, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
-  k_wgrad<<<dim3(kWgSplit + 1, active), 256, kWgSmem, s>>>(a);
+  const int wsplit = active < kWgTailActive ? 5 : 2;
+  k_wgrad<<<dim3(wsplit + 1, active), 256, kWgSmem, s>>>(a, wsplit);
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
 }
