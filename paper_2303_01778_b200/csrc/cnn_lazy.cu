@@ -137,10 +137,10 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 // zeroed when the Gram tile leaves TMEM.
 // grid (njt, active), 128 threads
 // ---------------------------------------------------------------------------
-constexpr int kGrA = 128 * 128;                // 16 KB: 128 rows x 32 fp32
+constexpr int kGrA = 128 * 128;                // 16 KB: 128 rows x 32 fp32 (one K atom)
 constexpr int kGrB = 32 * 128;                 // 4 KB
-constexpr int kGrStage = kGrA + kGrB;          // 20 KB
-constexpr int kGrStages = 8;
+constexpr int kGrStage = 2 * (kGrA + kGrB);    // 40 KB: two K atoms per stage
+constexpr int kGrStages = 5;
 constexpr int kGxT = 4 * 32 * 128;             // Gx^T: 4 K-atoms of [32 i][32 j], 16 KB
 constexpr size_t kGramFwdSmem = 1024 + kGrStages * kGrStage + kGxT;
 constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = a.step, jlim = t * a.BS, j0 = jt * 128, njt = njt_of(a);
-  constexpr int nA = (FWD ? kFlat : kH1) / 32;   // 98 | 16
+  constexpr int nA = (FWD ? kFlat : kH1) / 64;   // 49 | 8 stages of two K atoms
   const int hrow = int(sl.hist) + j0, crow = int(sl.hist + int64_t(t) * a.BS);
   uint8_t* sGxT = smem + kGrStages * kGrStage;
   if (warp == 0) tmem_alloc<FWD ? 256 : 32>(&tmem_base);
@@ -174,15 +174,23 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   if (tid == 0) {
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, kGrStage);
-      pb::tma::load_2d(st, ta, c * 32, hrow, f);
-      pb::tma::load_2d(st + kGrA, tb, c * 32, crow, f);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint8_t* sh = st + h * (kGrA + kGrB);
+        pb::tma::load_2d(sh, ta, (2 * c + h) * 32, hrow, f);
+        pb::tma::load_2d(sh + kGrA, tb, (2 * c + h) * 32, crow, f);
+      }
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kGrA));
       const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sh = smem_u32(st + h * (kGrA + kGrB));
+        const uint64_t a0 = desc_sw128(sh), b0 = desc_sw128(sh + kGrA);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
+      }
     };
     tma_ring<kGrStages>(nA, smem, kGrStage, full, empty, issue, mma);
   }
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const int t = a.step, jlim = t * a.BS;
-  const int nj = (jlim + 31) >> 5;               // phase-2 chunks per slot
+  const int nj = (jlim + 63) >> 6;               // phase-2 stages per slot (two K atoms each)
   const int64_t tb = int64_t(t) * a.BS;
   constexpr int n1 = kH1 / 32;                   // 16
   if (tid == 0) {
@@ -422,9 +430,12 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
           if (sS[u].cnt > 0) pb::tma::load_2d(st + kShA + u * 32 * 128, &m.hdb, c * 32, rows[u], f);
       } else {
         const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
-        pb::tma::expect_tx(f, uint32_t(kShA + 32 * 128));
-        pb::tma::load_2d(st, &m.hxt128, int(sS[u].hist) + jc * 32, k0, f);
-        pb::tma::load_2d(st + kShA, &m.gdt, jc * 32, (g0 + u) * 32, f);
+        pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pb::tma::load_2d(st + h * kShA, &m.hxt128, int(sS[u].hist) + (2 * jc + h) * 32, k0, f);
+          pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.gdt, (2 * jc + h) * 32, (g0 + u) * 32, f);
+        }
       }
     };
     auto mma = [&](int c, uint8_t* st) {
@@ -438,8 +449,13 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         const int u = us[(c - n1) / nj];
         const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(tmem + u * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, true);
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t ah = desc_sw128(smem_u32(st + h * kShA));
+          const uint64_t bh = desc_sw128(smem_u32(st + 2 * kShA + h * 32 * 128));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_tf32(tmem + u * 32, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+        }
       }
     };
     tma_ring<kStages>(n, smem, kShStage, full, empty, issue, mma);
