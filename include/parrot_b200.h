@@ -321,6 +321,10 @@ int pb_umma_tf32_probe(const float* A, const float* B, float* D, const int* para
 int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, int naccum, long long* cycles,
                   void* stream);
 
+/* The same issue loop on `grid` CTAs at once (several per SM): per-CTA
+ * elapsed cycles and SM ids (device pointers; tests / DESIGN table only). */
+int pb_umma_bench_multi(int M, int N, int iters, int grid, long long* cycles, int* smid, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,7 @@ _SIGS = {
     "pb_cnn_train_group": (c_int, [POINTER(CnnTrainArgs), c_void_p]),
     "pb_cnn_lazy_fold": (c_int, [POINTER(LazyFoldArgs), c_void_p]),
     "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
+    "pb_umma_bench_multi": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "pb_tma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "pb_rn_conv_selftest": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -111,7 +111,8 @@ extern "C" int pb_umma_selftest(const void* A, const void* B, float* D, int M, i
 // ---------------------------------------------------------------------------
 namespace {
 __global__ void __launch_bounds__(128) umma_bench_kernel(int M, int N, int a_mode, int b_mode,
-                                                         int iters, int naccum, long long* cycles) {
+                                                         int iters, int naccum, long long* cycles,
+                                                         int* smid = nullptr) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
@@ -156,7 +157,12 @@ __global__ void __launch_bounds__(128) umma_bench_kernel(int M, int N, int a_mod
     }
     commit(&mbar);
     mbar_wait(&mbar, 0);
-    cycles[0] = clock64() - t0;
+    cycles[blockIdx.x] = clock64() - t0;
+    if (smid) {
+      uint32_t id;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+      smid[blockIdx.x] = int(id);
+    }
   }
   __syncthreads();
   if (tid != 0) mbar_wait(&mbar, 0);
@@ -174,6 +180,18 @@ extern "C" int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, in
   umma_bench_kernel<<<1, 128, smem, pb::as_stream(stream)>>>(M, N, a_mode, b_mode, iters, naccum,
                                                              cycles);
   return pb::check_launch("pb_umma_bench");
+}
+
+// Same issue loop on `grid` CTAs at once (K-major operands, one accumulator)
+// so that several CTAs share an SM: cycles[b], smid[b] per CTA.  Measures
+// whether the small-N tcgen05 issue floor is per CTA or per SM (tests only).
+extern "C" int pb_umma_bench_multi(int M, int N, int iters, int grid, long long* cycles, int* smid,
+                                   void* stream) {
+  if (grid < 1 || N > 256) return pb::fail(PB_ERR_INVALID, "pb_umma_bench_multi: bad arguments");
+  const size_t smem = size_t(M + 8 + N + 8) * 64 * 2;
+  cudaFuncSetAttribute(umma_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  umma_bench_kernel<<<grid, 128, smem, pb::as_stream(stream)>>>(M, N, 2, 1, iters, 1, cycles, smid);
+  return pb::check_launch("pb_umma_bench_multi");
 }
 
 // ---------------------------------------------------------------------------
