@@ -35,6 +35,9 @@ namespace {
 using namespace pb::umma;
 using namespace pb::cnn;
 using pb::tma::desc_sw128;
+using pb::tma::align1k;
+using pb::tma::ring_barriers;
+using pb::tma::tma_ring;
 
 constexpr int kStages = 4;
 
@@ -54,42 +57,6 @@ struct LzMaps {
 
 inline int njt_of_host(int step, int BS) { return (step * BS + 127) >> 7; }
 __device__ __forceinline__ int njt_of(const Args& a) { return (a.step * a.BS + 127) >> 7; }
-
-__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
-}
-
-// Single-thread TMA -> MMA ring over n chunks (call from ONE thread).
-// issue(c, stage, full) issues chunk c's TMA loads and its expect_tx on
-// `full`; mma(c, stage) issues its MMAs, then the ring commits them to
-// empty[stage] and refills the stage of chunk c-1 (S-1 chunks in flight).
-template <int S, class Issue, class Mma>
-__device__ __forceinline__ void tma_ring(int n, uint8_t* ring, int stage_bytes, uint64_t* full, uint64_t* empty,
-                                         Issue issue, Mma mma) {
-  for (int c = 0; c < n && c < S; ++c) issue(c, ring + c * stage_bytes, &full[c]);
-  for (int c = 0; c < n; ++c) {
-    const int st = c % S;
-    mbar_wait(&full[st], (c / S) & 1);
-    fence_after_sync();
-    mma(c, ring + st * stage_bytes);
-    commit(&empty[st]);
-    const int nx = c - 1 + S;
-    if (c >= 1 && nx < n) {
-      const int s2 = (c - 1) % S;
-      mbar_wait(&empty[s2], ((c - 1) / S) & 1);   // chunk c-1's MMAs released the stage
-      issue(nx, ring + s2 * stage_bytes, &full[s2]);
-    }
-  }
-  if (n > 0) mbar_wait(&empty[(n - 1) % S], ((n - 1) / S) & 1);
-}
-
-__device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, int S) {
-  for (int i = 0; i < S; ++i) {
-    mbar_init(&full[i], 1);
-    mbar_init(&empty[i], 1);
-  }
-  fence_init();
-}
 
 // ---------------------------------------------------------------------------
 // k_lz_w0t: w0t[k][o] = w0[fc1][o][k]  (once per round)

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "umma.cuh"
 
 namespace {
@@ -329,6 +330,77 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv(Net a, ConvK k, int ntile) {
 #pragma unroll
         for (int i4 = 0; i4 < 4; ++i4) d4[i4] = make_float4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
       }
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// k_rn_conv_fwd_tma: the forward implicit GEMM of stride-1 convolutions with
+// 64-channel blocks, every operand tile one TMA box.  An M tile of 128
+// output positions is whole output rows (Wo x Ht x Nt samples), so the A tile
+// of filter tap (r, s) and channel block cb is ONE 5-D box of the NHWC input
+// (64 ch x Wo x Ht x Nt x 1 slot) at coordinates shifted by (s - pad, r - pad):
+// out-of-bounds elements are zero-filled by the TMA unit, which IS the
+// convolution padding.  B is one 3-D box (64 K x ntile co x 1 client) of the
+// client's bf16 weights.  SWIZZLE_128B K-major tiles, one thread drives the
+// TMA -> MMA ring.  grid (M tiles, Cout / ntile, slots), 256 threads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) k_rn_conv_fwd_tma(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
+                                                            int ntile, int Ht, int Nt) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int s = blockIdx.z;
+  const Slot sl = a.slots[s];
+  const int cnt = sl.cnt;
+  if (cnt == 0) return;
+  const int HWo = k.Ho * k.Wo, M = cnt * HWo;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * ntile;
+  if (m0 >= M) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = pb::tma::align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t tmem_base;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) pb::tma::ring_barriers(full, empty, kStages);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const int nn = m0 / HWo, p0 = Nt > 1 ? 0 : (m0 - nn * HWo) / k.Wo;
+    const int ncb = k.Cinp / 64, n = k.R * k.R * ncb;
+    const uint32_t bytes = 128 * 128 + uint32_t(ntile) * 128;
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int rs = c / ncb, cb = c - rs * ncb, r = rs / k.R, q = rs - r * k.R;
+      pb::tma::expect_tx(f, bytes);
+      pb::tma::load_5d(st, &ta, cb * 64, q - k.pad, p0 + r - k.pad, nn, s, f);
+      pb::tma::load_3d(st + 128 * 128, &tb, rs * k.Cinp + cb * 64, n0, sl.r, f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = pb::tma::desc_sw128(smem_u32(st)), b0 = pb::tma::desc_sw128(smem_u32(st + 128 * 128));
+      const uint32_t idesc = idesc_bf16(128, ntile);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
+  const int row = (warp & 3) * 32 + lane, m = m0 + row;
+  const int half = warp >> 2, cols = ntile / 2;
+  float* dst = at<float>(a, s, k.z) + int64_t(m) * k.Cout + n0;
+#pragma unroll 1
+  for (int c16 = 0; c16 < cols; c16 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(half * cols + c16), v);
+    if (m < M) {
+      float4* d4 = reinterpret_cast<float4*>(dst + half * cols + c16);
+#pragma unroll
+      for (int i4 = 0; i4 < 4; ++i4) d4[i4] = make_float4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3]);
     }
   }
   fence_before_sync();
@@ -813,6 +885,8 @@ __global__ void __launch_bounds__(256) k_rn_head(Net a, int64_t act, int64_t gou
 namespace {
 
 struct ConvL {
+  CUtensorMap ta, tb;  // TMA maps of the forward implicit GEMM (tma != 0)
+  int tma, Ht, Nt;
   ConvK k;
   int Cin;           // master input channels (3 for the stem conv)
   int64_t w_off;     // fp32 master offset
@@ -928,9 +1002,41 @@ int conv_ntile(int n) { return n >= 256 ? 256 : n; }
 
 size_t gn_smem() { return kGnSmem; }
 
+// TMA maps for the stride-1, 64-channel-block forward convolutions: the
+// NHWC input over every slot (5-D) and each client's bf16 weights (3-D)
+int build_maps(Plan& pl, const Net& a, int64_t slots) {
+  for (ConvL& c : pl.convs) {
+    const ConvK& k = c.k;
+    c.tma = 0;
+    if (k.stride != 1 || k.Cinp % 64 || 128 % k.Wo) continue;
+    c.Ht = std::min(k.Ho, 128 / k.Wo);
+    c.Nt = 128 / (k.Wo * c.Ht);
+    const uint64_t da[5] = {uint64_t(k.Cinp), uint64_t(k.W), uint64_t(k.H), uint64_t(a.BS), uint64_t(slots)};
+    const uint64_t sa[4] = {uint64_t(k.Cinp) * 2, uint64_t(k.W) * k.Cinp * 2, uint64_t(k.H) * k.W * k.Cinp * 2,
+                            uint64_t(a.slot_bytes)};
+    const uint32_t ba[5] = {64, uint32_t(k.Wo), uint32_t(c.Ht), uint32_t(c.Nt), 1};
+    const uint64_t K = uint64_t(k.R) * k.R * k.Cinp;
+    const uint64_t db[3] = {K, uint64_t(k.Cout), uint64_t(slots)};
+    const uint64_t sb[2] = {K * 2, uint64_t(a.P16) * 2};
+    const uint32_t bb[3] = {64, uint32_t(conv_ntile(k.Cout)), 1};
+    int rc;
+    if ((rc = pb::tma::make_nd_bf16(&c.ta, a.arena + k.in, 5, da, sa, ba)) ||
+        (rc = pb::tma::make_nd_bf16(&c.tb, a.w16 + k.w16_off, 3, db, sb, bb)))
+      return rc;
+    c.tma = 1;
+  }
+  return PB_OK;
+}
+
 void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_t s) {
   const ConvK& k = c.k;
-  if (mode == FWD) {
+  if (mode == FWD && c.tma) {
+    const int nt = conv_ntile(k.Cout);
+    const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
+    pb::prof_begin(pb::K_RN_CONV_FWD, s);
+    k_rn_conv_fwd_tma<<<g, 256, kCvSmem + 1024, s>>>(c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
+    pb::prof_end(pb::K_RN_CONV_FWD, s);
+  } else if (mode == FWD) {
     const int nt = conv_ntile(k.Cout);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
@@ -1084,9 +1190,10 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
 int setup() {
   static int done = 0;
   if (done) return PB_OK;
-  const void* fns[] = {(const void*)k_rn_conv<FWD>, (const void*)k_rn_conv<DGRAD>, (const void*)k_rn_conv<WGRAD>};
+  const void* fns[] = {(const void*)k_rn_conv<FWD>, (const void*)k_rn_conv<DGRAD>, (const void*)k_rn_conv<WGRAD>,
+                       (const void*)k_rn_conv_fwd_tma};
   for (const void* fn : fns) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem));
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem + 1024));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_conv: ") + cudaGetErrorString(e));
   }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_rn_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1131,13 +1238,14 @@ extern "C" int pb_resnet_train_group(const pb_resnet_train_args* args, void* str
   if (t.g < 0 || t.C < 2 || t.C > 128 || t.BS < 1 || t.BS > kMaxBS || t.epochs < 1 || !t.w || !t.active ||
       t.sweeps < 0 || t.w_stride % 4 != 0)
     return pb::fail(PB_ERR_INVALID, "pb_resnet_train_group: bad arguments");
-  const Plan pl = make_plan(t.BS, t.C);
+  Plan pl = make_plan(t.BS, t.C);
   if (t.w_stride < pl.P) return pb::fail(PB_ERR_INVALID, "pb_resnet_train_group: w_stride < model size");
   if (t.g == 0 || t.sweeps == 0) return PB_OK;
   int rc = setup();
   if (rc) return rc;
   Net a = to_net(t, pl);
   cudaStream_t s = pb::as_stream(stream);
+  if ((rc = build_maps(pl, a, t.g))) return rc;
   if ((rc = refresh_w16(a, pl, int(t.g), s))) return rc;
   for (int step = 0; step < t.sweeps; ++step) {
     const int active = t.active[step];
@@ -1156,12 +1264,13 @@ extern "C" int pb_resnet_eval(const pb_resnet_train_args* args, int64_t rows, do
   if (!args || !out2 || rows < 0) return pb::fail(PB_ERR_INVALID, "pb_resnet_eval: bad arguments");
   const pb_resnet_train_args& t = *args;
   if (rows == 0) return PB_OK;
-  const Plan pl = make_plan(t.BS, t.C);
+  Plan pl = make_plan(t.BS, t.C);
   int rc = setup();
   if (rc) return rc;
   Net a = to_net(t, pl);
   a.eval = out2;
   cudaStream_t s = pb::as_stream(stream);
+  if ((rc = build_maps(pl, a, t.g))) return rc;
   if ((rc = refresh_w16(a, pl, 1, s))) return rc;
   const int64_t nslots = (rows + t.BS - 1) / t.BS;
   const int64_t cap = t.g;  // workspace capacity in slots
@@ -1217,14 +1326,20 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
   if (dz) cudaMemcpyAsync(arena + k.dz, dz, size_t(dzb), cudaMemcpyDeviceToDevice, s);
   Net a{};
   a.arena = arena; a.slot_bytes = arena_bytes; a.slots = slot;
-  a.w16 = reinterpret_cast<bf16*>(const_cast<void*>(w)); a.P16 = 0;
+  a.w16 = reinterpret_cast<bf16*>(const_cast<void*>(w)); a.P16 = (int64_t(Cout) * R * R * Cinp + 7) / 8 * 8;
   a.part = part; a.part_slot = k.nsplit * M * Cout;
   a.BS = BS;
   ConvL c{};
   c.k = k;
   if (mode == 0) {
     const int nt = conv_ntile(Cout);
-    k_rn_conv<FWD><<<dim3((BS * Ho * Ho + 127) / 128, Cout / nt, 1), 256, kCvSmem, s>>>(a, k, nt);
+    Plan pl;
+    pl.convs.push_back(c);
+    if ((rc = build_maps(pl, a, 1))) return rc;
+    if (pl.convs[0].tma)   // the network's path for stride-1 64-channel-block layers
+      launch_conv(a, pl.convs[0], FWD, 1, s);
+    else
+      k_rn_conv<FWD><<<dim3((BS * Ho * Ho + 127) / 128, Cout / nt, 1), 256, kCvSmem, s>>>(a, k, nt);
     cudaMemcpyAsync(out, arena + k.z, size_t(cnt) * Ho * Ho * Cout * 4, cudaMemcpyDeviceToDevice, s);
   } else if (mode == 1) {
     const int nt = conv_ntile(Cinp);

@@ -42,6 +42,23 @@ __device__ __forceinline__ void load_2d(void* dst, const CUtensorMap* map, int c
       : "memory");
 }
 
+__device__ __forceinline__ void load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          umma::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(umma::smem_u32(mbar))
+      : "memory");
+}
+
+__device__ __forceinline__ void load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                        uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(
+          umma::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(umma::smem_u32(mbar))
+      : "memory");
+}
+
 // SWIZZLE_128B K-major smem descriptor (sm_100): SBO = 1024 B (8 rows of 128 B),
 // LBO unused (1), layout type 2 at bits 61-63.
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
@@ -58,6 +75,48 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
   return uint32_t(r * 128 + ((((k >> 2) ^ (r & 7)) & 7) << 4) + (k & 3) * 4);
 }
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Single-thread TMA -> MMA ring over n chunks (call from ONE thread).
+// issue(c, stage, full) issues chunk c's TMA loads and its expect_tx on
+// `full`; mma(c, stage) issues its MMAs, then the ring commits them to
+// empty[stage] and refills the stage of chunk c-1 (S-1 chunks in flight).
+template <int S, class Issue, class Mma>
+__device__ __forceinline__ void tma_ring(int n, uint8_t* ring, int stage_bytes, uint64_t* full, uint64_t* empty,
+                                         Issue issue, Mma mma) {
+  for (int c = 0; c < n && c < S; ++c) issue(c, ring + c * stage_bytes, &full[c]);
+  for (int c = 0; c < n; ++c) {
+    const int st = c % S;
+    umma::mbar_wait(&full[st], (c / S) & 1);
+    umma::fence_after_sync();
+    mma(c, ring + st * stage_bytes);
+    umma::commit(&empty[st]);
+    const int nx = c - 1 + S;
+    if (c >= 1 && nx < n) {
+      const int s2 = (c - 1) % S;
+      umma::mbar_wait(&empty[s2], ((c - 1) / S) & 1);   // chunk c-1's MMAs released the stage
+      issue(nx, ring + s2 * stage_bytes, &full[s2]);
+    }
+  }
+  if (n > 0) umma::mbar_wait(&empty[(n - 1) % S], ((n - 1) / S) & 1);
+}
+
+__device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, int S) {
+  for (int i = 0; i < S; ++i) {
+    umma::mbar_init(&full[i], 1);
+    umma::mbar_init(&empty[i], 1);
+  }
+  umma::fence_init();
+}
+
+// N-D bf16 tensor map with 128-byte swizzle (box inner dimension = 64
+// elements); dims/strides as cuTensorMapEncodeTiled (strides in bytes for
+// dims 1..rank-1), out-of-bounds elements read as 0.
+int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box);
 
 }  // namespace tma
 }  // namespace pb
