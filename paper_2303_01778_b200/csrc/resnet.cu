@@ -60,8 +60,9 @@ struct Net {
   const int32_t* rank;
   float* w;          // [G][P] fp32 masters, updated in place
   int64_t P;         // row stride of w (floats)
-  bf16* w16;         // [G][P16] bf16 conv weights, channels padded to 8
-  int64_t P16;
+  bf16* w16;         // [G][P16] bf16 conv weights, channels padded to 8; each row
+  int64_t P16;       //   holds [co][r][s][ci] at w16_off and, T16 further on,
+  int64_t T16;       //   the transposed [ci][r][s][co] copy (dgrad B operand)
   uint8_t* arena;    // per-slot activations
   int64_t slot_bytes;
   float* part;       // per-slot wgrad partials
@@ -348,9 +349,13 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv(Net a, ConvK k, int ntile) {
 // client's bf16 weights.  SWIZZLE_128B K-major tiles, one thread drives the
 // TMA -> MMA ring.  grid (M tiles, Cout / ntile, slots), 256 threads
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_rn_conv_fwd_tma(const __grid_constant__ CUtensorMap ta,
-                                                            const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
-                                                            int ntile, int Ht, int Nt) {
+// DG = true: the stride-1 data gradient with the same structure -- A = dz
+// boxes at (pad - s, pad - r), B = boxes of the transposed weight copy
+// [ci][r][s][co] (K-major over (r, s, co)), D = dL/dx [(n,h,w)][ci].
+template <bool DG>
+__global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
+                                                        const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
+                                                        int ntile, int Ht, int Nt) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = blockIdx.z;
   const Slot sl = a.slots[s];
@@ -371,13 +376,14 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_fwd_tma(const __grid_constan
   const uint32_t tmem = tmem_base;
   if (tid == 0) {
     const int nn = m0 / HWo, p0 = Nt > 1 ? 0 : (m0 - nn * HWo) / k.Wo;
-    const int ncb = k.Cinp / 64, n = k.R * k.R * ncb;
+    const int kc = DG ? k.Cout : k.Cinp, ncb = kc / 64, n = k.R * k.R * ncb;
     const uint32_t bytes = 128 * 128 + uint32_t(ntile) * 128;
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       const int rs = c / ncb, cb = c - rs * ncb, r = rs / k.R, q = rs - r * k.R;
+      const int dx = DG ? k.pad - q : q - k.pad, dy = DG ? k.pad - r : r - k.pad;
       pb::tma::expect_tx(f, bytes);
-      pb::tma::load_5d(st, &ta, cb * 64, q - k.pad, p0 + r - k.pad, nn, s, f);
-      pb::tma::load_3d(st + 128 * 128, &tb, rs * k.Cinp + cb * 64, n0, sl.r, f);
+      pb::tma::load_5d(st, &ta, cb * 64, dx, p0 + dy, nn, s, f);
+      pb::tma::load_3d(st + 128 * 128, &tb, rs * kc + cb * 64, n0, sl.r, f);
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t a0 = pb::tma::desc_sw128(smem_u32(st)), b0 = pb::tma::desc_sw128(smem_u32(st + 128 * 128));
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_fwd_tma(const __grid_constan
   fence_after_sync();
   const int row = (warp & 3) * 32 + lane, m = m0 + row;
   const int half = warp >> 2, cols = ntile / 2;
-  float* dst = at<float>(a, s, k.z) + int64_t(m) * k.Cout + n0;
+  float* dst = DG ? at<float>(a, s, k.dx) + int64_t(m) * k.Cinp + n0 : at<float>(a, s, k.z) + int64_t(m) * k.Cout + n0;
 #pragma unroll 1
   for (int c16 = 0; c16 < cols; c16 += 16) {
     float v[16];
@@ -456,6 +462,37 @@ __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, 
       w[wi] = nw;
       w16[u] = __float2bfloat16(nw);
     }
+  }
+}
+
+// w16t[ci][rs][co] = w16[co][rs][ci] of one conv: for client rows 0..rows-1
+// (by_slot = 0) or for the clients of the active slots that stepped (by_slot)
+// grid (ceil(Cinp/32), Cout/32, RS * rows), (32, 8) threads
+__global__ void __launch_bounds__(256) k_rn_w16t(Net a, ConvK k, int by_slot) {
+  const int RS = k.R * k.R;
+  const int z = blockIdx.z / RS, rs = blockIdx.z - z * RS;
+  int r = z;
+  if (by_slot) {
+    const Slot sl = a.slots[z];
+    if (sl.cnt == 0) return;
+    r = sl.r;
+  }
+  __shared__ bf16 tile[32][34];
+  const int ci0 = blockIdx.x * 32, co0 = blockIdx.y * 32;
+  const bf16* w16 = a.w16 + int64_t(r) * a.P16 + k.w16_off;
+  bf16* w16t = a.w16 + int64_t(r) * a.P16 + a.T16 + k.w16_off;
+  const int ci = ci0 + threadIdx.x;
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const int co = co0 + threadIdx.y + 8 * y;
+    tile[threadIdx.y + 8 * y][threadIdx.x] =
+        ci < k.Cinp ? w16[(int64_t(co) * RS + rs) * k.Cinp + ci] : __float2bfloat16(0.0f);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    const int cc = ci0 + threadIdx.y + 8 * y;
+    if (cc < k.Cinp) w16t[(int64_t(cc) * RS + rs) * k.Cout + co0 + threadIdx.x] = tile[threadIdx.x][threadIdx.y + 8 * y];
   }
 }
 
@@ -886,7 +923,8 @@ namespace {
 
 struct ConvL {
   CUtensorMap ta, tb;  // TMA maps of the forward implicit GEMM (tma != 0)
-  int tma, Ht, Nt;
+  CUtensorMap tad, tbd;  // ... and of the stride-1 data gradient (tma_dg != 0)
+  int tma, tma_dg, Ht, Nt;
   ConvK k;
   int Cin;           // master input channels (3 for the stem conv)
   int64_t w_off;     // fp32 master offset
@@ -986,7 +1024,7 @@ Net to_net(const pb_resnet_train_args& t, const Plan& pl) {
   Net a{};
   a.X = t.X; a.Y = t.Y; a.order = t.order; a.order_off = t.order_off; a.n = t.n; a.rank = t.rank;
   a.w = t.w; a.P = t.w_stride;
-  a.w16 = reinterpret_cast<bf16*>(t.ws_w16); a.P16 = pl.P16;
+  a.w16 = reinterpret_cast<bf16*>(t.ws_w16); a.P16 = 2 * pl.P16; a.T16 = pl.P16;
   a.arena = t.ws_arena; a.slot_bytes = pl.slot_bytes;
   a.part = t.ws_part; a.part_slot = pl.part_slot;
   a.gnp = t.ws_gnp; a.gnp_slot = pl.gnp_slot;
@@ -1024,6 +1062,20 @@ int build_maps(Plan& pl, const Net& a, int64_t slots) {
         (rc = pb::tma::make_nd_bf16(&c.tb, a.w16 + k.w16_off, 3, db, sb, bb)))
       return rc;
     c.tma = 1;
+    c.tma_dg = 0;
+    if (k.dx < 0 || k.Cout % 64) continue;
+    // dgrad: A = dz [BS][Ho][Wo][Cout], B = transposed weights [ci][r][s][co]
+    const uint64_t dda[5] = {uint64_t(k.Cout), uint64_t(k.Wo), uint64_t(k.Ho), uint64_t(a.BS), uint64_t(slots)};
+    const uint64_t sda[4] = {uint64_t(k.Cout) * 2, uint64_t(k.Wo) * k.Cout * 2, uint64_t(k.Ho) * k.Wo * k.Cout * 2,
+                             uint64_t(a.slot_bytes)};
+    const uint64_t Kd = uint64_t(k.R) * k.R * k.Cout;
+    const uint64_t ddb[3] = {Kd, uint64_t(k.Cinp), uint64_t(slots)};
+    const uint64_t sdb[2] = {Kd * 2, uint64_t(a.P16) * 2};
+    const uint32_t bdb[3] = {64, uint32_t(conv_ntile(k.Cinp)), 1};
+    if ((rc = pb::tma::make_nd_bf16(&c.tad, a.arena + k.dz, 5, dda, sda, ba)) ||
+        (rc = pb::tma::make_nd_bf16(&c.tbd, a.w16 + a.T16 + k.w16_off, 3, ddb, sdb, bdb)))
+      return rc;
+    c.tma_dg = 1;
   }
   return PB_OK;
 }
@@ -1034,7 +1086,7 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const int nt = conv_ntile(k.Cout);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
-    k_rn_conv_fwd_tma<<<g, 256, kCvSmem + 1024, s>>>(c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
+    k_rn_conv_tma<false><<<g, 256, kCvSmem + 1024, s>>>(c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
   } else if (mode == FWD) {
     const int nt = conv_ntile(k.Cout);
@@ -1042,6 +1094,12 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
     k_rn_conv<FWD><<<g, 256, kCvSmem, s>>>(a, k, nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
+  } else if (mode == DGRAD && c.tma_dg) {
+    const int nt = conv_ntile(k.Cinp);
+    const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
+    pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
+    k_rn_conv_tma<true><<<g, 256, kCvSmem + 1024, s>>>(c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
@@ -1059,6 +1117,12 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     pb::prof_begin(pb::K_RN_SGD, s);
     k_rn_wsgd<<<g2, 256, 0, s>>>(a, k, c.w_off, c.Cin);
     pb::prof_end(pb::K_RN_SGD, s);
+    if (c.tma_dg) {  // refresh the transposed copy the TMA dgrad reads
+      pb::prof_begin(pb::K_RN_SGD, s);
+      k_rn_w16t<<<dim3(unsigned((k.Cinp + 31) / 32), unsigned(k.Cout / 32), unsigned(k.R * k.R * active)),
+                  dim3(32, 8), 0, s>>>(a, k, 1);
+      pb::prof_end(pb::K_RN_SGD, s);
+    }
   }
 }
 
@@ -1191,7 +1255,7 @@ int setup() {
   static int done = 0;
   if (done) return PB_OK;
   const void* fns[] = {(const void*)k_rn_conv<FWD>, (const void*)k_rn_conv<DGRAD>, (const void*)k_rn_conv<WGRAD>,
-                       (const void*)k_rn_conv_fwd_tma};
+                       (const void*)k_rn_conv_tma<false>, (const void*)k_rn_conv_tma<true>};
   for (const void* fn : fns) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem + 1024));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_conv: ") + cudaGetErrorString(e));
@@ -1217,6 +1281,13 @@ int refresh_w16(const Net& a, const Plan& pl, int rows, cudaStream_t s) {
   pb::prof_begin(pb::K_RN_SGD, s);
   k_rn_w16<<<dim3(64, rows, t.n), 256, 0, s>>>(a, t, nullptr);
   pb::prof_end(pb::K_RN_SGD, s);
+  for (const ConvL& c : pl.convs) {
+    const ConvK& k = c.k;
+    pb::prof_begin(pb::K_RN_SGD, s);
+    k_rn_w16t<<<dim3(unsigned((k.Cinp + 31) / 32), unsigned(k.Cout / 32), unsigned(k.R * k.R * rows)), dim3(32, 8),
+                0, s>>>(a, k, 0);
+    pb::prof_end(pb::K_RN_SGD, s);
+  }
   return pb::check_launch("resnet w16");
 }
 
@@ -1226,7 +1297,7 @@ extern "C" int pb_resnet_workspace(int BS, int C, int64_t* out4) {
   if (BS < 1 || BS > kMaxBS || C < 2 || C > 128 || !out4) return pb::fail(PB_ERR_INVALID, "pb_resnet_workspace: bad arguments");
   const Plan pl = make_plan(BS, C);
   out4[0] = pl.slot_bytes;
-  out4[1] = pl.P16;
+  out4[1] = 2 * pl.P16;   // each bf16 row: weights + transposed copy
   out4[2] = pl.part_slot;
   out4[3] = pl.gnp_slot;
   return PB_OK;
@@ -1326,7 +1397,13 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
   if (dz) cudaMemcpyAsync(arena + k.dz, dz, size_t(dzb), cudaMemcpyDeviceToDevice, s);
   Net a{};
   a.arena = arena; a.slot_bytes = arena_bytes; a.slots = slot;
-  a.w16 = reinterpret_cast<bf16*>(const_cast<void*>(w)); a.P16 = (int64_t(Cout) * R * R * Cinp + 7) / 8 * 8;
+  // weights + room for the transposed copy (the dgrad B operand), as in a client row
+  const int64_t wn = (int64_t(Cout) * R * R * Cinp + 7) / 8 * 8;
+  bf16* wrow = nullptr;
+  cudaMalloc(&wrow, size_t(2 * wn) * sizeof(bf16));
+  cudaMemcpyAsync(wrow, w, size_t(Cout) * R * R * Cinp * sizeof(bf16), cudaMemcpyDeviceToDevice, s);
+  a.w16 = wrow; a.P16 = 2 * wn;
+  a.T16 = wn;
   a.part = part; a.part_slot = k.nsplit * M * Cout;
   a.BS = BS;
   ConvL c{};
@@ -1343,7 +1420,15 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
     cudaMemcpyAsync(out, arena + k.z, size_t(cnt) * Ho * Ho * Cout * 4, cudaMemcpyDeviceToDevice, s);
   } else if (mode == 1) {
     const int nt = conv_ntile(Cinp);
-    k_rn_conv<DGRAD><<<dim3((BS * H * H + 127) / 128, Cinp / nt, 1), 256, kCvSmem, s>>>(a, k, nt);
+    Plan pl;
+    pl.convs.push_back(c);
+    if ((rc = build_maps(pl, a, 1))) return rc;
+    if (pl.convs[0].tma_dg) {   // the network's path: the transposed copy, then TMA
+      k_rn_w16t<<<dim3(unsigned((Cinp + 31) / 32), unsigned(Cout / 32), unsigned(R * R)), dim3(32, 8), 0, s>>>(a, k, 0);
+      launch_conv(a, pl.convs[0], DGRAD, 1, s);
+    } else {
+      k_rn_conv<DGRAD><<<dim3((BS * H * H + 127) / 128, Cinp / nt, 1), 256, kCvSmem, s>>>(a, k, nt);
+    }
     cudaMemcpyAsync(out, arena + k.dx, size_t(cnt) * H * H * Cinp * 4, cudaMemcpyDeviceToDevice, s);
   } else {
     const int nt = conv_ntile(Cout);
@@ -1356,5 +1441,6 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
   cudaFree(arena);
   cudaFree(slot);
   cudaFree(part);
+  cudaFree(wrow);
   return rc;
 }
