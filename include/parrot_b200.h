@@ -304,6 +304,11 @@ int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout, int H, in
  * conventions; tests only).  N % 16 == 0, N <= 256, K % 32 == 0. */
 int pb_tma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, void* stream);
 
+/* D[128][N] = A^T B for bf16 A [K][128], B [K][N] (row-major, MN contiguous)
+ * loaded by TMA as MN-major SWIZZLE_128B tiles; lbo/sbo are the descriptor
+ * byte offsets under test (tests only).  N % 64 == 0, K % 64 == 0. */
+int pb_tma_bf16_mn_selftest(const void* A, const void* B, float* D, int N, int K, int lbo, int sbo, void* stream);
+
 /* 128 x N x K tf32 tcgen05 GEMM D = A * B^T from fp32 row-major A [128,K],
  * B [N,K]; a_mn/b_mn select MN-major smem staging (tests only). */
 int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,

@@ -140,3 +140,83 @@ extern "C" int pb_tma_tf32_selftest(const float* A, const float* B, float* D, in
   k_tma_selftest<<<1, 128, smem, pb::as_stream(stream)>>>(ta, tb, D, N, K);
   return pb::check_launch("pb_tma_tf32_selftest");
 }
+
+// D[128][N] = sum_k A[k][m] B[k][n]: bf16 operands stored [K][MN] row-major
+// (MN contiguous), loaded by TMA as MN-major SWIZZLE_128B tiles (boxes of 64
+// MN elements x K rows; MN atoms `Kr * 128` bytes apart), descriptors with
+// the given LBO / SBO (bytes) -- pins the MN-major swizzled convention.
+namespace {
+__global__ void __launch_bounds__(128) k_tma_mn_selftest(const __grid_constant__ CUtensorMap ta,
+                                                         const __grid_constant__ CUtensorMap tb, float* D, int N,
+                                                         int K, uint32_t lbo, uint32_t sbo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = pb::tma::align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full, done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&full, 1);
+    mbar_init(&done, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  constexpr int Kr = 64;                    // K rows per stage
+  uint8_t* sA = smem;                       // 2 MN atoms of [64 K][64 M]
+  uint8_t* sB = smem + 2 * Kr * 128;        // N/64 atoms
+  for (int c = 0; c < K / Kr; ++c) {
+    if (tid == 0) {
+      pb::tma::expect_tx(&full, uint32_t((2 + N / 64) * Kr * 128));
+      for (int h = 0; h < 2; ++h) pb::tma::load_2d(sA + h * Kr * 128, &ta, h * 64, c * Kr, &full);
+      for (int h = 0; h < N / 64; ++h) pb::tma::load_2d(sB + h * Kr * 128, &tb, h * 64, c * Kr, &full);
+      mbar_wait(&full, c & 1);
+      fence_after_sync();
+      auto mk = [&](uint32_t addr) {
+        uint64_t d = 0;
+        d |= uint64_t((addr >> 4) & 0x3FFFu);
+        d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+        d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+        d |= uint64_t(1) << 46;
+        d |= uint64_t(2) << 61;
+        return d;
+      };
+      const uint32_t idesc = idesc_bf16(128, N, true, true);
+      for (int kk = 0; kk < Kr / 16; ++kk)
+        mma_bf16(tmem, mk(smem_u32(sA) + kk * 2048), mk(smem_u32(sB) + kk * 2048), idesc, c > 0 || kk > 0);
+      commit(&done);
+      mbar_wait(&done, c & 1);
+    }
+    __syncthreads();
+  }
+  fence_after_sync();
+  const int row = warp * 32 + lane;
+  for (int c16 = 0; c16 < N; c16 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c16), v);
+    for (int k = 0; k < 16; ++k) D[row * N + c16 + k] = v[k];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+}  // namespace
+
+extern "C" int pb_tma_bf16_mn_selftest(const void* A, const void* B, float* D, int N, int K, int lbo, int sbo,
+                                       void* stream) {
+  if (!A || !B || !D || N < 64 || N > 256 || N % 64 || K < 64 || K % 64)
+    return pb::fail(PB_ERR_INVALID, "pb_tma_bf16_mn_selftest: bad arguments");
+  CUtensorMap ta, tb;
+  const uint64_t da[2] = {128, uint64_t(K)}, sa[1] = {128 * 2};
+  const uint64_t db[2] = {uint64_t(N), uint64_t(K)}, sbb[1] = {uint64_t(N) * 2};
+  const uint32_t box[2] = {64, 64};
+  int rc;
+  if ((rc = pb::tma::make_nd_bf16(&ta, A, 2, da, sa, box)) || (rc = pb::tma::make_nd_bf16(&tb, B, 2, db, sbb, box)))
+    return rc;
+  const size_t smem = 1024 + size_t(2 + N / 64) * 64 * 128;
+  cudaFuncSetAttribute((const void*)k_tma_mn_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_tma_mn_selftest<<<1, 128, smem, pb::as_stream(stream)>>>(ta, tb, D, N, K, uint32_t(lbo), uint32_t(sbo));
+  return pb::check_launch("pb_tma_bf16_mn_selftest");
+}

@@ -86,3 +86,21 @@ def test_tma_sw128_tf32_gemm(N, K):
     trunc = lambda x: (x.view(torch.int32) & -8192).view(torch.float32).double()  # noqa: E731
     ref = trunc(A) @ trunc(B).t()
     assert float((D.double() - ref).norm() / ref.norm()) < 1e-6
+
+
+@pytest.mark.parametrize("N", [64, 128, 256])
+def test_tma_mn_sw128_bf16_gemm(N):
+    """MN-major SWIZZLE_128B bf16 tiles loaded by TMA (the ResNet weight
+    gradient's operands): LBO = stride between 64-element MN atoms, SBO =
+    1024 B (8 K rows) -- measured by tools/tma_mn_probe.py."""
+    import torch
+    from paper_2303_01778_b200._lib import lib, ptr
+    K = 128
+    g = torch.Generator(device="cuda").manual_seed(N)
+    A = torch.randn(K, 128, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+    D = torch.zeros(128, N, device="cuda")
+    lib.check(lib.pb_tma_bf16_mn_selftest(ptr(A), ptr(B), ptr(D), N, K, 64 * 128, 1024,
+                                          torch.cuda.current_stream().cuda_stream))
+    ref = A.double().t() @ B.double()
+    assert float((D.double() - ref).norm() / ref.norm()) < 1e-6
