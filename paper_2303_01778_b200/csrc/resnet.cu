@@ -415,6 +415,89 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
+// k_rn_wgrad_tma: the stride-1 weight gradient with MN-major SWIZZLE_128B
+// TMA tiles.  D[(r,s,ci)][co] = sum over output positions of
+// x[n, p+r-pad, q+s-pad, ci] dz[n, p, q, co]; K = positions, 64 per stage
+// (whole output rows: Wo x Hs x Ns).  The M tile is two 64-channel "atoms"
+// (tap, channel block) -- each one 5-D box of the input at tap-shifted
+// coordinates (zero-filled padding); B = ntile/64 boxes of dz.  Positions
+// split in chunks of 1024 per CTA, partials in the weight layout as before.
+// grid (ceil(RS*Cinp/128), Cout/ntile, slots * nsplit), 256 threads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
+                                                         const __grid_constant__ CUtensorMap tdz, Net a, ConvK k,
+                                                         int ntile, int Hs, int Ns) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int s = blockIdx.z / k.nsplit, split = blockIdx.z % k.nsplit;
+  const Slot sl = a.slots[s];
+  const int cnt = sl.cnt;
+  if (cnt == 0) return;
+  const int RS = k.R * k.R, M = RS * k.Cinp, HWo = k.Ho * k.Wo;
+  const int kbeg = split * kWgSplit, kend = min(cnt * HWo, kbeg + kWgSplit);
+  if (kbeg >= kend) return;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * ntile;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = pb::tma::align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t tmem_base;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) pb::tma::ring_barriers(full, empty, kStages);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const int ncb = k.Cinp / 64, natoms = RS * ncb;
+    const int a0i = m0 / 64, na = min(2, natoms - a0i);   // atoms of this M tile
+    const int nb = ntile / 64;
+    const int n = (kend - kbeg + 63) / 64;
+    const uint32_t bytes = uint32_t(na + nb) * 64 * 128;
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int pos = kbeg + c * 64, nn = pos / HWo, p0 = Ns > 1 ? 0 : (pos - nn * HWo) / k.Wo;
+      pb::tma::expect_tx(f, bytes);
+      for (int h = 0; h < na; ++h) {
+        const int at_ = a0i + h, rs = at_ / ncb, cb = at_ - rs * ncb, r = rs / k.R, q = rs - r * k.R;
+        pb::tma::load_5d(st + h * 8192, &tx, cb * 64, q - k.pad, p0 + r - k.pad, nn, s, f);
+      }
+      for (int h = 0; h < nb; ++h) pb::tma::load_5d(st + 16384 + h * 8192, &tdz, n0 + h * 64, 0, p0, nn, s, f);
+    };
+    auto mk = [](uint32_t addr) {   // MN-major SWIZZLE_128B: LBO = MN-atom stride, SBO = 8 K rows
+      uint64_t d = 0;
+      d |= uint64_t((addr >> 4) & 0x3FFFu);
+      d |= uint64_t(8192 >> 4) << 16;
+      d |= uint64_t(1024 >> 4) << 32;
+      d |= uint64_t(1) << 46;
+      d |= uint64_t(2) << 61;
+      return d;
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint32_t idesc = idesc_bf16(128, ntile, true, true);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16(tmem, mk(smem_u32(st) + kk * 2048), mk(smem_u32(st + 16384) + kk * 2048), idesc, c > 0 || kk > 0);
+    };
+    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
+  const int row = (warp & 3) * 32 + lane, m = m0 + row;
+  const int half = warp >> 2, cols = ntile / 2;
+  float* dst = a.part + int64_t(s) * a.part_slot + int64_t(split) * M * k.Cout + int64_t(n0) * M + m;
+#pragma unroll 1
+  for (int c16 = 0; c16 < cols; c16 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(half * cols + c16), v);
+    if (m < M) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dst[int64_t(half * cols + c16 + u) * M] = v[u];
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+
+// ---------------------------------------------------------------------------
 // k_rn_wsgd: W -= lr * sum_split partial (split order); refresh the bf16 copy
 // partial [split][co][(r,s,ci)] matches W [co][r][s][ci] element for element
 // (the stem's master has 3 input channels, its copies 8).
@@ -740,10 +823,22 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float
 }
 
 // G = (g0 [+ g1]) * (mask > 0); GN backward(s) -> bf16 dz; grid (active, BS)
+// Samples past the batch get dz = 0: the TMA weight-gradient boxes read
+// whole position tiles, and zero dz rows keep them out of the sum.
 __global__ void __launch_bounds__(kGnThreads) k_rn_gn_bwd(Net a, GnB f) {
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
-  if (i >= sl.cnt) return;
+  if (i >= sl.cnt) {
+    if (sl.cnt == 0) return;
+    const int64_t n8 = int64_t(f.HW) * f.C / 8;
+    uint4* z1 = reinterpret_cast<uint4*>(at<bf16>(a, s, f.dz) + int64_t(i) * f.HW * f.C);
+    uint4* z2 = f.z2 >= 0 ? reinterpret_cast<uint4*>(at<bf16>(a, s, f.dz2) + int64_t(i) * f.HW * f.C) : nullptr;
+    for (int64_t e = threadIdx.x; e < n8; e += kGnThreads) {
+      z1[e] = make_uint4(0, 0, 0, 0);
+      if (z2) z2[e] = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
   extern __shared__ double dsm[];
   const int C = f.C, HW = f.HW;
   const int64_t base = int64_t(i) * HW * C;
@@ -924,7 +1019,8 @@ namespace {
 struct ConvL {
   CUtensorMap ta, tb;  // TMA maps of the forward implicit GEMM (tma != 0)
   CUtensorMap tad, tbd;  // ... and of the stride-1 data gradient (tma_dg != 0)
-  int tma, tma_dg, Ht, Nt;
+  CUtensorMap twx, twd;  // ... and of the stride-1 weight gradient (tma_wg != 0)
+  int tma, tma_dg, tma_wg, Ht, Nt, Hs, Ns;
   ConvK k;
   int Cin;           // master input channels (3 for the stem conv)
   int64_t w_off;     // fp32 master offset
@@ -1063,6 +1159,20 @@ int build_maps(Plan& pl, const Net& a, int64_t slots) {
       return rc;
     c.tma = 1;
     c.tma_dg = 0;
+    // wgrad: x boxes of 64 positions (whole output rows) and dz boxes
+    c.Hs = std::min(k.Ho, 64 / k.Wo);
+    c.Ns = 64 / (k.Wo * c.Hs);
+    const uint32_t bw[5] = {64, uint32_t(k.Wo), uint32_t(c.Hs), uint32_t(c.Ns), 1};
+    const uint64_t dz5[5] = {uint64_t(k.Cout), uint64_t(k.Wo), uint64_t(k.Ho), uint64_t(a.BS), uint64_t(slots)};
+    const uint64_t sz5[4] = {uint64_t(k.Cout) * 2, uint64_t(k.Wo) * k.Cout * 2, uint64_t(k.Ho) * k.Wo * k.Cout * 2,
+                             uint64_t(a.slot_bytes)};
+    c.tma_wg = 0;
+    if (k.Cout % 64 == 0) {
+      if ((rc = pb::tma::make_nd_bf16(&c.twx, a.arena + k.in, 5, da, sa, bw)) ||
+          (rc = pb::tma::make_nd_bf16(&c.twd, a.arena + k.dz, 5, dz5, sz5, bw)))
+        return rc;
+      c.tma_wg = 1;
+    }
     if (k.dx < 0 || k.Cout % 64) continue;
     // dgrad: A = dz [BS][Ho][Wo][Cout], B = transposed weights [ci][r][s][co]
     const uint64_t dda[5] = {uint64_t(k.Cout), uint64_t(k.Wo), uint64_t(k.Ho), uint64_t(a.BS), uint64_t(slots)};
@@ -1110,7 +1220,10 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const int nt = conv_ntile(k.Cout);
     const dim3 g((k.R * k.R * k.Cinp + 127) / 128, k.Cout / nt, active * k.nsplit);
     pb::prof_begin(pb::K_RN_CONV_WGRAD, s);
-    k_rn_conv<WGRAD><<<g, 256, kCvSmem, s>>>(a, k, nt);
+    if (c.tma && c.tma_wg)
+      k_rn_wgrad_tma<<<g, 256, kCvSmem + 1024, s>>>(c.twx, c.twd, a, k, nt, c.Hs, c.Ns);
+    else
+      k_rn_conv<WGRAD><<<g, 256, kCvSmem, s>>>(a, k, nt);
     pb::prof_end(pb::K_RN_CONV_WGRAD, s);
     const int64_t n4 = int64_t(k.R) * k.R * k.Cinp * k.Cout / 4;
     const dim3 g2(unsigned((n4 + 255) / 256), active);
@@ -1255,7 +1368,8 @@ int setup() {
   static int done = 0;
   if (done) return PB_OK;
   const void* fns[] = {(const void*)k_rn_conv<FWD>, (const void*)k_rn_conv<DGRAD>, (const void*)k_rn_conv<WGRAD>,
-                       (const void*)k_rn_conv_tma<false>, (const void*)k_rn_conv_tma<true>};
+                       (const void*)k_rn_conv_tma<false>, (const void*)k_rn_conv_tma<true>,
+                       (const void*)k_rn_wgrad_tma};
   for (const void* fn : fns) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem + 1024));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_conv: ") + cudaGetErrorString(e));
@@ -1433,7 +1547,18 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
   } else {
     const int nt = conv_ntile(Cout);
     cudaMemsetAsync(part, 0, size_t(k.nsplit * M * Cout) * 4, s);
-    k_rn_conv<WGRAD><<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, kCvSmem, s>>>(a, k, nt);
+    Plan pl;
+    pl.convs.push_back(c);
+    if ((rc = build_maps(pl, a, 1))) return rc;
+    if (pl.convs[0].tma && pl.convs[0].tma_wg) {
+      // the network zeroes dz of samples past the batch (k_rn_gn_bwd)
+      const int64_t live = int64_t(cnt) * Ho * Ho * Cout * 2;
+      cudaMemsetAsync(arena + k.dz + live, 0, size_t(dzb - live), s);
+      k_rn_wgrad_tma<<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, kCvSmem + 1024, s>>>(
+          pl.convs[0].twx, pl.convs[0].twd, a, k, nt, pl.convs[0].Hs, pl.convs[0].Ns);
+    } else {
+      k_rn_conv<WGRAD><<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, kCvSmem, s>>>(a, k, nt);
+    }
     cudaMemcpyAsync(out, part, size_t(k.nsplit * M * Cout) * 4, cudaMemcpyDeviceToDevice, s);
   }
   rc = pb::check_launch("pb_rn_conv_selftest");
