@@ -45,9 +45,9 @@ constexpr int kStages = 4;
 struct LzMaps {
   CUtensorMap w0;      // W0 fc1 block  [512][3136],  box 128 rows
   CUtensorMap w0t;     // W0^T          [3136][512],  box 128
-  CUtensorMap hxa;     // HX            [rows][3136], box 128 (history tiles)
+  CUtensorMap hxa[4];  // HX            [rows][3136], box 32/64/96/128 rows (history tiles)
   CUtensorMap hxb;     // HX                          box 32  (current rows)
-  CUtensorMap hda;     // HD            [rows][512],  box 128
+  CUtensorMap hda[4];  // HD            [rows][512],  box 32/64/96/128
   CUtensorMap hdb;     // HD                          box 32
   CUtensorMap hdt;     // HD^T          [512][rows],  box 128
   CUtensorMap hxt128;  // HX^T          [3136][rows], box 128
@@ -136,11 +136,15 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const CUtensorMap* ta = FWD ? &m.hxa : &m.hda;
+  // the history box covers only the tile's live rows (rounded up to 32); the
+  // rows left stale give Gram rows that are zeroed on the way out
+  const int nsub = min(4, (jlim - j0 + 31) >> 5);
+  const CUtensorMap* ta = FWD ? &m.hxa[nsub - 1] : &m.hda[nsub - 1];
   const CUtensorMap* tb = FWD ? &m.hxb : &m.hdb;
   if (tid == 0) {
+    const uint32_t bytes = uint32_t(2 * (nsub + 1) * 32 * 128);
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      pb::tma::expect_tx(f, kGrStage);
+      pb::tma::expect_tx(f, bytes);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint8_t* sh = st + h * (kGrA + kGrB);
@@ -181,12 +185,13 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
     if (tid == 0) {
       fence_after_sync();
       const int hcol = int(sl.hist) + j0;
-      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = q*4 + jc
+      // K chunks (32 history columns) past the live rows contribute zero: skipped
+      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = q*nsub + jc
         pb::tma::expect_tx(f, kGrA);
-        pb::tma::load_2d(st, &m.hdt, hcol + (c & 3) * 32, (c >> 2) * 128, f);
+        pb::tma::load_2d(st, &m.hdt, hcol + (c % nsub) * 32, (c / nsub) * 128, f);
       };
       auto mma = [&](int c, uint8_t* st) {
-        const int q = c >> 2, jc = c & 3;
+        const int q = c / nsub, jc = c % nsub;
         const uint64_t a0 = desc_sw128(smem_u32(st));
         const uint64_t b0 = desc_sw128(smem_u32(sGxT + jc * 32 * 128));
         const uint32_t idesc = idesc_tf32(128, 32);
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
         for (int kk = 0; kk < 4; ++kk)
           mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
       };
-      tma_ring<kStages>(16, smem, kGrA, full2, empty2, issue, mma);
+      tma_ring<kStages>(4 * nsub, smem, kGrA, full2, empty2, issue, mma);
     }
     __syncthreads();
     fence_after_sync();
@@ -649,14 +654,16 @@ int lazy_fc1_prepare(Args& a, cudaStream_t s) {
   using pb::tma::make_2d_f32;
   if ((rc = make_2d_f32(&m->w0, a.w0 + oF1W, kFlat, kH1, kFlat, 128)) ||
       (rc = make_2d_f32(&m->w0t, a.w0t, kH1, kFlat, kH1, 128)) ||
-      (rc = make_2d_f32(&m->hxa, a.hx, kFlat, R, kFlat, 128)) ||
       (rc = make_2d_f32(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
-      (rc = make_2d_f32(&m->hda, a.hd, kH1, R, kH1, 128)) ||
       (rc = make_2d_f32(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
       (rc = make_2d_f32(&m->hdt, a.hdt, R, kH1, R, 128)) ||
       (rc = make_2d_f32(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
       (rc = make_2d_f32(&m->hxt256, a.hxt, R, kFlat, R, 256)))
     return rc;
+  for (int q = 0; q < 4; ++q)   // history boxes sized to the live rows of a tile
+    if ((rc = make_2d_f32(&m->hxa[q], a.hx, kFlat, R, kFlat, 32 * (q + 1))) ||
+        (rc = make_2d_f32(&m->hda[q], a.hd, kH1, R, kH1, 32 * (q + 1))))
+      return rc;
   return pb::check_launch("lazy fc1 prepare");
 }
 
