@@ -594,7 +594,7 @@ struct GnF {
 };
 
 constexpr int kGnThreads = 512;
-constexpr size_t kGnSmem = 5 * 1024 * sizeof(double);   // per-thread partials + per-channel sums
+constexpr size_t kGnSmem = (5 * 1024 + 64) * sizeof(double);   // partials, per-channel sums, scratch
 
 // Per-channel sums of two quantities over positions, 4 channels per thread
 // (float4 loads): thread t owns channel group (t % (C/4)) and every
@@ -649,20 +649,48 @@ __device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* 
   __syncthreads();
 }
 
-// mean / rstd of the two groups from per-channel sum and sum of squares
-__device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, const double* s2,
-                                           float (&mean)[kGroups], float (&rstd)[kGroups]) {
-  const int cg = C / kGroups;
-  const double inv_n = 1.0 / double(HW * cg);
+// Per-group sums of x1[c], x2[c] (thread c supplies them; C <= 512, groups
+// of >= 32 channels): a fixed xor-shuffle tree per warp, then the group's
+// warp partials in warp order -- deterministic, no thread loops over C.
+// Every thread receives both groups' sums.  scratch: 32 doubles.
+__device__ __forceinline__ void group_sums(int C, double v1, double v2, double* scratch, double (&t1)[kGroups],
+                                           double (&t2)[kGroups]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid >= C) v1 = v2 = 0.0;
+  for (int o = 16; o > 0; o >>= 1) {
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+  }
+  if (lane == 0) {
+    scratch[warp] = v1;
+    scratch[16 + warp] = v2;
+  }
+  __syncthreads();
+  const int wpg = (C / kGroups) >> 5;   // warps per group
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    double t1 = 0.0, t2 = 0.0;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) {
-      t1 += s1[c];
-      t2 += s2[c];
+    double a = 0.0, b = 0.0;
+    for (int w = g * wpg; w < (g + 1) * wpg; ++w) {
+      a += scratch[w];
+      b += scratch[16 + w];
     }
-    const double m = t1 * inv_n;
-    const double var = fmax(t2 * inv_n - m * m, 0.0);
+    t1[g] = a;
+    t2[g] = b;
+  }
+  __syncthreads();
+}
+
+// mean / rstd of the two groups from per-channel sum and sum of squares
+__device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, const double* s2, double* scratch,
+                                           float (&mean)[kGroups], float (&rstd)[kGroups]) {
+  const int cg = C / kGroups, tid = threadIdx.x;
+  const double inv_n = 1.0 / double(HW * cg);
+  double t1[kGroups], t2[kGroups];
+  group_sums(C, tid < C ? s1[tid] : 0.0, tid < C ? s2[tid] : 0.0, scratch, t1, t2);
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    const double m = t1[g] * inv_n;
+    const double var = fmax(t2[g] * inv_n - m * m, 0.0);
     mean[g] = float(m);
     rstd[g] = float(1.0 / sqrt(var + double(kEps)));
   }
@@ -691,12 +719,12 @@ __global__ void __launch_bounds__(kGnThreads) k_rn_gn_fwd(Net a, GnF f) {
     };
   };
   chan_sums(C, HW, p1, p2, r1, r2, sq(z));
-  gn_moments(C, HW, r1, r2, mean, rstd);
+  gn_moments(C, HW, r1, r2, r2 + 512, mean, rstd);
   __syncthreads();
   const float* z2 = f.z2 >= 0 ? at<float>(a, s, f.z2) + base : nullptr;
   if (z2) {
     chan_sums(C, HW, p1, p2, r1, r2, sq(z2));
-    gn_moments(C, HW, r1, r2, mean2, rstd2);
+    gn_moments(C, HW, r1, r2, r2 + 512, mean2, rstd2);
   }
   if (threadIdx.x == 0) {
     float* st = at<float>(a, s, f.stats) + i * 2 * kGroups;
@@ -756,7 +784,10 @@ struct GnB {
 
 // dgamma/dbeta partials of sample i and dz (bf16) for one GN given the gated
 // gradient G (fp32, materialised)
-__device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float* G, int64_t z_off,
+// MAT: the first GN of the kernel also materialises the gated gradient
+// G = (g0 [+ g1]) * (mask > 0) while it reduces it (one pass over the sources)
+template <bool MAT>
+__device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, int64_t z_off,
                            int64_t st_off, int64_t gam_off, int64_t dz_off, int64_t pg_off, double* dsm) {
   double* p1 = dsm;
   double* p2 = dsm + 4 * kGnThreads;
@@ -774,8 +805,31 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float
     rstd[g] = st[2 * g + 1];
   }
   // per channel: dbeta = sum G, dgamma = sum G * xhat
+  const float* g0 = MAT ? at<float>(a, s, f.g0) + base : nullptr;
+  const float* g1 = MAT && f.g1 >= 0 ? at<float>(a, s, f.g1) + base : nullptr;
+  const bf16* mask = MAT && f.mask >= 0 ? at<const bf16>(a, s, f.mask) + base : nullptr;
   chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c0, float* u, float* v) {
-    const float4 gv = *reinterpret_cast<const float4*>(G + p * C + c0);
+    float4 gv;
+    if (MAT) {
+      gv = *reinterpret_cast<const float4*>(g0 + p * C + c0);
+      if (g1) {
+        const float4 h = *reinterpret_cast<const float4*>(g1 + p * C + c0);
+        gv.x += h.x;
+        gv.y += h.y;
+        gv.z += h.z;
+        gv.w += h.w;
+      }
+      if (mask) {
+        const uint2 mb = *reinterpret_cast<const uint2*>(mask + p * C + c0);
+        if (!(__uint_as_float(mb.x << 16) > 0.0f)) gv.x = 0.0f;
+        if (!(__uint_as_float(mb.x & 0xffff0000u) > 0.0f)) gv.y = 0.0f;
+        if (!(__uint_as_float(mb.y << 16) > 0.0f)) gv.z = 0.0f;
+        if (!(__uint_as_float(mb.y & 0xffff0000u) > 0.0f)) gv.w = 0.0f;
+      }
+      *reinterpret_cast<float4*>(G + p * C + c0) = gv;
+    } else {
+      gv = *reinterpret_cast<const float4*>(G + p * C + c0);
+    }
     const float4 zv = *reinterpret_cast<const float4*>(z + p * C + c0);
     const int g = c0 >> cshift;
     u[0] = gv.x, u[1] = gv.y, u[2] = gv.z, u[3] = gv.w;
@@ -791,17 +845,16 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, const float
   }
   const double inv_n = 1.0 / double(HW * cg);
   float m1[kGroups], m2[kGroups];
+  {
+    const int c = threadIdx.x;
+    double t1[kGroups], t2[kGroups];
+    group_sums(C, c < C ? double(gam[c]) * r1[c] : 0.0, c < C ? double(gam[c]) * r2[c] : 0.0, r2 + 512, t1, t2);
 #pragma unroll
-  for (int g = 0; g < kGroups; ++g) {
-    double t1 = 0.0, t2 = 0.0;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) {
-      t1 += double(gam[c]) * r1[c];
-      t2 += double(gam[c]) * r2[c];
+    for (int g = 0; g < kGroups; ++g) {
+      m1[g] = float(t1[g] * inv_n);
+      m2[g] = float(t2[g] * inv_n);
     }
-    m1[g] = float(t1 * inv_n);
-    m2[g] = float(t2 * inv_n);
   }
-  __syncthreads();
   bf16* dz = at<bf16>(a, s, dz_off) + base;
   const int n4 = HW * C / 4;
   for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
@@ -843,35 +896,12 @@ __global__ void __launch_bounds__(kGnThreads) k_rn_gn_bwd(Net a, GnB f) {
   const int C = f.C, HW = f.HW;
   const int64_t base = int64_t(i) * HW * C;
   // the gated gradient is materialised once (fp32, in the gsc buffer or in
-  // place over g0) so the reductions below read it directly
+  // place over g0) by the first reduction pass; later passes read it
   float* G = f.gsc >= 0 ? at<float>(a, s, f.gsc) + base : at<float>(a, s, f.g0) + base;
-  const float* g0 = at<float>(a, s, f.g0) + base;
-  const float* g1 = f.g1 >= 0 ? at<float>(a, s, f.g1) + base : nullptr;
-  const bf16* mask = f.mask >= 0 ? at<const bf16>(a, s, f.mask) + base : nullptr;
-  const int n4 = HW * C / 4;
-  for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
-    float4 g = reinterpret_cast<const float4*>(g0)[e4];
-    if (g1) {
-      const float4 h = reinterpret_cast<const float4*>(g1)[e4];
-      g.x += h.x;
-      g.y += h.y;
-      g.z += h.z;
-      g.w += h.w;
-    }
-    if (mask) {
-      const uint2 mb = reinterpret_cast<const uint2*>(mask)[e4];
-      if (!(__uint_as_float(mb.x << 16) > 0.0f)) g.x = 0.0f;
-      if (!(__uint_as_float(mb.x & 0xffff0000u) > 0.0f)) g.y = 0.0f;
-      if (!(__uint_as_float(mb.y << 16) > 0.0f)) g.z = 0.0f;
-      if (!(__uint_as_float(mb.y & 0xffff0000u) > 0.0f)) g.w = 0.0f;
-    }
-    reinterpret_cast<float4*>(G)[e4] = g;
-  }
-  __syncthreads();
-  gn_bwd_one(a, s, i, f, G, f.z, f.stats, f.gamma, f.dz, f.pg, dsm);
+  gn_bwd_one<true>(a, s, i, f, G, f.z, f.stats, f.gamma, f.dz, f.pg, dsm);
   if (f.z2 >= 0) {
     __syncthreads();
-    gn_bwd_one(a, s, i, f, G, f.z2, f.stats2, f.gamma2, f.dz2, f.pg2, dsm);
+    gn_bwd_one<false>(a, s, i, f, G, f.z2, f.stats2, f.gamma2, f.dz2, f.pg2, dsm);
   }
 }
 
