@@ -548,6 +548,56 @@ __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, 
   }
 }
 
+// k_rn_wsgd_t: as k_rn_wsgd for convolutions whose data gradient reads the
+// transposed copy: 32 co x 128 ci tiles per filter tap, float4 partial /
+// master / copy accesses along ci, the transposed [ci][r][s][co] copy
+// written from smem along co.  Cin == Cinp, Cinp % 128 == 0 or Cinp == 64.
+// grid (ceil(Cinp/128), Cout/32, RS * active), (32, 8) threads
+__global__ void __launch_bounds__(256) k_rn_wsgd_t(Net a, ConvK k, int64_t w_off) {
+  const int RS = k.R * k.R;
+  const int s = blockIdx.z / RS, rs = blockIdx.z - s * RS;
+  const Slot sl = a.slots[s];
+  if (sl.cnt == 0) return;
+  __shared__ bf16 tile[32][128 + 8];
+  const int ci0 = blockIdx.x * 128, co0 = blockIdx.y * 32, cw = min(128, k.Cinp - ci0);
+  const int64_t M = int64_t(RS) * k.Cinp, n = M * k.Cout;
+  const int nsp = (sl.cnt * k.Ho * k.Wo + kWgSplit - 1) / kWgSplit;
+  const float* part = a.part + int64_t(s) * a.part_slot;
+  float* w = a.w + int64_t(sl.r) * a.P + w_off;
+  bf16* w16 = a.w16 + int64_t(sl.r) * a.P16 + k.w16_off;
+  bf16* w16t = w16 + a.T16;
+  const int cl = threadIdx.x * 4;
+  if (cl < cw) {
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int col = threadIdx.y + 8 * y, co = co0 + col;
+      const int64_t e = int64_t(co) * M + int64_t(rs) * k.Cinp + ci0 + cl;
+      float4 g = *reinterpret_cast<const float4*>(part + e);
+      for (int sp = 1; sp < nsp; ++sp) {
+        const float4 h = *reinterpret_cast<const float4*>(part + sp * n + e);
+        g.x += h.x;
+        g.y += h.y;
+        g.z += h.z;
+        g.w += h.w;
+      }
+      float4 wv = *reinterpret_cast<float4*>(w + e);
+      wv.x = fmaf(-a.lr, g.x, wv.x);
+      wv.y = fmaf(-a.lr, g.y, wv.y);
+      wv.z = fmaf(-a.lr, g.z, wv.z);
+      wv.w = fmaf(-a.lr, g.w, wv.w);
+      *reinterpret_cast<float4*>(w + e) = wv;
+      uint2 o;
+      o.x = pack_bf16(wv.x, wv.y);
+      o.y = pack_bf16(wv.z, wv.w);
+      *reinterpret_cast<uint2*>(w16 + e) = o;
+      *reinterpret_cast<uint2*>(&tile[col][cl]) = o;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.y; c < cw; c += 8)
+    w16t[(int64_t(ci0 + c) * RS + rs) * k.Cout + co0 + threadIdx.x] = tile[threadIdx.x][c];
+}
+
 // w16t[ci][rs][co] = w16[co][rs][ci] of one conv: for client rows 0..rows-1
 // (by_slot = 0) or for the clients of the active slots that stepped (by_slot)
 // grid (ceil(Cinp/32), Cout/32, RS * rows), (32, 8) threads
@@ -1255,17 +1305,15 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     else
       k_rn_conv<WGRAD><<<g, 256, kCvSmem, s>>>(a, k, nt);
     pb::prof_end(pb::K_RN_CONV_WGRAD, s);
-    const int64_t n4 = int64_t(k.R) * k.R * k.Cinp * k.Cout / 4;
-    const dim3 g2(unsigned((n4 + 255) / 256), active);
     pb::prof_begin(pb::K_RN_SGD, s);
-    k_rn_wsgd<<<g2, 256, 0, s>>>(a, k, c.w_off, c.Cin);
-    pb::prof_end(pb::K_RN_SGD, s);
-    if (c.tma_dg) {  // refresh the transposed copy the TMA dgrad reads
-      pb::prof_begin(pb::K_RN_SGD, s);
-      k_rn_w16t<<<dim3(unsigned((k.Cinp + 31) / 32), unsigned(k.Cout / 32), unsigned(k.R * k.R * active)),
-                  dim3(32, 8), 0, s>>>(a, k, 1);
-      pb::prof_end(pb::K_RN_SGD, s);
+    if (c.tma_dg) {  // also refresh the transposed copy the TMA dgrad reads
+      k_rn_wsgd_t<<<dim3(unsigned((k.Cinp + 127) / 128), unsigned(k.Cout / 32), unsigned(k.R * k.R * active)),
+                    dim3(32, 8), 0, s>>>(a, k, c.w_off);
+    } else {
+      const int64_t n4 = int64_t(k.R) * k.R * k.Cinp * k.Cout / 4;
+      k_rn_wsgd<<<dim3(unsigned((n4 + 255) / 256), active), 256, 0, s>>>(a, k, c.w_off, c.Cin);
     }
+    pb::prof_end(pb::K_RN_SGD, s);
   }
 }
 
