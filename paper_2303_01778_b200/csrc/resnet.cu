@@ -415,6 +415,95 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
+// k_rn_dgrad_s2_tma: stride-2 data gradient by sub-pixel decomposition.
+// Input positions (2i + ph, 2j + pw) of parity class (ph, pw) receive only
+// the taps with (ph + pad - r) and (pw + pad - s) even, reading dz at
+// (i + (ph + pad - r)/2, j + (pw + pad - s)/2): per class a stride-1-like
+// implicit GEMM over the Ho x Wo grid with 1, 2 or 4 taps (3x3) -- 9 taps in
+// all instead of the masked formulation's 36.  Out-of-range dz rows are
+// TMA zero-fill; a class without taps (1x1 downsample, odd parity) writes 0.
+// grid (M tiles over Ho x Wo, Cinp / ntile, slots * 4), 256 threads
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb, Net a,
+                                                            ConvK k, int ntile, int Ht, int Nt) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int s = blockIdx.z >> 2, ph = (blockIdx.z >> 1) & 1, pw = blockIdx.z & 1;
+  const Slot sl = a.slots[s];
+  const int cnt = sl.cnt;
+  if (cnt == 0) return;
+  const int HWo = k.Ho * k.Wo, M = cnt * HWo;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * ntile;
+  if (m0 >= M) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = pb::tma::align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t tmem_base;
+  __shared__ int taps[9][3];   // r*R + s, dy, dx
+  __shared__ int ntap;
+  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (tid == 0) {
+    pb::tma::ring_barriers(full, empty, kStages);
+    int n = 0;
+    for (int r = 0; r < k.R; ++r)
+      for (int q = 0; q < k.R; ++q) {
+        const int ey = ph + k.pad - r, ex = pw + k.pad - q;
+        if (ey < 0 || ex < 0 || (ey & 1) || (ex & 1)) continue;
+        taps[n][0] = r * k.R + q;
+        taps[n][1] = ey >> 1;
+        taps[n][2] = ex >> 1;
+        ++n;
+      }
+    ntap = n;
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const int nt = ntap;
+  if (tid == 0 && nt > 0) {
+    const int nn = m0 / HWo, p0 = Nt > 1 ? 0 : (m0 - nn * HWo) / k.Wo;
+    const int ncb = k.Cout / 64, n = nt * ncb;
+    const uint32_t bytes = 128 * 128 + uint32_t(ntile) * 128;
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int ti = c / ncb, cb = c - ti * ncb;
+      pb::tma::expect_tx(f, bytes);
+      pb::tma::load_5d(st, &ta, cb * 64, taps[ti][2], p0 + taps[ti][1], nn, s, f);
+      pb::tma::load_3d(st + 128 * 128, &tb, taps[ti][0] * k.Cout + cb * 64, n0, sl.r, f);
+    };
+    auto mma = [&](int c, uint8_t* st) {
+      const uint64_t a0 = pb::tma::desc_sw128(smem_u32(st)), b0 = pb::tma::desc_sw128(smem_u32(st + 128 * 128));
+      const uint32_t idesc = idesc_bf16(128, ntile);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+    };
+    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+  }
+  __syncthreads();
+  fence_after_sync();
+  const int row = (warp & 3) * 32 + lane, m = m0 + row;
+  const int half = warp >> 2, cols = ntile / 2;
+  const int mn = m / HWo, mi = (m - mn * HWo) / k.Wo, mj = m - mn * HWo - mi * k.Wo;
+  float* dst = at<float>(a, s, k.dx) + ((int64_t(mn) * k.H + 2 * mi + ph) * k.W + 2 * mj + pw) * k.Cinp + n0;
+#pragma unroll 1
+  for (int c16 = 0; c16 < cols; c16 += 16) {
+    float v[16];
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(half * cols + c16), v);
+    if (m < M) {
+      float4* d4 = reinterpret_cast<float4*>(dst + half * cols + c16);
+#pragma unroll
+      for (int i4 = 0; i4 < 4; ++i4)
+        d4[i4] = nt > 0 ? make_float4(v[4 * i4], v[4 * i4 + 1], v[4 * i4 + 2], v[4 * i4 + 3])
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<256>(tmem);
+}
+
+// ---------------------------------------------------------------------------
 // k_rn_wgrad_tma: the stride-1 weight gradient with MN-major SWIZZLE_128B
 // TMA tiles.  D[(r,s,ci)][co] = sum over output positions of
 // x[n, p+r-pad, q+s-pad, ci] dz[n, p, q, co]; K = positions, 64 per stage
@@ -1221,10 +1310,27 @@ size_t gn_smem() { return kGnSmem; }
 int build_maps(Plan& pl, const Net& a, int64_t slots) {
   for (ConvL& c : pl.convs) {
     const ConvK& k = c.k;
-    c.tma = 0;
-    if (k.stride != 1 || k.Cinp % 64 || 128 % k.Wo) continue;
+    c.tma = c.tma_dg = c.tma_wg = 0;
+    if (k.Cinp % 64 || 128 % k.Wo) continue;
     c.Ht = std::min(k.Ho, 128 / k.Wo);
     c.Nt = 128 / (k.Wo * c.Ht);
+    if (k.stride == 2) {   // only the (sub-pixel) data gradient runs on TMA
+      if (k.dx < 0 || k.Cout % 64) continue;
+      const uint64_t dda[5] = {uint64_t(k.Cout), uint64_t(k.Wo), uint64_t(k.Ho), uint64_t(a.BS), uint64_t(slots)};
+      const uint64_t sda[4] = {uint64_t(k.Cout) * 2, uint64_t(k.Wo) * k.Cout * 2,
+                               uint64_t(k.Ho) * k.Wo * k.Cout * 2, uint64_t(a.slot_bytes)};
+      const uint32_t bda[5] = {64, uint32_t(k.Wo), uint32_t(c.Ht), uint32_t(c.Nt), 1};
+      const uint64_t Kd = uint64_t(k.R) * k.R * k.Cout;
+      const uint64_t ddb[3] = {Kd, uint64_t(k.Cinp), uint64_t(slots)};
+      const uint64_t sdb[2] = {Kd * 2, uint64_t(a.P16) * 2};
+      const uint32_t bdb[3] = {64, uint32_t(conv_ntile(k.Cinp)), 1};
+      int rc;
+      if ((rc = pb::tma::make_nd_bf16(&c.tad, a.arena + k.dz, 5, dda, sda, bda)) ||
+          (rc = pb::tma::make_nd_bf16(&c.tbd, a.w16 + a.T16 + k.w16_off, 3, ddb, sdb, bdb)))
+        return rc;
+      c.tma_dg = 2;
+      continue;
+    }
     const uint64_t da[5] = {uint64_t(k.Cinp), uint64_t(k.W), uint64_t(k.H), uint64_t(a.BS), uint64_t(slots)};
     const uint64_t sa[4] = {uint64_t(k.Cinp) * 2, uint64_t(k.W) * k.Cinp * 2, uint64_t(k.H) * k.W * k.Cinp * 2,
                             uint64_t(a.slot_bytes)};
@@ -1284,6 +1390,12 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
     k_rn_conv<FWD><<<g, 256, kCvSmem, s>>>(a, k, nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
+  } else if (mode == DGRAD && c.tma_dg == 2) {
+    const int nt = conv_ntile(k.Cinp);
+    const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cinp / nt, active * 4);
+    pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
+    k_rn_dgrad_s2_tma<<<g, 256, kCvSmem + 1024, s>>>(c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD && c.tma_dg) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
@@ -1447,7 +1559,7 @@ int setup() {
   if (done) return PB_OK;
   const void* fns[] = {(const void*)k_rn_conv<FWD>, (const void*)k_rn_conv<DGRAD>, (const void*)k_rn_conv<WGRAD>,
                        (const void*)k_rn_conv_tma<false>, (const void*)k_rn_conv_tma<true>,
-                       (const void*)k_rn_wgrad_tma};
+                       (const void*)k_rn_wgrad_tma, (const void*)k_rn_dgrad_s2_tma};
   for (const void* fn : fns) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem + 1024));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_conv: ") + cudaGetErrorString(e));
