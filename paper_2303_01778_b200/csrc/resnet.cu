@@ -382,7 +382,9 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
       const int rs = c / ncb, cb = c - rs * ncb, r = rs / k.R, q = rs - r * k.R;
       const int dx = DG ? k.pad - q : q - k.pad, dy = DG ? k.pad - r : r - k.pad;
       pb::tma::expect_tx(f, bytes);
-      pb::tma::load_5d(st, &ta, cb * 64, dx, p0 + dy, nn, s, f);
+      // forward with stride 2: the box spans 2x the rows / columns and the
+      // map's traversal stride 2 loads every other one
+      pb::tma::load_5d(st, &ta, cb * 64, dx, p0 * (DG ? 1 : k.stride) + dy, nn, s, f);
       pb::tma::load_3d(st + 128 * 128, &tb, rs * kc + cb * 64, n0, sl.r, f);
     };
     auto mma = [&](int c, uint8_t* st) {
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__
       pb::tma::expect_tx(f, bytes);
       for (int h = 0; h < na; ++h) {
         const int at_ = a0i + h, rs = at_ / ncb, cb = at_ - rs * ncb, r = rs / k.R, q = rs - r * k.R;
-        pb::tma::load_5d(st + h * 8192, &tx, cb * 64, q - k.pad, p0 + r - k.pad, nn, s, f);
+        pb::tma::load_5d(st + h * 8192, &tx, cb * 64, q - k.pad, p0 * k.stride + r - k.pad, nn, s, f);
       }
       for (int h = 0; h < nb; ++h) pb::tma::load_5d(st + 16384 + h * 8192, &tdz, n0 + h * 64, 0, p0, nn, s, f);
     };
@@ -1329,6 +1331,31 @@ int build_maps(Plan& pl, const Net& a, int64_t slots) {
           (rc = pb::tma::make_nd_bf16(&c.tbd, a.w16 + a.T16 + k.w16_off, 3, ddb, sdb, bdb)))
         return rc;
       c.tma_dg = 2;
+      // forward and weight gradient: input boxes with traversal stride 2
+      const uint64_t da2[5] = {uint64_t(k.Cinp), uint64_t(k.W), uint64_t(k.H), uint64_t(a.BS), uint64_t(slots)};
+      const uint64_t sa2[4] = {uint64_t(k.Cinp) * 2, uint64_t(k.W) * k.Cinp * 2,
+                               uint64_t(k.H) * k.W * k.Cinp * 2, uint64_t(a.slot_bytes)};
+      const uint32_t es2[5] = {1, 2, 2, 1, 1};
+      const uint32_t ba2[5] = {64, uint32_t(2 * k.Wo), uint32_t(2 * c.Ht), uint32_t(c.Nt), 1};
+      const uint64_t K = uint64_t(k.R) * k.R * k.Cinp;
+      const uint64_t db2[3] = {K, uint64_t(k.Cout), uint64_t(slots)};
+      const uint64_t sb2[2] = {K * 2, uint64_t(a.P16) * 2};
+      const uint32_t bb2[3] = {64, uint32_t(conv_ntile(k.Cout)), 1};
+      if ((rc = pb::tma::make_nd_bf16(&c.ta, a.arena + k.in, 5, da2, sa2, ba2, es2)) ||
+          (rc = pb::tma::make_nd_bf16(&c.tb, a.w16 + k.w16_off, 3, db2, sb2, bb2)))
+        return rc;
+      c.tma = 1;
+      c.Hs = std::min(k.Ho, 64 / k.Wo);
+      c.Ns = 64 / (k.Wo * c.Hs);
+      const uint32_t bw2[5] = {64, uint32_t(2 * k.Wo), uint32_t(2 * c.Hs), uint32_t(c.Ns), 1};
+      const uint32_t bwz[5] = {64, uint32_t(k.Wo), uint32_t(c.Hs), uint32_t(c.Ns), 1};
+      const uint64_t dz5[5] = {uint64_t(k.Cout), uint64_t(k.Wo), uint64_t(k.Ho), uint64_t(a.BS), uint64_t(slots)};
+      const uint64_t sz5[4] = {uint64_t(k.Cout) * 2, uint64_t(k.Wo) * k.Cout * 2,
+                               uint64_t(k.Ho) * k.Wo * k.Cout * 2, uint64_t(a.slot_bytes)};
+      if ((rc = pb::tma::make_nd_bf16(&c.twx, a.arena + k.in, 5, da2, sa2, bw2, es2)) ||
+          (rc = pb::tma::make_nd_bf16(&c.twd, a.arena + k.dz, 5, dz5, sz5, bwz)))
+        return rc;
+      c.tma_wg = 1;
       continue;
     }
     const uint64_t da[5] = {uint64_t(k.Cinp), uint64_t(k.W), uint64_t(k.H), uint64_t(a.BS), uint64_t(slots)};

@@ -43,7 +43,7 @@ int make_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows
 }
 
 int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                 const uint32_t* box) {
+                 const uint32_t* box, const uint32_t* estr) {
   EncodeFn fn = encode_fn();
   if (!fn) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (rank < 2 || rank > 5 || (reinterpret_cast<uintptr_t>(base) & 15) || box[0] * 2 != 128)
@@ -53,7 +53,7 @@ int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* d
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    es[i] = 1;
+    es[i] = estr ? estr[i] : 1;
     if (i > 0) {
       st[i - 1] = strides[i - 1];
       if (strides[i - 1] % 16) return fail(PB_ERR_INVALID, "make_nd_bf16: stride not a multiple of 16");

@@ -115,8 +115,10 @@ __device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, i
 // N-D bf16 tensor map with 128-byte swizzle (box inner dimension = 64
 // elements); dims/strides as cuTensorMapEncodeTiled (strides in bytes for
 // dims 1..rank-1), out-of-bounds elements read as 0.
+// estr: per-dimension traversal strides (nullptr = all 1); with a stride e
+// along a dimension the box spans box[i] elements of which every e-th loads.
 int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                 const uint32_t* box);
+                 const uint32_t* box, const uint32_t* estr = nullptr);
 
 }  // namespace tma
 }  // namespace pb
