@@ -27,6 +27,7 @@ codec of the reference are not rebuilt (NCCL replaces them).
 from __future__ import annotations
 
 import math
+import threading
 import time
 from dataclasses import dataclass
 from pathlib import Path
@@ -333,6 +334,7 @@ class SimulationEngine:
         self.store, self.eval_data, self.results_path = store, eval_data, results_path
         self.eval_every = max(1, eval_every)
         self.history = history if history is not None else TimingHistory()
+        self._prefetch = None       # (round, thread, result box) of a round prepared ahead
         self.gauge = ReplicaGauge()
         self.next_round = start_round
         self.sizes = np.array([p.sample_count for p in self.profiles], dtype=np.int64)
@@ -418,7 +420,49 @@ class SimulationEngine:
         """Host half of a round: selection, workload fits, schedule, the
         virtual-clock timing records (added to the history now, exactly the
         records the reference's devices report) and the local clients'
-        minibatch orders.  Deterministic in (seed, round, history)."""
+        minibatch orders.  Deterministic in (seed, round, history).  A round
+        already prepared ahead by run_round is handed out, never re-prepared
+        (its timing records are in the history exactly once)."""
+        inp = self._take_prefetch(round_num)
+        if inp is None:
+            inp = self._prepare(round_num)
+        if self.cfg.clock == "virtual":
+            self._record(inp, None)
+        return inp
+
+    # -- host/device overlap ---------------------------------------------------
+    def _take_prefetch(self, round_num: int) -> "RoundInputs | None":
+        pf = self._prefetch
+        if pf is None:
+            return None
+        self._prefetch = None
+        pf[1].join()
+        if pf[0] != round_num:      # another round was asked for: drop it (no side effects)
+            return None
+        if "exc" in pf[2]:
+            raise pf[2]["exc"]
+        return pf[2]["inp"]
+
+    def _start_prefetch(self, round_num: int) -> None:
+        """Prepare ``round_num`` on a helper thread (virtual clock only: its
+        plan and minibatch orders depend on the history up to the previous
+        round, whose records are already in; its own records are added when
+        the round is handed out, so an unconsumed prefetch leaves no trace)."""
+        if self._prefetch is not None:
+            return
+        box: dict = {}
+
+        def work():
+            try:
+                box["inp"] = self._prepare(round_num)
+            except BaseException as exc:  # re-raised by the consumer
+                box["exc"] = exc
+
+        t = threading.Thread(target=work, name=f"prepare-round-{round_num}", daemon=True)
+        self._prefetch = (round_num, t, box)
+        t.start()
+
+    def _prepare(self, round_num: int) -> "RoundInputs":
         cfg = self.cfg
         wall0 = time.perf_counter()
         selection = select_clients(cfg, round_num)
@@ -443,8 +487,6 @@ class SimulationEngine:
             assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
         inp = RoundInputs(round_num, selection, sizes, fits, fit_seconds, schedule_seconds, plan,
                           fa_tasks, assign, self.runtime.prepare(assign, round_num), wall0)
-        if cfg.clock == "virtual":
-            self._record(inp, None)
         return inp
 
     def _record(self, inp: "RoundInputs", measured_per_client: float | None) -> None:
@@ -521,7 +563,13 @@ class SimulationEngine:
         return outcome
 
     def run_round(self, round_num: int) -> RoundOutcome:
-        return self.execute_round(self.prepare_round(round_num))
+        """One round through the public API.  Under the virtual clock the
+        next round's host half (selection, fits, schedule, minibatch orders)
+        runs on a helper thread while this round's kernels execute."""
+        inp = self.prepare_round(round_num)
+        if self.cfg.clock == "virtual" and round_num + 1 < self.cfg.total_rounds:
+            self._start_prefetch(round_num + 1)
+        return self.execute_round(inp)
 
     @staticmethod
     def io_bytes() -> tuple[int, int]:

@@ -317,3 +317,26 @@ def test_counters_and_replicas(pb):
         assert oc.costs.bytes_avg_params == 2 * 8 * (3 * 4 + 3)
         # all six clients of the round are live on the GPU at once (documented)
         assert oc.costs.peak_live_model_replicas == 6
+
+
+def test_engine_prefetch_matches_sequential(pb):
+    """run_round prepares round r+1 on a helper thread while round r runs:
+    globals, loads and the timing history equal the sequential
+    prepare/execute path, and an unconsumed prefetch leaves no records."""
+    ds = pb.generate(600, 6, 4, seed=9)
+    profiles = pb.partition(ds, 30, pb.PartitionSpec(quantity_skew=0.3), seed=9)
+    kw = dict(scheduling="time-window", time_window=2,
+              device_kw=dict(hetero=[0.0, 0.4, 0.8], noise=0.05))
+    a = _engine(pb, "PARROT", 3, profiles, 6, 9, 12, pb.FedAvg(lr=0.1, batch_size=5), **dict(kw))
+    b = _engine(pb, "PARROT", 3, profiles, 6, 9, 12, pb.FedAvg(lr=0.1, batch_size=5), **dict(kw))
+    outs_a = a.run(rounds=4)
+    outs_b = [b.execute_round(b.prepare_round(r)) for r in range(4)]
+    for oa, ob in zip(outs_a, outs_b):
+        assert oa.device_loads == ob.device_loads and oa.scheduling_mode == ob.scheduling_mode
+        for name in ("weights", "bias"):
+            assert np.array_equal(oa.new_global.numpy(name), ob.new_global.numpy(name))
+    assert a.history.size == b.history.size and not a.history.round_records(4)
+    for r in range(4):
+        ra = [(x.device_id, x.client_id, x.reported_seconds) for x in a.history.round_records(r)]
+        rb = [(x.device_id, x.client_id, x.reported_seconds) for x in b.history.round_records(r)]
+        assert ra == rb
