@@ -309,6 +309,12 @@ int pb_tma_tf32_selftest(const float* A, const float* B, float* D, int N, int K,
  * byte offsets under test (tests only).  N % 64 == 0, K % 64 == 0. */
 int pb_tma_bf16_mn_selftest(const void* A, const void* B, float* D, int N, int K, int lbo, int sbo, void* stream);
 
+/* TMA read-bandwidth probe (tools only): `ctas` CTAs stream `nbox` 16 KB
+ * boxes each from a [rows, cols] f32 buffer; mode 0 = boxes of 128 rows x
+ * 128 B at row pitch cols*4, mode 1 = the same bytes as contiguous tiles. */
+int pb_tma_bw_probe(const float* base, int mode, int64_t rows, int64_t cols, int ctas, int nbox,
+                    unsigned* sink, void* stream);
+
 /* 128 x N x K tf32 tcgen05 GEMM D = A * B^T from fp32 row-major A [128,K],
  * B [N,K]; a_mn/b_mn select MN-major smem staging (tests only). */
 int pb_umma_tf32_selftest(const float* A, const float* B, float* D, int N, int K, int a_mn,

@@ -105,6 +105,7 @@ _SIGS = {
     "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
     "pb_umma_bench_multi": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "pb_tma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
+    "pb_tma_bw_probe": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "pb_tma_bf16_mn_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                                         c_void_p]),
     "pb_rn_conv_selftest": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,

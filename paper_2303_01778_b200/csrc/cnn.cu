@@ -23,6 +23,8 @@
 //                positions) + update; conv1 wgrad/biases (SIMT) + update
 // Operands are bf16 with fp32 accumulation in TMEM; master weights, biases,
 // losses and all non-GEMM math are fp32 (loss reduction in double).
+#include <cooperative_groups.h>
+
 #include "cnn_common.cuh"
 
 namespace {
@@ -513,6 +515,203 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   }
 }
 
+// k_head_tail: the head of a sparse tail sweep.  One cluster of 8 CTAs per
+// client; CTA p owns fc1 outputs [64p, 64p+64).  Each CTA computes partial
+// logits over its outputs, the cluster sums them in part order through
+// distributed shared memory, every CTA then derives the same softmax / dlogits
+// and updates its 64 columns of fc2 (dH from 4 class groups, summed in group
+// order).  grid (8, active), cluster (8, 1, 1), 256 threads
+constexpr int kTailParts = 8;
+constexpr int kTailO = kH1 / kTailParts;   // 64
+constexpr int kTailCg = kHeadThreads / kTailO;   // 4 class groups
+constexpr int kTailS = kTailO + 4;         // padded smem row (conflict-free 16 B loads)
+__host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }
+static size_t head_tail_smem(int C, int BS) {
+  return (size_t(BS) * (2 * kTailS + kTailCg * kTailO + 2 * pad4(C)) + size_t(C) * kTailS + pad4(C)) * 4 +
+         size_t(BS) * 8;
+}
+
+__device__ __forceinline__ float nan_max(float x, float y) { return x != x ? x : (y != y ? y : fmaxf(x, y)); }
+
+__global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThreads) k_head_tail(Args a) {
+  namespace cgp = cooperative_groups;
+  cgp::cluster_group cluster = cgp::this_cluster();
+  const int slot = blockIdx.y, part = blockIdx.x;
+  const int olo = part * kTailO;
+  const Slot sl = a.slots[slot];
+  if (sl.cnt == 0) return;   // uniform over the cluster (same slot)
+  extern __shared__ __align__(16) float hs[];
+  const int C = a.C, Cp = pad4(C), BS = a.BS, cnt = sl.cnt, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* sH = hs;                          // [BS][kTailS] this CTA's h columns
+  float* sDH = sH + BS * kTailS;           // [BS][kTailS]
+  float* sAcc = sDH + BS * kTailS;         // [4][BS][64] dH partials per class group
+  float* sLp = sAcc + kTailCg * BS * kTailO;   // [BS][Cp] partial logits
+  float* sL = sLp + BS * Cp;               // [BS][Cp] logits -> dlogits (pad columns 0)
+  float* sW2 = sL + BS * Cp;               // [C][kTailS] this CTA's fc2 columns
+  float* sB2 = sW2 + C * kTailS;           // [Cp] fc2 bias
+  double* sLoss = reinterpret_cast<double*>(sB2 + Cp);   // [BS]
+  __shared__ int s_bad;
+  float* W = a.w + int64_t(sl.r) * a.P;
+  const float* W2 = W + oF2W;
+  // every global read of the kernel up front: h and fc2 column slices, fc2 bias
+  {
+    const float* hrow = a.h + sidx(slot, 0, BS) * kH1 + olo;
+    for (int e = tid; e < cnt * kTailO; e += kHeadThreads) sH[(e >> 6) * kTailS + (e & 63)] = hrow[(e >> 6) * kH1 + (e & 63)];
+    for (int e = tid; e < C * kTailO; e += kHeadThreads)
+      sW2[(e >> 6) * kTailS + (e & 63)] = W2[int64_t(e >> 6) * kH1 + olo + (e & 63)];
+    for (int c = tid; c < C; c += kHeadThreads) sB2[c] = W2[int64_t(C) * kH1 + c];
+  }
+  __syncthreads();
+  // partial logits over this CTA's 64 outputs: one thread per (sample, class)
+  for (int e = tid; e < cnt * C; e += kHeadThreads) {
+    const int i = e / C, c = e - i * C;
+    const float4* h4 = reinterpret_cast<const float4*>(sH + i * kTailS);
+    const float4* w4 = reinterpret_cast<const float4*>(sW2 + c * kTailS);
+    float v0 = 0.0f, v1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kTailO / 4; k += 2) {
+      const float4 h0 = h4[k], x0 = w4[k], h1 = h4[k + 1], x1 = w4[k + 1];
+      v0 = fmaf(h0.x, x0.x, v0); v0 = fmaf(h0.y, x0.y, v0); v0 = fmaf(h0.z, x0.z, v0); v0 = fmaf(h0.w, x0.w, v0);
+      v1 = fmaf(h1.x, x1.x, v1); v1 = fmaf(h1.y, x1.y, v1); v1 = fmaf(h1.z, x1.z, v1); v1 = fmaf(h1.w, x1.w, v1);
+    }
+    sLp[i * Cp + c] = v0 + v1;
+  }
+  cluster.sync();   // every part's partial logits are visible cluster-wide
+  for (int e = tid; e < cnt * Cp; e += kHeadThreads) {
+    const int c = e % Cp;
+    if (c >= C) {
+      sL[e] = 0.0f;
+      continue;
+    }
+    float p[kTailParts];
+#pragma unroll
+    for (int q = 0; q < kTailParts; ++q) p[q] = cluster.map_shared_rank(sLp, q)[e];
+    float v = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kTailParts; ++q) v += p[q];
+    sL[e] = v + sB2[c];
+  }
+  cluster.sync();   // remote reads done before any CTA moves on / exits
+  // softmax-CE and dlogits: one warp per sample, lanes over classes
+  const float inv = 1.0f / float(cnt);
+  for (int i = warp; i < cnt; i += kHeadThreads / 32) {
+    float* z = sL + i * Cp;
+    const int y = a.Y[a.order[sl.row_off + i]];
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = nan_max(m, z[c]);
+    for (int off = 16; off > 0; off >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float se = 0.0f;
+    for (int c = lane; c < C; c += 32) se += expf(z[c] - m);
+    for (int off = 16; off > 0; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
+    const float lse = logf(se);
+    if (lane == 0) sLoss[i] = double(lse) - double(z[y] - m);
+    __syncwarp();
+    for (int c = lane; c < C; c += 32) z[c] = (expf(z[c] - m - lse) - (c == y ? 1.0f : 0.0f)) * inv;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double lsum = 0.0;
+    for (int i = 0; i < cnt; ++i) lsum += sLoss[i];
+    const double loss = lsum / double(cnt);
+    s_bad = !isfinite(loss);
+    if (part != 0) {
+    } else if (s_bad) {
+      a.bad[sl.r] = a.steps[sl.r];
+    } else {
+      a.loss_sum[sl.r] += loss;
+      a.steps[sl.r] += 1;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (part == 0 && tid == 0) a.slots[slot].cnt = 0;
+    return;
+  }
+  // dH partials and the fc2 update of this CTA's 64 columns: thread = (column,
+  // class group), 16 classes per pass with their weights and gradients in
+  // registers; each (class, column) weight is owned by one thread
+  {
+    const int ol = tid & (kTailO - 1), grp = tid / kTailO, o = olo + ol;
+    const int cq = pad4((C + kTailCg - 1) / kTailCg), cA = min(C, grp * cq), cB = min(C, cA + cq);
+    float* acc_out = sAcc + grp * BS * kTailO + ol;
+    for (int c0 = cA; c0 < cB; c0 += 16) {
+      float w[16], g[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        w[u] = c0 + u < cB ? sW2[(c0 + u) * kTailS + ol] : 0.0f;
+        g[u] = 0.0f;
+      }
+      for (int i = 0; i < cnt; ++i) {
+        const float h = sH[i * kTailS + ol];
+        const float4* d4 = reinterpret_cast<const float4*>(sL + i * Cp + c0);
+        float d[16];
+#pragma unroll
+        for (int u4 = 0; u4 < 4; ++u4) {
+          const float4 t = c0 + 4 * u4 < Cp ? d4[u4] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          d[4 * u4] = t.x;
+          d[4 * u4 + 1] = t.y;
+          d[4 * u4 + 2] = t.z;
+          d[4 * u4 + 3] = t.w;
+        }
+        float s = c0 == cA ? 0.0f : acc_out[i * kTailO];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          s = fmaf(d[u], w[u], s);
+          g[u] = fmaf(d[u], h, g[u]);
+        }
+        acc_out[i * kTailO] = s;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (c0 + u < cB) {
+          const int64_t idx = oF2W + int64_t(c0 + u) * kH1 + o;
+          W[idx] = sgd(a, sl.r, idx, w[u], g[u]);
+        }
+    }
+    if (cA == cB)
+      for (int i = 0; i < cnt; ++i) acc_out[i * kTailO] = 0.0f;
+  }
+  __syncthreads();
+  const int64_t lzrow = sl.hist + int64_t(a.step) * BS;
+  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(slot, 0, BS) * kH1;
+  for (int e = tid; e < cnt * kTailO; e += kHeadThreads) {
+    const int i = e >> 6, c = e & 63;
+    float v = sAcc[i * kTailO + c];
+#pragma unroll
+    for (int q = 1; q < kTailCg; ++q) v += sAcc[(q * BS + i) * kTailO + c];
+    float gi = sH[i * kTailS + c] > 0.0f ? v : 0.0f;
+    if (a.hx) gi = tf32_rna(gi);
+    dh[int64_t(i) * kH1 + olo + c] = gi;
+    sDH[i * kTailS + c] = gi;
+  }
+  __syncthreads();
+  if (a.hx) {
+    float* hdt = a.hdt + sl.hist + int64_t(a.step) * BS;
+    for (int p = tid; p < cnt * kTailO; p += kHeadThreads) {
+      const int oo = p / cnt, i = p - oo * cnt;
+      hdt[int64_t(olo + oo) * a.hrows + i] = sDH[i * kTailS + oo];
+    }
+    for (int oo = tid; oo < kTailO; oo += kHeadThreads) {   // fc1 bias (sample order)
+      float g = 0.0f;
+      for (int i = 0; i < cnt; ++i) g += sDH[i * kTailS + oo];
+      const int64_t idx = oF1B + olo + oo;
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+    }
+  } else {
+    float* dht = a.dht + int64_t(slot) * kH1 * 32;
+    for (int p = tid; p < kTailO * 32; p += kHeadThreads) {
+      const int oo = p >> 5, i = p & 31;
+      dht[int64_t(olo + oo) * 32 + i] = i < cnt ? sDH[i * kTailS + oo] : 0.0f;
+    }
+  }
+  for (int c = tid; c < (part == 0 ? C : 0); c += kHeadThreads) {
+    float g = 0.0f;
+    for (int i = 0; i < cnt; ++i) g += sL[i * Cp + c];
+    const int64_t idx = oF2W + int64_t(C) * kH1 + c;
+    W[idx] = sgd(a, sl.r, idx, sB2[c], g);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // k_fc1_bwd: one pass over a 64-column slice of W1 per CTA (tf32 UMMA):
 //   dgrad  D1[k][i] = sum_o W1[o][k] dH[i][o]   (M=64, N=32, K=512, 8 stages)
@@ -966,29 +1165,36 @@ __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* bu
 //          output positions; double-buffered sample staging overlaps the
 //          MMAs) + update;
 //          x == nsplit: sum the per-sample conv1/bias partials (sample order) + update
-// grid (nsplit + 1, active), 256 threads; nsplit = 2 (ky 0-2 | 3-4) or 5
-__global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
+// Sparse sweeps split each client's samples over a cluster of sg CTAs per
+// split: every CTA computes the partial gradient of its samples, then CTA r
+// sums the sg partials (cluster rank order, distributed shared memory) for
+// its share of the co rows and applies the update.
+// grid ((nsplit + 1) * sg, active), cluster (sg, 1, 1), 256 threads;
+// nsplit = 2 (ky 0-2 | 3-4) or 5
+__global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit, int sg) {
   const Slot sl = a.slots[blockIdx.y];
-  if (sl.cnt == 0) return;
+  if (sl.cnt == 0) return;   // uniform over a cluster (same slot)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cnt = sl.cnt;
+  const int split = blockIdx.x / sg, rank = blockIdx.x - split * sg;
+  const int i_lo = rank * sl.cnt / sg, i_hi = (rank + 1) * sl.cnt / sg;
+  const int cnt = i_hi - i_lo;
   float* W = a.w + int64_t(sl.r) * a.P;
   const int64_t s0 = sidx(blockIdx.y, 0, a.BS);
-  if (blockIdx.x == nsplit) {
-    for (int k = tid; k < kPg; k += 256) {
+  if (split == nsplit) {
+    for (int k = rank * kPg / sg + tid; k < (rank + 1) * kPg / sg; k += 256) {
       float g = 0.0f;
 #pragma unroll 8
-      for (int i = 0; i < cnt; ++i) g += a.pg[(s0 + i) * kPg + k];
+      for (int i = 0; i < sl.cnt; ++i) g += a.pg[(s0 + i) * kPg + k];
       const int64_t idx = k < 800 ? oC1W + k : (k < 832 ? oC1B + (k - 800) : oC2B + (k - 832));
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
     return;
   }
-  const int ky0 = nsplit == 2 ? blockIdx.x * 3 : blockIdx.x;
-  const int nky = nsplit == 2 ? (blockIdx.x == 0 ? 3 : 2) : 1;
+  const int ky0 = nsplit == 2 ? split * 3 : split;
+  const int nky = nsplit == 2 ? (split == 0 ? 3 : 2) : 1;
   const int tap0 = ky0 * 5, ntap = nky * 5;
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -1001,12 +1207,12 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
   const uint32_t tmem = tmem_base;
   const uint32_t idesc64 = idesc_bf16(64, 64, true, true);
   const uint32_t idesc32 = idesc_bf16(64, 32, true, true);
-  wg_stage(a, s0, smem, tid);
+  if (cnt > 0) wg_stage(a, s0 + i_lo, smem, tid);
   for (int i = 0; i < cnt; ++i) {
     uint8_t* buf = smem + (i & 1) * kWgBuf;
     if (i + 1 < cnt) {
       if (i >= 1) mbar_wait(&mbar, (i - 1) & 1);  // MMAs of sample i-1 read the other buffer
-      wg_stage(a, s0 + i + 1, smem + ((i + 1) & 1) * kWgBuf, tid);
+      wg_stage(a, s0 + i_lo + i + 1, smem + ((i + 1) & 1) * kWgBuf, tid);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -1035,7 +1241,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
       commit(&mbar);
     }
   }
-  mbar_wait(&mbar, (cnt - 1) & 1);
+  if (cnt > 0) mbar_wait(&mbar, (cnt - 1) & 1);
   fence_after_sync();
   // epilogue: TMEM (M=64 rows in lanes 32q + [0,16)) -> smem tile [64][ntap*32]
   // -> coalesced SGD update of the contiguous W2[co][tap0*32 ...] row segments
@@ -1050,6 +1256,9 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
 #pragma unroll
       for (int c16 = 0; c16 < 2; ++c16) {
         tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(tl * 32 + c16 * 16), v);
+        if (cnt == 0)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = 0.0f;
         if (lane < 16) {
 #pragma unroll
           for (int k = 0; k < 16; ++k) sG[co * kWgStride + tl * 32 + c16 * 16 + k] = v[k];
@@ -1059,27 +1268,39 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit) {
   }
   fence_before_sync();
   __syncthreads();
-  // SGD on W2[co][tap0*32 ...]: 8 independent loads in flight per thread
-  for (int e0 = tid; e0 < 64 * width; e0 += 8 * 256) {
+  // SGD on W2[co][tap0*32 ...] for this CTA's co rows: 8 independent loads in
+  // flight per thread; with sg > 1 the gradient is the sum of the cluster's
+  // partial tiles in rank order
+  namespace cgp = cooperative_groups;
+  if (sg > 1) cgp::this_cluster().sync();
+  const int co_lo = rank * 64 / sg, n_e = ((rank + 1) * 64 / sg - co_lo) * width;
+  for (int e0 = tid; e0 < n_e; e0 += 8 * 256) {
     float wv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int e = e0 + k * 256;
-      if (e < 64 * width) {
-        const int co = e / width, c = e - co * width;
+      if (e < n_e) {
+        const int co = co_lo + e / width, c = e % width;
         wv[k] = W[oC2W + int64_t(co) * 800 + tap0 * 32 + c];
       }
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int e = e0 + k * 256;
-      if (e < 64 * width) {
-        const int co = e / width, c = e - co * width;
+      if (e < n_e) {
+        const int co = co_lo + e / width, c = e % width;
         const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
-        W[idx] = sgd(a, sl.r, idx, wv[k], sG[co * kWgStride + c]);
+        float g = sG[co * kWgStride + c];
+        if (sg > 1) {
+          cgp::cluster_group cl = cgp::this_cluster();
+          g = cl.map_shared_rank(sG, 0)[co * kWgStride + c];
+          for (int q = 1; q < sg; ++q) g += cl.map_shared_rank(sG, q)[co * kWgStride + c];
+        }
+        W[idx] = sgd(a, sl.r, idx, wv[k], g);
       }
     }
   }
+  if (sg > 1) cgp::this_cluster().sync();   // partner tiles stay alive until every read is done
   fence_before_sync();
   __syncthreads();
   if (warp == 0) tmem_free<512>(tmem);
@@ -1104,6 +1325,7 @@ static int cnn_setup() {
   if ((rc = set_smem((const void*)k_bwd_conv, kBwdSmem, "k_bwd_conv"))) return rc;
   if ((rc = set_smem((const void*)k_wgrad, kWgSmem, "k_wgrad"))) return rc;
   if ((rc = set_smem((const void*)k_head, 200 * 1024, "k_head"))) return rc;
+  if ((rc = set_smem((const void*)k_head_tail, head_tail_smem(128, 32), "k_head_tail"))) return rc;
   if ((rc = set_smem((const void*)k_fc1_bwd, kF1BwdSmem, "k_fc1_bwd"))) return rc;
   if ((rc = set_smem((const void*)k_fc1_fwd, kF1FwdSmem, "k_fc1_fwd"))) return rc;
   done = 1;
@@ -1151,8 +1373,12 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::prof_end(pb::K_CNN_FC1_FWD, s);
   }
   pb::prof_begin(pb::K_CNN_HEAD, s);
-  const int hparts = active < kWgTailActive ? 4 : 1;
-  k_head<<<dim3(hparts, active), kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+  if (train && active < kWgTailActive) {
+    k_head_tail<<<dim3(kTailParts, active), kHeadThreads, head_tail_smem(a.C, a.BS), s>>>(a);
+  } else {
+    const int hparts = active < kWgTailActive ? 4 : 1;
+    k_head<<<dim3(hparts, active), kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+  }
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
   if (a.hx) {
@@ -1169,7 +1395,26 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
   const int wsplit = active < kWgTailActive ? 5 : 2;
-  k_wgrad<<<dim3(wsplit + 1, active), 256, kWgSmem, s>>>(a, wsplit);
+  // sparse sweeps: split each client's samples over a cluster while the grid
+  // still fits one wave
+  const int wsg = wsplit == 5 ? std::max(1, std::min(4, sms / ((wsplit + 1) * active))) : 1;
+  if (wsg == 1) {
+    k_wgrad<<<dim3(wsplit + 1, active), 256, kWgSmem, s>>>(a, wsplit, 1);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((wsplit + 1) * wsg), unsigned(active));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kWgSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(wsg);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_wgrad, a, wsplit, wsg);
+  }
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
 }

@@ -27,6 +27,8 @@
 // map.  One thread drives a TMA -> MMA ring; the CTA's other warps only run
 // the epilogues.  Reductions have a fixed order (no atomics): results are
 // deterministic.
+#include <cooperative_groups.h>
+
 #include "cnn_common.cuh"
 #include "tma.cuh"
 
@@ -102,7 +104,11 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 //   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][i][j] = -lr * Gd
 // History rows j >= t*BS (the current step, later steps, other clients) are
 // zeroed when the Gram tile leaves TMEM.
-// grid (njt, active), 128 threads
+// Sparse sweeps split the forward Gram's K over a cluster of ks CTAs per
+// tile: each computes a partial Gram, all of them sum the ks partials in rank
+// order (distributed shared memory), and CTA r runs phase B for o-quarters
+// [4r/ks, 4(r+1)/ks).
+// grid (njt * ks, active), cluster (ks, 1, 1), 128 threads
 // ---------------------------------------------------------------------------
 constexpr int kGrA = 128 * 128;                // 16 KB: 128 rows x 32 fp32 (one K atom)
 constexpr int kGrB = 32 * 128;                 // 4 KB
@@ -113,8 +119,8 @@ constexpr size_t kGramFwdSmem = 1024 + kGrStages * kGrStage + kGxT;
 constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
 
 template <bool FWD>
-__global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMaps m, Args a) {
-  const int s = blockIdx.y, jt = blockIdx.x;   // a client's history tiles are adjacent
+__global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMaps m, Args a, int ks) {
+  const int s = blockIdx.y, jt = blockIdx.x / ks, rank = blockIdx.x - jt * ks;   // a client's tiles are adjacent
   const Slot sl = a.slots[s];
   const int cnt = sl.cnt;
   if (cnt == 0) return;
@@ -143,13 +149,14 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   const CUtensorMap* tb = FWD ? &m.hxb : &m.hdb;
   if (tid == 0) {
     const uint32_t bytes = uint32_t(2 * (nsub + 1) * 32 * 128);
+    const int ca = rank * nA / ks;
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, bytes);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint8_t* sh = st + h * (kGrA + kGrB);
-        pb::tma::load_2d(sh, ta, (2 * c + h) * 32, hrow, f);
-        pb::tma::load_2d(sh + kGrA, tb, (2 * c + h) * 32, crow, f);
+        pb::tma::load_2d(sh, ta, (2 * (ca + c) + h) * 32, hrow, f);
+        pb::tma::load_2d(sh + kGrA, tb, (2 * (ca + c) + h) * 32, crow, f);
       }
     };
     auto mma = [&](int c, uint8_t* st) {
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
           mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
       }
     };
-    tma_ring<kGrStages>(nA, smem, kGrStage, full, empty, issue, mma);
+    tma_ring<kGrStages>((rank + 1) * nA / ks - ca, smem, kGrStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -173,6 +180,24 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   float v[32];
   tmem_ld16(tmem + (uint32_t(warp * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
   tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
+  if (ks > 1) {
+    // partial Grams -> the (now idle) ring memory; every CTA sums them in rank order
+    namespace cgp = cooperative_groups;
+    cgp::cluster_group cl = cgp::this_cluster();
+    float* sGp = reinterpret_cast<float*>(smem);   // [128 j][33]
+#pragma unroll
+    for (int i = 0; i < 32; ++i) sGp[j * 33 + i] = v[i];
+    cl.sync();
+    const float* g0p = cl.map_shared_rank(sGp, 0);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = g0p[j * 33 + i];
+    for (int r = 1; r < ks; ++r) {
+      const float* gp = cl.map_shared_rank(sGp, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += gp[j * 33 + i];
+    }
+    cl.sync();   // partner partials read: the ring memory may be reused
+  }
   if (FWD) {
     // Gx^T (B operand of phase B, SWIZZLE_128B K-major: atom j/32, row i)
     uint8_t* atom = sGxT + (j >> 5) * (32 * 128);
@@ -186,12 +211,13 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
       fence_after_sync();
       const int hcol = int(sl.hist) + j0;
       // K chunks (32 history columns) past the live rows contribute zero: skipped
-      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = q*nsub + jc
+      const int q0 = rank * 4 / ks;
+      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = (q - q0)*nsub + jc
         pb::tma::expect_tx(f, kGrA);
-        pb::tma::load_2d(st, &m.hdt, hcol + (c % nsub) * 32, (c / nsub) * 128, f);
+        pb::tma::load_2d(st, &m.hdt, hcol + (c % nsub) * 32, (q0 + c / nsub) * 128, f);
       };
       auto mma = [&](int c, uint8_t* st) {
-        const int q = c / nsub, jc = c % nsub;
+        const int q = q0 + c / nsub, jc = c % nsub;
         const uint64_t a0 = desc_sw128(smem_u32(st));
         const uint64_t b0 = desc_sw128(smem_u32(sGxT + jc * 32 * 128));
         const uint32_t idesc = idesc_tf32(128, 32);
@@ -199,13 +225,13 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
         for (int kk = 0; kk < 4; ++kk)
           mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
       };
-      tma_ring<kStages>(4 * nsub, smem, kGrA, full2, empty2, issue, mma);
+      tma_ring<kStages>(((rank + 1) * 4 / ks - q0) * nsub, smem, kGrA, full2, empty2, issue, mma);
     }
     __syncthreads();
     fence_after_sync();
     float* zp = a.zp + (int64_t(s) * njt + jt) * kH1 * 32;
 #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
+    for (int q = rank * 4 / ks; q < (rank + 1) * 4 / ks; ++q) {
       const int o = q * 128 + warp * 32 + lane;
       float w[32];
       tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(32 + q * 32), *reinterpret_cast<float(*)[16]>(w));
@@ -333,27 +359,56 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
   if (warp == 0) tmem_free<256>(tmem);
 }
 
-// k_lz_fwd_epi: sum the ks split-K partials (split order), then as above.
-// grid (active), 512 threads (one per o)
-__global__ void __launch_bounds__(512) k_lz_fwd_epi(Args a, int active, int ks) {
-  const int s = blockIdx.x, o = threadIdx.x;
+// k_lz_fwd_epi: sum the ks split-K partials (split order), + b1 + the
+// history corrections zp (tile order), relu.  One thread per (o, 4 rows):
+// all of a thread's partial loads are independent and in flight together.
+// grid (active, kH1 * 8 / 256), 256 threads
+constexpr int kEpiThreads = 256;
+__global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, int ks) {
+  const int s = blockIdx.x, t = blockIdx.y * kEpiThreads + threadIdx.x;
+  const int o = t >> 3, i4 = t & 7;
   const Slot sl = a.slots[s];
-  if (sl.cnt == 0) return;
-  float v[32];
+  if (sl.cnt == 0 || i4 * 4 >= sl.cnt) return;
+  float4 p[kFwdSplitMax];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-  for (int kz = 0; kz < ks; ++kz) {
-    const float4* p = reinterpret_cast<const float4*>(a.fpart + ((int64_t(kz) * active + s) * kH1 + o) * 32);
+  for (int kz = 0; kz < kFwdSplitMax; ++kz)
+    if (kz < ks) p[kz] = reinterpret_cast<const float4*>(a.fpart + ((int64_t(kz) * active + s) * kH1 + o) * 32)[i4];
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
-    for (int i4 = 0; i4 < 8; ++i4) {
-      const float4 z = p[i4];
-      v[4 * i4] += z.x;
-      v[4 * i4 + 1] += z.y;
-      v[4 * i4 + 2] += z.z;
-      v[4 * i4 + 3] += z.w;
+  for (int kz = 0; kz < kFwdSplitMax; ++kz)
+    if (kz < ks) {
+      v.x += p[kz].x;
+      v.y += p[kz].y;
+      v.z += p[kz].z;
+      v.w += p[kz].w;
     }
+  const float b = a.w[int64_t(sl.r) * a.P + oF1B + o];
+  v.x += b;
+  v.y += b;
+  v.z += b;
+  v.w += b;
+  const int njt = njt_of(a);
+  const float4* zp = reinterpret_cast<const float4*>(a.zp + (int64_t(s) * njt * kH1 + o) * 32) + i4;
+  constexpr int kU = 8;
+  for (int j0 = 0; j0 < njt; j0 += kU) {
+    float4 z[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j0 + u < njt) z[u] = zp[int64_t(j0 + u) * kH1 * 8];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j0 + u < njt) {
+        v.x += z[u].x;
+        v.y += z[u].y;
+        v.z += z[u].z;
+        v.w += z[u].w;
+      }
   }
-  fwd_finish(a, s, sl, o, v, njt_of(a));
+  float* h = a.h + (sidx(s, 0, a.BS) + i4 * 4) * kH1 + o;
+  const float r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (i4 * 4 + q < sl.cnt) h[int64_t(q) * kH1] = relu_nan(r[q]);
 }
 
 // ---------------------------------------------------------------------------
@@ -373,6 +428,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = blockIdx.x * 128, g0 = blockIdx.y * spc;
+  if (spc == 1 && a.slots[g0].cnt == 0) return;
   if (tid < kSh8) {
     Slot z{};
     sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
@@ -386,7 +442,9 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   const int t = a.step, jlim = t * a.BS;
   const int nj = (jlim + 63) >> 6;               // phase-2 stages per slot (two K atoms each)
   const int64_t tb = int64_t(t) * a.BS;
-  constexpr int n1 = kH1 / 32;                   // 16
+  // phase-1 stages: one K atom for 8 slots, two for a single slot (the same
+  // 40 KB stage as phase 2, twice the bytes in flight)
+  const int n1 = spc == 1 ? kH1 / 64 : kH1 / 32;
   if (tid == 0) {
     int us[kSh8], rows[kSh8], nv = 0;
     for (int u = 0; u < spc; ++u) {
@@ -395,7 +453,14 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
     }
     const int n = n1 + (t > 0 ? nv * nj : 0);
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      if (c < n1) {
+      if (c < n1 && spc == 1) {
+        pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pb::tma::load_2d(st + h * kShA, &m.w0t, (2 * c + h) * 32, k0, f);
+          pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.hdb, (2 * c + h) * 32, rows[0], f);
+        }
+      } else if (c < n1) {
         pb::tma::expect_tx(f, uint32_t(kShA + nv * 32 * 128));
         pb::tma::load_2d(st, &m.w0t, c * 32, k0, f);
         for (int u = 0; u < spc; ++u)
@@ -412,7 +477,17 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
-      if (c < n1) {
+      if (c < n1 && spc == 1) {
+        const uint32_t idesc = idesc_tf32(128, 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t ah = desc_sw128(smem_u32(st + h * kShA));
+          const uint64_t bh = desc_sw128(smem_u32(st + 2 * kShA + h * 32 * 128));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_tf32(tmem, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
+        }
+      } else if (c < n1) {
         const uint32_t idesc = idesc_tf32(128, spc * 32);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -686,7 +761,26 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     pb::prof_end(pb::K_CNN_LZ_XT, s);
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, s);
-      k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(m, a);
+      // sparse sweeps: split K over a cluster while the grid fits one wave
+      const int sms = pb::sm_count();
+      const int gks = njt * active * 4 <= sms ? 4 : (njt * active * 2 <= sms ? 2 : 1);
+      if (gks == 1) {
+        k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(m, a, 1);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(njt * gks), unsigned(active));
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = kGramFwdSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(gks);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_lz_gram<true>, m, a, gks);
+      }
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
@@ -695,7 +789,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (ks > 1) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
-      k_lz_fwd_epi<<<active, kH1, 0, s>>>(a, active, ks);
+      k_lz_fwd_epi<<<dim3(active, kH1 * 8 / kEpiThreads), kEpiThreads, 0, s>>>(a, active, ks);
       pb::prof_end(pb::K_CNN_LZ_FWD, s);
     }
   } else {
@@ -704,7 +798,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
                                     uint64_t(njt) * 128, 32);
       if (rc) return rc;
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
-      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(m, a);
+      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(m, a, 1);
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);

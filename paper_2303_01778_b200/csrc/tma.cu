@@ -42,6 +42,27 @@ int make_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows
   return PB_OK;
 }
 
+int make_nd_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                const uint32_t* box) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (rank < 2 || rank > 5 || (reinterpret_cast<uintptr_t>(base) & 15) || box[0] != 32)
+    return fail(PB_ERR_INVALID, "make_nd_f32: bad rank, alignment or box");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i > 0) st[i - 1] = strides[i - 1];
+  }
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<void*>(base), d, st, b, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled (f32 nd) failed: " + std::to_string(int(r)));
+  return PB_OK;
+}
+
 int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                  const uint32_t* box, const uint32_t* estr) {
   EncodeFn fn = encode_fn();
@@ -219,4 +240,66 @@ extern "C" int pb_tma_bf16_mn_selftest(const void* A, const void* B, float* D, i
   cudaFuncSetAttribute((const void*)k_tma_mn_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k_tma_mn_selftest<<<1, 128, smem, pb::as_stream(stream)>>>(ta, tb, D, N, K, uint32_t(lbo), uint32_t(sbo));
   return pb::check_launch("pb_tma_bf16_mn_selftest");
+}
+
+// TMA read bandwidth probe: every CTA streams `nbox` boxes of 32 fp32 x 128
+// rows (16 KB) through an S-stage ring (no compute).  mode 0: 2-D tensor
+// [rows][cols] with row pitch `pitch` (a box = 128 rows of 128 B, `pitch`
+// bytes apart); mode 1: the same bytes blocked so each box is one contiguous
+// 16 KB tile.  Tells whether a box's DRAM row locality limits a kernel.
+namespace {
+constexpr int kBwStages = 8;
+__global__ void __launch_bounds__(32) k_tma_bw(const __grid_constant__ CUtensorMap map, int mode, int nbox,
+                                               int nchunk, int rows_per_cta, unsigned* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = pb::tma::align1k(smem_raw);
+  __shared__ __align__(8) uint64_t full[kBwStages];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kBwStages; ++i) pb::umma::mbar_init(&full[i], 1);
+  pb::umma::fence_init();
+  auto issue = [&](int c) {
+    uint8_t* st = smem + (c % kBwStages) * 16384;
+    uint64_t* f = &full[c % kBwStages];
+    pb::tma::expect_tx(f, 16384);
+    const int chunk = c % nchunk, rb = blockIdx.x * (rows_per_cta / 128) + (c / nchunk) % (rows_per_cta / 128);
+    if (mode == 0)
+      pb::tma::load_2d(st, &map, chunk * 32, rb * 128, f);
+    else
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+              pb::umma::smem_u32(st)),
+          "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(chunk * 128), "r"(rb), "r"(pb::umma::smem_u32(f))
+          : "memory");
+  };
+  for (int c = 0; c < nbox && c < kBwStages; ++c) issue(c);
+  unsigned acc = 0;
+  for (int c = 0; c < nbox; ++c) {
+    pb::umma::mbar_wait(&full[c % kBwStages], (c / kBwStages) & 1);
+    acc += smem[(c % kBwStages) * 16384 + (c & 1023)];
+    if (c + kBwStages < nbox) issue(c + kBwStages);
+  }
+  sink[blockIdx.x] = acc;
+}
+}  // namespace
+
+extern "C" int pb_tma_bw_probe(const float* base, int mode, int64_t rows, int64_t cols, int ctas, int nbox,
+                               unsigned* sink, void* stream) {
+  if (!base || rows % 128 || cols % 32 || ctas < 1 || rows % ctas || (rows / ctas) % 128)
+    return pb::fail(PB_ERR_INVALID, "pb_tma_bw_probe: bad arguments");
+  CUtensorMap map;
+  int rc;
+  if (mode == 0) {
+    if ((rc = pb::tma::make_2d_f32(&map, base, uint64_t(cols), uint64_t(rows), uint64_t(cols), 128))) return rc;
+  } else {
+    // [row block][chunk][128 rows][32 floats]: dims {32, chunk*128 + row, row block}
+    const uint64_t d[3] = {32, 128 * uint64_t(cols / 32), uint64_t(rows / 128)};
+    const uint64_t st[2] = {128, uint64_t(cols / 32) * 16384};
+    const uint32_t box[3] = {32, 128, 1};
+    if ((rc = pb::tma::make_nd_f32(&map, base, 3, d, st, box))) return rc;
+  }
+  const int nchunk = int(cols / 32);
+  const size_t smem = 1024 + kBwStages * 16384;
+  cudaFuncSetAttribute((const void*)k_tma_bw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_tma_bw<<<ctas, 32, smem, pb::as_stream(stream)>>>(map, mode, nbox, nchunk, int(rows / ctas), sink);
+  return pb::check_launch("pb_tma_bw_probe");
 }

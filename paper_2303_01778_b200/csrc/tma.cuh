@@ -112,6 +112,11 @@ __device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, i
   umma::fence_init();
 }
 
+// N-D fp32 tensor map, 128-byte swizzle, box inner dimension 32 elements
+// (strides in bytes for dims 1..rank-1), out-of-bounds elements read as 0.
+int make_nd_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                const uint32_t* box);
+
 // N-D bf16 tensor map with 128-byte swizzle (box inner dimension = 64
 // elements); dims/strides as cuTensorMapEncodeTiled (strides in bytes for
 // dims 1..rank-1), out-of-bounds elements read as 0.
