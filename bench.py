@@ -346,10 +346,38 @@ FC1_FLOP = 2 * 512 * 3136
 CNN_TRAIN_FLOP = 73.8e6
 
 
+_TRAFFIC = None
+
+
+def measured_traffic(name):
+    """DRAM bytes per launch of a kernel class (mean over one C2 round's
+    launches) from the committed ncu capture profiles/r1_traffic.json
+    (tools/traffic_summary.py), or None."""
+    global _TRAFFIC
+    if _TRAFFIC is None:
+        try:
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                   "r1_traffic.json")) as fh:
+                _TRAFFIC = json.load(fh)["kernels"]
+        except (OSError, ValueError, KeyError):
+            _TRAFFIC = {}
+    k = _TRAFFIC.get(name)
+    return None if k is None else k["dram_bytes_per_launch"]
+
+
 def roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src) -> dict:
     """A kernel vs its roofline: ALGORITHMIC work of the timed rounds divided by
     the kernel's total device time over those rounds (CUDA events recorded by
-    the library around each launch, on the launching stream)."""
+    the library around each launch, on the launching stream).  `traffic` is
+    the measured DRAM bytes per launch (ncu, profiles/r1_traffic.json)."""
+    out = _roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src)
+    out["traffic"] = measured_traffic(name)
+    if out["traffic"] is not None:
+        out["traffic_unit"] = "DRAM bytes per launch (ncu dram__bytes_read+write, mean over a round)"
+    return out
+
+
+def _roofline(name, ms, kernels, samples_timed, client_steps, peaks, peak_src) -> dict:
     if ms <= 0:
         return {"kernel": name, "bound": None, "achieved": None, "peak": None, "unit": None,
                 "frac": None, "traffic": None}
