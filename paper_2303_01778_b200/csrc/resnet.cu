@@ -747,22 +747,26 @@ __device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* 
                                           double* r2, F f) {
   const int tid = threadIdx.x, C4 = C >> 2, tpc = kGnThreads / C4;  // C4 <= 128 -> tpc >= 4
   const int cg = tid & (C4 - 1), pt = tid / C4, c0 = cg * 4;
-  double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
-  double a2[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
+  // a thread sums at most HW / tpc <= 256 positions: fp32 partials (four
+  // independent chains, all loads of an iteration in flight), double combine
+  float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+  float a2[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
   int p = pt;
-  for (; p + tpc < HW; p += 2 * tpc) {
-    float u[4], v[4], x[4], y[4];
+  for (; p + 3 * tpc < HW; p += 4 * tpc) {
+    float u[4], v[4], x[4], y[4], u2[4], v2[4], x2[4], y2[4];
     f(p, c0, u, v);
     f(p + tpc, c0, x, y);
+    f(p + 2 * tpc, c0, u2, v2);
+    f(p + 3 * tpc, c0, x2, y2);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      a[j] += u[j];
-      b[j] += v[j];
-      a2[j] += x[j];
-      b2[j] += y[j];
+      a[j] += u[j] + u2[j];
+      b[j] += v[j] + v2[j];
+      a2[j] += x[j] + x2[j];
+      b2[j] += y[j] + y2[j];
     }
   }
-  if (p < HW) {
+  for (; p < HW; p += tpc) {
     float u[4], v[4];
     f(p, c0, u, v);
 #pragma unroll
@@ -773,8 +777,8 @@ __device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* 
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    part1[tid * 4 + j] = a[j] + a2[j];
-    part2[tid * 4 + j] = b[j] + b2[j];
+    part1[tid * 4 + j] = double(a[j]) + double(a2[j]);
+    part2[tid * 4 + j] = double(b[j]) + double(b2[j]);
   }
   __syncthreads();
   for (int cc = tid; cc < C; cc += kGnThreads) {
@@ -838,7 +842,7 @@ __device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, cons
 }
 
 // out = relu(GN(z) [+ res | + GN2(z2)]) as bf16; grid (active, BS)
-__global__ void __launch_bounds__(kGnThreads) k_rn_gn_fwd(Net a, GnF f) {
+__global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
   if (i >= sl.cnt) return;
@@ -887,6 +891,7 @@ __global__ void __launch_bounds__(kGnThreads) k_rn_gn_fwd(Net a, GnF f) {
   const bf16* res = f.res >= 0 ? at<const bf16>(a, s, f.res) + base : nullptr;
   bf16* out = at<bf16>(a, s, f.out) + base;
   const int n4 = HW * C / 4;
+#pragma unroll 4
   for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
     const int c0 = (e4 * 4) & (C - 1), g = c0 >> cshift;
     const float4 zv = reinterpret_cast<const float4*>(z)[e4];
@@ -998,6 +1003,7 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
   }
   bf16* dz = at<bf16>(a, s, dz_off) + base;
   const int n4 = HW * C / 4;
+#pragma unroll 4
   for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
     const int c0 = (e4 * 4) & (C - 1), g = c0 >> cshift;
     const float4 gv = reinterpret_cast<const float4*>(G)[e4];
@@ -1019,7 +1025,7 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
 // G = (g0 [+ g1]) * (mask > 0); GN backward(s) -> bf16 dz; grid (active, BS)
 // Samples past the batch get dz = 0: the TMA weight-gradient boxes read
 // whole position tiles, and zero dz rows keep them out of the sum.
-__global__ void __launch_bounds__(kGnThreads) k_rn_gn_bwd(Net a, GnB f) {
+__global__ void __launch_bounds__(kGnThreads, 2) k_rn_gn_bwd(Net a, GnB f) {
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
   if (i >= sl.cnt) {
