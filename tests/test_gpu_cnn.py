@@ -163,3 +163,46 @@ def test_cnn_non_finite_detected(spec, femnist_like):
     with pytest.raises(NonFiniteLossError, match="client 3 round 1"):
         pb.client_execute(plugin, ClientProfile(3, 30, DataSlice(X, y, np.arange(30))), glob, None,
                           1, 10, 0.05, seed=0, round_num=1)
+
+
+def test_cnn_dense_sweeps_match_sparse(spec, femnist_like, monkeypatch):
+    """The bench's 1000-client rounds run the dense-sweep kernel variants
+    (>= 148 active clients: 8 clients share each W0 tile of the low-rank fc1;
+    >= 60: one-CTA head, 2-way wgrad split), which the small replays above
+    never reach.  200 clients trained in ONE group must match the same
+    clients trained one at a time (sparse variants: cluster head,
+    sample-split wgrad clusters, split-K Gram / forward).  Only summation
+    order differs, and bf16 rounding of the activations turns that into
+    ~1e-5 per step; a ReLU / max-pool flip (see above) then compounds, so
+    the check is per sweep: after one sweep median <= 1e-4 and every
+    client <= 1e-3; after two (first history corrections) median <= 1e-3,
+    every client <= 5e-2.  A wrong tile or slot would be O(1)."""
+    import paper_2303_01778_b200 as pb
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    from paper_2303_01778_b200.models import cnn_init
+    from paper_2303_01778_b200.trainer import ClientData, NamedParams, train_group
+    G = 200
+    sizes = np.random.default_rng(9).integers(11, 28, size=G)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    assert off[-1] <= len(femnist_like.labels)
+    profiles = [ClientProfile(c, int(sizes[c]),
+                              DataSlice(femnist_like.features[off[c]:off[c + 1]],
+                                        femnist_like.labels[off[c]:off[c + 1]], np.arange(sizes[c])))
+                for c in range(G)]
+    data = ClientData.from_profiles(profiles, n_classes=62)
+    plugin = pb.FedAvg(lr=0.05, batch_size=10)
+    glob = plugin.init_global(NamedParams.from_flat(spec, cnn_init(spec, 2)))
+    w0 = glob.flat(spec)
+    base = w0.cpu().numpy().astype(np.float64)
+    for sweeps, med, worst in ((1, 1e-4, 1e-3), (2, 1e-3, 5e-2)):
+        monkeypatch.setenv("PB_CNN_MAX_SWEEPS", str(sweeps))
+        dense = train_group(plugin, spec, data, list(range(G)), w0, glob, None, 2, 10, 0.05,
+                            seed=7, round_num=1).w_out.cpu().numpy().astype(np.float64)
+        errs = []
+        for c in range(0, G, 17):
+            one = train_group(plugin, spec, data, [c], w0, glob, None, 2, 10, 0.05, seed=7,
+                              round_num=1).w_out.cpu().numpy()[0].astype(np.float64)
+            errs.append(_rel(dense[c] - base, one - base))
+        errs = np.asarray(errs)
+        assert float(np.median(errs)) <= med, (sweeps, errs)
+        assert errs.max() <= worst, (sweeps, errs)

@@ -1,6 +1,6 @@
 """TMA read bandwidth: 16 KB boxes of 128 rows x 128 B with a row pitch
-(the history layout of the low-rank fc1) vs the same bytes as contiguous
-16 KB tiles.  python tools/tma_bw_probe.py"""
+(the history layouts of the low-rank fc1) vs the same bytes as contiguous
+16 KB tiles, per CTA count.  python tools/tma_bw_probe.py"""
 import sys
 sys.path.insert(0, ".")
 import torch  # noqa: E402
@@ -9,16 +9,14 @@ from paper_2303_01778_b200 import _lib  # noqa: E402
 lib = _lib.lib
 dev = torch.device("cuda", 0)
 sink = torch.zeros(4096, dtype=torch.int32, device=dev)
-for cols in (3136, 3136 * 8, 226304):
-    rows = (2 ** 30 // 4 // cols) // (128 * 148) * 128 * 148
+st = torch.cuda.current_stream().cuda_stream
+for cols, rows, ctas_list in ((3136, 128 * 148 * 4, (148, 74)), (262144, 128 * 8, (8, 4)),
+                              (262144, 128 * 64, (64, 32))):
     buf = torch.zeros(rows * cols, device=dev)
-    for ctas in (148, 66, 296):
+    for ctas in ctas_list:
         rpc = rows // ctas
-        if rpc % 128:
-            continue
-        nbox = (rpc // 128) * (cols // 32)
+        nbox = min((rpc // 128) * (cols // 32), 512)
         for mode in (0, 1):
-            st = torch.cuda.current_stream().cuda_stream
             for _ in range(2):
                 assert lib.pb_tma_bw_probe(buf.data_ptr(), mode, rows, cols, ctas, nbox, sink.data_ptr(), st) == 0
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -29,5 +27,6 @@ for cols in (3136, 3136 * 8, 226304):
             ms = e0.elapsed_time(e1)
             gb = ctas * nbox * 16384 / 1e9
             print(f"pitch {cols * 4:>8} B  ctas {ctas:3d}  {'blocked' if mode else 'pitched'}: "
-                  f"{gb / ms * 1e3:7.0f} GB/s ({ms:.3f} ms, {gb:.2f} GB)", flush=True)
+                  f"{gb / ms * 1e3:7.0f} GB/s total, {gb / ms * 1e3 / ctas:6.1f} GB/s per CTA ({ms:.3f} ms)",
+                  flush=True)
     del buf
