@@ -28,6 +28,8 @@
 // the epilogues.  Reductions have a fixed order (no atomics): results are
 // deterministic.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cnn_common.cuh"
 #include "tma.cuh"
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
   fence_after_sync();
   const int njt = njt_of(a);
   const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
-  const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
+  const int per = (spc + 1) >> 1, u0 = half * per, u1 = min(spc, u0 + per);   // slots of this warp half
 #pragma unroll 1
   for (int u = u0; u < u1; ++u) {
     const Slot sl = sS[u];
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   __syncthreads();
   fence_after_sync();
   const int k = k0 + (warp & 3) * 32 + lane, half = warp >> 2;
-  const int u0 = spc == 1 ? 0 : half * 4, u1 = spc == 1 ? (half == 0 ? 1 : 0) : half * 4 + 4;
+  const int per = (spc + 1) >> 1, u0 = half * per, u1 = min(spc, u0 + per);   // slots of this warp half
 #pragma unroll 1
   for (int u = u0; u < u1; ++u) {
     const Slot sl = sS[u];
@@ -747,13 +749,25 @@ void lazy_fc1_release(Args& a) {
   a.lzmaps = nullptr;
 }
 
+// clients per CTA of the shared-W0 GEMMs: 8 while the sweep fills the
+// machine; fewer in sparser sweeps (each CTA streams the W0 tiles once for
+// its spc clients, so spc trades W0 traffic against grid size)
+static int slots_per_cta(int active) {
+  static int th[3] = {-1, -1, -1};
+  if (th[0] < 0) {
+    th[0] = 148, th[1] = 74, th[2] = 37;   // measured: tools/spc_sweep.sh
+    if (const char* e = std::getenv("PB_LZ_SPC")) std::sscanf(e, "%d,%d,%d", &th[0], &th[1], &th[2]);
+  }
+  return active >= th[0] ? kSh8 : active >= th[1] ? 4 : active >= th[2] ? 2 : 1;
+}
+
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   LzMaps& m = *maps_of(a);
   const int njt = njt_of_host(a.step, a.BS);
   // head sweeps: 8 clients share each W0 tile (N = 256); tail sweeps (fewer
   // clients than SMs): one client per CTA, and the forward splits K so that
   // the grid still covers the machine
-  const int spc = active >= 148 ? kSh8 : 1;
+  const int spc = slots_per_cta(active);
   const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
     pb::prof_begin(pb::K_CNN_LZ_XT, s);
