@@ -24,6 +24,8 @@
 // Operands are bf16 with fp32 accumulation in TMEM; master weights, biases,
 // losses and all non-GEMM math are fp32 (loss reduction in double).
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "cnn_common.cuh"
 
@@ -1351,7 +1353,21 @@ static Args to_args(const pb_cnn_train_args& t) {
 
 static size_t head_smem(int C, int BS) { return size_t(2 * BS * kH1 + BS * C) * 4; }
 
+// active-client thresholds below which a sweep uses the cluster head and the
+// 5-way (per filter row) conv2 wgrad split
+static void tail_thresholds(int* head, int* wg) {
+  static int th[2] = {-1, -1};
+  if (th[0] < 0) {
+    th[0] = 120, th[1] = kWgTailActive;   // measured: tools/tail_sweep.sh
+    if (const char* e = std::getenv("PB_CNN_TAIL")) std::sscanf(e, "%d,%d", &th[0], &th[1]);
+  }
+  *head = th[0];
+  *wg = th[1];
+}
+
 static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream_t s) {
+  int head_thr, wg_thr;
+  tail_thresholds(&head_thr, &wg_thr);
   // samples per CTA of the per-sample conv kernels: enough CTAs to fill the
   // machine in the sparse tail sweeps, amortised weight staging otherwise
   const int sms = pb::sm_count();
@@ -1373,7 +1389,7 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::prof_end(pb::K_CNN_FC1_FWD, s);
   }
   pb::prof_begin(pb::K_CNN_HEAD, s);
-  if (train && active < kWgTailActive) {
+  if (train && active < head_thr) {
     k_head_tail<<<dim3(kTailParts, active), kHeadThreads, head_tail_smem(a.C, a.BS), s>>>(a);
   } else {
     const int hparts = active < kWgTailActive ? 4 : 1;
@@ -1394,7 +1410,7 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   k_bwd_conv<<<dim3(BSpb, active), kBwdThreads, kBwdSmem, s>>>(a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
-  const int wsplit = active < kWgTailActive ? 5 : 2;
+  const int wsplit = active < wg_thr ? 5 : 2;
   // sparse sweeps: split each client's samples over a cluster while the grid
   // still fits one wave
   const int wsg = wsplit == 5 ? std::max(1, std::min(4, sms / ((wsplit + 1) * active))) : 1;
