@@ -260,7 +260,10 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
 // Head sweeps: spc = 8, fused epilogue.  Tail sweeps (few clients): spc = 1
 // and K split over gridDim.z CTAs writing raw partials to fpart, summed in
 // split order by k_lz_fwd_epi (deterministic).
-// grid (4 o-tiles, ceil(active / spc), ks), 256 threads
+// Dense sweeps (spc = 8) take MT = 2 o-tiles per CTA (two M=128 accumulators,
+// 512 TMEM columns): the 8 clients' X tiles are read once per 256 outputs,
+// a third less tile traffic per FLOP.
+// grid (4 / MT o-tiles, ceil(active / spc), ks), 256 threads
 // ---------------------------------------------------------------------------
 constexpr int kSh8 = 8;                         // max slots per CTA (N = 8 x 32)
 constexpr int kShA = 128 * 128;                 // 16 KB
@@ -293,7 +296,11 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
     if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
 }
 
+template <int MT>
 __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  constexpr int S = MT == 1 ? kStages : 3;        // stages of MT*16 + 32 KB
+  constexpr int kStage = MT * kShA + kShB;
+  static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_fwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -306,8 +313,8 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     Slot z{};
     sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
   }
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
-  if (tid == 0) ring_barriers(full, empty, kStages);
+  if (warp == 0) tmem_alloc<MT * 256>(&tmem_base);
+  if (tid == 0) ring_barriers(full, empty, S);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -321,31 +328,39 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     }
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       const int k0 = (c0 + c) * 32;
-      pb::tma::expect_tx(f, uint32_t(kShA + nv * 32 * 128));
-      pb::tma::load_2d(st, &m.w0, k0, q * 128, f);
+      pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * 32 * 128));
+#pragma unroll
+      for (int t = 0; t < MT; ++t) pb::tma::load_2d(st + t * kShA, &m.w0, k0, (q * MT + t) * 128, f);
       for (int u = 0; u < spc; ++u)
-        if (sS[u].cnt > 0) pb::tma::load_2d(st + kShA + u * 32 * 128, &m.hxb, k0, rows[u], f);
+        if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * 32 * 128, &m.hxb, k0, rows[u], f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
+      const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
       const uint32_t idesc = idesc_tf32(128, spc * 32);
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+      for (int t = 0; t < MT; ++t) {
+        const uint64_t a0 = desc_sw128(smem_u32(st + t * kShA));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_tf32(tmem + t * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+      }
     };
-    tma_ring<kStages>(c1 - c0, smem, kShStage, full, empty, issue, mma);
+    tma_ring<S>(c1 - c0, smem, kStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
   const int njt = njt_of(a);
-  const int o = q * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
+  const int half = warp >> 2;
   const int per = (spc + 1) >> 1, u0 = half * per, u1 = min(spc, u0 + per);   // slots of this warp half
 #pragma unroll 1
-  for (int u = u0; u < u1; ++u) {
+  for (int tu = 0; tu < MT * (u1 - u0); ++tu) {
+    const int t = tu / (u1 - u0), u = u0 + tu % (u1 - u0);
+    const int o = (q * MT + t) * 128 + (warp & 3) * 32 + lane;
     const Slot sl = sS[u];
     float v[32];
-    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32), *reinterpret_cast<float(*)[16]>(v));
-    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
+    const uint32_t col = uint32_t(t * 256 + u * 32);
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col, *reinterpret_cast<float(*)[16]>(v));
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0) continue;
     const int s = g0 + u;
     if (ks == 1) {
@@ -358,7 +373,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  if (warp == 0) tmem_free<MT * 256>(tmem);
 }
 
 // k_lz_fwd_epi: sum the ks split-K partials (split order), + b1 + the
@@ -700,7 +715,8 @@ int setup() {
     const char* name;
   } attrs[] = {{(const void*)k_lz_gram<true>, kGramFwdSmem, "k_lz_gram<fwd>"},
                {(const void*)k_lz_gram<false>, kGramBwdSmem, "k_lz_gram<bwd>"},
-               {(const void*)k_lz_fwd, kShSmem, "k_lz_fwd"},
+               {(const void*)k_lz_fwd<1>, kShSmem, "k_lz_fwd"},
+               {(const void*)k_lz_fwd<2>, kShSmem, "k_lz_fwd"},
                {(const void*)k_lz_bwd, kShSmem, "k_lz_bwd"},
                {(const void*)k_lz_mat, kShSmem, "k_lz_mat"},
                {(const void*)k_lz_fold, kShSmem, "k_lz_fold"}};
@@ -799,7 +815,10 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
-    k_lz_fwd<<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
+    if (spc == kSh8)
+      k_lz_fwd<2><<<dim3(kH1 / 256, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
+    else
+      k_lz_fwd<1><<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (ks > 1) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
