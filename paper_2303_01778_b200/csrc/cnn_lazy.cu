@@ -433,34 +433,41 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 //   phase 1 (shared): M = 128 k, N = spc*32, K = 512 (A = w0t, B = dH_t rows)
 //   phase 2 (per slot, t > 0): M = 128 k, N = 32, K = t*BS into the slot's
 //   accumulator columns (A = the client's hxt columns, B = its gdt rows)
-// grid (25 k-tiles, ceil(active / spc)), 256 threads
+// Dense sweeps (spc = 8) take MT = 2 k-tiles per CTA (512 TMEM columns): the
+// dH_t and gdt tiles are read once per 256 k.
+// grid (ceil(25 / MT) k-tiles, ceil(active / spc)), 256 threads
 // ---------------------------------------------------------------------------
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
+template <int MT>
 __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  constexpr int S = MT == 1 ? kStages : 3;
+  constexpr int kStage = MT == 1 ? kShStage : MT * kShA + kShB;   // 48 | 64 KB
+  static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_bwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int k0 = blockIdx.x * 128, g0 = blockIdx.y * spc;
+  const int kt0 = blockIdx.x * MT, g0 = blockIdx.y * spc;
   if (spc == 1 && a.slots[g0].cnt == 0) return;
   if (tid < kSh8) {
     Slot z{};
     sS[tid] = tid < spc && g0 + tid < active ? a.slots[g0 + tid] : z;
   }
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
-  if (tid == 0) ring_barriers(full, empty, kStages);
+  if (warp == 0) tmem_alloc<MT * 256>(&tmem_base);
+  if (tid == 0) ring_barriers(full, empty, S);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const int t = a.step, jlim = t * a.BS;
-  const int nj = (jlim + 63) >> 6;               // phase-2 stages per slot (two K atoms each)
+  // phase-2 stages per slot: two K atoms (MT = 1) or one (MT = 2, two k-tiles)
+  const int nj = MT == 1 ? (jlim + 63) >> 6 : (jlim + 31) >> 5;
   const int64_t tb = int64_t(t) * a.BS;
-  // phase-1 stages: one K atom for 8 slots, two for a single slot (the same
-  // 40 KB stage as phase 2, twice the bytes in flight)
+  // phase-1 stages: one K atom for several slots, two for a single slot (the
+  // same 40 KB stage as phase 2, twice the bytes in flight)
   const int n1 = spc == 1 ? kH1 / 64 : kH1 / 32;
   if (tid == 0) {
     int us[kSh8], rows[kSh8], nv = 0;
@@ -474,26 +481,33 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pb::tma::load_2d(st + h * kShA, &m.w0t, (2 * c + h) * 32, k0, f);
+          pb::tma::load_2d(st + h * kShA, &m.w0t, (2 * c + h) * 32, kt0 * 128, f);
           pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.hdb, (2 * c + h) * 32, rows[0], f);
         }
       } else if (c < n1) {
-        pb::tma::expect_tx(f, uint32_t(kShA + nv * 32 * 128));
-        pb::tma::load_2d(st, &m.w0t, c * 32, k0, f);
+        pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * 32 * 128));
+#pragma unroll
+        for (int q = 0; q < MT; ++q) pb::tma::load_2d(st + q * kShA, &m.w0t, c * 32, (kt0 + q) * 128, f);
         for (int u = 0; u < spc; ++u)
-          if (sS[u].cnt > 0) pb::tma::load_2d(st + kShA + u * 32 * 128, &m.hdb, c * 32, rows[u], f);
-      } else {
+          if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * 32 * 128, &m.hdb, c * 32, rows[u], f);
+      } else if (MT == 1) {
         const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
         pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          pb::tma::load_2d(st + h * kShA, &m.hxt128, int(sS[u].hist) + (2 * jc + h) * 32, k0, f);
+          pb::tma::load_2d(st + h * kShA, &m.hxt128, int(sS[u].hist) + (2 * jc + h) * 32, kt0 * 128, f);
           pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.gdt, (2 * jc + h) * 32, (g0 + u) * 32, f);
         }
+      } else {
+        const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
+        pb::tma::expect_tx(f, uint32_t(MT * kShA + 32 * 128));
+#pragma unroll
+        for (int q = 0; q < MT; ++q)
+          pb::tma::load_2d(st + q * kShA, &m.hxt128, int(sS[u].hist) + jc * 32, (kt0 + q) * 128, f);
+        pb::tma::load_2d(st + MT * kShA, &m.gdt, jc * 32, (g0 + u) * 32, f);
       }
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
       if (c < n1 && spc == 1) {
         const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
@@ -506,10 +520,15 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         }
       } else if (c < n1) {
         const uint32_t idesc = idesc_tf32(128, spc * 32);
+        const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
-      } else {
+        for (int q = 0; q < MT; ++q) {
+          const uint64_t a0 = desc_sw128(smem_u32(st + q * kShA));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_tf32(tmem + q * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+        }
+      } else if (MT == 1) {
         const int u = us[(c - n1) / nj];
         const uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
@@ -520,20 +539,34 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
           for (int kk = 0; kk < 4; ++kk)
             mma_tf32(tmem + u * 32, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
         }
+      } else {
+        const int u = us[(c - n1) / nj];
+        const uint32_t idesc = idesc_tf32(128, 32);
+        const uint64_t bh = desc_sw128(smem_u32(st + MT * kShA));
+#pragma unroll
+        for (int q = 0; q < MT; ++q) {
+          const uint64_t ah = desc_sw128(smem_u32(st + q * kShA));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_tf32(tmem + q * 256 + u * 32, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+        }
       }
     };
-    tma_ring<kStages>(n, smem, kShStage, full, empty, issue, mma);
+    tma_ring<S>(n, smem, kStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
-  const int k = k0 + (warp & 3) * 32 + lane, half = warp >> 2;
+  const int half = warp >> 2;
   const int per = (spc + 1) >> 1, u0 = half * per, u1 = min(spc, u0 + per);   // slots of this warp half
 #pragma unroll 1
-  for (int u = u0; u < u1; ++u) {
+  for (int qu = 0; qu < MT * (u1 - u0); ++qu) {
+    const int q = qu / (u1 - u0), u = u0 + qu % (u1 - u0);
+    const int k = (kt0 + q) * 128 + (warp & 3) * 32 + lane;
     const Slot sl = sS[u];
     float v[32];
-    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32), *reinterpret_cast<float(*)[16]>(v));
-    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(u * 32 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
+    const uint32_t col = uint32_t(q * 256 + u * 32);
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col, *reinterpret_cast<float(*)[16]>(v));
+    tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0 || k >= kFlat) continue;
     float* dp2 = a.dp2 + sidx(g0 + u, 0, a.BS) * kFlat + k;
 #pragma unroll
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  if (warp == 0) tmem_free<MT * 256>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -717,7 +750,8 @@ int setup() {
                {(const void*)k_lz_gram<false>, kGramBwdSmem, "k_lz_gram<bwd>"},
                {(const void*)k_lz_fwd<1>, kShSmem, "k_lz_fwd"},
                {(const void*)k_lz_fwd<2>, kShSmem, "k_lz_fwd"},
-               {(const void*)k_lz_bwd, kShSmem, "k_lz_bwd"},
+               {(const void*)k_lz_bwd<1>, kShSmem, "k_lz_bwd"},
+               {(const void*)k_lz_bwd<2>, kShSmem, "k_lz_bwd"},
                {(const void*)k_lz_mat, kShSmem, "k_lz_mat"},
                {(const void*)k_lz_fold, kShSmem, "k_lz_fold"}};
   for (auto& x : attrs) {
@@ -835,7 +869,10 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
-    k_lz_bwd<<<dim3(kBwKT, groups), 256, kShSmem, s>>>(m, a, active, spc);
+    if (spc == kSh8)
+      k_lz_bwd<2><<<dim3((kBwKT + 1) / 2, groups), 256, kShSmem, s>>>(m, a, active, spc);
+    else
+      k_lz_bwd<1><<<dim3(kBwKT, groups), 256, kShSmem, s>>>(m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");
