@@ -45,6 +45,9 @@ int pb_device_sm_count(int device);
  *   21 rn_conv_fwd 22 rn_conv_dgrad 23 rn_conv_wgrad 24 rn_norm 25 rn_head 26 rn_sgd
  * recorded since the last collect (nslots >= 27), synchronising on them. */
 int pb_prof_enable(int on);
+/* Restrict profiling to the kernel classes whose bit (1 << class id) is set
+ * (default: all).  Each recorded launch adds two CUDA events to the stream. */
+int pb_prof_select(uint64_t mask);
 int64_t pb_launch_count(void);
 int pb_prof_collect(double* ms, int64_t* count, int nslots);
 

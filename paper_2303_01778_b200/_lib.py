@@ -75,6 +75,7 @@ _SIGS = {
     "pb_version": (c_int, []),
     "pb_device_sm_count": (c_int, [c_int]),
     "pb_prof_enable": (c_int, [c_int]),
+    "pb_prof_select": (c_int, [c_uint64]),
     "pb_launch_count": (c_int64, []),
     "pb_prof_collect": (c_int, [POINTER(c_double), POINTER(c_int64), c_int]),
     "pb_greedy_assign": (c_int, [POINTER(c_double), c_int64, POINTER(c_double), POINTER(c_double),

@@ -31,6 +31,7 @@ struct Rec {
 };
 std::mutex g_mu;
 bool g_prof = false;
+uint64_t g_mask = ~uint64_t(0);   // kernel classes recorded while profiling
 int64_t g_launches = 0;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
@@ -50,8 +51,7 @@ thread_local cudaEvent_t t_open = nullptr;
 void prof_begin(int id, cudaStream_t stream) {
   std::lock_guard<std::mutex> g(g_mu);
   ++g_launches;
-  (void)id;
-  if (!g_prof) return;
+  if (!g_prof || id < 0 || id >= 64 || !((g_mask >> id) & 1)) return;
   t_open = pooled();
   cudaEventRecord(t_open, stream);
 }
@@ -70,6 +70,12 @@ void prof_end(int id, cudaStream_t stream) {
 extern "C" int pb_prof_enable(int on) {
   std::lock_guard<std::mutex> g(pb::g_mu);
   pb::g_prof = on != 0;
+  return PB_OK;
+}
+
+extern "C" int pb_prof_select(uint64_t mask) {
+  std::lock_guard<std::mutex> g(pb::g_mu);
+  pb::g_mask = mask;
   return PB_OK;
 }
 
