@@ -38,6 +38,7 @@ using namespace pb::cnn;
 // k_slots: one thread per active slot -> (row, batch size, row-id offset)
 // ---------------------------------------------------------------------------
 __global__ void k_slots(Args a, int active) {
+  pb::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= active) return;
   const int r = a.rank[j];
@@ -69,6 +70,7 @@ constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * k
 // i&1, and then -- while those run -- finishes sample i-1 (TMEM -> bias/relu
 // -> maxpool -> p2).  The raw image of sample i+1 streams in by cp.async.
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.y];
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
@@ -253,6 +255,7 @@ constexpr size_t kF1FwdSmem = 2 * (kF1ABytes + kF1BBytes);
 // k_fc1_fwd: h = relu(p2 W1^T + b1); CTA = (client, 128 output rows)
 // D[o][i] (M=128, N=32, K=3136 in 49 stages of 64); grid (active, 4), 128 thr
 __global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -352,6 +355,7 @@ __device__ double block_sum_d(double v, double* scratch) {
 // (tail sweeps split a client over 4 CTAs; logits and softmax are recomputed
 // by each part, the bookkeeping and the fc2 bias belong to part 0)
 __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
+  pb::pdl_wait();
   const int slot = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
   const int olo = part * (kH1 / parts), ohi = olo + kH1 / parts;
   const Slot sl = a.slots[slot];
@@ -536,6 +540,7 @@ static size_t head_tail_smem(int C, int BS) {
 __device__ __forceinline__ float nan_max(float x, float y) { return x != x ? x : (y != y ? y : fmaxf(x, y)); }
 
 __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThreads) k_head_tail(Args a) {
+  pb::pdl_wait();
   namespace cgp = cooperative_groups;
   cgp::cluster_group cluster = cgp::this_cluster();
   const int slot = blockIdx.y, part = blockIdx.x;
@@ -752,6 +757,7 @@ constexpr int kF1SlicesPerCta = 4;      // setup amortised over 4 slices
 // stream through a 4-deep cp.async ring (raw W1 rows + dH columns); each chunk
 // is transposed smem->smem into the K-major dgrad operand.
 __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.x];
   if (sl.cnt == 0) return;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -965,6 +971,7 @@ __device__ __forceinline__ void stage_bytes(uint8_t* dst, const void* src, int b
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.y];
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
@@ -1174,6 +1181,7 @@ __device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* bu
 // grid ((nsplit + 1) * sg, active), cluster (sg, 1, 1), 256 threads;
 // nsplit = 2 (ky 0-2 | 3-4) or 5
 __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit, int sg) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.y];
   if (sl.cnt == 0) return;   // uniform over a cluster (same slot)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1378,22 +1386,22 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   pb::prof_begin(pb::K_CNN_FWD, s);
   // grids put a client's CTAs next to each other (slot = blockIdx.y), so the
   // sample-split / tap-split CTAs of one client share its data through L2
-  k_fwd<<<dim3(BSpb, active), kFwdThreads, kFwdSmem, s>>>(a, spb);
+  pb::launch_pdl(k_fwd, dim3(BSpb, active), dim3(kFwdThreads), kFwdSmem, s, 1, a, spb);
   pb::prof_end(pb::K_CNN_FWD, s);
   if (a.hx) {
     int rc = lazy_fc1_sweep(a, active, 0, s);
     if (rc) return rc;
   } else {
     pb::prof_begin(pb::K_CNN_FC1_FWD, s);
-    k_fc1_fwd<<<dim3(active, kH1 / 128), 128, kF1FwdSmem, s>>>(a);
+    pb::launch_pdl(k_fc1_fwd, dim3(active, kH1 / 128), dim3(128), kF1FwdSmem, s, 1, a);
     pb::prof_end(pb::K_CNN_FC1_FWD, s);
   }
   pb::prof_begin(pb::K_CNN_HEAD, s);
   if (train && active < head_thr) {
-    k_head_tail<<<dim3(kTailParts, active), kHeadThreads, head_tail_smem(a.C, a.BS), s>>>(a);
+    pb::launch_pdl(k_head_tail, dim3(kTailParts, active), dim3(kHeadThreads), head_tail_smem(a.C, a.BS), s, 1, a);
   } else {
     const int hparts = active < kWgTailActive ? 4 : 1;
-    k_head<<<dim3(hparts, active), kHeadThreads, head_smem(a.C, a.BS), s>>>(a);
+    pb::launch_pdl(k_head, dim3(hparts, active), dim3(kHeadThreads), head_smem(a.C, a.BS), s, 1, a);
   }
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
@@ -1402,12 +1410,11 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     if (rc) return rc;
   } else {
     pb::prof_begin(pb::K_CNN_FC1_BWD, s);
-    k_fc1_bwd<<<dim3(active, (kF1Slices + kF1SlicesPerCta - 1) / kF1SlicesPerCta), 256, kF1BwdSmem,
-                s>>>(a);
+    pb::launch_pdl(k_fc1_bwd, dim3(active, (kF1Slices + kF1SlicesPerCta - 1) / kF1SlicesPerCta), dim3(256), kF1BwdSmem, s, 1, a);
     pb::prof_end(pb::K_CNN_FC1_BWD, s);
   }
   pb::prof_begin(pb::K_CNN_BWD_CONV, s);
-  k_bwd_conv<<<dim3(BSpb, active), kBwdThreads, kBwdSmem, s>>>(a, spb);
+  pb::launch_pdl(k_bwd_conv, dim3(BSpb, active), dim3(kBwdThreads), kBwdSmem, s, 1, a, spb);
   pb::prof_end(pb::K_CNN_BWD_CONV, s);
   pb::prof_begin(pb::K_CNN_WGRAD, s);
   const int wsplit = active < wg_thr ? 5 : 2;
@@ -1415,21 +1422,10 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   // still fits one wave
   const int wsg = wsplit == 5 ? std::max(1, std::min(4, sms / ((wsplit + 1) * active))) : 1;
   if (wsg == 1) {
-    k_wgrad<<<dim3(wsplit + 1, active), 256, kWgSmem, s>>>(a, wsplit, 1);
+    pb::launch_pdl(k_wgrad, dim3(wsplit + 1, active), dim3(256), kWgSmem, s, 1, a, wsplit, 1);
   } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned((wsplit + 1) * wsg), unsigned(active));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = kWgSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(wsg);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_wgrad, a, wsplit, wsg);
+    pb::launch_pdl(k_wgrad, dim3(unsigned((wsplit + 1) * wsg), unsigned(active)), dim3(256), kWgSmem, s,
+                   unsigned(wsg), a, wsplit, wsg);
   }
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
@@ -1465,7 +1461,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     if (active <= 0) break;
     a.step = step;
     pb::prof_begin(pb::K_CNN_SLOTS, s);
-    k_slots<<<(active + 127) / 128, 128, 0, s>>>(a, active);
+    pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
     pb::prof_end(pb::K_CNN_SLOTS, s);
     if ((rc = launch_sweep(a, active, true, spb, s))) break;
   }

@@ -79,6 +79,7 @@ __global__ void k_lz_w0t(const float* __restrict__ w0, float* __restrict__ w0t) 
 // grid (active, 25 k-tiles of 128), 128 threads
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.x];
   const int cnt = sl.cnt;
   if (cnt == 0) return;
@@ -122,6 +123,7 @@ constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
 
 template <bool FWD>
 __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMaps m, Args a, int ks) {
+  pb::pdl_wait();
   const int s = blockIdx.y, jt = blockIdx.x / ks, rank = blockIdx.x - jt * ks;   // a client's tiles are adjacent
   const Slot sl = a.slots[s];
   const int cnt = sl.cnt;
@@ -298,6 +300,7 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
 
 template <int MT>
 __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;        // stages of MT*16 + 32 KB
   constexpr int kStage = MT * kShA + kShB;
   static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_fwd ring");
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
 // grid (active, kH1 * 8 / 256), 256 threads
 constexpr int kEpiThreads = 256;
 __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, int ks) {
+  pb::pdl_wait();
   const int s = blockIdx.x, t = blockIdx.y * kEpiThreads + threadIdx.x;
   const int o = t >> 3, i4 = t & 7;
   const Slot sl = a.slots[s];
@@ -441,6 +445,7 @@ constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
 template <int MT>
 __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+  pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;
   constexpr int kStage = MT == 1 ? kShStage : MT * kShA + kShB;   // 48 | 64 KB
   static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_bwd ring");
@@ -821,7 +826,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
     pb::prof_begin(pb::K_CNN_LZ_XT, s);
-    k_lz_xt<<<dim3(active, kBwKT), 128, 0, s>>>(a);
+    pb::launch_pdl(k_lz_xt, dim3(active, kBwKT), dim3(128), 0, s, 1, a);
     pb::prof_end(pb::K_CNN_LZ_XT, s);
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, s);
@@ -829,34 +834,23 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       const int sms = pb::sm_count();
       const int gks = njt * active * 4 <= sms ? 4 : (njt * active * 2 <= sms ? 2 : 1);
       if (gks == 1) {
-        k_lz_gram<true><<<dim3(njt, active), 128, kGramFwdSmem, s>>>(m, a, 1);
+        pb::launch_pdl(k_lz_gram<true>, dim3(njt, active), dim3(128), kGramFwdSmem, s, 1, m, a, 1);
       } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(unsigned(njt * gks), unsigned(active));
-        cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = kGramFwdSmem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = unsigned(gks);
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, k_lz_gram<true>, m, a, gks);
+        pb::launch_pdl(k_lz_gram<true>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128), kGramFwdSmem, s,
+                       unsigned(gks), m, a, gks);
       }
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
     if (spc == kSh8)
-      k_lz_fwd<2><<<dim3(kH1 / 256, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
+      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc);
     else
-      k_lz_fwd<1><<<dim3(kH1 / 128, groups, ks), 256, kShSmem, s>>>(m, a, active, spc);
+      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (ks > 1) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
-      k_lz_fwd_epi<<<dim3(active, kH1 * 8 / kEpiThreads), kEpiThreads, 0, s>>>(a, active, ks);
+      pb::launch_pdl(k_lz_fwd_epi, dim3(active, kH1 * 8 / kEpiThreads), dim3(kEpiThreads), 0, s, 1, a, active, ks);
       pb::prof_end(pb::K_CNN_LZ_FWD, s);
     }
   } else {
@@ -865,14 +859,14 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
                                     uint64_t(njt) * 128, 32);
       if (rc) return rc;
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
-      k_lz_gram<false><<<dim3(njt, active), 128, kGramBwdSmem, s>>>(m, a, 1);
+      pb::launch_pdl(k_lz_gram<false>, dim3(njt, active), dim3(128), kGramBwdSmem, s, 1, m, a, 1);
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
     if (spc == kSh8)
-      k_lz_bwd<2><<<dim3((kBwKT + 1) / 2, groups), 256, kShSmem, s>>>(m, a, active, spc);
+      pb::launch_pdl(k_lz_bwd<2>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc);
     else
-      k_lz_bwd<1><<<dim3(kBwKT, groups), 256, kShSmem, s>>>(m, a, active, spc);
+      pb::launch_pdl(k_lz_bwd<1>, dim3(kBwKT, groups), dim3(256), kShSmem, s, 1, m, a, active, spc);
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");

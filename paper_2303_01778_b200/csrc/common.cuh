@@ -37,6 +37,39 @@ inline unsigned grid_for(int64_t items, int threads, int waves = 8) {
   return unsigned(need < cap ? need : cap);
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+// The kernels of a training sweep are launched with programmatic stream
+// serialization, so a kernel's CTAs are dispatched while its predecessor
+// drains; every such kernel calls pdl_wait() before its first global access
+// (the predecessor has then completed and its writes are visible), so stream
+// order semantics are unchanged.  A no-op for kernels launched normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              unsigned cluster_x, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ---- launch accounting / optional per-kernel-class timing -----------------
 enum KernelId {
   K_FOLD1 = 0, K_FOLD_GROUP, K_LINCOMB, K_DELTA_AFFINE, K_STATE_GATHER, K_STATE_SCATTER,
