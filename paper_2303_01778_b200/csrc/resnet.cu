@@ -89,6 +89,7 @@ __device__ __forceinline__ T* at(const Net& a, int s, int64_t off) {
 // per-sweep slot table (same rule as the CNN path)
 // ---------------------------------------------------------------------------
 __global__ void k_rn_slots(Net a, int active) {
+  pb::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= active) return;
   const int r = a.rank[j];
@@ -106,6 +107,7 @@ __global__ void k_rn_slots(Net a, int active) {
 // stem: the batch's images (3072 fp32, NHWC 32x32x3) -> bf16 [32][32][8]
 // grid (active, BS), 256 threads
 __global__ void k_rn_stem(Net a, int64_t out) {
+  pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.x];
   const int i = blockIdx.y;
   if (i >= sl.cnt) return;
@@ -130,6 +132,7 @@ struct ConvWTable {
   int n;
 };
 __global__ void k_rn_w16(Net a, ConvWTable t, const int32_t* rows) {
+  pb::pdl_wait();
   const int r = rows ? rows[blockIdx.y] : blockIdx.y;
   const ConvW cw = t.c[blockIdx.z];
   const float* w = a.w + int64_t(r) * a.P + cw.w_off;
@@ -168,6 +171,7 @@ __device__ __forceinline__ uint32_t cv_off(int row, int ku) {  // K-major / MN-m
 
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) k_rn_conv(Net a, ConvK k, int ntile) {
+  pb::pdl_wait();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = MODE == WGRAD ? blockIdx.z / k.nsplit : blockIdx.z;
   const int split = MODE == WGRAD ? blockIdx.z % k.nsplit : 0;
@@ -356,6 +360,7 @@ template <bool DG>
 __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
                                                         const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
                                                         int ntile, int Ht, int Nt) {
+  pb::pdl_wait();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = blockIdx.z;
   const Slot sl = a.slots[s];
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
 __global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
                                                             const __grid_constant__ CUtensorMap tb, Net a,
                                                             ConvK k, int ntile, int Ht, int Nt) {
+  pb::pdl_wait();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = blockIdx.z >> 2, ph = (blockIdx.z >> 1) & 1, pw = blockIdx.z & 1;
   const Slot sl = a.slots[s];
@@ -518,6 +524,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constan
 __global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
                                                          const __grid_constant__ CUtensorMap tdz, Net a, ConvK k,
                                                          int ntile, int Hs, int Ns) {
+  pb::pdl_wait();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = blockIdx.z / k.nsplit, split = blockIdx.z % k.nsplit;
   const Slot sl = a.slots[s];
@@ -595,6 +602,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__
 // grid (ceil(Cout*M/4/256), active), 256 threads, 4 elements per thread
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, int Cin) {
+  pb::pdl_wait();
   const int s = blockIdx.y;
   const Slot sl = a.slots[s];
   if (sl.cnt == 0) return;
@@ -645,6 +653,7 @@ __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, 
 // written from smem along co.  Cin == Cinp, Cinp % 128 == 0 or Cinp == 64.
 // grid (ceil(Cinp/128), Cout/32, RS * active), (32, 8) threads
 __global__ void __launch_bounds__(256) k_rn_wsgd_t(Net a, ConvK k, int64_t w_off) {
+  pb::pdl_wait();
   const int RS = k.R * k.R;
   const int s = blockIdx.z / RS, rs = blockIdx.z - s * RS;
   const Slot sl = a.slots[s];
@@ -693,6 +702,7 @@ __global__ void __launch_bounds__(256) k_rn_wsgd_t(Net a, ConvK k, int64_t w_off
 // (by_slot = 0) or for the clients of the active slots that stepped (by_slot)
 // grid (ceil(Cinp/32), Cout/32, RS * rows), (32, 8) threads
 __global__ void __launch_bounds__(256) k_rn_w16t(Net a, ConvK k, int by_slot) {
+  pb::pdl_wait();
   const int RS = k.R * k.R;
   const int z = blockIdx.z / RS, rs = blockIdx.z - z * RS;
   int r = z;
@@ -843,6 +853,7 @@ __device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, cons
 
 // out = relu(GN(z) [+ res | + GN2(z2)]) as bf16; grid (active, BS)
 __global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
+  pb::pdl_wait();
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
   if (i >= sl.cnt) return;
@@ -1026,6 +1037,7 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
 // Samples past the batch get dz = 0: the TMA weight-gradient boxes read
 // whole position tiles, and zero dz rows keep them out of the sum.
 __global__ void __launch_bounds__(kGnThreads, 2) k_rn_gn_bwd(Net a, GnB f) {
+  pb::pdl_wait();
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
   if (i >= sl.cnt) {
@@ -1059,6 +1071,7 @@ struct GnSgd {
   int n;
 };
 __global__ void k_rn_gn_sgd(Net a, GnSgd t) {
+  pb::pdl_wait();
   const int s = blockIdx.x, j = blockIdx.y;
   const Slot sl = a.slots[s];
   if (sl.cnt == 0) return;
@@ -1088,6 +1101,7 @@ __device__ double block_sum_d(double v, double* scratch) {
 }
 
 __global__ void __launch_bounds__(256) k_rn_head(Net a, int64_t act, int64_t gout, int64_t fc_off) {
+  pb::pdl_wait();
   const int s = blockIdx.x;
   const Slot sl = a.slots[s];
   const int cnt = sl.cnt;
@@ -1415,48 +1429,47 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const int nt = conv_ntile(k.Cout);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
-    k_rn_conv_tma<false><<<g, 256, kCvSmem + 1024, s>>>(c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_conv_tma<false>, g, dim3(256), kCvSmem + 1024, s, 1, c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
   } else if (mode == FWD) {
     const int nt = conv_ntile(k.Cout);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
-    k_rn_conv<FWD><<<g, 256, kCvSmem, s>>>(a, k, nt);
+    pb::launch_pdl(k_rn_conv<FWD>, g, dim3(256), kCvSmem, s, 1, a, k, nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
   } else if (mode == DGRAD && c.tma_dg == 2) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cinp / nt, active * 4);
     pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
-    k_rn_dgrad_s2_tma<<<g, 256, kCvSmem + 1024, s>>>(c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_dgrad_s2_tma, g, dim3(256), kCvSmem + 1024, s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD && c.tma_dg) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
     pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
-    k_rn_conv_tma<true><<<g, 256, kCvSmem + 1024, s>>>(c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_conv_tma<true>, g, dim3(256), kCvSmem + 1024, s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
     pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
-    k_rn_conv<DGRAD><<<g, 256, kCvSmem, s>>>(a, k, nt);
+    pb::launch_pdl(k_rn_conv<DGRAD>, g, dim3(256), kCvSmem, s, 1, a, k, nt);
     pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else {
     const int nt = conv_ntile(k.Cout);
     const dim3 g((k.R * k.R * k.Cinp + 127) / 128, k.Cout / nt, active * k.nsplit);
     pb::prof_begin(pb::K_RN_CONV_WGRAD, s);
     if (c.tma && c.tma_wg)
-      k_rn_wgrad_tma<<<g, 256, kCvSmem + 1024, s>>>(c.twx, c.twd, a, k, nt, c.Hs, c.Ns);
+      pb::launch_pdl(k_rn_wgrad_tma, g, dim3(256), kCvSmem + 1024, s, 1, c.twx, c.twd, a, k, nt, c.Hs, c.Ns);
     else
-      k_rn_conv<WGRAD><<<g, 256, kCvSmem, s>>>(a, k, nt);
+      pb::launch_pdl(k_rn_conv<WGRAD>, g, dim3(256), kCvSmem, s, 1, a, k, nt);
     pb::prof_end(pb::K_RN_CONV_WGRAD, s);
     pb::prof_begin(pb::K_RN_SGD, s);
     if (c.tma_dg) {  // also refresh the transposed copy the TMA dgrad reads
-      k_rn_wsgd_t<<<dim3(unsigned((k.Cinp + 127) / 128), unsigned(k.Cout / 32), unsigned(k.R * k.R * active)),
-                    dim3(32, 8), 0, s>>>(a, k, c.w_off);
+      pb::launch_pdl(k_rn_wsgd_t, dim3(unsigned((k.Cinp + 127) / 128), unsigned(k.Cout / 32), unsigned(k.R * k.R * active)), dim3(32, 8), 0, s, 1, a, k, c.w_off);
     } else {
       const int64_t n4 = int64_t(k.R) * k.R * k.Cinp * k.Cout / 4;
-      k_rn_wsgd<<<dim3(unsigned((n4 + 255) / 256), active), 256, 0, s>>>(a, k, c.w_off, c.Cin);
+      pb::launch_pdl(k_rn_wsgd, dim3(unsigned((n4 + 255) / 256), active), dim3(256), 0, s, 1, a, k, c.w_off, c.Cin);
     }
     pb::prof_end(pb::K_RN_SGD, s);
   }
@@ -1476,13 +1489,13 @@ void launch_gn_fwd(const Net& a, const ConvL& c, int64_t res, const ConvL* c2, i
   f.gamma2 = c2 ? c2->gn_gamma : -1;
   f.out = out;
   pb::prof_begin(pb::K_RN_NORM, s);
-  k_rn_gn_fwd<<<dim3(active, a.BS), kGnThreads, gn_smem(), s>>>(a, f);
+  pb::launch_pdl(k_rn_gn_fwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
   pb::prof_end(pb::K_RN_NORM, s);
 }
 
 int forward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   pb::prof_begin(pb::K_RN_NORM, s);
-  k_rn_stem<<<dim3(active, a.BS), 256, 0, s>>>(a, pl.t0);
+  pb::launch_pdl(k_rn_stem, dim3(active, a.BS), dim3(256), 0, s, 1, a, pl.t0);
   pb::prof_end(pb::K_RN_NORM, s);
   launch_conv(a, pl.convs[0], FWD, active, s);
   launch_gn_fwd(a, pl.convs[0], -1, nullptr, pl.act0, active, s);
@@ -1499,7 +1512,7 @@ int forward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   }
   const size_t hsm = size_t(a.BS) * (512 + a.C) * 4;
   pb::prof_begin(pb::K_RN_HEAD, s);
-  k_rn_head<<<active, 256, hsm, s>>>(a, pl.blocks.back().act_out, pl.gout_last, pl.fc_off);
+  pb::launch_pdl(k_rn_head, dim3(active), dim3(256), hsm, s, 1, a, pl.blocks.back().act_out, pl.gout_last, pl.fc_off);
   pb::prof_end(pb::K_RN_HEAD, s);
   return pb::check_launch("resnet forward");
 }
@@ -1539,7 +1552,7 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
       f.z2 = cd.k.z; f.stats2 = cd.stats; f.gamma2 = cd.gn_gamma; f.dz2 = cd.k.dz; f.pg2 = cd.pg;
     }
     pb::prof_begin(pb::K_RN_NORM, s);
-    k_rn_gn_bwd<<<dim3(active, a.BS), kGnThreads, gn_smem(), s>>>(a, f);
+    pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(cb);
     launch_conv(a, cb, DGRAD, active, s);   // du (old weights)
@@ -1559,7 +1572,7 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
     m.z = ca.k.z; m.stats = ca.stats; m.gamma = ca.gn_gamma; m.dz = ca.k.dz; m.pg = ca.pg;
     m.z2 = m.stats2 = m.gamma2 = m.dz2 = m.pg2 = -1;
     pb::prof_begin(pb::K_RN_NORM, s);
-    k_rn_gn_bwd<<<dim3(active, a.BS), kGnThreads, gn_smem(), s>>>(a, m);
+    pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, m);
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(ca);
     launch_conv(a, ca, DGRAD, active, s);
@@ -1577,12 +1590,12 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   f.z = c0.k.z; f.stats = c0.stats; f.gamma = c0.gn_gamma; f.dz = c0.k.dz; f.pg = c0.pg;
   f.z2 = f.stats2 = f.gamma2 = f.dz2 = f.pg2 = -1;
   pb::prof_begin(pb::K_RN_NORM, s);
-  k_rn_gn_bwd<<<dim3(active, a.BS), kGnThreads, gn_smem(), s>>>(a, f);
+  pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
   pb::prof_end(pb::K_RN_NORM, s);
   add_gn(c0);
   launch_conv(a, c0, WGRAD, active, s);
   pb::prof_begin(pb::K_RN_SGD, s);
-  k_rn_gn_sgd<<<dim3(active, gs.n), 256, 0, s>>>(a, gs);
+  pb::launch_pdl(k_rn_gn_sgd, dim3(active, gs.n), dim3(256), 0, s, 1, a, gs);
   pb::prof_end(pb::K_RN_SGD, s);
   return pb::check_launch("resnet backward");
 }
@@ -1616,13 +1629,12 @@ ConvWTable wtable(const Plan& pl) {
 int refresh_w16(const Net& a, const Plan& pl, int rows, cudaStream_t s) {
   const ConvWTable t = wtable(pl);
   pb::prof_begin(pb::K_RN_SGD, s);
-  k_rn_w16<<<dim3(64, rows, t.n), 256, 0, s>>>(a, t, nullptr);
+  pb::launch_pdl(k_rn_w16, dim3(64, rows, t.n), dim3(256), 0, s, 1, a, t, nullptr);
   pb::prof_end(pb::K_RN_SGD, s);
   for (const ConvL& c : pl.convs) {
     const ConvK& k = c.k;
     pb::prof_begin(pb::K_RN_SGD, s);
-    k_rn_w16t<<<dim3(unsigned((k.Cinp + 31) / 32), unsigned(k.Cout / 32), unsigned(k.R * k.R * rows)), dim3(32, 8),
-                0, s>>>(a, k, 0);
+    pb::launch_pdl(k_rn_w16t, dim3(unsigned((k.Cinp + 31) / 32), unsigned(k.Cout / 32), unsigned(k.R * k.R * rows)), dim3(32, 8), 0, s, 1, a, k, 0);
     pb::prof_end(pb::K_RN_SGD, s);
   }
   return pb::check_launch("resnet w16");
@@ -1660,7 +1672,7 @@ extern "C" int pb_resnet_train_group(const pb_resnet_train_args* args, void* str
     if (active <= 0) break;
     a.step = step;
     pb::prof_begin(pb::K_RN_NORM, s);
-    k_rn_slots<<<(active + 127) / 128, 128, 0, s>>>(a, active);
+    pb::launch_pdl(k_rn_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
     pb::prof_end(pb::K_RN_NORM, s);
     if ((rc = forward(a, pl, active, s))) return rc;
     if ((rc = backward(a, pl, active, s))) return rc;
