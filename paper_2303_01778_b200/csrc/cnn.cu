@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
 // (also the eval head when a.eval != null)
 // ---------------------------------------------------------------------------
 constexpr int kHeadThreads = 256;
+__host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }   // logit rows padded for 16 B loads
 
 __device__ double block_sum_d(double v, double* scratch) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -363,8 +364,9 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   extern __shared__ float hs[];
   const int C = a.C, cnt = sl.cnt, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* sH = hs;                      // [cnt][512]
-  float* sL = sH + cnt * kH1;          // [cnt][C] logits -> dlogits
-  float* sDH = sL + cnt * a.C;         // [cnt][512] dH
+  const int Cp = pad4(a.C);
+  float* sL = sH + cnt * kH1;          // [cnt][Cp] logits -> dlogits
+  float* sDH = sL + cnt * Cp;          // [cnt][512] dH
   __shared__ double scratch[kHeadThreads / 32];
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
@@ -397,14 +399,14 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
       if (lane == 0)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (i0 + q < cnt) sL[(i0 + q) * C + c] = s[q] + bc;
+          if (i0 + q < cnt) sL[(i0 + q) * Cp + c] = s[q] + bc;
     }
   }
   __syncthreads();
   double lpart = 0.0, cpart = 0.0;
   const float inv = 1.0f / float(cnt);
   if (tid < cnt) {
-    float* z = sL + tid * C;
+    float* z = sL + tid * Cp;
     const int y = a.Y[a.order[sl.row_off + tid]];
     float m = z[0];
     int best = 0;
@@ -450,46 +452,45 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
   const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
   float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(slot, 0, a.BS) * kH1;
-  // one pass over W2 per output o (thread-owned column): dH[i][o] from the
-  // old W2[c][o], then the fc2 update of that element (fused; sample order)
+  // per output o (thread-owned column), 8 classes per pass: their W2 loads
+  // are in flight together, the samples stream from smem (dlogits as 16 B
+  // loads), dH[i][o] accumulates in sDH in class order, the fc2 gradient of
+  // each (class, o) in registers in sample order, then its update (fused)
   for (int o = olo + tid; o < ohi; o += kHeadThreads) {
-    float hreg[32], acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      hreg[i] = i < cnt ? sH[i * kH1 + o] : 0.0f;
-      acc[i] = 0.0f;
-    }
-    // 8 classes per pass: their W2 loads are all in flight before any store
     for (int c0 = 0; c0 < C; c0 += 8) {
-      float wv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        wv[u] = c0 + u < C ? W[oF2W + int64_t(c0 + u) * kH1 + o] : 0.0f;
+      float wv[8], g[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u;
-        if (c >= C) break;
-        float g = 0.0f;
+        wv[u] = c0 + u < C ? W[oF2W + int64_t(c0 + u) * kH1 + o] : 0.0f;
+        g[u] = 0.0f;
+      }
+      for (int i = 0; i < cnt; ++i) {
+        const float h = sH[i * kH1 + o];
+        const float4 d0 = *reinterpret_cast<const float4*>(sL + i * Cp + c0);
+        const float4 d1 = c0 + 4 < Cp ? *reinterpret_cast<const float4*>(sL + i * Cp + c0 + 4)
+                                      : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        float acc = c0 == 0 ? 0.0f : sDH[i * kH1 + o];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i < cnt) {
-            const float d = sL[i * C + c];
-            acc[i] = fmaf(d, wv[u], acc[i]);
-            g = fmaf(d, hreg[i], g);
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < C) {
+            acc = fmaf(d[u], wv[u], acc);
+            g[u] = fmaf(d[u], h, g[u]);
           }
-        }
-        const int64_t idx = oF2W + int64_t(c) * kH1 + o;
-        W[idx] = sgd(a, sl.r, idx, wv[u], g);
+        sDH[i * kH1 + o] = acc;
       }
-    }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i < cnt) {
-        float gi = hreg[i] > 0.0f ? acc[i] : 0.0f;
-        if (a.hx) gi = tf32_rna(gi);
-        dh[i * kH1 + o] = gi;
-        sDH[i * kH1 + o] = gi;
-      }
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < C) {
+          const int64_t idx = oF2W + int64_t(c0 + u) * kH1 + o;
+          W[idx] = sgd(a, sl.r, idx, wv[u], g[u]);
+        }
+    }
+    for (int i = 0; i < cnt; ++i) {
+      float gi = sH[i * kH1 + o] > 0.0f ? sDH[i * kH1 + o] : 0.0f;
+      if (a.hx) gi = tf32_rna(gi);
+      dh[i * kH1 + o] = gi;
+      sDH[i * kH1 + o] = gi;
     }
   }
   __syncthreads();  // sDH complete
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   }
   for (int c = tid; c < (part == 0 ? C : 0); c += kHeadThreads) {
     float g = 0.0f;
-    for (int i = 0; i < cnt; ++i) g += sL[i * C + c];
+    for (int i = 0; i < cnt; ++i) g += sL[i * Cp + c];
     const int64_t idx = oF2W + int64_t(C) * kH1 + c;
     W[idx] = sgd(a, sl.r, idx, W[idx], g);
   }
@@ -531,7 +532,6 @@ constexpr int kTailParts = 8;
 constexpr int kTailO = kH1 / kTailParts;   // 64
 constexpr int kTailCg = kHeadThreads / kTailO;   // 4 class groups
 constexpr int kTailS = kTailO + 4;         // padded smem row (conflict-free 16 B loads)
-__host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }
 static size_t head_tail_smem(int C, int BS) {
   return (size_t(BS) * (2 * kTailS + kTailCg * kTailO + 2 * pad4(C)) + size_t(C) * kTailS + pad4(C)) * 4 +
          size_t(BS) * 8;
@@ -1359,7 +1359,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   return a;
 }
 
-static size_t head_smem(int C, int BS) { return size_t(2 * BS * kH1 + BS * C) * 4; }
+static size_t head_smem(int C, int BS) { return size_t(2 * BS * kH1 + BS * pad4(C)) * 4; }
 
 // active-client thresholds below which a sweep uses the cluster head and the
 // 5-way (per filter row) conv2 wgrad split
