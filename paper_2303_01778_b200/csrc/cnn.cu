@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
 // (also the eval head when a.eval != null)
 // ---------------------------------------------------------------------------
 constexpr int kHeadThreads = 256;
+constexpr int kHeadDenseThreads = 512;   // k_head: one fc1 output column per thread
 __host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }   // logit rows padded for 16 B loads
 
 __device__ double block_sum_d(double v, double* scratch) {
@@ -355,7 +356,7 @@ __device__ double block_sum_d(double v, double* scratch) {
 // grid (parts, active): part p owns fc1 outputs [p*512/parts, (p+1)*512/parts)
 // (tail sweeps split a client over 4 CTAs; logits and softmax are recomputed
 // by each part, the bookkeeping and the fc2 bias belong to part 0)
-__global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
+__global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   pb::pdl_wait();
   const int slot = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
   const int olo = part * (kH1 / parts), ohi = olo + kH1 / parts;
@@ -367,18 +368,18 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   const int Cp = pad4(a.C);
   float* sL = sH + cnt * kH1;          // [cnt][Cp] logits -> dlogits
   float* sDH = sL + cnt * Cp;          // [cnt][512] dH
-  __shared__ double scratch[kHeadThreads / 32];
+  __shared__ double scratch[kHeadDenseThreads / 32];
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
   const float* W2 = W + oF2W;          // [C][512], read from L2 (coalesced rows)
   const float* hrow = a.h + sidx(slot, 0, a.BS) * kH1;
 #pragma unroll 8
-  for (int e = tid; e < cnt * kH1; e += kHeadThreads) sH[e] = hrow[e];
+  for (int e = tid; e < cnt * kH1; e += kHeadDenseThreads) sH[e] = hrow[e];
   __syncthreads();
   const float* b2 = W2 + int64_t(C) * kH1;
   // logits: one warp per class c holds W2[c] in registers (16 per lane, all
   // loads in flight at once); lanes split each 512-long dot product
-  for (int c = warp; c < C; c += kHeadThreads / 32) {
+  for (int c = warp; c < C; c += kHeadDenseThreads / 32) {
     const float* wc = W2 + int64_t(c) * kH1;
     float wr[16];
 #pragma unroll
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   // are in flight together, the samples stream from smem (dlogits as 16 B
   // loads), dH[i][o] accumulates in sDH in class order, the fc2 gradient of
   // each (class, o) in registers in sample order, then its update (fused)
-  for (int o = olo + tid; o < ohi; o += kHeadThreads) {
+  for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {
     for (int c0 = 0; c0 < C; c0 += 8) {
       float wv[8], g[8];
 #pragma unroll
@@ -497,11 +498,11 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
   if (a.hx) {
     // dH^T columns of the global [512][hrows] history (row pitch hrows)
     float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
-    for (int p = tid; p < cnt * (ohi - olo); p += kHeadThreads) {
+    for (int p = tid; p < cnt * (ohi - olo); p += kHeadDenseThreads) {
       const int o = olo + p / cnt, i = p - (o - olo) * cnt;
       hdt[int64_t(o) * a.hrows + i] = sDH[i * kH1 + o];
     }
-    for (int o = olo + tid; o < ohi; o += kHeadThreads) {  // fc1 bias (sample order)
+    for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
       const int64_t idx = oF1B + o;
@@ -509,12 +510,12 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(Args a) {
     }
   } else {
     float* dht = a.dht + int64_t(slot) * kH1 * 32;
-    for (int p = olo * 32 + tid; p < ohi * 32; p += kHeadThreads) {
+    for (int p = olo * 32 + tid; p < ohi * 32; p += kHeadDenseThreads) {
       const int o = p >> 5, i = p & 31;
       dht[p] = i < cnt ? sDH[i * kH1 + o] : 0.0f;
     }
   }
-  for (int c = tid; c < (part == 0 ? C : 0); c += kHeadThreads) {
+  for (int c = tid; c < (part == 0 ? C : 0); c += kHeadDenseThreads) {
     float g = 0.0f;
     for (int i = 0; i < cnt; ++i) g += sL[i * Cp + c];
     const int64_t idx = oF2W + int64_t(C) * kH1 + c;
@@ -1401,7 +1402,7 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
     pb::launch_pdl(k_head_tail, dim3(kTailParts, active), dim3(kHeadThreads), head_tail_smem(a.C, a.BS), s, 1, a);
   } else {
     const int hparts = active < kWgTailActive ? 4 : 1;
-    pb::launch_pdl(k_head, dim3(hparts, active), dim3(kHeadThreads), head_smem(a.C, a.BS), s, 1, a);
+    pb::launch_pdl(k_head, dim3(hparts, active), dim3(kHeadDenseThreads), head_smem(a.C, a.BS), s, 1, a);
   }
   pb::prof_end(pb::K_CNN_HEAD, s);
   if (!train) return pb::check_launch("cnn eval sweep");
