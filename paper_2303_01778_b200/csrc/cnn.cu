@@ -202,10 +202,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
           arg = d;
         }
       }
-      const float v = relu_nan(best);
+      const __nv_bfloat16 vb = __float2bfloat16(relu_nan(best));
       *reinterpret_cast<__nv_bfloat16*>(sPl + (c1 >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 +
-                                        (c1 & 7) * 2) = __float2bfloat16(v);
-      am1[pp * kC1 + c1] = uint8_t(arg);
+                                        (c1 & 7) * 2) = vb;
+      // pool argmax, bit 2: the stored p1 value is > 0 (relu' for the backward)
+      am1[pp * kC1 + c1] = uint8_t(arg | (__bfloat162float(vb) > 0.0f ? 4 : 0));
     }
     fence_async_smem();
     __syncthreads();
@@ -956,17 +957,20 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // tcgen05 -> dp1 (TMEM -> smem) -> pool1/relu backward fused with the conv1
 // weight gradient and the conv1/conv2 bias gradients of this sample
 // (per-sample partials, summed in sample order by k_wgrad: deterministic).
-// grid (ceil(BS/spb), active), 256 threads
+// Software-pipelined over the CTA's samples: the TMEM accumulators are
+// double-buffered, so the dgrad MMAs of sample i run while the CTA copies its
+// dz2 planes out and finishes sample i-1 (dp1, conv1 gradients); the pool2
+// inputs of sample i+1 stream into smem (cp.async) meanwhile.
+// grid (ceil(BS/spb), active), 512 threads
 // ---------------------------------------------------------------------------
-// per-sample inputs of k_bwd_conv, staged by one cp.async burst per sample
-constexpr int kInDp2 = 0, kInP2 = kInDp2 + kFlat * 4, kInAm2 = kInP2 + kFlat * 4,
-              kInAm1 = kInAm2 + kFlat, kInImg = kInAm1 + kP1, kInP1 = kInImg + kImg * kImg * 4,
-              kInBytes = kInP1 + kP1Bytes;   // 59,136 B
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kInBytes;
-
 constexpr int kBwdThreads = 512;
+constexpr int kBwdIn = 2 * kFlat * 4 + kFlat;            // dp2, p2 (fp32), am2 of one sample
+constexpr int kBwdDp1 = 196 * kC1 * 4;                   // dp1 [196][32] fp32
+constexpr int kBwdRed = 8 * 832 * 4;                     // warp-pair partials (aliases dp1 + image)
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdIn + kBwdDp1 + 1024 * 4 + 3 * kP1;   // 221,632 B
+static_assert(kBwdRed <= kBwdDp1 + 1024 * 4, "k_bwd_conv reduction scratch");
 
-__device__ __forceinline__ void stage_bytes(uint8_t* dst, const void* src, int bytes, int tid) {
+__device__ __forceinline__ void bwd_stage(uint8_t* dst, const void* src, int bytes, int tid) {
   const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
   for (int e = tid * 16; e < bytes; e += kBwdThreads * 16) cp_async16(dst + e, s8 + e);
 }
@@ -977,38 +981,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float sB2[kBwdThreads / 64][64];
+  __shared__ float sB2[2][kBwdThreads / 64][64];
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
-  uint8_t* sIn = sDz + kDzBytes;
-  const float* iDp2 = reinterpret_cast<const float*>(sIn + kInDp2);
-  const float* iP2 = reinterpret_cast<const float*>(sIn + kInP2);
-  const uint8_t* iAm2 = sIn + kInAm2;
-  const uint8_t* iAm1 = sIn + kInAm1;
-  const float* iImg = reinterpret_cast<const float*>(sIn + kInImg);
-  const uint8_t* iP1 = sIn + kInP1;
-  // after the dgrad MMAs the dz region is reused:
-  float* sDp1 = reinterpret_cast<float*>(sDz);           // [196][32] dp1 (25,088 B)
-  float* sX = sDp1 + 196 * 32;                           // [32][32] padded image
-  float* sRed = reinterpret_cast<float*>(sDz);           // [8][kPg-64] warp-pair partials (after sync)
+  uint8_t* sIn = sDz + kDzBytes;                         // dp2 | p2 | am2 of the next sample
+  const float* iDp2 = reinterpret_cast<const float*>(sIn);
+  const float* iP2 = iDp2 + kFlat;
+  const uint8_t* iAm2 = sIn + 2 * kFlat * 4;
+  float* sDp1 = reinterpret_cast<float*>(sIn + kBwdIn);
+  float* sX = sDp1 + 196 * kC1;                          // [32][32] padded image
+  float* sRed = sDp1;                                    // [8][832] (after the conv1 loop)
+  uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 1024);  // 3 x [196][32] pool1 argmax / relu'
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  auto stage_inputs = [&](int i) {
+  auto stage_in = [&](int i) {   // pool2 inputs of sample i; its pool1 bytes into buffer i % 3
     const int64_t sid = sidx(blockIdx.y, i, a.BS);
-    stage_bytes(sIn + kInDp2, a.dp2 + sid * kFlat, kFlat * 4, tid);
-    stage_bytes(sIn + kInP2, p2_row(a, sl, blockIdx.y, i), kFlat * 4, tid);
-    stage_bytes(sIn + kInAm2, a.am2 + sid * kFlat, kFlat, tid);
-    stage_bytes(sIn + kInAm1, a.am1 + sid * kP1, kP1, tid);
-    stage_bytes(sIn + kInImg, a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg), kImg * kImg * 4, tid);
-    stage_bytes(sIn + kInP1, a.p1g + sid * kP1Bytes, kP1Bytes, tid);
+    bwd_stage(sIn, a.dp2 + sid * kFlat, kFlat * 4, tid);
+    bwd_stage(sIn + kFlat * 4, p2_row(a, sl, blockIdx.y, i), kFlat * 4, tid);
+    bwd_stage(sIn + 2 * kFlat * 4, a.am2 + sid * kFlat, kFlat, tid);
+    bwd_stage(sAm1 + (i % 3) * kP1, a.am1 + sid * kP1, kP1, tid);
     cp_async_commit();
   };
-  stage_inputs(i0);
+  stage_in(i0);
   stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, kBwdThreads);
-  if (warp == 0) tmem_alloc<64>(&tmem_base);
+  // the dz2 planes: borders stay zero; every sample rewrites all 4 candidates
+  // of each pooled position
+  for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
+  if (warp == 0) tmem_alloc<128>(&tmem_base);
   if (tid == 0) {
-    mbar_init(&mbar, 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     fence_init();
   }
   fence_before_sync();
@@ -1016,96 +1019,109 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const uint32_t idesc = idesc_bf16(128, 32, false, true);
-  uint32_t phase = 0;
-  for (int i = i0; i < i1; ++i) {
-    const int64_t sid = sidx(blockIdx.y, i, a.BS);
-    for (int e = tid; e < kDzBytes / 16; e += kBwdThreads)
-      reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
-    cp_async_wait<0>();
-    __syncthreads();
-    float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
-    for (int o = tid; o < kFlat; o += kBwdThreads) {
-      const int pp = o >> 6, co = o & 63;
-      const int py = pp / 7, px = pp - py * 7;
-      const int d = iAm2[o];
-      const float g = iP2[o] > 0.0f ? iDp2[o] : 0.0f;
-      b2part += g;
-      const int row = (2 * py + (d >> 1) + 2) * kG + 2 * px + (d & 1) + 2;
-      *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) =
-          __float2bfloat16(g);
-    }
-    sB2[tid >> 6][tid & 63] = b2part;
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      fence_after_sync();
-      const uint64_t a0 = desc(smem_u32(sDz), kPlane, 128);
-      const uint64_t b0 = desc(smem_u32(sW2), 128, 1024);
+  for (int i = i0; i <= i1; ++i) {
+    if (i < i1) {
+      // ---- sample i: dz2 planes (the MMAs of sample i-1 must be done with them) ----
+      const int b = i & 1;
+      const int64_t sid = sidx(blockIdx.y, i, a.BS);
+      if (i > i0) mbar_wait(&mbar[b ^ 1], ((i - 1 - i0) >> 1) & 1);
+      cp_async_wait<0>();
+      __syncthreads();
+      float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
+      for (int o = tid; o < kFlat; o += kBwdThreads) {
+        const int pp = o >> 6, co = o & 63;
+        const int py = pp / 7, px = pp - py * 7;
+        const int d = iAm2[o];
+        const float g = iP2[o] > 0.0f ? iDp2[o] : 0.0f;
+        b2part += g;
+        const __nv_bfloat16 gb = __float2bfloat16(g), zb = __float2bfloat16(0.0f);
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
+        for (int q = 0; q < 4; ++q) {
+          const int row = (2 * py + (q >> 1) + 2) * kG + 2 * px + (q & 1) + 2;
+          *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) = q == d ? gb : zb;
+        }
+      }
+      sB2[b][tid >> 6][tid & 63] = b2part;
+      fence_async_smem();
+      fence_before_sync();
+      __syncthreads();
+      if (i + 1 < i1) stage_in(i + 1);   // staged inputs consumed: prefetch the next sample
+      if (tid == 0) {
+        fence_after_sync();
+        uint64_t a0 = desc(smem_u32(sDz), kPlane, 128);
+        uint64_t b0 = desc(smem_u32(sW2), 128, 1024);
+        // opaque per sample: keeps the 200 descriptors from being hoisted
+        // out of the sample loop (register spills)
+        asm volatile("" : "+l"(a0), "+l"(b0));
 #pragma unroll
-        for (int tap = 0; tap < 25; ++tap)   // flipped tap: weights (4-ky, 4-kx)
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
-          for (int kq = 0; kq < 4; ++kq)
-            mma_bf16(tmem + t * 32, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + kq * (2 * kPlane / 16)),
-                     b0 + uint64_t((24 - tap) * 256 + kq * 16), idesc, tap > 0 || kq > 0);
-      commit(&mbar);
-    }
-    {
+          for (int tap = 0; tap < 25; ++tap)   // flipped tap: weights (4-ky, 4-kx)
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq)
+              mma_bf16(tmem + b * 64 + t * 32,
+                       a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + kq * (2 * kPlane / 16)),
+                       b0 + uint64_t((24 - tap) * 256 + kq * 16), idesc, tap > 0 || kq > 0);
+        commit(&mbar[b]);
+      }
+      // dz2 planes to global for k_wgrad (overlaps the MMAs)
       uint4* dst = reinterpret_cast<uint4*>(a.dzg + sid * kDzBytes);
       const uint4* src = reinterpret_cast<const uint4*>(sDz);
       for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) dst[e] = src[e];
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    fence_after_sync();
-    __syncthreads();  // the dz2 copy-out is done: the region can be reused
-    if (warp < 4) {
+    if (i > i0) {
+      // ---- sample j = i-1 (its MMAs completed before sample i's planes were
+      // built): dp1 from TMEM, pool1 / relu backward, conv1 gradients ----
+      const int j = i - 1, b = j & 1;
+      const int64_t sid = sidx(blockIdx.y, j, a.BS);
+      const uint8_t* am1 = sAm1 + (j % 3) * kP1;   // staged with sample j's pool2 inputs
+      if (i == i1) mbar_wait(&mbar[b], ((j - i0) >> 1) & 1);   // (earlier: waited before sample i)
+      fence_after_sync();
+      if (warp < 4) {
 #pragma unroll 1
-      for (int t = 0; t < 2; ++t) {
-        const int row = t * 128 + warp * 32 + lane;
-        const int y = row / kG, x = row - y * kG;
-        float v[16];
+        for (int t = 0; t < 2; ++t) {
+          const int row = t * 128 + warp * 32 + lane;
+          const int y = row / kG, x = row - y * kG;
+          float v[16];
 #pragma unroll
-        for (int c16 = 0; c16 < 2; ++c16) {
-          tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(t * 32 + c16 * 16), v);
-          if (y < 14 && x < 14) {
+          for (int c16 = 0; c16 < 2; ++c16) {
+            tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(b * 64 + t * 32 + c16 * 16), v);
+            if (y < 14 && x < 14) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kC1 + c16 * 16 + k] = v[k];
+              for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kC1 + c16 * 16 + k] = v[k];
+            }
           }
         }
+      } else {
+        const float* img = a.X + int64_t(a.order[sl.row_off + j]) * (kImg * kImg);
+        for (int e = tid - 128; e < 1024; e += kBwdThreads - 128) {
+          const int yy = e >> 5, xx = e & 31;
+          sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+        }
       }
-    } else {
-      for (int e = tid - 128; e < 1024; e += kBwdThreads - 128) {
-        const int yy = e >> 5, xx = e & 31;
-        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? iImg[(yy - 2) * kImg + (xx - 2)] : 0.0f;
-      }
-    }
-    fence_before_sync();
-    __syncthreads();
-    // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
-    // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
-    {
+      fence_before_sync();
+      __syncthreads();
+      // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
+      // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
       float acc[25];
 #pragma unroll
       for (int t = 0; t < 25; ++t) acc[t] = 0.0f;
       float bacc = 0.0f;
       const int co = lane;
+#pragma unroll 1
       for (int pp = warp; pp < 196; pp += kBwdThreads / 32) {
         const int py = pp / 14, px = pp - py * 14;
-        const float pv = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
-            iP1 + (co >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 + (co & 7) * 2));
-        const float g = pv > 0.0f ? sDp1[pp * kC1 + co] : 0.0f;
+        const int dm = am1[pp * kC1 + co];   // pool1 argmax, bit 2: relu'
+        const float g = (dm & 4) ? sDp1[pp * kC1 + co] : 0.0f;
         bacc += g;
-        const int d = iAm1[pp * kC1 + co];
+        const int d = dm & 3;
         const float* xw = sX + (2 * py + (d >> 1)) * 32 + 2 * px + (d & 1);
 #pragma unroll
         for (int ky = 0; ky < 5; ++ky)
 #pragma unroll
           for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * 32 + kx], acc[ky * 5 + kx]);
       }
-      __syncthreads();  // all reads of sDp1/sX and the staged inputs done
-      if (i + 1 < i1) stage_inputs(i + 1);  // next sample's inputs stream in meanwhile
+      __syncthreads();  // all reads of dp1 / the image done: sRed may overwrite them
       // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
       // them to their own, then the 8 pair sums are added in warp order
       if (warp >= 8) {
@@ -1119,9 +1135,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] += acc[t];
         sRed[warp * 832 + 800 + co] += bacc;
       }
-    }
-    __syncthreads();
-    {
+      __syncthreads();
       float* pg = a.pg + sid * kPg;
       for (int k = tid; k < 832; k += kBwdThreads) {
         float s8 = 0.0f;
@@ -1130,15 +1144,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         pg[k] = s8;
       }
       if (tid < 64) {
-        float b = 0.0f;
+        float b2 = 0.0f;
 #pragma unroll
-        for (int q = 0; q < kBwdThreads / 64; ++q) b += sB2[q][tid];
-        pg[832 + tid] = b;
+        for (int q = 0; q < kBwdThreads / 64; ++q) b2 += sB2[b][q][tid];
+        pg[832 + tid] = b2;
       }
+      fence_before_sync();
+      __syncthreads();   // sRed / dp1 free; TMEM half b read before its next MMAs
     }
-    __syncthreads();
   }
-  if (warp == 0) tmem_free<64>(tmem);
+  fence_after_sync();
+  if (warp == 0) tmem_free<128>(tmem);
 }
 
 // ---------------------------------------------------------------------------
