@@ -967,8 +967,11 @@ constexpr int kBwdThreads = 512;
 constexpr int kBwdIn = 2 * kFlat * 4 + kFlat;            // dp2, p2 (fp32), am2 of one sample
 constexpr int kBwdDp1 = 196 * kC1 * 4;                   // dp1 [196][32] fp32
 constexpr int kBwdRed = 8 * 832 * 4;                     // warp-pair partials (aliases dp1 + image)
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdIn + kBwdDp1 + 1024 * 4 + 3 * kP1;   // 221,632 B
-static_assert(kBwdRed <= kBwdDp1 + 1024 * 4, "k_bwd_conv reduction scratch");
+// image row stride 34: the 4 pool candidates' windows (offsets 0, 1, 34, 35)
+// of the 32 channel lanes fall in distinct banks
+constexpr int kXS = 34;
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdIn + kBwdDp1 + 32 * kXS * 4 + 3 * kP1;   // 221,888 B
+static_assert(kBwdRed <= kBwdDp1 + 32 * kXS * 4, "k_bwd_conv reduction scratch");
 
 __device__ __forceinline__ void bwd_stage(uint8_t* dst, const void* src, int bytes, int tid) {
   const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
@@ -991,9 +994,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const float* iP2 = iDp2 + kFlat;
   const uint8_t* iAm2 = sIn + 2 * kFlat * 4;
   float* sDp1 = reinterpret_cast<float*>(sIn + kBwdIn);
-  float* sX = sDp1 + 196 * kC1;                          // [32][32] padded image
+  float* sX = sDp1 + 196 * kC1;                          // [32][kXS] padded image
   float* sRed = sDp1;                                    // [8][832] (after the conv1 loop)
-  uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 1024);  // 3 x [196][32] pool1 argmax / relu'
+  uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 32 * kXS);  // 3 x [196][32] pool1 argmax / relu'
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   auto stage_in = [&](int i) {   // pool2 inputs of sample i; its pool1 bytes into buffer i % 3
     const int64_t sid = sidx(blockIdx.y, i, a.BS);
@@ -1096,7 +1099,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         const float* img = a.X + int64_t(a.order[sl.row_off + j]) * (kImg * kImg);
         for (int e = tid - 128; e < 1024; e += kBwdThreads - 128) {
           const int yy = e >> 5, xx = e & 31;
-          sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+          sX[yy * kXS + xx] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
         }
       }
       fence_before_sync();
@@ -1115,11 +1118,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         const float g = (dm & 4) ? sDp1[pp * kC1 + co] : 0.0f;
         bacc += g;
         const int d = dm & 3;
-        const float* xw = sX + (2 * py + (d >> 1)) * 32 + 2 * px + (d & 1);
+        const float* xw = sX + (2 * py + (d >> 1)) * kXS + 2 * px + (d & 1);
 #pragma unroll
         for (int ky = 0; ky < 5; ++ky)
 #pragma unroll
-          for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * 32 + kx], acc[ky * 5 + kx]);
+          for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * kXS + kx], acc[ky * 5 + kx]);
       }
       __syncthreads();  // all reads of dp1 / the image done: sRed may overwrite them
       // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
