@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(128, 2) k_fc1_fwd(Args a) {
 // ---------------------------------------------------------------------------
 constexpr int kHeadThreads = 256;
 constexpr int kHeadDenseThreads = 512;   // k_head: one fc1 output column per thread
+constexpr int kDHS = kH1 + 1;            // k_head dH row stride (conflict-free column reads)
 __host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }   // logit rows padded for 16 B loads
 
 __device__ double block_sum_d(double v, double* scratch) {
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   float* sH = hs;                      // [cnt][512]
   const int Cp = pad4(a.C);
   float* sL = sH + cnt * kH1;          // [cnt][Cp] logits -> dlogits
-  float* sDH = sL + cnt * Cp;          // [cnt][512] dH
+  float* sDH = sL + cnt * Cp;          // [cnt][kDHS] dH
   __shared__ double scratch[kHeadDenseThreads / 32];
   __shared__ int s_bad;
   float* W = a.w + int64_t(sl.r) * a.P;
@@ -472,14 +473,14 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
         const float4 d1 = c0 + 4 < Cp ? *reinterpret_cast<const float4*>(sL + i * Cp + c0 + 4)
                                       : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-        float acc = c0 == 0 ? 0.0f : sDH[i * kH1 + o];
+        float acc = c0 == 0 ? 0.0f : sDH[i * kDHS + o];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (c0 + u < C) {
             acc = fmaf(d[u], wv[u], acc);
             g[u] = fmaf(d[u], h, g[u]);
           }
-        sDH[i * kH1 + o] = acc;
+        sDH[i * kDHS + o] = acc;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -489,10 +490,10 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
         }
     }
     for (int i = 0; i < cnt; ++i) {
-      float gi = sH[i * kH1 + o] > 0.0f ? sDH[i * kH1 + o] : 0.0f;
+      float gi = sH[i * kH1 + o] > 0.0f ? sDH[i * kDHS + o] : 0.0f;
       if (a.hx) gi = tf32_rna(gi);
       dh[i * kH1 + o] = gi;
-      sDH[i * kH1 + o] = gi;
+      sDH[i * kDHS + o] = gi;
     }
   }
   __syncthreads();  // sDH complete
@@ -501,11 +502,11 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
     for (int p = tid; p < cnt * (ohi - olo); p += kHeadDenseThreads) {
       const int o = olo + p / cnt, i = p - (o - olo) * cnt;
-      hdt[int64_t(o) * a.hrows + i] = sDH[i * kH1 + o];
+      hdt[int64_t(o) * a.hrows + i] = sDH[i * kDHS + o];
     }
     for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
-      for (int i = 0; i < cnt; ++i) g += sDH[i * kH1 + o];
+      for (int i = 0; i < cnt; ++i) g += sDH[i * kDHS + o];
       const int64_t idx = oF1B + o;
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     float* dht = a.dht + int64_t(slot) * kH1 * 32;
     for (int p = olo * 32 + tid; p < ohi * 32; p += kHeadDenseThreads) {
       const int o = p >> 5, i = p & 31;
-      dht[p] = i < cnt ? sDH[i * kH1 + o] : 0.0f;
+      dht[p] = i < cnt ? sDH[i * kDHS + o] : 0.0f;
     }
   }
   for (int c = tid; c < (part == 0 ? C : 0); c += kHeadDenseThreads) {
@@ -965,7 +966,8 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // ---------------------------------------------------------------------------
 constexpr int kBwdThreads = 512;
 constexpr int kBwdIn = 2 * kFlat * 4 + kFlat;            // dp2, p2 (fp32), am2 of one sample
-constexpr int kBwdDp1 = 196 * kC1 * 4;                   // dp1 [196][32] fp32
+constexpr int kDp1S = kC1 + 1;                           // dp1 row stride (conflict-free TMEM unload)
+constexpr int kBwdDp1 = 196 * kDp1S * 4;                 // dp1 [196][33] fp32
 constexpr int kBwdRed = 8 * 832 * 4;                     // warp-pair partials (aliases dp1 + image)
 // image row stride 34: the 4 pool candidates' windows (offsets 0, 1, 34, 35)
 // of the 32 channel lanes fall in distinct banks
@@ -994,7 +996,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const float* iP2 = iDp2 + kFlat;
   const uint8_t* iAm2 = sIn + 2 * kFlat * 4;
   float* sDp1 = reinterpret_cast<float*>(sIn + kBwdIn);
-  float* sX = sDp1 + 196 * kC1;                          // [32][kXS] padded image
+  float* sX = sDp1 + 196 * kDp1S;                        // [32][kXS] padded image
   float* sRed = sDp1;                                    // [8][832] (after the conv1 loop)
   uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 32 * kXS);  // 3 x [196][32] pool1 argmax / relu'
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1091,7 +1093,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
             tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(b * 64 + t * 32 + c16 * 16), v);
             if (y < 14 && x < 14) {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kC1 + c16 * 16 + k] = v[k];
+              for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kDp1S + c16 * 16 + k] = v[k];
             }
           }
         }
@@ -1115,7 +1117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       for (int pp = warp; pp < 196; pp += kBwdThreads / 32) {
         const int py = pp / 14, px = pp - py * 14;
         const int dm = am1[pp * kC1 + co];   // pool1 argmax, bit 2: relu'
-        const float g = (dm & 4) ? sDp1[pp * kC1 + co] : 0.0f;
+        const float g = (dm & 4) ? sDp1[pp * kDp1S + co] : 0.0f;
         bacc += g;
         const int d = dm & 3;
         const float* xw = sX + (2 * py + (d >> 1)) * kXS + 2 * px + (d & 1);
@@ -1379,7 +1381,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   return a;
 }
 
-static size_t head_smem(int C, int BS) { return size_t(2 * BS * kH1 + BS * pad4(C)) * 4; }
+static size_t head_smem(int C, int BS) { return size_t(BS * kH1 + BS * kDHS + BS * pad4(C)) * 4; }
 
 // active-client thresholds below which a sweep uses the cluster head and the
 // 5-way (per filter row) conv2 wgrad split

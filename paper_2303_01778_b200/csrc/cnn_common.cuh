@@ -127,21 +127,26 @@ __device__ __forceinline__ uint32_t w2_off(int co, int tap, int ci) {
 __device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthreads) {
   const float4* w2 = reinterpret_cast<const float4*>(W + oC2W);
   constexpr int kUnits = 64 * 800 / 8, kU = 5;
+  // unit u = ((tap * 8 + co / 8) * 8 + co % 8) * 4 + ci / 8: a warp reads 8
+  // co rows x 128 contiguous bytes (one tap) and writes four 128-byte runs of
+  // the UMMA layout (the minimum 4 wavefronts per 512 bytes)
   for (int u0 = tid; u0 < kUnits; u0 += kU * nthreads) {
     float4 v[kU][2];
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
       const int u = u0 + k * nthreads;
       if (u < kUnits) {
-        v[k][0] = w2[2 * u];
-        v[k][1] = w2[2 * u + 1];
+        const int cg = u & 3, co = ((u >> 5) & 7) * 8 + ((u >> 2) & 7), tap = u >> 8;
+        const int src = (co * 800 + tap * 32 + cg * 8) >> 2;
+        v[k][0] = w2[src];
+        v[k][1] = w2[src + 1];
       }
     }
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
       const int u = u0 + k * nthreads;
       if (u >= kUnits) break;
-      const int e = u * 8, co = e / 800, rem = e - co * 800, tap = rem >> 5, ci = rem & 31;
+      const int cg = u & 3, co = ((u >> 5) & 7) * 8 + ((u >> 2) & 7), tap = u >> 8, ci = cg * 8;
       uint4 o;
       o.x = pack_bf16(v[k][0].x, v[k][0].y);
       o.y = pack_bf16(v[k][0].z, v[k][0].w);
