@@ -856,7 +856,15 @@ __global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
   pb::pdl_wait();
   const int s = blockIdx.x, i = blockIdx.y;
   const Slot sl = a.slots[s];
-  if (i >= sl.cnt) return;
+  if (i >= sl.cnt) {
+    // samples past a partial batch: zero activations, so the TMA weight
+    // gradients (whole position tiles, dz = 0 there) never multiply stale
+    // (possibly non-finite) workspace contents
+    if (sl.cnt == 0) return;
+    uint4* o = reinterpret_cast<uint4*>(at<bf16>(a, s, f.out) + int64_t(i) * f.HW * f.C);
+    for (int64_t e = threadIdx.x; e < int64_t(f.HW) * f.C / 8; e += kGnThreads) o[e] = make_uint4(0, 0, 0, 0);
+    return;
+  }
   extern __shared__ double dsm[];
   double* p1 = dsm;
   double* p2 = dsm + 4 * kGnThreads;

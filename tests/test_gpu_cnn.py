@@ -206,3 +206,20 @@ def test_cnn_dense_sweeps_match_sparse(spec, femnist_like, monkeypatch):
             errs = np.asarray([_rel(dense[c] - base, single[c] - base) for c in single if c < g])
             assert float(np.median(errs)) <= med, (g, sweeps, errs)
             assert errs.max() <= worst, (g, sweeps, errs)
+
+
+def test_cnn_stale_workspace_nan(spec, femnist_like, monkeypatch):
+    """A partial-batch client trained on CNN workspaces poisoned with NaN bit
+    patterns matches the clean run bit for bit (no kernel reads a sample row
+    past the batch without masking it)."""
+    import paper_2303_01778_b200.cnn as cnn
+    from paper_2303_01778_b200.models import cnn_init
+    X, y = femnist_like.features[:57], femnist_like.labels[:57]
+    w0 = cnn_init(spec, seed=1)
+    clean = _device_after(spec, w0, X, y, 20, 2, 0, monkeypatch)
+    for ws in (cnn._WS.buf, cnn._LZ.buf):
+        for t in ws.values():
+            t.fill_(float("nan")) if t.is_floating_point() else t.fill_(255)
+    poisoned = _device_after(spec, w0, X, y, 20, 2, 0, monkeypatch)
+    assert np.all(np.isfinite(poisoned[0])) and np.isfinite(poisoned[1])
+    assert np.array_equal(clean[0], poisoned[0]) and clean[1] == poisoned[1]

@@ -131,3 +131,20 @@ def test_resnet_fedavg_rounds_vs_oracle(spec, cifar_like):
         acc, loss = R.evaluate(ref, ev.features, ev.labels, 10)
         assert abs(oc.accuracy - acc) <= 0.03, (oc.round, oc.accuracy, acc)
         assert abs(oc.loss - loss) / loss <= 0.01, (oc.round, oc.loss, loss)
+
+
+def test_resnet_stale_workspace_nan(spec, cifar_like):
+    """Workspace memory is reused across groups, tests and other models: a
+    partial batch (13 samples, batch 5) trained on a workspace poisoned with
+    NaN bit patterns gives the same result as on a clean one (samples past
+    the batch must never feed the whole-tile weight gradients)."""
+    import paper_2303_01778_b200.resnet as rn
+    from paper_2303_01778_b200.models import resnet_init
+    X, y = cifar_like.features[:13], cifar_like.labels[:13]
+    w0 = resnet_init(spec, seed=1)
+    clean = _device(spec, w0, X, y, 5, 1, 0.02)
+    for t in rn._WS.buf.values():
+        t.view(-1).view(dtype=t.dtype).fill_(float("nan")) if t.is_floating_point() else t.fill_(255)
+    poisoned = _device(spec, w0, X, y, 5, 1, 0.02)
+    assert np.all(np.isfinite(poisoned[0])) and np.isfinite(poisoned[1])
+    assert np.array_equal(clean[0], poisoned[0]) and clean[1] == poisoned[1]
