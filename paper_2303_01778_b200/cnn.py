@@ -50,9 +50,10 @@ class _LazyWorkspace:
     def _get(self, name: str, numel: int, device) -> torch.Tensor:
         t = self.buf.get(name)
         if t is None or t.numel() < numel or t.device != device:
-            # 25% headroom: round sizes vary, and a reallocation synchronises
+            # 50% headroom: round sizes vary (the longest client sets the
+            # history length), and a reallocation synchronises
             self.buf.pop(name, None)
-            t = torch.empty(max(int(numel * 1.25), 4), dtype=torch.float32, device=device)
+            t = torch.empty(max(int(numel * 1.5), 4), dtype=torch.float32, device=device)
             self.buf[name] = t
         return t
 
