@@ -203,7 +203,7 @@ typedef struct {
   float* lz_w0t;            /* [3136*512] f32 scratch (W1 of w0 transposed)   */
   float* lz_zp;             /* max_t active_t*njt_t * 512*32 f32, njt_t = ceil(t*BS/128) */
   float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
-  float* lz_fpart;          /* 74*512*32 f32: tail split-K partials           */
+  float* lz_fpart;          /* max(74, g)*512*32 f32: forward GEMM partials   */
   int64_t lz_rows;          /* total history rows (multiple of 32)            */
   int32_t lz_defer;         /* 1: leave the fc1 block of w unmaterialised      */
                             /*    (fold it with pb_cnn_lazy_fold instead)      */

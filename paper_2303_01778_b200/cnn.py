@@ -57,11 +57,11 @@ class _LazyWorkspace:
             self.buf[name] = t
         return t
 
-    def get(self, rows: int, zp: int, gdt: int, device) -> dict[str, torch.Tensor]:
+    def get(self, rows: int, zp: int, gdt: int, slots: int, device) -> dict[str, torch.Tensor]:
         out = {"hx": self._get("hx", rows * 3136, device), "hxt": self._get("hxt", rows * 3136, device),
                "hd": self._get("hd", rows * 512, device), "hdt": self._get("hdt", rows * 512, device),
                "w0t": self._get("w0t", 3136 * 512, device), "zp": self._get("zp", zp, device),
-               "gdt": self._get("gdt", gdt, device), "fpart": self._get("fpart", 74 * 512 * 32, device)}
+               "gdt": self._get("gdt", gdt, device), "fpart": self._get("fpart", max(74, slots) * 512 * 32, device)}
         for k, width in (("hx", 3136), ("hxt", 3136), ("hd", 512), ("hdt", 512)):
             out[k][:rows * width].zero_()
         return out
@@ -196,7 +196,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     handle = None
     if lazy:
         hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
-        lz = _LZ.get(rows, zp, gdt, d)
+        lz = _LZ.get(rows, zp, gdt, G, d)
         hlen_d = torch.from_numpy(hlen).to(d)
         hoff_d = torch.from_numpy(hoff).to(d)
         a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),

@@ -299,7 +299,8 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
 }
 
 template <int MT>
-__global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+__global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
+                                                   int fuse) {
   pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;        // stages of MT*16 + 32 KB
   constexpr int kStage = MT * kShA + kShB;
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0) continue;
     const int s = g0 + u;
-    if (ks == 1) {
+    if (fuse) {
       fwd_finish(a, s, sl, o, v, njt);
     } else {
       float4* dst = reinterpret_cast<float4*>(a.fpart + ((int64_t(kz) * active + s) * kH1 + o) * 32);
@@ -804,6 +805,24 @@ void lazy_fc1_release(Args& a) {
   a.lzmaps = nullptr;
 }
 
+// side stream (+ fork / join events) of the calling stream's device
+struct Side {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static Side& side_of(cudaStream_t) {
+  static Side sides[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Side& sd = sides[dev & 63];
+  if (!sd.stream) {
+    cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
+  }
+  return sd;
+}
+
 // clients per CTA of the shared-W0 GEMMs: 8 while the sweep fills the
 // machine; fewer in sparser sweeps (each CTA streams the W0 tiles once for
 // its spc clients, so spc trades W0 traffic against grid size)
@@ -825,30 +844,44 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   const int spc = slots_per_cta(active);
   const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
-    pb::prof_begin(pb::K_CNN_LZ_XT, s);
-    pb::launch_pdl(k_lz_xt, dim3(active, kBwKT), dim3(128), 0, s, 1, a);
-    pb::prof_end(pb::K_CNN_LZ_XT, s);
+    // the history transpose and the forward Gram (HBM-bound) run on a side
+    // stream concurrently with the shared-W0 GEMM (tensor / L2-bound); the
+    // GEMM then leaves raw partials, and the epilogue (b1 + partials +
+    // history corrections, relu) joins both
+    cudaStream_t sg = s;
+    const bool fork = njt > 0;
+    if (fork) {
+      Side& side = side_of(s);
+      sg = side.stream;
+      cudaEventRecord(side.fork, s);
+      cudaStreamWaitEvent(sg, side.fork, 0);
+    }
+    pb::prof_begin(pb::K_CNN_LZ_XT, sg);
+    pb::launch_pdl(k_lz_xt, dim3(active, kBwKT), dim3(128), 0, sg, 1, a);
+    pb::prof_end(pb::K_CNN_LZ_XT, sg);
     if (njt > 0) {
-      pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, s);
+      pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, sg);
       // sparse sweeps: split K over a cluster while the grid fits one wave
       const int sms = pb::sm_count();
       const int gks = njt * active * 4 <= sms ? 4 : (njt * active * 2 <= sms ? 2 : 1);
-      if (gks == 1) {
-        pb::launch_pdl(k_lz_gram<true>, dim3(njt, active), dim3(128), kGramFwdSmem, s, 1, m, a, 1);
-      } else {
-        pb::launch_pdl(k_lz_gram<true>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128), kGramFwdSmem, s,
-                       unsigned(gks), m, a, gks);
-      }
-      pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, s);
+      pb::launch_pdl(k_lz_gram<true>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128), kGramFwdSmem, sg,
+                     unsigned(gks), m, a, gks);
+      pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, sg);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
+    const int fuse = !fork && ks == 1;
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
     if (spc == kSh8)
-      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc);
+      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse);
     else
-      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc);
+      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
-    if (ks > 1) {
+    if (fork) {
+      Side& side = side_of(s);
+      cudaEventRecord(side.join, sg);
+      cudaStreamWaitEvent(s, side.join, 0);
+    }
+    if (!fuse) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
       pb::launch_pdl(k_lz_fwd_epi, dim3(active, kH1 * 8 / kEpiThreads), dim3(kEpiThreads), 0, s, 1, a, active, ks);
       pb::prof_end(pb::K_CNN_LZ_FWD, s);
