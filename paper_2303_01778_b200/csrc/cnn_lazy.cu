@@ -53,6 +53,8 @@ struct LzMaps {
   CUtensorMap hxb;     // HX                          box 32  (current rows)
   CUtensorMap hda[4];  // HD            [rows][512],  box 32/64/96/128
   CUtensorMap hdb;     // HD                          box 32
+  CUtensorMap hxs;     // HX                          box rs rows (packed current rows, spc > 1)
+  CUtensorMap hds;     // HD                          box rs rows
   CUtensorMap hdt;     // HD^T          [512][rows],  box 128
   CUtensorMap hxt128;  // HX^T          [3136][rows], box 128
   CUtensorMap hxt256;  // HX^T                        box 256
@@ -249,7 +251,9 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
     const int64_t jstride = int64_t(njt) * 128;
     float* g = a.gdt + int64_t(s) * 32 * jstride + j0 + j;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) g[i * jstride] = live ? tf32_rna(nlr * v[i]) : 0.0f;
+    // rows past the batch are exactly zero: the backward's packed slots
+    // (rs < 32 rows each) accumulate these 32-row products into the next slot
+    for (int i = 0; i < 32; ++i) g[i * jstride] = live && i < cnt ? tf32_rna(nlr * v[i]) : 0.0f;
   }
   fence_before_sync();
   __syncthreads();
@@ -300,7 +304,7 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
 
 template <int MT>
 __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
-                                                   int fuse) {
+                                                   int fuse, int rs) {
   pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;        // stages of MT*16 + 32 KB
   constexpr int kStage = MT * kShA + kShB;
@@ -332,15 +336,15 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     }
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       const int k0 = (c0 + c) * 32;
-      pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * 32 * 128));
+      pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * rs * 128));
 #pragma unroll
       for (int t = 0; t < MT; ++t) pb::tma::load_2d(st + t * kShA, &m.w0, k0, (q * MT + t) * 128, f);
       for (int u = 0; u < spc; ++u)
-        if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * 32 * 128, &m.hxb, k0, rows[u], f);
+        if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * rs * 128, rs == 32 ? &m.hxb : &m.hxs, k0, rows[u], f);
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
-      const uint32_t idesc = idesc_tf32(128, spc * 32);
+      const uint32_t idesc = idesc_tf32(128, spc * rs);
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const uint64_t a0 = desc_sw128(smem_u32(st + t * kShA));
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     const int o = (q * MT + t) * 128 + (warp & 3) * 32 + lane;
     const Slot sl = sS[u];
     float v[32];
-    const uint32_t col = uint32_t(t * 256 + u * 32);
+    const uint32_t col = uint32_t(t * 256 + u * rs);
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col, *reinterpret_cast<float(*)[16]>(v));
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0) continue;
@@ -445,7 +449,8 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
 template <int MT>
-__global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc) {
+__global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
+                                                   int rs) {
   pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;
   constexpr int kStage = MT == 1 ? kShStage : MT * kShA + kShB;   // 48 | 64 KB
@@ -491,11 +496,12 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
           pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.hdb, (2 * c + h) * 32, rows[0], f);
         }
       } else if (c < n1) {
-        pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * 32 * 128));
+        pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * rs * 128));
 #pragma unroll
         for (int q = 0; q < MT; ++q) pb::tma::load_2d(st + q * kShA, &m.w0t, c * 32, (kt0 + q) * 128, f);
         for (int u = 0; u < spc; ++u)
-          if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * 32 * 128, &m.hdb, c * 32, rows[u], f);
+          if (sS[u].cnt > 0)
+            pb::tma::load_2d(st + MT * kShA + u * rs * 128, rs == 32 ? &m.hdb : &m.hds, c * 32, rows[u], f);
       } else if (MT == 1) {
         const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
         pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
             mma_tf32(tmem, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
         }
       } else if (c < n1) {
-        const uint32_t idesc = idesc_tf32(128, spc * 32);
+        const uint32_t idesc = idesc_tf32(128, spc * rs);
         const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
           const uint64_t bh = desc_sw128(smem_u32(st + 2 * kShA + h * 32 * 128));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem + u * 32, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+            mma_tf32(tmem + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
         }
       } else {
         const int u = us[(c - n1) / nj];
@@ -554,7 +560,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
           const uint64_t ah = desc_sw128(smem_u32(st + q * kShA));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem + q * 256 + u * 32, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+            mma_tf32(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
         }
       }
     };
@@ -570,7 +576,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
     const int k = (kt0 + q) * 128 + (warp & 3) * 32 + lane;
     const Slot sl = sS[u];
     float v[32];
-    const uint32_t col = uint32_t(q * 256 + u * 32);
+    const uint32_t col = uint32_t(q * 256 + u * rs);
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col, *reinterpret_cast<float(*)[16]>(v));
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + col + 16u, *reinterpret_cast<float(*)[16]>(v + 16));
     if (sl.cnt == 0 || k >= kFlat) continue;
@@ -789,6 +795,8 @@ int lazy_fc1_prepare(Args& a, cudaStream_t s) {
       (rc = make_2d_f32(&m->w0t, a.w0t, kH1, kFlat, kH1, 128)) ||
       (rc = make_2d_f32(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
       (rc = make_2d_f32(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
+      (rc = make_2d_f32(&m->hxs, a.hx, kFlat, R, kFlat, uint32_t((a.BS + 7) & ~7))) ||
+      (rc = make_2d_f32(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))) ||
       (rc = make_2d_f32(&m->hdt, a.hdt, R, kH1, R, 128)) ||
       (rc = make_2d_f32(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
       (rc = make_2d_f32(&m->hxt256, a.hxt, R, kFlat, R, 256)))
@@ -870,11 +878,14 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     const int fuse = !fork && ks == 1;
+    const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;   // B rows per slot: packed when several share a CTA
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
     if (spc == kSh8)
-      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse);
+      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
+                     rs);
     else
-      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse);
+      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
+                     rs);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (fork) {
       Side& side = side_of(s);
@@ -896,10 +907,13 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
-    if (spc == kSh8)
-      pb::launch_pdl(k_lz_bwd<2>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc);
-    else
-      pb::launch_pdl(k_lz_bwd<1>, dim3(kBwKT, groups), dim3(256), kShSmem, s, 1, m, a, active, spc);
+    {
+      const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;
+      if (spc == kSh8)
+        pb::launch_pdl(k_lz_bwd<2>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
+      else
+        pb::launch_pdl(k_lz_bwd<1>, dim3(kBwKT, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
+    }
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");
