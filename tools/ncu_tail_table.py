@@ -6,7 +6,7 @@ import io
 import subprocess
 import sys
 
-print("| kernel | grid | cluster | µs | DRAM MB | warps active % | issue % | top stalls |")
+print("| kernel | grid | cluster | duration µs | DRAM MB | warps active % | issue % | top stalls |")
 print("|---|---|---|---|---|---|---|---|")
 for rep in sys.argv[1:]:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -30,6 +30,6 @@ for rep in sys.argv[1:]:
         name = d["Kernel Name"].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
         mb = sum(num(k) * scale.get(units.get(k, "Mbyte"), 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         print(f"| {name} | {d.get('launch__grid_size')} | {d.get('launch__cluster_dim_x', '') or '-'} | "
-              f"{num('gpu__time_duration.sum'):.1f} | {mb:.1f} | "
+              f"{num('gpu__time_duration.sum') * {'ns': 1e-3, 'us': 1.0, 'ms': 1e3, 'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(units.get('gpu__time_duration.sum'), 1.0):.1f} | {mb:.1f} | "
               f"{num('sm__warps_active.avg.pct_of_peak_sustained_active'):.0f} | "
               f"{num('smsp__issue_active.avg.pct_of_peak_sustained_active'):.0f} | {stalls} |")
