@@ -182,6 +182,15 @@ class DeviceRuntime:
         self.cfg, self.plugin, self.spec, self.data = cfg, plugin, spec, data
         self.store, self.gauge = store, gauge
         self.last_device_seconds = 0.0
+        self.pending: GroupOutcome | None = None   # group whose result read is outstanding
+
+    def resolve(self) -> None:
+        """Complete the outstanding result read of the last group (raises on a
+        diverged client)."""
+        go, self.pending = self.pending, None
+        if go is not None:
+            go.resolve()
+            self.last_device_seconds = go.seconds
 
     def prepare(self, assignments: dict[int, list[int]], round_num: int) -> GroupInputs | None:
         """Host side of a round for the local devices: minibatch row ids of all
@@ -216,11 +225,15 @@ class DeviceRuntime:
             # FedAvg folds exactly the end models: the CNN's low-rank fc1 can be
             # folded from the round's history without materialising them
             defer = spec.kind == "cnn" and type(plugin) is FedAvg
+            # the group's result read (failures, losses, device time) can wait
+            # for the end of the round unless something needs it now
+            late = self.cfg.clock == "virtual" and not plugin.collect_local_loss
             go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
                              self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
-                             round_num, inputs=inputs, defer_fc1=defer)
+                             round_num, inputs=inputs, defer_fc1=defer, defer_check=late)
         finally:
             self.gauge.release(len(clients))
+        self.pending = go if go.pending is not None else None
         self.last_device_seconds = go.seconds
         groups, new_state = finalize_results(plugin, spec, go, w0, bundle, work)
         if go.lazy is not None:
@@ -261,6 +274,7 @@ class DeviceWorker:
         rt = self._rt(bundle)
         partial = rt.execute({self.device.device_id: list(clients)}, bundle, round_num)[
             self.device.device_id]
+        rt.resolve()
         timings = [TimingRecord(self.device.device_id, m, round_num,
                                 int(rt.data.sizes[m]),
                                 self._reported(rt, m, round_num, len(clients)))
@@ -549,6 +563,10 @@ class SimulationEngine:
         ledger.peak_live_model_replicas = self.gauge.peak
         if self.store is not None:
             ledger.state_bytes_disk = self.store.stats().bytes_on_disk
+        try:
+            self.runtime.resolve()   # the round's result read (queued after training)
+        except Exception as exc:
+            raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
         if sync:
             torch.cuda.synchronize()
         outcome = RoundOutcome(round=round_num, scheme=cfg.scheme, scheduling_mode=inp.plan.mode,

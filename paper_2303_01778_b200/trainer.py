@@ -243,6 +243,27 @@ class GroupOutcome:
     w_out: torch.Tensor     # [G, P] end models
     seconds: float          # device time of the training launch
     lazy: object | None = None  # deferred low-rank fc1 (cnn.LazyFc1): fc1_w rows unmaterialised
+    pending: object | None = None  # deferred result read (train_group(defer_check=True))
+
+    def resolve(self) -> None:
+        """Finish a deferred result read: wait for the group's [bad | steps |
+        loss] copy, raise on a diverged client, fill loss_mean / seconds."""
+        if self.pending is None:
+            return
+        res_h, done, t0, t1, round_num = self.pending
+        self.pending = None
+        done.synchronize()
+        res = res_h.numpy()
+        _IO["d2h"] += res.size * 8
+        G = len(self.clients)
+        bad_h, steps_h, loss_h = res[:G], res[G:2 * G].astype(np.int64), res[2 * G:]
+        self.seconds = max(t0.elapsed_time(t1) / 1e3, 1e-9)
+        for j in range(G):
+            if bad_h[j] >= 0:
+                raise NonFiniteLossError(f"client {self.clients[j]} round {round_num}: loss diverged")
+        if not np.array_equal(steps_h, self.steps):
+            raise RuntimeError(f"round {round_num}: device step counts differ from the plan")
+        self.loss_mean = loss_h / np.maximum(steps_h, 1)
 
 
 @dataclass
@@ -317,7 +338,7 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                 clients: Sequence[int], w0: torch.Tensor, global_bundle: ParamBundle,
                 state_work: torch.Tensor | None, epochs: int, batch_size: int, lr: float,
                 seed: int, round_num: int, inputs: GroupInputs | None = None,
-                defer_fc1: bool = False) -> GroupOutcome:
+                defer_fc1: bool = False, defer_check: bool = False) -> GroupOutcome:
     """Run every listed client's full local schedule concurrently on the GPU.
 
     defer_fc1 (CNN, plain SGD): leave the clients' fc1_w columns of w_out
@@ -365,6 +386,20 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     else:
         raise ValueError(f"unknown model kind {spec.kind!r}")
     t1.record()
+    if defer_check:
+        # the step counts are the plan's (a diverged client raises when the
+        # read completes, GroupOutcome.resolve); the read itself is queued
+        # behind the training without blocking the host
+        bs = n if batch_size <= 0 else np.minimum(batch_size, n)
+        steps_plan = (epochs * ((n + bs - 1) // bs)).astype(np.int64)
+        res_h = torch.empty(3 * G, dtype=torch.float64, pin_memory=True)
+        res_h.copy_(torch.cat([bad.double(), steps.double(), loss]), non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        if lazy is not None:
+            lazy.set_steps(steps_plan)
+        return GroupOutcome(clients, n, steps_plan, np.full(G, np.nan), w_out, float("nan"), lazy,
+                            pending=(res_h, done, t0, t1, round_num))
     # one device->host read per group: failures, step counts, losses
     res = torch.cat([bad.double(), steps.double(), loss]).cpu().numpy()
     _IO["d2h"] += res.size * 8

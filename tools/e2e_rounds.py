@@ -27,3 +27,14 @@ for r in range(3, 13):
     wall = (time.perf_counter() - t0) * 1e3
     print(f"round {r}: wall {wall:.1f} ms  events {e0.elapsed_time(e1):.1f} ms  train-launch {oc.device_seconds * 1e3:.1f} ms", flush=True)
 # same rounds' work device-timed back to back
+
+# host-side profile of run_round (the device work dominates cumulative time of
+# the blocking sync; the rest is the per-round host overhead)
+import cProfile  # noqa: E402
+import pstats  # noqa: E402
+pr = cProfile.Profile()
+pr.enable()
+for r in range(13, 16):
+    eng.run_round(r)
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
