@@ -152,9 +152,9 @@ int pb_lr_eval(const float* X, const int32_t* Y, int64_t rows, int F, int C, con
  *     per sweep; conv2 forward/dgrad/wgrad run on tcgen05 (bf16 operands,
  *     fp32 TMEM accumulation), the rest in fp32.  Workspace buffers are
  *     caller-allocated, sized per slot (= client) for BS samples:
- *       ws_slots 32 B, ws_p1 BS*21504 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
+ *       ws_slots 32 B, ws_p1 BS*21568 B, ws_am1 BS*6272 B, ws_p2 BS*3136 f32,
  *       ws_am2 BS*3136 B, ws_h/ws_dh BS*512 f32, ws_dp2 BS*3136 f32,
- *       ws_dz BS*43008 B, ws_dp1 BS*6272 f32 (per-sample conv1/bias gradient
+ *       ws_dz BS*43136 B, ws_dp1 BS*6272 f32 (per-sample conv1/bias gradient
  *       partials, 896 used), ws_dht 16384 f32 per slot.
  * ------------------------------------------------------------------------- */
 typedef struct {

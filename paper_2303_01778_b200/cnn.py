@@ -13,8 +13,8 @@ from ._lib import CnnTrainArgs, LazyFoldArgs, lib, ptr, stream_of
 from .models import ModelSpec
 
 # bytes per sample of each workspace buffer (include/parrot_b200.h)
-_PER_SAMPLE = {"p1": 4 * 336 * 16, "am1": 6272, "p2": 3136 * 4, "am2": 3136, "h": 512 * 4, "dh": 512 * 4,
-               "dp2": 3136 * 4, "dz": 8 * 336 * 16, "dp1": 6272 * 4}
+_PER_SAMPLE = {"p1": 4 * 337 * 16, "am1": 6272, "p2": 3136 * 4, "am2": 3136, "h": 512 * 4, "dh": 512 * 4,
+               "dp2": 3136 * 4, "dz": 8 * 337 * 16, "dp1": 6272 * 4}
 MAX_BATCH = 32
 
 

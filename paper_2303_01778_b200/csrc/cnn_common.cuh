@@ -18,7 +18,10 @@ using namespace pb::umma;
 constexpr int kImg = 28, kC1 = 32, kC2 = 64, kH1 = 512, kFlat = 7 * 7 * kC2;  // 3136
 constexpr int kP1 = 14 * 14 * kC1;   // 6272 pooled conv1 outputs
 constexpr int kG = 18;               // padded 14x14 grid width (2-pixel border)
-constexpr int kRows = 336;           // plane rows (>= 256 + 4*18 + 4 = 332)
+// plane rows (>= 256 + 4*18 + 4 = 332); 337 puts consecutive planes 16 B
+// apart modulo 128 B, so the 4 planes a warp of 32 channel lanes writes fall
+// in distinct banks
+constexpr int kRows = 337;
 constexpr int kPlane = kRows * 16;   // bytes per plane (8 channels x bf16)
 constexpr int kP1Bytes = 4 * kPlane;   // p1 image, 4 channel planes
 constexpr int kDzBytes = 8 * kPlane;   // dz2 image, 8 channel planes
