@@ -1525,6 +1525,36 @@ int forward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   return pb::check_launch("resnet forward");
 }
 
+// Side stream of the calling device: each convolution's weight gradient + SGD
+// step runs there, concurrently with the data-gradient chain of the layers
+// below (they share only read-only inputs; the SGD follows the layer's own
+// data gradient, which read the old weights).
+struct RnSide {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static RnSide& rn_side() {
+  static RnSide sides[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  RnSide& sd = sides[dev & 63];
+  if (!sd.stream) {
+    cudaStreamCreateWithFlags(&sd.stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
+  }
+  return sd;
+}
+
+// weight gradient + SGD of conv c on the side stream, after everything queued
+// on s so far (its dz and the layer's data gradient)
+static void wgrad_side(const Net& a, const ConvL& c, int active, cudaStream_t s) {
+  RnSide& sd = rn_side();
+  cudaEventRecord(sd.fork, s);
+  cudaStreamWaitEvent(sd.stream, sd.fork, 0);
+  launch_conv(a, c, WGRAD, active, sd.stream);
+}
+
 int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   const int nb = int(pl.blocks.size());
   GnSgd gs{};
@@ -1564,11 +1594,11 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(cb);
     launch_conv(a, cb, DGRAD, active, s);   // du (old weights)
-    launch_conv(a, cb, WGRAD, active, s);   // + SGD
+    wgrad_side(a, cb, active, s);   // + SGD
     if (b.conv_d >= 0) {
       add_gn(pl.convs[b.conv_d]);
       launch_conv(a, pl.convs[b.conv_d], DGRAD, active, s);
-      launch_conv(a, pl.convs[b.conv_d], WGRAD, active, s);
+      wgrad_side(a, pl.convs[b.conv_d], active, s);
     }
     GnB m{};
     m.C = ca.k.Cout;
@@ -1584,7 +1614,7 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(ca);
     launch_conv(a, ca, DGRAD, active, s);
-    launch_conv(a, ca, WGRAD, active, s);
+    wgrad_side(a, ca, active, s);
   }
   // stem: gradient of act0 = block 0's conv_a dgrad + its identity shortcut
   const ConvL& c0 = pl.convs[0];
@@ -1601,7 +1631,12 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
   pb::prof_end(pb::K_RN_NORM, s);
   add_gn(c0);
-  launch_conv(a, c0, WGRAD, active, s);
+  wgrad_side(a, c0, active, s);   // (the side stream also serialises the shared partial buffer)
+  {  // join the side stream's weight updates
+    RnSide& sd = rn_side();
+    cudaEventRecord(sd.join, sd.stream);
+    cudaStreamWaitEvent(s, sd.join, 0);
+  }
   pb::prof_begin(pb::K_RN_SGD, s);
   pb::launch_pdl(k_rn_gn_sgd, dim3(active, gs.n), dim3(256), 0, s, 1, a, gs);
   pb::prof_end(pb::K_RN_SGD, s);
