@@ -164,6 +164,12 @@ constexpr int kCvA = 128 * 64 * 2;            // 16 KB: 128 rows x 64 bf16 K
 constexpr int kCvB = 256 * 64 * 2;            // 32 KB
 constexpr int kCvStage = kCvA + kCvB;
 constexpr size_t kCvSmem = kStages * kCvStage;  // 192 KB
+// TMA convolution rings: tiles up to 128 wide use a 96 KB ring (4 stages of
+// 24 KB at N=64, 3 of 32 KB at N=128) so two CTAs -- two independent
+// TMA->MMA chains -- share an SM; 256-wide tiles keep the 192 KB ring
+__host__ __device__ constexpr int cv_stage_bytes(int ntile) { return kCvA + ntile * 128; }
+__host__ __device__ constexpr int cv_stages(int ntile) { return ntile >= 256 ? 4 : (ntile > 64 ? 3 : 4); }
+inline size_t cv_smem(int ntile) { return size_t(cv_stages(ntile)) * cv_stage_bytes(ntile) + 1024; }
 
 __device__ __forceinline__ uint32_t cv_off(int row, int ku) {  // K-major / MN-major unit slot
   return uint32_t((row >> 3) * 1024 + ku * 128 + (row & 7) * 16);
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv(Net a, ConvK k, int ntile) {
 // boxes at (pad - s, pad - r), B = boxes of the transposed weight copy
 // [ci][r][s][co] (K-major over (r, s, co)), D = dL/dx [(n,h,w)][ci].
 template <bool DG>
-__global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(256, 2) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
                                                         const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
                                                         int ntile, int Ht, int Nt) {
   pb::pdl_wait();
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   if (warp == 0) tmem_alloc<256>(&tmem_base);
-  if (tid == 0) pb::tma::ring_barriers(full, empty, kStages);
+  if (tid == 0) pb::tma::ring_barriers(full, empty, cv_stages(ntile));
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
       for (int kk = 0; kk < 4; ++kk)
         mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
     };
-    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+    pb::tma::tma_ring_rt(cv_stages(ntile), n, smem, cv_stage_bytes(ntile), full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv_tma(const __grid_constant__ 
 // TMA zero-fill; a class without taps (1x1 downsample, odd parity) writes 0.
 // grid (M tiles over Ho x Wo, Cinp / ntile, slots * 4), 256 threads
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(256, 2) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
                                                             const __grid_constant__ CUtensorMap tb, Net a,
                                                             ConvK k, int ntile, int Ht, int Nt) {
   pb::pdl_wait();
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constan
   __shared__ int ntap;
   if (warp == 0) tmem_alloc<256>(&tmem_base);
   if (tid == 0) {
-    pb::tma::ring_barriers(full, empty, kStages);
+    pb::tma::ring_barriers(full, empty, cv_stages(ntile));
     int n = 0;
     for (int r = 0; r < k.R; ++r)
       for (int q = 0; q < k.R; ++q) {
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constan
       for (int kk = 0; kk < 4; ++kk)
         mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
     };
-    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+    pb::tma::tma_ring_rt(cv_stages(ntile), n, smem, cv_stage_bytes(ntile), full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_dgrad_s2_tma(const __grid_constan
 // split in chunks of 1024 per CTA, partials in the weight layout as before.
 // grid (ceil(RS*Cinp/128), Cout/ntile, slots * nsplit), 256 threads
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
+__global__ void __launch_bounds__(256, 2) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
                                                          const __grid_constant__ CUtensorMap tdz, Net a, ConvK k,
                                                          int ntile, int Hs, int Ns) {
   pb::pdl_wait();
@@ -539,7 +545,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
   if (warp == 0) tmem_alloc<256>(&tmem_base);
-  if (tid == 0) pb::tma::ring_barriers(full, empty, kStages);
+  if (tid == 0) pb::tma::ring_barriers(full, empty, cv_stages(ntile));
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_wgrad_tma(const __grid_constant__
       for (int kk = 0; kk < 4; ++kk)
         mma_bf16(tmem, mk(smem_u32(st) + kk * 2048), mk(smem_u32(st + 16384) + kk * 2048), idesc, c > 0 || kk > 0);
     };
-    pb::tma::tma_ring<kStages>(n, smem, kCvStage, full, empty, issue, mma);
+    pb::tma::tma_ring_rt(cv_stages(ntile), n, smem, cv_stage_bytes(ntile), full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -1437,7 +1443,7 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const int nt = conv_ntile(k.Cout);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cout / nt, active);
     pb::prof_begin(pb::K_RN_CONV_FWD, s);
-    pb::launch_pdl(k_rn_conv_tma<false>, g, dim3(256), kCvSmem + 1024, s, 1, c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_conv_tma<false>, g, dim3(256), cv_smem(nt), s, 1, c.ta, c.tb, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_FWD, s);
   } else if (mode == FWD) {
     const int nt = conv_ntile(k.Cout);
@@ -1449,13 +1455,13 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.Ho * k.Wo + 127) / 128, k.Cinp / nt, active * 4);
     pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
-    pb::launch_pdl(k_rn_dgrad_s2_tma, g, dim3(256), kCvSmem + 1024, s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_dgrad_s2_tma, g, dim3(256), cv_smem(nt), s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD && c.tma_dg) {
     const int nt = conv_ntile(k.Cinp);
     const dim3 g((a.BS * k.H * k.W + 127) / 128, k.Cinp / nt, active);
     pb::prof_begin(pb::K_RN_CONV_DGRAD, s);
-    pb::launch_pdl(k_rn_conv_tma<true>, g, dim3(256), kCvSmem + 1024, s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
+    pb::launch_pdl(k_rn_conv_tma<true>, g, dim3(256), cv_smem(nt), s, 1, c.tad, c.tbd, a, k, nt, c.Ht, c.Nt);
     pb::prof_end(pb::K_RN_CONV_DGRAD, s);
   } else if (mode == DGRAD) {
     const int nt = conv_ntile(k.Cinp);
@@ -1468,7 +1474,7 @@ void launch_conv(const Net& a, const ConvL& c, int mode, int active, cudaStream_
     const dim3 g((k.R * k.R * k.Cinp + 127) / 128, k.Cout / nt, active * k.nsplit);
     pb::prof_begin(pb::K_RN_CONV_WGRAD, s);
     if (c.tma && c.tma_wg)
-      pb::launch_pdl(k_rn_wgrad_tma, g, dim3(256), kCvSmem + 1024, s, 1, c.twx, c.twd, a, k, nt, c.Hs, c.Ns);
+      pb::launch_pdl(k_rn_wgrad_tma, g, dim3(256), cv_smem(nt), s, 1, c.twx, c.twd, a, k, nt, c.Hs, c.Ns);
     else
       pb::launch_pdl(k_rn_conv<WGRAD>, g, dim3(256), kCvSmem, s, 1, a, k, nt);
     pb::prof_end(pb::K_RN_CONV_WGRAD, s);
@@ -1832,7 +1838,7 @@ extern "C" int pb_rn_conv_selftest(int mode, int BS, int cnt, int Cinp, int Cout
       // the network zeroes dz of samples past the batch (k_rn_gn_bwd)
       const int64_t live = int64_t(cnt) * Ho * Ho * Cout * 2;
       cudaMemsetAsync(arena + k.dz + live, 0, size_t(dzb - live), s);
-      k_rn_wgrad_tma<<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, kCvSmem + 1024, s>>>(
+      k_rn_wgrad_tma<<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, cv_smem(nt), s>>>(
           pl.convs[0].twx, pl.convs[0].twd, a, k, nt, pl.convs[0].Hs, pl.convs[0].Ns);
     } else {
       k_rn_conv<WGRAD><<<dim3(int((M + 127) / 128), Cout / nt, k.nsplit), 256, kCvSmem, s>>>(a, k, nt);

@@ -104,6 +104,31 @@ __device__ __forceinline__ void tma_ring(int n, uint8_t* ring, int stage_bytes, 
   if (n > 0) umma::mbar_wait(&empty[(n - 1) % S], ((n - 1) / S) & 1);
 }
 
+// tma_ring with the stage count chosen at run time (S <= the barrier arrays)
+template <class Issue, class Mma>
+__device__ __forceinline__ void tma_ring_rt(int S, int n, uint8_t* ring, int stage_bytes, uint64_t* full,
+                                            uint64_t* empty, Issue issue, Mma mma) {
+  for (int c = 0; c < n && c < S; ++c) issue(c, ring + c * stage_bytes, &full[c]);
+  int st = 0, ph = 0;   // stage and parity of chunk c
+  for (int c = 0; c < n; ++c) {
+    umma::mbar_wait(&full[st], ph);
+    umma::fence_after_sync();
+    mma(c, ring + st * stage_bytes);
+    umma::commit(&empty[st]);
+    const int nx = c - 1 + S;
+    if (c >= 1 && nx < n) {
+      const int s2 = st == 0 ? S - 1 : st - 1, p2 = st == 0 ? ph ^ 1 : ph;   // chunk c-1
+      umma::mbar_wait(&empty[s2], p2);   // chunk c-1's MMAs released the stage
+      issue(nx, ring + s2 * stage_bytes, &full[s2]);
+    }
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+  if (n > 0) umma::mbar_wait(&empty[(n - 1) % S], ((n - 1) / S) & 1);
+}
+
 __device__ __forceinline__ void ring_barriers(uint64_t* full, uint64_t* empty, int S) {
   for (int i = 0; i < S; ++i) {
     umma::mbar_init(&full[i], 1);
