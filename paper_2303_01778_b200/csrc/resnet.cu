@@ -164,11 +164,12 @@ constexpr int kCvA = 128 * 64 * 2;            // 16 KB: 128 rows x 64 bf16 K
 constexpr int kCvB = 256 * 64 * 2;            // 32 KB
 constexpr int kCvStage = kCvA + kCvB;
 constexpr size_t kCvSmem = kStages * kCvStage;  // 192 KB
-// TMA convolution rings: tiles up to 128 wide use a 96 KB ring (4 stages of
-// 24 KB at N=64, 3 of 32 KB at N=128) so two CTAs -- two independent
-// TMA->MMA chains -- share an SM; 256-wide tiles keep the 192 KB ring
+// TMA convolution rings: tiles up to 128 wide use 3-stage rings (72 KB at
+// N=64, 96 KB at N=128) and only the TMEM columns they need, so three / two
+// CTAs -- independent TMA->MMA chains -- share an SM; 256-wide tiles keep the
+// 192 KB ring
 __host__ __device__ constexpr int cv_stage_bytes(int ntile) { return kCvA + ntile * 128; }
-__host__ __device__ constexpr int cv_stages(int ntile) { return ntile >= 256 ? 4 : (ntile > 64 ? 3 : 4); }
+__host__ __device__ constexpr int cv_stages(int ntile) { return ntile >= 256 ? 4 : 3; }
 inline size_t cv_smem(int ntile) { return size_t(cv_stages(ntile)) * cv_stage_bytes(ntile) + 1024; }
 
 __device__ __forceinline__ uint32_t cv_off(int row, int ku) {  // K-major / MN-major unit slot
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(256, 1) k_rn_conv(Net a, ConvK k, int ntile) {
 // boxes at (pad - s, pad - r), B = boxes of the transposed weight copy
 // [ci][r][s][co] (K-major over (r, s, co)), D = dL/dx [(n,h,w)][ci].
 template <bool DG>
-__global__ void __launch_bounds__(256, 2) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(256, 3) k_rn_conv_tma(const __grid_constant__ CUtensorMap ta,
                                                         const __grid_constant__ CUtensorMap tb, Net a, ConvK k,
                                                         int ntile, int Ht, int Nt) {
   pb::pdl_wait();
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_conv_tma(const __grid_constant__ 
   uint8_t* smem = pb::tma::align1k(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (warp == 0) tmem_alloc_rt(&tmem_base, uint32_t(ntile));
   if (tid == 0) pb::tma::ring_barriers(full, empty, cv_stages(ntile));
   fence_before_sync();
   __syncthreads();
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_conv_tma(const __grid_constant__ 
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  if (warp == 0) tmem_free_rt(tmem, uint32_t(ntile));
 }
 
 // ---------------------------------------------------------------------------
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_conv_tma(const __grid_constant__ 
 // TMA zero-fill; a class without taps (1x1 downsample, odd parity) writes 0.
 // grid (M tiles over Ho x Wo, Cinp / ntile, slots * 4), 256 threads
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(256, 3) k_rn_dgrad_s2_tma(const __grid_constant__ CUtensorMap ta,
                                                             const __grid_constant__ CUtensorMap tb, Net a,
                                                             ConvK k, int ntile, int Ht, int Nt) {
   pb::pdl_wait();
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_dgrad_s2_tma(const __grid_constan
   __shared__ uint32_t tmem_base;
   __shared__ int taps[9][3];   // r*R + s, dy, dx
   __shared__ int ntap;
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (warp == 0) tmem_alloc_rt(&tmem_base, uint32_t(ntile));
   if (tid == 0) {
     pb::tma::ring_barriers(full, empty, cv_stages(ntile));
     int n = 0;
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_dgrad_s2_tma(const __grid_constan
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  if (warp == 0) tmem_free_rt(tmem, uint32_t(ntile));
 }
 
 // ---------------------------------------------------------------------------
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_dgrad_s2_tma(const __grid_constan
 // split in chunks of 1024 per CTA, partials in the weight layout as before.
 // grid (ceil(RS*Cinp/128), Cout/ntile, slots * nsplit), 256 threads
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
+__global__ void __launch_bounds__(256, 3) k_rn_wgrad_tma(const __grid_constant__ CUtensorMap tx,
                                                          const __grid_constant__ CUtensorMap tdz, Net a, ConvK k,
                                                          int ntile, int Hs, int Ns) {
   pb::pdl_wait();
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_wgrad_tma(const __grid_constant__
   uint8_t* smem = pb::tma::align1k(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t tmem_base;
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  if (warp == 0) tmem_alloc_rt(&tmem_base, uint32_t(ntile));
   if (tid == 0) pb::tma::ring_barriers(full, empty, cv_stages(ntile));
   fence_before_sync();
   __syncthreads();
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(256, 2) k_rn_wgrad_tma(const __grid_constant__
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  if (warp == 0) tmem_free_rt(tmem, uint32_t(ntile));
 }
 
 // ---------------------------------------------------------------------------
