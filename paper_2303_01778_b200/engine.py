@@ -129,6 +129,7 @@ class RoundInputs:
     assign: dict
     group: GroupInputs | None
     wall0: float
+    records: list | None = None   # virtual-clock timing records, committed at hand-out
 
     def upload(self) -> "RoundInputs":
         if self.group is not None:
@@ -441,7 +442,7 @@ class SimulationEngine:
         if inp is None:
             inp = self._prepare(round_num)
         if self.cfg.clock == "virtual":
-            self._record(inp, None)
+            self.history.add_many(inp.records)
         return inp
 
     # -- host/device overlap ---------------------------------------------------
@@ -501,9 +502,11 @@ class SimulationEngine:
             assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
         inp = RoundInputs(round_num, selection, sizes, fits, fit_seconds, schedule_seconds, plan,
                           fa_tasks, assign, self.runtime.prepare(assign, round_num), wall0)
+        if cfg.clock == "virtual":   # built here (possibly on the helper thread), added at hand-out
+            inp.records = self._records(inp, None)
         return inp
 
-    def _record(self, inp: "RoundInputs", measured_per_client: float | None) -> None:
+    def _records(self, inp: "RoundInputs", measured_per_client: float | None) -> list:
         """Timing records in the reference's order: device order, plan order
         (fedsim/engine.py:689-697), or completion order for FA_DIST."""
         r = inp.round
@@ -512,9 +515,12 @@ class SimulationEngine:
         else:
             tasks = [(dev, m) for dev in range(self.cfg.num_devices)
                      for m in inp.plan.assignments.get(dev, [])]
-        for dev, m in tasks:
-            record(self.history, TimingRecord(dev, m, r, inp.sizes[m],
-                                              self._reported(dev, m, r, measured_per_client)))
+        return [TimingRecord(dev, m, r, inp.sizes[m], self._reported(dev, m, r, measured_per_client))
+                for dev, m in tasks]
+
+    def _record(self, inp: "RoundInputs", measured_per_client: float | None) -> None:
+        for rec in self._records(inp, measured_per_client):
+            record(self.history, rec)
 
     def execute_round(self, inp: "RoundInputs", sync: bool = True) -> RoundOutcome:
         """Device half of a round: batched training, hierarchical fold,
