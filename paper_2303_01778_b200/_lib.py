@@ -7,6 +7,8 @@ every non-zero return code becomes ``NativeError`` carrying pb_last_error().
 from __future__ import annotations
 
 import ctypes
+
+import numpy as np
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint64, c_void_p
 from pathlib import Path
 
@@ -158,6 +160,14 @@ def prof_collect() -> dict[str, tuple[float, int]]:
     cnt = (c_int64 * n)()
     lib.check(lib.pb_prof_collect(ms, cnt, n))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES) if cnt[i]}
+
+
+def h2d(a, device):
+    """Small host array -> device without a host stall: pinned staging and an
+    asynchronous copy on the current stream (a pageable copy would wait for
+    all queued device work first)."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(device, non_blocking=True)
 
 
 def ptr(t) -> int | None:

@@ -9,7 +9,7 @@ import os
 import numpy as np
 import torch
 
-from ._lib import CnnTrainArgs, LazyFoldArgs, lib, ptr, stream_of
+from ._lib import CnnTrainArgs, LazyFoldArgs, h2d, lib, ptr, stream_of
 from .models import ModelSpec
 
 # bytes per sample of each workspace buffer (include/parrot_b200.h)
@@ -118,9 +118,9 @@ class LazyFc1:
         r = np.asarray(rows)
         lo = int(self.hoff[r[0]])
         hi = int(self.hoff[r[-1]] + self.hlen[r[-1]])
-        hoff = torch.from_numpy(self.hoff[r].astype(np.int64)).to(d)
-        nrows = torch.from_numpy((self.steps[r] * self.BS).astype(np.int32)).to(d)
-        w = torch.from_numpy(np.asarray(weights, dtype=np.float32)).to(d)
+        hoff = h2d(self.hoff[r].astype(np.int64), d)
+        nrows = h2d((self.steps[r] * self.BS).astype(np.int32), d)
+        w = h2d(np.asarray(weights, dtype=np.float32), d)
         part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
         f = LazyFoldArgs()
         f.acc, f.w0, f.hxt, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hxt"]), ptr(self.lz["hdt"])
@@ -174,8 +174,8 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     loss.zero_()
     steps.zero_()
     bad.fill_(-1)
-    rank_d = torch.from_numpy(rank).to(d)
-    n_d = torch.from_numpy(n.astype(np.int32)).to(d)
+    rank_d = h2d(rank, d)
+    n_d = h2d(n.astype(np.int32), d)
     ws = _WS.get(G, BS, d)
     a = CnnTrainArgs()
     a.X, a.Y, a.order, a.order_off, a.n, a.rank = (ptr(data.X), ptr(data.Y), ptr(rows_d),
@@ -197,8 +197,8 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     if lazy:
         hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
         lz = _LZ.get(rows, zp, gdt, G, d)
-        hlen_d = torch.from_numpy(hlen).to(d)
-        hoff_d = torch.from_numpy(hoff).to(d)
+        hlen_d = h2d(hlen, d)
+        hoff_d = h2d(hoff, d)
         a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),
                                                 ptr(lz["hdt"]))
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
