@@ -1508,34 +1508,12 @@ void launch_gn_fwd(const Net& a, const ConvL& c, int64_t res, const ConvL* c2, i
   pb::prof_end(pb::K_RN_NORM, s);
 }
 
-int forward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
-  pb::prof_begin(pb::K_RN_NORM, s);
-  pb::launch_pdl(k_rn_stem, dim3(active, a.BS), dim3(256), 0, s, 1, a, pl.t0);
-  pb::prof_end(pb::K_RN_NORM, s);
-  launch_conv(a, pl.convs[0], FWD, active, s);
-  launch_gn_fwd(a, pl.convs[0], -1, nullptr, pl.act0, active, s);
-  for (const Block& b : pl.blocks) {
-    launch_conv(a, pl.convs[b.conv_a], FWD, active, s);
-    launch_gn_fwd(a, pl.convs[b.conv_a], -1, nullptr, b.u, active, s);
-    launch_conv(a, pl.convs[b.conv_b], FWD, active, s);
-    if (b.conv_d >= 0) {
-      launch_conv(a, pl.convs[b.conv_d], FWD, active, s);
-      launch_gn_fwd(a, pl.convs[b.conv_b], -1, &pl.convs[b.conv_d], b.act_out, active, s);
-    } else {
-      launch_gn_fwd(a, pl.convs[b.conv_b], b.act_in, nullptr, b.act_out, active, s);
-    }
-  }
-  const size_t hsm = size_t(a.BS) * (512 + a.C) * 4;
-  pb::prof_begin(pb::K_RN_HEAD, s);
-  pb::launch_pdl(k_rn_head, dim3(active), dim3(256), hsm, s, 1, a, pl.blocks.back().act_out, pl.gout_last, pl.fc_off);
-  pb::prof_end(pb::K_RN_HEAD, s);
-  return pb::check_launch("resnet forward");
-}
-
-// Side stream of the calling device: each convolution's weight gradient + SGD
-// step runs there, concurrently with the data-gradient chain of the layers
-// below (they share only read-only inputs; the SGD follows the layer's own
-// data gradient, which read the old weights).
+// Side stream of the calling device.  Forward: the downsample convolution of
+// a block runs there, concurrently with the block's main branch.  Backward:
+// each convolution's weight gradient + SGD step runs there, concurrently
+// with the data-gradient chain of the layers below (they share only
+// read-only inputs; the SGD follows the layer's own data gradient, which
+// read the old weights).
 struct RnSide {
   cudaStream_t stream = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -1551,6 +1529,37 @@ static RnSide& rn_side() {
     cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
   }
   return sd;
+}
+
+int forward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
+  pb::prof_begin(pb::K_RN_NORM, s);
+  pb::launch_pdl(k_rn_stem, dim3(active, a.BS), dim3(256), 0, s, 1, a, pl.t0);
+  pb::prof_end(pb::K_RN_NORM, s);
+  launch_conv(a, pl.convs[0], FWD, active, s);
+  launch_gn_fwd(a, pl.convs[0], -1, nullptr, pl.act0, active, s);
+  for (const Block& b : pl.blocks) {
+    if (b.conv_d >= 0) {   // the downsample branch reads only the block input: side stream
+      RnSide& sd = rn_side();
+      cudaEventRecord(sd.fork, s);
+      cudaStreamWaitEvent(sd.stream, sd.fork, 0);
+      launch_conv(a, pl.convs[b.conv_d], FWD, active, sd.stream);
+      cudaEventRecord(sd.join, sd.stream);
+    }
+    launch_conv(a, pl.convs[b.conv_a], FWD, active, s);
+    launch_gn_fwd(a, pl.convs[b.conv_a], -1, nullptr, b.u, active, s);
+    launch_conv(a, pl.convs[b.conv_b], FWD, active, s);
+    if (b.conv_d >= 0) {
+      cudaStreamWaitEvent(s, rn_side().join, 0);
+      launch_gn_fwd(a, pl.convs[b.conv_b], -1, &pl.convs[b.conv_d], b.act_out, active, s);
+    } else {
+      launch_gn_fwd(a, pl.convs[b.conv_b], b.act_in, nullptr, b.act_out, active, s);
+    }
+  }
+  const size_t hsm = size_t(a.BS) * (512 + a.C) * 4;
+  pb::prof_begin(pb::K_RN_HEAD, s);
+  pb::launch_pdl(k_rn_head, dim3(active), dim3(256), hsm, s, 1, a, pl.blocks.back().act_out, pl.gout_last, pl.fc_off);
+  pb::prof_end(pb::K_RN_HEAD, s);
+  return pb::check_launch("resnet forward");
 }
 
 // weight gradient + SGD of conv c on the side stream, after everything queued
