@@ -159,9 +159,11 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
 
 def client_train(flat_w0, X: np.ndarray, y: np.ndarray, client_id: int, seed: int, rnd: int,
                  epochs: int, batch_size: int, lr: float, n_classes: int,
-                 dtype=torch.float64, emulate_bf16: bool = False):
-    """Returns (flat end parameters, steps, mean per-step loss)."""
+                 dtype=torch.float64, emulate_bf16: bool = False, mu: float = 0.0):
+    """Returns (flat end parameters, steps, mean per-step loss).  mu > 0 adds
+    FedProx's proximal gradient mu * (w - w0) (fedsim/trainer.py:249-257)."""
     params = [p.requires_grad_(True) for p in unflatten(flat_w0, n_classes, dtype)]
+    anchor = [p.detach().clone() for p in params]
     Xt = torch.as_tensor(np.asarray(X), dtype=dtype)
     yt = torch.as_tensor(np.asarray(y), dtype=torch.long)
     n = len(y)
@@ -173,8 +175,8 @@ def client_train(flat_w0, X: np.ndarray, y: np.ndarray, client_id: int, seed: in
             loss = F.cross_entropy(forward(params, Xt[idx], emulate_bf16), yt[idx])
             grads = torch.autograd.grad(loss, params)
             with torch.no_grad():
-                for p, g in zip(params, grads):
-                    p -= lr * g
+                for p, g, p0 in zip(params, grads, anchor):
+                    p -= lr * (g + mu * (p - p0)) if mu else lr * g
             loss_sum += float(loss.detach())
             steps += 1
     return flatten(params), steps, loss_sum / steps

@@ -223,3 +223,85 @@ def test_cnn_stale_workspace_nan(spec, femnist_like, monkeypatch):
     poisoned = _device_after(spec, w0, X, y, 20, 2, 0, monkeypatch)
     assert np.all(np.isfinite(poisoned[0])) and np.isfinite(poisoned[1])
     assert np.array_equal(clean[0], poisoned[0]) and clean[1] == poisoned[1]
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.5], ids=["fedavg_direct", "fedprox"])
+def test_cnn_direct_fc1_local_run_vs_oracle(spec, femnist_like, mu, monkeypatch):
+    """The direct per-client fc1 kernels with the fused plugin term (FedProx's
+    mu * (w - w0); the low-rank form covers plain SGD only) over a whole local
+    run (3 epochs of a 45-sample client, 9 steps) against the oracle with the
+    device's operand rounding: the update w - w0 agrees within the compounded
+    bf16 / tf32 step noise (the proximal term itself is pinned per step by
+    test_cnn_fedprox_step_replay)."""
+    import paper_2303_01778_b200 as pb
+    from oracle import cnn_oracle
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    from paper_2303_01778_b200.models import cnn_init
+    from paper_2303_01778_b200.trainer import NamedParams
+    monkeypatch.setenv("PB_CNN_LAZY", "0")
+    X, y = femnist_like.features[300:345], femnist_like.labels[300:345]
+    w0 = cnn_init(spec, seed=5)
+
+    def device(m):
+        plugin = pb.FedProx(mu=m, lr=0.05, batch_size=16, collect_local_loss=True) if m else \
+            pb.FedAvg(lr=0.05, batch_size=16, collect_local_loss=True)
+        glob = plugin.init_global(NamedParams.from_flat(spec, w0))
+        rep = pb.client_execute(plugin, ClientProfile(7, 45, DataSlice(X, y, np.arange(45))), glob,
+                                None, 3, 16, 0.05, seed=2, round_num=1)
+        return (np.concatenate([rep.client_result.numpy(nm).reshape(-1) for nm in spec.names])
+                .astype(np.float64), float(rep.client_result.numpy("local_loss")[0]))
+
+    got, dev_loss = device(mu)
+    ref, steps, loss = cnn_oracle.client_train(w0.astype(np.float64), X, y, 7, 2, 1, 3, 16, 0.05, 62,
+                                               emulate_bf16=True, mu=mu)
+    d, r = got - w0, ref - w0
+    assert steps == 9
+    err = np.linalg.norm(d - r) / np.linalg.norm(r)
+    cos = float(d @ r / (np.linalg.norm(d) * np.linalg.norm(r)))
+    print(f"mu={mu}: update error {err:.3e}, cos {cos:.5f}, loss {dev_loss:.6f} vs {loss:.6f}")
+    # 9 steps compound the per-step ReLU / max-pool flips (see
+    # test_cnn_kernel_arithmetic_per_step): measured 6.6e-2 / 0.9978 at mu=0
+    assert err <= 0.15 and cos >= 0.99, (err, cos)
+    assert abs(dev_loss - loss) / loss <= 2e-3, (dev_loss, loss)
+
+
+def test_cnn_fedprox_step_replay(spec, femnist_like, monkeypatch):
+    """FedProx's fused proximal term on the direct fc1 path, one step at a
+    time: the device's second step (from its own weights after the first) is
+    replayed in the emulating oracle with and without mu * (w - w0).  The
+    term moves this step by ~mu * lr = 2.5%; the device must match the
+    oracle with the term (<= 1e-2) and be several times closer to it than to
+    the oracle without it."""
+    import torch
+    import torch.nn.functional as F
+    import paper_2303_01778_b200 as pb
+    from oracle import cnn_oracle, fedsim_oracle
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    from paper_2303_01778_b200.models import cnn_init
+    from paper_2303_01778_b200.trainer import NamedParams
+    monkeypatch.setenv("PB_CNN_LAZY", "0")
+    mu, lr, bs = 0.5, 0.05, 16
+    X, y = femnist_like.features[300:345], femnist_like.labels[300:345]
+    w0 = cnn_init(spec, seed=5)
+
+    def after(sweeps):
+        monkeypatch.setenv("PB_CNN_MAX_SWEEPS", str(sweeps))
+        plugin = pb.FedProx(mu=mu, lr=lr, batch_size=bs)
+        glob = plugin.init_global(NamedParams.from_flat(spec, w0))
+        rep = pb.client_execute(plugin, ClientProfile(7, 45, DataSlice(X, y, np.arange(45))), glob,
+                                None, 1, bs, lr, seed=2, round_num=1)
+        return np.concatenate([rep.client_result.numpy(nm).reshape(-1) for nm in spec.names]).astype(np.float64)
+
+    w1, w2 = after(1), after(2)
+    order = fedsim_oracle.minibatch_orders(2, 7, 1, 45, 1)[0]
+    idx = torch.as_tensor(order[bs:2 * bs])
+    params = [p.requires_grad_(True) for p in cnn_oracle.unflatten(w1, 62)]
+    loss = F.cross_entropy(cnn_oracle.forward(params, torch.as_tensor(X)[idx], True),
+                           torch.as_tensor(y, dtype=torch.long)[idx])
+    g = np.concatenate([t.detach().reshape(-1).numpy() for t in torch.autograd.grad(loss, params)])
+    step_dev = w2 - w1
+    with_prox = -lr * (g + mu * (w1 - w0.astype(np.float64)))
+    plain = -lr * g
+    e_prox = np.linalg.norm(step_dev - with_prox) / np.linalg.norm(with_prox)
+    e_plain = np.linalg.norm(step_dev - plain) / np.linalg.norm(plain)
+    assert e_prox <= 1e-2 and e_prox * 4 <= e_plain, (e_prox, e_plain)
