@@ -27,6 +27,8 @@ codec of the reference are not rebuilt (NCCL replaces them).
 from __future__ import annotations
 
 import math
+import os
+import sys
 import threading
 import time
 from dataclasses import dataclass
@@ -58,6 +60,23 @@ RESULTS_HEADER = ("round\tscheme\tscheduling\tsim_seconds\twall_seconds\t"
 class DeviceFailureError(RuntimeError):
     """A device's client execution raised; the round aborts with the cause."""
 
+
+_TRACE = os.environ.get("PB_TRACE_ROUND") == "1"   # per-round host timeline on stderr (diagnostics)
+
+
+_PREWARMED = False
+
+
+def _prewarm_small_pool(blocks: int = 96) -> None:
+    """Reserve small-block segments of torch's caching allocator once: the
+    per-round input uploads (< 1 MB each) then never hit a fresh cudaMalloc,
+    which was measured to stall a round's launch by up to ~100 ms."""
+    global _PREWARMED
+    if _PREWARMED or not torch.cuda.is_available():
+        return
+    _PREWARMED = True
+    keep = [torch.empty(1 << 20, dtype=torch.uint8, device=device()) for _ in range(blocks)]
+    del keep
 
 @dataclass(frozen=True)
 class DeviceModel:
@@ -205,6 +224,7 @@ class DeviceRuntime:
                 round_num: int, inputs: GroupInputs | None = None) -> dict[int, DevicePartial]:
         """Train every assigned client of the local devices in one batched
         launch, then fold each device's clients in its plan order."""
+        t_in = time.perf_counter()
         order = [(dev, m) for dev in sorted(assignments) for m in assignments[dev]]
         partials = {dev: DevicePartial(device_id=dev) for dev in assignments}
         self.last_device_seconds = 0.0
@@ -234,9 +254,11 @@ class DeviceRuntime:
                              round_num, inputs=inputs, defer_fc1=defer, defer_check=late)
         finally:
             self.gauge.release(len(clients))
+        t_tr = time.perf_counter()
         self.pending = go if go.pending is not None else None
         self.last_device_seconds = go.seconds
         groups, new_state = finalize_results(plugin, spec, go, w0, bundle, work)
+        t_fin = time.perf_counter()
         if go.lazy is not None:
             for g in groups:
                 if g.op is AggOp.WEIGHTED_AVERAGE:
@@ -248,6 +270,10 @@ class DeviceRuntime:
             k = len(assignments[dev])
             fold_group(partials[dev], groups, list(range(pos, pos + k)), assignments[dev])
             pos += k
+        if _TRACE:
+            t_end = time.perf_counter()
+            print(f"  execute: train_group {1e3 * (t_tr - t_in):.1f} finalize {1e3 * (t_fin - t_tr):.1f} "
+                  f"fold {1e3 * (t_end - t_fin):.1f} ms", file=sys.stderr, flush=True)
         return partials
 
 
@@ -350,6 +376,7 @@ class SimulationEngine:
         self.eval_every = max(1, eval_every)
         self.history = history if history is not None else TimingHistory()
         self._prefetch = None       # (round, thread, result box) of a round prepared ahead
+        self._after_enqueue = None  # run_round's hook: start that preparation
         self.gauge = ReplicaGauge()
         self.next_round = start_round
         self.sizes = np.array([p.sample_count for p in self.profiles], dtype=np.int64)
@@ -377,6 +404,7 @@ class SimulationEngine:
         from .distributed import local_devices
         self.local_devices = local_devices(cfg.num_devices, self._world, self._rank)
         self.runtime = DeviceRuntime(cfg, plugin, self.spec, self.data, store, self.gauge)
+        _prewarm_small_pool()
         if cfg.scheme == "PARROT" and cfg.scheduling in ("full-history", "time-window"):
             warm_jit()
 
@@ -526,12 +554,15 @@ class SimulationEngine:
         """Device half of a round: batched training, hierarchical fold,
         (multi-GPU) partial all-reduce, server rule, evaluation."""
         cfg, round_num = self.cfg, inp.round
+        trace = _TRACE and [(time.perf_counter(), "start")]
         ledger = CostLedger(round=round_num, scheme=cfg.scheme)
         schema = result_schema(self.plugin, self.spec)
         try:
             got = self.runtime.execute(inp.assign, self.global_bundle, round_num, inp.group)
         except Exception as exc:
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
+        if trace:
+            trace.append((time.perf_counter(), "train+fold enqueued"))
         partials = [got[k] for k in sorted(inp.assign)]
         if cfg.clock == "real":
             g = max(len(inp.selection.selected), 1)
@@ -569,12 +600,26 @@ class SimulationEngine:
         ledger.peak_live_model_replicas = self.gauge.peak
         if self.store is not None:
             ledger.state_bytes_disk = self.store.stats().bytes_on_disk
+        # all of the round's device work is queued: the next round's host
+        # preparation may start now (it then overlaps the wait below instead
+        # of competing with this thread for the interpreter while enqueueing)
+        cb, self._after_enqueue = self._after_enqueue, None
+        if cb is not None:
+            cb()
+        if trace:
+            trace.append((time.perf_counter(), "all enqueued"))
         try:
             self.runtime.resolve()   # the round's result read (queued after training)
         except Exception as exc:
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
+        if trace:
+            trace.append((time.perf_counter(), "result read"))
         if sync:
             torch.cuda.synchronize()
+        if trace:
+            trace.append((time.perf_counter(), "synced"))
+            print("round", round_num, " ".join(f"{n}@{1e3 * (t - trace[0][0]):.1f}" for t, n in trace[1:]),
+                  file=sys.stderr, flush=True)
         outcome = RoundOutcome(round=round_num, scheme=cfg.scheme, scheduling_mode=inp.plan.mode,
                                simulated_round_seconds=sim_seconds,
                                wall_seconds=time.perf_counter() - inp.wall0, device_loads=loads,
@@ -589,10 +634,11 @@ class SimulationEngine:
     def run_round(self, round_num: int) -> RoundOutcome:
         """One round through the public API.  Under the virtual clock the
         next round's host half (selection, fits, schedule, minibatch orders)
-        runs on a helper thread while this round's kernels execute."""
+        runs on a helper thread while this round's kernels execute (started
+        once the round's device work is queued)."""
         inp = self.prepare_round(round_num)
         if self.cfg.clock == "virtual" and round_num + 1 < self.cfg.total_rounds:
-            self._start_prefetch(round_num + 1)
+            self._after_enqueue = lambda: self._start_prefetch(round_num + 1)
         return self.execute_round(inp)
 
     @staticmethod
