@@ -50,10 +50,10 @@ class _LazyWorkspace:
     def _get(self, name: str, numel: int, device) -> torch.Tensor:
         t = self.buf.get(name)
         if t is None or t.numel() < numel or t.device != device:
-            # 50% headroom: round sizes vary (the longest client sets the
+            # 2x headroom: round sizes vary (the longest client sets the
             # history length), and a reallocation synchronises
             self.buf.pop(name, None)
-            t = torch.empty(max(int(numel * 1.5), 4), dtype=torch.float32, device=device)
+            t = torch.empty(max(int(numel * 2.0), 4), dtype=torch.float32, device=device)
             self.buf[name] = t
         return t
 
@@ -88,27 +88,6 @@ def lazy_plan(total: np.ndarray, active: np.ndarray, BS: int):
     njt = (np.arange(len(active)) * BS + 127) // 128
     cap = int((active.astype(np.int64) * njt).max()) if len(active) else 0
     return hlen, hoff, int(hlen.sum()), cap * 512 * 32, cap * 32 * 128
-
-
-_BOUNDS: dict = {}
-
-
-def _lazy_bound(data, G: int, batch_size: int, epochs: int, BS: int) -> tuple[int, int, int]:
-    """Workspace bounds (rows, zp, gdt) of the worst group of G clients of
-    `data` (the G largest clients): lazy_plan of that group."""
-    key = (id(data), G, batch_size, epochs, BS)
-    hit = _BOUNDS.get(key)
-    if hit is None:
-        sizes = np.sort(np.asarray(data.sizes, dtype=np.int64))[::-1][:G]
-        sizes = sizes[sizes > 0]
-        if len(sizes) == 0:
-            hit = (0, 0, 0)
-        else:
-            _, total, _, active = sweep_plan(sizes, batch_size, epochs)
-            _, _, rows, zp, gdt = lazy_plan(total, active, BS)
-            hit = (rows, zp, gdt)
-        _BOUNDS[key] = hit
-    return hit
 
 
 class LazyFc1:
@@ -217,11 +196,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     handle = None
     if lazy:
         hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
-        # size the history workspace once for the largest group these clients
-        # can form (its G biggest clients): a mid-run regrowth costs a large
-        # cudaMalloc inside a round
-        rb, zb, gb = _lazy_bound(data, G, batch_size, epochs, BS)
-        lz = _LZ.get(max(rows, rb), max(zp, zb), max(gdt, gb), G, d)
+        lz = _LZ.get(rows, zp, gdt, G, d)
         hlen_d = h2d(hlen, d)
         hoff_d = h2d(hoff, d)
         a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),
