@@ -75,7 +75,11 @@ def _prewarm_small_pool(blocks: int = 96) -> None:
     if _PREWARMED or not torch.cuda.is_available():
         return
     _PREWARMED = True
-    keep = [torch.empty(1 << 20, dtype=torch.uint8, device=device()) for _ in range(blocks)]
+    d = device()
+    # small pool (<= 1 MB requests, 2 MB segments) and the 1-10 MB class of
+    # the large pool (20 MB segments): per-round inputs / partials live there
+    keep = [torch.empty(1 << 20, dtype=torch.uint8, device=d) for _ in range(blocks)]
+    keep += [torch.empty(4 << 20, dtype=torch.uint8, device=d) for _ in range(blocks // 2)]
     del keep
 
 @dataclass(frozen=True)
