@@ -345,6 +345,8 @@ constexpr int kHeadDenseThreads = 512;   // k_head: one fc1 output column per th
 constexpr int kDHS = kH1 + 1;            // k_head dH row stride (conflict-free column reads)
 __host__ __device__ constexpr int pad4(int c) { return (c + 3) & ~3; }   // logit rows padded for 16 B loads
 
+__device__ __forceinline__ float nan_max(float x, float y) { return x != x ? x : (y != y ? y : fmaxf(x, y)); }
+
 __device__ double block_sum_d(double v, double* scratch) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
@@ -406,28 +408,25 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     }
   }
   __syncthreads();
-  double lpart = 0.0, cpart = 0.0;
   const float inv = 1.0f / float(cnt);
-  if (tid < cnt) {
-    float* z = sL + tid * Cp;
-    const int y = a.Y[a.order[sl.row_off + tid]];
-    float m = z[0];
-    int best = 0;
-    for (int c = 1; c < C; ++c)
-      if (takes_max(z[c], m) && m == m) {
-        m = z[c];
-        best = c;
-      }
-    float se = 0.0f;
-    for (int c = 0; c < C; ++c) se += expf(z[c] - m);
-    const float lse = logf(se);
-    lpart = double(lse) - double(z[y] - m);
-    cpart = best == y ? 1.0 : 0.0;
-    if (!a.eval)
-      for (int c = 0; c < C; ++c) z[c] = (expf(z[c] - m - lse) - (c == y ? 1.0f : 0.0f)) * inv;
-  }
-  const double lsum = block_sum_d(lpart, scratch);
-  if (a.eval) {
+  if (a.eval) {   // accuracy needs the argmax: one thread per sample
+    double lpart = 0.0, cpart = 0.0;
+    if (tid < cnt) {
+      float* z = sL + tid * Cp;
+      const int y = a.Y[a.order[sl.row_off + tid]];
+      float m = z[0];
+      int best = 0;
+      for (int c = 1; c < C; ++c)
+        if (takes_max(z[c], m) && m == m) {
+          m = z[c];
+          best = c;
+        }
+      float se = 0.0f;
+      for (int c = 0; c < C; ++c) se += expf(z[c] - m);
+      lpart = double(logf(se)) - double(z[y] - m);
+      cpart = best == y ? 1.0 : 0.0;
+    }
+    const double lsum = block_sum_d(lpart, scratch);
     const double csum = block_sum_d(cpart, scratch);
     if (tid == 0 && part == 0) {
       atomicAdd(a.eval, csum);
@@ -435,7 +434,26 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     }
     return;
   }
+  // training: softmax-CE and dlogits, one warp per sample, lanes over classes
+  __shared__ double sLoss[32];
+  for (int i = warp; i < cnt; i += kHeadDenseThreads / 32) {
+    float* z = sL + i * Cp;
+    const int y = a.Y[a.order[sl.row_off + i]];
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = nan_max(m, z[c]);
+    for (int off = 16; off > 0; off >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float se = 0.0f;
+    for (int c = lane; c < C; c += 32) se += expf(z[c] - m);
+    for (int off = 16; off > 0; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
+    const float lse = logf(se);
+    if (lane == 0) sLoss[i] = double(lse) - double(z[y] - m);
+    __syncwarp();
+    for (int c = lane; c < C; c += 32) z[c] = (expf(z[c] - m - lse) - (c == y ? 1.0f : 0.0f)) * inv;
+  }
+  __syncthreads();
   if (tid == 0) {
+    double lsum = 0.0;
+    for (int i = 0; i < cnt; ++i) lsum += sLoss[i];
     const double loss = lsum / double(cnt);
     s_bad = !isfinite(loss);
     if (part != 0) {
@@ -540,7 +558,6 @@ static size_t head_tail_smem(int C, int BS) {
          size_t(BS) * 8;
 }
 
-__device__ __forceinline__ float nan_max(float x, float y) { return x != x ? x : (y != y ? y : fmaxf(x, y)); }
 
 __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThreads) k_head_tail(Args a) {
   pb::pdl_wait();
