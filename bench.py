@@ -131,8 +131,14 @@ class ClockSampler:
         # sub-second timed region); nvidia-smi as the fallback
         try:
             import pynvml
+            import torch
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            try:   # the CUDA device's own GPU (NVML indices ignore CUDA_VISIBLE_DEVICES)
+                pr = torch.cuda.get_device_properties(self.index)
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             bits = (0x8, 0x40, 0x20, 0x4)   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
             while not self._stop.is_set():
