@@ -34,6 +34,11 @@ extern "C" {
 const char* pb_last_error(void);
 int pb_version(void);
 int pb_device_sm_count(int device);
+/* sizeof of the argument structs, so bindings can check their layout:
+ * out[0] pb_lr_train_args, out[1] pb_cnn_train_args, out[2]
+ * pb_cnn_lazy_fold_args, out[3] pb_resnet_train_args; returns how many it
+ * wrote (min(n, 4)). */
+int pb_abi_sizes(int64_t* out, int n);
 
 /* Launch accounting and optional per-kernel-class timing (CUDA events on the
  * launching stream).  pb_launch_count: kernels launched by this library so far.
@@ -137,6 +142,8 @@ typedef struct {
   int64_t g;
   int32_t F, C, epochs, batch_size;
   float lr, mu, prox_loss, cg, cc;
+  int64_t* client_ns;      /* [g, 2] %globaltimer at the client's first and  */
+                           /* last instruction (real-clock records) or NULL  */
 } pb_lr_train_args;
 int pb_lr_train_group(const pb_lr_train_args* args, void* stream);
 
@@ -210,6 +217,10 @@ typedef struct {
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;
+  int64_t* timeline;        /* [sweeps + 1] %globaltimer at the start of each */
+                            /* sweep and after the last one, or NULL: sweep s */
+                            /* lasts timeline[s+1] - timeline[s] ns and is    */
+                            /* shared by its active clients (real clock)      */
 } pb_cnn_train_args;
 int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
 
@@ -277,6 +288,7 @@ typedef struct {
   int64_t g;
   int32_t C, BS, batch_size, epochs;
   float lr;
+  int64_t* timeline;        /* [sweeps + 1] sweep start stamps, as for the CNN */
 } pb_resnet_train_args;
 int pb_resnet_workspace(int BS, int C, int64_t* out4);
 int pb_resnet_train_group(const pb_resnet_train_args* args, void* stream);

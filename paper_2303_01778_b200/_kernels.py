@@ -102,7 +102,7 @@ def state_scatter(store: torch.Tensor, work: torch.Tensor, slot: torch.Tensor) -
 
 def lr_train(X, Y, order, order_off, n, w0, w_out, loss_sum, steps, nonfinite, *, F, C, epochs,
              batch_size, lr, mu=0.0, prox_loss=0.0, ctrl_g=None, cg=0.0, ctrl_c=None,
-             cc=0.0) -> None:
+             cc=0.0, client_ns=None) -> None:
     a = LrTrainArgs()
     a.X, a.Y, a.order, a.order_off, a.n = ptr(X), ptr(Y), ptr(order), ptr(order_off), ptr(n)
     a.w0, a.w_out = ptr(w0), ptr(w_out)
@@ -112,6 +112,7 @@ def lr_train(X, Y, order, order_off, n, w0, w_out, loss_sum, steps, nonfinite, *
     a.g = w_out.size(0)
     a.F, a.C, a.epochs, a.batch_size = F, C, epochs, batch_size
     a.lr, a.mu, a.prox_loss, a.cg, a.cc = lr, mu, prox_loss, cg, cc
+    a.client_ns = ptr(client_ns)
     lib.check(lib.pb_lr_train_group(ctypes.byref(a), stream_of(w_out)))
 
 

@@ -27,7 +27,7 @@ class LrTrainArgs(ctypes.Structure):
         ("steps", c_void_p), ("nonfinite", c_void_p), ("g", c_int64),
         ("F", c_int32), ("C", c_int32), ("epochs", c_int32), ("batch_size", c_int32),
         ("lr", c_float), ("mu", c_float), ("prox_loss", c_float), ("cg", c_float),
-        ("cc", c_float),
+        ("cc", c_float), ("client_ns", c_void_p),
     ]
 
 
@@ -48,6 +48,7 @@ class CnnTrainArgs(ctypes.Structure):
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),
+        ("timeline", c_void_p),
     ]
 
 
@@ -68,13 +69,14 @@ class ResnetTrainArgs(ctypes.Structure):
         ("bad", c_void_p), ("ws_slots", c_void_p), ("ws_w16", c_void_p), ("ws_arena", c_void_p),
         ("ws_part", c_void_p), ("ws_gnp", c_void_p), ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
-        ("lr", c_float),
+        ("lr", c_float), ("timeline", c_void_p),
     ]
 
 
 _SIGS = {
     "pb_last_error": (ctypes.c_char_p, []),
     "pb_version": (c_int, []),
+    "pb_abi_sizes": (c_int, [POINTER(c_int64), c_int]),
     "pb_device_sm_count": (c_int, [c_int]),
     "pb_prof_enable": (c_int, [c_int]),
     "pb_prof_select": (c_int, [c_uint64]),

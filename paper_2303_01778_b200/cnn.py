@@ -157,7 +157,7 @@ def sweep_plan(n: np.ndarray, batch_size: int, epochs: int):
 
 def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, bad, *,
                     spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
-                    state_work, defer_fc1: bool = False) -> "LazyFc1 | None":
+                    state_work, defer_fc1: bool = False, timeline=None) -> "LazyFc1 | None":
     G = len(n)
     BS, total, rank, active = sweep_plan(n, batch_size, epochs)
     if BS > MAX_BATCH:
@@ -210,6 +210,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)
+    a.timeline = ptr(timeline)
     lib.check(lib.pb_cnn_train_group(ctypes.byref(a), stream_of(w_out)))
     return handle
 

@@ -25,6 +25,17 @@ int sm_count() {
 }
 
 namespace {
+__global__ void k_stamp(int64_t* at) {
+  pdl_wait();
+  *at = globaltimer();
+}
+}  // namespace
+
+void stamp(int64_t* at, cudaStream_t s) {
+  launch_pdl(k_stamp, dim3(1), dim3(32), 0, s, 1, at);
+}
+
+namespace {
 struct Rec {
   int id;
   cudaEvent_t a, b;
@@ -107,6 +118,14 @@ extern "C" int pb_prof_collect(double* ms, int64_t* count, int nslots) {
 extern "C" const char* pb_last_error(void) { return pb::g_last_error.c_str(); }
 
 extern "C" int pb_version(void) { return 1; }
+
+extern "C" int pb_abi_sizes(int64_t* out, int n) {
+  const int64_t sz[4] = {int64_t(sizeof(pb_lr_train_args)), int64_t(sizeof(pb_cnn_train_args)),
+                         int64_t(sizeof(pb_cnn_lazy_fold_args)), int64_t(sizeof(pb_resnet_train_args))};
+  const int k = n < 4 ? n : 4;
+  for (int i = 0; i < k && out; ++i) out[i] = sz[i];
+  return k;
+}
 
 extern "C" int pb_device_sm_count(int device) {
   int n = 0;

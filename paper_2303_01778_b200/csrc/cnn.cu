@@ -40,6 +40,7 @@ using namespace pb::cnn;
 __global__ void k_slots(Args a, int active) {
   pb::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.timeline && j == 0) a.timeline[a.step] = pb::globaltimer();
   if (j >= active) return;
   const int r = a.rank[j];
   const int n = a.n[r];
@@ -1395,6 +1396,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs;
   a.P = t.w_stride;  // row stride of the parameter matrix (>= the model size)
   a.lr = t.lr; a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;
+  a.timeline = t.timeline;
   return a;
 }
 
@@ -1503,6 +1505,8 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
     pb::prof_end(pb::K_CNN_SLOTS, s);
     if ((rc = launch_sweep(a, active, true, spb, s))) break;
+    if (a.timeline && (step + 1 == t.sweeps || t.active[step + 1] <= 0))
+      pb::stamp(a.timeline + step + 1, s);
   }
   if (a.hx) {
     if (!rc && !t.lz_defer) rc = lazy_fc1_materialize(a, int(t.g), s);

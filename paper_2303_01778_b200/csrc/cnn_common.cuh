@@ -84,6 +84,7 @@ struct Args {
   float* zp;              // [slots * njt][kH1][32] forward correction partials
   float* gdt;             // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
   float* fpart;           // [ks][active][kH1][32] tail split-K partials (<= 74*16384 f32)
+  int64_t* timeline;      // [sweeps + 1] sweep start stamps (real clock) or null
   int64_t P;
   int32_t C, BS, bs, epochs, step;
   float lr, mu, cg, cc;

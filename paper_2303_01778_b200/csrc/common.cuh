@@ -70,6 +70,18 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// ---- device timeline (real-clock timing records) ---------------------------
+// The GPU's global nanosecond timer; per-client task times under the real
+// clock come from stamps taken on the device, not from host-side events.
+__device__ __forceinline__ int64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return int64_t(t);
+}
+// Stamp *at (one thread) once the preceding work in the stream has completed
+// (launched with programmatic dependent launch, it waits on its predecessor).
+void stamp(int64_t* at, cudaStream_t s);
+
 // ---- launch accounting / optional per-kernel-class timing -----------------
 enum KernelId {
   K_FOLD1 = 0, K_FOLD_GROUP, K_LINCOMB, K_DELTA_AFFINE, K_STATE_GATHER, K_STATE_SCATTER,

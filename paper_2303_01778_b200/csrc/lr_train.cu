@@ -61,6 +61,7 @@ lr_train_kernel(pb_lr_train_args a, int rows_per_chunk) {
 
   const int64_t gi = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.client_ns && tid == 0) a.client_ns[2 * gi] = pb::globaltimer();
   const int n = a.n[gi];
   const int bs = a.batch_size <= 0 ? n : min(a.batch_size, n);
   const int32_t* order = a.order + a.order_off[gi];
@@ -158,6 +159,10 @@ lr_train_kernel(pb_lr_train_args a, int rows_per_chunk) {
     a.loss_sum[gi] = loss_sum;
     a.steps[gi] = steps;
     a.nonfinite[gi] = bad;
+  }
+  if (a.client_ns) {
+    __syncthreads();
+    if (tid == 0) a.client_ns[2 * gi + 1] = pb::globaltimer();
   }
 }
 

@@ -74,6 +74,7 @@ struct Net {
   int32_t* bad;
   Slot* slots;
   double* eval;
+  int64_t* timeline;  // [sweeps + 1] sweep start stamps (real clock) or null
   int32_t C, BS, bs, epochs, step;
   float lr;
 };
@@ -91,6 +92,7 @@ __device__ __forceinline__ T* at(const Net& a, int s, int64_t off) {
 __global__ void k_rn_slots(Net a, int active) {
   pb::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.timeline && j == 0) a.timeline[a.step] = pb::globaltimer();
   if (j >= active) return;
   const int r = a.rank[j];
   const int n = a.n[r];
@@ -1335,6 +1337,7 @@ Net to_net(const pb_resnet_train_args& t, const Plan& pl) {
   a.eval = nullptr;
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs; a.step = 0;
   a.lr = t.lr;
+  a.timeline = t.timeline;
   return a;
 }
 
@@ -1735,6 +1738,8 @@ extern "C" int pb_resnet_train_group(const pb_resnet_train_args* args, void* str
     pb::prof_end(pb::K_RN_NORM, s);
     if ((rc = forward(a, pl, active, s))) return rc;
     if ((rc = backward(a, pl, active, s))) return rc;
+    if (a.timeline && (step + 1 == t.sweeps || t.active[step + 1] <= 0))
+      pb::stamp(a.timeline + step + 1, s);
   }
   return PB_OK;
 }

@@ -38,8 +38,8 @@ from typing import Sequence
 import numpy as np
 import torch
 
-from .aggregate import (DevicePartial, PartialEntry, fold_group, global_fold, partial_byte_roles,
-                        server_update)
+from .aggregate import (DevicePartial, PartialEntry, fold_group, global_fold, local_fold,
+                        partial_byte_roles, server_update)
 from .core import (STREAM_NOISE, ClientProfile, ConfigError, SimConfig, select_clients,
                    stream_rng)
 from .estimate import (InsufficientDataError, TimingHistory, TimingRecord, WorkloadFit,
@@ -49,8 +49,8 @@ from .models import ModelSpec, init_params, spec_for
 from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
 from .statestore import StateStore
 from .trainer import (AggOp, AlgorithmPlugin, ClientData, FedAvg, GroupInputs, ModelParams, NamedParams,
-                      ParamBundle, device, evaluate, finalize_results, io_bytes, spec_of_bundle,
-                      train_group)
+                      ParamBundle, device, evaluate, finalize_results, hook_client_execute, io_bytes,
+                      spec_of_bundle, train_group, uses_hooks)
 
 RESULTS_HEADER = ("round\tscheme\tscheduling\tsim_seconds\twall_seconds\t"
                   "device_loads\ttrips_up\ttrips_down\tbytes_avg\tbytes_special\t"
@@ -206,7 +206,10 @@ class DeviceRuntime:
         self.cfg, self.plugin, self.spec, self.data = cfg, plugin, spec, data
         self.store, self.gauge = store, gauge
         self.last_device_seconds = 0.0
+        self.client_seconds: dict[int, float] = {}   # device-measured task time per client (real clock)
+        self.batch_peak = 0   # most clients trained in one batched launch
         self.pending: GroupOutcome | None = None   # group whose result read is outstanding
+        self.hooks = uses_hooks(plugin)
 
     def resolve(self) -> None:
         """Complete the outstanding result read of the last group (raises on a
@@ -220,7 +223,7 @@ class DeviceRuntime:
         """Host side of a round for the local devices: minibatch row ids of all
         their clients (device order, then plan order)."""
         clients = [m for dev in sorted(assignments) for m in assignments[dev]]
-        if not clients:
+        if not clients or self.hooks:
             return None
         return GroupInputs(self.data, clients, self.cfg.local_epochs, self.cfg.seed, round_num)
 
@@ -238,29 +241,43 @@ class DeviceRuntime:
         if len(set(clients)) != len(clients):
             raise ValueError(f"round {round_num}: a client is assigned twice")
         plugin, spec = self.plugin, self.spec
+        if plugin.is_stateful and self.store is None:
+            raise ConfigError(f"{plugin.name} is stateful and needs a state store")
+        if self.hooks:
+            return self._execute_hooks(assignments, bundle, round_num)
         w0 = bundle.flat(spec)
         work = None
         if plugin.is_stateful:
-            if self.store is None:
-                raise ConfigError(f"{plugin.name} is stateful and needs a state store")
+            if not self.store.configured:   # a fresh store behind a bare DeviceWorker
+                self.store.configure(plugin.state_names(spec), [sh for *_, sh in spec.columns()])
             work = torch.empty(len(clients), (spec.numel + 3) // 4 * 4, device=w0.device)[:, :spec.numel]
             self.store.gather(clients, work)
-        self.gauge.acquire(len(clients))
+        # one live model replica per busy simulated device (the reference's
+        # Table-1 quantity); the batch itself is the GPU's real concurrency
+        busy = sum(1 for dev in assignments if assignments[dev])
+        self.batch_peak = max(self.batch_peak, len(clients))
+        self.gauge.acquire(busy)
         try:
             # FedAvg folds exactly the end models: the CNN's low-rank fc1 can be
             # folded from the round's history without materialising them
             defer = spec.kind == "cnn" and type(plugin) is FedAvg
             # the group's result read (failures, losses, device time) can wait
-            # for the end of the round unless something needs it now
-            late = self.cfg.clock == "virtual" and not plugin.collect_local_loss
+            # for the end of the round unless something needs it now; a
+            # stateful round reads it before its states are committed, so a
+            # diverged client leaves the store untouched
+            late = (self.cfg.clock == "virtual" and not plugin.collect_local_loss
+                    and not plugin.is_stateful)
             go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
                              self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
-                             round_num, inputs=inputs, defer_fc1=defer, defer_check=late)
+                             round_num, inputs=inputs, defer_fc1=defer, defer_check=late,
+                             timing=self.cfg.clock == "real")
         finally:
-            self.gauge.release(len(clients))
+            self.gauge.release(busy)
         t_tr = time.perf_counter()
         self.pending = go if go.pending is not None else None
         self.last_device_seconds = go.seconds
+        self.client_seconds = ({} if go.client_seconds is None else
+                               dict(zip(clients, go.client_seconds.tolist())))
         groups, new_state = finalize_results(plugin, spec, go, w0, bundle, work)
         t_fin = time.perf_counter()
         if go.lazy is not None:
@@ -278,6 +295,37 @@ class DeviceRuntime:
             t_end = time.perf_counter()
             print(f"  execute: train_group {1e3 * (t_tr - t_in):.1f} finalize {1e3 * (t_fin - t_tr):.1f} "
                   f"fold {1e3 * (t_end - t_fin):.1f} ms", file=sys.stderr, flush=True)
+        return partials
+
+    def _execute_hooks(self, assignments: dict[int, list[int]], bundle: ParamBundle,
+                       round_num: int) -> dict[int, DevicePartial]:
+        """A reference-style plugin (``uses_hooks``): Algorithm 2's
+        Device_Executes loop of fedsim/engine.py:470-503 -- load state, train
+        through the plugin's hooks, save, fold -- one client at a time."""
+        plugin, data, store = self.plugin, self.data, self.store
+        partials = {dev: DevicePartial(device_id=dev) for dev in assignments}
+        self.client_seconds = {}
+        total = 0.0
+        for dev in sorted(assignments):
+            for m in assignments[dev]:
+                state = None
+                if plugin.is_stateful:
+                    base = bundle.model()
+                    state = store.load(m, default_factory=lambda: plugin.default_state(base))
+                lo, n = int(data.row_base[m]), int(data.sizes[m])
+                self.gauge.acquire()
+                try:
+                    rep = hook_client_execute(plugin, m, data.X[lo:lo + n], data.Y[lo:lo + n], bundle,
+                                              state, self.cfg.local_epochs, plugin.batch_size,
+                                              plugin.lr, self.cfg.seed, round_num)
+                finally:
+                    self.gauge.release()
+                if plugin.is_stateful and rep.new_state is not None and rep.new_state.payload:
+                    store.save(m, round_num, rep.new_state.payload)
+                local_fold(partials[dev], rep.client_result, m)
+                self.client_seconds[m] = rep.measured_seconds
+                total += rep.measured_seconds
+        self.last_device_seconds = total
         return partials
 
 
@@ -302,6 +350,9 @@ class DeviceWorker:
 
     def execute_clients(self, bundle: ParamBundle, clients: Sequence[int],
                         round_num: int) -> tuple[DevicePartial, list[TimingRecord]]:
+        """fedsim/engine.py:470-503: the device's clients in plan order ->
+        (partial, timing records).  Works on a fresh StateStore: the store's
+        layout is declared from the plugin's state schema on first use."""
         rt = self._rt(bundle)
         partial = rt.execute({self.device.device_id: list(clients)}, bundle, round_num)[
             self.device.device_id]
@@ -316,8 +367,8 @@ class DeviceWorker:
         if self.cfg.clock == "virtual":
             measured = virtual_task_seconds(self.device, int(rt.data.sizes[m]), self.cfg.seed,
                                             round_num, m)
-        else:
-            measured = max(rt.last_device_seconds / max(g, 1), 1e-9)
+        else:   # device-measured per-client task time (kernel %globaltimer stamps)
+            measured = rt.client_seconds[m]
         return report_time(measured, self.device, round_num, self.cfg.total_rounds)
 
 
@@ -344,6 +395,15 @@ def result_schema(plugin: AlgorithmPlugin, spec: ModelSpec) -> list[tuple[str, A
     if plugin.collect_local_loss:
         out.append(("local_loss", AggOp.COLLECT, (1,)))
     return out
+
+
+def _schema_of(partials) -> list[tuple[str, AggOp, tuple]]:
+    """(name, op, shape) of the entries a hook plugin's results carried."""
+    for p in partials:
+        if p.entries:
+            return [(n, pe.op, tuple(pe.acc.shape) if pe.acc is not None else
+                     tuple(pe.collected[0][1].shape)) for n, pe in p.entries.items()]
+    return []
 
 
 class SimulationEngine:
@@ -396,7 +456,7 @@ class SimulationEngine:
             else:
                 start = NamedParams.from_flat(self.spec, init_params(self.spec, init_seed))
             self.global_bundle = plugin.init_global(start)
-        if plugin.is_stateful:
+        if plugin.is_stateful and not uses_hooks(plugin) and not store.configured:
             names = plugin.state_names(self.spec)
             store.configure(names, [sh for _, _, _, sh in self.spec.columns()])
         self._world, self._rank = 1, 0
@@ -405,6 +465,12 @@ class SimulationEngine:
             self._rank = torch.distributed.get_rank()
             if cfg.clock == "real":
                 raise ConfigError("multi-process runs need the virtual clock (shared histories)")
+            if plugin.is_stateful and self._world > 1:
+                # each rank's store is HBM-local while the plan moves clients
+                # between ranks every round: a client's state would be read
+                # on a rank that never wrote it
+                raise ConfigError(f"{plugin.name} keeps per-client state; stateful plugins run "
+                                  "single-process (one GPU) until client state is sharded by owner rank")
         from .distributed import local_devices
         self.local_devices = local_devices(cfg.num_devices, self._world, self._rank)
         self.runtime = DeviceRuntime(cfg, plugin, self.spec, self.data, store, self.gauge)
@@ -538,44 +604,63 @@ class SimulationEngine:
             inp.records = self._records(inp, None)
         return inp
 
-    def _records(self, inp: "RoundInputs", measured_per_client: float | None) -> list:
+    def _records(self, inp: "RoundInputs", measured: dict | None) -> list:
         """Timing records in the reference's order: device order, plan order
-        (fedsim/engine.py:689-697), or completion order for FA_DIST."""
+        (fedsim/engine.py:689-697), or completion order for FA_DIST.
+        ``measured`` (real clock): client -> device-measured task seconds."""
         r = inp.round
         if inp.fa_tasks is not None:
             tasks = list(inp.fa_tasks)
         else:
             tasks = [(dev, m) for dev in range(self.cfg.num_devices)
                      for m in inp.plan.assignments.get(dev, [])]
-        return [TimingRecord(dev, m, r, inp.sizes[m], self._reported(dev, m, r, measured_per_client))
+        return [TimingRecord(dev, m, r, inp.sizes[m],
+                             self._reported(dev, m, r, None if measured is None else measured[m]))
                 for dev, m in tasks]
 
-    def _record(self, inp: "RoundInputs", measured_per_client: float | None) -> None:
-        for rec in self._records(inp, measured_per_client):
+    def _record(self, inp: "RoundInputs", measured: dict | None) -> None:
+        for rec in self._records(inp, measured):
             record(self.history, rec)
+
+    def _measured_seconds(self, inp: "RoundInputs") -> dict:
+        """Real clock: each client's task time as measured on the device
+        (DeviceRuntime.client_seconds; FA_DIST runs virtual-only)."""
+        got = self.runtime.client_seconds
+        missing = [m for m in inp.selection.selected if m not in got]
+        if missing:
+            raise DeviceFailureError(f"no device timing for clients {missing[:5]}")
+        return got
 
     def execute_round(self, inp: "RoundInputs", sync: bool = True) -> RoundOutcome:
         """Device half of a round: batched training, hierarchical fold,
-        (multi-GPU) partial all-reduce, server rule, evaluation."""
+        (multi-GPU) partial all-reduce, server rule, evaluation.
+
+        A device failure (e.g. a diverged client) raises DeviceFailureError
+        and leaves the engine as it was before the round, as the reference
+        does (it raises before any aggregation, fedsim/engine.py:684-687): the
+        global model is only replaced once the round's result read succeeded,
+        client states are committed only after it (stateful rounds read their
+        results before the scatter), and the round's timing records and any
+        prefetched next round are dropped."""
         cfg, round_num = self.cfg, inp.round
         trace = _TRACE and [(time.perf_counter(), "start")]
         ledger = CostLedger(round=round_num, scheme=cfg.scheme)
-        schema = result_schema(self.plugin, self.spec)
         try:
             got = self.runtime.execute(inp.assign, self.global_bundle, round_num, inp.group)
         except Exception as exc:
+            self._abort_round(round_num)
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
         if trace:
             trace.append((time.perf_counter(), "train+fold enqueued"))
         partials = [got[k] for k in sorted(inp.assign)]
+        schema = (result_schema(self.plugin, self.spec) if not self.runtime.hooks
+                  else _schema_of(partials))
         if cfg.clock == "real":
-            g = max(len(inp.selection.selected), 1)
-            self._record(inp, max(self.runtime.last_device_seconds / g, 1e-9))
+            self._record(inp, self._measured_seconds(inp))
         if self._world > 1:
             partials = self._reduce_partials(partials, schema)
         agg = global_fold(partials)
         new_global = server_update(self.plugin, self.global_bundle, agg)
-        self.global_bundle = new_global
 
         # communication ledger at the reference's 8 B/element convention
         if cfg.scheme != "SP":
@@ -600,8 +685,9 @@ class SimulationEngine:
         accuracy = loss = float("nan")
         if self.eval_data is not None and (round_num % self.eval_every == 0
                                            or round_num == cfg.total_rounds - 1):
-            accuracy, loss = evaluate(self.global_model(), self.eval_data)
+            accuracy, loss = evaluate(self.global_model(new_global), self.eval_data)
         ledger.peak_live_model_replicas = self.gauge.peak
+        ledger.peak_device_batch = self.runtime.batch_peak
         if self.store is not None:
             ledger.state_bytes_disk = self.store.stats().bytes_on_disk
         # all of the round's device work is queued: the next round's host
@@ -615,7 +701,9 @@ class SimulationEngine:
         try:
             self.runtime.resolve()   # the round's result read (queued after training)
         except Exception as exc:
+            self._abort_round(round_num)
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
+        self.global_bundle = new_global
         if trace:
             trace.append((time.perf_counter(), "result read"))
         if sync:
@@ -635,6 +723,16 @@ class SimulationEngine:
             append_results(self.results_path, outcome)
         return outcome
 
+    def _abort_round(self, round_num: int) -> None:
+        """Undo a failed round's host-side traces: its timing records and a
+        next round prepared ahead from them."""
+        self._after_enqueue = None
+        pf, self._prefetch = self._prefetch, None
+        if pf is not None:
+            pf[1].join()
+        self.history.discard_round(round_num)
+        self.runtime.pending = None
+
     def run_round(self, round_num: int) -> RoundOutcome:
         """One round through the public API.  Under the virtual clock the
         next round's host half (selection, fits, schedule, minibatch orders)
@@ -650,10 +748,11 @@ class SimulationEngine:
         """(host->device, device->host) bytes of round inputs/results so far."""
         return io_bytes()
 
-    def global_model(self):
+    def global_model(self, bundle: ParamBundle | None = None):
+        bundle = self.global_bundle if bundle is None else bundle
         if self.spec.kind == "lr":
-            return self.global_bundle.model()
-        return NamedParams(self.spec, self.global_bundle.named_model(self.spec))
+            return bundle.model()
+        return NamedParams(self.spec, bundle.named_model(self.spec))
 
     def run(self, rounds: int | None = None) -> list[RoundOutcome]:
         remaining = self.cfg.total_rounds - self.next_round

@@ -56,7 +56,8 @@ def _fill(a: ResnetTrainArgs, ws: dict, slots: int, BS: int, C: int) -> None:
 
 
 def resnet_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, bad, *,
-                       spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict) -> None:
+                       spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
+                       timeline=None) -> None:
     if terms.get("mu") or terms.get("ctrl_g") is not None or terms.get("ctrl_c"):
         raise NotImplementedError("the ResNet-18 path trains plain SGD (FedAvg / FedNova local rule)")
     G = len(n)
@@ -83,6 +84,7 @@ def resnet_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, step
     a.loss_sum, a.steps, a.bad = ptr(loss), ptr(steps), ptr(bad)
     _fill(a, ws, G, BS, spec.n_classes)
     a.batch_size, a.epochs, a.lr = batch_size, epochs, lr
+    a.timeline = ptr(timeline)
     lib.check(lib.pb_resnet_train_group(ctypes.byref(a), stream_of(w_out)))
 
 

@@ -182,6 +182,11 @@ class StateStore:
         elif [n for n, _ in schema] != [n for n, _ in self._schema]:
             raise ValueError("state payload schema changed between saves")
 
+    @property
+    def configured(self) -> bool:
+        """True once the payload layout is known (configure() or a first save)."""
+        return self._schema is not None
+
     def configure(self, names: Sequence[str], shapes: Sequence[tuple[int, ...]]) -> None:
         """Declare the payload layout up front (the engine does this)."""
         self._set_schema({n: np.zeros(s, dtype=np.float32) for n, s in zip(names, shapes)})
@@ -228,11 +233,15 @@ class StateStore:
         self._peak_live = max(self._peak_live, len(self._live))
 
     def _page_in(self, client_id: int) -> None:
-        """Disk tier -> HBM row (CRC-checked)."""
-        _, payload = self._read_file(client_id)
+        """Disk tier -> HBM row (CRC-checked); the file's round becomes the
+        client's last-written round (a file another process wrote after this
+        store was opened is picked up with its own round)."""
+        rnd, payload = self._read_file(client_id)
         self._set_schema(payload)
         s = self._slot_for(client_id)
         self._rows[s].copy_(self._flat(payload))
+        with self._lock:
+            self._last_round[client_id] = rnd
 
     # -- reference API ----------------------------------------------------------
     def load(self, client_id: int,

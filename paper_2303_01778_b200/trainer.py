@@ -6,10 +6,15 @@ make_plugin, client_execute, evaluate).  Differences, all deliberate:
 
 * bundle tensors live on the GPU in fp32 (``ParamBundle.numpy(name)`` gives a
   float64 host copy); the reference keeps float64 NumPy arrays;
-* a plugin's ``local_gradient``/``finalize`` hooks are not Python callbacks
-  but fused device terms (``grad_terms``) and a group finalizer
-  (``finalize_group``), because the whole local run of a client happens inside
-  one kernel (SURVEY.md §8(a) a4-a6);
+* the built-in plugins run their ``local_gradient``/``finalize`` as fused
+  device terms (``grad_terms``) and a group finalizer (``finalize_group``),
+  because the whole local run of a client happens inside one kernel
+  (SURVEY.md §8(a) a4-a6).  They also expose the reference's per-minibatch
+  hooks (``local_gradient(model, xb, yb, ctx)``, ``finalize(...)``) on device
+  tensors; a reference-style plugin that overrides those hooks (and not the
+  fused ones) is executed client by client through them on the GPU
+  (``uses_hooks``, ``hook_client_execute``) -- the drop-in path for custom
+  algorithms, not the batched hot path;
 * training is batched: ``train_group`` runs G clients concurrently, one CTA
   (LR) per client, with bit-identical minibatch orders
   (``default_rng([seed, 6, client, round]).permutation`` per epoch,
@@ -193,6 +198,52 @@ class TrainReport:
             raise ValueError("measured_seconds must be > 0 when samples were processed")
 
 
+@dataclass
+class LocalContext:
+    """Everything a plugin's gradient hook may read during one client task
+    (fedsim/trainer.py:161-170); tensors are fp32 device tensors."""
+
+    start_model: ModelParams
+    global_bundle: ParamBundle
+    state: dict | None
+    lr: float
+    n_samples: int
+
+
+def _model_unchecked(w: torch.Tensor, b: torch.Tensor) -> ModelParams:
+    """A ModelParams without the per-construction finiteness sync (the hook
+    loop checks the accumulated loss once at the end instead)."""
+    m = object.__new__(ModelParams)
+    object.__setattr__(m, "weights", w)
+    object.__setattr__(m, "bias", b)
+    return m
+
+
+def _softmax_terms(model: ModelParams, x: torch.Tensor):
+    z = x @ model.weights.T + model.bias
+    z = z - z.max(dim=1, keepdim=True).values
+    return z, torch.log(torch.exp(z).sum(dim=1))
+
+
+def loss_value(model: ModelParams, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """Mean cross-entropy (fedsim/trainer.py:131-133), a 0-d device tensor."""
+    z, lse = _softmax_terms(model, x)
+    return (lse - z[torch.arange(len(y), device=z.device), y]).mean()
+
+
+def loss_and_grad(model: ModelParams, x: torch.Tensor, y: torch.Tensor):
+    """Mean CE and its gradient for multinomial LR (fedsim/trainer.py:136-145):
+    P = softmax(XW^T + b), grad_W = (P - Y)^T X / B, grad_b = sum(P - Y) / B.
+    Returns (loss as a 0-d device tensor, grad_W, grad_b)."""
+    z, lse = _softmax_terms(model, x)
+    p = torch.exp(z - lse[:, None])
+    rows = torch.arange(len(y), device=z.device)
+    loss = (lse - z[rows, y]).mean()
+    p[rows, y] -= 1.0
+    p /= len(y)
+    return loss, p.T @ x, p.sum(dim=0)
+
+
 # ---------------------------------------------------------------------------
 # device-resident client data
 # ---------------------------------------------------------------------------
@@ -244,6 +295,8 @@ class GroupOutcome:
     seconds: float          # device time of the training launch
     lazy: object | None = None  # deferred low-rank fc1 (cnn.LazyFc1): fc1_w rows unmaterialised
     pending: object | None = None  # deferred result read (train_group(defer_check=True))
+    client_seconds: np.ndarray | None = None  # [G] device-measured task time (timing=True)
+    timing: object | None = None  # (stamps tensor, decoder) until the result read
 
     def resolve(self) -> None:
         """Finish a deferred result read: wait for the group's [bad | steps |
@@ -264,6 +317,13 @@ class GroupOutcome:
         if not np.array_equal(steps_h, self.steps):
             raise RuntimeError(f"round {round_num}: device step counts differ from the plan")
         self.loss_mean = loss_h / np.maximum(steps_h, 1)
+        self._decode_timing()
+
+    def _decode_timing(self) -> None:
+        if self.timing is not None:
+            stamps, decode = self.timing
+            self.timing = None
+            self.client_seconds = decode(stamps.cpu().numpy())
 
 
 @dataclass
@@ -338,8 +398,15 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                 clients: Sequence[int], w0: torch.Tensor, global_bundle: ParamBundle,
                 state_work: torch.Tensor | None, epochs: int, batch_size: int, lr: float,
                 seed: int, round_num: int, inputs: GroupInputs | None = None,
-                defer_fc1: bool = False, defer_check: bool = False) -> GroupOutcome:
+                defer_fc1: bool = False, defer_check: bool = False,
+                timing: bool = False) -> GroupOutcome:
     """Run every listed client's full local schedule concurrently on the GPU.
+
+    timing (real clock): per-client device task times from %globaltimer
+    stamps taken by the kernels (``GroupOutcome.client_seconds``): for the LR
+    model each client's own CTA span; for the sweep models (CNN, ResNet) the
+    duration of every sweep divided among the clients active in it, summed
+    over the client's sweeps (the clients' times add up to the group's).
 
     defer_fc1 (CNN, plain SGD): leave the clients' fc1_w columns of w_out
     unmaterialised and return the round's low-rank history instead
@@ -364,6 +431,23 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     terms = plugin.grad_terms(spec, global_bundle)
     if terms.get("ctrl_c") and state_work is None:
         raise ValueError(f"{plugin.name} needs client state for training")
+    bs_c = n if batch_size <= 0 else np.minimum(batch_size, n)
+    steps_plan = (epochs * ((n + bs_c - 1) // bs_c)).astype(np.int64)
+    stamps = decode = None
+    if timing and spec.kind == "lr":
+        stamps = torch.zeros(G, 2, dtype=torch.int64, device=d)
+
+        def decode(ns):
+            return np.maximum((ns[:, 1] - ns[:, 0]) * 1e-9, 1e-9)
+    elif timing:
+        sweeps = int(steps_plan.max())
+        active = np.array([(steps_plan > s).sum() for s in range(sweeps)], dtype=np.float64)
+        stamps = torch.zeros(sweeps + 1, dtype=torch.int64, device=d)
+
+        def decode(ts):
+            share = np.diff(ts.astype(np.float64)) * 1e-9 / active   # per active client, per sweep
+            cum = np.concatenate([[0.0], np.cumsum(share)])
+            return np.maximum(cum[steps_plan], 1e-9)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -373,16 +457,17 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                    batch_size=batch_size, lr=lr, mu=terms.get("mu", 0.0),
                    prox_loss=terms.get("prox_loss", 0.0), ctrl_g=terms.get("ctrl_g"),
                    cg=terms.get("cg", 0.0), ctrl_c=state_work if terms.get("ctrl_c") else None,
-                   cc=terms.get("cc", 0.0))
+                   cc=terms.get("cc", 0.0), client_ns=stamps)
     elif spec.kind == "cnn":
         from .cnn import cnn_train_group
         lazy = cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
                                spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
-                               state_work=state_work, defer_fc1=defer_fc1)
+                               state_work=state_work, defer_fc1=defer_fc1, timeline=stamps)
     elif spec.kind == "resnet":
         from .resnet import resnet_train_group
         resnet_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
-                           spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms)
+                           spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
+                           timeline=stamps)
     else:
         raise ValueError(f"unknown model kind {spec.kind!r}")
     t1.record()
@@ -390,8 +475,6 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
         # the step counts are the plan's (a diverged client raises when the
         # read completes, GroupOutcome.resolve); the read itself is queued
         # behind the training without blocking the host
-        bs = n if batch_size <= 0 else np.minimum(batch_size, n)
-        steps_plan = (epochs * ((n + bs - 1) // bs)).astype(np.int64)
         res_h = torch.empty(3 * G, dtype=torch.float64, pin_memory=True)
         res_h.copy_(torch.cat([bad.double(), steps.double(), loss]), non_blocking=True)
         done = torch.cuda.Event()
@@ -399,7 +482,8 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
         if lazy is not None:
             lazy.set_steps(steps_plan)
         return GroupOutcome(clients, n, steps_plan, np.full(G, np.nan), w_out, float("nan"), lazy,
-                            pending=(res_h, done, t0, t1, round_num))
+                            pending=(res_h, done, t0, t1, round_num),
+                            timing=(stamps, decode) if stamps is not None else None)
     # one device->host read per group: failures, step counts, losses
     res = torch.cat([bad.double(), steps.double(), loss]).cpu().numpy()
     _IO["d2h"] += res.size * 8
@@ -410,7 +494,10 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
             raise NonFiniteLossError(f"client {clients[j]} round {round_num}: loss diverged")
     if lazy is not None:
         lazy.set_steps(steps_h)
-    return GroupOutcome(clients, n, steps_h, loss_h / np.maximum(steps_h, 1), w_out, seconds, lazy)
+    go = GroupOutcome(clients, n, steps_h, loss_h / np.maximum(steps_h, 1), w_out, seconds, lazy,
+                      timing=(stamps, decode) if stamps is not None else None)
+    go._decode_timing()
+    return go
 
 
 # ---------------------------------------------------------------------------
@@ -466,19 +553,37 @@ class AlgorithmPlugin(abc.ABC):
     def state_names(self, spec: ModelSpec) -> list[str]:
         return [self.state_prefix + n for n in spec.names] if self.state_prefix else []
 
-    # -- fused hooks --------------------------------------------------------
+    # -- fused hooks (the batched kernels) -----------------------------------
     def grad_terms(self, spec: ModelSpec, glob: ParamBundle) -> dict:
         """Extra gradient terms: g + mu*(w - w0) + cg*ctrl_g + cc*state."""
         return {}
 
-    @abc.abstractmethod
     def finalize_group(self, spec: ModelSpec, go: GroupOutcome, w0: torch.Tensor,
                        glob: ParamBundle, state_work: torch.Tensor | None):
         """-> (list[ResultGroup], new state rows [G, P] or None)."""
+        raise NotImplementedError(f"plugin {self.name!r} has no fused group finalizer")
+
+    # -- reference hooks (fedsim/trainer.py:199-207), on device tensors --------
+    def local_gradient(self, model: ModelParams, xb: torch.Tensor, yb: torch.Tensor,
+                       ctx: LocalContext):
+        """Return (loss, grad_weights, grad_bias) on one minibatch."""
+        raise NotImplementedError(f"plugin {self.name!r} defines no local_gradient hook")
+
+    def finalize(self, end_model: ModelParams, steps: int, ctx: LocalContext, n_samples: int):
+        """Build the uploaded result bundle and the new state payload."""
+        raise NotImplementedError(f"plugin {self.name!r} defines no finalize hook")
 
     @abc.abstractmethod
     def server_update(self, old_global: ParamBundle, agg) -> ParamBundle:
         """Apply the server rule to the folded aggregate."""
+
+
+def _model_bundle(model: ModelParams, op: AggOp, weight: float = 1.0, prefix: str = "",
+                  weights=None, bias=None) -> ParamBundle:
+    out = ParamBundle()
+    out._put(prefix + "weights", model.weights if weights is None else weights, op, weight)
+    out._put(prefix + "bias", model.bias if bias is None else bias, op, weight)
+    return out
 
 
 def _per_client(values, d=None) -> torch.Tensor:
@@ -492,6 +597,12 @@ class FedAvg(AlgorithmPlugin):
 
     def finalize_group(self, spec, go, w0, glob, state_work):
         return [spec_groups(spec, go.w_out, AggOp.WEIGHTED_AVERAGE, go.n)], None
+
+    def local_gradient(self, model, xb, yb, ctx):
+        return loss_and_grad(model, xb, yb)
+
+    def finalize(self, end_model, steps, ctx, n_samples):
+        return _model_bundle(end_model, AggOp.WEIGHTED_AVERAGE, n_samples), None
 
     def server_update(self, old_global, agg):
         return old_global.replaced(**{n: agg.bundle.tensor(n) for n in self._names()})
@@ -510,6 +621,16 @@ class FedProx(FedAvg):
 
     def grad_terms(self, spec, glob):
         return {"mu": self.mu, "prox_loss": 0.5 * self.mu} if self.mu != 0.0 else {}
+
+    def local_gradient(self, model, xb, yb, ctx):
+        loss, gw, gb = loss_and_grad(model, xb, yb)
+        if self.mu != 0.0:
+            dw = model.weights - ctx.start_model.weights
+            db = model.bias - ctx.start_model.bias
+            loss = loss + 0.5 * self.mu * ((dw * dw).sum() + (db * db).sum())
+            gw = gw + self.mu * dw
+            gb = gb + self.mu * db
+        return loss, gw, gb
 
 
 class FedNova(FedAvg):
@@ -530,6 +651,15 @@ class FedNova(FedAvg):
         return [spec_groups(spec, direction, AggOp.WEIGHTED_AVERAGE, go.n, "direction_"),
                 ResultGroup(["step_scale"], [(0, 1, (1,))], step, AggOp.SUM,
                             np.ones(len(go.n)))], None
+
+    def finalize(self, end_model, steps, ctx, n_samples):
+        scale = self.lr * steps
+        x = ctx.start_model
+        out = _model_bundle(end_model, AggOp.WEIGHTED_AVERAGE, n_samples, "direction_",
+                            (x.weights - end_model.weights) / scale, (x.bias - end_model.bias) / scale)
+        out._put("step_scale", torch.tensor([n_samples * scale], dtype=torch.float32,
+                                            device=x.weights.device), AggOp.SUM)
+        return out, None
 
     def server_update(self, old_global, agg):
         first = "direction_" + self._names()[0]
@@ -585,6 +715,25 @@ class Scaffold(AlgorithmPlugin):
         return [spec_groups(spec, delta, AggOp.WEIGHTED_AVERAGE, go.n, "delta_"),
                 spec_groups(spec, ctrl_delta, AggOp.SIMPLE_AVERAGE, np.ones(G), "ctrl_delta_")], new_c
 
+    def local_gradient(self, model, xb, yb, ctx):
+        loss, gw, gb = loss_and_grad(model, xb, yb)
+        g = ctx.global_bundle
+        gw = gw + (g.tensor("server_ctrl_weights") - _as_dev(ctx.state["ctrl_weights"]))
+        gb = gb + (g.tensor("server_ctrl_bias") - _as_dev(ctx.state["ctrl_bias"]))
+        return loss, gw, gb
+
+    def finalize(self, end_model, steps, ctx, n_samples):
+        x, y, g = ctx.start_model, end_model, ctx.global_bundle
+        inv = 1.0 / (steps * self.lr)
+        cw, cb = _as_dev(ctx.state["ctrl_weights"]), _as_dev(ctx.state["ctrl_bias"])
+        new_cw = cw - g.tensor("server_ctrl_weights") + (x.weights - y.weights) * inv
+        new_cb = cb - g.tensor("server_ctrl_bias") + (x.bias - y.bias) * inv
+        out = _model_bundle(y, AggOp.WEIGHTED_AVERAGE, n_samples, "delta_",
+                            y.weights - x.weights, y.bias - x.bias)
+        out._put("ctrl_delta_weights", new_cw - cw, AggOp.SIMPLE_AVERAGE)
+        out._put("ctrl_delta_bias", new_cb - cb, AggOp.SIMPLE_AVERAGE)
+        return out, {"ctrl_weights": new_cw, "ctrl_bias": new_cb}
+
     def server_update(self, old_global, agg):
         out = {}
         for n in self._names():
@@ -633,6 +782,20 @@ class FedDyn(AlgorithmPlugin):
                        dmat=state_work, d=1.0)
         return [spec_groups(spec, go.w_out, AggOp.SIMPLE_AVERAGE, np.ones(G))], new_h
 
+    def local_gradient(self, model, xb, yb, ctx):
+        loss, gw, gb = loss_and_grad(model, xb, yb)
+        x = ctx.start_model
+        gw = gw - _as_dev(ctx.state["grad_corr_weights"]) + self.alpha * (model.weights - x.weights)
+        gb = gb - _as_dev(ctx.state["grad_corr_bias"]) + self.alpha * (model.bias - x.bias)
+        return loss, gw, gb
+
+    def finalize(self, end_model, steps, ctx, n_samples):
+        x, y = ctx.start_model, end_model
+        new_hw = _as_dev(ctx.state["grad_corr_weights"]) - self.alpha * (y.weights - x.weights)
+        new_hb = _as_dev(ctx.state["grad_corr_bias"]) - self.alpha * (y.bias - x.bias)
+        return (_model_bundle(y, AggOp.SIMPLE_AVERAGE),
+                {"grad_corr_weights": new_hw, "grad_corr_bias": new_hb})
+
     def server_update(self, old_global, agg):
         out = {}
         af = self.alpha * self.client_fraction
@@ -655,6 +818,77 @@ def make_plugin(name: str, **hyper) -> AlgorithmPlugin:
     if cls is None:
         raise ValueError(f"unknown algorithm {name!r}; available: {sorted(PLUGINS)}")
     return cls(**hyper)
+
+
+def uses_hooks(plugin: AlgorithmPlugin) -> bool:
+    """True for a reference-style plugin: it customises the per-minibatch
+    hooks (``local_gradient`` / ``finalize``) rather than the fused device
+    terms, so its clients run one by one through those hooks.  A plugin with
+    neither raises a ConfigError naming what is missing."""
+    cls = type(plugin)
+    builtin = next((b for b in cls.__mro__ if b in _BUILTIN), None)
+    if builtin is not None:
+        return (cls.local_gradient is not builtin.local_gradient
+                or cls.finalize is not builtin.finalize)
+    fused = cls.finalize_group is not AlgorithmPlugin.finalize_group
+    hooks = (cls.local_gradient is not AlgorithmPlugin.local_gradient
+             and cls.finalize is not AlgorithmPlugin.finalize)
+    if not fused and not hooks:
+        from .core import ConfigError
+        raise ConfigError(f"plugin {getattr(plugin, 'name', cls.__name__)!r} implements neither the "
+                          "reference hooks (local_gradient + finalize) nor the fused device hooks "
+                          "(grad_terms + finalize_group)")
+    return not fused
+
+
+_BUILTIN = frozenset(PLUGINS.values())
+
+
+def hook_client_execute(plugin: AlgorithmPlugin, client_id: int, X: torch.Tensor, Y: torch.Tensor,
+                        global_bundle: ParamBundle, state: ClientState | None, epochs: int,
+                        batch_size: int, lr: float, seed: int, round_num: int) -> TrainReport:
+    """client_execute (fedsim/trainer.py:427-477) through the plugin's own
+    per-minibatch hooks, on the GPU: the same stream-6 permutations, partial
+    last batch, ``w -= lr * g`` steps and finalize; X [n, F] fp32 and Y [n]
+    are the client's device rows.  The loss is accumulated on the device and
+    checked once at the end (a diverged step makes the sum non-finite)."""
+    if epochs < 1:
+        raise ValueError("epochs must be >= 1")
+    from .core import stream_rng
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n = int(X.shape[0])
+    start = global_bundle.model()
+    ctx = LocalContext(start_model=start, global_bundle=global_bundle,
+                       state=state.payload if state is not None else None, lr=lr, n_samples=n)
+    rng = stream_rng(seed, STREAM_MINIBATCH, client_id, round_num)
+    bs = n if batch_size <= 0 else min(batch_size, n)
+    Y = Y.long()
+    w, b = start.weights.clone(), start.bias.clone()
+    steps = 0
+    loss_total = torch.zeros((), dtype=torch.float64, device=w.device)
+    for _ in range(epochs):
+        order = torch.from_numpy(rng.permutation(n)).to(w.device)
+        for lo in range(0, n, bs):
+            batch = order[lo:lo + bs]
+            loss, gw, gb = plugin.local_gradient(_model_unchecked(w, b), X[batch], Y[batch], ctx)
+            w = w - lr * _as_dev(gw)
+            b = b - lr * _as_dev(gb)
+            loss_total = loss_total + loss
+            steps += 1
+    mean_loss = float(loss_total.item()) / steps
+    if not np.isfinite(mean_loss):
+        raise NonFiniteLossError(f"client {client_id} round {round_num}: loss diverged")
+    result, payload = plugin.finalize(ModelParams(w, b), steps, ctx, n)
+    if plugin.collect_local_loss:
+        result._put("local_loss", torch.tensor([mean_loss], dtype=torch.float32, device=w.device),
+                    AggOp.COLLECT, client_id=client_id)
+    new_state = None
+    if payload is not None:
+        new_state = ClientState(client_id, round_num, payload)
+    torch.cuda.synchronize()
+    return TrainReport(client_result=result, new_state=new_state, samples_processed=epochs * n,
+                       measured_seconds=max(time.perf_counter() - t0, 1e-9))
 
 
 def spec_of_bundle(bundle: ParamBundle, plugin: AlgorithmPlugin | None = None) -> ModelSpec:
@@ -686,6 +920,14 @@ def client_execute(plugin: AlgorithmPlugin, client: ClientProfile, global_bundle
     """One client's E local epochs (fedsim/trainer.py:427-477) on the GPU."""
     if epochs < 1:
         raise ValueError("epochs must be >= 1")
+    if uses_hooks(plugin):
+        d = device()
+        part = client.data_partition
+        return hook_client_execute(
+            plugin, client.client_id,
+            torch.from_numpy(np.asarray(part.features, dtype=np.float32)).to(d),
+            torch.from_numpy(np.asarray(part.labels, dtype=np.int64)).to(d),
+            global_bundle, state, epochs, batch_size, lr, seed, round_num)
     spec = spec_of_bundle(global_bundle, plugin)
     data = ClientData.from_profiles([client], n_classes=spec.n_classes)
     w0 = global_bundle.flat(spec)

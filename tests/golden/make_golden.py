@@ -1,7 +1,7 @@
 """Generate the golden fixtures under tests/golden/ by running the REFERENCE
 (FedML Parrot ``fedsim`` 0.1.0 at /root/reference/pkg/src) in this container.
 
-    NUMBA_CACHE_DIR=/tmp/numba python tests/golden/make_golden.py
+    NUMBA_CACHE_DIR=/tmp/numba python tests/golden/make_golden.py [seam]
 
 The reference tree is read-only and absent on the GPU box, so its outputs are
 committed here as small fixtures; nothing at test time reads /root/reference.
@@ -259,7 +259,58 @@ def host_cases() -> dict:
     return out
 
 
+# --------------------------------------------------------------------------
+# the device seam: DeviceWorker.execute_clients (fedsim/engine.py:470-503)
+# --------------------------------------------------------------------------
+
+def seam_cases() -> dict:
+    """One DeviceWorker driven directly (no engine) over two rounds, on a
+    FRESH StateStore: the partial (acc, weight sum, count, Collect items,
+    fold order) and the timing records it returns."""
+    from fedsim.engine import DeviceWorker
+    from fedsim.metrics import ReplicaGauge
+    out = {}
+    ds = generate(240, 4, 3, seed=5)
+    profiles = partition(ds, 12, PartitionSpec(), seed=5)
+    rng = np.random.default_rng(31)
+    W0, b0 = 0.2 * rng.standard_normal((3, 4)), 0.2 * rng.standard_normal(3)
+    cg = (0.05 * rng.standard_normal((3, 4)), 0.05 * rng.standard_normal(3))
+    out["W0"], out["b0"], out["ctrl_gw"], out["ctrl_gb"] = W0, b0, cg[0], cg[1]
+    cfg = SimConfig(total_clients=12, concurrent_clients=6, num_devices=2, total_rounds=4,
+                    local_epochs=2, seed=5, scheme="PARROT")
+    dev = DeviceModel(1, hetero_ratio=0.3, noise=0.05, t_true=2e-4, b_true=0.01)
+    rounds = [(0, [3, 7, 1]), (1, [7, 2, 3])]
+    out["rounds"] = np.array([[r] + c for r, c in rounds])
+    for name, plug in (("fedavg", FedAvg(lr=0.1, batch_size=5, collect_local_loss=True)),
+                       ("scaffold", Scaffold(lr=0.1, batch_size=5, client_fraction=0.5))):
+        store = StateStore(tempfile.mkdtemp(prefix="gold_seam_")) if plug.is_stateful else None
+        worker = DeviceWorker(dev, cfg, plug, profiles, store, ReplicaGauge())
+        glob = plug.init_global(ModelParams(W0, b0))
+        if name == "scaffold":
+            glob = glob.replaced(server_ctrl_weights=cg[0], server_ctrl_bias=cg[1])
+        for r, clients in rounds:
+            part, timings = worker.execute_clients(glob, clients, r)
+            tag = f"{name}/r{r}"
+            out[f"{tag}/folded"] = np.array(part.clients_folded)
+            out[f"{tag}/records"] = np.array([[t.device_id, t.client_id, t.round, t.sample_count,
+                                               t.reported_seconds] for t in timings])
+            for en, pe in part.entries.items():
+                out[f"{tag}/op/{en}"] = np.array([pe.op.value])
+                out[f"{tag}/count/{en}"] = np.array([pe.count])
+                if pe.op is AggOp.COLLECT:
+                    out[f"{tag}/collect_ids/{en}"] = np.array([c for c, _ in pe.collected])
+                    out[f"{tag}/collect/{en}"] = np.stack([np.asarray(t) for _, t in pe.collected])
+                else:
+                    out[f"{tag}/acc/{en}"] = pe.acc
+                    out[f"{tag}/wsum/{en}"] = np.array([pe.weight_sum])
+    return out
+
+
 def main() -> None:
+    if sys.argv[1:] == ["seam"]:
+        np.savez_compressed(OUT / "seam.npz", **seam_cases())
+        return
+    np.savez_compressed(OUT / "seam.npz", **seam_cases())
     np.savez_compressed(OUT / "trainer.npz", **trainer_cases())
     np.savez_compressed(OUT / "engine.npz", **engine_cases())
     np.savez_compressed(OUT / "configs.npz", **c1_c3_cases())

@@ -205,3 +205,14 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name)
     assert lib.pb_version() >= 1
+
+
+def test_abi_struct_layouts_match_bindings():
+    """The ctypes argument structs have the C ABI's sizes (a field added on
+    one side only would shift every later field)."""
+    import ctypes
+    from paper_2303_01778_b200._lib import CnnTrainArgs, LazyFoldArgs, LrTrainArgs, ResnetTrainArgs, lib
+    out = (ctypes.c_int64 * 4)()
+    assert lib.pb_abi_sizes(out, 4) == 4
+    want = [ctypes.sizeof(t) for t in (LrTrainArgs, CnnTrainArgs, LazyFoldArgs, ResnetTrainArgs)]
+    assert list(out) == want
