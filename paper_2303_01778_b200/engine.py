@@ -49,7 +49,7 @@ from .models import ModelSpec, init_params, spec_for
 from .schedule import MODE_GREEDY, RoundPlan, schedule, uniform_division, warm_jit
 from .statestore import StateStore
 from .trainer import (AggOp, AlgorithmPlugin, ClientData, FedAvg, GroupInputs, ModelParams, NamedParams,
-                      ParamBundle, device, evaluate, finalize_results, hook_client_execute, io_bytes,
+                      NonFiniteLossError, ParamBundle, device, evaluate, finalize_results, hook_client_execute, io_bytes,
                       spec_of_bundle, train_group, uses_hooks)
 
 RESULTS_HEADER = ("round\tscheme\tscheduling\tsim_seconds\twall_seconds\t"
@@ -153,6 +153,7 @@ class RoundInputs:
     group: GroupInputs | None
     wall0: float
     records: list | None = None   # virtual-clock timing records, committed at hand-out
+    executed: list | None = None  # multi-process: every rank's clients (state exchange)
 
     def upload(self) -> "RoundInputs":
         if self.group is not None:
@@ -210,6 +211,7 @@ class DeviceRuntime:
         self.batch_peak = 0   # most clients trained in one batched launch
         self.pending: GroupOutcome | None = None   # group whose result read is outstanding
         self.hooks = uses_hooks(plugin)
+        self.shard = None   # distributed.ShardedState: stateful clients owned across ranks
 
     def resolve(self) -> None:
         """Complete the outstanding result read of the last group (raises on a
@@ -228,14 +230,22 @@ class DeviceRuntime:
         return GroupInputs(self.data, clients, self.cfg.local_epochs, self.cfg.seed, round_num)
 
     def execute(self, assignments: dict[int, list[int]], bundle: ParamBundle,
-                round_num: int, inputs: GroupInputs | None = None) -> dict[int, DevicePartial]:
+                round_num: int, inputs: GroupInputs | None = None,
+                executed: list[list[int]] | None = None) -> dict[int, DevicePartial]:
         """Train every assigned client of the local devices in one batched
-        launch, then fold each device's clients in its plan order."""
+        launch, then fold each device's clients in its plan order.
+        ``executed`` (multi-process stateful rounds): every rank's clients,
+        for the owner-sharded state exchange."""
         t_in = time.perf_counter()
         order = [(dev, m) for dev in sorted(assignments) for m in assignments[dev]]
         partials = {dev: DevicePartial(device_id=dev) for dev in assignments}
         self.last_device_seconds = 0.0
         if not order:
+            if self.shard is not None:   # an idle rank still takes part in the state exchange
+                width = self.spec.numel
+                self.shard.gather(executed, torch.empty(0, width, device=device()))
+                self._failure_vote(None, round_num)
+                self.shard.scatter(executed, round_num, torch.empty(0, width, device=device()))
             return partials
         clients = [m for _, m in order]
         if len(set(clients)) != len(clients):
@@ -251,7 +261,10 @@ class DeviceRuntime:
             if not self.store.configured:   # a fresh store behind a bare DeviceWorker
                 self.store.configure(plugin.state_names(spec), [sh for *_, sh in spec.columns()])
             work = torch.empty(len(clients), (spec.numel + 3) // 4 * 4, device=w0.device)[:, :spec.numel]
-            self.store.gather(clients, work)
+            if self.shard is not None:
+                self.shard.gather(executed, work)
+            else:
+                self.store.gather(clients, work)
         # one live model replica per busy simulated device (the reference's
         # Table-1 quantity); the batch itself is the GPU's real concurrency
         busy = sum(1 for dev in assignments if assignments[dev])
@@ -267,10 +280,18 @@ class DeviceRuntime:
             # diverged client leaves the store untouched
             late = (self.cfg.clock == "virtual" and not plugin.collect_local_loss
                     and not plugin.is_stateful)
-            go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
-                             self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
-                             round_num, inputs=inputs, defer_fc1=defer, defer_check=late,
-                             timing=self.cfg.clock == "real")
+            err = None
+            try:
+                go = train_group(plugin, spec, self.data, clients, w0, bundle, work,
+                                 self.cfg.local_epochs, plugin.batch_size, plugin.lr, self.cfg.seed,
+                                 round_num, inputs=inputs, defer_fc1=defer, defer_check=late,
+                                 timing=self.cfg.clock == "real")
+            except Exception as exc:
+                err = exc
+            if self.shard is not None:
+                self._failure_vote(err, round_num)
+            elif err is not None:
+                raise err
         finally:
             self.gauge.release(busy)
         t_tr = time.perf_counter()
@@ -285,7 +306,10 @@ class DeviceRuntime:
                 if g.op is AggOp.WEIGHTED_AVERAGE:
                     g.lazy = go.lazy
         if plugin.is_stateful and new_state is not None:
-            self.store.scatter(clients, round_num, new_state)
+            if self.shard is not None:
+                self.shard.scatter(executed, round_num, new_state)
+            else:
+                self.store.scatter(clients, round_num, new_state)
         pos = 0
         for dev in sorted(assignments):
             k = len(assignments[dev])
@@ -296,6 +320,18 @@ class DeviceRuntime:
             print(f"  execute: train_group {1e3 * (t_tr - t_in):.1f} finalize {1e3 * (t_fin - t_tr):.1f} "
                   f"fold {1e3 * (t_end - t_fin):.1f} ms", file=sys.stderr, flush=True)
         return partials
+
+    def _failure_vote(self, err: Exception | None, round_num: int) -> None:
+        """Multi-process stateful rounds: every rank learns whether any rank's
+        clients diverged before a state is committed (one small all-reduce),
+        so all ranks abort together instead of one hanging in the exchange."""
+        import torch.distributed as dist
+        flag = torch.tensor([0.0 if err is None else 1.0], device=device())
+        dist.all_reduce(flag)
+        if err is not None:
+            raise err
+        if flag.item() > 0:
+            raise NonFiniteLossError(f"round {round_num}: a client on another rank diverged")
 
     def _execute_hooks(self, assignments: dict[int, list[int]], bundle: ParamBundle,
                        round_num: int) -> dict[int, DevicePartial]:
@@ -465,15 +501,18 @@ class SimulationEngine:
             self._rank = torch.distributed.get_rank()
             if cfg.clock == "real":
                 raise ConfigError("multi-process runs need the virtual clock (shared histories)")
-            if plugin.is_stateful and self._world > 1:
-                # each rank's store is HBM-local while the plan moves clients
-                # between ranks every round: a client's state would be read
-                # on a rank that never wrote it
-                raise ConfigError(f"{plugin.name} keeps per-client state; stateful plugins run "
-                                  "single-process (one GPU) until client state is sharded by owner rank")
+            if uses_hooks(plugin) and self._world > 1:
+                raise ConfigError(f"reference-style plugin {plugin.name!r} (per-minibatch hooks) runs "
+                                  "single-process; multi-GPU rounds need a fused plugin")
+
         from .distributed import local_devices
         self.local_devices = local_devices(cfg.num_devices, self._world, self._rank)
         self.runtime = DeviceRuntime(cfg, plugin, self.spec, self.data, store, self.gauge)
+        if plugin.is_stateful and self._world > 1:
+            # the plan moves clients between ranks every round: each client's
+            # state lives with its owner rank and travels around the round
+            from .distributed import ShardedState
+            self.runtime.shard = ShardedState(store, self._world, self._rank)
         _prewarm_small_pool()
         if cfg.scheme == "PARROT" and cfg.scheduling in ("full-history", "time-window"):
             warm_jit()
@@ -521,12 +560,20 @@ class SimulationEngine:
                 idx += 1
         return done
 
-    def _reduce_partials(self, partials: list[DevicePartial], schema) -> list[DevicePartial]:
-        """Multi-process: one all-reduce of this rank's packed partials (NCCL)."""
+    def _reduce_partials(self, partials: list[DevicePartial], schema,
+                         inp: "RoundInputs") -> list[DevicePartial]:
+        """Multi-process: ONE all-reduce of this rank's packed partials (NCCL);
+        weight sums, counts and fold order come from the plan every rank holds
+        (built-in plugins weight a client by its sample count)."""
         from . import _kernels as K
         from .distributed import allreduce_partials
+        if inp.fa_tasks is not None:
+            assign = {i: [m] for i, (_, m) in enumerate(inp.fa_tasks)}
+        else:
+            assign = {k: list(inp.plan.assignments.get(k, [])) for k in range(self.cfg.num_devices)}
         return [allreduce_partials(partials, schema, device=device(),
-                                   fold=lambda acc, x: K.fold(acc, x, 1.0))]
+                                   fold=lambda acc, x: K.fold(acc, x, 1.0),
+                                   assign=assign, weights=inp.sizes)]
 
     # -- the round ----------------------------------------------------------------
     def prepare_round(self, round_num: int) -> "RoundInputs":
@@ -600,6 +647,11 @@ class SimulationEngine:
             assign = {k: list(plan.assignments.get(k, [])) for k in self.local_devices}
         inp = RoundInputs(round_num, selection, sizes, fits, fit_seconds, schedule_seconds, plan,
                           fa_tasks, assign, self.runtime.prepare(assign, round_num), wall0)
+        if self._world > 1 and self.plugin.is_stateful:
+            from .distributed import rank_clients
+            if fa_tasks is not None:
+                raise ConfigError("FA_DIST with a stateful plugin runs single-process")
+            inp.executed = rank_clients(plan.assignments, cfg.num_devices, self._world)
         if cfg.clock == "virtual":   # built here (possibly on the helper thread), added at hand-out
             inp.records = self._records(inp, None)
         return inp
@@ -646,7 +698,8 @@ class SimulationEngine:
         trace = _TRACE and [(time.perf_counter(), "start")]
         ledger = CostLedger(round=round_num, scheme=cfg.scheme)
         try:
-            got = self.runtime.execute(inp.assign, self.global_bundle, round_num, inp.group)
+            got = self.runtime.execute(inp.assign, self.global_bundle, round_num, inp.group,
+                                       inp.executed)
         except Exception as exc:
             self._abort_round(round_num)
             raise DeviceFailureError(f"device {self._rank} failed: {exc!r}") from exc
@@ -658,7 +711,7 @@ class SimulationEngine:
         if cfg.clock == "real":
             self._record(inp, self._measured_seconds(inp))
         if self._world > 1:
-            partials = self._reduce_partials(partials, schema)
+            partials = self._reduce_partials(partials, schema, inp)
         agg = global_fold(partials)
         new_global = server_update(self.plugin, self.global_bundle, agg)
 
@@ -706,7 +759,7 @@ class SimulationEngine:
         self.global_bundle = new_global
         if trace:
             trace.append((time.perf_counter(), "result read"))
-        if sync:
+        if sync and torch.cuda.is_available():
             torch.cuda.synchronize()
         if trace:
             trace.append((time.perf_counter(), "synced"))

@@ -1,6 +1,8 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU round plumbing: device
-ownership, the packed all-reduce of device partials, Collect gathering, and
-that every rank derives the identical plan (host-side, bit-exact)."""
+ownership, the packed all-reduce of device partials, Collect gathering,
+that every rank derives the identical plan (host-side, bit-exact), and whole
+SimulationEngine rounds across ranks on a mocked device layer
+(tests/cpu_device.py), stateful clients included."""
 
 import os
 import socket
@@ -47,8 +49,10 @@ def _worker(rank, world, port, out_dir):
         mine, _ = _partials_for(rank, world)
         schema = [("w", AggOp.WEIGHTED_AVERAGE, (3, 5)), ("c", AggOp.SIMPLE_AVERAGE, (2,)),
                   ("local_loss", AggOp.COLLECT, (1,))]
+        assign = {k: [10 * k, 10 * k + 1] for k in range(4)}
+        weights = {10 * k + j: 3.5 + 0.5 * k for k in range(4) for j in range(2)}
         got = allreduce_partials(mine, schema, device=torch.device("cpu"),
-                                 fold=lambda acc, x: acc.add_(x))
+                                 fold=lambda acc, x: acc.add_(x), assign=assign, weights=weights)
         res = {"w": got.entries["w"].acc.numpy(), "wsum": got.entries["w"].weight_sum,
                "c": got.entries["c"].acc.numpy(), "cnt": got.entries["c"].count,
                "loss": sorted((c, float(t[0])) for c, t in got.entries["local_loss"].collected),
@@ -91,3 +95,73 @@ def test_local_devices_partition():
             owned = [local_devices(k, world, r) for r in range(world)]
             flat = sorted(d for o in owned for d in o)
             assert flat == list(range(k))
+
+
+# ---------------------------------------------------------------------------
+# SimulationEngine end to end across 2 ranks (mocked device layer, gloo)
+# ---------------------------------------------------------------------------
+
+def _engine_worker(rank, world, port, out_dir, plugin_name):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import cpu_device
+    cpu_device.install()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2303_01778_b200 as pb
+        ds = pb.generate(600, 6, 4, seed=9)
+        profiles = pb.partition(ds, 30, pb.PartitionSpec(quantity_skew=0.3), seed=9)
+        cfg = pb.SimConfig(total_clients=30, concurrent_clients=12, num_devices=4, total_rounds=4,
+                           seed=9, scheme="PARROT", scheduling="time-window", time_window=2)
+        devs = pb.make_device_models(4, hetero=[0.0, 0.3, 0.6, 0.9], noise=0.05)
+        if plugin_name == "scaffold":
+            plugin = pb.Scaffold(lr=0.1, batch_size=5, client_fraction=0.5)
+            store = pb.StateStore(device=torch.device("cpu"))
+        else:
+            plugin, store = pb.FedAvg(lr=0.1, batch_size=5, collect_local_loss=True), None
+        eng = pb.SimulationEngine(cfg, plugin, profiles, devs, store=store)
+        res = {"globals": [], "plans": [], "records": []}
+        for oc in eng.run():
+            res["globals"].append({n: e.tensor.clone() for n, e in oc.new_global.entries.items()})
+            res["records"].append([(x.device_id, x.client_id, x.reported_seconds)
+                                   for x in eng.history.round_records(oc.round)])
+            res["modes"] = res.get("modes", []) + [oc.scheduling_mode]
+        if store is not None:
+            res["state"] = {c: store._rows[s].clone() for c, s in store._slot.items()}
+            res["rounds"] = dict(store._last_round)
+        torch.save(res, os.path.join(out_dir, f"{plugin_name}_w{world}_r{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("plugin_name", ["fedavg", "scaffold"])
+def test_engine_rounds_world2_match_world1(tmp_path, plugin_name):
+    """SimulationEngine across 2 ranks (devices k % 2 per rank, ONE packed
+    all-reduce per round, Collect values in the same buffer, stateful
+    clients owned by rank m % 2 and exchanged with all_to_all) equals the
+    single-process run: same plans and records (bit-exact), same globals
+    (fp32 reassociation tolerance), and the union of the ranks' stores equals
+    the single store."""
+    for world in (1, 2):
+        mp.spawn(_engine_worker, args=(world, _free_port(), str(tmp_path), plugin_name),
+                 nprocs=world, join=True)
+    one = torch.load(tmp_path / f"{plugin_name}_w1_r0.pt", weights_only=False)
+    two = [torch.load(tmp_path / f"{plugin_name}_w2_r{r}.pt", weights_only=False) for r in (0, 1)]
+    assert "greedy" in one["modes"]
+    for res in two:
+        assert res["records"] == one["records"] and res["modes"] == one["modes"]
+        for g1, g2 in zip(one["globals"], res["globals"]):
+            assert set(g1) == set(g2)
+            for name in g1:
+                assert torch.allclose(g1[name], g2[name], atol=1e-6, rtol=1e-5), name
+    assert all(torch.equal(two[0]["globals"][-1][n], two[1]["globals"][-1][n])
+               for n in two[0]["globals"][-1])   # replicated
+    if plugin_name == "scaffold":
+        merged = {**two[0]["state"], **two[1]["state"]}
+        assert set(two[0]["state"]).isdisjoint(two[1]["state"])
+        assert all(c % 2 == r for r in (0, 1) for c in two[r]["state"])   # owner = m % world
+        assert set(merged) == set(one["state"])
+        for c, row in one["state"].items():
+            assert torch.allclose(merged[c], row, atol=1e-6), c
+        assert {**two[0]["rounds"], **two[1]["rounds"]} == one["rounds"]
