@@ -157,6 +157,53 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     return h @ f2w.t() + f2b
 
 
+def decision_margins(params, x: torch.Tensor, fc1_base: torch.Tensor | None = None) -> dict:
+    """How close one step's discrete decisions sit to flipping, under the
+    emulating forward (emulate_bf16=True): for every ReLU the smallest
+    |pre-activation|, for every 2x2 max-pool the smallest gap between the
+    window's largest and second-largest input -- each divided by the RMS of
+    that layer's pre-activations.  A decision whose margin is below the
+    device-vs-oracle arithmetic noise (fp32 accumulation in another order,
+    ~1e-6 relative) can legitimately go the other way on the device; a step
+    without such a decision cannot flip anything, so its update must match
+    tightly (tests/test_gpu_c2_headline.py)."""
+    c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = [p.detach() for p in params]
+
+    def rms(z):
+        return float(z.pow(2).mean().sqrt()) or 1.0
+
+    def pool_gap(a, z):
+        """[B, C, H, W] relu outputs -> smallest top1 - top2 over the 2x2
+        windows with two positive candidates (a window with at most one
+        positive input has a fixed argmax unless that input crosses zero,
+        which the ReLU margin covers; zeros tie harmlessly)."""
+        w = a.unfold(2, 2, 2).unfold(3, 2, 2).reshape(*a.shape[:2], a.shape[2] // 2, a.shape[3] // 2, 4)
+        top = w.topk(2, dim=-1).values
+        gap = torch.where(top[..., 1] > 0, top[..., 0] - top[..., 1], torch.full_like(top[..., 0], np.inf))
+        return float(gap.min()) / rms(z)
+
+    out = {}
+    with torch.no_grad():
+        h = x.reshape(-1, 1, 28, 28)
+        z1 = F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)
+        out["relu1"] = float(z1.abs().min()) / rms(z1)
+        a1 = F.relu(z1)
+        out["pool1"] = pool_gap(a1, z1)
+        h = F.max_pool2d(a1, 2)
+        z2 = F.conv2d(_RoundValue.apply(h), _RoundValue.apply(c2w).permute(0, 3, 1, 2), padding=2) \
+            + c2b.view(1, -1, 1, 1)
+        out["relu2"] = float(z2.abs().min()) / rms(z2)
+        a2 = F.relu(z2)
+        out["pool2"] = pool_gap(a2, z2)
+        h = F.max_pool2d(a2, 2).permute(0, 2, 3, 1).reshape(a2.shape[0], -1)
+        if fc1_base is None:
+            z3 = _tf32(h) @ _tf32(f1w).t() + f1b
+        else:
+            z3 = _tf32_rna(h) @ (f1w - fc1_base + _tf32(fc1_base)).t() + f1b
+        out["relu3"] = float(z3.abs().min()) / rms(z3)
+    return out
+
+
 def client_train(flat_w0, X: np.ndarray, y: np.ndarray, client_id: int, seed: int, rnd: int,
                  epochs: int, batch_size: int, lr: float, n_classes: int,
                  dtype=torch.float64, emulate_bf16: bool = False, mu: float = 0.0):
