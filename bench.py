@@ -214,9 +214,19 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_sample_rounds_per_s(sizes, n_clients: int = 6, threads: int | None = None):
-    """Oracle port (torch CPU fp32, all host threads) on a bounded sample of the
-    round: n_clients clients' full local runs, extrapolated to 1000 clients."""
+def round_selection(r: int) -> list[int]:
+    from paper_2303_01778_b200.core import SimConfig, select_clients
+    cfg = SimConfig(total_clients=M_TOTAL, concurrent_clients=M_ROUND, num_devices=1,
+                    total_rounds=r + 2, seed=0, scheme="PARROT")
+    return [int(m) for m in select_clients(cfg, r).selected]
+
+
+def cpu_sample_rounds_per_s(sizes, selected, stride: int, offset: int = 0, threads: int | None = None):
+    """Oracle port (torch CPU fp32, all host threads) on a stratified sample
+    of one round: the round's clients sorted by sample count, every
+    `stride`-th from `offset` (so the sample spans the size distribution),
+    each running its full local schedule on FEMNIST-shaped Gaussian-mixture
+    data; rounds/s = 1 / (measured seconds per sample x the round's samples)."""
     import torch
     from oracle import cnn_oracle
     from paper_2303_01778_b200.models import cnn_init, cnn_spec
@@ -224,22 +234,23 @@ def cpu_sample_rounds_per_s(sizes, n_clients: int = 6, threads: int | None = Non
         torch.set_num_threads(threads)
     spec = cnn_spec(N_CLASSES)
     w0 = cnn_init(spec, seed=0)
-    rng = np.random.default_rng(1)
-    picks = rng.choice(M_TOTAL, size=n_clients, replace=False)
-    samples = 0
-    t0 = time.perf_counter()
+    ranked = sorted(selected, key=lambda m: (int(sizes[m]), m))
+    picks = ranked[offset::stride]
+    rng = np.random.default_rng(100 + offset)
+    means = rng.standard_normal((N_CLASSES, 784)).astype(np.float32)
+    means *= 3.0 / np.linalg.norm(means, axis=1, keepdims=True)
+    samples, secs = 0, 0.0
     for m in picks:
         n = int(sizes[m])
-        X = rng.standard_normal((n, 784)).astype(np.float32)
         y = rng.integers(0, N_CLASSES, n)
-        cnn_oracle.client_train(w0, X, y, int(m), 0, 0, EPOCHS, BS, LR, N_CLASSES,
-                                dtype=torch.float32)
+        X = means[y] + rng.standard_normal((n, 784), dtype=np.float32)
+        t0 = time.perf_counter()
+        cnn_oracle.client_train(w0, X, y, int(m), 0, 0, EPOCHS, BS, LR, N_CLASSES, dtype=torch.float32)
+        secs += time.perf_counter() - t0
         samples += n
-    dt = time.perf_counter() - t0
-    per_sample = dt / samples
-    mean_round_samples = float(np.mean(sizes)) * M_ROUND
-    return 1.0 / (per_sample * mean_round_samples), {
-        "clients": n_clients, "samples": samples, "seconds": dt,
+    round_samples = int(sum(int(sizes[m]) for m in selected))
+    return samples / secs / round_samples, {
+        "clients": len(picks), "samples": samples, "seconds": secs, "round_samples": round_samples,
         "threads": torch.get_num_threads()}
 
 
@@ -336,6 +347,8 @@ def run_b200(args) -> dict:
     state = state_microbench(dev) if args.agg and world == 1 else None
     # ---- config 4 (ResNet-18-GN) rounds, 1 GPU, secondary ----
     c4 = resnet_round_bench(dev) if args.c4 and world == 1 else None
+    # ---- configs 1 and 3 (LR) next to the reference engine itself ----
+    c13 = lr_configs_bench(dev) if args.c13 and world == 1 and rank == 0 else None
 
     peaks, peak_src = load_peaks()
     samples_round = float(np.sum(sizes)) / M_TOTAL * M_ROUND
@@ -357,9 +370,12 @@ def run_b200(args) -> dict:
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "bf16 (conv2 tcgen05 operands) / fp32 (master weights, other layers)",
-        "data": "synthetic FEMNIST-shaped Gaussian mixture generated on device; "
-                "Dirichlet(1.0) client sizes bit-exact with fedsim.partition",
+        "dtype": "bf16 (conv2 tcgen05 operands) / tf32 (fc1 tcgen05 operands) / fp32 (master "
+                 "weights, accumulation, conv1, fc2, loss)",
+        "data": "synthetic FEMNIST-shaped: fedsim.data.generate's construction (unit class means x 3 "
+                "+ N(0,1)) drawn from torch's device RNG instead of the reference's NumPy stream (the "
+                "values do not change the work); per-client sample counts Dirichlet(1.0), min 10, "
+                "bit-exact with fedsim.partition",
         "config": {"workload": "C2: FedAvg 2-layer CNN (P=1,690,046), 3400 clients, 1000 per round, "
                                "bs=20, E=1, lr=0.05, PARROT greedy schedule over the GPUs",
                    "clients_per_round": M_ROUND, "total_clients": M_TOTAL,
@@ -391,13 +407,18 @@ def run_b200(args) -> dict:
         out["state_store"] = state
     if c4 is not None:
         out["c4_resnet"] = c4
+    if c13 is not None:
+        out["c1_c3_lr"] = c13
     if rank == 0 and args.cpu_baseline and world == 1:
-        v, info = cpu_sample_rounds_per_s(sizes)
+        sel = round_selection(0)
+        v, info = cpu_sample_rounds_per_s(sizes, sel, stride=4)
         out["cpu_baseline"] = {"value": v, "unit": "rounds/s", "cores": info["threads"],
                                "kind": "port",
-                               "sample": f"{info['clients']} clients' full local runs "
-                                         f"({info['samples']} samples, {info['seconds']:.1f} s, "
-                                         f"torch CPU fp32 oracle port) extrapolated to a 1000-client round"}
+                               "sample": f"stratified quarter of round 0: every 4th of its 1000 clients "
+                                         f"by sample count ({info['clients']} clients, {info['samples']} of "
+                                         f"{info['round_samples']} samples, full local runs, "
+                                         f"{info['seconds']:.1f} s), torch CPU fp32 oracle port (the "
+                                         f"reference has no CNN), scaled by the round's samples"}
     return out if rank == 0 else None
 
 
@@ -649,31 +670,171 @@ def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# configs 1 and 3 (the reference's own LR model): GPU rounds next to the
+# REFERENCE package itself (fedsim 0.1.0 installed under baseline/_ref) timed
+# on this box's host cores in a child process
+# ---------------------------------------------------------------------------
+C13_ROUNDS = 12
+
+
+def _lr_worlds(mod):
+    """C1 and C3 inputs from a package exposing the fedsim API (the reference
+    itself, or this package, whose generate/partition are bit-exact with it:
+    tests/test_host_parity.py)."""
+    ds = mod.generate(60000, 784, 10, seed=0)
+    ev = mod.generate(10000, 784, 10, seed=0, sample_set=1)
+    c1 = mod.partition(ds, 100, mod.PartitionSpec(), seed=0)
+    c3 = mod.partition(ds, 1000, mod.PartitionSpec(quantity_skew=0.5, min_samples_per_client=5), seed=0)
+    return ev, c1, c3
+
+
+def _c13_engines(mod, ev, c1, c3, rounds, store):
+    cfg1 = mod.SimConfig(total_clients=100, concurrent_clients=10, num_devices=1, total_rounds=rounds,
+                         seed=0, scheme="SP")
+    cfg3 = mod.SimConfig(total_clients=1000, concurrent_clients=100, num_devices=8, total_rounds=rounds,
+                         seed=0, scheme="PARROT")
+    hetero = [0.1 * k for k in range(8)]
+    e1 = mod.SimulationEngine(cfg1, mod.FedAvg(lr=0.1, batch_size=20), c1, mod.make_device_models(1),
+                              eval_data=ev)
+    e3 = mod.SimulationEngine(cfg3, mod.Scaffold(lr=0.05, batch_size=20, client_fraction=0.1), c3,
+                              mod.make_device_models(8, hetero=hetero), store=store, eval_data=ev)
+    return e1, e3
+
+
+def reference_c13_child() -> None:
+    """Child process (OPENBLAS_NUM_THREADS=1, NUMBA_CACHE_DIR set): the
+    reference engine on C1 (SP, K=1) and C3 (PARROT, K=8 device threads,
+    SCAFFOLD with its fsynced file StateStore); median of 3 x C13_ROUNDS
+    rounds after 2 warm-up rounds and warm_jit."""
+    import tempfile
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    import fedsim
+    from fedsim.schedule import warm_jit
+    warm_jit()
+    ev, c1, c3 = _lr_worlds(fedsim)
+    out = {"fedsim": fedsim.__file__, "cores": os.cpu_count()}
+    with tempfile.TemporaryDirectory() as root:
+        e1, e3 = _c13_engines(fedsim, ev, c1, c3, 2 + 3 * C13_ROUNDS, fedsim.StateStore(root))
+        for name, eng in (("c1", e1), ("c3", e3)):
+            eng.run(2)
+            rates = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                eng.run(C13_ROUNDS)
+                rates.append(C13_ROUNDS / (time.perf_counter() - t0))
+            out[name] = float(np.median(rates))
+    print(json.dumps(out), flush=True)
+
+
+def reference_c13() -> dict:
+    ref = ROOT / "baseline" / "_ref" / "fedsim"
+    if not ref.exists():
+        return {"unavailable": "baseline/_ref (the reference package) is not installed"}
+    import tempfile
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMBA_CACHE_DIR=tempfile.mkdtemp(prefix="numba_"))
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--_ref_c13"], capture_output=True,
+                         text=True, env=env, timeout=900)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    if res.returncode != 0 or not lines:
+        return {"unavailable": f"reference child failed rc={res.returncode}: {res.stderr[-300:]}"}
+    return json.loads(lines[-1])
+
+
+def _time_lr_engine(eng, r0: int, rounds: int) -> dict:
+    """Device-timed rounds (inputs prepared and resident) and end-to-end
+    rounds through run_round (host preparation, copies, result reads)."""
+    import torch
+    for r in range(r0, r0 + 2):
+        eng.run_round(r)
+    r0 += 2
+    prepared = [eng.prepare_round(r0 + i) for i in range(rounds)]
+    for p in prepared:
+        p.upload()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for p in prepared:
+        eng.execute_round(p, sync=False)
+    b.record()
+    torch.cuda.synchronize()
+    dev_ms = a.elapsed_time(b)
+    r0 += rounds
+    eng.run_round(r0)
+    r0 += 1
+    h0, d0 = eng.io_bytes()
+    t0 = time.perf_counter()
+    for i in range(rounds):
+        eng.run_round(r0 + i)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h1, d1 = eng.io_bytes()
+    return {"rounds_per_s": rounds / (dev_ms / 1e3), "e2e_rounds_per_s": rounds / e2e_s,
+            "h2d_bytes_per_round": int((h1 - h0) / rounds), "d2h_bytes_per_round": int((d1 - d0) / rounds)}
+
+
+def lr_configs_bench(dev) -> dict:
+    """C1 (FedAvg LR, 100 clients, 10 per round, SP K=1) and C3 (SCAFFOLD LR,
+    1000 clients, 100 per round, PARROT over 8 simulated devices, HBM state
+    store) on one GPU, with the evaluation of every round as in the
+    reference, beside the reference engine itself on the host cores."""
+    import paper_2303_01778_b200 as pb
+    ev, c1, c3 = _lr_worlds(pb)
+    rounds = 6 + 2 * C13_ROUNDS
+    e1, e3 = _c13_engines(pb, ev, c1, c3, rounds, pb.StateStore())
+    out = {"c1": {"workload": "C1: FedAvg LR 784x10, 100 clients, 10 per round, bs 20, E 1, "
+                              "lr 0.1, SP K=1, eval 10k every round", **_time_lr_engine(e1, 0, C13_ROUNDS)},
+           "c3": {"workload": "C3: SCAFFOLD LR 784x10, 1000 clients (quantity skew 0.5), 100 per round, "
+                              "bs 20, lr 0.05, PARROT K=8 simulated devices (hetero 0..0.7) on one GPU, "
+                              "HBM state store (reference: fsynced files), eval every round",
+                  **_time_lr_engine(e3, 0, C13_ROUNDS)}}
+    ref = reference_c13()
+    out["reference"] = ref
+    for k in ("c1", "c3"):
+        if k in ref:
+            out[k]["reference_rounds_per_s"] = ref[k]
+            out[k]["e2e_vs_reference"] = out[k]["e2e_rounds_per_s"] / ref[k]
+    return out
+
+
+# ---------------------------------------------------------------------------
 # the reference (CPU oracle port) arm
 # ---------------------------------------------------------------------------
 
 def run_reference(args) -> dict | None:
+    """The reference arm: the reference has no CNN and no compiled path, so
+    C2's CPU implementation is the torch CPU fp32 oracle port
+    (oracle/cnn_oracle.py, a restatement of client_execute) on all host
+    threads.  Step i times stratum i mod 32 of round 0's clients sorted by
+    sample count (about 31 clients spanning the size distribution, full local
+    runs), scaled to the round's samples; value = the median over steps."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     import torch
     sizes = client_sizes()
-    vals = []
-    for _ in range(args.warmup):
-        cpu_sample_rounds_per_s(sizes, n_clients=1)
+    sel = round_selection(0)
+    vals, secs = [], 0.0
+    for i in range(args.warmup):
+        cpu_sample_rounds_per_s(sizes, sel, stride=32, offset=(7 * i + 3) % 32)
     for i in range(args.steps):
-        v, info = cpu_sample_rounds_per_s(sizes, n_clients=2)
+        v, info = cpu_sample_rounds_per_s(sizes, sel, stride=32, offset=i % 32)
         vals.append(v)
+        secs += info["seconds"]
     v = float(np.median(vals))
     return {"metric": "FL rounds/sec (1000 clients, FEMNIST-CNN)", "value": v, "unit": "rounds/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic FEMNIST-shaped", "config": {"workload": "C2 (see B200 arm)"},
+            "data": "synthetic FEMNIST-shaped Gaussian mixture; client sizes = the B200 arm's "
+                    "(Dirichlet(1.0), bit-exact with fedsim.partition)",
+            "config": {"workload": "C2: FedAvg 2-layer CNN (P=1,690,046), 3400 clients, 1000 per round, "
+                                   "bs=20, E=1, lr=0.05"},
             "cpu_baseline": {"value": v, "unit": "rounds/s", "cores": torch.get_num_threads(),
                              "kind": "port",
-                             "sample": "per step: 2 clients' full local runs with the torch CPU "
-                                       "oracle port (the reference has no CNN and no compiled "
-                                       "path), extrapolated to a 1000-client round"},
+                             "sample": f"per step: one 1/32 stratum of round 0's 1000 clients by sample "
+                                       f"count (~31 clients, full local runs; {secs:.0f} s of CPU work "
+                                       f"over the {args.steps} steps), torch CPU fp32 oracle port "
+                                       f"(the reference has no CNN), scaled to the round's samples"},
             "e2e": {"value": v, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -686,7 +847,12 @@ def main():
     ap.add_argument("--no-agg", dest="agg", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-c4", dest="c4", action="store_false")
+    ap.add_argument("--no-c13", dest="c13", action="store_false")
+    ap.add_argument("--_ref_c13", dest="ref_c13", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_c13:
+        reference_c13_child()
+        return
     out = run_reference(args) if args.impl == "reference" else run_b200(args)
     if out is not None:
         print(json.dumps(out), flush=True)
