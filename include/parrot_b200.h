@@ -350,6 +350,11 @@ int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, int naccum, l
 /* The same issue loop on `grid` CTAs at once (several per SM): per-CTA
  * elapsed cycles and SM ids (device pointers; tests / DESIGN table only). */
 int pb_umma_bench_multi(int M, int N, int iters, int grid, long long* cycles, int* smid, void* stream);
+/* The conv kernels' MMA pattern on resident smem operands: `ngroups`
+ * accumulators, group g's A start g*a_goff bytes further, 8 K steps of
+ * `kstep` bytes per group, `iters` passes, on `grid` CTAs (diagnostic). */
+int pb_umma_bench2(int M, int N, int a_mn, int b_mn, uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo,
+                   uint32_t kstep, int ngroups, uint32_t a_goff, int iters, int grid, long long* cycles, void* stream);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 
 import numpy as np
-from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint64, c_void_p
+from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
 _PATH = Path(__file__).resolve().parent / "libparrot_b200.so"
@@ -109,6 +109,8 @@ _SIGS = {
     "pb_cnn_lazy_fold": (c_int, [POINTER(LazyFoldArgs), c_void_p]),
     "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
     "pb_umma_bench_multi": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "pb_umma_bench2": (c_int, [c_int, c_int, c_int, c_int, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_int,
+                               c_uint32, c_int, c_int, c_void_p, c_void_p]),
     "pb_tma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "pb_tma_bw_probe": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "pb_tma_bf16_mn_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,

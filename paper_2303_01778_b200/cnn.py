@@ -30,7 +30,9 @@ class _Workspace:
             torch.cuda.empty_cache()
             self.slots, self.bs = max(slots, self.slots), max(bs, self.bs)
             n = self.slots * self.bs
-            self.buf = {k: torch.empty(n * v, dtype=torch.uint8, device=device)
+            # one plane (5392 B) of slack: the conv kernels' TMA views of
+            # the p1 / dz2 planes may read a few rows past the last plane
+            self.buf = {k: torch.empty(n * v + 5392, dtype=torch.uint8, device=device)
                         for k, v in _PER_SAMPLE.items()}
             self.buf["slots"] = torch.empty(self.slots * 32, dtype=torch.uint8, device=device)
             self.buf["dht"] = torch.empty(self.slots * 512 * 32 * 4, dtype=torch.uint8, device=device)

@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "cnn_common.cuh"
+#include "tma.cuh"
 
 namespace {
 
@@ -1181,51 +1182,65 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
 }
 
 // ---------------------------------------------------------------------------
-// k_wgrad: y<2: conv2 wgrad for taps [13y, 13y+13) on tcgen05 + update;
-//          y==2: conv1 wgrad + conv1/conv2 bias grads (SIMT) + update
-// grid (3, active), 256 threads
+// k_wgrad: conv2 weight gradient on tcgen05 with M = 128, operands by TMA.
+//   D[(kxl, ci)][co] += sum_p p1[p + ky*18 + kx0 + kxl][ci] * dz2[p + 38][co]
+// over the output positions p (K, 16 per MMA) of every sample of the client.
+// A (M = 128, MN-major) is 16 planes at one uniform stride: the client's 4 p1
+// planes (ci blocks) and three copies of them shifted up by kxl = 1, 2, 3
+// rows, so M-core j = (kxl = j / 4, ci block j % 4), lane m = kxl*32 + ci,
+// and one MMA covers the four horizontally adjacent filter taps (ky, kx0 ..
+// kx0 + 3); the tap's row offset is a 16 B start-address advance.  B (N = 64
+// co, MN-major) is the 8 dz2 planes.  A "group" is (ky, kx0), kx0 in {0, 4}:
+// kx0 = 0 covers taps kx 0-3, kx0 = 4 tap 4 (its other 96 lanes unused), so
+// 10 MMAs per K step cover the 25 taps (the previous M = 64 form issued 15).
+// Every MMA with N <= 64 costs the same ~52 cycles (tools/umma_bench2.py),
+// so the instruction count is what matters.
+// Staging, per (sample, K half) chunk of 128 positions: ONE TMA box brings
+// the 4 p1 planes (a view whose 128 B inner rows are 8 plane rows: 22 rows
+// per plane, any start row), one box the 8 dz2 planes; warps 1-7 then build
+// the three shifted copies in shared memory (L2 reads 27 KB per chunk
+// instead of 61), and thread 0 issues the MMAs: a 3-stage ring with
+// full (TMA) -> ready (copies) -> empty (MMAs) barriers.  The accumulators
+// stay in TMEM over the client's samples.
 // ---------------------------------------------------------------------------
-// One staged sample: the p1 planes, the same planes shifted by one grid row
-// (so that horizontally adjacent taps (ky, kx), (ky, kx+1) form ONE N=64 MMA:
-// N-groups 0-3 read tap kx, N-groups 4-7 tap kx+1 at a uniform plane stride)
-// and the dz2 planes.
-constexpr int kWgP1 = 2 * kP1Bytes;             // 8 planes: shift 0, shift 1
-constexpr int kWgBuf = kWgP1 + kDzBytes;        // 86,016 B
-constexpr size_t kWgSmem = 2 * kWgBuf;          // double-buffered
-// filter rows per CTA: head sweeps 2 CTAs (ky 0-2 | 3-4); tail sweeps (few
-// clients) one CTA per ky row, so each client's MMA chain is 5x shorter
-constexpr int kWgTailActive = 60;
-constexpr int kWgStride = 15 * 32 + 1;          // fp32 row of the gradient tile (epilogue)
+constexpr int kWgKH = 128;                      // output positions per chunk (8 K steps)
+constexpr int kWgRH = 176;                      // p1 rows per plane and chunk: 128 + 2*18 + 4 + 3, in 8s
+constexpr int kWgPS = kWgRH * 16;               // A plane stride (2816 B)
+constexpr int kWgBS = kWgKH * 16;               // B plane stride (2048 B)
+constexpr int kWgABytes = 16 * kWgPS;           // 4 copies x 4 planes
+constexpr int kWgBBytes = 8 * kWgBS;            // 8 dz2 planes
+constexpr int kWgStage = kWgABytes + kWgBBytes; // 61,440 B
+constexpr int kWgLoad = 4 * kWgPS + kWgBBytes;  // TMA bytes per chunk (base planes + dz2)
+constexpr int kWgStages = 3;
+constexpr size_t kWgSmem = size_t(kWgStages) * kWgStage + 128;
+constexpr int kWgTailActive = 60;               // below: one CTA per filter row (5-way split)
+constexpr int kWgStride = 15 * 32 + 4;          // fp32 row of the gradient tile (epilogue, float4 rows)
+constexpr int kWgCopyRows = kWgRH - 8;          // rows of a shifted copy the MMAs read (<= 168)
+static_assert(64 * kWgStride * 4 <= kWgStages * kWgStage, "k_wgrad epilogue tile");
+static_assert(kWgABytes % 128 == 0 && kWgStage % 128 == 0 && kWgPS % 128 == 0, "TMA destinations 128 B aligned");
+static_assert(kWgCopyRows >= kWgKH + 40 && kWgCopyRows + 3 <= kWgRH, "shifted copies");
 
-__device__ __forceinline__ void wg_stage(const Args& a, int64_t sid, uint8_t* buf, int tid) {
-  const uint8_t* s1 = a.p1g + sid * kP1Bytes;
-  const uint8_t* s2 = a.dzg + sid * kDzBytes;
-  for (int e = tid; e < kP1Bytes / 16; e += 256) cp_async16(buf + e * 16, s1 + e * 16);
-  for (int e = tid; e < kP1Bytes / 16; e += 256) {   // plane c row r <- p1 plane c row r+1
-    const bool v = (e % kRows) + 1 < kRows;
-    cp_async16_zfill(buf + kP1Bytes + e * 16, s1 + (v ? (e + 1) * 16 : 0), v);
-  }
-  for (int e = tid; e < kDzBytes / 16; e += 256) cp_async16(buf + kWgP1 + e * 16, s2 + e * 16);
-  cp_async_commit();
-}
+struct ConvMaps {
+  CUtensorMap p1;   // p1 planes as {8 rows x 8 ci (128 B), row groups, samples*4 planes}: box {64, 22, 4}
+  CUtensorMap dz;   // dz2 planes, same view: box {64, 16, 8}
+};
 
-// k_wgrad: x < nsplit: conv2 wgrad for the taps of its filter rows ky on
-//          tcgen05 (M=64 co x N=64 (two taps x 32 ci) / N=32 (kx = 4), K =
-//          output positions; double-buffered sample staging overlaps the
-//          MMAs) + update;
-//          x == nsplit: sum the per-sample conv1/bias partials (sample order) + update
-// Sparse sweeps split each client's samples over a cluster of sg CTAs per
-// split: every CTA computes the partial gradient of its samples, then CTA r
-// sums the sg partials (cluster rank order, distributed shared memory) for
-// its share of the co rows and applies the update.
-// grid ((nsplit + 1) * sg, active), cluster (sg, 1, 1), 256 threads;
-// nsplit = 2 (ky 0-2 | 3-4) or 5
-__global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit, int sg) {
+// k_wgrad: CTA x: conv2 wgrad for the groups [10x/nsplit, 10(x+1)/nsplit)
+// (nsplit = 2: taps 0-13 | 14-24; nsplit = 5: one filter row) + update; its
+// copy warps also sum a share of the per-sample conv1/bias partials (sample
+// order) + update.  Sparse sweeps split each client's samples over a cluster
+// of sg CTAs per split: every CTA computes the partial gradient of its
+// samples, then CTA r sums the sg partials (cluster rank order, distributed
+// shared memory) for its share of the co rows and applies the update.
+// grid (nsplit * sg, active), cluster (sg, 1, 1), 256 threads
+__global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant__ ConvMaps maps, int nsplit,
+                                                  int sg) {
   pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.y];
   if (sl.cnt == 0) return;   // uniform over a cluster (same slot)
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t full[kWgStages], ready[kWgStages], empty[kWgStages];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int split = blockIdx.x / sg, rank = blockIdx.x - split * sg;
@@ -1233,85 +1248,121 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit, int sg) {
   const int cnt = i_hi - i_lo;
   float* W = a.w + int64_t(sl.r) * a.P;
   const int64_t s0 = sidx(blockIdx.y, 0, a.BS);
-  if (split == nsplit) {
-    for (int k = rank * kPg / sg + tid; k < (rank + 1) * kPg / sg; k += 256) {
+  // conv1 weights/bias + conv2 bias: sum of the per-sample partials (sample
+  // order), outputs [q*kPg/nq, (q+1)*kPg/nq) of CTA q of the client; run by
+  // the copy warps (tid >= 32) while thread 0 drives the first chunks
+  auto conv1_update = [&]() {
+    const int nq = nsplit * sg, q = split * sg + rank;
+    for (int k = q * kPg / nq + tid - 32; k < (q + 1) * kPg / nq; k += 224) {
       float g = 0.0f;
 #pragma unroll 8
       for (int i = 0; i < sl.cnt; ++i) g += a.pg[(s0 + i) * kPg + k];
       const int64_t idx = k < 800 ? oC1W + k : (k < 832 ? oC1B + (k - 800) : oC2B + (k - 832));
       W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
-    return;
-  }
-  const int ky0 = nsplit == 2 ? split * 3 : split;
-  const int nky = nsplit == 2 ? (split == 0 ? 3 : 2) : 1;
-  const int tap0 = ky0 * 5, ntap = nky * 5;
+  };
+  // groups G = 2*ky + (kx0 / 4) of this CTA; taps [tap0, tap0 + ntap)
+  const int g_lo = 10 * split / nsplit, g_hi = 10 * (split + 1) / nsplit, ng = g_hi - g_lo;
+  const int kyb = g_lo >> 1;                         // first filter row: A starts there
+  const int tap0 = (g_lo >> 1) * 5 + (g_lo & 1) * 4;
+  const int tap1 = ((g_hi - 1) >> 1) * 5 + ((g_hi - 1) & 1 ? 5 : 4);
+  const int ntap = tap1 - tap0;
   if (warp == 0) tmem_alloc<512>(&tmem_base);
+  if (warp == 1) {   // this CTA's W2 row segments -> L2 for the epilogue (the rows are cold)
+    for (int co = rank * 64 / sg + lane; co < (rank + 1) * 64 / sg; co += 32)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(W + oC2W + int64_t(co) * 800 + tap0 * 32),
+                   "r"(uint32_t(ntap * 128))
+                   : "memory");
+  }
   if (tid == 0) {
-    mbar_init(&mbar, 1);
+    pb::tma::prefetch(&maps.p1);
+    pb::tma::prefetch(&maps.dz);
+    for (int i = 0; i < kWgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&ready[i], 7);   // one arrive per copy warp
+      mbar_init(&empty[i], 1);
+    }
     fence_init();
   }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t idesc64 = idesc_bf16(64, 64, true, true);
-  const uint32_t idesc32 = idesc_bf16(64, 32, true, true);
-  if (cnt > 0) wg_stage(a, s0 + i_lo, smem, tid);
-  for (int i = 0; i < cnt; ++i) {
-    uint8_t* buf = smem + (i & 1) * kWgBuf;
-    if (i + 1 < cnt) {
-      if (i >= 1) mbar_wait(&mbar, (i - 1) & 1);  // MMAs of sample i-1 read the other buffer
-      wg_stage(a, s0 + i_lo + i + 1, smem + ((i + 1) & 1) * kWgBuf, tid);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+  const int n = 2 * cnt;   // chunks: (sample, K half)
+  if (tid == 0 && n > 0) {
+    const uint32_t idesc = idesc_bf16(128, 64, true, true);
+    auto issue = [&](int c, uint8_t* st, uint64_t* f) {
+      const int sid = int(s0 + i_lo + (c >> 1)), h = c & 1;
+      pb::tma::expect_tx(f, uint32_t(kWgLoad));
+      pb::tma::load_3d(st, &maps.p1, 8 * (h * kWgKH + kyb * kG), 0, sid * 4, f);
+      pb::tma::load_3d(st + kWgABytes, &maps.dz, 8 * (2 * kG + 2 + h * kWgKH), 0, sid * 8, f);
+    };
+    for (int c = 0; c < n && c < kWgStages; ++c) issue(c, smem + c * kWgStage, &full[c]);
+    for (int c = 0; c < n; ++c) {
+      const int stg = c % kWgStages;
+      uint8_t* st = smem + stg * kWgStage;
+      mbar_wait(&ready[stg], (c / kWgStages) & 1);
       fence_after_sync();
-      // A[co][p] = dz2 plane row p + 2*18 + 2 (MN-major); B[(tap, ci)][p] =
-      // p1 (shift-0 / shift-1 copies) row p + ky*18 + kx
-      const uint64_t a0 = desc(smem_u32(buf) + kWgP1, 128, kPlane) + uint64_t(2 * kG + 2);
-      const uint64_t b00 = desc(smem_u32(buf), 128, kPlane);
+      const uint32_t sa = smem_u32(st), sb = sa + kWgABytes;
+      const uint64_t b0 = desc(sb, 128, kWgBS);
 #pragma unroll 1
-      for (int yy = 0; yy < nky; ++yy) {
-        const int ky = ky0 + yy;
+      for (int g = 0; g < ng; ++g) {
+        const int G = g_lo + g, off = ((G >> 1) - kyb) * kG + (G & 1) * 4;
+        const uint64_t a0 = desc(sa + off * 16, 128, kWgPS);
 #pragma unroll
-        for (int kx = 0; kx < 5; kx += 2) {
-          const int tl = yy * 5 + kx;
-          const uint64_t b0 = b00 + uint64_t(ky * kG + kx);
-#pragma unroll
-          for (int ks = 0; ks < 16; ++ks)
-            mma_bf16(tmem + tl * 32, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), kx < 4 ? idesc64 : idesc32,
-                     i > 0 || ks > 0);
-        }
+        for (int ks = 0; ks < kWgKH / 16; ++ks)
+          mma_bf16(tmem + g * 64, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), idesc, c > 0 || ks > 0);
       }
-      commit(&mbar);
+      commit(&empty[stg]);
+      const int nx = c - 1 + kWgStages;   // refill the stage of chunk c-1
+      if (c >= 1 && nx < n) {
+        const int s2 = (c - 1) % kWgStages;
+        mbar_wait(&empty[s2], ((c - 1) / kWgStages) & 1);
+        issue(nx, smem + s2 * kWgStage, &full[s2]);
+      }
     }
+    mbar_wait(&empty[(n - 1) % kWgStages], ((n - 1) / kWgStages) & 1);
+  } else if (warp >= 1) {
+    // copy warps: plane (kxl, cb) row r <- base plane cb row r + kxl
+    const int ct = tid - 32;
+    for (int c = 0; c < n; ++c) {
+      const int stg = c % kWgStages;
+      uint8_t* st = smem + stg * kWgStage;
+      mbar_wait(&full[stg], (c / kWgStages) & 1);
+      constexpr int kUnits = 3 * 4 * kWgCopyRows;
+      for (int u = ct; u < kUnits; u += 224) {
+        const int r = u % kWgCopyRows, pc = u / kWgCopyRows, kxl = 1 + (pc >> 2), cb = pc & 3;
+        *reinterpret_cast<uint4*>(st + (kxl * 4 + cb) * kWgPS + r * 16) =
+            *reinterpret_cast<const uint4*>(st + cb * kWgPS + (r + kxl) * 16);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&ready[stg])) : "memory");
+      if (c == 0) conv1_update();
+    }
+    if (n == 0) conv1_update();
   }
-  if (cnt > 0) mbar_wait(&mbar, (cnt - 1) & 1);
+  __syncthreads();
   fence_after_sync();
-  // epilogue: TMEM (M=64 rows in lanes 32q + [0,16)) -> smem tile [64][ntap*32]
-  // -> coalesced SGD update of the contiguous W2[co][tap0*32 ...] row segments
-  float* sG = reinterpret_cast<float*>(smem);  // 64 x 481 fp32 = 123 KB (buffers are free)
+  // epilogue: TMEM lane kxl*32 + ci, column g*64 + co -> smem tile
+  // sG[co][(tap - tap0)*32 + ci] -> coalesced SGD update of W2[co][tap0*32 ...]
+  float* sG = reinterpret_cast<float*>(smem);   // 64 x 481 fp32 (the ring is idle)
   const int width = ntap * 32;
   {
-    const int q = warp & 3, part = warp >> 2;
-    const int co = q * 16 + lane;
+    const int q = warp & 3, half = warp >> 2;
 #pragma unroll 1
-    for (int tl = part; tl < ntap; tl += 2) {
-      float v[16];
+    for (int g = 0; g < ng; ++g) {
+      const int G = g_lo + g, kx = (G & 1) * 4 + q;
+      if (kx > 4) continue;   // warp-uniform
+      const int tl = (G >> 1) * 5 + kx - tap0;
 #pragma unroll
       for (int c16 = 0; c16 < 2; ++c16) {
-        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(tl * 32 + c16 * 16), v);
-        if (cnt == 0)
+        float v[16];
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(g * 64 + half * 32 + c16 * 16), v);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = 0.0f;
-        if (lane < 16) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) sG[co * kWgStride + tl * 32 + c16 * 16 + k] = v[k];
+        for (int k = 0; k < 16; ++k) {
+          const int co = half * 32 + c16 * 16 + k;
+          sG[co * kWgStride + tl * 32 + lane] = cnt > 0 ? v[k] : 0.0f;
         }
       }
     }
@@ -1323,31 +1374,49 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, int nsplit, int sg) {
   // partial tiles in rank order
   namespace cgp = cooperative_groups;
   if (sg > 1) cgp::this_cluster().sync();
-  const int co_lo = rank * 64 / sg, n_e = ((rank + 1) * 64 / sg - co_lo) * width;
-  for (int e0 = tid; e0 < n_e; e0 += 8 * 256) {
-    float wv[8];
+  // FedAvg / plain SGD, no cluster: float4 units, 16 loads in flight per
+  // thread (the rows were prefetched to L2), compact straight-line code
+  const int co_lo = rank * 64 / sg, w4 = width >> 2, n_u = ((rank + 1) * 64 / sg - co_lo) * w4;
+  const bool plain = a.mu == 0.0f && a.ctrl_g == nullptr && a.ctrl_c == nullptr;
+  if (plain && sg == 1) {
+    const float nlr = -a.lr;
+    for (int u0 = tid; u0 < n_u; u0 += 16 * 256) {
+      float4 wv[16];
+      int64_t off[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = e0 + k * 256;
-      if (e < n_e) {
-        const int co = co_lo + e / width, c = e % width;
-        wv[k] = W[oC2W + int64_t(co) * 800 + tap0 * 32 + c];
+      for (int k = 0; k < 16; ++k) {
+        const int u = min(u0 + k * 256, n_u - 1), co = co_lo + u / w4, c4 = u - (u / w4) * w4;
+        off[k] = int64_t(co) * 800 + c4 * 4;
+        wv[k] = *reinterpret_cast<const float4*>(W + oC2W + tap0 * 32 + off[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (u0 + k * 256 < n_u) {
+          const int co = int(off[k] / 800), c = int(off[k] - int64_t(co) * 800);
+          const float4 g = *reinterpret_cast<const float4*>(sG + co * kWgStride + c);
+          float4 w = wv[k];
+          w.x = fmaf(nlr, g.x, w.x);
+          w.y = fmaf(nlr, g.y, w.y);
+          w.z = fmaf(nlr, g.z, w.z);
+          w.w = fmaf(nlr, g.w, w.w);
+          *reinterpret_cast<float4*>(W + oC2W + tap0 * 32 + off[k]) = w;
+        }
       }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = e0 + k * 256;
-      if (e < n_e) {
-        const int co = co_lo + e / width, c = e % width;
-        const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
-        float g = sG[co * kWgStride + c];
-        if (sg > 1) {
-          cgp::cluster_group cl = cgp::this_cluster();
-          g = cl.map_shared_rank(sG, 0)[co * kWgStride + c];
-          for (int q = 1; q < sg; ++q) g += cl.map_shared_rank(sG, q)[co * kWgStride + c];
-        }
-        W[idx] = sgd(a, sl.r, idx, wv[k], g);
+  } else {
+    // plugin terms and / or the cluster sum of partial tiles (rank order)
+    namespace cgp = cooperative_groups;
+#pragma unroll 1
+    for (int e = tid; e < n_u * 4; e += 256) {
+      const int co = co_lo + e / width, c = e % width;
+      const int64_t idx = oC2W + int64_t(co) * 800 + tap0 * 32 + c;
+      float g = sG[co * kWgStride + c];
+      if (sg > 1) {
+        cgp::cluster_group cl = cgp::this_cluster();
+        g = cl.map_shared_rank(sG, 0)[co * kWgStride + c];
+        for (int q = 1; q < sg; ++q) g += cl.map_shared_rank(sG, q)[co * kWgStride + c];
       }
+      W[idx] = sgd(a, sl.r, idx, W[idx], g);
     }
   }
   if (sg > 1) cgp::this_cluster().sync();   // partner tiles stay alive until every read is done
@@ -1400,6 +1469,23 @@ static Args to_args(const pb_cnn_train_args& t) {
   return a;
 }
 
+// TMA maps of the per-sample conv planes (p1, dz2) of a group's workspace
+static int conv_maps(const Args& a, int64_t slots, ConvMaps* m) {
+  const uint64_t ns = uint64_t(slots) * uint64_t(a.BS);
+  // view of a plane whose 128 B inner rows are 8 consecutive plane rows (any
+  // start row: the inner coordinate is 8 x the row); a box of G groups reads
+  // rows [row, row + 8G).  Boxes may run past the 337 plane rows into the
+  // next plane (never read by the MMAs); the workspace keeps one plane of
+  // slack at the end (cnn.py), so they never leave the allocation.
+  const uint64_t dp[3] = {uint64_t(kRows) * 8, uint64_t(kRows) / 8 + 1, ns * 4}, sp[2] = {128, uint64_t(kPlane)};
+  const uint32_t bp[3] = {64, uint32_t(kWgRH / 8), 4};
+  const uint64_t dd[3] = {uint64_t(kRows) * 8, uint64_t(kRows) / 8 + 1, ns * 8};
+  const uint32_t bd[3] = {64, uint32_t(kWgKH / 8), 8};
+  int rc;
+  if ((rc = pb::tma::make_nd_bf16_plain(&m->p1, a.p1g, 3, dp, sp, bp))) return rc;
+  return pb::tma::make_nd_bf16_plain(&m->dz, a.dzg, 3, dd, sp, bd);
+}
+
 static size_t head_smem(int C, int BS) { return size_t(BS * kH1 + BS * kDHS + BS * pad4(C)) * 4; }
 
 // active-client thresholds below which a sweep uses the cluster head and the
@@ -1414,7 +1500,7 @@ static void tail_thresholds(int* head, int* wg) {
   *wg = th[1];
 }
 
-static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream_t s) {
+static int launch_sweep(Args& a, const ConvMaps* maps, int active, bool train, int max_spb, cudaStream_t s) {
   int head_thr, wg_thr;
   tail_thresholds(&head_thr, &wg_thr);
   // samples per CTA of the per-sample conv kernels: enough CTAs to fill the
@@ -1461,12 +1547,12 @@ static int launch_sweep(Args& a, int active, bool train, int max_spb, cudaStream
   const int wsplit = active < wg_thr ? 5 : 2;
   // sparse sweeps: split each client's samples over a cluster while the grid
   // still fits one wave
-  const int wsg = wsplit == 5 ? std::max(1, std::min(4, sms / ((wsplit + 1) * active))) : 1;
+  const int wsg = wsplit == 5 ? std::max(1, std::min(4, sms / (wsplit * active))) : 1;
   if (wsg == 1) {
-    pb::launch_pdl(k_wgrad, dim3(wsplit + 1, active), dim3(256), kWgSmem, s, 1, a, wsplit, 1);
+    pb::launch_pdl(k_wgrad, dim3(wsplit, active), dim3(256), kWgSmem, s, 1, a, *maps, wsplit, 1);
   } else {
-    pb::launch_pdl(k_wgrad, dim3(unsigned((wsplit + 1) * wsg), unsigned(active)), dim3(256), kWgSmem, s,
-                   unsigned(wsg), a, wsplit, wsg);
+    pb::launch_pdl(k_wgrad, dim3(unsigned(wsplit * wsg), unsigned(active)), dim3(256), kWgSmem, s,
+                   unsigned(wsg), a, *maps, wsplit, wsg);
   }
   pb::prof_end(pb::K_CNN_WGRAD, s);
   return pb::check_launch("cnn train sweep");
@@ -1484,6 +1570,8 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   int rc = cnn_setup();
   if (rc) return rc;
   Args a = to_args(t);
+  ConvMaps maps;
+  if ((rc = conv_maps(a, t.g, &maps))) return rc;
   cudaStream_t s = pb::as_stream(stream);
   const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
   if (a.hx) {
@@ -1504,7 +1592,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     pb::prof_begin(pb::K_CNN_SLOTS, s);
     pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
     pb::prof_end(pb::K_CNN_SLOTS, s);
-    if ((rc = launch_sweep(a, active, true, spb, s))) break;
+    if ((rc = launch_sweep(a, &maps, active, true, spb, s))) break;
     if (a.timeline && (step + 1 == t.sweeps || t.active[step + 1] <= 0))
       pb::stamp(a.timeline + step + 1, s);
   }
@@ -1539,7 +1627,7 @@ extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* 
       host[size_t(j)] = Slot{0, int32_t(std::min<int64_t>(t.BS, rows - first)), first};
     }
     cudaMemcpyAsync(a.slots, host.data(), sizeof(Slot) * size_t(active), cudaMemcpyHostToDevice, s);
-    if ((rc = launch_sweep(a, active, false, t.samples_per_cta > 0 ? t.samples_per_cta : 10, s)))
+    if ((rc = launch_sweep(a, nullptr, active, false, t.samples_per_cta > 0 ? t.samples_per_cta : 10, s)))
       return rc;
     cudaStreamSynchronize(s);  // host slot table is reused
   }

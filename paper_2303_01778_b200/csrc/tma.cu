@@ -87,6 +87,31 @@ int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* d
   return PB_OK;
 }
 
+int make_nd_bf16_plain(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                       const uint32_t* box) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (rank < 2 || rank > 5 || (reinterpret_cast<uintptr_t>(base) & 15) || (box[0] * 2) % 16)
+    return fail(PB_ERR_INVALID, "make_nd_bf16_plain: bad rank, alignment or box");
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i > 0) {
+      st[i - 1] = strides[i - 1];
+      if (strides[i - 1] % 16) return fail(PB_ERR_INVALID, "make_nd_bf16_plain: stride not a multiple of 16");
+    }
+  }
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cuuint32_t(rank), const_cast<void*>(base), d, st, b,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 plain view) failed: " + std::to_string(int(r)));
+  return PB_OK;
+}
+
 }  // namespace tma
 }  // namespace pb
 

@@ -50,6 +50,15 @@ __device__ __forceinline__ void load_3d(void* dst, const CUtensorMap* map, int c
       : "memory");
 }
 
+__device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                        uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+          umma::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(umma::smem_u32(mbar))
+      : "memory");
+}
+
 __device__ __forceinline__ void load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
                                         uint64_t* mbar) {
   asm volatile(
@@ -149,6 +158,14 @@ int make_nd_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* di
 // along a dimension the box spans box[i] elements of which every e-th loads.
 int make_nd_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                  const uint32_t* box, const uint32_t* estr = nullptr);
+
+// N-D bf16 tensor map without swizzle (box inner dimension a multiple of 8
+// elements); strides may overlap (views where two dimensions step through the
+// same rows).  A box lands densely in shared memory, [dim rank-1]...[dim 0]:
+// the "plane" operands of the conv kernels (rows 16 B apart = the canonical
+// SWIZZLE_NONE core-matrix rows).
+int make_nd_bf16_plain(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                       const uint32_t* box);
 
 }  // namespace tma
 }  // namespace pb

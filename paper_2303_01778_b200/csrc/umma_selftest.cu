@@ -342,3 +342,68 @@ extern "C" int pb_umma_tf32_probe(const float* A, const float* B, float* D, cons
   umma_tf32_probe_kernel<<<1, 128, 65536 + 8192, pb::as_stream(stream)>>>(A, B, D, params);
   return pb::check_launch("pb_umma_tf32_probe");
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic: the conv kernels' MMA issue pattern on resident smem operands.
+// `ngroups` accumulators (N columns each), group g's A start advanced by
+// g*a_goff bytes, 8 K steps per group (A/B advance kstep bytes per K step),
+// `iters` passes.  Reports cycles from first issue to completion (tests and
+// tools/umma_bench.py only).
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128) umma_bench2_kernel(int M, int N, int a_mn, int b_mn, uint32_t a_lbo,
+                                                          uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo,
+                                                          uint32_t kstep, int ngroups, uint32_t a_goff,
+                                                          int iters, int smem_bytes, long long* cycles) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < smem_bytes / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0x3f803f80u);
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    const uint32_t a0 = smem_u32(smem), b0 = a0 + uint32_t(smem_bytes / 2);
+    const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    const uint64_t bd = desc(b0, b_lbo, b_sbo);
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it)
+#pragma unroll 1
+      for (int g = 0; g < ngroups; ++g) {
+        const uint64_t ad = desc(a0 + uint32_t(g) * a_goff, a_lbo, a_sbo);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16(tbase + uint32_t(g * N), ad + uint64_t(ks * (kstep >> 4)), bd + uint64_t(ks * (kstep >> 4)), idesc,
+                   it > 0 || ks > 0);
+      }
+    commit(&mbar);
+    mbar_wait(&mbar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  __syncthreads();
+  if (tid != 0) mbar_wait(&mbar, 0);
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(tbase);
+}
+}  // namespace
+
+extern "C" int pb_umma_bench2(int M, int N, int a_mn, int b_mn, uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo,
+                              uint32_t b_sbo, uint32_t kstep, int ngroups, uint32_t a_goff, int iters, int grid,
+                              long long* cycles, void* stream) {
+  if (ngroups < 1 || ngroups * N > 512 || grid < 1) return pb::fail(PB_ERR_INVALID, "pb_umma_bench2: bad arguments");
+  const int smem = 200 * 1024;
+  cudaFuncSetAttribute(umma_bench2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  umma_bench2_kernel<<<grid, 128, smem, pb::as_stream(stream)>>>(M, N, a_mn, b_mn, a_lbo, a_sbo, b_lbo, b_sbo, kstep,
+                                                                 ngroups, a_goff, iters, smem, cycles);
+  return pb::check_launch("pb_umma_bench2");
+}
