@@ -352,9 +352,13 @@ int pb_umma_bench(int M, int N, int a_mode, int b_mode, int iters, int naccum, l
 int pb_umma_bench_multi(int M, int N, int iters, int grid, long long* cycles, int* smid, void* stream);
 /* The conv kernels' MMA pattern on resident smem operands: `ngroups`
  * accumulators, group g's A start g*a_goff bytes further, 8 K steps of
- * `kstep` bytes per group, `iters` passes, on `grid` CTAs (diagnostic). */
+ * `kstep` (A) / `b_kstep` (B, 0 = kstep) bytes per group, `iters` passes, on `grid` CTAs (diagnostic). */
+/* TMEM -> register load throughput: `warps` warps per CTA (148 CTAs) each read
+ * `cols` columns of their lane quarter `iters` times (diagnostic). */
+int pb_tmem_ld_bench(int warps, int cols, int iters, long long* cycles, float* sink, void* stream);
 int pb_umma_bench2(int M, int N, int a_mn, int b_mn, uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo,
-                   uint32_t kstep, int ngroups, uint32_t a_goff, int iters, int grid, long long* cycles, void* stream);
+                   uint32_t kstep, int ngroups, uint32_t a_goff, int iters, int grid, long long* cycles,
+                   uint32_t b_kstep, void* stream);
 
 #ifdef __cplusplus
 }

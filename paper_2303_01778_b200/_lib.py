@@ -109,8 +109,9 @@ _SIGS = {
     "pb_cnn_lazy_fold": (c_int, [POINTER(LazyFoldArgs), c_void_p]),
     "pb_resnet_workspace": (c_int, [c_int, c_int, POINTER(c_int64)]),
     "pb_umma_bench_multi": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "pb_tmem_ld_bench": (c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "pb_umma_bench2": (c_int, [c_int, c_int, c_int, c_int, c_uint32, c_uint32, c_uint32, c_uint32, c_uint32, c_int,
-                               c_uint32, c_int, c_int, c_void_p, c_void_p]),
+                               c_uint32, c_int, c_int, c_void_p, c_uint32, c_void_p]),
     "pb_tma_tf32_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "pb_tma_bw_probe": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "pb_tma_bf16_mn_selftest": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,

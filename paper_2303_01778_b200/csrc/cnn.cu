@@ -974,29 +974,50 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 
 // ---------------------------------------------------------------------------
 // k_bwd_conv: per sample, dz2 planes (pool2/relu backward) -> conv2 dgrad on
-// tcgen05 -> dp1 (TMEM -> smem) -> pool1/relu backward fused with the conv1
-// weight gradient and the conv1/conv2 bias gradients of this sample
-// (per-sample partials, summed in sample order by k_wgrad: deterministic).
-// Software-pipelined over the CTA's samples: the TMEM accumulators are
-// double-buffered, so the dgrad MMAs of sample i run while the CTA copies its
-// dz2 planes out and finishes sample i-1 (dp1, conv1 gradients); the pool2
-// inputs of sample i+1 stream into smem (cp.async) meanwhile.
-// grid (ceil(BS/spb), active), 512 threads
+// tcgen05 -> dp1 -> pool1/relu backward fused with the conv1 weight gradient
+// and the conv1/conv2 bias gradients of this sample (per-sample partials,
+// summed in sample order by k_wgrad: deterministic).
+//
+// dgrad MMAs, column-blocked: for filter row ky ONE N = 128 MMA multiplies
+// the dz2 planes (A, K-major over co) by the four weight tiles W[ky][kx =
+// 0..3] side by side (B, MN-major: in the UMMA weight layout the 16 (kx, ci
+// block) core-matrix columns of one filter row sit 1024 B apart), and one
+// N = 32 MMA adds tap (ky, 4) into block 3 (its A one row earlier).  Block j
+// accumulates the contribution of tap (ky, j) to output row q = p - 3 + j,
+// so the epilogue sums out[q] = D3[q] + D2[q+1] + D1[q+2] + D0[q+3] (warp
+// shuffles, a 3-row halo between lane quarters).  Every MMA with N <= 64
+// costs the same ~52 cycles (tools/umma_bench2.py): 40 MMAs per sample (20 at
+// N = 128) replace 200 N = 32 ones.  M tiles: output rows [0, 125) from tile
+// rows [0, 128), rows [125, 248) from [124, 252) (row q = y*18 + x; x >= 14
+// discarded).
+// Warp-specialised pipeline over the CTA's samples.  Warp 16 (one thread)
+// issues the MMAs of sample i into TMEM set i&1 as soon as its dz2 planes are
+// built, bulk-copies the planes to global for k_wgrad and the sample's pool1
+// argmaxes into smem; warps 0-15 build the planes of sample i from registers
+// prefetched during sample i-1, then -- while the MMAs run -- finish sample
+// i-1 (TMEM -> dp1, pool1/relu backward, conv1 gradients).  mbarriers:
+// dz_full (planes built), mma_done[set], dz_free (MMAs + plane store of the
+// sample done), tmem_idle[set] (set read out), am1_full[buffer].
+// grid (ceil(BS/spb), active), 544 threads
 // ---------------------------------------------------------------------------
-constexpr int kBwdThreads = 512;
-constexpr int kBwdIn = 2 * kFlat * 4 + kFlat;            // dp2, p2 (fp32), am2 of one sample
-constexpr int kDp1S = kC1 + 1;                           // dp1 row stride (conflict-free TMEM unload)
+constexpr int kBwdWork = 512;                            // warps 0-15: SIMT work
+constexpr int kBwdThreads = kBwdWork + 32;               // + warp 16: MMA / bulk-copy issue
+constexpr int kDp1S = kC1 + 1;                           // dp1 row stride (conflict-free)
 constexpr int kBwdDp1 = 196 * kDp1S * 4;                 // dp1 [196][33] fp32
 constexpr int kBwdRed = 8 * 832 * 4;                     // warp-pair partials (aliases dp1 + image)
 // image row stride 34: the 4 pool candidates' windows (offsets 0, 1, 34, 35)
 // of the 32 channel lanes fall in distinct banks
 constexpr int kXS = 34;
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdIn + kBwdDp1 + 32 * kXS * 4 + 3 * kP1;   // 221,888 B
-static_assert(kBwdRed <= kBwdDp1 + 32 * kXS * 4, "k_bwd_conv reduction scratch");
+constexpr int kBwdX = 32 * kXS * 4;
+constexpr int kBwdG = 49 * 64 * 4;                       // g = relu'(p2) * dp2 of one sample
+constexpr int kBwdHalo = 4 * 4 * 3 * 3 * 8 * 4;          // [quarter][ci group][lane 0-2][block 0-2][8]
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdDp1 + kBwdX + 2 * kP1 + kBwdG + kBwdHalo;   // 205,456 B
+static_assert(kBwdRed <= kBwdDp1 + kBwdX, "k_bwd_conv reduction scratch");
 
-__device__ __forceinline__ void bwd_stage(uint8_t* dst, const void* src, int bytes, int tid) {
-  const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
-  for (int e = tid * 16; e < bytes; e += kBwdThreads * 16) cp_async16(dst + e, s8 + e);
+// barrier 1 over the 512 work threads (warp 16 never joins it)
+__device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, 512;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
@@ -1005,180 +1026,262 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t dz_full, dz_free, mma_done[2], tmem_idle[2], am1_full[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float sB2[2][kBwdThreads / 64][64];
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
-  uint8_t* sIn = sDz + kDzBytes;                         // dp2 | p2 | am2 of the next sample
-  const float* iDp2 = reinterpret_cast<const float*>(sIn);
-  const float* iP2 = iDp2 + kFlat;
-  const uint8_t* iAm2 = sIn + 2 * kFlat * 4;
-  float* sDp1 = reinterpret_cast<float*>(sIn + kBwdIn);
+  float* sDp1 = reinterpret_cast<float*>(sDz + kDzBytes);
   float* sX = sDp1 + 196 * kDp1S;                        // [32][kXS] padded image
   float* sRed = sDp1;                                    // [8][832] (after the conv1 loop)
-  uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 32 * kXS);  // 3 x [196][32] pool1 argmax / relu'
+  uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 32 * kXS);   // 2 x [196][32] pool1 argmax / relu'
+  float* sG = reinterpret_cast<float*>(sAm1 + 2 * kP1);  // [49][64]
+  float* sHalo = sG + 49 * 64;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  auto stage_in = [&](int i) {   // pool2 inputs of sample i; its pool1 bytes into buffer i % 3
-    const int64_t sid = sidx(blockIdx.y, i, a.BS);
-    bwd_stage(sIn, a.dp2 + sid * kFlat, kFlat * 4, tid);
-    bwd_stage(sIn + kFlat * 4, p2_row(a, sl, blockIdx.y, i), kFlat * 4, tid);
-    bwd_stage(sIn + 2 * kFlat * 4, a.am2 + sid * kFlat, kFlat, tid);
-    bwd_stage(sAm1 + (i % 3) * kP1, a.am1 + sid * kP1, kP1, tid);
-    cp_async_commit();
-  };
-  stage_in(i0);
   stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, kBwdThreads);
   // the dz2 planes: borders stay zero; every sample rewrites all 4 candidates
   // of each pooled position
   for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) tmem_alloc<128>(&tmem_base);
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&dz_full, 16);   // one arrive per work warp
+    mbar_init(&dz_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&mma_done[b], 1);
+      mbar_init(&tmem_idle[b], 16);
+      mbar_init(&am1_full[b], 1);
+    }
     fence_init();
   }
+  fence_async_smem();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t idesc = idesc_bf16(128, 32, false, true);
-  for (int i = i0; i <= i1; ++i) {
-    if (i < i1) {
-      // ---- sample i: dz2 planes (the MMAs of sample i-1 must be done with them) ----
-      const int b = i & 1;
-      const int64_t sid = sidx(blockIdx.y, i, a.BS);
-      if (i > i0) mbar_wait(&mbar[b ^ 1], ((i - 1 - i0) >> 1) & 1);
-      cp_async_wait<0>();
-      __syncthreads();
-      float b2part = 0.0f;  // conv2 bias partial of channel tid & 63
-      for (int o = tid; o < kFlat; o += kBwdThreads) {
-        const int pp = o >> 6, co = o & 63;
-        const int py = pp / 7, px = pp - py * 7;
-        const int d = iAm2[o];
-        const float g = iP2[o] > 0.0f ? iDp2[o] : 0.0f;
-        b2part += g;
-        const __nv_bfloat16 gb = __float2bfloat16(g), zb = __float2bfloat16(0.0f);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int row = (2 * py + (q >> 1) + 2) * kG + 2 * px + (q & 1) + 2;
-          *reinterpret_cast<__nv_bfloat16*>(sDz + (co >> 3) * kPlane + row * 16 + (co & 7) * 2) = q == d ? gb : zb;
-        }
-      }
-      sB2[b][tid >> 6][tid & 63] = b2part;
-      fence_async_smem();
-      fence_before_sync();
-      __syncthreads();
-      if (i + 1 < i1) stage_in(i + 1);   // staged inputs consumed: prefetch the next sample
-      if (tid == 0) {
+
+  if (warp == 16) {
+    // ---------------- MMA / bulk-copy issue (one thread) ----------------
+    if (lane == 0) {
+      const uint32_t sdz = smem_u32(sDz), sw = smem_u32(sW2);
+      const uint32_t id128 = idesc_bf16(128, 128, false, true), id32 = idesc_bf16(128, 32, false, true);
+      for (int i = i0; i < i1; ++i) {
+        const int64_t sid = sidx(blockIdx.y, i, a.BS);
+        mbar_wait(&dz_full, (i - i0) & 1);
+        if (i - i0 >= 2) mbar_wait(&tmem_idle[i & 1], ((i - 2 - i0) >> 1) & 1);   // set read out (sample i-2)
         fence_after_sync();
-        uint64_t a0 = desc(smem_u32(sDz), kPlane, 128);
-        uint64_t b0 = desc(smem_u32(sW2), 128, 1024);
-        // opaque per sample: keeps the 200 descriptors from being hoisted
-        // out of the sample loop (register spills)
-        asm volatile("" : "+l"(a0), "+l"(b0));
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int tap = 0; tap < 25; ++tap)   // flipped tap: weights (4-ky, 4-kx)
-#pragma unroll
-            for (int kq = 0; kq < 4; ++kq)
-              mma_bf16(tmem + b * 64 + t * 32,
-                       a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + kq * (2 * kPlane / 16)),
-                       b0 + uint64_t((24 - tap) * 256 + kq * 16), idesc, tap > 0 || kq > 0);
-        commit(&mbar[b]);
-      }
-      // dz2 planes to global for k_wgrad (overlaps the MMAs)
-      uint4* dst = reinterpret_cast<uint4*>(a.dzg + sid * kDzBytes);
-      const uint4* src = reinterpret_cast<const uint4*>(sDz);
-      for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) dst[e] = src[e];
-    }
-    if (i > i0) {
-      // ---- sample j = i-1 (its MMAs completed before sample i's planes were
-      // built): dp1 from TMEM, pool1 / relu backward, conv1 gradients ----
-      const int j = i - 1, b = j & 1;
-      const int64_t sid = sidx(blockIdx.y, j, a.BS);
-      const uint8_t* am1 = sAm1 + (j % 3) * kP1;   // staged with sample j's pool2 inputs
-      if (i == i1) mbar_wait(&mbar[b], ((j - i0) >> 1) & 1);   // (earlier: waited before sample i)
-      fence_after_sync();
-      if (warp < 4) {
+        const uint32_t dset = tmem + uint32_t((i & 1) * 256);
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
-          const int row = t * 128 + warp * 32 + lane;
-          const int y = row / kG, x = row - y * kG;
-          float v[16];
+          const int base = t ? 124 : 0;
+          const uint32_t dt = dset + uint32_t(t * 128);
+#pragma unroll 1
+          for (int ky = 0; ky < 5; ++ky) {
+            const uint64_t ab = desc(sdz + uint32_t(base + 73 - kG * ky) * 16, kPlane, 128);
+            const uint64_t a4 = desc(sdz + uint32_t(base + 72 - kG * ky) * 16, kPlane, 128);
+            const uint64_t bb = desc(sw + uint32_t(ky * 5 * 4 * 1024), 128, 1024);
+            const uint64_t b4 = desc(sw + uint32_t((ky * 5 + 4) * 4 * 1024), 128, 1024);
 #pragma unroll
-          for (int c16 = 0; c16 < 2; ++c16) {
-            tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + uint32_t(b * 64 + t * 32 + c16 * 16), v);
-            if (y < 14 && x < 14) {
-#pragma unroll
-              for (int k = 0; k < 16; ++k) sDp1[(y * 14 + x) * kDp1S + c16 * 16 + k] = v[k];
+            for (int kq = 0; kq < 4; ++kq) {
+              mma_bf16(dt, ab + uint64_t(kq * (2 * kPlane / 16)), bb + uint64_t(kq * 16), id128, ky > 0 || kq > 0);
+              mma_bf16(dt + 96, a4 + uint64_t(kq * (2 * kPlane / 16)), b4 + uint64_t(kq * 16), id32, true);
             }
           }
         }
-      } else {
-        const float* img = a.X + int64_t(a.order[sl.row_off + j]) * (kImg * kImg);
-        for (int e = tid - 128; e < 1024; e += kBwdThreads - 128) {
-          const int yy = e >> 5, xx = e & 31;
-          sX[yy * kXS + xx] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+        commit(&mma_done[i & 1]);
+        // dz2 planes -> global for k_wgrad; pool1 argmaxes of sample i -> smem
+        pb::tma::bulk_store(a.dzg + sid * kDzBytes, sDz, uint32_t(kDzBytes));
+        pb::tma::expect_tx(&am1_full[i & 1], uint32_t(kP1));
+        pb::tma::bulk_load(sAm1 + (i & 1) * kP1, a.am1 + sid * kP1, uint32_t(kP1), &am1_full[i & 1]);
+        pb::tma::bulk_wait_reads();
+        mbar_wait(&mma_done[i & 1], ((i - i0) >> 1) & 1);
+        mbar_arrive(&dz_free);   // the plane buffer may be rebuilt
+      }
+      pb::tma::bulk_wait_all();
+    }
+  } else {
+    // ---------------- work warps 0-15 ----------------
+    // dz2 build unit of this thread: pooled position pp, channel block cb
+    const int upp = tid >> 3, ucb = tid & 7;
+    const bool unit = tid < 49 * 8;
+    float4 rd[2], rp[2];
+    uint2 ra = make_uint2(0, 0);
+    auto prefetch_in = [&](int i) {   // pool2 inputs of sample i -> registers
+      if (!unit) return;
+      const int64_t sid = sidx(blockIdx.y, i, a.BS);
+      const float4* d4 = reinterpret_cast<const float4*>(a.dp2 + sid * kFlat + upp * 64 + ucb * 8);
+      const float4* p4 = reinterpret_cast<const float4*>(p2_row(a, sl, blockIdx.y, i) + upp * 64 + ucb * 8);
+      rd[0] = d4[0];
+      rd[1] = d4[1];
+      rp[0] = p4[0];
+      rp[1] = p4[1];
+      ra = *reinterpret_cast<const uint2*>(a.am2 + sid * kFlat + upp * 64 + ucb * 8);
+    };
+    float rx[2];
+    auto prefetch_img = [&](int i) {   // padded image of sample i -> registers (2 px per thread)
+      const float* img = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = tid + k * kBwdWork, yy = e >> 5, xx = e & 31;
+        rx[k] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+      }
+    };
+    prefetch_in(i0);
+    prefetch_img(i0);
+    const int qw = warp & 3, cg = warp >> 2;   // epilogue: lane quarter, ci group of 8
+    for (int i = i0; i <= i1; ++i) {
+      if (i < i1) {
+        const int64_t sid = sidx(blockIdx.y, i, a.BS);
+        // ---- sample i: dz2 planes (MMAs + plane store of sample i-1 done) ----
+        if (i > i0) mbar_wait(&dz_free, (i - 1 - i0) & 1);
+        if (unit) {
+          const float dv[8] = {rd[0].x, rd[0].y, rd[0].z, rd[0].w, rd[1].x, rd[1].y, rd[1].z, rd[1].w};
+          const float pv[8] = {rp[0].x, rp[0].y, rp[0].z, rp[0].w, rp[1].x, rp[1].y, rp[1].z, rp[1].w};
+          float g[8];
+          uint32_t d[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            g[k] = pv[k] > 0.0f ? dv[k] : 0.0f;
+            d[k] = ((k < 4 ? ra.x : ra.y) >> (8 * (k & 3))) & 0xFFu;
+          }
+          const int py = upp / 7, px = upp - py * 7;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              w[k] = pack_bf16(d[2 * k] == uint32_t(q) ? g[2 * k] : 0.0f,
+                               d[2 * k + 1] == uint32_t(q) ? g[2 * k + 1] : 0.0f);
+            const int row = (2 * py + (q >> 1) + 2) * kG + 2 * px + (q & 1) + 2;
+            *reinterpret_cast<uint4*>(sDz + ucb * kPlane + row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          *reinterpret_cast<float4*>(sG + upp * 64 + ucb * 8) = make_float4(g[0], g[1], g[2], g[3]);
+          *reinterpret_cast<float4*>(sG + upp * 64 + ucb * 8 + 4) = make_float4(g[4], g[5], g[6], g[7]);
         }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dz_full);
+        work_sync();   // sG complete
+        // conv2 bias partial of sample i: 8 threads per channel (lanes
+        // 8c'+k, k = pooled-position stripe), combined in stripe order
+        {
+          const int ch = (warp << 2) | (lane >> 3), k8 = lane & 7;   // 64 channels x 8
+          float b2 = 0.0f;
+          for (int pp = k8; pp < 49; pp += 8) b2 += sG[pp * 64 + ch];
+          b2 += __shfl_down_sync(0xffffffffu, b2, 4, 8);
+          b2 += __shfl_down_sync(0xffffffffu, b2, 2, 8);
+          b2 += __shfl_down_sync(0xffffffffu, b2, 1, 8);
+          if (k8 == 0) a.pg[sid * kPg + 832 + ch] = b2;
+        }
+        if (i + 1 < i1) prefetch_in(i + 1);
       }
-      fence_before_sync();
-      __syncthreads();
-      // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
-      // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
-      float acc[25];
+      if (i > i0) {
+        // ---- sample j = i-1: dp1, pool1 / relu backward, conv1 gradients ----
+        const int j = i - 1, set = j & 1;
+        const int64_t sid = sidx(blockIdx.y, j, a.BS);
+        mbar_wait(&mma_done[set], ((j - i0) >> 1) & 1);
+        fence_after_sync();
+        uint32_t r[2][4][8];
 #pragma unroll
-      for (int t = 0; t < 25; ++t) acc[t] = 0.0f;
-      float bacc = 0.0f;
-      const int co = lane;
+        for (int t = 0; t < 2; ++t) {
+          const uint32_t ta = tmem + (uint32_t(qw * 32) << 16) + uint32_t(set * 256 + t * 128 + cg * 8);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tmem_ld8_nw(ta + uint32_t(b * 32), r[t][b]);
+          tmem_wait_ld32(r[t][0], r[t][1], r[t][2], r[t][3]);
+        }
+        fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_idle[set]);   // the MMAs of sample j+2 may overwrite the set
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (lane < 3)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                sHalo[(((qw * 4 + cg) * 3 + lane) * 3 + b) * 8 + c] = __uint_as_float(r[t][b][c]);
+          work_sync();
+          const int p = qw * 32 + lane, q = (t ? 124 : 0) + p;
+          const int y = q / kG, x = q - y * kG;
+          const bool valid = (t == 0 ? p <= 124 : (p >= 1 && q <= 247)) && x < 14;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float s = __uint_as_float(r[t][3][c]);
+#pragma unroll
+            for (int b = 2; b >= 0; --b) {
+              const int off = 3 - b;
+              float v = __shfl_down_sync(0xffffffffu, __uint_as_float(r[t][b][c]), off);
+              if (lane + off >= 32)
+                v = qw < 3 ? sHalo[((((qw + 1) * 4 + cg) * 3 + (lane + off - 32)) * 3 + b) * 8 + c] : 0.0f;
+              s += v;
+            }
+            if (valid) sDp1[(y * 14 + x) * kDp1S + cg * 8 + c] = s;
+          }
+          work_sync();   // halo reused by the next tile
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int e = tid + k * kBwdWork;
+          sX[(e >> 5) * kXS + (e & 31)] = rx[k];
+        }
+        if (i < i1) prefetch_img(i);
+        mbar_wait(&am1_full[set], ((j - i0) >> 1) & 1);
+        work_sync();
+        // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
+        // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
+        const uint8_t* am1 = sAm1 + set * kP1;
+        float acc[25];
+#pragma unroll
+        for (int tt = 0; tt < 25; ++tt) acc[tt] = 0.0f;
+        float bacc = 0.0f;
+        const int co = lane;
+        int dm_n = am1[warp * kC1 + co];
+        float g_n = sDp1[warp * kDp1S + co];
 #pragma unroll 1
-      for (int pp = warp; pp < 196; pp += kBwdThreads / 32) {
-        const int py = pp / 14, px = pp - py * 14;
-        const int dm = am1[pp * kC1 + co];   // pool1 argmax, bit 2: relu'
-        const float g = (dm & 4) ? sDp1[pp * kDp1S + co] : 0.0f;
-        bacc += g;
-        const int d = dm & 3;
-        const float* xw = sX + (2 * py + (d >> 1)) * kXS + 2 * px + (d & 1);
+        for (int pp = warp; pp < 196; pp += 16) {
+          const int py = pp / 14, px = pp - py * 14;
+          const int dm = dm_n;   // pool1 argmax, bit 2: relu'
+          const float g = (dm & 4) ? g_n : 0.0f;
+          if (pp + 16 < 196) {
+            dm_n = am1[(pp + 16) * kC1 + co];
+            g_n = sDp1[(pp + 16) * kDp1S + co];
+          }
+          bacc += g;
+          const int d = dm & 3;
+          const float* xw = sX + (2 * py + (d >> 1)) * kXS + 2 * px + (d & 1);
 #pragma unroll
-        for (int ky = 0; ky < 5; ++ky)
+          for (int ky = 0; ky < 5; ++ky)
 #pragma unroll
-          for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * kXS + kx], acc[ky * 5 + kx]);
+            for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * kXS + kx], acc[ky * 5 + kx]);
+        }
+        work_sync();  // all reads of dp1 / the image done: sRed may overwrite them
+        // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
+        // them to their own, then the 8 pair sums are added in warp order
+        if (warp >= 8) {
+#pragma unroll
+          for (int tt = 0; tt < 25; ++tt) sRed[(warp - 8) * 832 + co * 25 + tt] = acc[tt];
+          sRed[(warp - 8) * 832 + 800 + co] = bacc;
+        }
+        work_sync();
+        if (warp < 8) {
+#pragma unroll
+          for (int tt = 0; tt < 25; ++tt) sRed[warp * 832 + co * 25 + tt] += acc[tt];
+          sRed[warp * 832 + 800 + co] += bacc;
+        }
+        work_sync();
+        float* pg = a.pg + sid * kPg;
+        for (int k = tid; k < 832; k += kBwdWork) {
+          float s8 = 0.0f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) s8 += sRed[w * 832 + k];
+          pg[k] = s8;
+        }
+        work_sync();   // sRed / dp1 / sX free
       }
-      __syncthreads();  // all reads of dp1 / the image done: sRed may overwrite them
-      // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
-      // them to their own, then the 8 pair sums are added in warp order
-      if (warp >= 8) {
-#pragma unroll
-        for (int t = 0; t < 25; ++t) sRed[(warp - 8) * 832 + co * 25 + t] = acc[t];
-        sRed[(warp - 8) * 832 + 800 + co] = bacc;
-      }
-      __syncthreads();
-      if (warp < 8) {
-#pragma unroll
-        for (int t = 0; t < 25; ++t) sRed[warp * 832 + co * 25 + t] += acc[t];
-        sRed[warp * 832 + 800 + co] += bacc;
-      }
-      __syncthreads();
-      float* pg = a.pg + sid * kPg;
-      for (int k = tid; k < 832; k += kBwdThreads) {
-        float s8 = 0.0f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s8 += sRed[w * 832 + k];
-        pg[k] = s8;
-      }
-      if (tid < 64) {
-        float b2 = 0.0f;
-#pragma unroll
-        for (int q = 0; q < kBwdThreads / 64; ++q) b2 += sB2[b][q][tid];
-        pg[832 + tid] = b2;
-      }
-      fence_before_sync();
-      __syncthreads();   // sRed / dp1 free; TMEM half b read before its next MMAs
     }
   }
+  fence_before_sync();
+  __syncthreads();
   fence_after_sync();
-  if (warp == 0) tmem_free<128>(tmem);
+  if (warp == 0) tmem_free<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------

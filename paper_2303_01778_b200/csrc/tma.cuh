@@ -68,6 +68,25 @@ __device__ __forceinline__ void load_5d(void* dst, const CUtensorMap* map, int c
       : "memory");
 }
 
+// 1-D bulk copies (no tensor map): global -> smem completing on an mbarrier,
+// smem -> global in the thread's bulk group; sizes multiples of 16 B.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   umma::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(umma::smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(umma::smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+// the smem sources of this thread's bulk stores may be overwritten
+__device__ __forceinline__ void bulk_wait_reads() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// this thread's bulk stores are complete (visible in global memory)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 // SWIZZLE_128B K-major smem descriptor (sm_100): SBO = 1024 B (8 rows of 128 B),
 // LBO unused (1), layout type 2 at bits 61-63.
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {

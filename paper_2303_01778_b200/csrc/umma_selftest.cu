@@ -354,7 +354,8 @@ namespace {
 __global__ void __launch_bounds__(128) umma_bench2_kernel(int M, int N, int a_mn, int b_mn, uint32_t a_lbo,
                                                           uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo,
                                                           uint32_t kstep, int ngroups, uint32_t a_goff,
-                                                          int iters, int smem_bytes, long long* cycles) {
+                                                          int iters, int smem_bytes, long long* cycles,
+                                                          uint32_t b_kstep) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(128) umma_bench2_kernel(int M, int N, int a_mn
         const uint64_t ad = desc(a0 + uint32_t(g) * a_goff, a_lbo, a_sbo);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          mma_bf16(tbase + uint32_t(g * N), ad + uint64_t(ks * (kstep >> 4)), bd + uint64_t(ks * (kstep >> 4)), idesc,
+          mma_bf16(tbase + uint32_t(g * N), ad + uint64_t(ks * (kstep >> 4)), bd + uint64_t(ks * (b_kstep >> 4)), idesc,
                    it > 0 || ks > 0);
       }
     commit(&mbar);
@@ -399,11 +400,51 @@ __global__ void __launch_bounds__(128) umma_bench2_kernel(int M, int N, int a_mn
 
 extern "C" int pb_umma_bench2(int M, int N, int a_mn, int b_mn, uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo,
                               uint32_t b_sbo, uint32_t kstep, int ngroups, uint32_t a_goff, int iters, int grid,
-                              long long* cycles, void* stream) {
+                              long long* cycles, uint32_t b_kstep, void* stream) {
   if (ngroups < 1 || ngroups * N > 512 || grid < 1) return pb::fail(PB_ERR_INVALID, "pb_umma_bench2: bad arguments");
   const int smem = 200 * 1024;
   cudaFuncSetAttribute(umma_bench2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   umma_bench2_kernel<<<grid, 128, smem, pb::as_stream(stream)>>>(M, N, a_mn, b_mn, a_lbo, a_sbo, b_lbo, b_sbo, kstep,
-                                                                 ngroups, a_goff, iters, smem, cycles);
+                                                                 ngroups, a_goff, iters, smem, cycles,
+                                                                 b_kstep ? b_kstep : kstep);
   return pb::check_launch("pb_umma_bench2");
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostic: TMEM -> register load throughput.  `warps` warps (4 lane
+// quarters x warps/4 column groups) each read `cols` columns of their lane
+// quarter `iters` times with tcgen05.ld.32x32b.x16; cycles of the slowest warp.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(512) tmem_ld_bench_kernel(int cols, int iters, long long* cycles, float* sink) {
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t t = tmem_base + (uint32_t((warp & 3) * 32) << 16);
+  const int ngrp = int(blockDim.x >> 5) / 4, grp = warp >> 2;
+  float acc = 0.0f;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it)
+    for (int c = grp * 16; c < cols; c += ngrp * 16) {
+      float v[16];
+      tmem_ld16(t + uint32_t(c), v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc += v[k];
+    }
+  const long long t1 = clock64();
+  if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(cycles), (unsigned long long)(t1 - t0));
+  sink[blockIdx.x * blockDim.x + tid] = acc;
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(tmem_base);
+}
+}  // namespace
+
+extern "C" int pb_tmem_ld_bench(int warps, int cols, int iters, long long* cycles, float* sink, void* stream) {
+  if (warps < 4 || warps > 16 || warps % 4 || cols < 16 || cols > 512) return pb::fail(PB_ERR_INVALID, "pb_tmem_ld_bench");
+  tmem_ld_bench_kernel<<<148, warps * 32, 0, pb::as_stream(stream)>>>(cols, iters, cycles, sink);
+  return pb::check_launch("pb_tmem_ld_bench");
 }

@@ -19,10 +19,29 @@ cases = [
     ("K/K contiguous M128 N128", 128, 128, 0, 0, 128, 1024, 128, 1024, 256, 4, 0),
     ("K/K contiguous M128 N256", 128, 256, 0, 0, 128, 1024, 128, 1024, 256, 2, 0),
     ("dgrad M128 N32 K/MN", 128, 32, 0, 1, 5392, 128, 128, 1024, 32, 5, 16),
+    ("dgrad new N128 K/MN (kstep A 2 planes, B 256)", 128, 128, 0, 1, 5392, 128, 128, 1024, 10784, 4, 16 * 18, 256),
+    ("dgrad new N32  K/MN", 128, 32, 0, 1, 5392, 128, 128, 1024, 10784, 4, 16 * 18, 256),
+    ("N128 K/K A plane-strided, B contiguous", 128, 128, 0, 0, 5392, 128, 128, 1024, 10784, 4, 16 * 18, 256),
+    ("N128 K/MN A contiguous", 128, 128, 0, 1, 128, 1024, 128, 1024, 256, 4, 0, 256),
+    ("N128 MN/MN", 128, 128, 1, 1, 128, 1024, 128, 1024, 256, 4, 0, 256),
+    ("N256 K/MN A plane-strided", 128, 256, 0, 1, 5392, 128, 128, 1024, 10784, 2, 16 * 18, 256),
 ]
-for name, M, N, amn, bmn, al, asb, bl, bsb, ks, ng, goff in cases:
-    lib.check(lib.pb_umma_bench2(M, N, amn, bmn, al, asb, bl, bsb, ks, ng, goff, ITERS, 148, cyc.data_ptr(), 0))
+for case in cases:
+    name, M, N, amn, bmn, al, asb, bl, bsb, ks, ng, goff = case[:12]
+    bks = case[12] if len(case) > 12 else 0
+    lib.check(lib.pb_umma_bench2(M, N, amn, bmn, al, asb, bl, bsb, ks, ng, goff, ITERS, 148, cyc.data_ptr(), bks, 0))
     torch.cuda.synchronize()
     n = ITERS * ng * 8
     c = cyc.double().max().item() / n
     print(f"{name:40s}: {c:6.1f} cyc/MMA  {2 * M * N * 16 / c:6.0f} flop/cyc/SM", flush=True)
+
+# TMEM -> registers: bytes per cycle per SM
+sink = torch.zeros(148 * 512, device="cuda")
+for warps in (4, 8, 16):
+    for cols in (128, 512):
+        c1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        lib.check(lib.pb_tmem_ld_bench(warps, cols, 100, c1.data_ptr(), sink.data_ptr(), 0))
+        torch.cuda.synchronize()
+        byts = 100 * cols * 128 * 4
+        print(f"tmem ld: {warps:2d} warps, {cols} cols x 128 lanes x100: {c1.item():8d} cyc -> {byts / c1.item():6.1f} B/cyc/SM",
+              flush=True)
