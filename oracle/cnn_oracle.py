@@ -66,6 +66,25 @@ class _RoundGrad(torch.autograd.Function):
         return g.to(torch.bfloat16).to(g.dtype)
 
 
+class _Conv1Bf16(torch.autograd.Function):
+    """conv1 as the device computes it (csrc/cnn.cu k_fwd): bf16 image and
+    weights on the tensor cores, fp32 accumulation; the weight gradient uses
+    the fp32 image (the backward kernel's SIMT conv1 gradient)."""
+
+    @staticmethod
+    def forward(ctx, x, w):   # x [B, 1, 28, 28], w NHWC [32, 5, 5, 1]
+        ctx.save_for_backward(x, w)
+        xr = x.to(torch.bfloat16).to(x.dtype)
+        wr = w.to(torch.bfloat16).to(w.dtype).permute(0, 3, 1, 2)
+        return F.conv2d(xr, wr, padding=2)
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        gw = torch.nn.grad.conv2d_weight(x, (w.shape[0], w.shape[3], w.shape[1], w.shape[2]), g, padding=2)
+        return None, gw.permute(0, 2, 3, 1)
+
+
 def _tf32(x: torch.Tensor) -> torch.Tensor:
     """fp32 -> tf32 by truncation (how tcgen05 kind::tf32 reads fp32 operands,
     measured in tests/test_gpu_umma.py)."""
@@ -125,7 +144,8 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     """x [B, 784] -> logits; conv weights are NHWC ([co, ky, kx, ci]).
 
     emulate_bf16=True rounds exactly the operands the device feeds to its
-    tensor cores -- bf16 for conv2 (p1 and W2 in the forward, dL/dz2 in both
+    tensor cores -- bf16 for conv1 (the image and W1 in the forward; its weight
+    gradient uses the fp32 image), bf16 for conv2 (p1 and W2 in the forward, dL/dz2 in both
     backward GEMMs) and tf32 truncation for fc1 (X and W1 in the forward, dL/dz1
     in both backward GEMMs); everything else stays in the oracle's precision.
     Used to check the kernels' arithmetic separately from the effect of the
@@ -139,7 +159,10 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     that path stores them."""
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
-    h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
+    if emulate_bf16:
+        h = F.max_pool2d(F.relu(_Conv1Bf16.apply(h, c1w) + c1b.view(1, -1, 1, 1)), 2)
+    else:
+        h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
     if emulate_bf16:
         z = F.conv2d(_RoundValue.apply(h), _RoundValue.apply(c2w).permute(0, 3, 1, 2), padding=2)
         h = F.max_pool2d(F.relu(_RoundGrad.apply(z) + c2b.view(1, -1, 1, 1)), 2)
@@ -185,7 +208,7 @@ def decision_margins(params, x: torch.Tensor, fc1_base: torch.Tensor | None = No
     out = {}
     with torch.no_grad():
         h = x.reshape(-1, 1, 28, 28)
-        z1 = F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)
+        z1 = F.conv2d(_RoundValue.apply(h), _RoundValue.apply(c1w).permute(0, 3, 1, 2), c1b, padding=2)
         out["relu1"] = float(z1.abs().min()) / rms(z1)
         a1 = F.relu(z1)
         out["pool1"] = pool_gap(a1, z1)

@@ -57,188 +57,276 @@ __global__ void k_slots(Args a, int active) {
   a.slots[j] = s;
 }
 
-// ---------------------------------------------------------------------------
-// k_fwd: conv1 (SIMT) -> p1 planes -> conv2 (tcgen05) -> relu/pool epilogue
-// grid (ceil(BS/spb), active), 256 threads
-// ---------------------------------------------------------------------------
-constexpr int kFwdThreads = 512;
-constexpr int kZStride = 65;  // padded fp32 row of the conv2 output tile
-constexpr int kRawImg = kImg * kImg * 4;   // 3136 B
-constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg +
-                            (1024 + 832 + 64) * 4;   // 225,920 B
+// barrier 1 over the 512 work threads of the warp-specialised kernels (their
+// MMA-issue warp never joins it)
+__device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, 512;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
 
-// Software-pipelined over the CTA's samples: iteration i runs conv1 of
-// sample i (SIMT) into p1 buffer i&1, issues its conv2 MMAs into TMEM half
-// i&1, and then -- while those run -- finishes sample i-1 (TMEM -> bias/relu
-// -> maxpool -> p2).  The raw image of sample i+1 streams in by cp.async.
-__global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(Args a, int spb) {
+// ---------------------------------------------------------------------------
+// k_fwd: conv1 (tcgen05) -> relu/pool -> p1 planes -> conv2 (tcgen05) ->
+// relu/pool epilogue.  grid (ceil(BS/spb), active), 544 threads
+//
+// conv1 + 2x2 max-pool as ONE tensor-core GEMM over pooled positions: row pp
+// = (py, px) of A holds the 6x6 padded-image window at (2py, 2px) (K = 6 rows
+// x 8 bf16, the last 2 of each row weighted 0), and the N = 128 columns of B
+// are the filter placed at the four pool offsets d = (dy, dx) of that window
+// (column d*32 + co).  D[pp][d*32 + co] is conv1 at pool candidate d, so the
+// epilogue pools in registers (bias, NaN-propagating first maximum in d
+// order, relu, bf16) with no data exchange: 6 MMAs per sample.  conv2 as
+// before: the A operand is the padded p1 image itself, one shifted descriptor
+// per filter tap.
+// Warp-specialised: warp 16 issues conv1(i) once A(i) is built and conv2(i)
+// once the p1 planes of i are written (mbarriers a_ready / p1_ready; the
+// tensor pipe runs conv1(i), conv2(i), conv1(i+1), ... in issue order, so
+// conv1(i) done => conv2(i-1) done); warps 0-15 run the conv1 epilogue of
+// i, build A(i+1), copy p1(i) out and finish conv2 of sample i-1 (two
+// 32-channel halves through smem).
+// ---------------------------------------------------------------------------
+constexpr int kFwdWork = 512;                // warps 0-15
+constexpr int kFwdThreads = kFwdWork + 32;   // + warp 16: MMA issue
+constexpr int kZStride = 33;                 // padded fp32 row of the conv2 output half-tile
+constexpr int kRawImg = kImg * kImg * 4;     // 3136 B
+constexpr int kC1ABytes = 6 * 4096;          // conv1 A: 6 K cores x 256 rows x 16 B
+constexpr int kC1BBytes = 6 * 2048;          // conv1 B: 6 K cores x 128 cols x 16 B
+constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 1024 * 4 + kC1ABytes +
+                            kC1BBytes + (32 + 64) * 4;   // 203,264 B
+
+__global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.y];
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t c1_done, c2_done[2], a_ready, p1_ready;
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
-  uint8_t* sPl0 = sW2 + kW2Bytes;                       // 2 p1 buffers
-  float* sZ = reinterpret_cast<float*>(sPl0 + 2 * kP1Bytes);
-  uint8_t* sRaw = reinterpret_cast<uint8_t*>(sZ + 256 * kZStride);   // 2 raw images
-  float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);
-  float* sW1 = sX + 1024;
-  float* sB2 = sW1 + 832;
+  uint8_t* sPl = sW2 + kW2Bytes;                                   // p1 planes (one sample)
+  float* sZ = reinterpret_cast<float*>(sPl + kP1Bytes);           // conv2 half tile
+  uint8_t* sRaw = reinterpret_cast<uint8_t*>(sZ + 256 * kZStride); // 2 raw images
+  float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);       // [32][32] padded image
+  uint8_t* sA1 = reinterpret_cast<uint8_t*>(sX + 1024);           // conv1 A [u][pp][8] bf16
+  uint8_t* sB1w = sA1 + kC1ABytes;                                 // conv1 B [u][n][8] bf16
+  float* sB1 = reinterpret_cast<float*>(sB1w + kC1BBytes);
+  float* sB2 = sB1 + 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float* W = a.w + int64_t(sl.r) * a.P;
-  auto fetch_img = [&](int i) {
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg));
-    uint8_t* dst = sRaw + (i & 1) * kRawImg;
-    for (int e = tid * 16; e < kRawImg; e += kFwdThreads * 16) cp_async16(dst + e, src + e);
-    cp_async_commit();
-  };
-  fetch_img(i0);
   stage_w2(sW2, W, tid, kFwdThreads);
-  for (int e = tid; e < 832; e += kFwdThreads) sW1[e] = W[oC1W + e];
+  // conv1 B: column n = d*32 + co, K = (u, v) of the 6x6 window:
+  // W1[co][u - dy][v - dx] when inside the 5x5 filter, else 0
+  for (int e = tid; e < 6 * 128 * 8; e += kFwdThreads) {
+    const int u = e >> 10, n = (e >> 3) & 127, v = e & 7;
+    const int d = n >> 5, co = n & 31, ky = u - (d >> 1), kx = v - (d & 1);
+    const float w = (ky >= 0 && ky < 5 && kx >= 0 && kx < 5) ? W[oC1W + co * 25 + ky * 5 + kx] : 0.0f;
+    *reinterpret_cast<__nv_bfloat16*>(sB1w + u * 2048 + (n >> 3) * 128 + (n & 7) * 16 + v * 2) = __float2bfloat16(w);
+  }
+  for (int e = tid; e < 32; e += kFwdThreads) sB1[e] = W[oC1B + e];
   for (int e = tid; e < 64; e += kFwdThreads) sB2[e] = W[oC2B + e];
-  for (int e = tid; e < 2 * kP1Bytes / 16; e += kFwdThreads)
-    reinterpret_cast<uint4*>(sPl0)[e] = make_uint4(0, 0, 0, 0);
-  fence_async_smem();
-  if (warp == 0) tmem_alloc<256>(&tmem_base);
+  for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < kC1ABytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sA1)[e] = make_uint4(0, 0, 0, 0);
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&c1_done, 1);
+    mbar_init(&c2_done[0], 1);
+    mbar_init(&c2_done[1], 1);
+    mbar_init(&a_ready, 16);    // one arrive per work warp
+    mbar_init(&p1_ready, 16);
     fence_init();
   }
+  fence_async_smem();
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const uint32_t idesc = idesc_bf16(128, 64);
 
-  // conv1 weights of this thread's output channel live in registers
-  const int c1 = lane;
-  float wr[25];
+  if (warp == 16) {
+    // ---------------- MMA issue (one thread) ----------------
+    if (lane == 0) {
+      const uint32_t idesc1 = idesc_bf16(128, 128), idesc2 = idesc_bf16(128, 64);
+      const uint32_t sa1 = smem_u32(sA1), sb1 = smem_u32(sB1w);
+      const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
+      const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
+      for (int i = i0; i < i1; ++i) {
+        mbar_wait(&a_ready, (i - i0) & 1);
+        fence_after_sync();
 #pragma unroll
-  for (int t = 0; t < 25; ++t) wr[t] = sW1[c1 * 25 + t];
-  const float b1 = sW1[800 + c1];
-
-  // finish sample j: TMEM half (j&1) -> relu(z + b2) -> maxpool -> p2, am2
-  auto epilogue = [&](int j) {
-    mbar_wait(&mbar[j & 1], ((j - i0) >> 1) & 1);
-    fence_after_sync();
-    const uint32_t th = tmem + uint32_t((j & 1) * 128);
-    {
-      // 16 warps: lane quarter q = warp & 3, 16-column slice warp >> 2
-      const int q = warp & 3, part = warp >> 2;
+        for (int t = 0; t < 2; ++t)   // conv1(i) -> TMEM cols 256 + 128t
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int row = t * 128 + q * 32 + lane;
-        float v[16];
-        tmem_ld16(th + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + part * 16), v);
+          for (int ks = 0; ks < 3; ++ks)
+            mma_bf16(tmem + 256 + t * 128, desc(sa1 + uint32_t(t * 2048 + ks * 8192), 4096, 128),
+                     desc(sb1 + uint32_t(ks * 4096), 2048, 128), idesc1, ks > 0);
+        commit(&c1_done);
+        mbar_wait(&p1_ready, (i - i0) & 1);
+        fence_after_sync();
+        const uint32_t th = tmem + uint32_t((i & 1) * 128);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int co = part * 16 + k;
-          sZ[row * kZStride + co] = relu_nan(v[k] + sB2[co]);
-        }
+        for (int t = 0; t < 2; ++t)   // conv2(i) -> TMEM half i&1
+#pragma unroll
+          for (int tap = 0; tap < 25; ++tap)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
+                       b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc2, tap > 0 || hh > 0);
+        commit(&c2_done[i & 1]);
       }
     }
-    fence_before_sync();
-    __syncthreads();
-    const int64_t sid = sidx(blockIdx.y, j, a.BS);
-    float* p2 = p2_row(a, sl, blockIdx.y, j);
-    uint8_t* am2 = a.am2 + sid * kFlat;
-    for (int o = tid; o < kFlat; o += kFwdThreads) {
-      const int pp = o >> 6, co = o & 63;
-      const int py = pp / 7, px = pp - py * 7;
-      const int r0 = (2 * py) * kG + 2 * px;
-      const int rows[4] = {r0, r0 + 1, r0 + kG, r0 + kG + 1};
-      float best = -INFINITY;
-      int arg = 0;
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const float z = sZ[rows[d] * kZStride + co];
-        if (takes_max(z, best) && best == best) {
-          best = z;
-          arg = d;
-        }
-      }
-      p2[o] = a.hx ? tf32_rna(best) : best;
-      am2[o] = uint8_t(arg);
-    }
-    __syncthreads();  // sZ is free again
-  };
-
-  for (int i = i0; i < i1; ++i) {
-    const int64_t sid = sidx(blockIdx.y, i, a.BS);
-    uint8_t* sPl = sPl0 + (i & 1) * kP1Bytes;
-    cp_async_wait<0>();
-    __syncthreads();
-    {
+  } else {
+    // ---------------- work warps 0-15 ----------------
+    auto fetch_img = [&](int i) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg));
+      uint8_t* dst = sRaw + (i & 1) * kRawImg;
+      for (int e = tid * 16; e < kRawImg; e += kFwdWork * 16) cp_async16(dst + e, src + e);
+      cp_async_commit();
+    };
+    // padded image (fp32) of sample i, then the conv1 A windows (bf16); the
+    // raw image must have landed (cp.async group waited by the caller)
+    auto build_a = [&](int i) {
       const float* x = reinterpret_cast<const float*>(sRaw + (i & 1) * kRawImg);
-      for (int e = tid; e < 1024; e += kFwdThreads) {
+      for (int e = tid; e < 1024; e += kFwdWork) {
         const int yy = e >> 5, xx = e & 31;
         sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
       }
-    }
-    __syncthreads();
-    if (i + 1 < i1) fetch_img(i + 1);
-    // conv1 + relu + maxpool2 (warp = pooled position, lane = channel)
-    uint8_t* am1 = a.am1 + sid * kP1;
-    for (int pp = warp; pp < 196; pp += kFwdThreads / 32) {
-      const int py = pp / 14, px = pp - py * 14;
-      float win[6][6];
+      work_sync();
+      for (int e = tid; e < 6 * 196; e += kFwdWork) {   // K core u, pooled position pp
+        const int u = e / 196, pp = e - u * 196, py = pp / 14, px = pp - py * 14;
+        const float2* src = reinterpret_cast<const float2*>(sX + (2 * py + u) * 32 + 2 * px);
+        const float2 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+        *reinterpret_cast<uint4*>(sA1 + u * 4096 + pp * 16) =
+            make_uint4(pack_bf16(v0.x, v0.y), pack_bf16(v1.x, v1.y), pack_bf16(v2.x, v2.y), pack_bf16(v3.x, v3.y));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_ready);
+    };
+    // finish conv2 of sample j: TMEM half (j&1) -> relu(z + b2) -> maxpool -> p2, am2
+    auto epilogue2 = [&](int j) {
+      mbar_wait(&c2_done[j & 1], ((j - i0) >> 1) & 1);
+      fence_after_sync();
+      const uint32_t th = tmem + uint32_t((j & 1) * 128);
+      const int64_t sid = sidx(blockIdx.y, j, a.BS);
+      float* p2 = p2_row(a, sl, blockIdx.y, j);
+      uint8_t* am2 = a.am2 + sid * kFlat;
+      const int q = warp & 3, part = warp >> 2;   // lane quarter, 8-column slice
+#pragma unroll 1
+      for (int hc = 0; hc < 2; ++hc) {             // output channels [32hc, 32hc + 32)
 #pragma unroll
-      for (int u = 0; u < 6; ++u)
+        for (int t = 0; t < 2; ++t) {
+          const int row = t * 128 + q * 32 + lane;
+          uint32_t r[8];
+          tmem_ld8_nw(th + (uint32_t(q * 32) << 16) + uint32_t(t * 64 + hc * 32 + part * 8), r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int v = 0; v < 6; ++v) win[u][v] = sX[(2 * py + u) * 32 + 2 * px + v];
-      float best = -INFINITY;
-      int arg = 0;
+          for (int k = 0; k < 8; ++k) {
+            const int cl = part * 8 + k;
+            sZ[row * kZStride + cl] = relu_nan(__uint_as_float(r[k]) + sB2[hc * 32 + cl]);
+          }
+        }
+        fence_before_sync();
+        work_sync();
+        for (int o = tid; o < 49 * 32; o += kFwdWork) {
+          const int pp = o >> 5, cl = o & 31, co = hc * 32 + cl;
+          const int py = pp / 7, px = pp - py * 7;
+          const int r0 = (2 * py) * kG + 2 * px;
+          const int rows[4] = {r0, r0 + 1, r0 + kG, r0 + kG + 1};
+          float best = -INFINITY;
+          int arg = 0;
 #pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const int dy = d >> 1, dx = d & 1;
-        float z = b1;
+          for (int d = 0; d < 4; ++d) {
+            const float z = sZ[rows[d] * kZStride + cl];
+            if (takes_max(z, best) && best == best) {
+              best = z;
+              arg = d;
+            }
+          }
+          p2[pp * 64 + co] = a.hx ? tf32_rna(best) : best;
+          am2[pp * 64 + co] = uint8_t(arg);
+        }
+        work_sync();  // sZ is free again
+      }
+    };
+
+    fetch_img(i0);
+    cp_async_wait<0>();
+    work_sync();
+    build_a(i0);
+    if (i0 + 1 < i1) fetch_img(i0 + 1);
+    const int q = warp & 3, cg = warp >> 2;   // conv1 epilogue: lane quarter, 8-channel group
+    for (int i = i0; i < i1; ++i) {
+      const int64_t sid = sidx(blockIdx.y, i, a.BS);
+      // ---- conv1 epilogue of sample i (conv1(i) done => conv2(i-1) done
+      // with the p1 planes) ----
+      mbar_wait(&c1_done, (i - i0) & 1);
+      fence_after_sync();
+      uint8_t* am1 = a.am1 + sid * kP1;
 #pragma unroll
-        for (int ky = 0; ky < 5; ++ky)
+      for (int t = 0; t < 2; ++t) {
+        uint32_t r[4][8];   // r[d][k]: conv1 of channel cg*8 + k at pool candidate d
 #pragma unroll
-          for (int kx = 0; kx < 5; ++kx) z = fmaf(win[dy + ky][dx + kx], wr[ky * 5 + kx], z);
-        if (takes_max(z, best) && best == best) {
-          best = z;
-          arg = d;
+        for (int d = 0; d < 4; ++d)
+          tmem_ld8_nw(tmem + 256 + (uint32_t(q * 32) << 16) + uint32_t(t * 128 + d * 32 + cg * 8), r[d]);
+        tmem_wait_ld32(r[0], r[1], r[2], r[3]);
+        const int pp = t * 128 + q * 32 + lane;
+        if (pp < 196) {
+          uint32_t w[4], am[2];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float bias = sB1[cg * 8 + k];
+            float best = __uint_as_float(r[0][k]) + bias;
+            uint32_t arg = 0;
+#pragma unroll
+            for (int d = 1; d < 4; ++d) {
+              const float z = __uint_as_float(r[d][k]) + bias;
+              if (takes_max(z, best) && best == best) {
+                best = z;
+                arg = uint32_t(d);
+              }
+            }
+            const __nv_bfloat16 vb = __float2bfloat16(relu_nan(best));
+            const uint32_t code = arg | (__bfloat162float(vb) > 0.0f ? 4u : 0u);
+            const uint32_t h = __bfloat16_as_ushort(vb);
+            if (k & 1)
+              w[k >> 1] |= h << 16;
+            else
+              w[k >> 1] = h;
+            if (k & 3)
+              am[k >> 2] |= code << (8 * (k & 3));
+            else
+              am[k >> 2] = code;
+          }
+          const int py = pp / 14, px = pp - py * 14;
+          *reinterpret_cast<uint4*>(sPl + cg * kPlane + ((py + 2) * kG + px + 2) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint2*>(am1 + pp * kC1 + cg * 8) = make_uint2(am[0], am[1]);
         }
       }
-      const __nv_bfloat16 vb = __float2bfloat16(relu_nan(best));
-      *reinterpret_cast<__nv_bfloat16*>(sPl + (c1 >> 3) * kPlane + ((py + 2) * kG + px + 2) * 16 +
-                                        (c1 & 7) * 2) = vb;
-      // pool argmax, bit 2: the stored p1 value is > 0 (relu' for the backward)
-      am1[pp * kC1 + c1] = uint8_t(arg | (__bfloat162float(vb) > 0.0f ? 4 : 0));
+      fence_async_smem();
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p1_ready);
+      // ---- next sample's A (conv1(i) done with it) ----
+      if (i + 1 < i1) {
+        cp_async_wait<0>();
+        work_sync();
+        build_a(i + 1);
+        if (i + 2 < i1) fetch_img(i + 2);
+      }
+      // all p1 planes written (the MMA warp read them only after every work
+      // warp arrived): copy them out for the backward kernels; they are
+      // rewritten only after conv1(i+1), issued after conv2(i)
+      work_sync();
+      {
+        uint4* dst = reinterpret_cast<uint4*>(a.p1g + sid * kP1Bytes);
+        const uint4* src = reinterpret_cast<const uint4*>(sPl);
+        for (int e = tid; e < kP1Bytes / 16; e += kFwdWork) dst[e] = src[e];
+      }
+      if (i > i0) epilogue2(i - 1);
     }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      fence_after_sync();
-      const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
-      const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
-      const uint32_t th = tmem + uint32_t((i & 1) * 128);
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int tap = 0; tap < 25; ++tap)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-            mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
-                     b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc, tap > 0 || hh > 0);
-      commit(&mbar[i & 1]);
-    }
-    // p1 image to global for the backward kernels (overlaps the MMAs)
-    {
-      uint4* dst = reinterpret_cast<uint4*>(a.p1g + sid * kP1Bytes);
-      const uint4* src = reinterpret_cast<const uint4*>(sPl);
-      for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) dst[e] = src[e];
-    }
-    if (i > i0) epilogue(i - 1);
+    epilogue2(i1 - 1);
   }
-  epilogue(i1 - 1);
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<256>(tmem);
+  fence_after_sync();
+  if (warp == 0) tmem_free<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1014,11 +1102,6 @@ constexpr int kBwdHalo = 4 * 4 * 3 * 3 * 8 * 4;          // [quarter][ci group][
 constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdDp1 + kBwdX + 2 * kP1 + kBwdG + kBwdHalo;   // 205,456 B
 static_assert(kBwdRed <= kBwdDp1 + kBwdX, "k_bwd_conv reduction scratch");
 
-// barrier 1 over the 512 work threads (warp 16 never joins it)
-__device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, 512;\n" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
-}
 
 __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   pb::pdl_wait();

@@ -154,7 +154,9 @@ def _oracle_decisions(params, x, fc1_base):
         return top[..., 0] - top[..., 1], top[..., 1]
 
     with torch.no_grad():
-        z1 = F.conv2d(x.reshape(-1, 1, 28, 28), c1w.permute(0, 3, 1, 2), c1b, padding=2)
+        # conv1 as the device runs it: bf16 image and weights on the tensor cores
+        z1 = F.conv2d(O._RoundValue.apply(x.reshape(-1, 1, 28, 28)), O._RoundValue.apply(c1w).permute(0, 3, 1, 2),
+                      c1b, padding=2)
         r1 = float(z1.pow(2).mean().sqrt())
         w1 = windows(z1)
         best1 = w1.max(-1).values
