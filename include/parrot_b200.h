@@ -199,8 +199,11 @@ typedef struct {
    * round_up(steps_r*BS, 32);
    * step t's sample i is row t*BS + i.  Every client's fc1 weights stay
    * W0 - lr * sum_t dH_t^T X_t during the round (never materialised per
-   * step); they are written to w once, after the last sweep.  The four
-   * history buffers must be zeroed by the caller before the call. */
+   * step); they are written to w once, after the last sweep.  The history
+   * GEMMs read whole 32-row chunks and multiply the rows a client has not
+   * written by exact zeros (the kernels zero each client's dH^T pad
+   * columns), so the four history buffers need only hold FINITE values on
+   * entry (zero them once after allocation or after a diverged client). */
   float* lz_hx;             /* [lz_rows, 3136] f32                            */
   float* lz_hxt;            /* [3136, lz_rows] f32                            */
   float* lz_hd;             /* [lz_rows, 512] f32                             */
@@ -214,6 +217,12 @@ typedef struct {
   int64_t lz_rows;          /* total history rows (multiple of 32)            */
   int32_t lz_defer;         /* 1: leave the fc1 block of w unmaterialised      */
                             /*    (fold it with pb_cnn_lazy_fold instead)      */
+  int32_t lz_switch;        /* > 0: from sweep lz_switch on, the clients still */
+                            /* stepping (more than lz_switch steps) leave the  */
+                            /* low-rank form: their fc1 is materialised once   */
+                            /* and trained by the direct kernels (the history */
+                            /* re-read grows with the step count).  Their w   */
+                            /* rows hold the final fc1 even with lz_defer.    */
   int64_t g;
   int32_t C, BS, batch_size, epochs, samples_per_cta;
   float lr, mu, cg, cc;

@@ -44,6 +44,7 @@ class CnnTrainArgs(ctypes.Structure):
         ("lz_hx", c_void_p), ("lz_hxt", c_void_p), ("lz_hd", c_void_p), ("lz_hdt", c_void_p),
         ("lz_hoff", c_void_p), ("lz_hlen", c_void_p), ("lz_w0t", c_void_p), ("lz_zp", c_void_p),
         ("lz_gdt", c_void_p), ("lz_fpart", c_void_p), ("lz_rows", c_int64), ("lz_defer", c_int32),
+        ("lz_switch", c_int32),
         ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),

@@ -46,8 +46,14 @@ class _LazyWorkspace:
     """Grow-only buffers of the low-rank fc1 (csrc/cnn_lazy.cu): the round's
     (X, dH) history per client plus the per-sweep partials."""
 
+    HISTORY = ("hx", "hxt", "hd", "hdt")
+
     def __init__(self):
         self.buf: dict[str, torch.Tensor] = {}
+        # True while the history buffers may hold non-finite values: fresh
+        # allocations, or a round whose result read has not confirmed every
+        # client finite (GroupOutcome.resolve clears it)
+        self.dirty = True
 
     def _get(self, name: str, numel: int, device) -> torch.Tensor:
         t = self.buf.get(name)
@@ -57,6 +63,8 @@ class _LazyWorkspace:
             self.buf.pop(name, None)
             t = torch.empty(max(int(numel * 2.0), 4), dtype=torch.float32, device=device)
             self.buf[name] = t
+            if name in self.HISTORY:
+                self.dirty = True
         return t
 
     def get(self, rows: int, zp: int, gdt: int, slots: int, device) -> dict[str, torch.Tensor]:
@@ -64,8 +72,16 @@ class _LazyWorkspace:
                "hd": self._get("hd", rows * 512, device), "hdt": self._get("hdt", rows * 512, device),
                "w0t": self._get("w0t", 3136 * 512, device), "zp": self._get("zp", zp, device),
                "gdt": self._get("gdt", gdt, device), "fpart": self._get("fpart", max(74, slots) * 512 * 32, device)}
-        for k, width in (("hx", 3136), ("hxt", 3136), ("hd", 512), ("hdt", 512)):
-            out[k][:rows * width].zero_()
+        # The history GEMMs read whole 32-row chunks: rows a client has not
+        # written this round are multiplied by exact zeros (dH^T pad columns
+        # are zeroed by the head kernels, Gram rows past the live ones are
+        # selected to 0), which needs every stale value to be finite.  Stale
+        # values are the previous round's (finite) history, so the buffers
+        # are only cleared when fresh or after a round with a diverged client.
+        if self.dirty:
+            for k in self.HISTORY:
+                out[k].zero_()
+        self.dirty = True   # until this round's result read confirms it
         return out
 
 
@@ -103,34 +119,60 @@ class LazyFc1:
     SPLITS = 32
 
     def __init__(self, lz: dict, hoff: np.ndarray, hlen: np.ndarray, rows: int, BS: int, lr: float,
-                 w0: torch.Tensor):
+                 w0: torch.Tensor, switch: int = 0):
         self.lz, self.hoff, self.hlen, self.rows, self.BS, self.lr, self.w0 = lz, hoff, hlen, rows, BS, lr, w0
+        self.switch = switch   # clients with more steps left the low-rank form (w rows hold fc1)
         self.steps = None
 
     def set_steps(self, steps: np.ndarray) -> None:
         self.steps = np.asarray(steps, dtype=np.int64)
 
-    def fold(self, acc: torch.Tensor, rows: list[int], weights: np.ndarray) -> None:
-        """acc += sum_j w_j * fc1_w of client rows `rows` (contiguous)."""
+    def fold(self, acc: torch.Tensor, rows: list[int], weights: np.ndarray, mat: torch.Tensor | None = None) -> None:
+        """acc += sum_j w_j * fc1_w of client rows `rows` (contiguous); ``mat``
+        (the group's fc1_w columns) holds the rows of switched clients."""
         if not rows:
             return
         if rows != list(range(rows[0], rows[0] + len(rows))):
             raise ValueError("lazy fc1 fold needs a contiguous run of group rows")
         d = acc.device
         r = np.asarray(rows)
+        weights = np.asarray(weights, dtype=np.float32)
+        nr = (self.steps[r] * self.BS).astype(np.int32)
+        switched = self.steps[r] > self.switch if self.switch > 0 else np.zeros(len(r), dtype=bool)
+        if switched.any():
+            if mat is None:
+                raise ValueError("switched clients fold from their materialised rows: pass mat")
+            from . import _kernels as K
+            sel = r[switched]
+            K.fold_group(acc, mat, h2d(sel.astype(np.int32), d), h2d(weights[switched], d))
+            if switched.all():
+                return
+            # their history columns (pads included) are scaled to exact zeros
+            weights = np.where(switched, np.float32(0.0), weights)
+            nr = np.where(switched, self.hlen[r], nr).astype(np.int32)
         lo = int(self.hoff[r[0]])
         hi = int(self.hoff[r[-1]] + self.hlen[r[-1]])
         hoff = h2d(self.hoff[r].astype(np.int64), d)
-        nrows = h2d((self.steps[r] * self.BS).astype(np.int32), d)
-        w = h2d(np.asarray(weights, dtype=np.float32), d)
+        nrows = h2d(nr, d)
+        w = h2d(weights, d)
         part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
         f = LazyFoldArgs()
         f.acc, f.w0, f.hxt, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hxt"]), ptr(self.lz["hdt"])
         f.hrows, f.row_lo, f.row_hi = self.rows, lo, hi
         f.hoff, f.nrows, f.w, f.nclients = ptr(hoff), ptr(nrows), ptr(w), len(rows)
         f.part, f.splits = ptr(part), self.SPLITS
-        f.wsum, f.lr = float(np.sum(np.asarray(weights, dtype=np.float64))), self.lr
+        f.wsum, f.lr = float(np.sum(weights.astype(np.float64))), self.lr
         lib.check(lib.pb_cnn_lazy_fold(ctypes.byref(f), stream_of(acc)))
+
+
+def lz_switch_step(sweeps: int) -> int:
+    """Sweep at which a low-rank round's remaining clients leave the
+    low-rank form (0 = never): the history a step re-reads grows with the
+    step count (2 x 250 KB per past step at bs 20) while the direct fc1
+    streams a fixed 19 MB, and the sparse tail sweeps are latency-bound on
+    the history GEMMs.  PB_LZ_SWITCH overrides (0 disables)."""
+    s = int(os.environ.get("PB_LZ_SWITCH", "32"))
+    return s if 0 < s < sweeps else 0
 
 
 def _samples_per_cta() -> int:
@@ -198,6 +240,8 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
     handle = None
     if lazy:
         hlen, hoff, rows, zp, gdt = lazy_plan(total, active, BS)
+        if limit > 0:
+            _LZ.dirty = True   # truncated clients never reach the step that zeroes their pad columns
         lz = _LZ.get(rows, zp, gdt, G, d)
         hlen_d = h2d(hlen, d)
         hoff_d = h2d(hoff, d)
@@ -207,8 +251,9 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
         a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
         a.lz_rows = rows
         a.lz_defer = 1 if defer else 0
+        a.lz_switch = lz_switch_step(len(active))
         if defer:
-            handle = LazyFc1(lz, hoff, hlen, rows, BS, lr, w0)
+            handle = LazyFc1(lz, hoff, hlen, rows, BS, lr, w0, a.lz_switch)
     a.C, a.batch_size, a.epochs = spec.n_classes, batch_size, epochs
     a.lr, a.mu = lr, terms.get("mu", 0.0)
     a.cg, a.cc = terms.get("cg", 0.0), terms.get("cc", 0.0)

@@ -53,7 +53,12 @@ __global__ void k_slots(Args a, int active) {
   s.cnt = (e < a.epochs && a.bad[r] < 0) ? min(bs, n - b * bs) : 0;
   s.row_off = a.order_off[r] + int64_t(e) * n + int64_t(b) * bs;
   s.hist = a.hoff ? a.hoff[r] : 0;
-  s.pad_ = 0;
+  // lazy fc1: end of the history columns this step owns (relative to hist):
+  // the step's BS columns, or up to the client's 32-aligned history length on
+  // its last step.  The head zeroes dH^T columns [step*BS + cnt, end), so the
+  // history GEMMs that read whole 32-column chunks see exact zeros there
+  // (no per-round memset of the history buffers).
+  s.pad_ = a.hlen ? (a.step + 1 == a.epochs * nb ? a.hlen[r] : int64_t(a.step + 1) * a.BS) : 0;
   a.slots[j] = s;
 }
 
@@ -90,8 +95,12 @@ constexpr int kZStride = 33;                 // padded fp32 row of the conv2 out
 constexpr int kRawImg = kImg * kImg * 4;     // 3136 B
 constexpr int kC1ABytes = 6 * 4096;          // conv1 A: 6 K cores x 256 rows x 16 B
 constexpr int kC1BBytes = 6 * 2048;          // conv1 B: 6 K cores x 128 cols x 16 B
-constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 1024 * 4 + kC1ABytes +
-                            kC1BBytes + (32 + 64) * 4;   // 203,264 B
+// padded-image row stride: the A build reads rows 2py+u at column 2px of 14
+// pooled positions per row; 46 (= 14 mod 32 in float2 units) puts the
+// positions of consecutive pooled rows in distinct banks
+constexpr int kSXS = 46;
+constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 32 * kSXS * 4 + kC1ABytes +
+                            kC1BBytes + (32 + 64) * 4;   // 205,056 B
 
 __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   pb::pdl_wait();
@@ -105,13 +114,21 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   uint8_t* sPl = sW2 + kW2Bytes;                                   // p1 planes (one sample)
   float* sZ = reinterpret_cast<float*>(sPl + kP1Bytes);           // conv2 half tile
   uint8_t* sRaw = reinterpret_cast<uint8_t*>(sZ + 256 * kZStride); // 2 raw images
-  float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);       // [32][32] padded image
-  uint8_t* sA1 = reinterpret_cast<uint8_t*>(sX + 1024);           // conv1 A [u][pp][8] bf16
+  float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);       // [32][kSXS] padded image
+  uint8_t* sA1 = reinterpret_cast<uint8_t*>(sX + 32 * kSXS);      // conv1 A [u][pp][8] bf16
   uint8_t* sB1w = sA1 + kC1ABytes;                                 // conv1 B [u][n][8] bf16
   float* sB1 = reinterpret_cast<float*>(sB1w + kC1BBytes);
   float* sB2 = sB1 + 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float* W = a.w + int64_t(sl.r) * a.P;
+  if (a.hx && blockIdx.x == 0) {
+    // lazy fc1: the history rows [cnt, pad) of this step (partial batch,
+    // 32-row padding after the last step) are exact zeros
+    const int64_t r0 = sl.hist + int64_t(a.step) * a.BS;
+    float4* z = reinterpret_cast<float4*>(a.hx + (r0 + sl.cnt) * kFlat);
+    const int n4 = int(sl.pad_ - int64_t(a.step) * a.BS - sl.cnt) * (kFlat / 4);
+    for (int e = tid; e < n4; e += kFwdThreads) z[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  }
   stage_w2(sW2, W, tid, kFwdThreads);
   // conv1 B: column n = d*32 + co, K = (u, v) of the 6x6 window:
   // W1[co][u - dy][v - dx] when inside the 5x5 filter, else 0
@@ -125,6 +142,10 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   for (int e = tid; e < 64; e += kFwdThreads) sB2[e] = W[oC2B + e];
   for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
   for (int e = tid; e < kC1ABytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sA1)[e] = make_uint4(0, 0, 0, 0);
+  // the A build reads 8 columns per window (the last 2 weighted 0), i.e. up
+  // to column 33 of a row: the row padding [32, kSXS) stays zero (0 * NaN
+  // garbage would not be 0)
+  for (int e = tid; e < 32 * kSXS; e += kFwdThreads) sX[e] = 0.0f;
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     mbar_init(&c1_done, 1);
@@ -156,6 +177,9 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
           for (int ks = 0; ks < 3; ++ks)
             mma_bf16(tmem + 256 + t * 128, desc(sa1 + uint32_t(t * 2048 + ks * 8192), 4096, 128),
                      desc(sb1 + uint32_t(ks * 4096), 2048, 128), idesc1, ks > 0);
+        // the conv1 epilogue of i rewrites the p1 planes: the bulk store of
+        // p1(i-1) must have read them first
+        pb::tma::bulk_wait_reads();
         commit(&c1_done);
         mbar_wait(&p1_ready, (i - i0) & 1);
         fence_after_sync();
@@ -169,7 +193,10 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
               mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
                        b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc2, tap > 0 || hh > 0);
         commit(&c2_done[i & 1]);
+        // p1 planes of i -> global for the backward kernels (read concurrently with the conv2 MMAs)
+        pb::tma::bulk_store(a.p1g + sidx(blockIdx.y, i, a.BS) * kP1Bytes, sPl, uint32_t(kP1Bytes));
       }
+      pb::tma::bulk_wait_all();
     }
   } else {
     // ---------------- work warps 0-15 ----------------
@@ -185,12 +212,12 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       const float* x = reinterpret_cast<const float*>(sRaw + (i & 1) * kRawImg);
       for (int e = tid; e < 1024; e += kFwdWork) {
         const int yy = e >> 5, xx = e & 31;
-        sX[e] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+        sX[yy * kSXS + xx] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? x[(yy - 2) * kImg + (xx - 2)] : 0.0f;
       }
       work_sync();
       for (int e = tid; e < 6 * 196; e += kFwdWork) {   // K core u, pooled position pp
         const int u = e / 196, pp = e - u * 196, py = pp / 14, px = pp - py * 14;
-        const float2* src = reinterpret_cast<const float2*>(sX + (2 * py + u) * 32 + 2 * px);
+        const float2* src = reinterpret_cast<const float2*>(sX + (2 * py + u) * kSXS + 2 * px);
         const float2 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
         *reinterpret_cast<uint4*>(sA1 + u * 4096 + pp * 16) =
             make_uint4(pack_bf16(v0.x, v0.y), pack_bf16(v1.x, v1.y), pack_bf16(v2.x, v2.y), pack_bf16(v3.x, v3.y));
@@ -310,15 +337,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
         build_a(i + 1);
         if (i + 2 < i1) fetch_img(i + 2);
       }
-      // all p1 planes written (the MMA warp read them only after every work
-      // warp arrived): copy them out for the backward kernels; they are
-      // rewritten only after conv1(i+1), issued after conv2(i)
-      work_sync();
-      {
-        uint4* dst = reinterpret_cast<uint4*>(a.p1g + sid * kP1Bytes);
-        const uint4* src = reinterpret_cast<const uint4*>(sPl);
-        for (int e = tid; e < kP1Bytes / 16; e += kFwdWork) dst[e] = src[e];
-      }
+      // (the MMA thread bulk-stores the p1 planes for the backward kernels)
       if (i > i0) epilogue2(i - 1);
     }
     epilogue2(i1 - 1);
@@ -608,10 +627,13 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   if (a.hx) {
     // dH^T columns of the global [512][hrows] history (row pitch hrows)
     float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
-    for (int p = tid; p < cnt * (ohi - olo); p += kHeadDenseThreads) {
-      const int o = olo + p / cnt, i = p - (o - olo) * cnt;
-      hdt[int64_t(o) * a.hrows + i] = sDH[i * kDHS + o];
+    const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);   // columns [cnt, zc) -> 0
+    for (int p = tid; p < zc * (ohi - olo); p += kHeadDenseThreads) {
+      const int o = olo + p / zc, i = p - (o - olo) * zc;
+      hdt[int64_t(o) * a.hrows + i] = i < cnt ? sDH[i * kDHS + o] : 0.0f;
     }
+    for (int p = tid; p < (zc - cnt) * (ohi - olo); p += kHeadDenseThreads)   // and rows [cnt, zc) of hd
+      dh[int64_t(cnt + p / (ohi - olo)) * kH1 + olo + p % (ohi - olo)] = 0.0f;
     for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kDHS + o];
@@ -804,10 +826,13 @@ __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThread
   __syncthreads();
   if (a.hx) {
     float* hdt = a.hdt + sl.hist + int64_t(a.step) * BS;
-    for (int p = tid; p < cnt * kTailO; p += kHeadThreads) {
-      const int oo = p / cnt, i = p - oo * cnt;
-      hdt[int64_t(olo + oo) * a.hrows + i] = sDH[i * kTailS + oo];
+    const int zc = int(sl.pad_ - int64_t(a.step) * BS);   // columns [cnt, zc) -> 0
+    for (int p = tid; p < zc * kTailO; p += kHeadThreads) {
+      const int oo = p / zc, i = p - oo * zc;
+      hdt[int64_t(olo + oo) * a.hrows + i] = i < cnt ? sDH[i * kTailS + oo] : 0.0f;
     }
+    for (int p = tid; p < (zc - cnt) * kTailO; p += kHeadThreads)   // and rows [cnt, zc) of hd
+      dh[int64_t(cnt + p / kTailO) * kH1 + olo + p % kTailO] = 0.0f;
     for (int oo = tid; oo < kTailO; oo += kHeadThreads) {   // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kTailS + oo];
@@ -1243,17 +1268,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&dz_full);
         work_sync();   // sG complete
-        // conv2 bias partial of sample i: 8 threads per channel (lanes
-        // 8c'+k, k = pooled-position stripe), combined in stripe order
-        {
-          const int ch = (warp << 2) | (lane >> 3), k8 = lane & 7;   // 64 channels x 8
+        // conv2 bias partial of sample i: warps 14-15, one channel per lane
+        // (conflict-free rows of sG), pooled positions in order; the other
+        // warps go on to the next sample's prefetch
+        if (warp >= 14) {
+          const int ch = (warp - 14) * 32 + lane;
           float b2 = 0.0f;
-          for (int pp = k8; pp < 49; pp += 8) b2 += sG[pp * 64 + ch];
-          b2 += __shfl_down_sync(0xffffffffu, b2, 4, 8);
-          b2 += __shfl_down_sync(0xffffffffu, b2, 2, 8);
-          b2 += __shfl_down_sync(0xffffffffu, b2, 1, 8);
-          if (k8 == 0) a.pg[sid * kPg + 832 + ch] = b2;
+#pragma unroll 7
+          for (int pp = 0; pp < 49; ++pp) b2 += sG[pp * 64 + ch];
+          a.pg[sid * kPg + 832 + ch] = b2;
         }
+        // the next sample's build rewrites sG: after the first sample no
+        // epilogue (with its barriers) separates the two
+        if (i == i0 && i + 1 < i1) work_sync();
         if (i + 1 < i1) prefetch_in(i + 1);
       }
       if (i > i0) {
@@ -1771,20 +1798,33 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
       return rc;
     }
   }
+  // low-rank runs switch to the direct fc1 at sweep lz_switch: `lz` keeps
+  // the history arguments for the end-of-round materialisation
+  Args lz = a;
+  const int sw = a.hx && t.lz_switch > 0 && t.lz_switch < t.sweeps ? t.lz_switch : 0;
   for (int step = 0; step < t.sweeps; ++step) {
     const int active = t.active[step];
     if (active <= 0) break;
     a.step = step;
+    lz.step = step;
     pb::prof_begin(pb::K_CNN_SLOTS, s);
     pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
     pb::prof_end(pb::K_CNN_SLOTS, s);
+    if (sw && step == sw) {
+      // the still-active clients' fc1 after sw steps -> their w rows; from
+      // here on they train on the direct kernels (p2 / dH in the workspace)
+      if ((rc = lazy_fc1_switch(lz, active, s))) break;
+      a.hx = a.hxt = a.hd = a.hdt = nullptr;
+      a.hoff = nullptr;
+      a.hlen = nullptr;
+    }
     if ((rc = launch_sweep(a, &maps, active, true, spb, s))) break;
     if (a.timeline && (step + 1 == t.sweeps || t.active[step + 1] <= 0))
       pb::stamp(a.timeline + step + 1, s);
   }
-  if (a.hx) {
-    if (!rc && !t.lz_defer) rc = lazy_fc1_materialize(a, int(t.g), s);
-    lazy_fc1_release(a);  // the maps were copied into the launches' parameters
+  if (lz.hx) {
+    if (!rc && !t.lz_defer) rc = lazy_fc1_materialize(lz, int(t.g), sw, s);
+    lazy_fc1_release(lz);  // the maps were copied into the launches' parameters
   }
   return rc;
 }

@@ -70,8 +70,8 @@ struct Args {
   double* eval;    // [2] correct, loss (eval mode)
   // ---- lazy fc1 (plain SGD): the round's (X, dH) history, see cnn_lazy.cu --
   // Client row r owns history rows [hist_off[r], hist_off[r] + L_r) of
-  // hrows (L_r a multiple of 32); step t's sample i is row t*BS + i.  All
-  // four buffers are zeroed before the round.
+  // hrows (L_r a multiple of 32); step t's sample i is row t*BS + i.  Stale
+  // rows are finite and meet exact zeros (dH^T pad columns, Gram selects).
   float* hx;              // [hrows, kFlat]  X_t (the p2 activations)
   float* hxt;             // [kFlat, hrows]  X transposed
   float* hd;              // [hrows, kH1]    dH_t = dL/dz1
@@ -165,8 +165,12 @@ __device__ inline void stage_w2(uint8_t* sW2, const float* W, int tid, int nthre
 // the head (forward correction + shared forward), phase 1: after it
 // (backward Gram rows + shared/corrected dgrad).
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s);
-// Write each client's end fc1 weights W0 - lr * dH^T X (cnn_lazy.cu).
-int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s);
+// Write each client's end fc1 weights W0 - lr * dH^T X (cnn_lazy.cu),
+// skipping clients with more than switch_step steps (> 0: switched).
+int lazy_fc1_materialize(const Args& a, int g, int switch_step, cudaStream_t s);
+// Leave the low-rank form at sweep a.step: write the fc1 weights of the
+// active slots' clients (their a.step steps so far) into their w rows.
+int lazy_fc1_switch(const Args& a, int active, cudaStream_t s);
 // Transpose the fc1 block of w0 into a.w0t and encode the round's tensor
 // maps (a.lzmaps); lazy_fc1_release frees them (cnn_lazy.cu).
 int lazy_fc1_prepare(Args& a, cudaStream_t s);

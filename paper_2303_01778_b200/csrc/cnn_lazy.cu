@@ -94,9 +94,11 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
   }
   __syncthreads();
   float* xt = a.hxt + int64_t(k0) * a.hrows + sl.hist + int64_t(a.step) * a.BS;
-  for (int e = threadIdx.x; e < cnt * kn; e += 128) {
-    const int kk = e / cnt, i = e - kk * cnt;
-    xt[int64_t(kk) * a.hrows + i] = tile[i][kk];
+  // columns [cnt, zc) (partial batch, padding after the last step) -> 0
+  const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);
+  for (int e = threadIdx.x; e < zc * kn; e += 128) {
+    const int kk = e / zc, i = e - kk * zc;
+    xt[int64_t(kk) * a.hrows + i] = i < cnt ? tile[i][kk] : 0.0f;
   }
 }
 
@@ -594,11 +596,19 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
 // k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hxt[k][j]
 // (M = 128 o, N = 256 k, K = steps_r * BS rounded to 32 -- within the
 // client's 32-aligned history); grid (13, 4, g), 256 threads -- the client
-// is the slowest grid dimension, so its 52 tiles re-read its history from L2
+// is the slowest grid dimension, so its 52 tiles re-read its history from L2.
+// switch_step > 0: clients that took more steps left the low-rank form at
+// that sweep (their w rows already hold the final fc1) and are skipped.
+// Switch mode (kfix > 0): the clients of the current slots, K = kfix rows
+// (the steps before the switch), grid (13, 4, active).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMaps m, Args a) {
-  const int r = blockIdx.z, q = blockIdx.y, k0 = blockIdx.x * 256;
-  const int K = a.steps[r] * a.BS;
+__global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMaps m, Args a, int kfix,
+                                                   int switch_step) {
+  pb::pdl_wait();
+  const int r = kfix > 0 ? a.slots[blockIdx.z].r : int(blockIdx.z), q = blockIdx.y, k0 = blockIdx.x * 256;
+  if (kfix > 0 && a.slots[blockIdx.z].cnt == 0) return;
+  if (kfix == 0 && switch_step > 0 && a.steps[r] > switch_step) return;
+  const int K = kfix > 0 ? kfix : a.steps[r] * a.BS;
   if (K == 0) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
@@ -919,12 +929,21 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   return pb::check_launch(phase == 0 ? "lazy fc1 forward" : "lazy fc1 backward");
 }
 
-int lazy_fc1_materialize(const Args& a, int g, cudaStream_t s) {
+int lazy_fc1_materialize(const Args& a, int g, int switch_step, cudaStream_t s) {
   if (g <= 0) return PB_OK;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
-  k_lz_mat<<<dim3((kFlat + 255) / 256, kH1 / 128, g), 256, kShSmem, s>>>(*maps_of(a), a);
+  k_lz_mat<<<dim3((kFlat + 255) / 256, kH1 / 128, g), 256, kShSmem, s>>>(*maps_of(a), a, 0, switch_step);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);
   return pb::check_launch("lazy fc1 materialise");
+}
+
+int lazy_fc1_switch(const Args& a, int active, cudaStream_t s) {
+  if (active <= 0 || a.step <= 0) return PB_OK;
+  pb::prof_begin(pb::K_CNN_LZ_MAT, s);
+  pb::launch_pdl(k_lz_mat, dim3((kFlat + 255) / 256, kH1 / 128, unsigned(active)), dim3(256), kShSmem, s, 1,
+                 *maps_of(a), a, a.step * a.BS, 0);
+  pb::prof_end(pb::K_CNN_LZ_MAT, s);
+  return pb::check_launch("lazy fc1 switch");
 }
 
 }  // namespace cnn

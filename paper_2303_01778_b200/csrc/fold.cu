@@ -69,15 +69,29 @@ fold_group_vec(float4* __restrict__ acc, const float* __restrict__ xs, int64_t s
   }
 }
 
+// (unaligned / odd-sized entries, e.g. a 62-class bias: few threads, so the
+// row loads are batched kDepth deep -- the chain over g rows is latency-bound)
+template <int kDepth>
 __global__ void fold_group_scalar(float* __restrict__ acc, const float* __restrict__ xs,
                                   int64_t stride, const int32_t* __restrict__ order,
                                   const float* __restrict__ w, int g, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     float a = acc[i];
-    for (int j = 0; j < g; ++j) {
-      const int64_t row = order ? order[j] : j;
-      a = fmaf(w ? w[j] : 1.0f, xs[row * stride + i], a);
+    for (int j0 = 0; j0 < g; j0 += kDepth) {
+      float v[kDepth], wj[kDepth];
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u) {
+        const int j = j0 + u;
+        if (j < g) {
+          const int64_t row = order ? order[j] : j;
+          v[u] = __ldcs(xs + row * stride + i);
+          wj[u] = w ? w[j] : 1.0f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kDepth; ++u)
+        if (j0 + u < g) a = fmaf(wj[u], v[u], a);
     }
     acc[i] = a;
   }
@@ -146,13 +160,19 @@ extern "C" int pb_fold_group_f32(float* acc, const float* xs, int64_t x_stride,
     // one float4 per thread, no grid-stride re-walk of the g rows
     const int64_t blocks = (n4 + kThreads - 1) / kThreads;
     pb::prof_begin(pb::K_FOLD_GROUP, s);
-    fold_group_vec<8><<<unsigned(blocks), kThreads, 0, s>>>(
-        reinterpret_cast<float4*>(acc), xs, x_stride, order, w, int(g), n4);
+    // small entries (biases, conv1) have too few threads to cover the row
+    // latency: keep 32 rows in flight instead of 8
+    if (blocks < pb::sm_count())
+      fold_group_vec<32><<<unsigned(blocks), kThreads, 0, s>>>(
+          reinterpret_cast<float4*>(acc), xs, x_stride, order, w, int(g), n4);
+    else
+      fold_group_vec<8><<<unsigned(blocks), kThreads, 0, s>>>(
+          reinterpret_cast<float4*>(acc), xs, x_stride, order, w, int(g), n4);
     pb::prof_end(pb::K_FOLD_GROUP, s);
   } else {
     const int64_t blocks = (n + kThreads - 1) / kThreads;
     pb::prof_begin(pb::K_FOLD_GROUP, s);
-    fold_group_scalar<<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
+    fold_group_scalar<32><<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
     pb::prof_end(pb::K_FOLD_GROUP, s);
   }
   return pb::check_launch("pb_fold_group_f32");

@@ -297,6 +297,7 @@ class GroupOutcome:
     pending: object | None = None  # deferred result read (train_group(defer_check=True))
     client_seconds: np.ndarray | None = None  # [G] device-measured task time (timing=True)
     timing: object | None = None  # (stamps tensor, decoder) until the result read
+    lazy_history: bool = False  # trained on the low-rank fc1 history workspace (cnn._LZ)
 
     def resolve(self) -> None:
         """Finish a deferred result read: wait for the group's [bad | steps |
@@ -316,6 +317,9 @@ class GroupOutcome:
                 raise NonFiniteLossError(f"client {self.clients[j]} round {round_num}: loss diverged")
         if not np.array_equal(steps_h, self.steps):
             raise RuntimeError(f"round {round_num}: device step counts differ from the plan")
+        if self.lazy_history:
+            from .cnn import _LZ
+            _LZ.dirty = False   # every client finite: the history may stay as stale operands
         self.loss_mean = loss_h / np.maximum(steps_h, 1)
         self._decode_timing()
 
@@ -451,6 +455,7 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
+    lz_used = False
     if spec.kind == "lr":
         K.lr_train(data.X, data.Y, inputs.rows_d, inputs.off_d, inputs.n_d, w0, w_out, loss,
                    steps, bad, F=spec.n_features, C=spec.n_classes, epochs=epochs,
@@ -459,7 +464,8 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
                    cg=terms.get("cg", 0.0), ctrl_c=state_work if terms.get("ctrl_c") else None,
                    cc=terms.get("cc", 0.0), client_ns=stamps)
     elif spec.kind == "cnn":
-        from .cnn import cnn_train_group
+        from .cnn import cnn_train_group, lazy_enabled
+        lz_used = lazy_enabled(terms)
         lazy = cnn_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
                                spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
                                state_work=state_work, defer_fc1=defer_fc1, timeline=stamps)
@@ -483,7 +489,8 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
             lazy.set_steps(steps_plan)
         return GroupOutcome(clients, n, steps_plan, np.full(G, np.nan), w_out, float("nan"), lazy,
                             pending=(res_h, done, t0, t1, round_num),
-                            timing=(stamps, decode) if stamps is not None else None)
+                            timing=(stamps, decode) if stamps is not None else None,
+                            lazy_history=lz_used)
     # one device->host read per group: failures, step counts, losses
     res = torch.cat([bad.double(), steps.double(), loss]).cpu().numpy()
     _IO["d2h"] += res.size * 8
@@ -494,6 +501,9 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
             raise NonFiniteLossError(f"client {clients[j]} round {round_num}: loss diverged")
     if lazy is not None:
         lazy.set_steps(steps_h)
+    if lz_used:
+        from .cnn import _LZ
+        _LZ.dirty = False   # every client finite: the history may stay as stale operands
     go = GroupOutcome(clients, n, steps_h, loss_h / np.maximum(steps_h, 1), w_out, seconds, lazy,
                       timing=(stamps, decode) if stamps is not None else None)
     go._decode_timing()

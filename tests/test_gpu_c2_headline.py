@@ -122,8 +122,11 @@ def _group(c2, monkeypatch, sweeps: int):
             am1 = ws["am1"][sid * 6272:(sid + cnt) * 6272].view(cnt, 6272).cpu().numpy()
             am2 = ws["am2"][sid * 3136:(sid + cnt) * 3136].view(cnt, 3136).cpu().numpy()
             h = ws["h"].view(torch.float32)[sid * 512:(sid + cnt) * 512].view(cnt, 512).cpu().numpy()
-            base = int(hoff[c]) + t * BS
-            p2 = hx[base * 3136:(base + cnt) * 3136].view(cnt, 3136).cpu().numpy()
+            if 0 < cnn.lz_switch_step(sweeps) <= t:   # past the switch: direct fc1, p2 in the workspace
+                p2 = ws["p2"].view(torch.float32)[sid * 3136:(sid + cnt) * 3136].view(cnt, 3136).cpu().numpy()
+            else:
+                base = int(hoff[c]) + t * BS
+                p2 = hx[base * 3136:(base + cnt) * 3136].view(cnt, 3136).cpu().numpy()
             dec[c] = (am1 & 3, am1 >> 2, am2, p2 > 0, h > 0)
     return rows, dec
 
@@ -173,7 +176,10 @@ def _oracle_decisions(params, x, fc1_base):
         arg2 = (first_argmax(windows(a2)).reshape(B, -1), (torch.minimum(g2, zb.abs()) / r2).reshape(B, -1))
         relu2 = ((zb > 0).reshape(B, -1), (zb.abs() / r2).reshape(B, -1))
         hp = F.max_pool2d(a2, 2).permute(0, 2, 3, 1).reshape(B, -1)
-        z3 = O._tf32_rna(hp) @ (f1w - fc1_base + O._tf32(fc1_base)).t() + f1b
+        if fc1_base is None:   # direct fc1 (after the low-rank switch): tf32 truncation
+            z3 = O._tf32(hp) @ O._tf32(f1w).t() + f1b
+        else:
+            z3 = O._tf32_rna(hp) @ (f1w - fc1_base + O._tf32(fc1_base)).t() + f1b
         relu3 = (z3 > 0, z3.abs() / float(z3.pow(2).mean().sqrt()))
     return [(d.numpy(), m.numpy()) for d, m in (arg1, relu1, arg2, relu2, relu3)]
 
@@ -189,8 +195,13 @@ def test_c2_headline_group_per_step_parity(c2, monkeypatch):
     fc1_base = torch.as_tensor(w0[o1:o1 + s1]).view(512, 3136)
     prev = {c: w0.copy() for c in picks}
     report = []
+    from paper_2303_01778_b200 import cnn
+    switch = cnn.lz_switch_step(int(steps.max()))
     for k in range(1, int(max(steps[c] for c in picks)) + 1):
         rows, dec = _group(c2, monkeypatch, k)
+        # steps from the switch sweep on run the direct fc1 (tf32 truncation
+        # of the materialised weights) instead of the low-rank form
+        base_k = None if 0 < switch <= k - 1 else fc1_base
         for i, c in enumerate(picks):
             if steps[c] < k:
                 continue
@@ -200,7 +211,7 @@ def test_c2_headline_group_per_step_parity(c2, monkeypatch):
             idx = torch.as_tensor(order[(k - 1) * BS:k * BS])
             xb = torch.as_tensor(X, dtype=torch.float64)[idx]
             params = [p.requires_grad_(True) for p in cnn_oracle.unflatten(prev[c], 62)]
-            loss = F.cross_entropy(cnn_oracle.forward(params, xb, True, fc1_base),
+            loss = F.cross_entropy(cnn_oracle.forward(params, xb, True, base_k),
                                    torch.as_tensor(y)[idx])
             grads = torch.autograd.grad(loss, params)
             ref = np.concatenate([(p - LR * g).detach().reshape(-1).numpy() for p, g in zip(params, grads)])
@@ -209,7 +220,7 @@ def test_c2_headline_group_per_step_parity(c2, monkeypatch):
                       for _, o, s, _ in spec.columns())
             # decisions: device (workspace) vs oracle, and the margin of every flip
             flips, margins = [], []
-            for (want, margin), got in zip(_oracle_decisions(params, xb, fc1_base), dec[c]):
+            for (want, margin), got in zip(_oracle_decisions(params, xb, base_k), dec[c]):
                 diff = np.asarray(got) != np.asarray(want)
                 flips.append(int(diff.sum()))
                 margins.append(float(margin[diff].max()) if diff.any() else 0.0)

@@ -211,15 +211,22 @@ def test_cnn_dense_sweeps_match_sparse(spec, femnist_like, monkeypatch):
 def test_cnn_stale_workspace_nan(spec, femnist_like, monkeypatch):
     """A partial-batch client trained on CNN workspaces poisoned with NaN bit
     patterns matches the clean run bit for bit (no kernel reads a sample row
-    past the batch without masking it)."""
+    past the batch without masking it).  The low-rank history buffers are
+    kept across rounds without clearing: rows a client has not written are
+    multiplied by exact zeros, so they are poisoned with huge FINITE values
+    (the buffers' contract: finite unless flagged dirty, cnn._LZ)."""
     import paper_2303_01778_b200.cnn as cnn
     from paper_2303_01778_b200.models import cnn_init
     X, y = femnist_like.features[:57], femnist_like.labels[:57]
     w0 = cnn_init(spec, seed=1)
     clean = _device_after(spec, w0, X, y, 20, 2, 0, monkeypatch)
+    assert not cnn._LZ.dirty
     for ws in (cnn._WS.buf, cnn._LZ.buf):
-        for t in ws.values():
-            t.fill_(float("nan")) if t.is_floating_point() else t.fill_(255)
+        for k, t in ws.items():
+            if ws is cnn._LZ.buf and k in cnn._LZ.HISTORY:
+                t.fill_(-3.0e38)
+            else:
+                t.fill_(float("nan")) if t.is_floating_point() else t.fill_(255)
     poisoned = _device_after(spec, w0, X, y, 20, 2, 0, monkeypatch)
     assert np.all(np.isfinite(poisoned[0])) and np.isfinite(poisoned[1])
     assert np.array_equal(clean[0], poisoned[0]) and clean[1] == poisoned[1]
