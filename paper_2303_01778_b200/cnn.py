@@ -169,9 +169,12 @@ def lz_switch_step(sweeps: int) -> int:
     """Sweep at which a low-rank round's remaining clients leave the
     low-rank form (0 = never): the history a step re-reads grows with the
     step count (2 x 250 KB per past step at bs 20) while the direct fc1
-    streams a fixed 19 MB, and the sparse tail sweeps are latency-bound on
-    the history GEMMs.  PB_LZ_SWITCH overrides (0 disables)."""
-    s = int(os.environ.get("PB_LZ_SWITCH", "32"))
+    streams a fixed 19 MB.  Off by default: measured on the C2 round, the
+    direct kernels are slower than the low-rank ones in every sweep they
+    would take over (switching at sweep 16 / 24 / 32 / 40 costs +15.9 /
+    +7.0 / +3.4 / +2.1 ms per round; tools/sweep_times.py), because the
+    sparse tail is latency-bound, not HBM-bound.  PB_LZ_SWITCH=s enables it."""
+    s = int(os.environ.get("PB_LZ_SWITCH", "0"))
     return s if 0 < s < sweeps else 0
 
 
