@@ -937,9 +937,22 @@ int lazy_fc1_materialize(const Args& a, int g, int switch_step, cudaStream_t s) 
   return pb::check_launch("lazy fc1 materialise");
 }
 
+// switch mode of k_lz_mat reads whole 32-column chunks: the history columns
+// [K, round_up(K, 32)) of the active clients (their next steps, stale) must
+// be zero in hdt first.  grid (active), 256 threads
+__global__ void k_lz_zero_tail(Args a, int K) {
+  pb::pdl_wait();
+  const Slot sl = a.slots[blockIdx.x];
+  const int n = ((K + 31) & ~31) - K;
+  if (sl.cnt == 0 || n == 0) return;
+  for (int e = threadIdx.x; e < kH1 * n; e += blockDim.x)
+    a.hdt[int64_t(e / n) * a.hrows + sl.hist + K + e % n] = 0.0f;
+}
+
 int lazy_fc1_switch(const Args& a, int active, cudaStream_t s) {
   if (active <= 0 || a.step <= 0) return PB_OK;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
+  pb::launch_pdl(k_lz_zero_tail, dim3(unsigned(active)), dim3(256), 0, s, 1, a, a.step * a.BS);
   pb::launch_pdl(k_lz_mat, dim3((kFlat + 255) / 256, kH1 / 128, unsigned(active)), dim3(256), kShSmem, s, 1,
                  *maps_of(a), a, a.step * a.BS, 0);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);

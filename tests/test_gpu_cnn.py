@@ -312,3 +312,66 @@ def test_cnn_fedprox_step_replay(spec, femnist_like, monkeypatch):
     e_prox = np.linalg.norm(step_dev - with_prox) / np.linalg.norm(with_prox)
     e_plain = np.linalg.norm(step_dev - plain) / np.linalg.norm(plain)
     assert e_prox <= 1e-2 and e_prox * 4 <= e_plain, (e_prox, e_plain)
+
+
+def test_cnn_lowrank_switch_to_direct(spec, femnist_like, monkeypatch):
+    """PB_LZ_SWITCH=s (off by default, cnn.lz_switch_step): clients still
+    stepping at sweep s leave the low-rank fc1 -- their fc1 is materialised
+    from the history and the direct kernels train it from there.  (1) The
+    end models agree with the all-low-rank run up to the operand rounding
+    the two fc1 forms differ in (tf32 round-to-nearest history vs truncated
+    weights): one step after the switch every client's update within 5e-2
+    (median 2e-2), whole runs within 0.15 (the bound of the direct-fc1 local
+    run against the emulating oracle); clients that finish before sweep s
+    are bit-identical.  (2) An engine FedAvg
+    round under the switch folds the switched clients from their
+    materialised rows and the others from the history
+    (cnn.LazyFc1.fold): the global equals the float64 sample-weighted mean
+    of the same clients' end models to 1e-5."""
+    import torch
+    import paper_2303_01778_b200 as pb
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    from paper_2303_01778_b200.models import cnn_init
+    from paper_2303_01778_b200.trainer import ClientData, NamedParams, train_group
+    G, SW = 48, 3
+    sizes = np.random.default_rng(4).integers(10, 120, size=G)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    profiles = [ClientProfile(c, int(sizes[c]),
+                              DataSlice(femnist_like.features[off[c]:off[c + 1]],
+                                        femnist_like.labels[off[c]:off[c + 1]], np.arange(sizes[c])))
+                for c in range(G)]
+    data = ClientData.from_profiles(profiles, n_classes=62)
+    plugin = pb.FedAvg(lr=0.05, batch_size=20)
+    glob = plugin.init_global(NamedParams.from_flat(spec, cnn_init(spec, 6)))
+    w0 = glob.flat(spec)
+    base = w0.cpu().numpy().astype(np.float64)
+    steps = -(-sizes // 20)
+    assert steps.max() > SW + 2 and (steps <= SW).any()
+
+    def group(switch, sweeps=0):
+        monkeypatch.setenv("PB_LZ_SWITCH", str(switch))
+        monkeypatch.setenv("PB_CNN_MAX_SWEEPS", str(sweeps))
+        return train_group(plugin, spec, data, list(range(G)), w0, glob, None, 1, 20, 0.05, seed=3,
+                           round_num=1).w_out.cpu().numpy().astype(np.float64)
+    # one direct step after the switch: single-step operand-rounding noise
+    lowrank, switched = group(0, SW + 1), group(SW, SW + 1)
+    errs = np.asarray([_rel(switched[c] - base, lowrank[c] - base) for c in range(G)])
+    assert np.array_equal(switched[steps <= SW], lowrank[steps <= SW])
+    assert errs.max() <= 5e-2 and float(np.median(errs[steps > SW])) <= 2e-2, errs
+    # whole runs: the rounding differences compound (ill-conditioned near initialisation)
+    lowrank, switched = group(0), group(SW)
+    errs = np.asarray([_rel(switched[c] - base, lowrank[c] - base) for c in range(G)])
+    assert np.array_equal(switched[steps <= SW], lowrank[steps <= SW])
+    assert errs.max() <= 0.15, errs
+    monkeypatch.setenv("PB_CNN_MAX_SWEEPS", "0")
+    # the engine round folds the switched clients from their materialised rows
+    cfg = pb.SimConfig(total_clients=G, concurrent_clients=G, num_devices=1, total_rounds=2,
+                       warmup_rounds=0, seed=3, scheme="PARROT")
+    eng = pb.SimulationEngine(cfg, plugin, profiles, pb.make_device_models(1), client_data=data,
+                              initial_global=glob)
+    monkeypatch.setenv("PB_LZ_SWITCH", str(SW))
+    out = eng.run_round(1)
+    got = np.concatenate([out.new_global.numpy(nm).reshape(-1) for nm in spec.names])
+    ends = group(SW)
+    want = (sizes[:, None].astype(np.float64) * ends).sum(0) / float(sizes.sum())
+    assert _rel(got, want) <= 1e-5
