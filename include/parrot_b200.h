@@ -298,6 +298,15 @@ typedef struct {
   int32_t C, BS, batch_size, epochs;
   float lr;
   int64_t* timeline;        /* [sweeps + 1] sweep start stamps, as for the CNN */
+  /* Plugin terms of the local gradient, as for the CNN (fedsim/trainer.py
+   * :237-257 FedProx, :288-348 SCAFFOLD): every SGD step uses
+   *   g + mu * (w - w0) + cg * ctrl_g + cc * ctrl_c[client row]
+   * (all terms off: mu = 0, ctrl_g = ctrl_c = NULL -- FedAvg / FedNova).     */
+  const float* w0;          /* [P] round-start model (FedProx)                */
+  const float* ctrl_g;      /* [P] or NULL (SCAFFOLD server control)          */
+  const float* ctrl_c;      /* [g, ctrl_stride] or NULL (client controls)     */
+  int64_t ctrl_stride;
+  float mu, cg, cc;
 } pb_resnet_train_args;
 int pb_resnet_workspace(int BS, int C, int64_t* out4);
 int pb_resnet_train_group(const pb_resnet_train_args* args, void* stream);

@@ -71,6 +71,8 @@ class ResnetTrainArgs(ctypes.Structure):
         ("ws_part", c_void_p), ("ws_gnp", c_void_p), ("g", c_int64),
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("lr", c_float), ("timeline", c_void_p),
+        ("w0", c_void_p), ("ctrl_g", c_void_p), ("ctrl_c", c_void_p), ("ctrl_stride", c_int64),
+        ("mu", c_float), ("cg", c_float), ("cc", c_float),
     ]
 
 

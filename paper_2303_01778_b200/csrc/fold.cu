@@ -172,7 +172,12 @@ extern "C" int pb_fold_group_f32(float* acc, const float* xs, int64_t x_stride,
   } else {
     const int64_t blocks = (n + kThreads - 1) / kThreads;
     pb::prof_begin(pb::K_FOLD_GROUP, s);
-    fold_group_scalar<32><<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
+    // small entries: 32 rows in flight; large ones have the threads to hide
+    // the latency and run at full occupancy one row at a time
+    if (blocks < pb::sm_count())
+      fold_group_scalar<32><<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
+    else
+      fold_group_scalar<1><<<unsigned(blocks), kThreads, 0, s>>>(acc, xs, x_stride, order, w, int(g), n);
     pb::prof_end(pb::K_FOLD_GROUP, s);
   }
   return pb::check_launch("pb_fold_group_f32");

@@ -77,7 +77,21 @@ struct Net {
   int64_t* timeline;  // [sweeps + 1] sweep start stamps (real clock) or null
   int32_t C, BS, bs, epochs, step;
   float lr;
+  // plugin terms: g + mu*(w - w0) + cg*ctrl_g + cc*ctrl_c[r] (FedProx, SCAFFOLD)
+  const float* w0;
+  const float* ctrl_g;
+  const float* ctrl_c;
+  int64_t ctrl_stride;
+  float mu, cg, cc;
 };
+
+// one SGD update of parameter idx (flat index in the model) of client row r
+__device__ __forceinline__ float rn_sgd(const Net& a, int r, int64_t idx, float w, float g) {
+  if (a.mu != 0.0f) g = fmaf(a.mu, w - a.w0[idx], g);
+  if (a.ctrl_g) g = fmaf(a.cg, a.ctrl_g[idx], g);
+  if (a.ctrl_c) g = fmaf(a.cc, a.ctrl_c[int64_t(r) * a.ctrl_stride + idx], g);
+  return fmaf(-a.lr, g, w);
+}
 
 __device__ __forceinline__ float relu_f(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
 
@@ -633,10 +647,10 @@ __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, 
   const float gg[4] = {g.x, g.y, g.z, g.w};
   if (Cin == k.Cinp) {
     float4 wv = *reinterpret_cast<float4*>(w + e);
-    wv.x = fmaf(-a.lr, gg[0], wv.x);
-    wv.y = fmaf(-a.lr, gg[1], wv.y);
-    wv.z = fmaf(-a.lr, gg[2], wv.z);
-    wv.w = fmaf(-a.lr, gg[3], wv.w);
+    wv.x = rn_sgd(a, sl.r, w_off + e, wv.x, gg[0]);
+    wv.y = rn_sgd(a, sl.r, w_off + e + 1, wv.y, gg[1]);
+    wv.z = rn_sgd(a, sl.r, w_off + e + 2, wv.z, gg[2]);
+    wv.w = rn_sgd(a, sl.r, w_off + e + 3, wv.w, gg[3]);
     *reinterpret_cast<float4*>(w + e) = wv;
     uint2 o;
     o.x = pack_bf16(wv.x, wv.y);
@@ -649,7 +663,7 @@ __global__ void __launch_bounds__(256) k_rn_wsgd(Net a, ConvK k, int64_t w_off, 
       const int ci = int((e + u) - crs * k.Cinp);
       if (ci >= Cin) continue;
       const int64_t wi = crs * Cin + ci;
-      const float nw = fmaf(-a.lr, gg[u], w[wi]);
+      const float nw = rn_sgd(a, sl.r, w_off + wi, w[wi], gg[u]);
       w[wi] = nw;
       w16[u] = __float2bfloat16(nw);
     }
@@ -690,10 +704,10 @@ __global__ void __launch_bounds__(256) k_rn_wsgd_t(Net a, ConvK k, int64_t w_off
         g.w += h.w;
       }
       float4 wv = *reinterpret_cast<float4*>(w + e);
-      wv.x = fmaf(-a.lr, g.x, wv.x);
-      wv.y = fmaf(-a.lr, g.y, wv.y);
-      wv.z = fmaf(-a.lr, g.z, wv.z);
-      wv.w = fmaf(-a.lr, g.w, wv.w);
+      wv.x = rn_sgd(a, sl.r, w_off + e, wv.x, g.x);
+      wv.y = rn_sgd(a, sl.r, w_off + e + 1, wv.y, g.y);
+      wv.z = rn_sgd(a, sl.r, w_off + e + 2, wv.z, g.z);
+      wv.w = rn_sgd(a, sl.r, w_off + e + 3, wv.w, g.w);
       *reinterpret_cast<float4*>(w + e) = wv;
       uint2 o;
       o.x = pack_bf16(wv.x, wv.y);
@@ -1098,7 +1112,7 @@ __global__ void k_rn_gn_sgd(Net a, GnSgd t) {
   for (int c = threadIdx.x; c < 2 * C; c += blockDim.x) {
     float g = 0.0f;
     for (int i = 0; i < sl.cnt; ++i) g += pg[int64_t(i) * 2 * C + c];
-    w[c] = fmaf(-a.lr, g, w[c]);   // [gamma | beta] are contiguous in the layout
+    w[c] = rn_sgd(a, sl.r, t.gamma[j] + c, w[c], g);   // [gamma | beta] are contiguous in the layout
   }
 }
 
@@ -1208,12 +1222,13 @@ __global__ void __launch_bounds__(256) k_rn_head(Net a, int64_t act, int64_t gou
     const int k = e >> 9, c = e & 511;
     float t = 0.0f;
     for (int i = 0; i < cnt; ++i) t = fmaf(sL[i * C + k], sP[i * 512 + c], t);
-    W[fc_off + e] = fmaf(-a.lr, t, W[fc_off + e]);
+    W[fc_off + e] = rn_sgd(a, sl.r, fc_off + e, W[fc_off + e], t);
   }
   for (int k = tid; k < C; k += 256) {
     float t = 0.0f;
     for (int i = 0; i < cnt; ++i) t += sL[i * C + k];
-    W[fc_off + int64_t(C) * 512 + k] = fmaf(-a.lr, t, W[fc_off + int64_t(C) * 512 + k]);
+    W[fc_off + int64_t(C) * 512 + k] = rn_sgd(a, sl.r, fc_off + int64_t(C) * 512 + k,
+                                              W[fc_off + int64_t(C) * 512 + k], t);
   }
 }
 
@@ -1338,6 +1353,8 @@ Net to_net(const pb_resnet_train_args& t, const Plan& pl) {
   a.C = t.C; a.BS = t.BS; a.bs = t.batch_size; a.epochs = t.epochs; a.step = 0;
   a.lr = t.lr;
   a.timeline = t.timeline;
+  a.w0 = t.w0; a.ctrl_g = t.ctrl_g; a.ctrl_c = t.ctrl_c; a.ctrl_stride = t.ctrl_stride;
+  a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;
   return a;
 }
 
@@ -1718,7 +1735,7 @@ extern "C" int pb_resnet_train_group(const pb_resnet_train_args* args, void* str
   if (!args) return pb::fail(PB_ERR_INVALID, "pb_resnet_train_group: null args");
   const pb_resnet_train_args& t = *args;
   if (t.g < 0 || t.C < 2 || t.C > 128 || t.BS < 1 || t.BS > kMaxBS || t.epochs < 1 || !t.w || !t.active ||
-      t.sweeps < 0 || t.w_stride % 4 != 0)
+      t.sweeps < 0 || t.w_stride % 4 != 0 || (t.mu != 0.0f && !t.w0) || (t.ctrl_c && t.ctrl_stride <= 0))
     return pb::fail(PB_ERR_INVALID, "pb_resnet_train_group: bad arguments");
   Plan pl = make_plan(t.BS, t.C);
   if (t.w_stride < pl.P) return pb::fail(PB_ERR_INVALID, "pb_resnet_train_group: w_stride < model size");

@@ -57,9 +57,10 @@ def _fill(a: ResnetTrainArgs, ws: dict, slots: int, BS: int, C: int) -> None:
 
 def resnet_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, bad, *,
                        spec: ModelSpec, epochs: int, batch_size: int, lr: float, terms: dict,
-                       timeline=None) -> None:
-    if terms.get("mu") or terms.get("ctrl_g") is not None or terms.get("ctrl_c"):
-        raise NotImplementedError("the ResNet-18 path trains plain SGD (FedAvg / FedNova local rule)")
+                       state_work=None, timeline=None) -> None:
+    """Every client's local SGD run (pb_resnet_train_group); ``terms`` are the
+    plugin's fused gradient terms (FedProx mu, SCAFFOLD controls with the
+    clients' control rows in ``state_work``), as on the CNN path."""
     G = len(n)
     BS, _, rank, active = sweep_plan(n, batch_size, epochs)
     if BS > MAX_BATCH:
@@ -85,6 +86,14 @@ def resnet_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, step
     _fill(a, ws, G, BS, spec.n_classes)
     a.batch_size, a.epochs, a.lr = batch_size, epochs, lr
     a.timeline = ptr(timeline)
+    a.w0 = ptr(w0)
+    a.mu = terms.get("mu", 0.0)
+    a.ctrl_g, a.cg = ptr(terms.get("ctrl_g")), terms.get("cg", 0.0)
+    ctrl_c = state_work if terms.get("ctrl_c") else None
+    if terms.get("ctrl_c") and ctrl_c is None:
+        raise ValueError("SCAFFOLD control terms need the clients' state rows")
+    a.ctrl_c, a.ctrl_stride, a.cc = ptr(ctrl_c), (ctrl_c.stride(0) if ctrl_c is not None else 0), \
+        terms.get("cc", 0.0)
     lib.check(lib.pb_resnet_train_group(ctypes.byref(a), stream_of(w_out)))
 
 

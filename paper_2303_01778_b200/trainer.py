@@ -473,7 +473,7 @@ def train_group(plugin: "AlgorithmPlugin", spec: ModelSpec, data: ClientData,
         from .resnet import resnet_train_group
         resnet_train_group(data, inputs.rows_d, inputs.off_d, n, w0, w_out, loss, steps, bad,
                            spec=spec, epochs=epochs, batch_size=batch_size, lr=lr, terms=terms,
-                           timeline=stamps)
+                           state_work=state_work, timeline=stamps)
     else:
         raise ValueError(f"unknown model kind {spec.kind!r}")
     t1.record()

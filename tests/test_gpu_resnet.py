@@ -26,6 +26,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
 @pytest.fixture(scope="module")
 def spec():
     from paper_2303_01778_b200.models import resnet_spec
@@ -148,3 +152,51 @@ def test_resnet_stale_workspace_nan(spec, cifar_like):
     poisoned = _device(spec, w0, X, y, 5, 1, 0.02)
     assert np.all(np.isfinite(poisoned[0])) and np.isfinite(poisoned[1])
     assert np.array_equal(clean[0], poisoned[0]) and clean[1] == poisoned[1]
+
+
+def test_resnet_plugin_terms_exact(spec, cifar_like, monkeypatch):
+    """FedProx and SCAFFOLD on the ResNet path (fused into every SGD kernel:
+    conv weights with their bf16 copies, GroupNorm, fc; fedsim/trainer.py
+    :237-257, :288-348).  The terms are pinned by algebra against the FedAvg
+    run on the same data, so no operand rounding enters the comparison:
+    * SCAFFOLD, one step from w0: the forward/backward are FedAvg's, so
+      w1_scaffold - w1_fedavg = -lr * (c - c_m) (random server and client
+      controls) to fp32 rounding;
+    * FedProx, two steps: step one equals FedAvg's (w = w0), step two sees
+      the same weights and adds mu * (w1 - w0), so
+      w2_prox - w2_fedavg = -lr * mu * (w1 - w0)."""
+    import torch
+    import paper_2303_01778_b200 as pb
+    from paper_2303_01778_b200.core import ClientProfile, DataSlice
+    from paper_2303_01778_b200.models import init_params
+    from paper_2303_01778_b200.trainer import ClientData, NamedParams, train_group
+    X, y = cifar_like.features[:40], cifar_like.labels[:40]
+    data = ClientData.from_profiles([ClientProfile(0, 40, DataSlice(X, y, np.arange(40)))], n_classes=10)
+    lr, mu, P = 0.05, 0.5, spec.numel
+    w0 = torch.from_numpy(init_params(spec, 3)).cuda()
+    base = w0.cpu().numpy().astype(np.float64)
+
+    def run(plugin, sweeps, glob=None, work=None):
+        monkeypatch.setenv("PB_CNN_MAX_SWEEPS", str(sweeps))
+        glob = glob if glob is not None else plugin.init_global(NamedParams.from_flat(spec, w0))
+        go = train_group(plugin, spec, data, [0], w0, glob, work, 1, 20, lr, 4, 1)
+        return go.w_out[0].cpu().numpy().astype(np.float64)
+
+    avg1, avg2 = run(pb.FedAvg(lr=lr, batch_size=20), 1), run(pb.FedAvg(lr=lr, batch_size=20), 2)
+    prox2 = run(pb.FedProx(mu=mu, lr=lr, batch_size=20), 2)
+    want = -lr * mu * (avg1 - base)
+    assert np.linalg.norm(want) > 0
+    assert _rel(prox2 - avg2, want) <= 1e-3
+    sc = pb.Scaffold(lr=lr, batch_size=20)
+    glob = sc.init_global(NamedParams.from_flat(spec, w0))
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    for nm in spec.names:
+        t = glob.tensor("server_ctrl_" + nm)
+        t.copy_(1e-2 * torch.randn(t.shape, generator=gen, device="cuda"))
+    work = torch.zeros(1, (P + 3) // 4 * 4, device="cuda")[:, :P]
+    work.copy_(1e-2 * torch.randn(1, P, generator=gen, device="cuda"))
+    sc1 = run(sc, 1, glob, work)
+    c = glob.flat(spec, "server_ctrl_").cpu().numpy().astype(np.float64)
+    cm = work[0].cpu().numpy().astype(np.float64)
+    assert _rel(sc1 - avg1, -lr * (c - cm)) <= 1e-4
+    monkeypatch.setenv("PB_CNN_MAX_SWEEPS", "0")
