@@ -578,12 +578,37 @@ def state_microbench(dev, P: int = 11_173_962, slots: int = 1000, clients: int =
     ok = bool(torch.equal(store[torch.from_numpy(rows).long().to(dev)], work))
     peaks, src = load_peaks()
     gbs = 16.0 * clients * P / (best / 1e3) / 1e9
-    del store, work
+    del store
+    # the StateStore's pinned host tier (clients beyond the HBM budget): the
+    # same kernels read / write the device-mapped rows over the host link
+    hc = 8
+    host = torch.empty(hc, pad, pin_memory=True)[:, :P]
+    host.normal_()
+    hslot = torch.arange(hc, dtype=torch.int32, device=dev)
+    hwork = work[:hc]
+    K.state_gather(hwork, host, hslot)
+    K.state_scatter(host, hwork, hslot)
+    torch.cuda.synchronize()
+    hbest = float("inf")
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        K.state_gather(hwork, host, hslot)
+        K.state_scatter(host, hwork, hslot)
+        b.record()
+        torch.cuda.synchronize()
+        hbest = min(hbest, a.elapsed_time(b))
+    host_ok = bool(torch.equal(host.to(dev), hwork))
+    del work, host
     torch.cuda.empty_cache()
     return {"params": P, "store_slots": slots, "clients": clients, "gather_scatter_ms": best,
             "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
             "algorithmic_bytes": "16 B per parameter per client (gather read+write, scatter read+write)",
-            "round_trip_exact": ok}
+            "round_trip_exact": ok,
+            "host_tier": {"clients": hc, "gather_scatter_ms": hbest,
+                          "link_gbs": 8.0 * hc * P / (hbest / 1e3) / 1e9,
+                          "link_bytes": "8 B per parameter per client over the host link (read + write)",
+                          "round_trip_exact": host_ok}}
 
 
 # ---------------------------------------------------------------------------

@@ -110,7 +110,11 @@ int pb_delta_affine_group(float* out, int64_t out_stride, const float* a, int64_
 /* ---------------------------------------------------------------------------
  * (c) client-state gather / scatter -- fedsim/statestore.py:147-210
  *     (StateStore.load/save) + default_state (fedsim/trainer.py:315-317,
- *     :376-378): slot < 0 gathers the all-zero default state.
+ *     :376-378): gather slot -1 writes the all-zero default state, slot <= -2
+ *     leaves the work row alone (the client lives in another tier); scatter
+ *     skips slot < 0.  `store` may be an HBM matrix or pinned (device-mapped)
+ *     host memory: the host tier of a store larger than its HBM budget is
+ *     moved by the same kernels over the host link.
  * ------------------------------------------------------------------------- */
 int pb_state_gather(float* work, int64_t work_stride, const float* store, int64_t store_stride,
                     const int32_t* slot, int64_t g, int64_t width, void* stream);

@@ -24,7 +24,7 @@ move_rows_vec(V* __restrict__ dst, int64_t dst_stride, const V* __restrict__ src
               const int32_t* __restrict__ slot, int64_t width) {
   const int64_t j = blockIdx.y;
   const int32_t s = slot[j];
-  if (!kGather && s < 0) return;
+  if (kGather ? s < -1 : s < 0) return;   // gather: -1 = default (zeros), <= -2 = another tier
   V* d = kGather ? dst + j * dst_stride : dst + int64_t(s) * dst_stride;
   const V* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride : nullptr) : src + j * src_stride;
   // each CTA streams one contiguous 64 KB chunk of the row, kU independent
@@ -53,7 +53,7 @@ __global__ void move_rows_scalar(float* __restrict__ dst, int64_t dst_stride,
                                  const int32_t* __restrict__ slot, int64_t width) {
   const int64_t j = blockIdx.y;
   const int32_t s = slot[j];
-  if (!kGather && s < 0) return;
+  if (kGather ? s < -1 : s < 0) return;
   float* d = kGather ? dst + j * dst_stride : dst + int64_t(s) * dst_stride;
   const float* srow = kGather ? (s >= 0 ? src + int64_t(s) * src_stride : nullptr)
                               : src + j * src_stride;

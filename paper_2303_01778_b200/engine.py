@@ -259,7 +259,8 @@ class DeviceRuntime:
         work = None
         if plugin.is_stateful:
             if not self.store.configured:   # a fresh store behind a bare DeviceWorker
-                self.store.configure(plugin.state_names(spec), [sh for *_, sh in spec.columns()])
+                self.store.configure(plugin.state_names(spec), [sh for *_, sh in spec.columns()],
+                                     capacity=self.cfg.total_clients)
             work = torch.empty(len(clients), (spec.numel + 3) // 4 * 4, device=w0.device)[:, :spec.numel]
             if self.shard is not None:
                 self.shard.gather(executed, work)
@@ -494,7 +495,7 @@ class SimulationEngine:
             self.global_bundle = plugin.init_global(start)
         if plugin.is_stateful and not uses_hooks(plugin) and not store.configured:
             names = plugin.state_names(self.spec)
-            store.configure(names, [sh for _, _, _, sh in self.spec.columns()])
+            store.configure(names, [sh for _, _, _, sh in self.spec.columns()], capacity=cfg.total_clients)
         self._world, self._rank = 1, 0
         if torch.distributed.is_available() and torch.distributed.is_initialized():
             self._world = torch.distributed.get_world_size()

@@ -21,7 +21,15 @@ persist="async" -- files are written by a background thread, ``flush()``
                    waits for them;
 persist="none"  -- HBM only (the bench's mode); ``flush_to_disk()`` can still
                    spill everything on demand.
+
+Capacity tiers (``hbm_bytes``): when M x width exceeds the HBM budget, the
+first clients to save fill the HBM matrix and the rest live in a pinned
+(device-mapped) host tier of fixed-size chunks; the same gather/scatter
+kernels move both tiers, the host tier over the host link (one launch per
+tier and chunk, no staging copy).  ``configure(..., capacity=M)`` sizes the
+HBM matrix once, so a store never grows by reallocating and copying it.
 """
+
 
 from __future__ import annotations
 
@@ -109,7 +117,8 @@ class StateStore:
     """Per-client state, HBM-resident, optionally mirrored to FSST files."""
 
     def __init__(self, root: str | Path | None = None, persist: str | None = None,
-                 device: torch.device | None = None):
+                 device: torch.device | None = None, hbm_bytes: int | None = None,
+                 host_chunk_bytes: int = 256 << 20):
         if persist is None:
             persist = "sync" if root is not None else "none"
         if persist not in ("sync", "async", "none"):
@@ -125,8 +134,14 @@ class StateStore:
         self._saves = 0
         self._live: set[int] = set()
         self._peak_live = 0
-        self._slot: dict[int, int] = {}
+        self._slot: dict[int, int] = {}            # HBM tier: client -> row of _rows
         self._rows: torch.Tensor | None = None
+        self._hbm_budget = hbm_bytes               # None: no HBM limit
+        self._capacity: int | None = None          # expected clients (configure)
+        self._hslot: dict[int, tuple[int, int]] = {}   # host tier: client -> (chunk, row)
+        self._hchunks: list[torch.Tensor] = []     # pinned [chunk_rows, width] views
+        self._host_chunk_bytes = int(host_chunk_bytes)
+        self._chunk_rows = 0
         self._schema: list[tuple[str, tuple[int, ...]]] | None = None
         self._width = 0
         self._queue: "queue.Queue | None" = None
@@ -187,30 +202,73 @@ class StateStore:
         """True once the payload layout is known (configure() or a first save)."""
         return self._schema is not None
 
-    def configure(self, names: Sequence[str], shapes: Sequence[tuple[int, ...]]) -> None:
-        """Declare the payload layout up front (the engine does this)."""
+    def configure(self, names: Sequence[str], shapes: Sequence[tuple[int, ...]],
+                  capacity: int | None = None) -> None:
+        """Declare the payload layout up front (the engine does this, with
+        capacity = the number of clients, so the HBM matrix is allocated once)."""
         self._set_schema({n: np.zeros(s, dtype=np.float32) for n, s in zip(names, shapes)})
+        if capacity is not None:
+            self._capacity = int(capacity)
+            if self._rows is None:
+                self._ensure_rows(min(self._capacity, self._hbm_cap()))
+
+    def _pad(self) -> int:
+        # row stride padded to 16 bytes: the gather/scatter kernels move rows
+        # with 16-byte vectors
+        return (self._width + 3) // 4 * 4
+
+    def _hbm_cap(self) -> int:
+        """Most rows the HBM tier may hold (the budget over the padded row)."""
+        if self._hbm_budget is None:
+            return 1 << 62
+        return int(self._hbm_budget) // (4 * self._pad())
 
     def _ensure_rows(self, need: int) -> None:
         cap = 0 if self._rows is None else self._rows.shape[0]
-        if need <= cap:
+        if need <= cap or need <= 0:
             return
-        new_cap = max(need, 2 * cap, 64)
-        # row stride padded to 16 bytes: the gather/scatter kernels move rows
-        # with 16-byte vectors
-        pad = (self._width + 3) // 4 * 4
-        rows = torch.zeros(new_cap, pad, device=self._dev())[:, :self._width]
+        if self._capacity is not None:   # sized once for every client the HBM tier can hold
+            new_cap = max(need, min(self._capacity, self._hbm_cap()))
+        else:
+            new_cap = min(max(need, 2 * cap, 64), self._hbm_cap())
+        rows = torch.zeros(new_cap, self._pad(), device=self._dev())[:, :self._width]
         if self._rows is not None:
             rows[:cap].copy_(self._rows)
         self._rows = rows
 
     def _slot_for(self, client_id: int) -> int:
+        """The client's HBM row, or -2 when it lives in the host tier (a home
+        is assigned at the first save and never changes)."""
         s = self._slot.get(client_id)
-        if s is None:
+        if s is not None:
+            return s
+        if client_id in self._hslot:
+            return -2
+        if len(self._slot) < self._hbm_cap():
             s = len(self._slot)
             self._slot[client_id] = s
             self._ensure_rows(s + 1)
-        return s
+            return s
+        n = len(self._hslot)
+        if self._chunk_rows == 0:
+            self._chunk_rows = max(1, self._host_chunk_bytes // (4 * self._pad()))
+        k, r = divmod(n, self._chunk_rows)
+        if k == len(self._hchunks):
+            self._hchunks.append(torch.zeros(self._chunk_rows, self._pad(),
+                                             pin_memory=True)[:, :self._width])
+        self._hslot[client_id] = (k, r)
+        return -2
+
+    def _row(self, client_id: int) -> torch.Tensor:
+        """The client's stored row (an HBM or pinned-host view)."""
+        s = self._slot_for(client_id)
+        if s >= 0:
+            return self._rows[s]
+        k, r = self._hslot[client_id]
+        return self._hchunks[k][r]
+
+    def _has_row(self, client_id: int) -> bool:
+        return client_id in self._slot or client_id in self._hslot
 
     def _flat(self, payload: Mapping[str, object]) -> torch.Tensor:
         parts = []
@@ -238,23 +296,22 @@ class StateStore:
         store was opened is picked up with its own round)."""
         rnd, payload = self._read_file(client_id)
         self._set_schema(payload)
-        s = self._slot_for(client_id)
-        self._rows[s].copy_(self._flat(payload))
+        self._row(client_id).copy_(self._flat(payload))
         with self._lock:
             self._last_round[client_id] = rnd
 
     # -- reference API ----------------------------------------------------------
     def load(self, client_id: int,
              default_factory: Callable[[], Mapping[str, object]] | None = None) -> ClientState | None:
-        if client_id not in self._slot and self._has_file(client_id):
+        if not self._has_row(client_id) and self._has_file(client_id):
             self._page_in(client_id)
-        if client_id not in self._slot:
+        if not self._has_row(client_id):
             if default_factory is None:
                 return None
             with self._lock:
                 self._track_checkout(client_id)
             return ClientState(client_id, -1, dict(default_factory()))
-        row = self._rows[self._slot[client_id]].clone()
+        row = self._row(client_id).to(self._dev(), copy=True)
         with self._lock:
             self._loads += 1
             self._track_checkout(client_id)
@@ -263,9 +320,9 @@ class StateStore:
     def save(self, client_id: int, round_num: int, payload: Mapping[str, object]) -> None:
         self._check_rounds([client_id], round_num)
         self._set_schema(payload)
-        s = self._slot_for(client_id)
-        self._rows[s].copy_(self._flat(payload))
-        self._commit([client_id], round_num, rows=self._rows[s:s + 1])
+        row = self._row(client_id)
+        row.copy_(self._flat(payload))
+        self._commit([client_id], round_num, rows=row.view(1, -1))
 
     def stats(self) -> StateStoreStats:
         self.flush()
@@ -281,19 +338,25 @@ class StateStore:
         """Load the listed clients' states into work rows [G, width] (zeros for
         never-saved clients) with one gather kernel."""
         from . import _kernels as K
-        for c in client_ids:
-            if c not in self._slot and self._has_file(c):
+        ids = [int(c) for c in client_ids]
+        for c in ids:
+            if not self._has_row(c) and self._has_file(c):
                 self._page_in(c)
-        slots = np.array([self._slot.get(int(c), -1) for c in client_ids], dtype=np.int32)
+        # -1: never saved (default zeros), -2: the row lives in another tier
+        slots = np.array([self._slot.get(c, -2 if c in self._hslot else -1) for c in ids], dtype=np.int32)
         with self._lock:
-            self._loads += int((slots >= 0).sum())
-            for c in client_ids:
-                self._track_checkout(int(c))
-        if self._rows is None:
-            work.zero_()
-            return
-        slot_d = torch.from_numpy(slots).to(work.device)
-        K.state_gather(work, self._rows, slot_d)
+            self._loads += sum(1 for c in ids if self._has_row(c))
+            for c in ids:
+                self._track_checkout(c)
+        if self._rows is not None:
+            K.state_gather(work, self._rows, torch.from_numpy(slots).to(work.device))
+        elif (slots == -1).any():
+            work[torch.from_numpy(np.flatnonzero(slots == -1)).to(work.device)] = 0.0
+        for k, chunk in enumerate(self._hchunks):   # host tier: read over the host link
+            hs = np.array([self._hslot[c][1] if self._hslot.get(c, (-1, 0))[0] == k else -2 for c in ids],
+                          dtype=np.int32)
+            if (hs >= 0).any():
+                K.state_gather(work, chunk, torch.from_numpy(hs).to(work.device))
 
     def scatter(self, client_ids: Sequence[int], round_num: int, work: torch.Tensor) -> None:
         """Persist the group's new states (rows of ``work``) for ``round_num``."""
@@ -305,7 +368,13 @@ class StateStore:
         if self._schema is None:
             raise ValueError("state store schema unknown; call configure() first")
         slots = np.array([self._slot_for(c) for c in ids], dtype=np.int32)
-        K.state_scatter(self._rows, work, torch.from_numpy(slots).to(work.device))
+        if self._rows is not None and (slots >= 0).any():
+            K.state_scatter(self._rows, work, torch.from_numpy(slots).to(work.device))
+        for k, chunk in enumerate(self._hchunks):   # host tier: written over the host link
+            hs = np.array([self._hslot[c][1] if self._hslot.get(c, (-1, 0))[0] == k else -1 for c in ids],
+                          dtype=np.int32)
+            if (hs >= 0).any():
+                K.state_scatter(chunk, work, torch.from_numpy(hs).to(work.device))
         self._commit(ids, round_num, rows=work)
 
     # -- commit / persistence -----------------------------------------------------
@@ -392,14 +461,24 @@ class StateStore:
             self.root.mkdir(parents=True, exist_ok=True)
         if self.root is None:
             raise ValueError("no root directory to flush to")
-        if self._rows is None:
-            return
-        host = self._rows.detach().to("cpu", torch.float64).numpy()
-        for c, s in self._slot.items():
-            self._write_file(c, self._last_round[c], host[s])
+        if self._rows is not None:
+            host = self._rows.detach().to("cpu", torch.float64).numpy()
+            for c, s in self._slot.items():
+                self._write_file(c, self._last_round[c], host[s])
+        torch.cuda.synchronize(self._dev())   # host-tier rows written by kernels
+        for c, (k, r) in self._hslot.items():
+            self._write_file(c, self._last_round[c], self._hchunks[k][r].double().numpy())
 
     def hbm_bytes(self) -> int:
-        return 0 if self._rows is None else self._rows.numel() * 4
+        return 0 if self._rows is None else self._rows.shape[0] * self._pad() * 4
+
+    def host_bytes(self) -> int:
+        """Pinned host-tier bytes (clients beyond the HBM budget)."""
+        return sum(c.shape[0] * self._pad() * 4 for c in self._hchunks)
+
+    def tier_of(self, client_id: int) -> str | None:
+        """'hbm', 'host' or None (never saved in this process)."""
+        return "hbm" if client_id in self._slot else ("host" if client_id in self._hslot else None)
 
     def close(self) -> None:
         self.flush()
