@@ -198,9 +198,10 @@ typedef struct {
   float* ws_dp1;
   float* ws_dht;            /* per slot: 512*32 f32 (dH transposed, zero-padded) */
   /* Low-rank fc1 for plain SGD (mu = 0, no control variates); all NULL for
-   * the direct per-client fc1.  Client row r owns history rows
-   * [lz_hoff[r], lz_hoff[r] + lz_hlen[r]) of lz_rows, lz_hlen[r] =
-   * round_up(steps_r*BS, 32);
+   * the direct per-client fc1.  The history and W0 copies are bf16 (the
+   * tensor-core operands, rounded to nearest once when written).  Client row
+   * r owns history rows [lz_hoff[r], lz_hoff[r] + lz_hlen[r]) of lz_rows,
+   * lz_hlen[r] = round_up(steps_r*BS, 64);
    * step t's sample i is row t*BS + i.  Every client's fc1 weights stay
    * W0 - lr * sum_t dH_t^T X_t during the round (never materialised per
    * step); they are written to w once, after the last sweep.  The history
@@ -208,17 +209,18 @@ typedef struct {
    * written by exact zeros (the kernels zero each client's dH^T pad
    * columns), so the four history buffers need only hold FINITE values on
    * entry (zero them once after allocation or after a diverged client). */
-  float* lz_hx;             /* [lz_rows, 3136] f32                            */
-  float* lz_hxt;            /* [3136, lz_rows] f32                            */
-  float* lz_hd;             /* [lz_rows, 512] f32                             */
-  float* lz_hdt;            /* [512, lz_rows] f32                             */
+  void* lz_hx;              /* [lz_rows, 3136] bf16                           */
+  void* lz_hxt;             /* [3136, lz_rows] bf16                           */
+  void* lz_hd;              /* [lz_rows, 512] bf16                            */
+  void* lz_hdt;             /* [512, lz_rows] bf16                            */
   const int64_t* lz_hoff;   /* [g]                                            */
   const int32_t* lz_hlen;   /* [g]                                            */
-  float* lz_w0t;            /* [3136*512] f32 scratch (W1 of w0 transposed)   */
+  void* lz_w0t;             /* 2*3136*512 bf16 scratch: W1 of w0 transposed,  */
+                            /* then as is                                     */
   float* lz_zp;             /* max_t active_t*njt_t * 512*32 f32, njt_t = ceil(t*BS/128) */
-  float* lz_gdt;            /* max_t active_t*njt_t * 32*128 f32              */
+  void* lz_gdt;             /* max_t active_t*njt_t * 32*128 bf16             */
   float* lz_fpart;          /* max(74, g)*512*32 f32: forward GEMM partials   */
-  int64_t lz_rows;          /* total history rows (multiple of 32)            */
+  int64_t lz_rows;          /* total history rows (multiple of 64)            */
   int32_t lz_defer;         /* 1: leave the fc1 block of w unmaterialised      */
                             /*    (fold it with pb_cnn_lazy_fold instead)      */
   int32_t lz_switch;        /* > 0: from sweep lz_switch on, the clients still */
@@ -242,13 +244,15 @@ int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
  *   acc += wsum * W0 - lr * sum_j w_j * HD_j^T HX_j
  * over the device's clients j, whose history rows are [row_lo, row_hi) of
  * the round's [lz_rows] history (pb_cnn_train_group with lz_defer = 1).
- * Scales the clients' hdt columns in place (round scratch).  part: splits *
- * 512 * 3136 f32 scratch. */
+ * The weighted dH^T columns w_j * dH_j are split into two bf16 terms (high
+ * part in hdt in place -- round scratch --, low part in hdt_lo), so the
+ * weighting is exact to ~2^-17 and both terms run on bf16 tensor cores.
+ * part: splits * 512 * 3136 f32 scratch. */
 typedef struct {
   float* acc;               /* [512*3136] fc1_w accumulator of the partial     */
   const float* w0;          /* [P] round-start model                           */
-  const float* hxt;         /* [3136, hrows]                                   */
-  float* hdt;               /* [512, hrows] (scaled in place)                  */
+  const void* hxt;          /* [3136, hrows] bf16                              */
+  void* hdt;                /* [512, hrows] bf16 (overwritten: w_j * dH, high) */
   int64_t hrows, row_lo, row_hi;
   const int64_t* hoff;      /* [nclients] first history row of each client    */
   const int32_t* nrows;     /* [nclients] live history rows (steps * BS)       */
@@ -257,6 +261,7 @@ typedef struct {
   float* part;
   int32_t splits;
   float wsum, lr;
+  void* hdt_lo;             /* [512, hrows] bf16 scratch: w_j * dH, low part   */
 } pb_cnn_lazy_fold_args;
 int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream);
 

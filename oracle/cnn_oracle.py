@@ -92,6 +92,11 @@ def _tf32(x: torch.Tensor) -> torch.Tensor:
     return (f.view(torch.int32) & -8192).view(torch.float32).to(x.dtype)
 
 
+def _bf16(x: torch.Tensor) -> torch.Tensor:
+    """round to nearest bf16 (how the low-rank fc1 stores W0, X and dH)."""
+    return x.to(torch.bfloat16).to(x.dtype)
+
+
 def _tf32_rna(x: torch.Tensor) -> torch.Tensor:
     """fp32 -> tf32 rounded to nearest, ties away (cvt.rna.tf32.f32): how the
     low-rank fc1 stores X and dH."""
@@ -153,10 +158,11 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
 
     fc1_base (with emulate_bf16): the round-start fc1 weights W0 of a device
     run that used the low-rank fc1 (csrc/cnn_lazy.cu), whose tensor cores see
-    tf32(W0) plus the client's accumulated update in (near) full precision
-    instead of tf32(W_t): the emulated weight is tf32(W0) + (W_t - W0), and X
-    and dL/dz1 (fc1 bias gradient included) are rounded to nearest tf32, as
-    that path stores them."""
+    bf16(W0) plus the client's accumulated update in (near) full precision
+    instead of a rounded W_t: the emulated weight is bf16(W0) + (W_t - W0),
+    and X and dL/dz1 (fc1 bias gradient included) are rounded to nearest
+    bf16, as that path stores them (its Gram corrections carry high + low
+    bf16 terms, i.e. are exact to ~2^-17)."""
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
     if emulate_bf16:
@@ -173,8 +179,8 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
         if fc1_base is None:
             h = F.relu(_TruncGrad.apply(_TruncValue.apply(h) @ _TruncValue.apply(f1w).t()) + f1b)
         else:
-            w1 = f1w - fc1_base + _tf32(fc1_base)
-            h = F.relu(_RnaGrad.apply(_RnaValue.apply(h) @ w1.t() + f1b))
+            w1 = f1w - fc1_base + _bf16(fc1_base)
+            h = F.relu(_RoundGrad.apply(_RoundValue.apply(h) @ w1.t() + f1b))
     else:
         h = F.relu(h @ f1w.t() + f1b)
     return h @ f2w.t() + f2b
@@ -222,7 +228,7 @@ def decision_margins(params, x: torch.Tensor, fc1_base: torch.Tensor | None = No
         if fc1_base is None:
             z3 = _tf32(h) @ _tf32(f1w).t() + f1b
         else:
-            z3 = _tf32_rna(h) @ (f1w - fc1_base + _tf32(fc1_base)).t() + f1b
+            z3 = _bf16(h) @ (f1w - fc1_base + _bf16(fc1_base)).t() + f1b
         out["relu3"] = float(z3.abs().min()) / rms(z3)
     return out
 

@@ -55,23 +55,25 @@ class _LazyWorkspace:
         # client finite (GroupOutcome.resolve clears it)
         self.dirty = True
 
-    def _get(self, name: str, numel: int, device) -> torch.Tensor:
+    def _get(self, name: str, numel: int, device, dtype=torch.float32) -> torch.Tensor:
         t = self.buf.get(name)
-        if t is None or t.numel() < numel or t.device != device:
+        if t is None or t.numel() < numel or t.device != device or t.dtype != dtype:
             # 2x headroom: round sizes vary (the longest client sets the
             # history length), and a reallocation synchronises
             self.buf.pop(name, None)
-            t = torch.empty(max(int(numel * 2.0), 4), dtype=torch.float32, device=device)
+            t = torch.empty(max(int(numel * 2.0), 8), dtype=dtype, device=device)
             self.buf[name] = t
             if name in self.HISTORY:
                 self.dirty = True
         return t
 
     def get(self, rows: int, zp: int, gdt: int, slots: int, device) -> dict[str, torch.Tensor]:
-        out = {"hx": self._get("hx", rows * 3136, device), "hxt": self._get("hxt", rows * 3136, device),
-               "hd": self._get("hd", rows * 512, device), "hdt": self._get("hdt", rows * 512, device),
-               "w0t": self._get("w0t", 3136 * 512, device), "zp": self._get("zp", zp, device),
-               "gdt": self._get("gdt", gdt, device), "fpart": self._get("fpart", max(74, slots) * 512 * 32, device)}
+        b16 = torch.bfloat16   # the history and the W0 copies are bf16 tensor-core operands
+        out = {"hx": self._get("hx", rows * 3136, device, b16), "hxt": self._get("hxt", rows * 3136, device, b16),
+               "hd": self._get("hd", rows * 512, device, b16), "hdt": self._get("hdt", rows * 512, device, b16),
+               "w0t": self._get("w0t", 2 * 3136 * 512, device, b16), "zp": self._get("zp", zp, device),
+               "gdt": self._get("gdt", gdt, device, b16),
+               "fpart": self._get("fpart", max(74, slots) * 512 * 32, device)}
         # The history GEMMs read whole 32-row chunks: rows a client has not
         # written this round are multiplied by exact zeros (dH^T pad columns
         # are zeroed by the head kernels, Gram rows past the live ones are
@@ -97,15 +99,17 @@ def lazy_enabled(terms: dict) -> bool:
 
 
 def lazy_plan(total: np.ndarray, active: np.ndarray, BS: int):
-    """History layout: client row r owns hlen[r] = round_up(steps_r * BS, 32)
-    rows from hoff[r]; partial-buffer capacities over the sweeps."""
-    hlen = ((total * BS + 31) // 32 * 32).astype(np.int32)
+    """History layout: client row r owns hlen[r] = round_up(steps_r * BS, 64)
+    rows from hoff[r] (64 bf16 = one 128-byte operand row of history
+    columns); partial-buffer capacities over the sweeps (the Gram rows hold
+    a high and a low bf16 term: 64 rows per slot)."""
+    hlen = ((total * BS + 63) // 64 * 64).astype(np.int32)
     hoff = np.zeros(len(total), dtype=np.int64)
     if len(total) > 1:
         hoff[1:] = np.cumsum(hlen[:-1], dtype=np.int64)
     njt = (np.arange(len(active)) * BS + 127) // 128
     cap = int((active.astype(np.int64) * njt).max()) if len(active) else 0
-    return hlen, hoff, int(hlen.sum()), cap * 512 * 32, cap * 32 * 128
+    return hlen, hoff, int(hlen.sum()), cap * 512 * 32, cap * 64 * 128
 
 
 class LazyFc1:
@@ -156,12 +160,14 @@ class LazyFc1:
         nrows = h2d(nr, d)
         w = h2d(weights, d)
         part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
+        lo_buf = _LZ._get("hdt_lo", self.rows * 512, d, torch.bfloat16)
         f = LazyFoldArgs()
         f.acc, f.w0, f.hxt, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hxt"]), ptr(self.lz["hdt"])
         f.hrows, f.row_lo, f.row_hi = self.rows, lo, hi
         f.hoff, f.nrows, f.w, f.nclients = ptr(hoff), ptr(nrows), ptr(w), len(rows)
         f.part, f.splits = ptr(part), self.SPLITS
         f.wsum, f.lr = float(np.sum(weights.astype(np.float64))), self.lr
+        f.hdt_lo = ptr(lo_buf)
         lib.check(lib.pb_cnn_lazy_fold(ctypes.byref(f), stream_of(acc)))
 
 

@@ -123,11 +123,11 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   const float* W = a.w + int64_t(sl.r) * a.P;
   if (a.hx && blockIdx.x == 0) {
     // lazy fc1: the history rows [cnt, pad) of this step (partial batch,
-    // 32-row padding after the last step) are exact zeros
+    // 64-row padding after the last step) are exact zeros
     const int64_t r0 = sl.hist + int64_t(a.step) * a.BS;
-    float4* z = reinterpret_cast<float4*>(a.hx + (r0 + sl.cnt) * kFlat);
-    const int n4 = int(sl.pad_ - int64_t(a.step) * a.BS - sl.cnt) * (kFlat / 4);
-    for (int e = tid; e < n4; e += kFwdThreads) z[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    uint4* z = reinterpret_cast<uint4*>(a.hx + (r0 + sl.cnt) * kFlat);
+    const int n8 = int(sl.pad_ - int64_t(a.step) * a.BS - sl.cnt) * (kFlat / 8);
+    for (int e = tid; e < n8; e += kFwdThreads) z[e] = make_uint4(0, 0, 0, 0);
   }
   stage_w2(sW2, W, tid, kFwdThreads);
   // conv1 B: column n = d*32 + co, K = (u, v) of the 6x6 window:
@@ -233,6 +233,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       const uint32_t th = tmem + uint32_t((j & 1) * 128);
       const int64_t sid = sidx(blockIdx.y, j, a.BS);
       float* p2 = p2_row(a, sl, blockIdx.y, j);
+      bf16* hxr = a.hx ? hx_row(a, sl, j) : nullptr;   // lazy fc1: X_t into the bf16 history
       uint8_t* am2 = a.am2 + sid * kFlat;
       const int q = warp & 3, part = warp >> 2;   // lane quarter, 8-column slice
 #pragma unroll 1
@@ -266,7 +267,10 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
               arg = d;
             }
           }
-          p2[pp * 64 + co] = a.hx ? tf32_rna(best) : best;
+          if (hxr)
+            hxr[pp * 64 + co] = __float2bfloat16_rn(best);
+          else
+            p2[pp * 64 + co] = best;
           am2[pp * 64 + co] = uint8_t(arg);
         }
         work_sync();  // sZ is free again
@@ -581,7 +585,8 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   // dH = dlogits W2 (old weights) masked by relu'; stored [i][o] and [o][i<32]
   // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
   const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
-  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(slot, 0, a.BS) * kH1;
+  float* dh = a.dh + sidx(slot, 0, a.BS) * kH1;
+  bf16* dhb = a.hx ? a.hd + lzrow * kH1 : nullptr;   // lazy fc1: the bf16 history rows
   // per output o (thread-owned column), 8 classes per pass: their W2 loads
   // are in flight together, the samples stream from smem (dlogits as 16 B
   // loads), dH[i][o] accumulates in sDH in class order, the fc2 gradient of
@@ -618,22 +623,26 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     }
     for (int i = 0; i < cnt; ++i) {
       float gi = sH[i * kH1 + o] > 0.0f ? sDH[i * kDHS + o] : 0.0f;
-      if (a.hx) gi = tf32_rna(gi);
-      dh[i * kH1 + o] = gi;
+      if (dhb) {
+        gi = bf16r(gi);
+        dhb[i * kH1 + o] = __float2bfloat16_rn(gi);
+      } else {
+        dh[i * kH1 + o] = gi;
+      }
       sDH[i * kDHS + o] = gi;
     }
   }
   __syncthreads();  // sDH complete
   if (a.hx) {
     // dH^T columns of the global [512][hrows] history (row pitch hrows)
-    float* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
+    bf16* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
     const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);   // columns [cnt, zc) -> 0
     for (int p = tid; p < zc * (ohi - olo); p += kHeadDenseThreads) {
       const int o = olo + p / zc, i = p - (o - olo) * zc;
-      hdt[int64_t(o) * a.hrows + i] = i < cnt ? sDH[i * kDHS + o] : 0.0f;
+      hdt[int64_t(o) * a.hrows + i] = __float2bfloat16_rn(i < cnt ? sDH[i * kDHS + o] : 0.0f);
     }
     for (int p = tid; p < (zc - cnt) * (ohi - olo); p += kHeadDenseThreads)   // and rows [cnt, zc) of hd
-      dh[int64_t(cnt + p / (ohi - olo)) * kH1 + olo + p % (ohi - olo)] = 0.0f;
+      dhb[int64_t(cnt + p / (ohi - olo)) * kH1 + olo + p % (ohi - olo)] = __float2bfloat16_rn(0.0f);
     for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kDHS + o];
@@ -812,27 +821,32 @@ __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThread
   }
   __syncthreads();
   const int64_t lzrow = sl.hist + int64_t(a.step) * BS;
-  float* dh = a.hx ? a.hd + lzrow * kH1 : a.dh + sidx(slot, 0, BS) * kH1;
+  float* dh = a.dh + sidx(slot, 0, BS) * kH1;
+  bf16* dhb = a.hx ? a.hd + lzrow * kH1 : nullptr;   // lazy fc1: the bf16 history rows
   for (int e = tid; e < cnt * kTailO; e += kHeadThreads) {
     const int i = e >> 6, c = e & 63;
     float v = sAcc[i * kTailO + c];
 #pragma unroll
     for (int q = 1; q < kTailCg; ++q) v += sAcc[(q * BS + i) * kTailO + c];
     float gi = sH[i * kTailS + c] > 0.0f ? v : 0.0f;
-    if (a.hx) gi = tf32_rna(gi);
-    dh[int64_t(i) * kH1 + olo + c] = gi;
+    if (dhb) {
+      gi = bf16r(gi);
+      dhb[int64_t(i) * kH1 + olo + c] = __float2bfloat16_rn(gi);
+    } else {
+      dh[int64_t(i) * kH1 + olo + c] = gi;
+    }
     sDH[i * kTailS + c] = gi;
   }
   __syncthreads();
   if (a.hx) {
-    float* hdt = a.hdt + sl.hist + int64_t(a.step) * BS;
+    bf16* hdt = a.hdt + sl.hist + int64_t(a.step) * BS;
     const int zc = int(sl.pad_ - int64_t(a.step) * BS);   // columns [cnt, zc) -> 0
     for (int p = tid; p < zc * kTailO; p += kHeadThreads) {
       const int oo = p / zc, i = p - oo * zc;
-      hdt[int64_t(olo + oo) * a.hrows + i] = i < cnt ? sDH[i * kTailS + oo] : 0.0f;
+      hdt[int64_t(olo + oo) * a.hrows + i] = __float2bfloat16_rn(i < cnt ? sDH[i * kTailS + oo] : 0.0f);
     }
     for (int p = tid; p < (zc - cnt) * kTailO; p += kHeadThreads)   // and rows [cnt, zc) of hd
-      dh[int64_t(cnt + p / kTailO) * kH1 + olo + p % kTailO] = 0.0f;
+      dhb[int64_t(cnt + p / kTailO) * kH1 + olo + p % kTailO] = __float2bfloat16_rn(0.0f);
     for (int oo = tid; oo < kTailO; oo += kHeadThreads) {   // fc1 bias (sample order)
       float g = 0.0f;
       for (int i = 0; i < cnt; ++i) g += sDH[i * kTailS + oo];
@@ -1216,11 +1230,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       if (!unit) return;
       const int64_t sid = sidx(blockIdx.y, i, a.BS);
       const float4* d4 = reinterpret_cast<const float4*>(a.dp2 + sid * kFlat + upp * 64 + ucb * 8);
-      const float4* p4 = reinterpret_cast<const float4*>(p2_row(a, sl, blockIdx.y, i) + upp * 64 + ucb * 8);
       rd[0] = d4[0];
       rd[1] = d4[1];
-      rp[0] = p4[0];
-      rp[1] = p4[1];
+      if (a.hx) {   // lazy fc1: X_t (only its sign matters here) in the bf16 history
+        const uint4 u = *reinterpret_cast<const uint4*>(hx_row(a, sl, i) + upp * 64 + ucb * 8);
+        const float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y), f2 = unpack_bf16(u.z), f3 = unpack_bf16(u.w);
+        rp[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
+        rp[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+      } else {
+        const float4* p4 = reinterpret_cast<const float4*>(p2_row(a, sl, blockIdx.y, i) + upp * 64 + ucb * 8);
+        rp[0] = p4[0];
+        rp[1] = p4[1];
+      }
       ra = *reinterpret_cast<const uint2*>(a.am2 + sid * kFlat + upp * 64 + ucb * 8);
     };
     float rx[2];
@@ -1670,8 +1691,10 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.rank = t.rank; a.w = t.w; a.w0 = t.w0; a.ctrl_g = t.ctrl_g; a.ctrl_c = t.ctrl_c;
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
-  a.hx = t.lz_hx; a.hxt = t.lz_hxt; a.hd = t.lz_hd; a.hdt = t.lz_hdt; a.hoff = t.lz_hoff;
-  a.hlen = t.lz_hlen; a.w0t = t.lz_w0t; a.zp = t.lz_zp; a.gdt = t.lz_gdt; a.fpart = t.lz_fpart;
+  a.hx = static_cast<bf16*>(t.lz_hx); a.hxt = static_cast<bf16*>(t.lz_hxt);
+  a.hd = static_cast<bf16*>(t.lz_hd); a.hdt = static_cast<bf16*>(t.lz_hdt); a.hoff = t.lz_hoff;
+  a.hlen = t.lz_hlen; a.w0t = static_cast<bf16*>(t.lz_w0t); a.zp = t.lz_zp;
+  a.gdt = static_cast<bf16*>(t.lz_gdt); a.fpart = t.lz_fpart;
   a.hrows = t.lz_rows;
   a.p1g = t.ws_p1; a.am1 = t.ws_am1; a.p2 = t.ws_p2; a.am2 = t.ws_am2; a.h = t.ws_h;
   a.dh = t.ws_dh; a.dp2 = t.ws_dp2; a.dzg = t.ws_dz; a.pg = t.ws_dp1; a.dht = t.ws_dht; a.eval = nullptr;
@@ -1790,7 +1813,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
     if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hxt || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
-        !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 32 || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
+        !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 64 || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
         !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
       return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
     if ((rc = lazy_fc1_prepare(a, s))) {

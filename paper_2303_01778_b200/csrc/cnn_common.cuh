@@ -13,6 +13,7 @@ namespace pb {
 namespace cnn {
 
 using namespace pb::umma;
+using bf16 = __nv_bfloat16;
 
 // ---- model geometry --------------------------------------------------------
 constexpr int kImg = 28, kC1 = 32, kC2 = 64, kH1 = 512, kFlat = 7 * 7 * kC2;  // 3136
@@ -70,19 +71,20 @@ struct Args {
   double* eval;    // [2] correct, loss (eval mode)
   // ---- lazy fc1 (plain SGD): the round's (X, dH) history, see cnn_lazy.cu --
   // Client row r owns history rows [hist_off[r], hist_off[r] + L_r) of
-  // hrows (L_r a multiple of 32); step t's sample i is row t*BS + i.  Stale
-  // rows are finite and meet exact zeros (dH^T pad columns, Gram selects).
-  float* hx;              // [hrows, kFlat]  X_t (the p2 activations)
-  float* hxt;             // [kFlat, hrows]  X transposed
-  float* hd;              // [hrows, kH1]    dH_t = dL/dz1
-  float* hdt;             // [kH1, hrows]    dH transposed
+  // hrows (L_r a multiple of 64); step t's sample i is row t*BS + i.  The
+  // history is bf16 (the tensor-core operands, rounded once when written).
+  // Stale rows are finite and meet exact zeros (pad rows/columns, Gram selects).
+  bf16* hx;               // [hrows, kFlat]  X_t (the p2 activations)
+  bf16* hxt;              // [kFlat, hrows]  X transposed
+  bf16* hd;               // [hrows, kH1]    dH_t = dL/dz1
+  bf16* hdt;              // [kH1, hrows]    dH transposed
   const int64_t* hoff;    // [G] first history row of client row r
-  const int32_t* hlen;    // [G] L_r (multiple of 32)
-  int64_t hrows;          // total history rows (multiple of 32)
+  const int32_t* hlen;    // [G] L_r (multiple of 64)
+  int64_t hrows;          // total history rows (multiple of 64)
   const void* lzmaps;     // host: the round's TMA tensor maps (cnn_lazy.cu)
-  const float* w0t;       // [kFlat][kH1] fc1 block of w0, transposed
+  bf16* w0t;              // [kFlat][kH1] bf16 fc1 block of w0 transposed, then [kH1][kFlat] as is
   float* zp;              // [slots * njt][kH1][32] forward correction partials
-  float* gdt;             // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
+  bf16* gdt;              // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
   float* fpart;           // [ks][active][kH1][32] tail split-K partials (<= 74*16384 f32)
   int64_t* timeline;      // [sweeps + 1] sweep start stamps (real clock) or null
   int64_t P;
@@ -99,20 +101,23 @@ __device__ __forceinline__ float sgd(const Args& a, int r, int64_t idx, float w,
 
 __device__ __forceinline__ int64_t sidx(int j, int i, int BS) { return int64_t(j) * BS + i; }
 
-// Row i of slot j's p2 activations (the fc1 input X_t).  Lazy runs write it
-// straight into the history, where step t of the client is row t*BS + i.
+// Row i of slot j's p2 activations (the fc1 input X_t) in the workspace
+// (direct fc1).  Lazy runs write X_t straight into the bf16 history instead,
+// where step t of the client is row t*BS + i (hx_row).
 __device__ __forceinline__ float* p2_row(const Args& a, const Slot& sl, int j, int i) {
-  return a.hx ? a.hx + (sl.hist + int64_t(a.step) * a.BS + i) * kFlat
-              : a.p2 + sidx(j, i, a.BS) * kFlat;
+  return a.p2 + sidx(j, i, a.BS) * kFlat;
+}
+__device__ __forceinline__ bf16* hx_row(const Args& a, const Slot& sl, int i) {
+  return a.hx + (sl.hist + int64_t(a.step) * a.BS + i) * kFlat;
 }
 
-// fp32 -> tf32, round to nearest (ties away).  The low-rank fc1 stores its
-// tensor-core operands (X, dH and the Gram rows) pre-rounded, so the MMA's
-// truncation is exact and no operand carries truncation bias.
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// fp32 -> bf16 -> fp32 (round to nearest even): the low-rank fc1 keeps its
+// tensor-core operands (X, dH, the Gram rows, W0) as bf16, and every fp32
+// consumer of a stored operand (the fc1 bias gradient) sees the same value.
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+// two packed bf16 (low half first) -> float2
+__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
 }
 
 // NaN-propagating relu / max (torch semantics; fmaxf would drop a NaN and

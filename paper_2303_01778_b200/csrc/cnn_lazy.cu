@@ -12,21 +12,23 @@
 //   forward  Z_t  = X_t W0^T  - lr * sum_s (X_t X_s^T) dH_s      (+ b1, relu)
 //   dgrad    dX_t = dH_t W0   - lr * sum_s (dH_t dH_s^T) X_s
 // The W0 products are shared by all clients of a sweep (one tensor-core GEMM
-// with N = 8 clients x 32 rows); the corrections are rank-(t*BS) products
+// with N = 8 clients x 24 rows); the corrections are rank-(t*BS) products
 // with the client's own history.  After the last sweep each client's W1 is
-// materialised once (W0 - lr * HD^T HX), so the fold and every API above see
-// ordinary per-client weights.
+// materialised once (W0 - lr * HD^T HX) -- or, in FedAvg engine rounds,
+// folded straight from the history (pb_cnn_lazy_fold).
 //
-// All contractions are tcgen05 kind::tf32 (fp32 accumulation in TMEM).  The
-// history operands (X, dH) and the Gram rows are stored rounded to nearest
-// tf32, so the MMA's operand truncation is exact for them and the
-// corrections carry no truncation bias; W0 is truncated.  Every operand tile
-// is one TMA box (32 fp32 of K x up to 256 rows, SWIZZLE_128B K-major,
-// tma.cuh) -- the history is kept as plain row-major matrices ([rows, K] and
-// the transposed [K, rows]) so each client's block is a box of one tensor
-// map.  One thread drives a TMA -> MMA ring; the CTA's other warps only run
-// the epilogues.  Reductions have a fixed order (no atomics): results are
-// deterministic.
+// Precision: the history (X, dH) and a copy of W0 are bf16 -- the operands of
+// kind::f16 tcgen05 MMAs with fp32 accumulation in TMEM, like conv2 -- rounded
+// to nearest once when written; every fp32 consumer of a stored operand (the
+// fc1 bias gradient) uses the same rounded value.  The Gram rows (X_t X_s^T,
+// dH_t dH_s^T), fp32 products of bf16 operands, re-enter a GEMM as TWO bf16
+// terms (high + low, ~2^-17 relative), so the corrections carry no rounding
+// beyond the stored operands'.  Every operand tile is one TMA box of 64 bf16
+// of K (128 B) x up to 256 rows, SWIZZLE_128B K-major (tma.cuh); the history
+// is kept as plain row-major matrices ([rows, K] and the transposed [K, rows])
+// so each client's block is a box of one tensor map.  One thread drives a
+// TMA -> MMA ring; the CTA's other warps run the epilogues.  Reductions have a
+// fixed order (no atomics): results are deterministic.
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
@@ -44,36 +46,51 @@ using pb::tma::ring_barriers;
 using pb::tma::tma_ring;
 
 constexpr int kStages = 4;
+constexpr int kAK = 64;   // K elements (bf16) per 128-byte operand row: one "atom"
 
 // tensor maps of the round (host-encoded, passed as __grid_constant__)
 struct LzMaps {
-  CUtensorMap w0;      // W0 fc1 block  [512][3136],  box 128 rows
-  CUtensorMap w0t;     // W0^T          [3136][512],  box 128
-  CUtensorMap hxa[4];  // HX            [rows][3136], box 32/64/96/128 rows (history tiles)
-  CUtensorMap hxb;     // HX                          box 32  (current rows)
-  CUtensorMap hda[4];  // HD            [rows][512],  box 32/64/96/128
-  CUtensorMap hdb;     // HD                          box 32
-  CUtensorMap hxs;     // HX                          box rs rows (packed current rows, spc > 1)
-  CUtensorMap hds;     // HD                          box rs rows
-  CUtensorMap hdt;     // HD^T          [512][rows],  box 128
-  CUtensorMap hxt128;  // HX^T          [3136][rows], box 128
-  CUtensorMap hxt256;  // HX^T                        box 256
-  CUtensorMap gdt;     // Gram rows     [slots*32][njt*128], box 32 (per sweep)
+  CUtensorMap w0;      // W0 fc1 block bf16 [512][3136],  box 128 rows
+  CUtensorMap w0t;     // W0^T bf16         [3136][512],  box 128
+  CUtensorMap hxa[4];  // HX [rows][3136], box 32/64/96/128 rows (history tiles)
+  CUtensorMap hxb;     // HX               box 32  (current rows)
+  CUtensorMap hda[4];  // HD [rows][512],  box 32/64/96/128
+  CUtensorMap hdb;     // HD               box 32
+  CUtensorMap hxs;     // HX               box rs rows (packed current rows, spc > 1)
+  CUtensorMap hds;     // HD               box rs rows
+  CUtensorMap hdt;     // HD^T [512][rows], box 128
+  CUtensorMap hdtl;    // low part of the weighted HD^T (deferred fold), box 128
+  CUtensorMap hxt128;  // HX^T [3136][rows], box 128
+  CUtensorMap hxt256;  // HX^T               box 256
+  CUtensorMap gdt;     // Gram rows [slots*64][njt*128] (per slot 32 high then 32 low rows), box 32
 };
 
 inline int njt_of_host(int step, int BS) { return (step * BS + 127) >> 7; }
 __device__ __forceinline__ int njt_of(const Args& a) { return (a.step * a.BS + 127) >> 7; }
 
+// fp32 -> high + low bf16 terms (x ~= hi + lo to ~2^-17 relative)
+__device__ __forceinline__ void split_bf16(float x, bf16& hi, bf16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
 // ---------------------------------------------------------------------------
-// k_lz_w0t: w0t[k][o] = w0[fc1][o][k]  (once per round)
+// k_lz_w0t: the fc1 block of w0 as bf16 operands, once per round:
+// w0t[k][o] = W1[o][k] and (at w0t + kFlat*kH1) w0b[o][k] = W1[o][k]
 // ---------------------------------------------------------------------------
-__global__ void k_lz_w0t(const float* __restrict__ w0, float* __restrict__ w0t) {
+__global__ void k_lz_w0t(const float* __restrict__ w0, bf16* __restrict__ w0t) {
   __shared__ float tile[32][33];
   const int k0 = blockIdx.x * 32, o0 = blockIdx.y * 32;
   const float* W1 = w0 + oF1W;
-  for (int y = threadIdx.y; y < 32; y += 8) tile[y][threadIdx.x] = W1[int64_t(o0 + y) * kFlat + k0 + threadIdx.x];
+  bf16* w0b = w0t + int64_t(kFlat) * kH1;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const float v = W1[int64_t(o0 + y) * kFlat + k0 + threadIdx.x];
+    tile[y][threadIdx.x] = v;
+    w0b[int64_t(o0 + y) * kFlat + k0 + threadIdx.x] = __float2bfloat16_rn(v);
+  }
   __syncthreads();
-  for (int y = threadIdx.y; y < 32; y += 8) w0t[int64_t(k0 + y) * kH1 + o0 + threadIdx.x] = tile[threadIdx.x][y];
+  for (int y = threadIdx.y; y < 32; y += 8)
+    w0t[int64_t(k0 + y) * kH1 + o0 + threadIdx.x] = __float2bfloat16_rn(tile[threadIdx.x][y]);
 }
 
 // ---------------------------------------------------------------------------
@@ -85,20 +102,21 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
   const Slot sl = a.slots[blockIdx.x];
   const int cnt = sl.cnt;
   if (cnt == 0) return;
-  __shared__ float tile[32][129];
+  __shared__ __align__(16) bf16 tile[32][136];
   const int k0 = blockIdx.y * 128, kn = min(128, kFlat - k0);
-  const float* x = p2_row(a, sl, blockIdx.x, 0);
-  for (int e = threadIdx.x; e < cnt * 128; e += 128) {
-    const int i = e >> 7, kk = e & 127;
-    if (kk < kn) tile[i][kk] = x[int64_t(i) * kFlat + k0 + kk];
+  const bf16* x = hx_row(a, sl, 0);
+  for (int e = threadIdx.x; e < cnt * 16; e += 128) {   // 16-byte units: 8 bf16 of a row
+    const int i = e >> 4, k8 = (e & 15) * 8;
+    if (k8 < kn)
+      *reinterpret_cast<uint4*>(&tile[i][k8]) = *reinterpret_cast<const uint4*>(x + int64_t(i) * kFlat + k0 + k8);
   }
   __syncthreads();
-  float* xt = a.hxt + int64_t(k0) * a.hrows + sl.hist + int64_t(a.step) * a.BS;
+  bf16* xt = a.hxt + int64_t(k0) * a.hrows + sl.hist + int64_t(a.step) * a.BS;
   // columns [cnt, zc) (partial batch, padding after the last step) -> 0
   const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);
   for (int e = threadIdx.x; e < zc * kn; e += 128) {
     const int kk = e / zc, i = e - kk * zc;
-    xt[int64_t(kk) * a.hrows + i] = i < cnt ? tile[i][kk] : 0.0f;
+    xt[int64_t(kk) * a.hrows + i] = i < cnt ? tile[i][kk] : __float2bfloat16_rn(0.0f);
   }
 }
 
@@ -107,8 +125,9 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 // current step's rows (M = 128 history rows, N = 32 current rows):
 //   FWD : Gx[j][i] = X_j . X_t,i  (K = 3136), then the forward correction
 //         partial  zp[s][jt][o][i] = -lr * sum_{j in tile} dH_j[o] Gx[j][i]
-//         (M = 4 x 128 o, N = 32, K = 128; A = hdt columns, B = Gx^T in smem)
-//   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][i][j] = -lr * Gd
+//         (M = 4 x 128 o, N = 32, K = 128; A = hdt columns, B = Gx^T in smem
+//         as high + low bf16 terms)
+//   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][hi|lo][i][j] = -lr * Gd
 // History rows j >= t*BS (the current step, later steps, other clients) are
 // zeroed when the Gram tile leaves TMEM.
 // Sparse sweeps split the forward Gram's K over a cluster of ks CTAs per
@@ -117,11 +136,12 @@ __global__ void __launch_bounds__(128) k_lz_xt(Args a) {
 // [4r/ks, 4(r+1)/ks).
 // grid (njt * ks, active), cluster (ks, 1, 1), 128 threads
 // ---------------------------------------------------------------------------
-constexpr int kGrA = 128 * 128;                // 16 KB: 128 rows x 32 fp32 (one K atom)
-constexpr int kGrB = 32 * 128;                 // 4 KB
-constexpr int kGrStage = 2 * (kGrA + kGrB);    // 40 KB: two K atoms per stage
-constexpr int kGrStages = 5;
-constexpr int kGxT = 4 * 32 * 128;             // Gx^T: 4 K-atoms of [32 i][32 j], 16 KB
+constexpr int kGrA = 128 * 128;                // 16 KB: 128 history rows x one K atom
+constexpr int kGrB = 32 * 128;                 // 4 KB: 32 current rows
+constexpr int kGrStage = kGrA + kGrB;          // 20 KB per K atom (64 features)
+constexpr int kGrStages = 8;
+constexpr int kGxAtom = 32 * 128;              // Gx^T: [32 i][64 j] bf16, 4 KB
+constexpr int kGxT = 2 * 2 * kGxAtom;          // two j atoms, high + low terms: 16 KB
 constexpr size_t kGramFwdSmem = 1024 + kGrStages * kGrStage + kGxT;
 constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
 
@@ -138,7 +158,7 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = a.step, jlim = t * a.BS, j0 = jt * 128, njt = njt_of(a);
-  constexpr int nA = (FWD ? kFlat : kH1) / 64;   // 49 | 8 stages of two K atoms
+  constexpr int nA = (FWD ? kFlat : kH1) / kAK;   // 49 | 8 K atoms
   const int hrow = int(sl.hist) + j0, crow = int(sl.hist + int64_t(t) * a.BS);
   uint8_t* sGxT = smem + kGrStages * kGrStage;
   if (warp == 0) tmem_alloc<FWD ? 256 : 32>(&tmem_base);
@@ -156,27 +176,20 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
   const CUtensorMap* ta = FWD ? &m.hxa[nsub - 1] : &m.hda[nsub - 1];
   const CUtensorMap* tb = FWD ? &m.hxb : &m.hdb;
   if (tid == 0) {
-    const uint32_t bytes = uint32_t(2 * (nsub + 1) * 32 * 128);
+    const uint32_t bytes = uint32_t((nsub + 1) * 32 * 128);
     const int ca = rank * nA / ks;
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, bytes);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint8_t* sh = st + h * (kGrA + kGrB);
-        pb::tma::load_2d(sh, ta, (2 * (ca + c) + h) * 32, hrow, f);
-        pb::tma::load_2d(sh + kGrA, tb, (2 * (ca + c) + h) * 32, crow, f);
-      }
+      pb::tma::load_2d(st, ta, (ca + c) * kAK, hrow, f);
+      pb::tma::load_2d(st + kGrA, tb, (ca + c) * kAK, crow, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint32_t idesc = idesc_tf32(128, 32);
+      const uint32_t idesc = idesc_bf16(128, 32);
+      const uint32_t sh = smem_u32(st);
+      const uint64_t a0 = desc_sw128(sh), b0 = desc_sw128(sh + kGrA);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t sh = smem_u32(st + h * (kGrA + kGrB));
-        const uint64_t a0 = desc_sw128(sh), b0 = desc_sw128(sh + kGrA);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
-      }
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
     };
     tma_ring<kGrStages>((rank + 1) * nA / ks - ca, smem, kGrStage, full, empty, issue, mma);
   }
@@ -207,33 +220,44 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
     cl.sync();   // partner partials read: the ring memory may be reused
   }
   if (FWD) {
-    // Gx^T (B operand of phase B, SWIZZLE_128B K-major: atom j/32, row i)
-    uint8_t* atom = sGxT + (j >> 5) * (32 * 128);
+    // Gx^T (B operand of phase B, SWIZZLE_128B K-major: atom j/64, row i),
+    // high and low bf16 terms
+    uint8_t* hi_atom = sGxT + (j >> 6) * kGxAtom;
+    uint8_t* lo_atom = hi_atom + 2 * kGxAtom;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      *reinterpret_cast<float*>(atom + pb::tma::sw128_off(i, j & 31)) = live ? tf32_rna(v[i]) : 0.0f;
+    for (int i = 0; i < 32; ++i) {
+      bf16 hi, lo;
+      split_bf16(live ? v[i] : 0.0f, hi, lo);
+      *reinterpret_cast<bf16*>(hi_atom + pb::tma::sw128_off_b16(i, j & 63)) = hi;
+      *reinterpret_cast<bf16*>(lo_atom + pb::tma::sw128_off_b16(i, j & 63)) = lo;
+    }
     fence_async_smem();
     fence_before_sync();
     __syncthreads();
+    // K atoms (64 history columns) past the live rows contribute zero: skipped
+    const int natom = min(2, (jlim - j0 + 63) >> 6);
     if (tid == 0) {
       fence_after_sync();
       const int hcol = int(sl.hist) + j0;
-      // K chunks (32 history columns) past the live rows contribute zero: skipped
       const int q0 = rank * 4 / ks;
-      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = (q - q0)*nsub + jc
+      auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = (q - q0)*natom + jc
         pb::tma::expect_tx(f, kGrA);
-        pb::tma::load_2d(st, &m.hdt, hcol + (c % nsub) * 32, (q0 + c / nsub) * 128, f);
+        pb::tma::load_2d(st, &m.hdt, hcol + (c % natom) * kAK, (q0 + c / natom) * 128, f);
       };
       auto mma = [&](int c, uint8_t* st) {
-        const int q = q0 + c / nsub, jc = c % nsub;
+        const int q = q0 + c / natom, jc = c % natom;
         const uint64_t a0 = desc_sw128(smem_u32(st));
-        const uint64_t b0 = desc_sw128(smem_u32(sGxT + jc * 32 * 128));
-        const uint32_t idesc = idesc_tf32(128, 32);
+        const uint64_t bh = desc_sw128(smem_u32(sGxT + jc * kGxAtom));
+        const uint64_t bl = desc_sw128(smem_u32(sGxT + (2 + jc) * kGxAtom));
+        const uint32_t idesc = idesc_bf16(128, 32);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
+          mma_bf16(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), bl + uint64_t(kk * 2), idesc, true);
       };
-      tma_ring<kStages>(((rank + 1) * 4 / ks - q0) * nsub, smem, kGrA, full2, empty2, issue, mma);
+      tma_ring<kStages>(((rank + 1) * 4 / ks - q0) * natom, smem, kGrA, full2, empty2, issue, mma);
     }
     __syncthreads();
     fence_after_sync();
@@ -250,12 +274,18 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
         dst[i4] = make_float4(nlr * w[4 * i4], nlr * w[4 * i4 + 1], nlr * w[4 * i4 + 2], nlr * w[4 * i4 + 3]);
     }
   } else {
+    // gdt rows of slot s: 32 high then 32 low rows, row pitch njt*128.  Rows
+    // past the batch are exactly zero: the backward's packed slots (rs < 32
+    // rows each) accumulate these 32-row products into the next slot
     const int64_t jstride = int64_t(njt) * 128;
-    float* g = a.gdt + int64_t(s) * 32 * jstride + j0 + j;
+    bf16* g = a.gdt + int64_t(s) * 64 * jstride + j0 + j;
 #pragma unroll
-    // rows past the batch are exactly zero: the backward's packed slots
-    // (rs < 32 rows each) accumulate these 32-row products into the next slot
-    for (int i = 0; i < 32; ++i) g[i * jstride] = live && i < cnt ? tf32_rna(nlr * v[i]) : 0.0f;
+    for (int i = 0; i < 32; ++i) {
+      bf16 hi, lo;
+      split_bf16(live && i < cnt ? nlr * v[i] : 0.0f, hi, lo);
+      g[i * jstride] = hi;
+      g[(32 + i) * jstride] = lo;
+    }
   }
   fence_before_sync();
   __syncthreads();
@@ -263,24 +293,23 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_fwd: h = relu(X_t W0^T + b1 + sum_jt zp) for spc slots x 32 rows
-// (M = 128 o, N = spc*32, K = 3136; W0 shared by every client of the sweep).
+// k_lz_fwd: h = relu(X_t W0^T + b1 + sum_jt zp) for spc slots x rs rows
+// (M = 128 o, N = spc*rs, K = 3136; W0 shared by every client of the sweep).
 // Head sweeps: spc = 8, fused epilogue.  Tail sweeps (few clients): spc = 1
 // and K split over gridDim.z CTAs writing raw partials to fpart, summed in
 // split order by k_lz_fwd_epi (deterministic).
 // Dense sweeps (spc = 8) take MT = 2 o-tiles per CTA (two M=128 accumulators,
-// 512 TMEM columns): the 8 clients' X tiles are read once per 256 outputs,
-// a third less tile traffic per FLOP.
+// 512 TMEM columns): the 8 clients' X tiles are read once per 256 outputs.
 // grid (4 / MT o-tiles, ceil(active / spc), ks), 256 threads
 // ---------------------------------------------------------------------------
-constexpr int kSh8 = 8;                         // max slots per CTA (N = 8 x 32)
-constexpr int kShA = 128 * 128;                 // 16 KB
+constexpr int kSh8 = 8;                         // max slots per CTA (N = 8 x 24)
+constexpr int kShA = 128 * 128;                 // 16 KB: 128 rows x one K atom
 constexpr int kShB = 256 * 128;                 // 32 KB
 constexpr int kShStage = kShA + kShB;           // 48 KB
 constexpr size_t kShSmem = 1024 + kStages * kShStage;
-constexpr int kFwdChunks = kFlat / 32;          // 98
+constexpr int kFwdChunks = kFlat / kAK;         // 49 K atoms
 constexpr int kTailCtas = 296;                  // 2 x 148 SMs: tail grids aim for this
-constexpr int kFwdSplitMax = 7;                 // 98 chunks = 7 x 14
+constexpr int kFwdSplitMax = 7;                 // 49 atoms = 7 x 7
 
 __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl, int o, float (&v)[32],
                                            int njt) {
@@ -337,7 +366,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
       nv += sS[u].cnt > 0;
     }
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      const int k0 = (c0 + c) * 32;
+      const int k0 = (c0 + c) * kAK;
       pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * rs * 128));
 #pragma unroll
       for (int t = 0; t < MT; ++t) pb::tma::load_2d(st + t * kShA, &m.w0, k0, (q * MT + t) * 128, f);
@@ -346,13 +375,13 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
-      const uint32_t idesc = idesc_tf32(128, spc * rs);
+      const uint32_t idesc = idesc_bf16(128, spc * rs);
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const uint64_t a0 = desc_sw128(smem_u32(st + t * kShA));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(tmem + t * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+          mma_bf16(tmem + t * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
       }
     };
     tma_ring<S>(c1 - c0, smem, kStage, full, empty, issue, mma);
@@ -440,10 +469,11 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_bwd: dp2 = dH_t W0 + sum_j hxt[k][j] gdt[i][j] for spc slots x 32 rows
-//   phase 1 (shared): M = 128 k, N = spc*32, K = 512 (A = w0t, B = dH_t rows)
+// k_lz_bwd: dp2 = dH_t W0 + sum_j hxt[k][j] gdt[i][j] for spc slots x rs rows
+//   phase 1 (shared): M = 128 k, N = spc*rs, K = 512 (A = w0t, B = dH_t rows)
 //   phase 2 (per slot, t > 0): M = 128 k, N = 32, K = t*BS into the slot's
-//   accumulator columns (A = the client's hxt columns, B = its gdt rows)
+//   accumulator columns (A = the client's hxt columns, B = its gdt rows, the
+//   high and the low term against the same A tile)
 // Dense sweeps (spc = 8) take MT = 2 k-tiles per CTA (512 TMEM columns): the
 // dH_t and gdt tiles are read once per 256 k.
 // grid (ceil(25 / MT) k-tiles, ceil(active / spc)), 256 threads
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
                                                    int rs) {
   pb::pdl_wait();
   constexpr int S = MT == 1 ? kStages : 3;
-  constexpr int kStage = MT == 1 ? kShStage : MT * kShA + kShB;   // 48 | 64 KB
+  constexpr int kStage = MT * kShA + kShB;   // 48 | 64 KB
   static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_bwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
@@ -476,12 +506,9 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   fence_after_sync();
   const uint32_t tmem = tmem_base;
   const int t = a.step, jlim = t * a.BS;
-  // phase-2 stages per slot: two K atoms (MT = 1) or one (MT = 2, two k-tiles)
-  const int nj = MT == 1 ? (jlim + 63) >> 6 : (jlim + 31) >> 5;
+  const int nj = (jlim + kAK - 1) / kAK;   // phase-2 K atoms per slot
   const int64_t tb = int64_t(t) * a.BS;
-  // phase-1 stages: one K atom for several slots, two for a single slot (the
-  // same 40 KB stage as phase 2, twice the bytes in flight)
-  const int n1 = spc == 1 ? kH1 / 64 : kH1 / 32;
+  constexpr int n1 = kH1 / kAK;             // phase-1 K atoms: 8
   if (tid == 0) {
     int us[kSh8], rows[kSh8], nv = 0;
     for (int u = 0; u < spc; ++u) {
@@ -490,79 +517,48 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
     }
     const int n = n1 + (t > 0 ? nv * nj : 0);
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      if (c < n1 && spc == 1) {
-        pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          pb::tma::load_2d(st + h * kShA, &m.w0t, (2 * c + h) * 32, kt0 * 128, f);
-          pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.hdb, (2 * c + h) * 32, rows[0], f);
-        }
-      } else if (c < n1) {
+      if (c < n1) {
         pb::tma::expect_tx(f, uint32_t(MT * kShA + nv * rs * 128));
 #pragma unroll
-        for (int q = 0; q < MT; ++q) pb::tma::load_2d(st + q * kShA, &m.w0t, c * 32, (kt0 + q) * 128, f);
+        for (int q = 0; q < MT; ++q) pb::tma::load_2d(st + q * kShA, &m.w0t, c * kAK, (kt0 + q) * 128, f);
         for (int u = 0; u < spc; ++u)
           if (sS[u].cnt > 0)
-            pb::tma::load_2d(st + MT * kShA + u * rs * 128, rs == 32 ? &m.hdb : &m.hds, c * 32, rows[u], f);
-      } else if (MT == 1) {
-        const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
-        pb::tma::expect_tx(f, uint32_t(2 * (kShA + 32 * 128)));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          pb::tma::load_2d(st + h * kShA, &m.hxt128, int(sS[u].hist) + (2 * jc + h) * 32, kt0 * 128, f);
-          pb::tma::load_2d(st + 2 * kShA + h * 32 * 128, &m.gdt, (2 * jc + h) * 32, (g0 + u) * 32, f);
-        }
+            pb::tma::load_2d(st + MT * kShA + u * rs * 128, rs == 32 ? &m.hdb : &m.hds, c * kAK, rows[u], f);
       } else {
         const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
-        pb::tma::expect_tx(f, uint32_t(MT * kShA + 32 * 128));
+        pb::tma::expect_tx(f, uint32_t(MT * kShA + 2 * 32 * 128));
 #pragma unroll
         for (int q = 0; q < MT; ++q)
-          pb::tma::load_2d(st + q * kShA, &m.hxt128, int(sS[u].hist) + jc * 32, (kt0 + q) * 128, f);
-        pb::tma::load_2d(st + MT * kShA, &m.gdt, jc * 32, (g0 + u) * 32, f);
+          pb::tma::load_2d(st + q * kShA, &m.hxt128, int(sS[u].hist) + jc * kAK, (kt0 + q) * 128, f);
+        pb::tma::load_2d(st + MT * kShA, &m.gdt, jc * kAK, (g0 + u) * 64, f);
+        pb::tma::load_2d(st + MT * kShA + 32 * 128, &m.gdt, jc * kAK, (g0 + u) * 64 + 32, f);
       }
     };
     auto mma = [&](int c, uint8_t* st) {
-      if (c < n1 && spc == 1) {
-        const uint32_t idesc = idesc_tf32(128, 32);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint64_t ah = desc_sw128(smem_u32(st + h * kShA));
-          const uint64_t bh = desc_sw128(smem_u32(st + 2 * kShA + h * 32 * 128));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, c > 0 || h > 0 || kk > 0);
-        }
-      } else if (c < n1) {
-        const uint32_t idesc = idesc_tf32(128, spc * rs);
+      if (c < n1) {
+        const uint32_t idesc = idesc_bf16(128, spc * rs);
         const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
           const uint64_t a0 = desc_sw128(smem_u32(st + q * kShA));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem + q * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
-        }
-      } else if (MT == 1) {
-        const int u = us[(c - n1) / nj];
-        const uint32_t idesc = idesc_tf32(128, 32);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint64_t ah = desc_sw128(smem_u32(st + h * kShA));
-          const uint64_t bh = desc_sw128(smem_u32(st + 2 * kShA + h * 32 * 128));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+            mma_bf16(tmem + q * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
         }
       } else {
         const int u = us[(c - n1) / nj];
-        const uint32_t idesc = idesc_tf32(128, 32);
+        const uint32_t idesc = idesc_bf16(128, 32);
         const uint64_t bh = desc_sw128(smem_u32(st + MT * kShA));
+        const uint64_t bl = desc_sw128(smem_u32(st + MT * kShA + 32 * 128));
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
           const uint64_t ah = desc_sw128(smem_u32(st + q * kShA));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_tf32(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+            mma_bf16(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bl + uint64_t(kk * 2), idesc, true);
         }
       }
     };
@@ -594,8 +590,8 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
 
 // ---------------------------------------------------------------------------
 // k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hxt[k][j]
-// (M = 128 o, N = 256 k, K = steps_r * BS rounded to 32 -- within the
-// client's 32-aligned history); grid (13, 4, g), 256 threads -- the client
+// (M = 128 o, N = 256 k, K = steps_r * BS rounded to 64 -- within the
+// client's 64-aligned history); grid (13, 4, g), 256 threads -- the client
 // is the slowest grid dimension, so its 52 tiles re-read its history from L2.
 // switch_step > 0: clients that took more steps left the low-rank form at
 // that sweep (their w rows already hold the final fc1) and are skipped.
@@ -625,17 +621,17 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
     const int hcol = int(a.hoff[r]);
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, kShStage);
-      pb::tma::load_2d(st, &m.hdt, hcol + c * 32, q * 128, f);
-      pb::tma::load_2d(st + kShA, &m.hxt256, hcol + c * 32, k0, f);
+      pb::tma::load_2d(st, &m.hdt, hcol + c * kAK, q * 128, f);
+      pb::tma::load_2d(st + kShA, &m.hxt256, hcol + c * kAK, k0, f);
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
-      const uint32_t idesc = idesc_tf32(128, 256);
+      const uint32_t idesc = idesc_bf16(128, 256);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
     };
-    tma_ring<kStages>((K + 31) / 32, smem, kShStage, full, empty, issue, mma);
+    tma_ring<kStages>((K + kAK - 1) / kAK, smem, kShStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -668,19 +664,27 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
 //   sum_j w_j W1_j = (sum_j w_j) W0 - lr * sum_j w_j HD_j^T HX_j
 // over its clients j (contiguous history rows [row_lo, row_hi)), so the
 // per-client fc1 weights are never materialised.
-//   k_lz_scale   hdt columns of client j *= w_j          (HDT is round scratch)
-//   k_lz_fold    split-K GEMM D[o][k] = sum_rows hdt[o][row] hxt[k][row]
+//   k_lz_scale   hdt columns of client j -> w_j * dH as high (in place) +
+//                low (hdt_lo) bf16 terms               (HDT is round scratch)
+//   k_lz_fold    split-K GEMM D[o][k] = sum_rows (hdt + hdt_lo)[o][row] hxt[k][row]
 //                -> part[split][512][3136]   grid (13, 4, splits)
 //   k_lz_fold_reduce  acc += wsum * W0 - lr * sum_split part (split order)
 // ---------------------------------------------------------------------------
-__global__ void k_lz_scale(float* __restrict__ hdt, int64_t hrows, const int64_t* __restrict__ hoff,
-                           const int32_t* __restrict__ nrows, const float* __restrict__ w) {
+__global__ void k_lz_scale(bf16* __restrict__ hdt, bf16* __restrict__ hdtl, int64_t hrows,
+                           const int64_t* __restrict__ hoff, const int32_t* __restrict__ nrows,
+                           const float* __restrict__ w) {
   const int j = blockIdx.y;
-  const int64_t c0 = hoff[j], n = nrows[j];
+  const int64_t c0 = hoff[j], n = (int64_t(nrows[j]) + kAK - 1) / kAK * kAK;   // whole 64-column atoms
   const float wj = w[j];
   for (int o = blockIdx.x; o < kH1; o += gridDim.x) {
-    float* row = hdt + int64_t(o) * hrows + c0;
-    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) row[c] *= wj;
+    bf16* row = hdt + int64_t(o) * hrows + c0;
+    bf16* rowl = hdtl + int64_t(o) * hrows + c0;
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+      bf16 hi, lo;
+      split_bf16(wj * __bfloat162float(row[c]), hi, lo);
+      row[c] = hi;
+      rowl[c] = lo;
+    }
   }
 }
 
@@ -699,21 +703,23 @@ __global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMa
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  if (tid == 0 && c1 > c0) {
+  const int nc = c1 - c0;
+  if (tid == 0 && nc > 0) {
+    // every chunk twice: the high then the low term of the weighted dH^T
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      const int col = row_lo + (c0 + c) * 32;
+      const int col = row_lo + (c0 + c % nc) * kAK;
       pb::tma::expect_tx(f, kShStage);
-      pb::tma::load_2d(st, &m.hdt, col, q * 128, f);
+      pb::tma::load_2d(st, c < nc ? &m.hdt : &m.hdtl, col, q * 128, f);
       pb::tma::load_2d(st + kShA, &m.hxt256, col, k0, f);
     };
     auto mma = [&](int c, uint8_t* st) {
       const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
-      const uint32_t idesc = idesc_tf32(128, 256);
+      const uint32_t idesc = idesc_bf16(128, 256);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
     };
-    tma_ring<kStages>(c1 - c0, smem, kShStage, full, empty, issue, mma);
+    tma_ring<kStages>(2 * nc, smem, kShStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMa
     tmem_ld16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col), v);
     const int kk = k0 + col;
     if (kk >= kFlat) continue;
-    if (c1 <= c0) {
+    if (nc <= 0) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.0f;
     }
@@ -759,6 +765,18 @@ __global__ void k_lz_fold_reduce(float* __restrict__ acc, const float* __restric
     a.w += fmaf(wsum, w.w, nlr * g.w);
     reinterpret_cast<float4*>(acc)[e] = a;
   }
+}
+
+// switch mode of k_lz_mat reads whole 64-column atoms: the history columns
+// [K, round_up(K, 64)) of the active clients (their next steps, stale) must
+// be zero in hdt first.  grid (active), 256 threads
+__global__ void k_lz_zero_tail(Args a, int K) {
+  pb::pdl_wait();
+  const Slot sl = a.slots[blockIdx.x];
+  const int n = ((K + kAK - 1) / kAK) * kAK - K;
+  if (sl.cnt == 0 || n == 0) return;
+  for (int e = threadIdx.x; e < kH1 * n; e += blockDim.x)
+    a.hdt[int64_t(e / n) * a.hrows + sl.hist + K + e % n] = __float2bfloat16_rn(0.0f);
 }
 
 int setup() {
@@ -795,25 +813,26 @@ int lazy_fc1_prepare(Args& a, cudaStream_t s) {
   int rc = setup();
   if (rc) return rc;
   pb::prof_begin(pb::K_CNN_LZ_XT, s);
-  k_lz_w0t<<<dim3(kFlat / 32, kH1 / 32), dim3(32, 8), 0, s>>>(a.w0, const_cast<float*>(a.w0t));
+  k_lz_w0t<<<dim3(kFlat / 32, kH1 / 32), dim3(32, 8), 0, s>>>(a.w0, a.w0t);
   pb::prof_end(pb::K_CNN_LZ_XT, s);
   LzMaps* m = new LzMaps();
   a.lzmaps = m;
   const uint64_t R = uint64_t(a.hrows);
-  using pb::tma::make_2d_f32;
-  if ((rc = make_2d_f32(&m->w0, a.w0 + oF1W, kFlat, kH1, kFlat, 128)) ||
-      (rc = make_2d_f32(&m->w0t, a.w0t, kH1, kFlat, kH1, 128)) ||
-      (rc = make_2d_f32(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
-      (rc = make_2d_f32(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
-      (rc = make_2d_f32(&m->hxs, a.hx, kFlat, R, kFlat, uint32_t((a.BS + 7) & ~7))) ||
-      (rc = make_2d_f32(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))) ||
-      (rc = make_2d_f32(&m->hdt, a.hdt, R, kH1, R, 128)) ||
-      (rc = make_2d_f32(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
-      (rc = make_2d_f32(&m->hxt256, a.hxt, R, kFlat, R, 256)))
+  const bf16* w0b = a.w0t + int64_t(kFlat) * kH1;
+  using pb::tma::make_2d_bf16;
+  if ((rc = make_2d_bf16(&m->w0, w0b, kFlat, kH1, kFlat, 128)) ||
+      (rc = make_2d_bf16(&m->w0t, a.w0t, kH1, kFlat, kH1, 128)) ||
+      (rc = make_2d_bf16(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
+      (rc = make_2d_bf16(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
+      (rc = make_2d_bf16(&m->hxs, a.hx, kFlat, R, kFlat, uint32_t((a.BS + 7) & ~7))) ||
+      (rc = make_2d_bf16(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))) ||
+      (rc = make_2d_bf16(&m->hdt, a.hdt, R, kH1, R, 128)) ||
+      (rc = make_2d_bf16(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
+      (rc = make_2d_bf16(&m->hxt256, a.hxt, R, kFlat, R, 256)))
     return rc;
   for (int q = 0; q < 4; ++q)   // history boxes sized to the live rows of a tile
-    if ((rc = make_2d_f32(&m->hxa[q], a.hx, kFlat, R, kFlat, 32 * (q + 1))) ||
-        (rc = make_2d_f32(&m->hda[q], a.hd, kH1, R, kH1, 32 * (q + 1))))
+    if ((rc = make_2d_bf16(&m->hxa[q], a.hx, kFlat, R, kFlat, 32 * (q + 1))) ||
+        (rc = make_2d_bf16(&m->hda[q], a.hd, kH1, R, kH1, 32 * (q + 1))))
       return rc;
   return pb::check_launch("lazy fc1 prepare");
 }
@@ -856,9 +875,9 @@ static int slots_per_cta(int active) {
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   LzMaps& m = *maps_of(a);
   const int njt = njt_of_host(a.step, a.BS);
-  // head sweeps: 8 clients share each W0 tile (N = 256); tail sweeps (fewer
-  // clients than SMs): one client per CTA, and the forward splits K so that
-  // the grid still covers the machine
+  // head sweeps: 8 clients share each W0 tile (N = 8 x 24); tail sweeps
+  // (fewer clients than SMs): one client per CTA, and the forward splits K so
+  // that the grid still covers the machine
   const int spc = slots_per_cta(active);
   const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
@@ -909,8 +928,8 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     }
   } else {
     if (njt > 0) {
-      int rc = pb::tma::make_2d_f32(&m.gdt, a.gdt, uint64_t(njt) * 128, uint64_t(active) * 32,
-                                    uint64_t(njt) * 128, 32);
+      int rc = pb::tma::make_2d_bf16(&m.gdt, a.gdt, uint64_t(njt) * 128, uint64_t(active) * 64,
+                                     uint64_t(njt) * 128, 32);
       if (rc) return rc;
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
       pb::launch_pdl(k_lz_gram<false>, dim3(njt, active), dim3(128), kGramBwdSmem, s, 1, m, a, 1);
@@ -937,18 +956,6 @@ int lazy_fc1_materialize(const Args& a, int g, int switch_step, cudaStream_t s) 
   return pb::check_launch("lazy fc1 materialise");
 }
 
-// switch mode of k_lz_mat reads whole 32-column chunks: the history columns
-// [K, round_up(K, 32)) of the active clients (their next steps, stale) must
-// be zero in hdt first.  grid (active), 256 threads
-__global__ void k_lz_zero_tail(Args a, int K) {
-  pb::pdl_wait();
-  const Slot sl = a.slots[blockIdx.x];
-  const int n = ((K + 31) & ~31) - K;
-  if (sl.cnt == 0 || n == 0) return;
-  for (int e = threadIdx.x; e < kH1 * n; e += blockDim.x)
-    a.hdt[int64_t(e / n) * a.hrows + sl.hist + K + e % n] = 0.0f;
-}
-
 int lazy_fc1_switch(const Args& a, int active, cudaStream_t s) {
   if (active <= 0 || a.step <= 0) return PB_OK;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
@@ -966,24 +973,26 @@ extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream)
   using namespace pb::cnn;
   if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: null args");
   const pb_cnn_lazy_fold_args& f = *args;
-  if (!f.acc || !f.w0 || !f.hxt || !f.hdt || !f.hoff || !f.nrows || !f.w || !f.part || f.hrows <= 0 ||
-      f.hrows % 32 || f.nclients < 0 || f.splits < 1 || f.row_lo < 0 || f.row_hi < f.row_lo ||
-      f.row_lo % 32 || f.row_hi > f.hrows || !pb::aligned16(f.acc) || !pb::aligned16(f.w0) ||
-      !pb::aligned16(f.part))
+  if (!f.acc || !f.w0 || !f.hxt || !f.hdt || !f.hdt_lo || !f.hoff || !f.nrows || !f.w || !f.part ||
+      f.hrows <= 0 || f.hrows % kAK || f.nclients < 0 || f.splits < 1 || f.row_lo < 0 || f.row_hi < f.row_lo ||
+      f.row_lo % kAK || f.row_hi > f.hrows || !pb::aligned16(f.acc) || !pb::aligned16(f.w0) ||
+      !pb::aligned16(f.part) || !pb::aligned16(f.hdt_lo))
     return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: bad arguments");
   if (f.nclients == 0) return PB_OK;
   int rc = setup();
   if (rc) return rc;
   cudaStream_t s = pb::as_stream(stream);
   LzMaps m{};
-  using pb::tma::make_2d_f32;
+  using pb::tma::make_2d_bf16;
   const uint64_t R = uint64_t(f.hrows);
-  if ((rc = make_2d_f32(&m.hdt, f.hdt, R, kH1, R, 128)) || (rc = make_2d_f32(&m.hxt256, f.hxt, R, kFlat, R, 256)))
+  if ((rc = make_2d_bf16(&m.hdt, f.hdt, R, kH1, R, 128)) || (rc = make_2d_bf16(&m.hdtl, f.hdt_lo, R, kH1, R, 128)) ||
+      (rc = make_2d_bf16(&m.hxt256, f.hxt, R, kFlat, R, 256)))
     return rc;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
-  k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(f.hdt, f.hrows, f.hoff, f.nrows, f.w);
+  k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(static_cast<bf16*>(f.hdt), static_cast<bf16*>(f.hdt_lo),
+                                                            f.hrows, f.hoff, f.nrows, f.w);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);
-  const int chunks = int((f.row_hi - f.row_lo + 31) / 32);
+  const int chunks = int((f.row_hi - f.row_lo + kAK - 1) / kAK);
   const int per = (chunks + f.splits - 1) / f.splits;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
   k_lz_fold<<<dim3((kFlat + 255) / 256, kH1 / 128, unsigned(f.splits)), 256, kShSmem, s>>>(

@@ -42,6 +42,14 @@ int make_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows
   return PB_OK;
 }
 
+int make_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+                 uint32_t box_rows) {
+  if (box_rows < 1 || box_rows > 256) return fail(PB_ERR_INVALID, "make_2d_bf16: bad box");
+  const uint64_t dims[2] = {cols, rows}, strides[1] = {pitch * 2};
+  const uint32_t box[2] = {64, box_rows};
+  return make_nd_bf16(map, base, 2, dims, strides, box);
+}
+
 int make_nd_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                 const uint32_t* box) {
   EncodeFn fn = encode_fn();

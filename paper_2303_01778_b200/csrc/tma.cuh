@@ -22,6 +22,10 @@ namespace tma {
 // {32 cols, box_rows}, 128-byte swizzle, out-of-bounds elements read as 0.
 int make_2d_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
                 uint32_t box_rows);
+// 2-D bf16 tensor [rows][cols], row pitch `pitch` elements; box {64 cols
+// (128 B), box_rows}, 128-byte swizzle, out-of-bounds elements read as 0.
+int make_2d_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+                 uint32_t box_rows);
 
 // ---- device -----------------------------------------------------------------
 __device__ __forceinline__ void prefetch(const CUtensorMap* map) {
@@ -102,6 +106,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 // byte offset of fp32 element (r, k) (k < 32) in a SWIZZLE_128B K-major tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int k) {
   return uint32_t(r * 128 + ((((k >> 2) ^ (r & 7)) & 7) << 4) + (k & 3) * 4);
+}
+// byte offset of bf16 element (r, k) (k < 64) in a SWIZZLE_128B K-major tile
+__device__ __forceinline__ uint32_t sw128_off_b16(int r, int k) {
+  return uint32_t(r * 128 + ((((k >> 3) ^ (r & 7)) & 7) << 4) + (k & 7) * 2);
 }
 
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {

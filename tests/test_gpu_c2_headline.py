@@ -10,7 +10,7 @@ restatement (oracle/cnn_oracle.py, restatement-pinned).
 1. Kernel arithmetic, every local step of eight clients spanning the size
    distribution (1 to 72 steps): the group is re-run stopped after k sweeps
    (PB_CNN_MAX_SWEEPS) and step k of each client is replayed in the
-   bf16/tf32-emulating oracle from the DEVICE's weights after step k-1, so
+   bf16-emulating oracle from the DEVICE's weights after step k-1, so
    errors cannot compound.  The device's own discrete decisions of that step
    (pool-1 argmax + ReLU bit, pool-2 argmax, ReLU-2 and ReLU-3 signs, read
    from its workspace) are compared with the oracle's: every decision that
@@ -28,7 +28,7 @@ restatement (oracle/cnn_oracle.py, restatement-pinned).
    precision floor measured here on the same client -- the error of the
    oracle's own bf16-emulating run (or of its float32 run) against the exact
    one.  That floor is large: near initialisation (loss ~ ln 62) the update
-   is ill-conditioned in the operand rounding, so bf16 conv2 / tf32 fc1
+   is ill-conditioned in the operand rounding, so bf16 conv2 / fc1
    operands alone move a single step by 2-5 % and a 16-72-step run by 40-60 %
    (measured: device 0.40 vs emulating oracle 0.39 at 16 steps, 0.57 vs 0.61
    at 72), while the loss trajectories agree to 2e-4.
@@ -126,7 +126,7 @@ def _group(c2, monkeypatch, sweeps: int):
                 p2 = ws["p2"].view(torch.float32)[sid * 3136:(sid + cnt) * 3136].view(cnt, 3136).cpu().numpy()
             else:
                 base = int(hoff[c]) + t * BS
-                p2 = hx[base * 3136:(base + cnt) * 3136].view(cnt, 3136).cpu().numpy()
+                p2 = hx[base * 3136:(base + cnt) * 3136].view(cnt, 3136).float().cpu().numpy()
             dec[c] = (am1 & 3, am1 >> 2, am2, p2 > 0, h > 0)
     return rows, dec
 
@@ -179,7 +179,7 @@ def _oracle_decisions(params, x, fc1_base):
         if fc1_base is None:   # direct fc1 (after the low-rank switch): tf32 truncation
             z3 = O._tf32(hp) @ O._tf32(f1w).t() + f1b
         else:
-            z3 = O._tf32_rna(hp) @ (f1w - fc1_base + O._tf32(fc1_base)).t() + f1b
+            z3 = O._bf16(hp) @ (f1w - fc1_base + O._bf16(fc1_base)).t() + f1b
         relu3 = (z3 > 0, z3.abs() / float(z3.pow(2).mean().sqrt()))
     return [(d.numpy(), m.numpy()) for d, m in (arg1, relu1, arg2, relu2, relu3)]
 

@@ -98,8 +98,8 @@ def test_cnn_kernel_arithmetic_per_step(spec, femnist_like, lazy, monkeypatch):
     path).  Over the 12 steps of four clients (full, partial and single
     batches, three epochs): median step error <= 1e-3, at least two thirds
     of the steps <= 2e-3, every step <= 5e-2.  FedAvg runs the low-rank fc1
-    by default (csrc/cnn_lazy.cu), replayed with tf32(W0) + (W_t - W0) as the
-    fc1 weight and tf32-rounded X / dL/dz1 (what its tensor cores see);
+    by default (csrc/cnn_lazy.cu), replayed with bf16(W0) + (W_t - W0) as the
+    fc1 weight and bf16-rounded X / dL/dz1 (what its tensor cores see);
     PB_CNN_LAZY=0 forces the direct per-client fc1.  Both are checked."""
     errs = []
     for n, bs, epochs in [(100, 20, 1), (45, 16, 1), (7, 20, 1), (20, 20, 3)]:
@@ -319,7 +319,7 @@ def test_cnn_lowrank_switch_to_direct(spec, femnist_like, monkeypatch):
     stepping at sweep s leave the low-rank fc1 -- their fc1 is materialised
     from the history and the direct kernels train it from there.  (1) The
     end models agree with the all-low-rank run up to the operand rounding
-    the two fc1 forms differ in (tf32 round-to-nearest history vs truncated
+    the two fc1 forms differ in (bf16 history and W0 vs tf32-truncated
     weights): one step after the switch every client's update within 5e-2
     (median 2e-2), whole runs within 0.15 (the bound of the direct-fc1 local
     run against the emulating oracle); clients that finish before sweep s
