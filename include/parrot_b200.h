@@ -210,7 +210,8 @@ typedef struct {
    * columns), so the four history buffers need only hold FINITE values on
    * entry (zero them once after allocation or after a diverged client). */
   void* lz_hx;              /* [lz_rows, 3136] bf16                           */
-  void* lz_hxt;             /* [3136, lz_rows] bf16                           */
+  void* lz_hxt;             /* unused (the GEMMs over history rows read lz_hx */
+                            /* MN-major); may be NULL                         */
   void* lz_hd;              /* [lz_rows, 512] bf16                            */
   void* lz_hdt;             /* [512, lz_rows] bf16                            */
   const int64_t* lz_hoff;   /* [g]                                            */
@@ -251,7 +252,7 @@ int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
 typedef struct {
   float* acc;               /* [512*3136] fc1_w accumulator of the partial     */
   const float* w0;          /* [P] round-start model                           */
-  const void* hxt;          /* [3136, hrows] bf16                              */
+  const void* hx;           /* [hrows, 3136] bf16: the X history              */
   void* hdt;                /* [512, hrows] bf16 (overwritten: w_j * dH, high) */
   int64_t hrows, row_lo, row_hi;
   const int64_t* hoff;      /* [nclients] first history row of each client    */

@@ -46,7 +46,7 @@ class _LazyWorkspace:
     """Grow-only buffers of the low-rank fc1 (csrc/cnn_lazy.cu): the round's
     (X, dH) history per client plus the per-sweep partials."""
 
-    HISTORY = ("hx", "hxt", "hd", "hdt")
+    HISTORY = ("hx", "hd", "hdt")
 
     def __init__(self):
         self.buf: dict[str, torch.Tensor] = {}
@@ -69,7 +69,7 @@ class _LazyWorkspace:
 
     def get(self, rows: int, zp: int, gdt: int, slots: int, device) -> dict[str, torch.Tensor]:
         b16 = torch.bfloat16   # the history and the W0 copies are bf16 tensor-core operands
-        out = {"hx": self._get("hx", rows * 3136, device, b16), "hxt": self._get("hxt", rows * 3136, device, b16),
+        out = {"hx": self._get("hx", rows * 3136, device, b16),
                "hd": self._get("hd", rows * 512, device, b16), "hdt": self._get("hdt", rows * 512, device, b16),
                "w0t": self._get("w0t", 2 * 3136 * 512, device, b16), "zp": self._get("zp", zp, device),
                "gdt": self._get("gdt", gdt, device, b16),
@@ -162,7 +162,7 @@ class LazyFc1:
         part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
         lo_buf = _LZ._get("hdt_lo", self.rows * 512, d, torch.bfloat16)
         f = LazyFoldArgs()
-        f.acc, f.w0, f.hxt, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hxt"]), ptr(self.lz["hdt"])
+        f.acc, f.w0, f.hx, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hx"]), ptr(self.lz["hdt"])
         f.hrows, f.row_lo, f.row_hi = self.rows, lo, hi
         f.hoff, f.nrows, f.w, f.nclients = ptr(hoff), ptr(nrows), ptr(w), len(rows)
         f.part, f.splits = ptr(part), self.SPLITS
@@ -254,8 +254,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
         lz = _LZ.get(rows, zp, gdt, G, d)
         hlen_d = h2d(hlen, d)
         hoff_d = h2d(hoff, d)
-        a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = (ptr(lz["hx"]), ptr(lz["hxt"]), ptr(lz["hd"]),
-                                                ptr(lz["hdt"]))
+        a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = ptr(lz["hx"]), None, ptr(lz["hd"]), ptr(lz["hdt"])
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
         a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
         a.lz_rows = rows

@@ -1691,7 +1691,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.rank = t.rank; a.w = t.w; a.w0 = t.w0; a.ctrl_g = t.ctrl_g; a.ctrl_c = t.ctrl_c;
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
-  a.hx = static_cast<bf16*>(t.lz_hx); a.hxt = static_cast<bf16*>(t.lz_hxt);
+  a.hx = static_cast<bf16*>(t.lz_hx);
   a.hd = static_cast<bf16*>(t.lz_hd); a.hdt = static_cast<bf16*>(t.lz_hdt); a.hoff = t.lz_hoff;
   a.hlen = t.lz_hlen; a.w0t = static_cast<bf16*>(t.lz_w0t); a.zp = t.lz_zp;
   a.gdt = static_cast<bf16*>(t.lz_gdt); a.fpart = t.lz_fpart;
@@ -1812,8 +1812,8 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
-    if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hxt || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
-        !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 64 || !pb::aligned16(a.hx) || !pb::aligned16(a.hxt) ||
+    if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
+        !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 64 || !pb::aligned16(a.hx) ||
         !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
       return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
     if ((rc = lazy_fc1_prepare(a, s))) {
@@ -1837,7 +1837,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
       // the still-active clients' fc1 after sw steps -> their w rows; from
       // here on they train on the direct kernels (p2 / dH in the workspace)
       if ((rc = lazy_fc1_switch(lz, active, s))) break;
-      a.hx = a.hxt = a.hd = a.hdt = nullptr;
+      a.hx = a.hd = a.hdt = nullptr;
       a.hoff = nullptr;
       a.hlen = nullptr;
     }

@@ -75,7 +75,6 @@ struct Args {
   // history is bf16 (the tensor-core operands, rounded once when written).
   // Stale rows are finite and meet exact zeros (pad rows/columns, Gram selects).
   bf16* hx;               // [hrows, kFlat]  X_t (the p2 activations)
-  bf16* hxt;              // [kFlat, hrows]  X transposed
   bf16* hd;               // [hrows, kH1]    dH_t = dL/dz1
   bf16* hdt;              // [kH1, hrows]    dH transposed
   const int64_t* hoff;    // [G] first history row of client row r

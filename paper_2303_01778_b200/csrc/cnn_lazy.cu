@@ -25,8 +25,9 @@
 // terms (high + low, ~2^-17 relative), so the corrections carry no rounding
 // beyond the stored operands'.  Every operand tile is one TMA box of 64 bf16
 // of K (128 B) x up to 256 rows, SWIZZLE_128B K-major (tma.cuh); the history
-// is kept as plain row-major matrices ([rows, K] and the transposed [K, rows])
-// so each client's block is a box of one tensor map.  One thread drives a
+// is kept as plain row-major matrices ([rows, K]; dH also transposed, [K,
+// rows]) so each client's block is a box of one tensor map; GEMMs that
+// contract over history rows read X MN-major (no transposed copy).  One thread drives a
 // TMA -> MMA ring; the CTA's other warps run the epilogues.  Reductions have a
 // fixed order (no atomics): results are deterministic.
 #include <cooperative_groups.h>
@@ -52,7 +53,8 @@ constexpr int kAK = 64;   // K elements (bf16) per 128-byte operand row: one "at
 struct LzMaps {
   CUtensorMap w0;      // W0 fc1 block bf16 [512][3136],  box 128 rows
   CUtensorMap w0t;     // W0^T bf16         [3136][512],  box 128
-  CUtensorMap hxa[4];  // HX [rows][3136], box 32/64/96/128 rows (history tiles)
+  CUtensorMap hxa[4];  // HX [rows][3136], box 32/64/96/128 rows (history tiles; hxa[1]
+                       // is also the 64-feature x 64-row MN-major atom of the dgrad/mat GEMMs)
   CUtensorMap hxb;     // HX               box 32  (current rows)
   CUtensorMap hda[4];  // HD [rows][512],  box 32/64/96/128
   CUtensorMap hdb;     // HD               box 32
@@ -60,13 +62,25 @@ struct LzMaps {
   CUtensorMap hds;     // HD               box rs rows
   CUtensorMap hdt;     // HD^T [512][rows], box 128
   CUtensorMap hdtl;    // low part of the weighted HD^T (deferred fold), box 128
-  CUtensorMap hxt128;  // HX^T [3136][rows], box 128
-  CUtensorMap hxt256;  // HX^T               box 256
   CUtensorMap gdt;     // Gram rows [slots*64][njt*128] (per slot 32 high then 32 low rows), box 32
 };
 
 inline int njt_of_host(int step, int BS) { return (step * BS + 127) >> 7; }
 __device__ __forceinline__ int njt_of(const Args& a) { return (a.step * a.BS + 127) >> 7; }
+
+// MN-major SWIZZLE_128B bf16 operand (the history X read straight from its
+// row-major [rows][3136] layout as an [M or N = features][K = history rows]
+// operand): atoms of 64 features x 64 K rows (one TMA box each, 8 KB),
+// LBO = atom stride, SBO = 8 K rows; a K step of 16 advances 2048 B.
+__device__ __forceinline__ uint64_t desc_mn(uint32_t addr) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFFu);
+  d |= uint64_t(8192 >> 4) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
 
 // fp32 -> high + low bf16 terms (x ~= hi + lo to ~2^-17 relative)
 __device__ __forceinline__ void split_bf16(float x, bf16& hi, bf16& lo) {
@@ -91,33 +105,6 @@ __global__ void k_lz_w0t(const float* __restrict__ w0, bf16* __restrict__ w0t) {
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += 8)
     w0t[int64_t(k0 + y) * kH1 + o0 + threadIdx.x] = __float2bfloat16_rn(tile[threadIdx.x][y]);
-}
-
-// ---------------------------------------------------------------------------
-// k_lz_xt: history columns hxt[k][hist + t*BS + i] = X_t[i][k] of this sweep
-// grid (active, 25 k-tiles of 128), 128 threads
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_lz_xt(Args a) {
-  pb::pdl_wait();
-  const Slot sl = a.slots[blockIdx.x];
-  const int cnt = sl.cnt;
-  if (cnt == 0) return;
-  __shared__ __align__(16) bf16 tile[32][136];
-  const int k0 = blockIdx.y * 128, kn = min(128, kFlat - k0);
-  const bf16* x = hx_row(a, sl, 0);
-  for (int e = threadIdx.x; e < cnt * 16; e += 128) {   // 16-byte units: 8 bf16 of a row
-    const int i = e >> 4, k8 = (e & 15) * 8;
-    if (k8 < kn)
-      *reinterpret_cast<uint4*>(&tile[i][k8]) = *reinterpret_cast<const uint4*>(x + int64_t(i) * kFlat + k0 + k8);
-  }
-  __syncthreads();
-  bf16* xt = a.hxt + int64_t(k0) * a.hrows + sl.hist + int64_t(a.step) * a.BS;
-  // columns [cnt, zc) (partial batch, padding after the last step) -> 0
-  const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);
-  for (int e = threadIdx.x; e < zc * kn; e += 128) {
-    const int kk = e / zc, i = e - kk * zc;
-    xt[int64_t(kk) * a.hrows + i] = i < cnt ? tile[i][kk] : __float2bfloat16_rn(0.0f);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -469,10 +456,10 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_bwd: dp2 = dH_t W0 + sum_j hxt[k][j] gdt[i][j] for spc slots x rs rows
+// k_lz_bwd: dp2 = dH_t W0 + sum_j hx[j][k] gdt[i][j] for spc slots x rs rows
 //   phase 1 (shared): M = 128 k, N = spc*rs, K = 512 (A = w0t, B = dH_t rows)
 //   phase 2 (per slot, t > 0): M = 128 k, N = 32, K = t*BS into the slot's
-//   accumulator columns (A = the client's hxt columns, B = its gdt rows, the
+//   accumulator columns (A = the client's X history rows read MN-major, B = its gdt rows, the
 //   high and the low term against the same A tile)
 // Dense sweeps (spc = 8) take MT = 2 k-tiles per CTA (512 TMEM columns): the
 // dH_t and gdt tiles are read once per 256 k.
@@ -528,8 +515,11 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         const int c2 = c - n1, u = us[c2 / nj], jc = c2 % nj;
         pb::tma::expect_tx(f, uint32_t(MT * kShA + 2 * 32 * 128));
 #pragma unroll
-        for (int q = 0; q < MT; ++q)
-          pb::tma::load_2d(st + q * kShA, &m.hxt128, int(sS[u].hist) + jc * kAK, (kt0 + q) * 128, f);
+        for (int q = 0; q < MT; ++q)   // X rows of the history, MN-major: two 64-feature atoms
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            pb::tma::load_2d(st + q * kShA + h * 8192, &m.hxa[1], (kt0 + q) * 128 + h * 64,
+                             int(sS[u].hist) + jc * kAK, f);
         pb::tma::load_2d(st + MT * kShA, &m.gdt, jc * kAK, (g0 + u) * 64, f);
         pb::tma::load_2d(st + MT * kShA + 32 * 128, &m.gdt, jc * kAK, (g0 + u) * 64 + 32, f);
       }
@@ -547,18 +537,18 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         }
       } else {
         const int u = us[(c - n1) / nj];
-        const uint32_t idesc = idesc_bf16(128, 32);
+        const uint32_t idesc = idesc_bf16(128, 32, true, false);
         const uint64_t bh = desc_sw128(smem_u32(st + MT * kShA));
         const uint64_t bl = desc_sw128(smem_u32(st + MT * kShA + 32 * 128));
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
-          const uint64_t ah = desc_sw128(smem_u32(st + q * kShA));
+          const uint32_t as = smem_u32(st + q * kShA);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, true);
+            mma_bf16(tmem + q * 256 + u * rs, desc_mn(as + kk * 2048), bh + uint64_t(kk * 2), idesc, true);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16(tmem + q * 256 + u * rs, ah + uint64_t(kk * 2), bl + uint64_t(kk * 2), idesc, true);
+            mma_bf16(tmem + q * 256 + u * rs, desc_mn(as + kk * 2048), bl + uint64_t(kk * 2), idesc, true);
         }
       }
     };
@@ -589,7 +579,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hxt[k][j]
+// k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hx[j][k]
 // (M = 128 o, N = 256 k, K = steps_r * BS rounded to 64 -- within the
 // client's 64-aligned history); grid (13, 4, g), 256 threads -- the client
 // is the slowest grid dimension, so its 52 tiles re-read its history from L2.
@@ -622,14 +612,17 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, kShStage);
       pb::tma::load_2d(st, &m.hdt, hcol + c * kAK, q * 128, f);
-      pb::tma::load_2d(st + kShA, &m.hxt256, hcol + c * kAK, k0, f);
+#pragma unroll
+      for (int h = 0; h < 4; ++h)   // X rows of the history, MN-major: four 64-feature atoms
+        pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, hcol + c * kAK, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
-      const uint32_t idesc = idesc_bf16(128, 256);
+      const uint64_t a0 = desc_sw128(smem_u32(st));
+      const uint32_t bs = smem_u32(st + kShA);
+      const uint32_t idesc = idesc_bf16(128, 256, false, true);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
     };
     tma_ring<kStages>((K + kAK - 1) / kAK, smem, kShStage, full, empty, issue, mma);
   }
@@ -666,7 +659,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
 // per-client fc1 weights are never materialised.
 //   k_lz_scale   hdt columns of client j -> w_j * dH as high (in place) +
 //                low (hdt_lo) bf16 terms               (HDT is round scratch)
-//   k_lz_fold    split-K GEMM D[o][k] = sum_rows (hdt + hdt_lo)[o][row] hxt[k][row]
+//   k_lz_fold    split-K GEMM D[o][k] = sum_rows (hdt + hdt_lo)[o][row] hx[row][k]
 //                -> part[split][512][3136]   grid (13, 4, splits)
 //   k_lz_fold_reduce  acc += wsum * W0 - lr * sum_split part (split order)
 // ---------------------------------------------------------------------------
@@ -710,14 +703,17 @@ __global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMa
       const int col = row_lo + (c0 + c % nc) * kAK;
       pb::tma::expect_tx(f, kShStage);
       pb::tma::load_2d(st, c < nc ? &m.hdt : &m.hdtl, col, q * 128, f);
-      pb::tma::load_2d(st + kShA, &m.hxt256, col, k0, f);
+#pragma unroll
+      for (int h = 0; h < 4; ++h)   // X rows of the history, MN-major: four 64-feature atoms
+        pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, col, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st)), b0 = desc_sw128(smem_u32(st + kShA));
-      const uint32_t idesc = idesc_bf16(128, 256);
+      const uint64_t a0 = desc_sw128(smem_u32(st));
+      const uint32_t bs = smem_u32(st + kShA);
+      const uint32_t idesc = idesc_bf16(128, 256, false, true);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, a0 + uint64_t(kk * 2), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
     };
     tma_ring<kStages>(2 * nc, smem, kShStage, full, empty, issue, mma);
   }
@@ -826,9 +822,7 @@ int lazy_fc1_prepare(Args& a, cudaStream_t s) {
       (rc = make_2d_bf16(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
       (rc = make_2d_bf16(&m->hxs, a.hx, kFlat, R, kFlat, uint32_t((a.BS + 7) & ~7))) ||
       (rc = make_2d_bf16(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))) ||
-      (rc = make_2d_bf16(&m->hdt, a.hdt, R, kH1, R, 128)) ||
-      (rc = make_2d_bf16(&m->hxt128, a.hxt, R, kFlat, R, 128)) ||
-      (rc = make_2d_bf16(&m->hxt256, a.hxt, R, kFlat, R, 256)))
+      (rc = make_2d_bf16(&m->hdt, a.hdt, R, kH1, R, 128)))
     return rc;
   for (int q = 0; q < 4; ++q)   // history boxes sized to the live rows of a tile
     if ((rc = make_2d_bf16(&m->hxa[q], a.hx, kFlat, R, kFlat, 32 * (q + 1))) ||
@@ -881,8 +875,8 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   const int spc = slots_per_cta(active);
   const unsigned groups = unsigned((active + spc - 1) / spc);
   if (phase == 0) {
-    // the history transpose and the forward Gram (HBM-bound) run on a side
-    // stream concurrently with the shared-W0 GEMM (tensor / L2-bound); the
+    // the forward Gram (HBM-bound) runs on a side stream concurrently with
+    // the shared-W0 GEMM (tensor / L2-bound); the
     // GEMM then leaves raw partials, and the epilogue (b1 + partials +
     // history corrections, relu) joins both
     cudaStream_t sg = s;
@@ -893,9 +887,6 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       cudaEventRecord(side.fork, s);
       cudaStreamWaitEvent(sg, side.fork, 0);
     }
-    pb::prof_begin(pb::K_CNN_LZ_XT, sg);
-    pb::launch_pdl(k_lz_xt, dim3(active, kBwKT), dim3(128), 0, sg, 1, a);
-    pb::prof_end(pb::K_CNN_LZ_XT, sg);
     if (njt > 0) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, sg);
       // sparse sweeps: split K over a cluster while the grid fits one wave
@@ -973,7 +964,7 @@ extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream)
   using namespace pb::cnn;
   if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: null args");
   const pb_cnn_lazy_fold_args& f = *args;
-  if (!f.acc || !f.w0 || !f.hxt || !f.hdt || !f.hdt_lo || !f.hoff || !f.nrows || !f.w || !f.part ||
+  if (!f.acc || !f.w0 || !f.hx || !f.hdt || !f.hdt_lo || !f.hoff || !f.nrows || !f.w || !f.part ||
       f.hrows <= 0 || f.hrows % kAK || f.nclients < 0 || f.splits < 1 || f.row_lo < 0 || f.row_hi < f.row_lo ||
       f.row_lo % kAK || f.row_hi > f.hrows || !pb::aligned16(f.acc) || !pb::aligned16(f.w0) ||
       !pb::aligned16(f.part) || !pb::aligned16(f.hdt_lo))
@@ -986,7 +977,7 @@ extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream)
   using pb::tma::make_2d_bf16;
   const uint64_t R = uint64_t(f.hrows);
   if ((rc = make_2d_bf16(&m.hdt, f.hdt, R, kH1, R, 128)) || (rc = make_2d_bf16(&m.hdtl, f.hdt_lo, R, kH1, R, 128)) ||
-      (rc = make_2d_bf16(&m.hxt256, f.hxt, R, kFlat, R, 256)))
+      (rc = make_2d_bf16(&m.hxa[1], f.hx, kFlat, R, kFlat, 64)))
     return rc;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
   k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(static_cast<bf16*>(f.hdt), static_cast<bf16*>(f.hdt_lo),
