@@ -213,7 +213,7 @@ typedef struct {
   void* lz_hxt;             /* unused (the GEMMs over history rows read lz_hx */
                             /* MN-major); may be NULL                         */
   void* lz_hd;              /* [lz_rows, 512] bf16                            */
-  void* lz_hdt;             /* [512, lz_rows] bf16                            */
+  void* lz_hdt;             /* unused (history rows are read MN-major); NULL  */
   const int64_t* lz_hoff;   /* [g]                                            */
   const int32_t* lz_hlen;   /* [g]                                            */
   void* lz_w0t;             /* 2*3136*512 bf16 scratch: W1 of w0 transposed,  */
@@ -245,15 +245,15 @@ int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
  *   acc += wsum * W0 - lr * sum_j w_j * HD_j^T HX_j
  * over the device's clients j, whose history rows are [row_lo, row_hi) of
  * the round's [lz_rows] history (pb_cnn_train_group with lz_defer = 1).
- * The weighted dH^T columns w_j * dH_j are split into two bf16 terms (high
- * part in hdt in place -- round scratch --, low part in hdt_lo), so the
+ * The weighted dH rows w_j * dH_j are split into two bf16 terms (high part
+ * in hd in place -- round scratch --, low part in hd_lo), so the
  * weighting is exact to ~2^-17 and both terms run on bf16 tensor cores.
  * part: splits * 512 * 3136 f32 scratch. */
 typedef struct {
   float* acc;               /* [512*3136] fc1_w accumulator of the partial     */
   const float* w0;          /* [P] round-start model                           */
   const void* hx;           /* [hrows, 3136] bf16: the X history              */
-  void* hdt;                /* [512, hrows] bf16 (overwritten: w_j * dH, high) */
+  void* hd;                 /* [hrows, 512] bf16 (overwritten: w_j * dH, high) */
   int64_t hrows, row_lo, row_hi;
   const int64_t* hoff;      /* [nclients] first history row of each client    */
   const int32_t* nrows;     /* [nclients] live history rows (steps * BS)       */
@@ -262,7 +262,7 @@ typedef struct {
   float* part;
   int32_t splits;
   float wsum, lr;
-  void* hdt_lo;             /* [512, hrows] bf16 scratch: w_j * dH, low part   */
+  void* hd_lo;              /* [hrows, 512] bf16 scratch: w_j * dH, low part   */
 } pb_cnn_lazy_fold_args;
 int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream);
 

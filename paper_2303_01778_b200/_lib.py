@@ -55,10 +55,10 @@ class CnnTrainArgs(ctypes.Structure):
 
 class LazyFoldArgs(ctypes.Structure):
     _fields_ = [
-        ("acc", c_void_p), ("w0", c_void_p), ("hx", c_void_p), ("hdt", c_void_p),
+        ("acc", c_void_p), ("w0", c_void_p), ("hx", c_void_p), ("hd", c_void_p),
         ("hrows", c_int64), ("row_lo", c_int64), ("row_hi", c_int64), ("hoff", c_void_p),
         ("nrows", c_void_p), ("w", c_void_p), ("nclients", c_int64), ("part", c_void_p),
-        ("splits", c_int32), ("wsum", c_float), ("lr", c_float), ("hdt_lo", c_void_p),
+        ("splits", c_int32), ("wsum", c_float), ("lr", c_float), ("hd_lo", c_void_p),
     ]
 
 

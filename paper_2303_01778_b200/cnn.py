@@ -46,7 +46,7 @@ class _LazyWorkspace:
     """Grow-only buffers of the low-rank fc1 (csrc/cnn_lazy.cu): the round's
     (X, dH) history per client plus the per-sweep partials."""
 
-    HISTORY = ("hx", "hd", "hdt")
+    HISTORY = ("hx", "hd")
 
     def __init__(self):
         self.buf: dict[str, torch.Tensor] = {}
@@ -69,8 +69,7 @@ class _LazyWorkspace:
 
     def get(self, rows: int, zp: int, gdt: int, slots: int, device) -> dict[str, torch.Tensor]:
         b16 = torch.bfloat16   # the history and the W0 copies are bf16 tensor-core operands
-        out = {"hx": self._get("hx", rows * 3136, device, b16),
-               "hd": self._get("hd", rows * 512, device, b16), "hdt": self._get("hdt", rows * 512, device, b16),
+        out = {"hx": self._get("hx", rows * 3136, device, b16), "hd": self._get("hd", rows * 512, device, b16),
                "w0t": self._get("w0t", 2 * 3136 * 512, device, b16), "zp": self._get("zp", zp, device),
                "gdt": self._get("gdt", gdt, device, b16),
                "fpart": self._get("fpart", max(74, slots) * 512 * 32, device)}
@@ -160,14 +159,14 @@ class LazyFc1:
         nrows = h2d(nr, d)
         w = h2d(weights, d)
         part = _LZ._get("fold_part", self.SPLITS * 512 * 3136, d)
-        lo_buf = _LZ._get("hdt_lo", self.rows * 512, d, torch.bfloat16)
+        lo_buf = _LZ._get("hd_lo", self.rows * 512, d, torch.bfloat16)
         f = LazyFoldArgs()
-        f.acc, f.w0, f.hx, f.hdt = ptr(acc), ptr(self.w0), ptr(self.lz["hx"]), ptr(self.lz["hdt"])
+        f.acc, f.w0, f.hx, f.hd = ptr(acc), ptr(self.w0), ptr(self.lz["hx"]), ptr(self.lz["hd"])
         f.hrows, f.row_lo, f.row_hi = self.rows, lo, hi
         f.hoff, f.nrows, f.w, f.nclients = ptr(hoff), ptr(nrows), ptr(w), len(rows)
         f.part, f.splits = ptr(part), self.SPLITS
         f.wsum, f.lr = float(np.sum(weights.astype(np.float64))), self.lr
-        f.hdt_lo = ptr(lo_buf)
+        f.hd_lo = ptr(lo_buf)
         lib.check(lib.pb_cnn_lazy_fold(ctypes.byref(f), stream_of(acc)))
 
 
@@ -254,7 +253,7 @@ def cnn_train_group(data, rows_d, off_d, n: np.ndarray, w0, w_out, loss, steps, 
         lz = _LZ.get(rows, zp, gdt, G, d)
         hlen_d = h2d(hlen, d)
         hoff_d = h2d(hoff, d)
-        a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = ptr(lz["hx"]), None, ptr(lz["hd"]), ptr(lz["hdt"])
+        a.lz_hx, a.lz_hxt, a.lz_hd, a.lz_hdt = ptr(lz["hx"]), None, ptr(lz["hd"]), None
         a.lz_hoff, a.lz_hlen, a.lz_w0t = ptr(hoff_d), ptr(hlen_d), ptr(lz["w0t"])
         a.lz_zp, a.lz_gdt, a.lz_fpart = ptr(lz["zp"]), ptr(lz["gdt"]), ptr(lz["fpart"])
         a.lz_rows = rows

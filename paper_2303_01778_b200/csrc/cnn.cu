@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
     return;
   }
   // dH = dlogits W2 (old weights) masked by relu'; stored [i][o] and [o][i<32]
-  // (lazy fc1: into the history rows hd[t*BS + i] and columns hdt[o][t*BS + i])
+  // (lazy fc1: into the bf16 history rows hd[t*BS + i])
   const int64_t lzrow = sl.hist + int64_t(a.step) * a.BS;
   float* dh = a.dh + sidx(slot, 0, a.BS) * kH1;
   bf16* dhb = a.hx ? a.hd + lzrow * kH1 : nullptr;   // lazy fc1: the bf16 history rows
@@ -635,13 +635,8 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   __syncthreads();  // sDH complete
   if (a.hx) {
     // dH^T columns of the global [512][hrows] history (row pitch hrows)
-    bf16* hdt = a.hdt + sl.hist + int64_t(a.step) * a.BS;
-    const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);   // columns [cnt, zc) -> 0
-    for (int p = tid; p < zc * (ohi - olo); p += kHeadDenseThreads) {
-      const int o = olo + p / zc, i = p - (o - olo) * zc;
-      hdt[int64_t(o) * a.hrows + i] = __float2bfloat16_rn(i < cnt ? sDH[i * kDHS + o] : 0.0f);
-    }
-    for (int p = tid; p < (zc - cnt) * (ohi - olo); p += kHeadDenseThreads)   // and rows [cnt, zc) of hd
+    const int zc = int(sl.pad_ - int64_t(a.step) * a.BS);   // history rows [cnt, zc) -> 0
+    for (int p = tid; p < (zc - cnt) * (ohi - olo); p += kHeadDenseThreads)
       dhb[int64_t(cnt + p / (ohi - olo)) * kH1 + olo + p % (ohi - olo)] = __float2bfloat16_rn(0.0f);
     for (int o = olo + tid; o < ohi; o += kHeadDenseThreads) {  // fc1 bias (sample order)
       float g = 0.0f;
@@ -839,13 +834,8 @@ __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThread
   }
   __syncthreads();
   if (a.hx) {
-    bf16* hdt = a.hdt + sl.hist + int64_t(a.step) * BS;
-    const int zc = int(sl.pad_ - int64_t(a.step) * BS);   // columns [cnt, zc) -> 0
-    for (int p = tid; p < zc * kTailO; p += kHeadThreads) {
-      const int oo = p / zc, i = p - oo * zc;
-      hdt[int64_t(olo + oo) * a.hrows + i] = __float2bfloat16_rn(i < cnt ? sDH[i * kTailS + oo] : 0.0f);
-    }
-    for (int p = tid; p < (zc - cnt) * kTailO; p += kHeadThreads)   // and rows [cnt, zc) of hd
+    const int zc = int(sl.pad_ - int64_t(a.step) * BS);   // history rows [cnt, zc) -> 0
+    for (int p = tid; p < (zc - cnt) * kTailO; p += kHeadThreads)
       dhb[int64_t(cnt + p / kTailO) * kH1 + olo + p % kTailO] = __float2bfloat16_rn(0.0f);
     for (int oo = tid; oo < kTailO; oo += kHeadThreads) {   // fc1 bias (sample order)
       float g = 0.0f;
@@ -1692,7 +1682,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.ctrl_stride = t.ctrl_stride; a.loss_sum = t.loss_sum; a.steps = t.steps; a.bad = t.bad;
   a.slots = reinterpret_cast<Slot*>(t.ws_slots);
   a.hx = static_cast<bf16*>(t.lz_hx);
-  a.hd = static_cast<bf16*>(t.lz_hd); a.hdt = static_cast<bf16*>(t.lz_hdt); a.hoff = t.lz_hoff;
+  a.hd = static_cast<bf16*>(t.lz_hd); a.hoff = t.lz_hoff;
   a.hlen = t.lz_hlen; a.w0t = static_cast<bf16*>(t.lz_w0t); a.zp = t.lz_zp;
   a.gdt = static_cast<bf16*>(t.lz_gdt); a.fpart = t.lz_fpart;
   a.hrows = t.lz_rows;
@@ -1812,9 +1802,9 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
-    if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hd || !a.hdt || !a.hoff || !a.hlen ||
+    if (a.mu != 0.0f || a.ctrl_g || a.ctrl_c || !a.hd || !a.hoff || !a.hlen ||
         !a.w0t || !a.zp || !a.gdt || !a.fpart || a.hrows <= 0 || a.hrows % 64 || !pb::aligned16(a.hx) ||
-        !pb::aligned16(a.hd) || !pb::aligned16(a.hdt) || !pb::aligned16(a.w0t))
+        !pb::aligned16(a.hd) || !pb::aligned16(a.w0t))
       return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad lazy-fc1 workspace");
     if ((rc = lazy_fc1_prepare(a, s))) {
       lazy_fc1_release(a);
@@ -1837,7 +1827,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
       // the still-active clients' fc1 after sw steps -> their w rows; from
       // here on they train on the direct kernels (p2 / dH in the workspace)
       if ((rc = lazy_fc1_switch(lz, active, s))) break;
-      a.hx = a.hd = a.hdt = nullptr;
+      a.hx = a.hd = nullptr;
       a.hoff = nullptr;
       a.hlen = nullptr;
     }

@@ -76,7 +76,6 @@ struct Args {
   // Stale rows are finite and meet exact zeros (pad rows/columns, Gram selects).
   bf16* hx;               // [hrows, kFlat]  X_t (the p2 activations)
   bf16* hd;               // [hrows, kH1]    dH_t = dL/dz1
-  bf16* hdt;              // [kH1, hrows]    dH transposed
   const int64_t* hoff;    // [G] first history row of client row r
   const int32_t* hlen;    // [G] L_r (multiple of 64)
   int64_t hrows;          // total history rows (multiple of 64)

@@ -25,9 +25,9 @@
 // terms (high + low, ~2^-17 relative), so the corrections carry no rounding
 // beyond the stored operands'.  Every operand tile is one TMA box of 64 bf16
 // of K (128 B) x up to 256 rows, SWIZZLE_128B K-major (tma.cuh); the history
-// is kept as plain row-major matrices ([rows, K]; dH also transposed, [K,
-// rows]) so each client's block is a box of one tensor map; GEMMs that
-// contract over history rows read X MN-major (no transposed copy).  One thread drives a
+// is kept as plain row-major matrices ([rows, K]) so each client's block is
+// a box of one tensor map; GEMMs that contract over history rows read X and
+// dH MN-major (no transposed copies).  One thread drives a
 // TMA -> MMA ring; the CTA's other warps run the epilogues.  Reductions have a
 // fixed order (no atomics): results are deterministic.
 #include <cooperative_groups.h>
@@ -56,12 +56,11 @@ struct LzMaps {
   CUtensorMap hxa[4];  // HX [rows][3136], box 32/64/96/128 rows (history tiles; hxa[1]
                        // is also the 64-feature x 64-row MN-major atom of the dgrad/mat GEMMs)
   CUtensorMap hxb;     // HX               box 32  (current rows)
-  CUtensorMap hda[4];  // HD [rows][512],  box 32/64/96/128
+  CUtensorMap hda[4];  // HD [rows][512],  box 32/64/96/128 (hda[1]: the MN-major dH atom)
   CUtensorMap hdb;     // HD               box 32
   CUtensorMap hxs;     // HX               box rs rows (packed current rows, spc > 1)
   CUtensorMap hds;     // HD               box rs rows
-  CUtensorMap hdt;     // HD^T [512][rows], box 128
-  CUtensorMap hdtl;    // low part of the weighted HD^T (deferred fold), box 128
+  CUtensorMap hdl;     // low part of the weighted HD (deferred fold), box 64 x 64 (MN-major atoms)
   CUtensorMap gdt;     // Gram rows [slots*64][njt*128] (per slot 32 high then 32 low rows), box 32
 };
 
@@ -112,7 +111,8 @@ __global__ void k_lz_w0t(const float* __restrict__ w0, bf16* __restrict__ w0t) {
 // current step's rows (M = 128 history rows, N = 32 current rows):
 //   FWD : Gx[j][i] = X_j . X_t,i  (K = 3136), then the forward correction
 //         partial  zp[s][jt][o][i] = -lr * sum_{j in tile} dH_j[o] Gx[j][i]
-//         (M = 4 x 128 o, N = 32, K = 128; A = hdt columns, B = Gx^T in smem
+//         (M = 4 x 128 o, N = 32, K = 128; A = the dH history rows read
+//         MN-major, B = Gx^T in smem
 //         as high + low bf16 terms)
 //   !FWD: Gd[j][i] = dH_j . dH_t,i (K = 512) -> gdt[s][hi|lo][i][j] = -lr * Gd
 // History rows j >= t*BS (the current step, later steps, other clients) are
@@ -229,20 +229,22 @@ __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMa
       const int q0 = rank * 4 / ks;
       auto issue = [&](int c, uint8_t* st, uint64_t* f) {   // c = (q - q0)*natom + jc
         pb::tma::expect_tx(f, kGrA);
-        pb::tma::load_2d(st, &m.hdt, hcol + (c % natom) * kAK, (q0 + c / natom) * 128, f);
+        const int o0 = (q0 + c / natom) * 128, row = hcol + (c % natom) * kAK;
+        pb::tma::load_2d(st, &m.hda[1], o0, row, f);          // dH history rows, MN-major:
+        pb::tma::load_2d(st + 8192, &m.hda[1], o0 + 64, row, f);   // two 64-output atoms
       };
       auto mma = [&](int c, uint8_t* st) {
         const int q = q0 + c / natom, jc = c % natom;
-        const uint64_t a0 = desc_sw128(smem_u32(st));
+        const uint32_t as = smem_u32(st);
         const uint64_t bh = desc_sw128(smem_u32(sGxT + jc * kGxAtom));
         const uint64_t bl = desc_sw128(smem_u32(sGxT + (2 + jc) * kGxAtom));
-        const uint32_t idesc = idesc_bf16(128, 32);
+        const uint32_t idesc = idesc_bf16(128, 32, true, false);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_bf16(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), bh + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
+          mma_bf16(tmem + 32 + q * 32, desc_mn(as + kk * 2048), bh + uint64_t(kk * 2), idesc, jc > 0 || kk > 0);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_bf16(tmem + 32 + q * 32, a0 + uint64_t(kk * 2), bl + uint64_t(kk * 2), idesc, true);
+          mma_bf16(tmem + 32 + q * 32, desc_mn(as + kk * 2048), bl + uint64_t(kk * 2), idesc, true);
       };
       tma_ring<kStages>(((rank + 1) * 4 / ks - q0) * natom, smem, kGrA, full2, empty2, issue, mma);
     }
@@ -579,7 +581,8 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
 }
 
 // ---------------------------------------------------------------------------
-// k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hdt[o][j] hx[j][k]
+// k_lz_mat: w[r][fc1][o][k] = w0[fc1][o][k] - lr * sum_j hd[j][o] hx[j][k]
+// (both operands the client's history rows, read MN-major)
 // (M = 128 o, N = 256 k, K = steps_r * BS rounded to 64 -- within the
 // client's 64-aligned history); grid (13, 4, g), 256 threads -- the client
 // is the slowest grid dimension, so its 52 tiles re-read its history from L2.
@@ -611,18 +614,19 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
     const int hcol = int(a.hoff[r]);
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       pb::tma::expect_tx(f, kShStage);
-      pb::tma::load_2d(st, &m.hdt, hcol + c * kAK, q * 128, f);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)   // dH rows of the history, MN-major: two 64-output atoms
+        pb::tma::load_2d(st + h * 8192, &m.hda[1], q * 128 + h * 64, hcol + c * kAK, f);
 #pragma unroll
       for (int h = 0; h < 4; ++h)   // X rows of the history, MN-major: four 64-feature atoms
         pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, hcol + c * kAK, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st));
-      const uint32_t bs = smem_u32(st + kShA);
-      const uint32_t idesc = idesc_bf16(128, 256, false, true);
+      const uint32_t as = smem_u32(st), bs = smem_u32(st + kShA);
+      const uint32_t idesc = idesc_bf16(128, 256, true, true);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, a0 + uint64_t(kk * 2), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, desc_mn(as + kk * 2048), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
     };
     tma_ring<kStages>((K + kAK - 1) / kAK, smem, kShStage, full, empty, issue, mma);
   }
@@ -657,27 +661,22 @@ __global__ void __launch_bounds__(256, 1) k_lz_mat(const __grid_constant__ LzMap
 //   sum_j w_j W1_j = (sum_j w_j) W0 - lr * sum_j w_j HD_j^T HX_j
 // over its clients j (contiguous history rows [row_lo, row_hi)), so the
 // per-client fc1 weights are never materialised.
-//   k_lz_scale   hdt columns of client j -> w_j * dH as high (in place) +
-//                low (hdt_lo) bf16 terms               (HDT is round scratch)
-//   k_lz_fold    split-K GEMM D[o][k] = sum_rows (hdt + hdt_lo)[o][row] hx[row][k]
+//   k_lz_scale   dH history rows of client j -> w_j * dH as high (in place)
+//                + low (hd_lo) bf16 terms                (HD is round scratch)
+//   k_lz_fold    split-K GEMM D[o][k] = sum_rows (hd + hd_lo)[row][o] hx[row][k]
 //                -> part[split][512][3136]   grid (13, 4, splits)
 //   k_lz_fold_reduce  acc += wsum * W0 - lr * sum_split part (split order)
 // ---------------------------------------------------------------------------
-__global__ void k_lz_scale(bf16* __restrict__ hdt, bf16* __restrict__ hdtl, int64_t hrows,
-                           const int64_t* __restrict__ hoff, const int32_t* __restrict__ nrows,
-                           const float* __restrict__ w) {
+__global__ void k_lz_scale(bf16* __restrict__ hd, bf16* __restrict__ hdl, const int64_t* __restrict__ hoff,
+                           const int32_t* __restrict__ nrows, const float* __restrict__ w) {
   const int j = blockIdx.y;
-  const int64_t c0 = hoff[j], n = (int64_t(nrows[j]) + kAK - 1) / kAK * kAK;   // whole 64-column atoms
+  const int64_t r0 = hoff[j], n = (int64_t(nrows[j]) + kAK - 1) / kAK * kAK;   // whole 64-row atoms
   const float wj = w[j];
-  for (int o = blockIdx.x; o < kH1; o += gridDim.x) {
-    bf16* row = hdt + int64_t(o) * hrows + c0;
-    bf16* rowl = hdtl + int64_t(o) * hrows + c0;
-    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
-      bf16 hi, lo;
-      split_bf16(wj * __bfloat162float(row[c]), hi, lo);
-      row[c] = hi;
-      rowl[c] = lo;
-    }
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * kH1; e += int64_t(gridDim.x) * blockDim.x) {
+    bf16 hi, lo;
+    split_bf16(wj * __bfloat162float(hd[r0 * kH1 + e]), hi, lo);
+    hd[r0 * kH1 + e] = hi;
+    hdl[r0 * kH1 + e] = lo;
   }
 }
 
@@ -700,20 +699,21 @@ __global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMa
   if (tid == 0 && nc > 0) {
     // every chunk twice: the high then the low term of the weighted dH^T
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      const int col = row_lo + (c0 + c % nc) * kAK;
+      const int row = row_lo + (c0 + c % nc) * kAK;
       pb::tma::expect_tx(f, kShStage);
-      pb::tma::load_2d(st, c < nc ? &m.hdt : &m.hdtl, col, q * 128, f);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)   // weighted dH rows (high, then low term), MN-major
+        pb::tma::load_2d(st + h * 8192, c < nc ? &m.hda[1] : &m.hdl, q * 128 + h * 64, row, f);
 #pragma unroll
       for (int h = 0; h < 4; ++h)   // X rows of the history, MN-major: four 64-feature atoms
-        pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, col, f);
+        pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, row, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint64_t a0 = desc_sw128(smem_u32(st));
-      const uint32_t bs = smem_u32(st + kShA);
-      const uint32_t idesc = idesc_bf16(128, 256, false, true);
+      const uint32_t as = smem_u32(st), bs = smem_u32(st + kShA);
+      const uint32_t idesc = idesc_bf16(128, 256, true, true);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, a0 + uint64_t(kk * 2), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, desc_mn(as + kk * 2048), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
     };
     tma_ring<kStages>(2 * nc, smem, kShStage, full, empty, issue, mma);
   }
@@ -763,16 +763,16 @@ __global__ void k_lz_fold_reduce(float* __restrict__ acc, const float* __restric
   }
 }
 
-// switch mode of k_lz_mat reads whole 64-column atoms: the history columns
+// switch mode of k_lz_mat reads whole 64-row atoms: the history rows
 // [K, round_up(K, 64)) of the active clients (their next steps, stale) must
-// be zero in hdt first.  grid (active), 256 threads
+// be zero in hd first.  grid (active), 256 threads
 __global__ void k_lz_zero_tail(Args a, int K) {
   pb::pdl_wait();
   const Slot sl = a.slots[blockIdx.x];
   const int n = ((K + kAK - 1) / kAK) * kAK - K;
   if (sl.cnt == 0 || n == 0) return;
   for (int e = threadIdx.x; e < kH1 * n; e += blockDim.x)
-    a.hdt[int64_t(e / n) * a.hrows + sl.hist + K + e % n] = __float2bfloat16_rn(0.0f);
+    a.hd[(sl.hist + K) * kH1 + e] = __float2bfloat16_rn(0.0f);
 }
 
 int setup() {
@@ -821,8 +821,7 @@ int lazy_fc1_prepare(Args& a, cudaStream_t s) {
       (rc = make_2d_bf16(&m->hxb, a.hx, kFlat, R, kFlat, 32)) ||
       (rc = make_2d_bf16(&m->hdb, a.hd, kH1, R, kH1, 32)) ||
       (rc = make_2d_bf16(&m->hxs, a.hx, kFlat, R, kFlat, uint32_t((a.BS + 7) & ~7))) ||
-      (rc = make_2d_bf16(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))) ||
-      (rc = make_2d_bf16(&m->hdt, a.hdt, R, kH1, R, 128)))
+      (rc = make_2d_bf16(&m->hds, a.hd, kH1, R, kH1, uint32_t((a.BS + 7) & ~7))))
     return rc;
   for (int q = 0; q < 4; ++q)   // history boxes sized to the live rows of a tile
     if ((rc = make_2d_bf16(&m->hxa[q], a.hx, kFlat, R, kFlat, 32 * (q + 1))) ||
@@ -964,10 +963,10 @@ extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream)
   using namespace pb::cnn;
   if (!args) return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: null args");
   const pb_cnn_lazy_fold_args& f = *args;
-  if (!f.acc || !f.w0 || !f.hx || !f.hdt || !f.hdt_lo || !f.hoff || !f.nrows || !f.w || !f.part ||
+  if (!f.acc || !f.w0 || !f.hx || !f.hd || !f.hd_lo || !f.hoff || !f.nrows || !f.w || !f.part ||
       f.hrows <= 0 || f.hrows % kAK || f.nclients < 0 || f.splits < 1 || f.row_lo < 0 || f.row_hi < f.row_lo ||
       f.row_lo % kAK || f.row_hi > f.hrows || !pb::aligned16(f.acc) || !pb::aligned16(f.w0) ||
-      !pb::aligned16(f.part) || !pb::aligned16(f.hdt_lo))
+      !pb::aligned16(f.part) || !pb::aligned16(f.hd_lo))
     return pb::fail(PB_ERR_INVALID, "pb_cnn_lazy_fold: bad arguments");
   if (f.nclients == 0) return PB_OK;
   int rc = setup();
@@ -976,12 +975,12 @@ extern "C" int pb_cnn_lazy_fold(const pb_cnn_lazy_fold_args* args, void* stream)
   LzMaps m{};
   using pb::tma::make_2d_bf16;
   const uint64_t R = uint64_t(f.hrows);
-  if ((rc = make_2d_bf16(&m.hdt, f.hdt, R, kH1, R, 128)) || (rc = make_2d_bf16(&m.hdtl, f.hdt_lo, R, kH1, R, 128)) ||
+  if ((rc = make_2d_bf16(&m.hda[1], f.hd, kH1, R, kH1, 64)) || (rc = make_2d_bf16(&m.hdl, f.hd_lo, kH1, R, kH1, 64)) ||
       (rc = make_2d_bf16(&m.hxa[1], f.hx, kFlat, R, kFlat, 64)))
     return rc;
   pb::prof_begin(pb::K_CNN_LZ_MAT, s);
-  k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(static_cast<bf16*>(f.hdt), static_cast<bf16*>(f.hdt_lo),
-                                                            f.hrows, f.hoff, f.nrows, f.w);
+  k_lz_scale<<<dim3(64, unsigned(f.nclients)), 256, 0, s>>>(static_cast<bf16*>(f.hd), static_cast<bf16*>(f.hd_lo),
+                                                            f.hoff, f.nrows, f.w);
   pb::prof_end(pb::K_CNN_LZ_MAT, s);
   const int chunks = int((f.row_hi - f.row_lo + kAK - 1) / kAK);
   const int per = (chunks + f.splits - 1) / f.splits;
