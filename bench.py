@@ -438,16 +438,18 @@ _TRAFFIC = None
 
 def measured_traffic(name):
     """DRAM bytes per launch of a kernel class (mean over one C2 round's
-    launches) from the committed ncu capture profiles/r1_traffic.json
+    launches) from the newest committed ncu capture profiles/r*_traffic.json
     (tools/traffic_summary.py), or None."""
     global _TRAFFIC
     if _TRAFFIC is None:
-        try:
-            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                   "r1_traffic.json")) as fh:
-                _TRAFFIC = json.load(fh)["kernels"]
-        except (OSError, ValueError, KeyError):
-            _TRAFFIC = {}
+        _TRAFFIC = {}
+        for name_ in ("r2_traffic.json", "r1_traffic.json"):
+            try:
+                with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name_)) as fh:
+                    _TRAFFIC = json.load(fh)["kernels"]
+                break
+            except (OSError, ValueError, KeyError):
+                continue
     k = _TRAFFIC.get(name)
     return None if k is None else k["dram_bytes_per_launch"]
 
