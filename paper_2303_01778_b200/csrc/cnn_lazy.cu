@@ -126,13 +126,13 @@ __global__ void k_lz_w0t(const float* __restrict__ w0, bf16* __restrict__ w0t) {
 constexpr int kGrA = 128 * 128;                // 16 KB: 128 history rows x one K atom
 constexpr int kGrB = 32 * 128;                 // 4 KB: 32 current rows
 constexpr int kGrStage = kGrA + kGrB;          // 20 KB per K atom (64 features)
-constexpr int kGrStages = 8;
+// ring depth: 4 stages (~97 KB, two CTAs per SM) when the grid exceeds one
+// wave at one CTA per SM, else 8 (the deepest ring for a handful of CTAs)
 constexpr int kGxAtom = 32 * 128;              // Gx^T: [32 i][64 j] bf16, 4 KB
 constexpr int kGxT = 2 * 2 * kGxAtom;          // two j atoms, high + low terms: 16 KB
-constexpr size_t kGramFwdSmem = 1024 + kGrStages * kGrStage + kGxT;
-constexpr size_t kGramBwdSmem = 1024 + kGrStages * kGrStage;
+constexpr size_t gram_smem(bool fwd, int stages) { return 1024 + stages * kGrStage + (fwd ? kGxT : 0); }
 
-template <bool FWD>
+template <bool FWD, int kGrStages>
 __global__ void __launch_bounds__(128, 1) k_lz_gram(const __grid_constant__ LzMaps m, Args a, int ks) {
   pb::pdl_wait();
   const int s = blockIdx.y, jt = blockIdx.x / ks, rank = blockIdx.x - jt * ks;   // a client's tiles are adjacent
@@ -296,6 +296,13 @@ constexpr int kShA = 128 * 128;                 // 16 KB: 128 rows x one K atom
 constexpr int kShB = 256 * 128;                 // 32 KB
 constexpr int kShStage = kShA + kShB;           // 48 KB
 constexpr size_t kShSmem = 1024 + kStages * kShStage;
+// MT = 1 variants (spc <= 4 slots of <= 32 rows: B <= 96 rows / 12 KB) use
+// 3 stages of 28 KB, so two CTAs (and their TMA -> MMA chains) share an SM
+// in the sparse sweeps
+constexpr int kShB1 = 96 * 128;
+constexpr int kSh1Stage = kShA + kShB1;
+constexpr size_t kSh1Smem = 1024 + 3 * kSh1Stage;       // 3 stages: two CTAs per SM
+constexpr size_t kSh1DeepSmem = 1024 + 6 * kSh1Stage;   // 6 stages for grids within one wave
 constexpr int kFwdChunks = kFlat / kAK;         // 49 K atoms
 constexpr int kTailCtas = 296;                  // 2 x 148 SMs: tail grids aim for this
 constexpr int kFwdSplitMax = 7;                 // 49 atoms = 7 x 7
@@ -322,16 +329,15 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
     if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
 }
 
-template <int MT>
+template <int MT, int S>
 __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
                                                    int fuse, int rs) {
   pb::pdl_wait();
-  constexpr int S = MT == 1 ? kStages : 3;        // stages of MT*16 + 32 KB
-  constexpr int kStage = MT * kShA + kShB;
-  static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_fwd ring");
+  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + kShB;   // 28 KB (MT = 1) or 64 KB (MT = 2)
+  static_assert(S <= 6 && 1024 + S * kStage <= 227 * 1024, "lz_fwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t full[6], empty[6];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -469,16 +475,15 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 // ---------------------------------------------------------------------------
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
-template <int MT>
+template <int MT, int S>
 __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
                                                    int rs) {
   pb::pdl_wait();
-  constexpr int S = MT == 1 ? kStages : 3;
-  constexpr int kStage = MT * kShA + kShB;   // 48 | 64 KB
-  static_assert(S <= kStages && 1024 + S * kStage <= kShSmem, "lz_bwd ring");
+  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + kShB;   // 28 | 64 KB
+  static_assert(S <= 6 && 1024 + S * kStage <= 227 * 1024, "lz_bwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t full[6], empty[6];
   __shared__ uint32_t tmem_base;
   __shared__ Slot sS[kSh8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -782,12 +787,16 @@ int setup() {
     const void* fn;
     size_t bytes;
     const char* name;
-  } attrs[] = {{(const void*)k_lz_gram<true>, kGramFwdSmem, "k_lz_gram<fwd>"},
-               {(const void*)k_lz_gram<false>, kGramBwdSmem, "k_lz_gram<bwd>"},
-               {(const void*)k_lz_fwd<1>, kShSmem, "k_lz_fwd"},
-               {(const void*)k_lz_fwd<2>, kShSmem, "k_lz_fwd"},
-               {(const void*)k_lz_bwd<1>, kShSmem, "k_lz_bwd"},
-               {(const void*)k_lz_bwd<2>, kShSmem, "k_lz_bwd"},
+  } attrs[] = {{(const void*)k_lz_gram<true, 4>, gram_smem(true, 4), "k_lz_gram<fwd>"},
+               {(const void*)k_lz_gram<true, 8>, gram_smem(true, 8), "k_lz_gram<fwd>"},
+               {(const void*)k_lz_gram<false, 4>, gram_smem(false, 4), "k_lz_gram<bwd>"},
+               {(const void*)k_lz_gram<false, 8>, gram_smem(false, 8), "k_lz_gram<bwd>"},
+               {(const void*)k_lz_fwd<1, 3>, kSh1Smem, "k_lz_fwd"},
+               {(const void*)k_lz_fwd<1, 6>, kSh1DeepSmem, "k_lz_fwd"},
+               {(const void*)k_lz_fwd<2, 3>, kShSmem, "k_lz_fwd"},
+               {(const void*)k_lz_bwd<1, 3>, kSh1Smem, "k_lz_bwd"},
+               {(const void*)k_lz_bwd<1, 6>, kSh1DeepSmem, "k_lz_bwd"},
+               {(const void*)k_lz_bwd<2, 3>, kShSmem, "k_lz_bwd"},
                {(const void*)k_lz_mat, kShSmem, "k_lz_mat"},
                {(const void*)k_lz_fold, kShSmem, "k_lz_fold"}};
   for (auto& x : attrs) {
@@ -891,19 +900,27 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       // sparse sweeps: split K over a cluster while the grid fits one wave
       const int sms = pb::sm_count();
       const int gks = njt * active * 4 <= sms ? 4 : (njt * active * 2 <= sms ? 2 : 1);
-      pb::launch_pdl(k_lz_gram<true>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128), kGramFwdSmem, sg,
-                     unsigned(gks), m, a, gks);
+      if (njt * active * gks <= sms)   // one wave at one CTA per SM: the deep ring
+        pb::launch_pdl(k_lz_gram<true, 8>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128),
+                       gram_smem(true, 8), sg, unsigned(gks), m, a, gks);
+      else
+        pb::launch_pdl(k_lz_gram<true, 4>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128),
+                       gram_smem(true, 4), sg, unsigned(gks), m, a, gks);
       pb::prof_end(pb::K_CNN_LZ_GRAM_FWD, sg);
     }
     const int ks = spc == 1 ? std::max(1, std::min(kFwdSplitMax, kTailCtas / (4 * active))) : 1;
     const int fuse = !fork && ks == 1;
     const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;   // B rows per slot: packed when several share a CTA
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
+    const int sms = pb::sm_count();
     if (spc == kSh8)
-      pb::launch_pdl(k_lz_fwd<2>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
+      pb::launch_pdl(k_lz_fwd<2, 3>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
                      rs);
+    else if (int(groups) * (kH1 / 128) * ks <= sms)
+      pb::launch_pdl(k_lz_fwd<1, 6>, dim3(kH1 / 128, groups, ks), dim3(256), kSh1DeepSmem, s, 1, m, a, active, spc,
+                     fuse, rs);
     else
-      pb::launch_pdl(k_lz_fwd<1>, dim3(kH1 / 128, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
+      pb::launch_pdl(k_lz_fwd<1, 3>, dim3(kH1 / 128, groups, ks), dim3(256), kSh1Smem, s, 1, m, a, active, spc, fuse,
                      rs);
     pb::prof_end(pb::K_CNN_LZ_FWD, s);
     if (fork) {
@@ -922,16 +939,21 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
                                      uint64_t(njt) * 128, 32);
       if (rc) return rc;
       pb::prof_begin(pb::K_CNN_LZ_GRAM_BWD, s);
-      pb::launch_pdl(k_lz_gram<false>, dim3(njt, active), dim3(128), kGramBwdSmem, s, 1, m, a, 1);
+      if (njt * active <= pb::sm_count())
+        pb::launch_pdl(k_lz_gram<false, 8>, dim3(njt, active), dim3(128), gram_smem(false, 8), s, 1, m, a, 1);
+      else
+        pb::launch_pdl(k_lz_gram<false, 4>, dim3(njt, active), dim3(128), gram_smem(false, 4), s, 1, m, a, 1);
       pb::prof_end(pb::K_CNN_LZ_GRAM_BWD, s);
     }
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
     {
       const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;
       if (spc == kSh8)
-        pb::launch_pdl(k_lz_bwd<2>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
+        pb::launch_pdl(k_lz_bwd<2, 3>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
+      else if (kBwKT * int(groups) <= pb::sm_count())
+        pb::launch_pdl(k_lz_bwd<1, 6>, dim3(kBwKT, groups), dim3(256), kSh1DeepSmem, s, 1, m, a, active, spc, rs);
       else
-        pb::launch_pdl(k_lz_bwd<1>, dim3(kBwKT, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
+        pb::launch_pdl(k_lz_bwd<1, 3>, dim3(kBwKT, groups), dim3(256), kSh1Smem, s, 1, m, a, active, spc, rs);
     }
     pb::prof_end(pb::K_CNN_LZ_BWD, s);
   }
