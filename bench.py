@@ -621,13 +621,13 @@ C4_TOTAL, C4_ROUND, C4_SAMPLES, C4_CLASSES = 1000, 100, 50_000, 10
 C4_FLOP_PER_SAMPLE = 3.34e9
 
 
-def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
-    """C4: 1000 clients with the reference's Dirichlet size rule (quantity
-    skew 0.1, min 5 samples), 100 per round, bs 20, E 1, lr 0.05 on one GPU;
-    synthetic CIFAR-shaped data generated on the device."""
+def c4_engine(dev, total_rounds: int):
+    """C4's engine: 1000 clients with the reference's Dirichlet size rule
+    (label skew 0.5, quantity skew 0.1, min 5 samples), 100 per round, bs 20,
+    E 1, lr 0.05 on one GPU; synthetic CIFAR-shaped data generated on the
+    device."""
     import torch
     import paper_2303_01778_b200 as pb
-    from paper_2303_01778_b200._lib import lib, prof_collect
     from paper_2303_01778_b200.core import STREAM_PARTITION, ClientProfile, DataSlice, stream_rng
     from paper_2303_01778_b200.data import PartitionSpec, client_sizes as sizes_fn
     from paper_2303_01778_b200.trainer import ClientData
@@ -647,9 +647,17 @@ def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
                                                   np.zeros(int(n), dtype=np.int64), np.arange(int(n))))
                 for c, n in enumerate(sizes)]
     cfg = pb.SimConfig(total_clients=C4_TOTAL, concurrent_clients=C4_ROUND, num_devices=1,
-                       total_rounds=warmup + 2 * steps + 1, warmup_rounds=1, seed=0, scheme="PARROT")
-    eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=LR, batch_size=BS), profiles, pb.make_device_models(1),
-                              model="resnet", client_data=data, init_seed=0)
+                       total_rounds=total_rounds, warmup_rounds=1, seed=0, scheme="PARROT")
+    return pb.SimulationEngine(cfg, pb.FedAvg(lr=LR, batch_size=BS), profiles, pb.make_device_models(1),
+                               model="resnet", client_data=data, init_seed=0)
+
+
+def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
+    """C4 rounds (c4_engine): a profiled pass for the per-kernel breakdown,
+    then device-timed rounds."""
+    import torch
+    from paper_2303_01778_b200._lib import lib, prof_collect
+    eng = c4_engine(dev, warmup + 2 * steps + 1)
     for r in range(warmup):
         eng.run_round(r)
     # profiled rounds (events around every launch) for the per-kernel breakdown

@@ -6,8 +6,8 @@ import io
 import subprocess
 import sys
 
-print("| kernel | grid | cluster | duration µs | DRAM MB | warps active % | issue % | top stalls |")
-print("|---|---|---|---|---|---|---|---|")
+print("| kernel | grid | cluster | duration µs | DRAM MB | warps active % | issue % | tensor pipe % | top stalls |")
+print("|---|---|---|---|---|---|---|---|---|")
 for rep in sys.argv[1:]:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -23,8 +23,11 @@ for rep in sys.argv[1:]:
         top = sorted(st.items(), key=lambda x: -x[1])[:3]
         stalls = ", ".join(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * v / tot:.0f}%" for k, v in top)
         def num(k):
+            v = d.get(k)
+            if v is None:   # some metrics carry a section prefix in the raw page
+                v = next((x for h_, x in d.items() if h_.endswith("." + k)), "")
             try:
-                return float(d.get(k, "").replace(",", ""))
+                return float(v.replace(",", ""))
             except ValueError:
                 return float("nan")
         name = d["Kernel Name"].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
@@ -32,4 +35,5 @@ for rep in sys.argv[1:]:
         print(f"| {name} | {d.get('launch__grid_size')} | {d.get('launch__cluster_dim_x', '') or '-'} | "
               f"{num('gpu__time_duration.sum') * {'ns': 1e-3, 'us': 1.0, 'ms': 1e3, 'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(units.get('gpu__time_duration.sum'), 1.0):.1f} | {mb:.1f} | "
               f"{num('sm__warps_active.avg.pct_of_peak_sustained_active'):.0f} | "
-              f"{num('smsp__issue_active.avg.pct_of_peak_sustained_active'):.0f} | {stalls} |")
+              f"{num('smsp__issue_active.avg.pct_of_peak_sustained_active'):.0f} | "
+              f"{num('sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed'):.0f} | {stalls} |")

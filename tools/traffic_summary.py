@@ -32,7 +32,10 @@ for r in rows:
 tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for (_, name), m in per.items():
     base = re.sub(r"\(.*", "", name).split("::")[-1].replace("void ", "").strip()
-    cls = next((c for k, c in CLASS if base == k or base.startswith(k)), None)
+    if base.startswith("k_lz_gram"):   # template args may be printed as <(bool)1, (int)8>
+        cls = "cnn_lz_gram_fwd" if re.search(r"k_lz_gram<(\(bool\))?(1|true)", name) else "cnn_lz_gram_bwd"
+    else:
+        cls = next((c for k, c in CLASS if base == k or base.startswith(k)), None)
     if cls is None:
         continue
     t = tot[cls]
