@@ -237,6 +237,9 @@ typedef struct {
                             /* sweep and after the last one, or NULL: sweep s */
                             /* lasts timeline[s+1] - timeline[s] ns and is    */
                             /* shared by its active clients (real clock)      */
+  void* ws_w2b;             /* [g][102400 B] scratch: bf16 conv2 weights in   */
+                            /* the tensor-core layout, rebuilt from w at the  */
+                            /* start of a call and kept in step with it       */
 } pb_cnn_train_args;
 int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream);
 

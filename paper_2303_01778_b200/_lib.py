@@ -49,7 +49,7 @@ class CnnTrainArgs(ctypes.Structure):
         ("C", c_int32), ("BS", c_int32), ("batch_size", c_int32), ("epochs", c_int32),
         ("samples_per_cta", c_int32),
         ("lr", c_float), ("mu", c_float), ("cg", c_float), ("cc", c_float),
-        ("timeline", c_void_p),
+        ("timeline", c_void_p), ("ws_w2b", c_void_p),
     ]
 
 

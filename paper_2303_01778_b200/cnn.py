@@ -35,6 +35,7 @@ class _Workspace:
             self.buf = {k: torch.empty(n * v + 5392, dtype=torch.uint8, device=device)
                         for k, v in _PER_SAMPLE.items()}
             self.buf["slots"] = torch.empty(self.slots * 32, dtype=torch.uint8, device=device)
+            self.buf["w2b"] = torch.empty(self.slots * 102400, dtype=torch.uint8, device=device)
             self.buf["dht"] = torch.empty(self.slots * 512 * 32 * 4, dtype=torch.uint8, device=device)
         return self.buf
 
@@ -189,6 +190,7 @@ def _samples_per_cta() -> int:
 
 def _fill(args: CnnTrainArgs, ws: dict, slots: int, BS: int) -> None:
     args.ws_slots = ptr(ws["slots"])
+    args.ws_w2b = ptr(ws["w2b"])
     for k in ("p1", "am1", "p2", "am2", "h", "dh", "dp2", "dz", "dp1", "dht"):
         setattr(args, "ws_" + k, ptr(ws[k]))
     args.g = slots

@@ -62,6 +62,22 @@ __global__ void k_slots(Args a, int active) {
   a.slots[j] = s;
 }
 
+// ---------------------------------------------------------------------------
+// k_w2b: conv2 weights of group rows -> bf16 UMMA B layout (w2_off), the
+// copy the conv kernels bulk-load; k_wgrad keeps it in step afterwards.
+// grid (ceil(6400/256), rows), 256 threads: one 16-byte unit (8 ci) each
+// ---------------------------------------------------------------------------
+__global__ void k_w2b(Args a) {
+  pb::pdl_wait();
+  const int r = blockIdx.y, u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= 64 * 100) return;
+  const int co = u / 100, tap = (u % 100) >> 2, cg = u & 3;
+  const float4* w = reinterpret_cast<const float4*>(a.w + int64_t(r) * a.P + oC2W + co * 800 + tap * 32 + cg * 8);
+  const float4 v0 = w[0], v1 = w[1];
+  *reinterpret_cast<uint4*>(a.w2b + int64_t(r) * kW2Bytes + w2_off(co, tap, cg * 8)) =
+      make_uint4(pack_bf16(v0.x, v0.y), pack_bf16(v0.z, v0.w), pack_bf16(v1.x, v1.y), pack_bf16(v1.z, v1.w));
+}
+
 // barrier 1 over the 512 work threads of the warp-specialised kernels (their
 // MMA-issue warp never joins it)
 __device__ __forceinline__ void work_sync() { asm volatile("bar.sync 1, 512;\n" ::: "memory"); }
@@ -108,7 +124,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t c1_done, c2_done[2], a_ready, p1_ready;
+  __shared__ __align__(8) uint64_t c1_done, c2_done[2], a_ready, p1_ready, w2_full;
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
   uint8_t* sPl = sW2 + kW2Bytes;                                   // p1 planes (one sample)
@@ -129,7 +145,6 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     const int n8 = int(sl.pad_ - int64_t(a.step) * a.BS - sl.cnt) * (kFlat / 8);
     for (int e = tid; e < n8; e += kFwdThreads) z[e] = make_uint4(0, 0, 0, 0);
   }
-  stage_w2(sW2, W, tid, kFwdThreads);
   // conv1 B: column n = d*32 + co, K = (u, v) of the 6x6 window:
   // W1[co][u - dy][v - dx] when inside the 5x5 filter, else 0
   for (int e = tid; e < 6 * 128 * 8; e += kFwdThreads) {
@@ -153,6 +168,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     mbar_init(&c2_done[1], 1);
     mbar_init(&a_ready, 16);    // one arrive per work warp
     mbar_init(&p1_ready, 16);
+    mbar_init(&w2_full, 1);
     fence_init();
   }
   fence_async_smem();
@@ -168,6 +184,9 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       const uint32_t sa1 = smem_u32(sA1), sb1 = smem_u32(sB1w);
       const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
       const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
+      // the client's conv2 weights (bf16, UMMA layout): one bulk copy
+      pb::tma::expect_tx(&w2_full, uint32_t(kW2Bytes));
+      pb::tma::bulk_load(sW2, a.w2b + int64_t(sl.r) * kW2Bytes, uint32_t(kW2Bytes), &w2_full);
       for (int i = i0; i < i1; ++i) {
         mbar_wait(&a_ready, (i - i0) & 1);
         fence_after_sync();
@@ -182,6 +201,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
         pb::tma::bulk_wait_reads();
         commit(&c1_done);
         mbar_wait(&p1_ready, (i - i0) & 1);
+        if (i == i0) mbar_wait(&w2_full, 0);
         fence_after_sync();
         const uint32_t th = tmem + uint32_t((i & 1) * 128);
 #pragma unroll
@@ -1138,7 +1158,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t dz_full, dz_free, mma_done[2], tmem_idle[2], am1_full[2];
+  __shared__ __align__(8) uint64_t dz_full, dz_free, mma_done[2], tmem_idle[2], am1_full[2], w2_full;
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
@@ -1149,7 +1169,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   float* sG = reinterpret_cast<float*>(sAm1 + 2 * kP1);  // [49][64]
   float* sHalo = sG + 49 * 64;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  stage_w2(sW2, a.w + int64_t(sl.r) * a.P, tid, kBwdThreads);
   // the dz2 planes: borders stay zero; every sample rewrites all 4 candidates
   // of each pooled position
   for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
@@ -1162,6 +1181,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       mbar_init(&tmem_idle[b], 16);
       mbar_init(&am1_full[b], 1);
     }
+    mbar_init(&w2_full, 1);
     fence_init();
   }
   fence_async_smem();
@@ -1175,9 +1195,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
     if (lane == 0) {
       const uint32_t sdz = smem_u32(sDz), sw = smem_u32(sW2);
       const uint32_t id128 = idesc_bf16(128, 128, false, true), id32 = idesc_bf16(128, 32, false, true);
+      // the client's conv2 weights (bf16, UMMA layout): one bulk copy
+      pb::tma::expect_tx(&w2_full, uint32_t(kW2Bytes));
+      pb::tma::bulk_load(sW2, a.w2b + int64_t(sl.r) * kW2Bytes, uint32_t(kW2Bytes), &w2_full);
       for (int i = i0; i < i1; ++i) {
         const int64_t sid = sidx(blockIdx.y, i, a.BS);
         mbar_wait(&dz_full, (i - i0) & 1);
+        if (i == i0) mbar_wait(&w2_full, 0);
         if (i - i0 >= 2) mbar_wait(&tmem_idle[i & 1], ((i - 2 - i0) >> 1) & 1);   // set read out (sample i-2)
         fence_after_sync();
         const uint32_t dset = tmem + uint32_t((i & 1) * 256);
@@ -1632,6 +1656,9 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
           w.z = fmaf(nlr, g.z, w.z);
           w.w = fmaf(nlr, g.w, w.w);
           *reinterpret_cast<float4*>(W + oC2W + tap0 * 32 + off[k]) = w;
+          const int cc = tap0 * 32 + c;   // (tap, ci) of the 4 weights -> the bf16 UMMA copy
+          *reinterpret_cast<uint2*>(a.w2b + int64_t(sl.r) * kW2Bytes + w2_off(co, cc >> 5, cc & 31)) =
+              make_uint2(pack_bf16(w.x, w.y), pack_bf16(w.z, w.w));
         }
       }
     }
@@ -1648,7 +1675,11 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
         g = cl.map_shared_rank(sG, 0)[co * kWgStride + c];
         for (int q = 1; q < sg; ++q) g += cl.map_shared_rank(sG, q)[co * kWgStride + c];
       }
-      W[idx] = sgd(a, sl.r, idx, W[idx], g);
+      const float nw = sgd(a, sl.r, idx, W[idx], g);
+      W[idx] = nw;
+      const int cc = tap0 * 32 + c;
+      *reinterpret_cast<__nv_bfloat16*>(a.w2b + int64_t(sl.r) * kW2Bytes + w2_off(co, cc >> 5, cc & 31)) =
+          __float2bfloat16(nw);
     }
   }
   if (sg > 1) cgp::this_cluster().sync();   // partner tiles stay alive until every read is done
@@ -1700,6 +1731,7 @@ static Args to_args(const pb_cnn_train_args& t) {
   a.P = t.w_stride;  // row stride of the parameter matrix (>= the model size)
   a.lr = t.lr; a.mu = t.mu; a.cg = t.cg; a.cc = t.cc;
   a.timeline = t.timeline;
+  a.w2b = static_cast<uint8_t*>(t.ws_w2b);
   return a;
 }
 
@@ -1804,9 +1836,11 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
   int rc = cnn_setup();
   if (rc) return rc;
   Args a = to_args(t);
+  if (!a.w2b || !pb::aligned16(a.w2b)) return pb::fail(PB_ERR_INVALID, "pb_cnn_train_group: bad ws_w2b");
   ConvMaps maps;
   if ((rc = conv_maps(a, t.g, &maps))) return rc;
   cudaStream_t s = pb::as_stream(stream);
+  pb::launch_pdl(k_w2b, dim3(25, unsigned(t.g)), dim3(256), 0, s, 1, a);
   const int spb = t.samples_per_cta != 0 ? t.samples_per_cta : 10;
   if (a.hx) {
     // the low-rank fc1 covers plain SGD only (no prox / control-variate terms)
@@ -1862,7 +1896,9 @@ extern "C" int pb_cnn_eval(const pb_cnn_train_args* args, int64_t rows, double* 
   Args a = to_args(t);
   a.eval = out2;
   a.hx = nullptr;  // evaluation reads the materialised weights
+  if (!a.w2b || !pb::aligned16(a.w2b)) return pb::fail(PB_ERR_INVALID, "pb_cnn_eval: bad ws_w2b");
   cudaStream_t s = pb::as_stream(stream);
+  pb::launch_pdl(k_w2b, dim3(25, 1), dim3(256), 0, s, 1, a);   // every slot reads row 0
   // slots: batches of BS consecutive rows of `order`, all on parameter row 0
   const int64_t nslots = (rows + t.BS - 1) / t.BS;
   const int64_t cap = t.g;  // workspace capacity in slots

@@ -85,6 +85,10 @@ struct Args {
   bf16* gdt;              // [slots][32][njt*128]   -lr * (dH_t . dH_j) Gram rows
   float* fpart;           // [ks][active][kH1][32] tail split-K partials (<= 74*16384 f32)
   int64_t* timeline;      // [sweeps + 1] sweep start stamps (real clock) or null
+  // conv2 weights of every group row as bf16 in the UMMA B layout (w2_off),
+  // kept in step with the fp32 masters by k_wgrad: the conv kernels stage
+  // them with one bulk copy instead of converting the fp32 rows per CTA
+  uint8_t* w2b;           // [G][kW2Bytes]
   int64_t P;
   int32_t C, BS, bs, epochs, step;
   float lr, mu, cg, cc;
