@@ -690,7 +690,7 @@ def resnet_round_bench(dev, steps: int = 2, warmup: int = 1) -> dict:
     tf = C4_FLOP_PER_SAMPLE * samples / (ms / 1e3) / 1e12
     conv_ms = sum(v[0] for k, v in kernels.items() if k.startswith("rn_conv"))
     conv_tf = C4_FLOP_PER_SAMPLE * prof_samples / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else None
-    del eng, data, X
+    del eng
     torch.cuda.empty_cache()
     return {"workload": "C4: FedAvg ResNet-18-GN (P=11,173,962), 1000 clients (Dirichlet sizes, "
                         "quantity skew 0.1), 100 per round, bs=20, E=1, lr=0.05, 1 GPU",
