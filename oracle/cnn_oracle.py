@@ -68,8 +68,9 @@ class _RoundGrad(torch.autograd.Function):
 
 class _Conv1Bf16(torch.autograd.Function):
     """conv1 as the device computes it (csrc/cnn.cu k_fwd): bf16 image and
-    weights on the tensor cores, fp32 accumulation; the weight gradient uses
-    the fp32 image (the backward kernel's SIMT conv1 gradient)."""
+    weights on the tensor cores, fp32 accumulation; the weight gradient is
+    also a bf16 tensor-core product (k_bwd_conv: bf16 image windows x the
+    bf16-rounded pre-pool gradient, which `forward` rounds with _RoundGrad)."""
 
     @staticmethod
     def forward(ctx, x, w):   # x [B, 1, 28, 28], w NHWC [32, 5, 5, 1]
@@ -81,7 +82,8 @@ class _Conv1Bf16(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         x, w = ctx.saved_tensors
-        gw = torch.nn.grad.conv2d_weight(x, (w.shape[0], w.shape[3], w.shape[1], w.shape[2]), g, padding=2)
+        gw = torch.nn.grad.conv2d_weight(_bf16(x), (w.shape[0], w.shape[3], w.shape[1], w.shape[2]), _bf16(g),
+                                         padding=2)
         return None, gw.permute(0, 2, 3, 1)
 
 
@@ -149,8 +151,8 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     """x [B, 784] -> logits; conv weights are NHWC ([co, ky, kx, ci]).
 
     emulate_bf16=True rounds exactly the operands the device feeds to its
-    tensor cores -- bf16 for conv1 (the image and W1 in the forward; its weight
-    gradient uses the fp32 image), bf16 for conv2 (p1 and W2 in the forward, dL/dz2 in both
+    tensor cores -- bf16 for conv1 (the image and W1 in the forward, the image
+    and dL/dz1 in its weight gradient), bf16 for conv2 (p1 and W2 in the forward, dL/dz2 in both
     backward GEMMs) and tf32 truncation for fc1 (X and W1 in the forward, dL/dz1
     in both backward GEMMs); everything else stays in the oracle's precision.
     Used to check the kernels' arithmetic separately from the effect of the
@@ -166,7 +168,7 @@ def forward(params, x: torch.Tensor, emulate_bf16: bool = False,
     c1w, c1b, c2w, c2b, f1w, f1b, f2w, f2b = params
     h = x.reshape(-1, 1, 28, 28)
     if emulate_bf16:
-        h = F.max_pool2d(F.relu(_Conv1Bf16.apply(h, c1w) + c1b.view(1, -1, 1, 1)), 2)
+        h = F.max_pool2d(F.relu(_RoundGrad.apply(_Conv1Bf16.apply(h, c1w) + c1b.view(1, -1, 1, 1))), 2)
     else:
         h = F.max_pool2d(F.relu(F.conv2d(h, c1w.permute(0, 3, 1, 2), c1b, padding=2)), 2)
     if emulate_bf16:

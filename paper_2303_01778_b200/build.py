@@ -49,7 +49,8 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
         return obj, ""
     inc = ["-I", str(INCLUDE), "-I", str(CSRC)]
     if src.suffix == ".cu":
-        cmd = [_nvcc(), *NVCC_FLAGS, *inc, "-c", str(src), "-o", str(obj)]
+        defs = os.environ.get("PB_NVCC_DEFS", "").split()   # e.g. -DPB_PHASE_TRACE (tools only)
+        cmd = [_nvcc(), *NVCC_FLAGS, *defs, *inc, "-c", str(src), "-o", str(obj)]
     else:
         cmd = ["g++", *CXX_FLAGS, *inc, "-I", "/usr/local/cuda/include", "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)

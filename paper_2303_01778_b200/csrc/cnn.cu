@@ -30,6 +30,32 @@
 #include "cnn_common.cuh"
 #include "tma.cuh"
 
+// Phase trace of k_bwd_conv (tools/phase_probe.py): built only with
+// -DPB_PHASE_TRACE (PB_NVCC_DEFS at build time); the product build has none.
+#ifdef PB_PHASE_TRACE
+__device__ unsigned long long g_phase[64][16];
+__device__ int g_phase_armed;
+#define PB_PHASE(cond, slot, k)                                                                 \
+  do {                                                                                          \
+    if (g_phase_armed && blockIdx.x == 0 && blockIdx.y == 0 && (cond) && (slot) < 64) {         \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      g_phase[slot][k] = t_;                                                                    \
+    }                                                                                           \
+  } while (0)
+extern "C" int pb_phase_arm() {
+  const int one = 1;
+  unsigned long long z[64 * 16] = {};
+  cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  return int(cudaMemcpyToSymbol(g_phase_armed, &one, sizeof(int)));
+}
+extern "C" int pb_phase_read(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase)));
+}
+#else
+#define PB_PHASE(cond, slot, k) do { } while (0)
+#endif
+
 namespace {
 
 using namespace pb::umma;
@@ -1111,8 +1137,8 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 
 // ---------------------------------------------------------------------------
 // k_bwd_conv: per sample, dz2 planes (pool2/relu backward) -> conv2 dgrad on
-// tcgen05 -> dp1 -> pool1/relu backward fused with the conv1 weight gradient
-// and the conv1/conv2 bias gradients of this sample (per-sample partials,
+// tcgen05 -> dp1 -> pool1/relu backward -> conv1 weight and bias gradients on
+// tcgen05, plus the conv2 bias gradient of this sample (per-sample partials,
 // summed in sample order by k_wgrad: deterministic).
 //
 // dgrad MMAs, column-blocked: for filter row ky ONE N = 128 MMA multiplies
@@ -1126,30 +1152,45 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // costs the same ~52 cycles (tools/umma_bench2.py): 40 MMAs per sample (20 at
 // N = 128) replace 200 N = 32 ones.  M tiles: output rows [0, 125) from tile
 // rows [0, 128), rows [125, 248) from [124, 252) (row q = y*18 + x; x >= 14
-// discarded).
+// discarded), i.e. pooled rows y 0-6 and 7-13.
+//
+// conv1 weight gradient, per M tile (98 pooled positions p, K padded to 112):
+//   H[(d, co)][n] += sum_p G_d[p][co] * Win[p][n]
+// M = 128 = pool candidate d (TMEM lane quarter) x channel co, G_d[p][co] =
+// bf16(relu' * dp1[p][co]) where pool1's argmax is d and 0 for the other
+// three candidates; N = 48 = the 36 cells of the 6x6 input window at
+// (2py, 2px) (bf16 image) + a ones cell (the bias) + zero pad.  Both
+// operands MN-major, no swizzle (K rows 16 B apart, core columns 1792 B
+// apart).  Then dW1[co][ky][kx] = sum_d H[(d, co)][(ky + dy)*6 + kx + dx]
+// and db1[co] = sum_d H[(d, co)][36] (smem, fixed order).  14 MMAs per sample
+// replace 157k SIMT FMAs and their 25 shared-memory loads per tap.
 // Warp-specialised pipeline over the CTA's samples.  Warp 16 (one thread)
-// issues the MMAs of sample i into TMEM set i&1 as soon as its dz2 planes are
-// built, bulk-copies the planes to global for k_wgrad and the sample's pool1
-// argmaxes into smem; warps 0-15 build the planes of sample i from registers
+// issues the dgrad MMAs of sample i into TMEM set i&1 as soon as its dz2
+// planes are built, bulk-copies the planes to global for k_wgrad and the
+// sample's pool1 argmaxes into smem, then the conv1-gradient MMAs of sample
+// i-1 (into columns [0, 48) of set (i-1)&1, read out by then) as each tile
+// of G lands; warps 0-15 build the planes of sample i from registers
 // prefetched during sample i-1, then -- while the MMAs run -- finish sample
-// i-1 (TMEM -> dp1, pool1/relu backward, conv1 gradients).  mbarriers:
-// dz_full (planes built), mma_done[set], dz_free (MMAs + plane store of the
-// sample done), tmem_idle[set] (set read out), am1_full[buffer].
+// i-1 (TMEM -> dp1 -> G and the window operand, H -> conv1 partials).
+// mbarriers: dz_full (planes built), mma_done[set], dz_free (MMAs + plane
+// store of the sample done), tmem_idle[set] (set read out), am1_full[buffer],
+// g_full (a G tile + the window operand written), g_free (tile 0's conv1
+// MMAs done: G may be rewritten), wg_done (H complete).
 // grid (ceil(BS/spb), active), 544 threads
 // ---------------------------------------------------------------------------
 constexpr int kBwdWork = 512;                            // warps 0-15: SIMT work
 constexpr int kBwdThreads = kBwdWork + 32;               // + warp 16: MMA / bulk-copy issue
-constexpr int kDp1S = kC1 + 1;                           // dp1 row stride (conflict-free)
-constexpr int kBwdDp1 = 196 * kDp1S * 4;                 // dp1 [196][33] fp32
-constexpr int kBwdRed = 8 * 832 * 4;                     // warp-pair partials (aliases dp1 + image)
-// image row stride 34: the 4 pool candidates' windows (offsets 0, 1, 34, 35)
-// of the 32 channel lanes fall in distinct banks
+constexpr int kC1K = 112;                                // conv1-gradient K rows per tile (98 positions + zeros)
+constexpr int kC1CS = kC1K * 16;                         // core-column stride of G and Win (1792 B)
+constexpr int kBwdGw = 16 * kC1CS;                       // G of one tile: 16 (d, co) core columns (28,672 B)
+constexpr int kBwdWin = 6 * kC1CS;                       // window operand of one tile: 6 cell core columns
+// padded image [32][34]: 8 B aligned window pairs for the operand build
 constexpr int kXS = 34;
 constexpr int kBwdX = 32 * kXS * 4;
-constexpr int kBwdG = 49 * 64 * 4;                       // g = relu'(p2) * dp2 of one sample
+constexpr int kBwdB2 = 13 * 64 * 4;                      // conv2 bias partials of the 13 build warps
 constexpr int kBwdHalo = 4 * 4 * 3 * 3 * 8 * 4;          // [quarter][ci group][lane 0-2][block 0-2][8]
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdDp1 + kBwdX + 2 * kP1 + kBwdG + kBwdHalo;   // 205,456 B
-static_assert(kBwdRed <= kBwdDp1 + kBwdX, "k_bwd_conv reduction scratch");
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdGw + 2 * kBwdWin + kBwdX + 2 * kP1 + kBwdB2 + kBwdHalo;   // 220,544 B
+static_assert(kBwdSmem + 256 <= 232448, "k_bwd_conv shared memory");
 
 
 __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
@@ -1158,30 +1199,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t dz_full, dz_free, mma_done[2], tmem_idle[2], am1_full[2], w2_full;
+  __shared__ __align__(8) uint64_t dz_full, dz_free, tile_full[3], tile_free[3], am1_full[2], w2_full, g_full, g_free,
+      h_free[2];
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
-  float* sDp1 = reinterpret_cast<float*>(sDz + kDzBytes);
-  float* sX = sDp1 + 196 * kDp1S;                        // [32][kXS] padded image
-  float* sRed = sDp1;                                    // [8][832] (after the conv1 loop)
+  uint8_t* sGw = sDz + kDzBytes;                         // G (one tile)
+  uint8_t* sWin = sGw + kBwdGw;                          // window operand, both tiles
+  float* sX = reinterpret_cast<float*>(sWin + 2 * kBwdWin);   // [32][kXS] padded image
   uint8_t* sAm1 = reinterpret_cast<uint8_t*>(sX + 32 * kXS);   // 2 x [196][32] pool1 argmax / relu'
-  float* sG = reinterpret_cast<float*>(sAm1 + 2 * kP1);  // [49][64]
-  float* sHalo = sG + 49 * 64;
+  float* sB2w = reinterpret_cast<float*>(sAm1 + 2 * kP1);   // [13][64]
+  float* sHalo = sB2w + 13 * 64;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the dz2 planes: borders stay zero; every sample rewrites all 4 candidates
-  // of each pooled position
+  // of each pooled position.  G: its pad rows (positions 98-111) stay zero.
   for (int e = tid; e < kDzBytes / 16; e += kBwdThreads) reinterpret_cast<uint4*>(sDz)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < kBwdGw / 16; e += kBwdThreads) reinterpret_cast<uint4*>(sGw)[e] = make_uint4(0, 0, 0, 0);
   if (warp == 0) tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     mbar_init(&dz_full, 16);   // one arrive per work warp
     mbar_init(&dz_free, 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&tile_full[b], 1);
+      mbar_init(&tile_free[b], 16);
+    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&mma_done[b], 1);
-      mbar_init(&tmem_idle[b], 16);
       mbar_init(&am1_full[b], 1);
+      mbar_init(&h_free[b], 4);   // the four readout warps
     }
     mbar_init(&w2_full, 1);
+    mbar_init(&g_full, 16);
+    mbar_init(&g_free, 1);
     fence_init();
   }
   fence_async_smem();
@@ -1189,26 +1237,47 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
+  // H of sample j: columns [384 + 48 hb, +48), hb = (j - i0) & 1
+  auto tmem_h = [&](int j) { return tmem + uint32_t(3 * 128 + ((j - i0) & 1) * 48); };
 
   if (warp == 16) {
     // ---------------- MMA / bulk-copy issue (one thread) ----------------
     if (lane == 0) {
-      const uint32_t sdz = smem_u32(sDz), sw = smem_u32(sW2);
+      const uint32_t sdz = smem_u32(sDz), sw = smem_u32(sW2), sg = smem_u32(sGw), swin = smem_u32(sWin);
       const uint32_t id128 = idesc_bf16(128, 128, false, true), id32 = idesc_bf16(128, 32, false, true);
+      const uint32_t id48 = idesc_bf16(128, 48, true, true);
+      // conv1 gradient MMAs of sample j into its H buffer (read out by then)
+      auto conv1_mmas = [&](int j) {
+        const int u = j - i0;
+        if (u >= 2) mbar_wait(&h_free[u & 1], uint32_t((u / 2 - 1) & 1));
+#pragma unroll 1
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&g_full, uint32_t(t));
+          fence_after_sync();
+          const uint64_t ga = desc(sg, 128, kC1CS), wb = desc(swin + uint32_t(t * kBwdWin), 128, kC1CS);
+#pragma unroll
+          for (int k = 0; k < kC1K / 16; ++k)
+            mma_bf16(tmem_h(j), ga + uint64_t(k * 16), wb + uint64_t(k * 16), id48, t > 0 || k > 0);
+          commit(&g_free);
+        }
+      };
       // the client's conv2 weights (bf16, UMMA layout): one bulk copy
       pb::tma::expect_tx(&w2_full, uint32_t(kW2Bytes));
       pb::tma::bulk_load(sW2, a.w2b + int64_t(sl.r) * kW2Bytes, uint32_t(kW2Bytes), &w2_full);
       for (int i = i0; i < i1; ++i) {
         const int64_t sid = sidx(blockIdx.y, i, a.BS);
-        mbar_wait(&dz_full, (i - i0) & 1);
+        const int u = i - i0;
+        mbar_wait(&dz_full, u & 1);
         if (i == i0) mbar_wait(&w2_full, 0);
-        if (i - i0 >= 2) mbar_wait(&tmem_idle[i & 1], ((i - 2 - i0) >> 1) & 1);   // set read out (sample i-2)
-        fence_after_sync();
-        const uint32_t dset = tmem + uint32_t((i & 1) * 256);
+        PB_PHASE(true, u, 12);
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
+          // TMEM tile buffers: a ring of three, tile n = 2u + t in buffer n % 3
+          const int n = 2 * u + t, buf = n % 3;
+          if (n >= 3) mbar_wait(&tile_free[buf], uint32_t((n / 3 - 1) & 1));   // tile n - 3 read out
+          fence_after_sync();
           const int base = t ? 124 : 0;
-          const uint32_t dt = dset + uint32_t(t * 128);
+          const uint32_t dt = tmem + uint32_t(buf * 128);
 #pragma unroll 1
           for (int ky = 0; ky < 5; ++ky) {
             const uint64_t ab = desc(sdz + uint32_t(base + 73 - kG * ky) * 16, kPlane, 128);
@@ -1221,23 +1290,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
               mma_bf16(dt + 96, a4 + uint64_t(kq * (2 * kPlane / 16)), b4 + uint64_t(kq * 16), id32, true);
             }
           }
+          commit(&tile_full[buf]);
         }
-        commit(&mma_done[i & 1]);
         // dz2 planes -> global for k_wgrad; pool1 argmaxes of sample i -> smem
         pb::tma::bulk_store(a.dzg + sid * kDzBytes, sDz, uint32_t(kDzBytes));
         pb::tma::expect_tx(&am1_full[i & 1], uint32_t(kP1));
         pb::tma::bulk_load(sAm1 + (i & 1) * kP1, a.am1 + sid * kP1, uint32_t(kP1), &am1_full[i & 1]);
+        PB_PHASE(true, u, 13);
+        if (i > i0) conv1_mmas(i - 1);   // queued behind the dgrad of sample i
+        PB_PHASE(true, u, 14);
         pb::tma::bulk_wait_reads();
-        mbar_wait(&mma_done[i & 1], ((i - i0) >> 1) & 1);
+        {
+          const int n = 2 * u + 1;   // tile 1's commit: all of sample i's MMAs done
+          mbar_wait(&tile_full[n % 3], uint32_t((n / 3) & 1));
+        }
+        PB_PHASE(true, u, 15);
         mbar_arrive(&dz_free);   // the plane buffer may be rebuilt
       }
+      conv1_mmas(i1 - 1);
       pb::tma::bulk_wait_all();
     }
   } else {
     // ---------------- work warps 0-15 ----------------
     // dz2 build unit of this thread: pooled position pp, channel block cb
+    // (threads 0-391)
     const int upp = tid >> 3, ucb = tid & 7;
     const bool unit = tid < 49 * 8;
+    // prefetched registers are only copied until their use (no stall here);
+    // the lazy path keeps its bf16 history bits in rp[0]
     float4 rd[2], rp[2];
     uint2 ra = make_uint2(0, 0);
     auto prefetch_in = [&](int i) {   // pool2 inputs of sample i -> registers
@@ -1247,10 +1327,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       rd[0] = d4[0];
       rd[1] = d4[1];
       if (a.hx) {   // lazy fc1: X_t (only its sign matters here) in the bf16 history
-        const uint4 u = *reinterpret_cast<const uint4*>(hx_row(a, sl, i) + upp * 64 + ucb * 8);
-        const float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y), f2 = unpack_bf16(u.z), f3 = unpack_bf16(u.w);
-        rp[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
-        rp[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+        rp[0] = *reinterpret_cast<const float4*>(hx_row(a, sl, i) + upp * 64 + ucb * 8);
       } else {
         const float4* p4 = reinterpret_cast<const float4*>(p2_row(a, sl, blockIdx.y, i) + upp * 64 + ucb * 8);
         rp[0] = p4[0];
@@ -1259,173 +1336,289 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       ra = *reinterpret_cast<const uint2*>(a.am2 + sid * kFlat + upp * 64 + ucb * 8);
     };
     float rx[2];
+    int row_nx = a.order[sl.row_off + i0];   // dataset row of the next image to prefetch
+    auto img_in = [&](int k) {   // pixel k of this thread inside the 28x28 image
+      const int e = tid + k * kBwdWork, yy = e >> 5, xx = e & 31;
+      return yy >= 2 && yy < 30 && xx >= 2 && xx < 30;
+    };
     auto prefetch_img = [&](int i) {   // padded image of sample i -> registers (2 px per thread)
-      const float* img = a.X + int64_t(a.order[sl.row_off + i]) * (kImg * kImg);
+      const float* img = a.X + int64_t(row_nx) * (kImg * kImg);
+      if (i + 1 < i1) row_nx = a.order[sl.row_off + i + 1];   // used one sample later: no stall
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int e = tid + k * kBwdWork, yy = e >> 5, xx = e & 31;
-        rx[k] = (yy >= 2 && yy < 30 && xx >= 2 && xx < 30) ? img[(yy - 2) * kImg + (xx - 2)] : 0.0f;
+        rx[k] = img[img_in(k) ? (yy - 2) * kImg + (xx - 2) : 0];
       }
     };
     prefetch_in(i0);
     prefetch_img(i0);
     const int qw = warp & 3, cg = warp >> 2;   // epilogue: lane quarter, ci group of 8
+    // H of sample j -> its conv1 weight / bias partials, by warps 12-15 (one
+    // per TMEM lane quarter).  TMEM lane m = co*4 + d, so a warp holds all
+    // four pool candidates of 8 channels and the candidate sum
+    //   dW1[co][ky][kx] = sum_d H[(co, d)][(ky + dy)*6 + kx + dx]
+    // is a 4-lane shuffle reduction; cell 36 (the ones column) is the bias.
+    auto h_readout = [&](int j) {
+      const int d = lane & 3, co = qw * 8 + (lane >> 2);
+      const uint32_t th = tmem_h(j) + (uint32_t(qw * 32) << 16);
+      float h0[16], h1[16], h2[16];
+      tmem_ld16(th, h0);
+      tmem_ld16(th + 16, h1);
+      tmem_ld16(th + 32, h2);
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&h_free[(j - i0) & 1]);   // the conv1 MMAs of sample j+2 may overwrite it
+      float* pg = a.pg + sidx(blockIdx.y, j, a.BS) * kPg;
+      auto cell = [&](int c) { return c < 16 ? h0[c] : (c < 32 ? h1[c - 16] : h2[c - 32]); };
+      // this lane's candidate d contribution to the 25 taps + the bias
+      const bool dy = d >> 1, dx = d & 1;
+      float v[28];
+#pragma unroll
+      for (int ky = 0; ky < 5; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx) {
+          const int c = ky * 6 + kx;
+          const float top = dx ? cell(c + 1) : cell(c), bot = dx ? cell(c + 7) : cell(c + 6);
+          v[ky * 5 + kx] = dy ? bot : top;
+        }
+      v[25] = cell(36);
+      v[26] = v[27] = 0.0f;
+      // reduce-scatter over the 4 candidate lanes: lane d ends with the sums
+      // of outputs [7d, 7d + 7)
+      float half[14];
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        const float other = __shfl_xor_sync(0xffffffffu, dy ? v[k] : v[14 + k], 2);
+        half[k] = (dy ? v[14 + k] : v[k]) + other;
+      }
+      float res[7];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const float other = __shfl_xor_sync(0xffffffffu, dx ? half[k] : half[7 + k], 1);
+        res[k] = (dx ? half[7 + k] : half[k]) + other;
+      }
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const int o = 7 * d + k;
+        if (o < 25) pg[co * 25 + o] = res[k];
+        else if (o == 25) pg[800 + co] = res[k];
+      }
+    };
     for (int i = i0; i <= i1; ++i) {
       if (i < i1) {
         const int64_t sid = sidx(blockIdx.y, i, a.BS);
         // ---- sample i: dz2 planes (MMAs + plane store of sample i-1 done) ----
+        PB_PHASE(tid == 0, i - i0, 0);
         if (i > i0) mbar_wait(&dz_free, (i - 1 - i0) & 1);
-        if (unit) {
-          const float dv[8] = {rd[0].x, rd[0].y, rd[0].z, rd[0].w, rd[1].x, rd[1].y, rd[1].z, rd[1].w};
-          const float pv[8] = {rp[0].x, rp[0].y, rp[0].z, rp[0].w, rp[1].x, rp[1].y, rp[1].z, rp[1].w};
+        PB_PHASE(tid == 0, i - i0, 1);
+        if (warp < 13) {
           float g[8];
-          uint32_t d[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) g[k] = 0.0f;
+          if (unit) {
+            const float dv[8] = {rd[0].x, rd[0].y, rd[0].z, rd[0].w, rd[1].x, rd[1].y, rd[1].z, rd[1].w};
+            float pv[8];
+            if (a.hx) {
+              const float2 f0 = unpack_bf16(__float_as_uint(rp[0].x)), f1 = unpack_bf16(__float_as_uint(rp[0].y)),
+                           f2 = unpack_bf16(__float_as_uint(rp[0].z)), f3 = unpack_bf16(__float_as_uint(rp[0].w));
+              pv[0] = f0.x; pv[1] = f0.y; pv[2] = f1.x; pv[3] = f1.y;
+              pv[4] = f2.x; pv[5] = f2.y; pv[6] = f3.x; pv[7] = f3.y;
+            } else {
+              pv[0] = rp[0].x; pv[1] = rp[0].y; pv[2] = rp[0].z; pv[3] = rp[0].w;
+              pv[4] = rp[1].x; pv[5] = rp[1].y; pv[6] = rp[1].z; pv[7] = rp[1].w;
+            }
+            uint32_t d[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              g[k] = pv[k] > 0.0f ? dv[k] : 0.0f;
+              d[k] = ((k < 4 ? ra.x : ra.y) >> (8 * (k & 3))) & 0xFFu;
+            }
+            const int py = upp / 7, px = upp - py * 7;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                w[k] = pack_bf16(d[2 * k] == uint32_t(q) ? g[2 * k] : 0.0f,
+                                 d[2 * k + 1] == uint32_t(q) ? g[2 * k + 1] : 0.0f);
+              const int row = (2 * py + (q >> 1) + 2) * kG + 2 * px + (q & 1) + 2;
+              *reinterpret_cast<uint4*>(sDz + ucb * kPlane + row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          // conv2 bias partial: the warp's 4 pooled positions (lanes 8 apart)
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            g[k] = pv[k] > 0.0f ? dv[k] : 0.0f;
-            d[k] = ((k < 4 ? ra.x : ra.y) >> (8 * (k & 3))) & 0xFFu;
+            g[k] += __shfl_xor_sync(0xffffffffu, g[k], 8);
+            g[k] += __shfl_xor_sync(0xffffffffu, g[k], 16);
           }
-          const int py = upp / 7, px = upp - py * 7;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              w[k] = pack_bf16(d[2 * k] == uint32_t(q) ? g[2 * k] : 0.0f,
-                               d[2 * k + 1] == uint32_t(q) ? g[2 * k + 1] : 0.0f);
-            const int row = (2 * py + (q >> 1) + 2) * kG + 2 * px + (q & 1) + 2;
-            *reinterpret_cast<uint4*>(sDz + ucb * kPlane + row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (lane < 8) {
+            float4* b4 = reinterpret_cast<float4*>(sB2w + warp * 64 + lane * 8);
+            b4[0] = make_float4(g[0], g[1], g[2], g[3]);
+            b4[1] = make_float4(g[4], g[5], g[6], g[7]);
           }
-          *reinterpret_cast<float4*>(sG + upp * 64 + ucb * 8) = make_float4(g[0], g[1], g[2], g[3]);
-          *reinterpret_cast<float4*>(sG + upp * 64 + ucb * 8 + 4) = make_float4(g[4], g[5], g[6], g[7]);
+          fence_async_smem();
         }
-        fence_async_smem();
+        // H of sample i-2 (its conv1 MMAs finished during the previous
+        // epilogue), read while the tensor pipe is idle: before dz_full
+        if (warp >= 12 && i - 2 >= i0) {
+          mbar_wait(&g_free, uint32_t((2 * (i - 2 - i0) + 1) & 1));
+          fence_after_sync();
+          h_readout(i - 2);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&dz_full);
-        work_sync();   // sG complete
-        // conv2 bias partial of sample i: warps 14-15, one channel per lane
-        // (conflict-free rows of sG), pooled positions in order; the other
-        // warps go on to the next sample's prefetch
-        if (warp >= 14) {
-          const int ch = (warp - 14) * 32 + lane;
+        work_sync();   // bias partials complete
+        PB_PHASE(tid == 0, i - i0, 2);
+        if (tid < 64) {   // conv2 bias of sample i: warp partials in order
           float b2 = 0.0f;
-#pragma unroll 7
-          for (int pp = 0; pp < 49; ++pp) b2 += sG[pp * 64 + ch];
-          a.pg[sid * kPg + 832 + ch] = b2;
+#pragma unroll
+          for (int w = 0; w < 13; ++w) b2 += sB2w[w * 64 + tid];
+          a.pg[sid * kPg + 832 + tid] = b2;
         }
-        // the next sample's build rewrites sG: after the first sample no
-        // epilogue (with its barriers) separates the two
-        if (i == i0 && i + 1 < i1) work_sync();
         if (i + 1 < i1) prefetch_in(i + 1);
+        // no epilogue before the next build rewrites the bias partials
+        if (i == i0 && i + 1 < i1) work_sync();
       }
       if (i > i0) {
-        // ---- sample j = i-1: dp1, pool1 / relu backward, conv1 gradients ----
-        const int j = i - 1, set = j & 1;
-        const int64_t sid = sidx(blockIdx.y, j, a.BS);
-        mbar_wait(&mma_done[set], ((j - i0) >> 1) & 1);
-        fence_after_sync();
-        uint32_t r[2][4][8];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const uint32_t ta = tmem + (uint32_t(qw * 32) << 16) + uint32_t(set * 256 + t * 128 + cg * 8);
-#pragma unroll
-          for (int b = 0; b < 4; ++b) tmem_ld8_nw(ta + uint32_t(b * 32), r[t][b]);
-          tmem_wait_ld32(r[t][0], r[t][1], r[t][2], r[t][3]);
-        }
-        fence_before_sync();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tmem_idle[set]);   // the MMAs of sample j+2 may overwrite the set
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (lane < 3)
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-#pragma unroll
-              for (int c = 0; c < 8; ++c)
-                sHalo[(((qw * 4 + cg) * 3 + lane) * 3 + b) * 8 + c] = __uint_as_float(r[t][b][c]);
-          work_sync();
-          const int p = qw * 32 + lane, q = (t ? 124 : 0) + p;
-          const int y = q / kG, x = q - y * kG;
-          const bool valid = (t == 0 ? p <= 124 : (p >= 1 && q <= 247)) && x < 14;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float s = __uint_as_float(r[t][3][c]);
-#pragma unroll
-            for (int b = 2; b >= 0; --b) {
-              const int off = 3 - b;
-              float v = __shfl_down_sync(0xffffffffu, __uint_as_float(r[t][b][c]), off);
-              if (lane + off >= 32)
-                v = qw < 3 ? sHalo[((((qw + 1) * 4 + cg) * 3 + (lane + off - 32)) * 3 + b) * 8 + c] : 0.0f;
-              s += v;
-            }
-            if (valid) sDp1[(y * 14 + x) * kDp1S + cg * 8 + c] = s;
-          }
-          work_sync();   // halo reused by the next tile
-        }
+        // ---- sample j = i-1: dp1 -> G, conv1 gradients on the tensor cores ----
+        const int j = i - 1, set = j & 1, u = j - i0;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int e = tid + k * kBwdWork;
-          sX[(e >> 5) * kXS + (e & 31)] = rx[k];
+          sX[(e >> 5) * kXS + (e & 31)] = img_in(k) ? rx[k] : 0.0f;
         }
         if (i < i1) prefetch_img(i);
-        mbar_wait(&am1_full[set], ((j - i0) >> 1) & 1);
-        work_sync();
-        // pool1/relu backward + conv1 weight/bias gradients: lane = channel,
-        // warp w takes pooled positions w, w+16, ...; 26 accumulators per thread
+        PB_PHASE(tid == 0, i - i0, 3);
         const uint8_t* am1 = sAm1 + set * kP1;
-        float acc[25];
 #pragma unroll
-        for (int tt = 0; tt < 25; ++tt) acc[tt] = 0.0f;
-        float bacc = 0.0f;
-        const int co = lane;
-        int dm_n = am1[warp * kC1 + co];
-        float g_n = sDp1[warp * kDp1S + co];
-#pragma unroll 1
-        for (int pp = warp; pp < 196; pp += 16) {
-          const int py = pp / 14, px = pp - py * 14;
-          const int dm = dm_n;   // pool1 argmax, bit 2: relu'
-          const float g = (dm & 4) ? g_n : 0.0f;
-          if (pp + 16 < 196) {
-            dm_n = am1[(pp + 16) * kC1 + co];
-            g_n = sDp1[(pp + 16) * kDp1S + co];
+        for (int t = 0; t < 2; ++t) {
+          const int n = 2 * u + t, buf = n % 3;
+          mbar_wait(&tile_full[buf], uint32_t((n / 3) & 1));
+          PB_PHASE(tid == 0 && t == 0, i - i0, 4);
+          fence_after_sync();
+          uint32_t r[4][8];
+          const uint32_t ta = tmem + (uint32_t(qw * 32) << 16) + uint32_t(buf * 128 + cg * 8);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tmem_ld8_nw(ta + uint32_t(b * 32), r[b]);
+          tmem_wait_ld32(r[0], r[1], r[2], r[3]);
+          fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tile_free[buf]);   // the dgrad of tile n + 3 may overwrite it
+          if (t == 1) work_sync();   // tile 0's halo reads done
+          if (lane < 3) {
+            float4* h4 = reinterpret_cast<float4*>(sHalo + ((qw * 4 + cg) * 3 + lane) * 24);
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              h4[2 * b] = make_float4(__uint_as_float(r[b][0]), __uint_as_float(r[b][1]), __uint_as_float(r[b][2]),
+                                      __uint_as_float(r[b][3]));
+              h4[2 * b + 1] = make_float4(__uint_as_float(r[b][4]), __uint_as_float(r[b][5]),
+                                          __uint_as_float(r[b][6]), __uint_as_float(r[b][7]));
+            }
           }
-          bacc += g;
-          const int d = dm & 3;
-          const float* xw = sX + (2 * py + (d >> 1)) * kXS + 2 * px + (d & 1);
+          work_sync();   // halo (and, for tile 0, the image) complete
+          PB_PHASE(tid == 0 && t == 0, i - i0, 5);
+          const int p = qw * 32 + lane, q = (t ? 124 : 0) + p;
+          const int y = q / kG, x = q - y * kG;
+          const bool valid = (t == 0 ? p <= 124 : (p >= 1 && q <= 247)) && x < 14;
+          float out[8];
 #pragma unroll
-          for (int ky = 0; ky < 5; ++ky)
+          for (int c = 0; c < 8; ++c) out[c] = __uint_as_float(r[3][c]);
 #pragma unroll
-            for (int kx = 0; kx < 5; ++kx) acc[ky * 5 + kx] = fmaf(g, xw[ky * kXS + kx], acc[ky * 5 + kx]);
+          for (int b = 2; b >= 0; --b) {
+            const int off = 3 - b;
+            float hv[8];
+            if (lane + off >= 32 && qw < 3) {
+              const float4* h4 =
+                  reinterpret_cast<const float4*>(sHalo + (((qw + 1) * 4 + cg) * 3 + (lane + off - 32)) * 24 + b * 8);
+              const float4 h0 = h4[0], h1 = h4[1];
+              hv[0] = h0.x; hv[1] = h0.y; hv[2] = h0.z; hv[3] = h0.w;
+              hv[4] = h1.x; hv[5] = h1.y; hv[6] = h1.z; hv[7] = h1.w;
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) hv[c] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float v = __shfl_down_sync(0xffffffffu, __uint_as_float(r[b][c]), off);
+              out[c] += lane + off >= 32 ? hv[c] : v;
+            }
+          }
+          // G (and, for tile 0, the window operand) are free once the
+          // previous conv1 MMAs (tile n - 1) are done
+          if (n >= 1) mbar_wait(&g_free, uint32_t((n - 1) & 1));
+          PB_PHASE(tid == 0, i - i0, t == 0 ? 6 : 8);
+          if (t == 0) {
+            // the window operand of both tiles: unit (tile, K row); rows >= 98
+            // zero; cell pairs (c, c+1), c even, are one 8 B load
+            if (tid < 2 * kC1K) {
+              const int wt = tid / kC1K, kp = tid - wt * kC1K;
+              const bool in = kp < 98;
+              const int wy = 7 * wt + (in ? kp / 14 : 0), wx = in ? kp % 14 : 0;
+              const float* xw = sX + 2 * wy * kXS + 2 * wx;
+              uint8_t* wrow = sWin + wt * kBwdWin + kp * 16;
+#pragma unroll
+              for (int nc = 0; nc < 6; ++nc) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int cell = nc * 8 + 2 * e;
+                  float2 f = make_float2(0.0f, 0.0f);
+                  if (cell < 36) {
+                    if (in) f = *reinterpret_cast<const float2*>(xw + (cell / 6) * kXS + cell % 6);
+                  } else if (cell == 36) {
+                    f.x = in ? 1.0f : 0.0f;
+                  }
+                  w[e] = pack_bf16(f.x, f.y);
+                }
+                *reinterpret_cast<uint4*>(wrow + nc * kC1CS) = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            }
+            mbar_wait(&am1_full[set], ((j - i0) >> 1) & 1);
+          }
+          if (valid) {
+            // pool1 / relu backward: the gradient goes to candidate d's rows
+            const int kp = (y - 7 * t) * 14 + x;
+            const uint2 m2 = *reinterpret_cast<const uint2*>(am1 + (y * 14 + x) * kC1 + cg * 8);
+            uint32_t dm[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dm[c] = ((c < 4 ? m2.x : m2.y) >> (8 * (c & 3))) & 0xFFu;
+            // G row m = co*4 + d: channels (2e, 2e+1) of this thread fill one
+            // 8-element core row, their candidate d's slot nonzero
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float gv[8];
+#pragma unroll
+              for (int dd = 0; dd < 4; ++dd) {
+                gv[dd] = dm[2 * e] == uint32_t(4 + dd) ? out[2 * e] : 0.0f;
+                gv[4 + dd] = dm[2 * e + 1] == uint32_t(4 + dd) ? out[2 * e + 1] : 0.0f;
+              }
+              *reinterpret_cast<uint4*>(sGw + (cg * 4 + e) * kC1CS + kp * 16) =
+                  make_uint4(pack_bf16(gv[0], gv[1]), pack_bf16(gv[2], gv[3]), pack_bf16(gv[4], gv[5]),
+                             pack_bf16(gv[6], gv[7]));
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&g_full);
+          PB_PHASE(tid == 0, i - i0, t == 0 ? 7 : 9);
         }
-        work_sync();  // all reads of dp1 / the image done: sRed may overwrite them
-        // fixed-order reduction: warps 8-15 park their partials, warps 0-7 add
-        // them to their own, then the 8 pair sums are added in warp order
-        if (warp >= 8) {
-#pragma unroll
-          for (int tt = 0; tt < 25; ++tt) sRed[(warp - 8) * 832 + co * 25 + tt] = acc[tt];
-          sRed[(warp - 8) * 832 + 800 + co] = bacc;
-        }
-        work_sync();
-        if (warp < 8) {
-#pragma unroll
-          for (int tt = 0; tt < 25; ++tt) sRed[warp * 832 + co * 25 + tt] += acc[tt];
-          sRed[warp * 832 + 800 + co] += bacc;
-        }
-        work_sync();
-        float* pg = a.pg + sid * kPg;
-        for (int k = tid; k < 832; k += kBwdWork) {
-          float s8 = 0.0f;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) s8 += sRed[w * 832 + k];
-          pg[k] = s8;
-        }
-        work_sync();   // sRed / dp1 / sX free
+        PB_PHASE(tid == 0, i - i0, 11);
       }
+    }
+    // ---- the last two samples' H ----
+    if (warp >= 12) {
+      mbar_wait(&g_free, uint32_t((2 * (i1 - 1 - i0) + 1) & 1));
+      fence_after_sync();
+      if (i1 - 2 >= i0) h_readout(i1 - 2);
+      h_readout(i1 - 1);
     }
   }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
+#ifdef PB_PHASE_TRACE
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) g_phase_armed = 0;
+#endif
   if (warp == 0) tmem_free<512>(tmem);
 }
 

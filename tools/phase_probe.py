@@ -1,0 +1,53 @@
+"""Phase trace of k_bwd_conv in a C2 round: per-sample timestamps of one CTA
+(block (0, 0)) of the first launch after arming -- a dense sweep.  Needs the
+trace build (run on the GPU box):
+
+    PB_NVCC_DEFS=-DPB_PHASE_TRACE python -m paper_2303_01778_b200.build --force
+    python tools/phase_probe.py
+
+Worker thread 0: 0 start, 1 dz_free, 2 planes built (bias-partial sync;
+warps 12-15 read H of sample i-2 first), 3 epilogue start, 4 tile 0 in TMEM,
+5 tile-0 halo sync, 6 G free (tile 0), 7 G tile 0 written, 8 G free (tile 1),
+9 G tile 1 written, 11 end.  MMA thread: 12 dz_full, 13 dgrad issued, 14
+conv1 MMAs of sample i-1 issued, 15 dgrad complete.  Times in us from the
+iteration's start (column 0; iteration 0 from its column 12).
+"""
+import ctypes
+import sys
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import bench  # noqa: E402
+import paper_2303_01778_b200 as pb  # noqa: E402
+from paper_2303_01778_b200 import _lib  # noqa: E402
+import torch  # noqa: E402
+
+dev = torch.device("cuda", 0)
+data, sizes = bench.build_device_data(dev)
+profiles = bench.light_profiles(sizes)
+cfg = pb.SimConfig(total_clients=bench.M_TOTAL, concurrent_clients=bench.M_ROUND, num_devices=1,
+                   total_rounds=3, warmup_rounds=1, seed=0, scheme="PARROT")
+eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=bench.LR, batch_size=bench.BS), profiles,
+                          pb.make_device_models(1), model="cnn", client_data=data)
+eng.run_round(0)
+torch.cuda.synchronize()
+dll = _lib.lib._dll
+if not hasattr(dll, "pb_phase_arm"):
+    sys.exit("not a PB_PHASE_TRACE build")
+assert dll.pb_phase_arm() == 0
+eng.run_round(1)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (64 * 16))()
+assert dll.pb_phase_read(buf) == 0
+ph = np.frombuffer(buf, dtype=np.uint64).reshape(64, 16).astype(np.int64)
+names = ["start", "dz_free", "built", "epi", "tile0", "halo0", "g_free0", "G0", "g_free1", "G1",
+         "-", "end", "m:dz_full", "m:dgrad", "m:conv1", "m:done"]
+print("iter " + " ".join(f"{n:>9s}" for n in names))
+for it in range(64):
+    row = ph[it]
+    if not row.any():
+        break
+    t0 = row[0] if row[0] else row[12]
+    print(f"{it:4d} " + " ".join(f"{(v - t0) / 1e3:9.2f}" if v else f"{'-':>9s}" for v in row))
+starts = ph[:, 0][ph[:, 0] > 0]
+if len(starts) > 2:
+    print("iteration period us (median):", float(np.median(np.diff(starts))) / 1e3)
