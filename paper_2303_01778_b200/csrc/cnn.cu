@@ -1188,8 +1188,8 @@ constexpr int kBwdWin = 6 * kC1CS;                       // window operand of on
 constexpr int kXS = 34;
 constexpr int kBwdX = 32 * kXS * 4;
 constexpr int kBwdB2 = 13 * 64 * 4;                      // conv2 bias partials of the 13 build warps
-constexpr int kBwdHalo = 4 * 4 * 3 * 3 * 8 * 4;          // [quarter][ci group][lane 0-2][block 0-2][8]
-constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdGw + 2 * kBwdWin + kBwdX + 2 * kP1 + kBwdB2 + kBwdHalo;   // 220,544 B
+constexpr int kBwdHalo = 4 * 4 * 4 * 4 * 8 * 4;          // [quarter][ci group][lane 0-3][block 0-3][8]
+constexpr size_t kBwdSmem = kW2Bytes + kDzBytes + kBwdGw + 2 * kBwdWin + kBwdX + 2 * kP1 + kBwdB2 + kBwdHalo;   // 224,128 B
 static_assert(kBwdSmem + 256 <= 232448, "k_bwd_conv shared memory");
 
 
@@ -1199,8 +1199,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t dz_full, dz_free, tile_full[3], tile_free[3], am1_full[2], w2_full, g_full, g_free,
-      h_free[2];
+  __shared__ __align__(8) uint64_t dz_full, dz_free, tile_full[3], tile_free[3], am1_full[2], w2_full, g_full, g_free;
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
   uint8_t* sDz = sW2 + kW2Bytes;
@@ -1223,10 +1222,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       mbar_init(&tile_full[b], 1);
       mbar_init(&tile_free[b], 16);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&am1_full[b], 1);
-      mbar_init(&h_free[b], 4);   // the four readout warps
-    }
+    for (int b = 0; b < 2; ++b) mbar_init(&am1_full[b], 1);
     mbar_init(&w2_full, 1);
     mbar_init(&g_full, 16);
     mbar_init(&g_free, 1);
@@ -1237,19 +1233,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  // H of sample j: columns [384 + 48 hb, +48), hb = (j - i0) & 1
-  auto tmem_h = [&](int j) { return tmem + uint32_t(3 * 128 + ((j - i0) & 1) * 48); };
+  // TMEM: a ring of three 160-column dgrad tiles (tile n = 2(i - i0) + t in
+  // buffer n % 3).  H of sample j lives in the first 48 columns of its tile
+  // 1's buffer: free once that tile is read (before G tile 0 is handed to the
+  // tensor pipe) and reused next by the dgrad of sample j+2, which starts
+  // only after H(j) is read (before dz_full of sample j+2)
+  auto tmem_h = [&](int j) { return tmem + uint32_t(((2 * (j - i0) + 1) % 3) * 160); };
 
   if (warp == 16) {
     // ---------------- MMA / bulk-copy issue (one thread) ----------------
     if (lane == 0) {
       const uint32_t sdz = smem_u32(sDz), sw = smem_u32(sW2), sg = smem_u32(sGw), swin = smem_u32(sWin);
-      const uint32_t id128 = idesc_bf16(128, 128, false, true), id32 = idesc_bf16(128, 32, false, true);
-      const uint32_t id48 = idesc_bf16(128, 48, true, true);
-      // conv1 gradient MMAs of sample j into its H buffer (read out by then)
+      const uint32_t id160 = idesc_bf16(128, 160, false, true), id48 = idesc_bf16(128, 48, true, true);
+      // conv1 gradient MMAs of sample j into H(j)
       auto conv1_mmas = [&](int j) {
-        const int u = j - i0;
-        if (u >= 2) mbar_wait(&h_free[u & 1], uint32_t((u / 2 - 1) & 1));
 #pragma unroll 1
         for (int t = 0; t < 2; ++t) {
           mbar_wait(&g_full, uint32_t(t));
@@ -1277,18 +1274,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
           if (n >= 3) mbar_wait(&tile_free[buf], uint32_t((n / 3 - 1) & 1));   // tile n - 3 read out
           fence_after_sync();
           const int base = t ? 124 : 0;
-          const uint32_t dt = tmem + uint32_t(buf * 128);
+          const uint32_t dt = tmem + uint32_t(buf * 160);
 #pragma unroll 1
           for (int ky = 0; ky < 5; ++ky) {
-            const uint64_t ab = desc(sdz + uint32_t(base + 73 - kG * ky) * 16, kPlane, 128);
-            const uint64_t a4 = desc(sdz + uint32_t(base + 72 - kG * ky) * 16, kPlane, 128);
+            // block kx (32 columns) of row p: A[p + base + 72 - 18 ky] . W[ky][kx]
+            const uint64_t ab = desc(sdz + uint32_t(base + 72 - kG * ky) * 16, kPlane, 128);
             const uint64_t bb = desc(sw + uint32_t(ky * 5 * 4 * 1024), 128, 1024);
-            const uint64_t b4 = desc(sw + uint32_t((ky * 5 + 4) * 4 * 1024), 128, 1024);
 #pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-              mma_bf16(dt, ab + uint64_t(kq * (2 * kPlane / 16)), bb + uint64_t(kq * 16), id128, ky > 0 || kq > 0);
-              mma_bf16(dt + 96, a4 + uint64_t(kq * (2 * kPlane / 16)), b4 + uint64_t(kq * 16), id32, true);
-            }
+            for (int kq = 0; kq < 4; ++kq)
+              mma_bf16(dt, ab + uint64_t(kq * (2 * kPlane / 16)), bb + uint64_t(kq * 16), id160, ky > 0 || kq > 0);
           }
           commit(&tile_full[buf]);
         }
@@ -1365,9 +1359,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       tmem_ld16(th, h0);
       tmem_ld16(th + 16, h1);
       tmem_ld16(th + 32, h2);
-      fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&h_free[(j - i0) & 1]);   // the conv1 MMAs of sample j+2 may overwrite it
       float* pg = a.pg + sidx(blockIdx.y, j, a.BS) * kPg;
       auto cell = [&](int c) { return c < 16 ? h0[c] : (c < 32 ? h1[c - 16] : h2[c - 32]); };
       // this lane's candidate d contribution to the 25 taps + the bias
@@ -1490,46 +1481,46 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
         if (i < i1) prefetch_img(i);
         PB_PHASE(tid == 0, i - i0, 3);
         const uint8_t* am1 = sAm1 + set * kP1;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
+        // dgrad tile t -> r: 5 kx blocks x this warp's 8 channels
+        uint32_t r[5][8];
+        auto load_tile = [&](int t) {
           const int n = 2 * u + t, buf = n % 3;
           mbar_wait(&tile_full[buf], uint32_t((n / 3) & 1));
-          PB_PHASE(tid == 0 && t == 0, i - i0, 4);
           fence_after_sync();
-          uint32_t r[4][8];
-          const uint32_t ta = tmem + (uint32_t(qw * 32) << 16) + uint32_t(buf * 128 + cg * 8);
+          const uint32_t ta = tmem + (uint32_t(qw * 32) << 16) + uint32_t(buf * 160 + cg * 8);
 #pragma unroll
           for (int b = 0; b < 4; ++b) tmem_ld8_nw(ta + uint32_t(b * 32), r[b]);
           tmem_wait_ld32(r[0], r[1], r[2], r[3]);
+          tmem_ld8_nw(ta + 128u, r[4]);
+          tmem_wait_ld8(r[4]);
           fence_before_sync();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tile_free[buf]);   // the dgrad of tile n + 3 may overwrite it
-          if (t == 1) work_sync();   // tile 0's halo reads done
-          if (lane < 3) {
-            float4* h4 = reinterpret_cast<float4*>(sHalo + ((qw * 4 + cg) * 3 + lane) * 24);
+        };
+        // blocks 0-3 of lanes 0-3 -> the halo read by the previous lane quarter
+        auto halo_put = [&]() {
+          if (lane < 4) {
+            float4* h4 = reinterpret_cast<float4*>(sHalo + ((qw * 4 + cg) * 4 + lane) * 32);
 #pragma unroll
-            for (int b = 0; b < 3; ++b) {
+            for (int b = 0; b < 4; ++b) {
               h4[2 * b] = make_float4(__uint_as_float(r[b][0]), __uint_as_float(r[b][1]), __uint_as_float(r[b][2]),
                                       __uint_as_float(r[b][3]));
               h4[2 * b + 1] = make_float4(__uint_as_float(r[b][4]), __uint_as_float(r[b][5]),
                                           __uint_as_float(r[b][6]), __uint_as_float(r[b][7]));
             }
           }
-          work_sync();   // halo (and, for tile 0, the image) complete
-          PB_PHASE(tid == 0 && t == 0, i - i0, 5);
-          const int p = qw * 32 + lane, q = (t ? 124 : 0) + p;
-          const int y = q / kG, x = q - y * kG;
-          const bool valid = (t == 0 ? p <= 124 : (p >= 1 && q <= 247)) && x < 14;
-          float out[8];
+        };
+        // out[q] = sum_kx D_kx[q + 4 - kx] (row q = lane of this quarter)
+        auto shift_sum = [&](float (&o)[8]) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) out[c] = __uint_as_float(r[3][c]);
+          for (int c = 0; c < 8; ++c) o[c] = __uint_as_float(r[4][c]);
 #pragma unroll
-          for (int b = 2; b >= 0; --b) {
-            const int off = 3 - b;
+          for (int b = 3; b >= 0; --b) {
+            const int off = 4 - b;
             float hv[8];
             if (lane + off >= 32 && qw < 3) {
               const float4* h4 =
-                  reinterpret_cast<const float4*>(sHalo + (((qw + 1) * 4 + cg) * 3 + (lane + off - 32)) * 24 + b * 8);
+                  reinterpret_cast<const float4*>(sHalo + (((qw + 1) * 4 + cg) * 4 + (lane + off - 32)) * 32 + b * 8);
               const float4 h0 = h4[0], h1 = h4[1];
               hv[0] = h0.x; hv[1] = h0.y; hv[2] = h0.z; hv[3] = h0.w;
               hv[4] = h1.x; hv[5] = h1.y; hv[6] = h1.z; hv[7] = h1.w;
@@ -1540,14 +1531,57 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const float v = __shfl_down_sync(0xffffffffu, __uint_as_float(r[b][c]), off);
-              out[c] += lane + off >= 32 ? hv[c] : v;
+              o[c] += lane + off >= 32 ? hv[c] : v;
             }
           }
-          // G (and, for tile 0, the window operand) are free once the
-          // previous conv1 MMAs (tile n - 1) are done
-          if (n >= 1) mbar_wait(&g_free, uint32_t((n - 1) & 1));
-          PB_PHASE(tid == 0, i - i0, t == 0 ? 6 : 8);
-          if (t == 0) {
+        };
+        // G rows of tile t (tile rows p <= 123 with x < 14)
+        auto g_write = [&](int t, const float (&out)[8]) {
+          const int p = qw * 32 + lane, q = t * 124 + p;
+          const int y = q / kG, x = q - y * kG;
+          const bool valid = p <= 123 && x < 14;
+          if (valid) {
+            // pool1 / relu backward: the gradient goes to candidate d's rows
+            const int kp = (y - 7 * t) * 14 + x;
+            const uint2 m2 = *reinterpret_cast<const uint2*>(am1 + (y * 14 + x) * kC1 + cg * 8);
+            uint32_t dm[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dm[c] = ((c < 4 ? m2.x : m2.y) >> (8 * (c & 3))) & 0xFFu;
+            // G row m = co*4 + d: channels (2e, 2e+1) of this thread fill one
+            // 8-element core row, their candidate d's slot nonzero
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float gv[8];
+#pragma unroll
+              for (int dd = 0; dd < 4; ++dd) {
+                gv[dd] = dm[2 * e] == uint32_t(4 + dd) ? out[2 * e] : 0.0f;
+                gv[4 + dd] = dm[2 * e + 1] == uint32_t(4 + dd) ? out[2 * e + 1] : 0.0f;
+              }
+              *reinterpret_cast<uint4*>(sGw + (cg * 4 + e) * kC1CS + kp * 16) =
+                  make_uint4(pack_bf16(gv[0], gv[1]), pack_bf16(gv[2], gv[3]), pack_bf16(gv[4], gv[5]),
+                             pack_bf16(gv[6], gv[7]));
+            }
+          }
+        };
+        auto g_hand = [&]() {   // this warp's G rows (and window rows) -> the tensor pipe
+          fence_async_smem();
+          fence_before_sync();   // the TMEM reads precede the conv1 MMAs (H(j) reuses tile 1's columns)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&g_full);
+        };
+        load_tile(0);
+        PB_PHASE(tid == 0, i - i0, 4);
+        halo_put();
+        work_sync();   // tile-0 halo and the image complete
+        PB_PHASE(tid == 0, i - i0, 5);
+        float out[8];
+        shift_sum(out);
+        load_tile(1);   // before G tile 0 is handed over: H(j) goes into this buffer
+        work_sync();    // tile-0 halo reads done
+        halo_put();
+        if (u >= 1) mbar_wait(&g_free, uint32_t((2 * u - 1) & 1));   // G and the window operand free
+        PB_PHASE(tid == 0, i - i0, 6);
+        {
             // the window operand of both tiles: unit (tile, K row); rows >= 98
             // zero; cell pairs (c, c+1), c even, are one 8 B load
             if (tid < 2 * kC1K) {
@@ -1574,34 +1608,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
               }
             }
             mbar_wait(&am1_full[set], ((j - i0) >> 1) & 1);
-          }
-          if (valid) {
-            // pool1 / relu backward: the gradient goes to candidate d's rows
-            const int kp = (y - 7 * t) * 14 + x;
-            const uint2 m2 = *reinterpret_cast<const uint2*>(am1 + (y * 14 + x) * kC1 + cg * 8);
-            uint32_t dm[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) dm[c] = ((c < 4 ? m2.x : m2.y) >> (8 * (c & 3))) & 0xFFu;
-            // G row m = co*4 + d: channels (2e, 2e+1) of this thread fill one
-            // 8-element core row, their candidate d's slot nonzero
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float gv[8];
-#pragma unroll
-              for (int dd = 0; dd < 4; ++dd) {
-                gv[dd] = dm[2 * e] == uint32_t(4 + dd) ? out[2 * e] : 0.0f;
-                gv[4 + dd] = dm[2 * e + 1] == uint32_t(4 + dd) ? out[2 * e + 1] : 0.0f;
-              }
-              *reinterpret_cast<uint4*>(sGw + (cg * 4 + e) * kC1CS + kp * 16) =
-                  make_uint4(pack_bf16(gv[0], gv[1]), pack_bf16(gv[2], gv[3]), pack_bf16(gv[4], gv[5]),
-                             pack_bf16(gv[6], gv[7]));
-            }
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&g_full);
-          PB_PHASE(tid == 0, i - i0, t == 0 ? 7 : 9);
         }
+        g_write(0, out);
+        g_hand();
+        PB_PHASE(tid == 0, i - i0, 7);
+        work_sync();   // tile-1 halo complete
+        shift_sum(out);
+        mbar_wait(&g_free, uint32_t((2 * u) & 1));   // tile 0's conv1 MMAs have read G
+        PB_PHASE(tid == 0, i - i0, 8);
+        g_write(1, out);
+        g_hand();
+        PB_PHASE(tid == 0, i - i0, 9);
         PB_PHASE(tid == 0, i - i0, 11);
       }
     }
