@@ -141,8 +141,8 @@ constexpr int kC1BBytes = 6 * 2048;          // conv1 B: 6 K cores x 128 cols x 
 // pooled positions per row; 46 (= 14 mod 32 in float2 units) puts the
 // positions of consecutive pooled rows in distinct banks
 constexpr int kSXS = 46;
-constexpr size_t kFwdSmem = kW2Bytes + kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 32 * kSXS * 4 + kC1ABytes +
-                            kC1BBytes + (32 + 64) * 4;   // 205,056 B
+constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 32 * kSXS * 4 + kC1ABytes +
+                            kC1BBytes + (32 + 64) * 4;   // 226,624 B
 
 __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   pb::pdl_wait();
@@ -153,8 +153,8 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   __shared__ __align__(8) uint64_t c1_done, c2_done[2], a_ready, p1_ready, w2_full;
   __shared__ uint32_t tmem_base;
   uint8_t* sW2 = smem;
-  uint8_t* sPl = sW2 + kW2Bytes;                                   // p1 planes (one sample)
-  float* sZ = reinterpret_cast<float*>(sPl + kP1Bytes);           // conv2 half tile
+  uint8_t* sPl = sW2 + kW2Bytes;                                   // p1 planes, two samples (k & 1)
+  float* sZ = reinterpret_cast<float*>(sPl + 2 * kP1Bytes);       // conv2 half tile
   uint8_t* sRaw = reinterpret_cast<uint8_t*>(sZ + 256 * kZStride); // 2 raw images
   float* sX = reinterpret_cast<float*>(sRaw + 2 * kRawImg);       // [32][kSXS] padded image
   uint8_t* sA1 = reinterpret_cast<uint8_t*>(sX + 32 * kSXS);      // conv1 A [u][pp][8] bf16
@@ -181,7 +181,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
   }
   for (int e = tid; e < 32; e += kFwdThreads) sB1[e] = W[oC1B + e];
   for (int e = tid; e < 64; e += kFwdThreads) sB2[e] = W[oC2B + e];
-  for (int e = tid; e < kP1Bytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
+  for (int e = tid; e < 2 * kP1Bytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sPl)[e] = make_uint4(0, 0, 0, 0);
   for (int e = tid; e < kC1ABytes / 16; e += kFwdThreads) reinterpret_cast<uint4*>(sA1)[e] = make_uint4(0, 0, 0, 0);
   // the A build reads 8 columns per window (the last 2 weighted 0), i.e. up
   // to column 33 of a row: the row padding [32, kSXS) stays zero (0 * NaN
@@ -208,39 +208,52 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     if (lane == 0) {
       const uint32_t idesc1 = idesc_bf16(128, 128), idesc2 = idesc_bf16(128, 64);
       const uint32_t sa1 = smem_u32(sA1), sb1 = smem_u32(sB1w);
-      const uint64_t a0 = desc(smem_u32(sPl), kPlane, 128);
       const uint64_t b0 = desc(smem_u32(sW2), 1024, 128);
       // the client's conv2 weights (bf16, UMMA layout): one bulk copy
       pb::tma::expect_tx(&w2_full, uint32_t(kW2Bytes));
       pb::tma::bulk_load(sW2, a.w2b + int64_t(sl.r) * kW2Bytes, uint32_t(kW2Bytes), &w2_full);
-      for (int i = i0; i < i1; ++i) {
-        mbar_wait(&a_ready, (i - i0) & 1);
-        fence_after_sync();
+      auto conv1_issue = [&]() {   // conv1 of the sample in sA1 -> TMEM cols 256 + 128t
 #pragma unroll
-        for (int t = 0; t < 2; ++t)   // conv1(i) -> TMEM cols 256 + 128t
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int ks = 0; ks < 3; ++ks)
             mma_bf16(tmem + 256 + t * 128, desc(sa1 + uint32_t(t * 2048 + ks * 8192), 4096, 128),
                      desc(sb1 + uint32_t(ks * 4096), 2048, 128), idesc1, ks > 0);
-        // the conv1 epilogue of i rewrites the p1 planes: the bulk store of
-        // p1(i-1) must have read them first
-        pb::tma::bulk_wait_reads();
-        commit(&c1_done);
-        mbar_wait(&p1_ready, (i - i0) & 1);
-        if (i == i0) mbar_wait(&w2_full, 0);
+      };
+      mbar_wait(&a_ready, 0);
+      fence_after_sync();
+      conv1_issue();
+      commit(&c1_done);
+      // per sample k, once p1(k) is written: conv1(k+1), then conv2(k).  The
+      // tensor pipe runs in issue order, so conv1(k+1) completes before
+      // conv2(k) starts and the conv1 epilogue of k+1 overlaps conv2(k).
+      for (int k = i0; k < i1; ++k) {
+        mbar_wait(&p1_ready, (k - i0) & 1);   // also: the conv1 TMEM and conv2 half k&1 are read out
         fence_after_sync();
-        const uint32_t th = tmem + uint32_t((i & 1) * 128);
+        if (k + 1 < i1) {
+          mbar_wait(&a_ready, (k + 1 - i0) & 1);
+          fence_after_sync();
+          conv1_issue();
+          // the conv1 epilogue of k+1 rewrites p1 buffer (k+1)&1: the bulk
+          // store of p1(k-1) must have read it (its conv2 MMAs precede this commit)
+          pb::tma::bulk_wait_reads();
+          commit(&c1_done);
+        }
+        if (k == i0) mbar_wait(&w2_full, 0);
+        const uint32_t th = tmem + uint32_t((k & 1) * 128);
+        const uint64_t a0 = desc(smem_u32(sPl) + uint32_t((k & 1) * kP1Bytes), kPlane, 128);
 #pragma unroll
-        for (int t = 0; t < 2; ++t)   // conv2(i) -> TMEM half i&1
+        for (int t = 0; t < 2; ++t)   // conv2(k) -> TMEM half k&1
 #pragma unroll
           for (int tap = 0; tap < 25; ++tap)
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
               mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
                        b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc2, tap > 0 || hh > 0);
-        commit(&c2_done[i & 1]);
-        // p1 planes of i -> global for the backward kernels (read concurrently with the conv2 MMAs)
-        pb::tma::bulk_store(a.p1g + sidx(blockIdx.y, i, a.BS) * kP1Bytes, sPl, uint32_t(kP1Bytes));
+        commit(&c2_done[k & 1]);
+        // p1 planes of k -> global for the backward kernels (read concurrently with the conv2 MMAs)
+        pb::tma::bulk_store(a.p1g + sidx(blockIdx.y, k, a.BS) * kP1Bytes, sPl + (k & 1) * kP1Bytes,
+                            uint32_t(kP1Bytes));
       }
       pb::tma::bulk_wait_all();
     }
@@ -331,10 +344,18 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     const int q = warp & 3, cg = warp >> 2;   // conv1 epilogue: lane quarter, 8-channel group
     for (int i = i0; i < i1; ++i) {
       const int64_t sid = sidx(blockIdx.y, i, a.BS);
-      // ---- conv1 epilogue of sample i (conv1(i) done => conv2(i-1) done
-      // with the p1 planes) ----
+      // ---- conv1(i) done (and with it conv2(i-2), which read p1 buffer i&1) ----
       mbar_wait(&c1_done, (i - i0) & 1);
       fence_after_sync();
+      // ---- next sample's A first: conv1(i+1) is issued together with conv2(i) ----
+      if (i + 1 < i1) {
+        cp_async_wait<0>();
+        work_sync();
+        build_a(i + 1);
+        if (i + 2 < i1) fetch_img(i + 2);
+      }
+      // ---- conv1 epilogue of sample i -> p1 buffer i&1 ----
+      uint8_t* pl = sPl + (i & 1) * kP1Bytes;
       uint8_t* am1 = a.am1 + sid * kP1;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
@@ -372,7 +393,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
               am[k >> 2] = code;
           }
           const int py = pp / 14, px = pp - py * 14;
-          *reinterpret_cast<uint4*>(sPl + cg * kPlane + ((py + 2) * kG + px + 2) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(pl + cg * kPlane + ((py + 2) * kG + px + 2) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
           *reinterpret_cast<uint2*>(am1 + pp * kC1 + cg * 8) = make_uint2(am[0], am[1]);
         }
       }
@@ -380,13 +401,6 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p1_ready);
-      // ---- next sample's A (conv1(i) done with it) ----
-      if (i + 1 < i1) {
-        cp_async_wait<0>();
-        work_sync();
-        build_a(i + 1);
-        if (i + 2 < i1) fetch_img(i + 2);
-      }
       // (the MMA thread bulk-stores the p1 planes for the backward kernels)
       if (i > i0) epilogue2(i - 1);
     }
