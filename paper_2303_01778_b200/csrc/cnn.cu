@@ -33,28 +33,31 @@
 // Phase trace of k_bwd_conv (tools/phase_probe.py): built only with
 // -DPB_PHASE_TRACE (PB_NVCC_DEFS at build time); the product build has none.
 #ifdef PB_PHASE_TRACE
-__device__ unsigned long long g_phase[64][16];
-__device__ int g_phase_armed;
-#define PB_PHASE(cond, slot, k)                                                                 \
+// [kernel: 0 k_bwd_conv, 1 k_fwd][sample][phase]
+__device__ unsigned long long g_phase[2][64][16];
+__device__ int g_phase_armed[2];
+#define PB_PHASE_K(kern, cond, slot, k)                                                         \
   do {                                                                                          \
-    if (g_phase_armed && blockIdx.x == 0 && blockIdx.y == 0 && (cond) && (slot) < 64) {         \
+    if (g_phase_armed[kern] && blockIdx.x == 0 && blockIdx.y == 0 && (cond) && (slot) < 64) {   \
       unsigned long long t_;                                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
-      g_phase[slot][k] = t_;                                                                    \
+      g_phase[kern][slot][k] = t_;                                                              \
     }                                                                                           \
   } while (0)
 extern "C" int pb_phase_arm() {
-  const int one = 1;
-  unsigned long long z[64 * 16] = {};
+  const int one[2] = {1, 1};
+  static unsigned long long z[2 * 64 * 16] = {};
   cudaMemcpyToSymbol(g_phase, z, sizeof(z));
-  return int(cudaMemcpyToSymbol(g_phase_armed, &one, sizeof(int)));
+  return int(cudaMemcpyToSymbol(g_phase_armed, one, sizeof(one)));
 }
 extern "C" int pb_phase_read(unsigned long long* out) {
   return int(cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase)));
 }
 #else
-#define PB_PHASE(cond, slot, k) do { } while (0)
+#define PB_PHASE_K(kern, cond, slot, k) do { } while (0)
 #endif
+#define PB_PHASE(cond, slot, k) PB_PHASE_K(0, cond, slot, k)
+#define PB_PHASE_F(cond, slot, k) PB_PHASE_K(1, cond, slot, k)
 
 namespace {
 
@@ -229,6 +232,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       // conv2(k) starts and the conv1 epilogue of k+1 overlaps conv2(k).
       for (int k = i0; k < i1; ++k) {
         mbar_wait(&p1_ready, (k - i0) & 1);   // also: the conv1 TMEM and conv2 half k&1 are read out
+        PB_PHASE_F(true, k - i0, 12);
         fence_after_sync();
         if (k + 1 < i1) {
           mbar_wait(&a_ready, (k + 1 - i0) & 1);
@@ -251,6 +255,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
               mma_bf16(th + t * 64, a0 + uint64_t(t * 128 + (tap / 5) * kG + tap % 5 + hh * (2 * kPlane / 16)),
                        b0 + uint64_t((tap * 4 + 2 * hh) * 64), idesc2, tap > 0 || hh > 0);
         commit(&c2_done[k & 1]);
+        PB_PHASE_F(true, k - i0, 13);
         // p1 planes of k -> global for the backward kernels (read concurrently with the conv2 MMAs)
         pb::tma::bulk_store(a.p1g + sidx(blockIdx.y, k, a.BS) * kP1Bytes, sPl + (k & 1) * kP1Bytes,
                             uint32_t(kP1Bytes));
@@ -288,6 +293,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     // finish conv2 of sample j: TMEM half (j&1) -> relu(z + b2) -> maxpool -> p2, am2
     auto epilogue2 = [&](int j) {
       mbar_wait(&c2_done[j & 1], ((j - i0) >> 1) & 1);
+      PB_PHASE_F(tid == 0, j + 1 - i0, 4);
       fence_after_sync();
       const uint32_t th = tmem + uint32_t((j & 1) * 128);
       const int64_t sid = sidx(blockIdx.y, j, a.BS);
@@ -311,6 +317,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
         }
         fence_before_sync();
         work_sync();
+        PB_PHASE_F(tid == 0, j + 1 - i0, 5 + 3 * hc);
         for (int o = tid; o < 49 * 32; o += kFwdWork) {
           const int pp = o >> 5, cl = o & 31, co = hc * 32 + cl;
           const int py = pp / 7, px = pp - py * 7;
@@ -333,6 +340,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
           am2[pp * 64 + co] = uint8_t(arg);
         }
         work_sync();  // sZ is free again
+        PB_PHASE_F(tid == 0, j + 1 - i0, 6 + 3 * hc);
       }
     };
 
@@ -345,7 +353,9 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
     for (int i = i0; i < i1; ++i) {
       const int64_t sid = sidx(blockIdx.y, i, a.BS);
       // ---- conv1(i) done (and with it conv2(i-2), which read p1 buffer i&1) ----
+      PB_PHASE_F(tid == 0, i - i0, 0);
       mbar_wait(&c1_done, (i - i0) & 1);
+      PB_PHASE_F(tid == 0, i - i0, 1);
       fence_after_sync();
       // ---- next sample's A first: conv1(i+1) is issued together with conv2(i) ----
       if (i + 1 < i1) {
@@ -355,6 +365,7 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
         if (i + 2 < i1) fetch_img(i + 2);
       }
       // ---- conv1 epilogue of sample i -> p1 buffer i&1 ----
+      PB_PHASE_F(tid == 0, i - i0, 2);
       uint8_t* pl = sPl + (i & 1) * kP1Bytes;
       uint8_t* am1 = a.am1 + sid * kP1;
 #pragma unroll
@@ -401,14 +412,19 @@ __global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p1_ready);
+      PB_PHASE_F(tid == 0, i - i0, 3);
       // (the MMA thread bulk-stores the p1 planes for the backward kernels)
       if (i > i0) epilogue2(i - 1);
+      PB_PHASE_F(tid == 0, i - i0, 11);
     }
     epilogue2(i1 - 1);
   }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
+#ifdef PB_PHASE_TRACE
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) g_phase_armed[1] = 0;
+#endif
   if (warp == 0) tmem_free<512>(tmem);
 }
 
@@ -1648,7 +1664,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
   __syncthreads();
   fence_after_sync();
 #ifdef PB_PHASE_TRACE
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) g_phase_armed = 0;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) g_phase_armed[0] = 0;
 #endif
   if (warp == 0) tmem_free<512>(tmem);
 }

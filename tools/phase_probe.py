@@ -36,18 +36,28 @@ if not hasattr(dll, "pb_phase_arm"):
 assert dll.pb_phase_arm() == 0
 eng.run_round(1)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (64 * 16))()
+buf = (ctypes.c_ulonglong * (2 * 64 * 16))()
 assert dll.pb_phase_read(buf) == 0
-ph = np.frombuffer(buf, dtype=np.uint64).reshape(64, 16).astype(np.int64)
-names = ["start", "dz_free", "built", "epi", "tile0", "halo0", "g_free0", "G0", "g_free1", "G1",
-         "-", "end", "m:dz_full", "m:dgrad", "m:conv1", "m:done"]
-print("iter " + " ".join(f"{n:>9s}" for n in names))
-for it in range(64):
-    row = ph[it]
-    if not row.any():
-        break
-    t0 = row[0] if row[0] else row[12]
-    print(f"{it:4d} " + " ".join(f"{(v - t0) / 1e3:9.2f}" if v else f"{'-':>9s}" for v in row))
-starts = ph[:, 0][ph[:, 0] > 0]
-if len(starts) > 2:
-    print("iteration period us (median):", float(np.median(np.diff(starts))) / 1e3)
+all_ph = np.frombuffer(buf, dtype=np.uint64).reshape(2, 64, 16).astype(np.int64)
+tables = {
+    "k_bwd_conv": ["start", "dz_free", "built", "epi", "tile0", "halo0", "g_free0", "G0", "g_free1", "G1",
+                   "-", "end", "m:dz_full", "m:dgrad", "m:conv1", "m:done"],
+    # k_fwd, worker thread 0 of sample i: 0 start, 1 conv1(i) done, 2 A(i+1)
+    # built, 3 p1(i) written; conv2 epilogue of i-1: 4 conv2 done, 5/8 half
+    # tile in smem, 6/9 pooled; 11 end.  MMA thread: 12 p1 ready, 13 conv2 issued
+    "k_fwd": ["start", "c1_done", "A built", "p1 ready", "c2_done", "sZ h0", "pool h0", "-", "sZ h1",
+              "pool h1", "-", "end", "m:p1", "m:conv2", "-", "-"],
+}
+for kern, (name, names) in enumerate(tables.items()):
+    ph = all_ph[kern]
+    print(name)
+    print("iter " + " ".join(f"{n:>9s}" for n in names))
+    for it in range(64):
+        row = ph[it]
+        if not row.any():
+            break
+        t0 = row[0] if row[0] else row[12]
+        print(f"{it:4d} " + " ".join(f"{(v - t0) / 1e3:9.2f}" if v else f"{'-':>9s}" for v in row))
+    starts = ph[:, 0][ph[:, 0] > 0]
+    if len(starts) > 2:
+        print("iteration period us (median):", float(np.median(np.diff(starts))) / 1e3)
