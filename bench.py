@@ -370,8 +370,8 @@ def run_b200(args) -> dict:
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "bf16 (tcgen05 operands of conv1, conv2 and the low-rank fc1: its X/dH history and "
-                 "W0 copy) / fp32 (master weights, TMEM accumulation, conv1 weight gradient, fc2, loss)",
+        "dtype": "bf16 (tcgen05 operands of conv1 incl. its weight gradient, conv2 and the low-rank fc1: "
+                 "its X/dH history and W0 copy) / fp32 (master weights, TMEM accumulation, fc2, loss)",
         "data": "synthetic FEMNIST-shaped: fedsim.data.generate's construction (unit class means x 3 "
                 "+ N(0,1)) drawn from torch's device RNG instead of the reference's NumPy stream (the "
                 "values do not change the work); per-client sample counts Dirichlet(1.0), min 10, "
