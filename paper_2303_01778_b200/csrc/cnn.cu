@@ -1681,15 +1681,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
 // co, MN-major) is the 8 dz2 planes.  A "group" is (ky, kx0), kx0 in {0, 4}:
 // kx0 = 0 covers taps kx 0-3, kx0 = 4 tap 4 (its other 96 lanes unused), so
 // 10 MMAs per K step cover the 25 taps (the previous M = 64 form issued 15).
-// Every MMA with N <= 64 costs the same ~52 cycles (tools/umma_bench2.py),
-// so the instruction count is what matters.
-// Staging, per (sample, K half) chunk of 128 positions: ONE TMA box brings
-// the 4 p1 planes (a view whose 128 B inner rows are 8 plane rows: 22 rows
-// per plane, any start row), one box the 8 dz2 planes, into a 4-stage
-// landing ring; warps 1-7 build the A operand (the base planes and their
-// three shifted copies) in one of two A buffers (L2 reads 27 KB per chunk
-// instead of 61), and thread 0 issues the MMAs (B straight from the landing
-// stage): full (TMA) -> ready (A built) -> afree / empty (MMAs done)
+// An MMA with fresh operands costs ~65 cycles for any N <= 128
+// (tools/umma_dgrad_bench.py) and the kernel is shared-memory-bound, so the
+// staging writes each operand byte once: per (sample, K half) chunk of 128
+// positions, FOUR TMA boxes of the 4 p1 planes (a view whose 128 B inner rows
+// are 8 plane rows: 22 rows per plane, any start row), box kxl starting kxl
+// rows later, land directly as the 16-plane A operand, and one box brings
+// the 8 dz2 planes (B), into a 3-stage ring; thread 0 issues the MMAs:
+// full (TMA) -> empty (MMAs done)
 // barriers.  The accumulators stay in TMEM over the client's samples.
 // ---------------------------------------------------------------------------
 constexpr int kWgKH = 128;                      // output positions per chunk (8 K steps)
@@ -1698,17 +1697,15 @@ constexpr int kWgPS = kWgRH * 16;               // A plane stride (2816 B)
 constexpr int kWgBS = kWgKH * 16;               // B plane stride (2048 B)
 constexpr int kWgABytes = 16 * kWgPS;           // the MMA's A: 4 shifts x 4 planes (45,056 B)
 constexpr int kWgBBytes = 8 * kWgBS;            // 8 dz2 planes
-constexpr int kWgLoad = 4 * kWgPS + kWgBBytes;  // TMA bytes per chunk (base planes + dz2): 27,648 B
-constexpr int kWgStages = 4;                    // TMA ring (the landing buffers)
-constexpr int kWgStage = kWgLoad;
-constexpr int kWgABufs = 2;                     // A operands built from the ring, double-buffered
-constexpr size_t kWgSmem = size_t(kWgStages) * kWgStage + size_t(kWgABufs) * kWgABytes + 128;   // 200,832 B
+constexpr int kWgStage = kWgABytes + kWgBBytes; // TMA bytes per chunk: 61,440 B
+constexpr int kWgStages = 3;                    // TMA ring
+constexpr size_t kWgSmem = size_t(kWgStages) * kWgStage + 128;   // 184,448 B
 constexpr int kWgTailActive = 60;               // below: one CTA per filter row (5-way split)
 constexpr int kWgStride = 15 * 32 + 4;          // fp32 row of the gradient tile (epilogue, float4 rows)
-constexpr int kWgCopyRows = kWgRH - 8;          // rows of a shifted copy the MMAs read (<= 168)
-static_assert(64 * kWgStride * 4 <= kWgStages * kWgStage + kWgABufs * kWgABytes, "k_wgrad epilogue tile");
+static_assert(64 * kWgStride * 4 <= kWgStages * kWgStage, "k_wgrad epilogue tile");
 static_assert(kWgABytes % 128 == 0 && kWgStage % 128 == 0 && kWgPS % 128 == 0, "TMA destinations 128 B aligned");
-static_assert(kWgCopyRows >= kWgKH + 40 && kWgCopyRows + 3 <= kWgRH, "shifted copies");
+// the MMAs read rows [off, off + 128) of a shifted plane, off <= 2*18 + 4
+static_assert(kWgKH + 2 * kG + 4 <= kWgRH, "shifted planes");
 
 struct ConvMaps {
   CUtensorMap p1;   // p1 planes as {8 rows x 8 ci (128 B), row groups, samples*4 planes}: box {64, 22, 4}
@@ -1730,9 +1727,8 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
   if (sl.cnt == 0) return;   // uniform over a cluster (same slot)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  __shared__ __align__(8) uint64_t full[kWgStages], empty[kWgStages], ready[kWgABufs], afree[kWgABufs];
+  __shared__ __align__(8) uint64_t full[kWgStages], empty[kWgStages];
   __shared__ uint32_t tmem_base;
-  uint8_t* sAbuf = smem + kWgStages * kWgStage;   // the MMA's A operands (double-buffered)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int split = blockIdx.x / sg, rank = blockIdx.x - split * sg;
   const int i_lo = rank * sl.cnt / sg, i_hi = (rank + 1) * sl.cnt / sg;
@@ -1772,10 +1768,6 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < kWgABufs; ++i) {
-      mbar_init(&ready[i], 7);   // one arrive per copy warp
-      mbar_init(&afree[i], 1);
-    }
     fence_init();
   }
   fence_before_sync();
@@ -1785,18 +1777,23 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
   const int n = 2 * cnt;   // chunks: (sample, K half)
   if (tid == 0 && n > 0) {
     const uint32_t idesc = idesc_bf16(128, 64, true, true);
+    // one chunk: the A operand as four boxes of the 4 p1 planes, box kxl
+    // starting kxl rows later (plane (kxl, cb) row r = p1 plane cb row r + kxl),
+    // and the 8 dz2 planes
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
       const int sid = int(s0 + i_lo + (c >> 1)), h = c & 1;
-      pb::tma::expect_tx(f, uint32_t(kWgLoad));
-      pb::tma::load_3d(st, &maps.p1, 8 * (h * kWgKH + kyb * kG), 0, sid * 4, f);
-      pb::tma::load_3d(st + 4 * kWgPS, &maps.dz, 8 * (2 * kG + 2 + h * kWgKH), 0, sid * 8, f);
+      pb::tma::expect_tx(f, uint32_t(kWgStage));
+#pragma unroll
+      for (int kxl = 0; kxl < 4; ++kxl)
+        pb::tma::load_3d(st + kxl * 4 * kWgPS, &maps.p1, 8 * (h * kWgKH + kyb * kG + kxl), 0, sid * 4, f);
+      pb::tma::load_3d(st + kWgABytes, &maps.dz, 8 * (2 * kG + 2 + h * kWgKH), 0, sid * 8, f);
     };
     for (int c = 0; c < n && c < kWgStages; ++c) issue(c, smem + c * kWgStage, &full[c]);
     for (int c = 0; c < n; ++c) {
-      const int stg = c % kWgStages, ab = c & 1;
-      mbar_wait(&ready[ab], (c >> 1) & 1);
+      const int stg = c % kWgStages;
+      mbar_wait(&full[stg], (c / kWgStages) & 1);
       fence_after_sync();
-      const uint32_t sa = smem_u32(sAbuf + ab * kWgABytes), sb = smem_u32(smem + stg * kWgStage + 4 * kWgPS);
+      const uint32_t sa = smem_u32(smem + stg * kWgStage), sb = sa + uint32_t(kWgABytes);
       const uint64_t b0 = desc(sb, 128, kWgBS);
 #pragma unroll 1
       for (int g = 0; g < ng; ++g) {
@@ -1806,8 +1803,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
         for (int ks = 0; ks < kWgKH / 16; ++ks)
           mma_bf16(tmem + g * 64, a0 + uint64_t(ks * 16), b0 + uint64_t(ks * 16), idesc, c > 0 || ks > 0);
       }
-      commit(&afree[ab]);    // the A buffer may be rebuilt (chunk c + 2)
-      commit(&empty[stg]);   // the landing stage may be refilled
+      commit(&empty[stg]);   // the stage may be refilled
       const int nx = c - 1 + kWgStages;   // refill the stage of chunk c-1
       if (c >= 1 && nx < n) {
         const int s2 = (c - 1) % kWgStages;
@@ -1817,26 +1813,7 @@ __global__ void __launch_bounds__(256, 1) k_wgrad(Args a, const __grid_constant_
     }
     mbar_wait(&empty[(n - 1) % kWgStages], ((n - 1) / kWgStages) & 1);
   } else if (warp >= 1) {
-    // copy warps: A plane (kxl, cb) row r <- landed base plane cb row r + kxl
-    // (a 4-deep TMA ring keeps 3 chunks of loads in flight behind the MMAs)
-    const int ct = tid - 32;
-    for (int c = 0; c < n; ++c) {
-      const int stg = c % kWgStages, ab = c & 1;
-      const uint8_t* st = smem + stg * kWgStage;
-      uint8_t* A = sAbuf + ab * kWgABytes;
-      mbar_wait(&full[stg], (c / kWgStages) & 1);
-      if (c >= 2) mbar_wait(&afree[ab], ((c - 2) >> 1) & 1);   // the MMAs of chunk c-2 read it
-      constexpr int kUnits = 4 * 4 * kWgCopyRows;
-      for (int u = ct; u < kUnits; u += 224) {
-        const int r = u % kWgCopyRows, pc = u / kWgCopyRows, kxl = pc >> 2, cb = pc & 3;
-        *reinterpret_cast<uint4*>(A + pc * kWgPS + r * 16) =
-            *reinterpret_cast<const uint4*>(st + cb * kWgPS + (r + kxl) * 16);
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&ready[ab])) : "memory");
-    }
-    conv1_update();   // while the tensor pipe drains the last chunks
+    conv1_update();   // warps 1-7, while the tensor pipe runs
   }
   __syncthreads();
   fence_after_sync();
