@@ -570,30 +570,55 @@ __global__ void __launch_bounds__(kHeadDenseThreads) k_head(Args a) {
   for (int e = tid; e < cnt * kH1; e += kHeadDenseThreads) sH[e] = hrow[e];
   __syncthreads();
   const float* b2 = W2 + int64_t(C) * kH1;
-  // logits: one warp per class c holds W2[c] in registers (16 per lane, all
-  // loads in flight at once); lanes split each 512-long dot product
-  for (int c = warp; c < C; c += kHeadDenseThreads / 32) {
-    const float* wc = W2 + int64_t(c) * kH1;
-    float wr[16];
+  // logits: one warp per class pair (c, c+1) holds both W2 rows in registers
+  // (16 per lane each, all loads in flight at once); lanes split each
+  // 512-long dot product, every sH load feeds both classes, and the 8 dot
+  // products of a 4-sample block are finished by a reduce-scatter over the
+  // lanes (9 shuffles instead of 40)
+  for (int cp = warp; 2 * cp < C; cp += kHeadDenseThreads / 32) {
+    const int c0 = 2 * cp;
+    const bool two = c0 + 1 < C;
+    const float* wc0 = W2 + int64_t(c0) * kH1;
+    const float* wc1 = W2 + int64_t(two ? c0 + 1 : c0) * kH1;
+    float wr0[16], wr1[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) wr[k] = wc[lane + 32 * k];
-    const float bc = b2[c];
-    // 4 samples per pass: independent FMA / shuffle chains (each dot product
-    // keeps its own summation order)
+    for (int k = 0; k < 16; ++k) {
+      wr0[k] = wc0[lane + 32 * k];
+      wr1[k] = wc1[lane + 32 * k];
+    }
+    const float bc0 = b2[c0], bc1 = two ? b2[c0 + 1] : 0.0f;
     for (int i0 = 0; i0 < cnt; i0 += 4) {
-      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float v[8];   // v[q]: class c0, sample i0+q; v[4+q]: class c0+1
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = 0.0f;
 #pragma unroll
       for (int k = 0; k < 16; ++k)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (i0 + q < cnt) s[q] = fmaf(sH[(i0 + q) * kH1 + lane + 32 * k], wr[k], s[q]);
-      for (int off = 16; off > 0; off >>= 1)
+        for (int q = 0; q < 4; ++q) {
+          const float h = i0 + q < cnt ? sH[(i0 + q) * kH1 + lane + 32 * k] : 0.0f;
+          v[q] = fmaf(h, wr0[k], v[q]);
+          v[4 + q] = fmaf(h, wr1[k], v[4 + q]);
+        }
+      // lane bits 4, 3, 2 pick which of the 8 sums the lane keeps; bits 1, 0
+      // are summed last
+      const bool b4 = lane & 16, b3 = lane & 8, b2l = lane & 4;
+      float w4[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], off);
-      if (lane == 0)
+      for (int q = 0; q < 4; ++q) {
+        const float o = __shfl_xor_sync(0xffffffffu, b4 ? v[q] : v[4 + q], 16);
+        w4[q] = (b4 ? v[4 + q] : v[q]) + o;
+      }
+      float w2[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (i0 + q < cnt) sL[(i0 + q) * Cp + c] = s[q] + bc;
+      for (int q = 0; q < 2; ++q) {
+        const float o = __shfl_xor_sync(0xffffffffu, b3 ? w4[q] : w4[2 + q], 8);
+        w2[q] = (b3 ? w4[2 + q] : w4[q]) + o;
+      }
+      float r = (b2l ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2l ? w2[0] : w2[1], 4);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      const int idx = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2l ? 1 : 0), q = idx & 3, c = c0 + (idx >> 2);
+      if ((lane & 3) == 0 && i0 + q < cnt && (idx < 4 || two)) sL[(i0 + q) * Cp + c] = r + (idx < 4 ? bc0 : bc1);
     }
   }
   __syncthreads();
