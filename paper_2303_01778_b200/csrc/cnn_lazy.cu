@@ -37,6 +37,42 @@
 #include "cnn_common.cuh"
 #include "tma.cuh"
 
+// Phase trace of k_lz_fwd / k_lz_bwd (tools/phase_probe.py; -DPB_PHASE_TRACE only)
+#ifdef PB_PHASE_TRACE
+__device__ unsigned long long g_lz_phase[2][64][4];
+__device__ int g_lz_armed[2], g_lz_skip[2];
+#define PB_LZ_PHASE(kern, cond, slot, k)                                                        \
+  do {                                                                                          \
+    if (g_lz_armed[kern] && g_lz_skip[kern] == 0 && blockIdx.x == 0 && blockIdx.y == 0 &&          \
+        blockIdx.z == 0 && (cond) &&                                                            \
+        (slot) < 64) {                                                                          \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      g_lz_phase[kern][slot][k] = t_;                                                           \
+    }                                                                                           \
+  } while (0)
+extern "C" int pb_lz_phase_arm(int skip) {   // record the (skip+1)-th launch of each kernel
+  const int one[2] = {1, 1}, sk[2] = {skip, skip};
+  static unsigned long long z[2 * 64 * 4] = {};
+  cudaMemcpyToSymbol(g_lz_phase, z, sizeof(z));
+  cudaMemcpyToSymbol(g_lz_skip, sk, sizeof(sk));
+  return int(cudaMemcpyToSymbol(g_lz_armed, one, sizeof(one)));
+}
+extern "C" int pb_lz_phase_read(unsigned long long* out) {
+  return int(cudaMemcpyFromSymbol(out, g_lz_phase, sizeof(g_lz_phase)));
+}
+#define PB_LZ_DISARM(kern)                                                                        \
+  do {                                                                                            \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {            \
+      if (g_lz_skip[kern] > 0) --g_lz_skip[kern];                                               \
+      else g_lz_armed[kern] = 0;                                                                \
+    }                                                                                           \
+  } while (0)
+#else
+#define PB_LZ_PHASE(kern, cond, slot, k) do { } while (0)
+#define PB_LZ_DISARM(kern) do { } while (0)
+#endif
+
 namespace {
 
 using namespace pb::umma;
@@ -303,6 +339,7 @@ constexpr int kShB1 = 96 * 128;
 constexpr int kSh1Stage = kShA + kShB1;
 constexpr size_t kSh1Smem = 1024 + 3 * kSh1Stage;       // 3 stages: two CTAs per SM
 constexpr size_t kSh1DeepSmem = 1024 + 6 * kSh1Stage;   // 6 stages for grids within one wave
+constexpr size_t kSh4Smem = 1024 + 4 * (2 * kShA + 192 * 128);   // MT = 2, 4 stages of 56 KB (spc*rs <= 192)
 constexpr int kFwdChunks = kFlat / kAK;         // 49 K atoms
 constexpr int kTailCtas = 296;                  // 2 x 148 SMs: tail grids aim for this
 constexpr int kFwdSplitMax = 7;                 // 49 atoms = 7 x 7
@@ -329,11 +366,13 @@ __device__ __forceinline__ void fwd_finish(const Args& a, int s, const Slot& sl,
     if (i < sl.cnt) h[int64_t(i) * kH1] = relu_nan(v[i]);
 }
 
-template <int MT, int S>
+// BR: B rows a stage holds (MT = 2): 256, or 192 when spc*rs <= 192 (bs <=
+// 24), which leaves room for a fourth 56 KB stage
+template <int MT, int S, int BR = 256>
 __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
                                                    int fuse, int rs) {
   pb::pdl_wait();
-  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + kShB;   // 28 KB (MT = 1) or 64 KB (MT = 2)
+  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + BR * 128;   // 28 KB (MT = 1) or 56 | 64 KB (MT = 2)
   static_assert(S <= 6 && 1024 + S * kStage <= 227 * 1024, "lz_fwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
@@ -369,6 +408,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
         if (sS[u].cnt > 0) pb::tma::load_2d(st + MT * kShA + u * rs * 128, rs == 32 ? &m.hxb : &m.hxs, k0, rows[u], f);
     };
     auto mma = [&](int c, uint8_t* st) {
+      PB_LZ_PHASE(0, true, c, 0);   // chunk c's operands landed
       const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
       const uint32_t idesc = idesc_bf16(128, spc * rs);
 #pragma unroll
@@ -379,7 +419,9 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
           mma_bf16(tmem + t * 256, a0 + uint64_t(kk * 2), b0 + uint64_t(kk * 2), idesc, c > 0 || kk > 0);
       }
     };
+    PB_LZ_PHASE(0, true, 63, 0);
     tma_ring<S>(c1 - c0, smem, kStage, full, empty, issue, mma);
+    PB_LZ_PHASE(0, true, 63, 1);
   }
   __syncthreads();
   fence_after_sync();
@@ -407,6 +449,8 @@ __global__ void __launch_bounds__(256, 1) k_lz_fwd(const __grid_constant__ LzMap
   }
   fence_before_sync();
   __syncthreads();
+  PB_LZ_PHASE(0, tid == 0, 63, 2);
+  PB_LZ_DISARM(0);
   if (warp == 0) tmem_free<MT * 256>(tmem);
 }
 
@@ -475,11 +519,11 @@ __global__ void __launch_bounds__(kEpiThreads) k_lz_fwd_epi(Args a, int active, 
 // ---------------------------------------------------------------------------
 constexpr int kBwKT = (kFlat + 127) / 128;      // 25
 
-template <int MT, int S>
+template <int MT, int S, int BR = 256>
 __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMaps m, Args a, int active, int spc,
                                                    int rs) {
   pb::pdl_wait();
-  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + kShB;   // 28 | 64 KB
+  constexpr int kStage = MT == 1 ? kSh1Stage : MT * kShA + BR * 128;   // 28 | 56 | 64 KB
   static_assert(S <= 6 && 1024 + S * kStage <= 227 * 1024, "lz_bwd ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
@@ -532,6 +576,7 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
       }
     };
     auto mma = [&](int c, uint8_t* st) {
+      PB_LZ_PHASE(1, true, c, 0);
       if (c < n1) {
         const uint32_t idesc = idesc_bf16(128, spc * rs);
         const uint64_t b0 = desc_sw128(smem_u32(st + MT * kShA));
@@ -559,7 +604,9 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
         }
       }
     };
+    PB_LZ_PHASE(1, true, 63, 0);
     tma_ring<S>(n, smem, kStage, full, empty, issue, mma);
+    PB_LZ_PHASE(1, true, 63, 1);
   }
   __syncthreads();
   fence_after_sync();
@@ -582,6 +629,8 @@ __global__ void __launch_bounds__(256, 1) k_lz_bwd(const __grid_constant__ LzMap
   }
   fence_before_sync();
   __syncthreads();
+  PB_LZ_PHASE(1, tid == 0, 63, 2);
+  PB_LZ_DISARM(1);
   if (warp == 0) tmem_free<MT * 256>(tmem);
 }
 
@@ -794,9 +843,11 @@ int setup() {
                {(const void*)k_lz_fwd<1, 3>, kSh1Smem, "k_lz_fwd"},
                {(const void*)k_lz_fwd<1, 6>, kSh1DeepSmem, "k_lz_fwd"},
                {(const void*)k_lz_fwd<2, 3>, kShSmem, "k_lz_fwd"},
+               {(const void*)k_lz_fwd<2, 4, 192>, kSh4Smem, "k_lz_fwd"},
                {(const void*)k_lz_bwd<1, 3>, kSh1Smem, "k_lz_bwd"},
                {(const void*)k_lz_bwd<1, 6>, kSh1DeepSmem, "k_lz_bwd"},
                {(const void*)k_lz_bwd<2, 3>, kShSmem, "k_lz_bwd"},
+               {(const void*)k_lz_bwd<2, 4, 192>, kSh4Smem, "k_lz_bwd"},
                {(const void*)k_lz_mat, kShSmem, "k_lz_mat"},
                {(const void*)k_lz_fold, kShSmem, "k_lz_fold"}};
   for (auto& x : attrs) {
@@ -913,7 +964,10 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;   // B rows per slot: packed when several share a CTA
     pb::prof_begin(pb::K_CNN_LZ_FWD, s);
     const int sms = pb::sm_count();
-    if (spc == kSh8)
+    if (spc == kSh8 && spc * rs <= 192)
+      pb::launch_pdl(k_lz_fwd<2, 4, 192>, dim3(kH1 / 256, groups, ks), dim3(256), kSh4Smem, s, 1, m, a, active, spc,
+                     fuse, rs);
+    else if (spc == kSh8)
       pb::launch_pdl(k_lz_fwd<2, 3>, dim3(kH1 / 256, groups, ks), dim3(256), kShSmem, s, 1, m, a, active, spc, fuse,
                      rs);
     else if (int(groups) * (kH1 / 128) * ks <= sms)
@@ -948,7 +1002,10 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
     pb::prof_begin(pb::K_CNN_LZ_BWD, s);
     {
       const int rs = spc == 1 ? 32 : (a.BS + 7) & ~7;
-      if (spc == kSh8)
+      if (spc == kSh8 && spc * rs <= 192)
+        pb::launch_pdl(k_lz_bwd<2, 4, 192>, dim3((kBwKT + 1) / 2, groups), dim3(256), kSh4Smem, s, 1, m, a, active,
+                       spc, rs);
+      else if (spc == kSh8)
         pb::launch_pdl(k_lz_bwd<2, 3>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
       else if (kBwKT * int(groups) <= pb::sm_count())
         pb::launch_pdl(k_lz_bwd<1, 6>, dim3(kBwKT, groups), dim3(256), kSh1DeepSmem, s, 1, m, a, active, spc, rs);

@@ -25,7 +25,7 @@ dev = torch.device("cuda", 0)
 data, sizes = bench.build_device_data(dev)
 profiles = bench.light_profiles(sizes)
 cfg = pb.SimConfig(total_clients=bench.M_TOTAL, concurrent_clients=bench.M_ROUND, num_devices=1,
-                   total_rounds=3, warmup_rounds=1, seed=0, scheme="PARROT")
+                   total_rounds=4, warmup_rounds=1, seed=0, scheme="PARROT")
 eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=bench.LR, batch_size=bench.BS), profiles,
                           pb.make_device_models(1), model="cnn", client_data=data)
 eng.run_round(0)
@@ -61,3 +61,21 @@ for kern, (name, names) in enumerate(tables.items()):
     starts = ph[:, 0][ph[:, 0] > 0]
     if len(starts) > 2:
         print("iteration period us (median):", float(np.median(np.diff(starts))) / 1e3)
+
+# low-rank fc1 kernels: CTA (0,0,0) of the 6th launch of k_lz_fwd / k_lz_bwd
+# in a round (sweep 5): per ring chunk the time its operands landed (us from
+# the ring start), then ring end and kernel end
+if hasattr(dll, "pb_lz_phase_arm"):
+    assert dll.pb_lz_phase_arm(5) == 0
+    eng.run_round(2)
+    torch.cuda.synchronize()
+    lbuf = (ctypes.c_ulonglong * (2 * 64 * 4))()
+    assert dll.pb_lz_phase_read(lbuf) == 0
+    lz = np.frombuffer(lbuf, dtype=np.uint64).reshape(2, 64, 4).astype(np.int64)
+    for kern, name in enumerate(("k_lz_fwd", "k_lz_bwd")):
+        t0 = lz[kern, 63, 0]
+        if not t0:
+            continue
+        chunks = [(c, (lz[kern, c, 0] - t0) / 1e3) for c in range(63) if lz[kern, c, 0]]
+        print(name, "chunks landed (us):", " ".join(f"{c}:{t:.2f}" for c, t in chunks))
+        print(name, f"ring end {(lz[kern, 63, 1] - t0) / 1e3:.2f} us, kernel end {(lz[kern, 63, 2] - t0) / 1e3:.2f} us")
