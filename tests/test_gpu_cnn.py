@@ -375,3 +375,50 @@ def test_cnn_lowrank_switch_to_direct(spec, femnist_like, monkeypatch):
     ends = group(SW)
     want = (sizes[:, None].astype(np.float64) * ends).sum(0) / float(sizes.sum())
     assert _rel(got, want) <= 1e-5
+
+
+_BS32_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2303_01778_b200 as pb
+from paper_2303_01778_b200.data import generate
+from paper_2303_01778_b200.models import cnn_spec
+ds = generate(4000, 784, 62, seed=0)
+train = pb.SyntheticDataset(ds.features[:3200], ds.labels[:3200], 62, 784, 3.0, 1.0) \
+    if len(np.unique(ds.labels[:3200])) == 62 else ds
+profiles = pb.partition(train, 40, pb.PartitionSpec(quantity_skew=1.0, min_samples_per_client=10), seed=0)
+cfg = pb.SimConfig(total_clients=40, concurrent_clients=24, num_devices=1, total_rounds=2, warmup_rounds=0,
+                   seed=7, scheme="SP")
+eng = pb.SimulationEngine(cfg, pb.FedAvg(lr=0.05, batch_size=32), profiles, pb.make_device_models(1),
+                          model="cnn", init_seed=3)
+oc = eng.run_round(0)
+np.save(sys.argv[1], np.concatenate([oc.new_global.numpy(nm).reshape(-1) for nm in cnn_spec(62).names]))
+"""
+
+
+def test_cnn_fl_round_bs32_matches_oracle(spec, femnist_like, tmp_path):
+    """bs = 32 with every sweep packing 8 clients per CTA (PB_LZ_SPC forces the
+    dense form): the low-rank fc1's 256-row B variants of k_lz_fwd / k_lz_bwd,
+    one FedAvg round vs the oracle (child process: the threshold is read once)."""
+    import os
+    import subprocess
+    import sys
+    import paper_2303_01778_b200 as pb
+    from oracle import cnn_oracle
+    from paper_2303_01778_b200.models import cnn_init
+    out = tmp_path / "got.npy"
+    env = dict(os.environ, PB_LZ_SPC="1,1,1")
+    subprocess.run([sys.executable, "-c", _BS32_CHILD, str(out)], check=True, env=env,
+                   cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    got = np.load(out)
+    ds = femnist_like
+    train = pb.SyntheticDataset(ds.features[:3200], ds.labels[:3200], 62, 784, 3.0, 1.0) \
+        if len(np.unique(ds.labels[:3200])) == 62 else ds
+    profiles = pb.partition(train, 40, pb.PartitionSpec(quantity_skew=1.0, min_samples_per_client=10),
+                            seed=0)
+    data = {p.client_id: (p.data_partition.features, p.data_partition.labels) for p in profiles}
+    cfg = pb.SimConfig(total_clients=40, concurrent_clients=24, num_devices=1, total_rounds=2, warmup_rounds=0,
+                       seed=7, scheme="SP")
+    sel = pb.select_clients(cfg, 0).selected
+    ref = cnn_oracle.fedavg_round(cnn_init(spec, seed=3).astype(np.float64), data, sel, 7, 0, 1, 32, 0.05, 62)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 5e-3
