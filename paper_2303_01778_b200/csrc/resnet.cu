@@ -29,6 +29,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "tma.cuh"
 #include "umma.cuh"
@@ -768,15 +770,17 @@ struct GnF {
 };
 
 constexpr int kGnThreads = 512;
-constexpr size_t kGnSmem = (5 * 1024 + 64) * sizeof(double);   // partials, per-channel sums, scratch
+// partials, per-channel sums, scratch, cluster totals
+constexpr size_t kGnSmem = (6 * 1024 + 64) * sizeof(double);
 
 // Per-channel sums of two quantities over positions, 4 channels per thread
 // (float4 loads): thread t owns channel group (t % (C/4)) and every
 // (512 / (C/4))-th position, two independent chains; the per-thread partials
 // are combined in part order into r1[c], r2[c] (double).  f(p, c0, u, v)
 // fills u[0..3], v[0..3] for channels c0..c0+3 at position p.  C <= 512.
+// Positions [p0, HW) of this CTA's share (the caller passes its range end as HW).
 template <class F>
-__device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* part2, double* r1,
+__device__ __forceinline__ void chan_sums(int C, int p0, int HW, double* part1, double* part2, double* r1,
                                           double* r2, F f) {
   const int tid = threadIdx.x, C4 = C >> 2, tpc = kGnThreads / C4;  // C4 <= 128 -> tpc >= 4
   const int cg = tid & (C4 - 1), pt = tid / C4, c0 = cg * 4;
@@ -784,7 +788,7 @@ __device__ __forceinline__ void chan_sums(int C, int HW, double* part1, double* 
   // independent chains, all loads of an iteration in flight), double combine
   float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
   float a2[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
-  int p = pt;
+  int p = p0 + pt;
   for (; p + 3 * tpc < HW; p += 4 * tpc) {
     float u[4], v[4], x[4], y[4], u2[4], v2[4], x2[4], y2[4];
     f(p, c0, u, v);
@@ -858,6 +862,36 @@ __device__ __forceinline__ void group_sums(int C, double v1, double v2, double* 
   __syncthreads();
 }
 
+// A sample's GroupNorm is split over a cluster of P CTAs (position ranges,
+// P fixed per layer): the per-channel sums r1, r2 of the P parts are added in
+// rank order into t1, t2 in every CTA (deterministic, independent of the
+// schedule); the second cluster barrier keeps r1, r2 alive until every CTA
+// has read them.
+__device__ __forceinline__ void cluster_chan_totals(int C, int P, const double* r1, const double* r2, double* t1,
+                                                    double* t2) {
+  namespace cgp = cooperative_groups;
+  if (P == 1) {
+    for (int c = threadIdx.x; c < C; c += kGnThreads) {
+      t1[c] = r1[c];
+      t2[c] = r2[c];
+    }
+    __syncthreads();
+    return;
+  }
+  cgp::cluster_group cl = cgp::this_cluster();
+  cl.sync();
+  for (int c = threadIdx.x; c < C; c += kGnThreads) {
+    double x1 = 0.0, x2 = 0.0;
+    for (int q = 0; q < P; ++q) {
+      x1 += cl.map_shared_rank(r1, q)[c];
+      x2 += cl.map_shared_rank(r2, q)[c];
+    }
+    t1[c] = x1;
+    t2[c] = x2;
+  }
+  cl.sync();
+}
+
 // mean / rstd of the two groups from per-channel sum and sum of squares
 __device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, const double* s2, double* scratch,
                                            float (&mean)[kGroups], float (&rstd)[kGroups]) {
@@ -875,17 +909,21 @@ __device__ __forceinline__ void gn_moments(int C, int HW, const double* s1, cons
 }
 
 // out = relu(GN(z) [+ res | + GN2(z2)]) as bf16; grid (active, BS)
-__global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
+// grid (active * P, BS), clusters of P along x: part = this CTA's share of
+// the sample's positions
+__global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f, int P) {
   pb::pdl_wait();
-  const int s = blockIdx.x, i = blockIdx.y;
+  const int s = blockIdx.x / P, part = blockIdx.x - s * P, i = blockIdx.y;
   const Slot sl = a.slots[s];
-  if (i >= sl.cnt) {
+  const int pa = f.HW * part / P, pb_ = f.HW * (part + 1) / P;   // positions [pa, pb_)
+  if (i >= sl.cnt) {   // uniform over the cluster
     // samples past a partial batch: zero activations, so the TMA weight
     // gradients (whole position tiles, dz = 0 there) never multiply stale
     // (possibly non-finite) workspace contents
     if (sl.cnt == 0) return;
     uint4* o = reinterpret_cast<uint4*>(at<bf16>(a, s, f.out) + int64_t(i) * f.HW * f.C);
-    for (int64_t e = threadIdx.x; e < int64_t(f.HW) * f.C / 8; e += kGnThreads) o[e] = make_uint4(0, 0, 0, 0);
+    for (int64_t e = int64_t(pa) * f.C / 8 + threadIdx.x; e < int64_t(pb_) * f.C / 8; e += kGnThreads)
+      o[e] = make_uint4(0, 0, 0, 0);
     return;
   }
   extern __shared__ double dsm[];
@@ -893,6 +931,8 @@ __global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
   double* p2 = dsm + 4 * kGnThreads;
   double* r1 = dsm + 8 * kGnThreads;
   double* r2 = r1 + 512;
+  double* t1 = r2 + 512 + 64;   // cluster totals (after the scratch)
+  double* t2 = t1 + 512;
   const int C = f.C, HW = f.HW, cshift = __ffs(C / kGroups) - 1;
   const int64_t base = int64_t(i) * HW * C;
   const float* z = at<float>(a, s, f.z) + base;
@@ -905,15 +945,17 @@ __global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
       v[0] = x.x * x.x, v[1] = x.y * x.y, v[2] = x.z * x.z, v[3] = x.w * x.w;
     };
   };
-  chan_sums(C, HW, p1, p2, r1, r2, sq(z));
-  gn_moments(C, HW, r1, r2, r2 + 512, mean, rstd);
+  chan_sums(C, pa, pb_, p1, p2, r1, r2, sq(z));
+  cluster_chan_totals(C, P, r1, r2, t1, t2);
+  gn_moments(C, HW, t1, t2, r2 + 512, mean, rstd);
   __syncthreads();
   const float* z2 = f.z2 >= 0 ? at<float>(a, s, f.z2) + base : nullptr;
   if (z2) {
-    chan_sums(C, HW, p1, p2, r1, r2, sq(z2));
-    gn_moments(C, HW, r1, r2, r2 + 512, mean2, rstd2);
+    chan_sums(C, pa, pb_, p1, p2, r1, r2, sq(z2));
+    cluster_chan_totals(C, P, r1, r2, t1, t2);
+    gn_moments(C, HW, t1, t2, r2 + 512, mean2, rstd2);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && part == 0) {
     float* st = at<float>(a, s, f.stats) + i * 2 * kGroups;
     for (int g = 0; g < kGroups; ++g) {
       st[2 * g] = mean[g];
@@ -932,9 +974,9 @@ __global__ void __launch_bounds__(kGnThreads, 3) k_rn_gn_fwd(Net a, GnF f) {
   const float* g2 = z2 ? W + f.gamma2 : nullptr;
   const bf16* res = f.res >= 0 ? at<const bf16>(a, s, f.res) + base : nullptr;
   bf16* out = at<bf16>(a, s, f.out) + base;
-  const int n4 = HW * C / 4;
+  const int n4 = pb_ * C / 4;
 #pragma unroll 4
-  for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
+  for (int e4 = pa * C / 4 + threadIdx.x; e4 < n4; e4 += kGnThreads) {
     const int c0 = (e4 * 4) & (C - 1), g = c0 >> cshift;
     const float4 zv = reinterpret_cast<const float4*>(z)[e4];
     float v[4] = {zv.x, zv.y, zv.z, zv.w};
@@ -976,11 +1018,14 @@ struct GnB {
 // G = (g0 [+ g1]) * (mask > 0) while it reduces it (one pass over the sources)
 template <bool MAT>
 __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, int64_t z_off,
-                           int64_t st_off, int64_t gam_off, int64_t dz_off, int64_t pg_off, double* dsm) {
+                           int64_t st_off, int64_t gam_off, int64_t dz_off, int64_t pg_off, double* dsm, int P,
+                           int part, int pa, int pb_) {
   double* p1 = dsm;
   double* p2 = dsm + 4 * kGnThreads;
   double* r1 = dsm + 8 * kGnThreads;
   double* r2 = r1 + 512;
+  double* t1s = r2 + 512 + 64;   // cluster totals (after the scratch)
+  double* t2s = t1s + 512;
   const int C = f.C, HW = f.HW, cg = C / kGroups, cshift = __ffs(cg) - 1;
   const int64_t base = int64_t(i) * HW * C;
   const float* z = at<float>(a, s, z_off) + base;
@@ -996,7 +1041,7 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
   const float* g0 = MAT ? at<float>(a, s, f.g0) + base : nullptr;
   const float* g1 = MAT && f.g1 >= 0 ? at<float>(a, s, f.g1) + base : nullptr;
   const bf16* mask = MAT && f.mask >= 0 ? at<const bf16>(a, s, f.mask) + base : nullptr;
-  chan_sums(C, HW, p1, p2, r1, r2, [&](int p, int c0, float* u, float* v) {
+  chan_sums(C, pa, pb_, p1, p2, r1, r2, [&](int p, int c0, float* u, float* v) {
     float4 gv;
     if (MAT) {
       gv = *reinterpret_cast<const float4*>(g0 + p * C + c0);
@@ -1026,17 +1071,19 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
     v[2] = gv.z * ((zv.z - mean[g]) * rstd[g]);
     v[3] = gv.w * ((zv.w - mean[g]) * rstd[g]);
   });
+  cluster_chan_totals(C, P, r1, r2, t1s, t2s);
   float* pg = a.gnp + int64_t(s) * a.gnp_slot + pg_off + int64_t(i) * 2 * C;
-  for (int c = threadIdx.x; c < C; c += kGnThreads) {
-    pg[c] = float(r2[c]);      // dgamma partial of sample i
-    pg[C + c] = float(r1[c]);  // dbeta partial
-  }
+  if (part == 0)
+    for (int c = threadIdx.x; c < C; c += kGnThreads) {
+      pg[c] = float(t2s[c]);      // dgamma partial of sample i
+      pg[C + c] = float(t1s[c]);  // dbeta partial
+    }
   const double inv_n = 1.0 / double(HW * cg);
   float m1[kGroups], m2[kGroups];
   {
     const int c = threadIdx.x;
     double t1[kGroups], t2[kGroups];
-    group_sums(C, c < C ? double(gam[c]) * r1[c] : 0.0, c < C ? double(gam[c]) * r2[c] : 0.0, r2 + 512, t1, t2);
+    group_sums(C, c < C ? double(gam[c]) * t1s[c] : 0.0, c < C ? double(gam[c]) * t2s[c] : 0.0, r2 + 512, t1, t2);
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
       m1[g] = float(t1[g] * inv_n);
@@ -1044,9 +1091,9 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
     }
   }
   bf16* dz = at<bf16>(a, s, dz_off) + base;
-  const int n4 = HW * C / 4;
+  const int n4 = pb_ * C / 4;
 #pragma unroll 4
-  for (int e4 = threadIdx.x; e4 < n4; e4 += kGnThreads) {
+  for (int e4 = pa * C / 4 + threadIdx.x; e4 < n4; e4 += kGnThreads) {
     const int c0 = (e4 * 4) & (C - 1), g = c0 >> cshift;
     const float4 gv = reinterpret_cast<const float4*>(G)[e4];
     const float4 zv = reinterpret_cast<const float4*>(z)[e4];
@@ -1067,16 +1114,18 @@ __device__ void gn_bwd_one(const Net& a, int s, int i, const GnB& f, float* G, i
 // G = (g0 [+ g1]) * (mask > 0); GN backward(s) -> bf16 dz; grid (active, BS)
 // Samples past the batch get dz = 0: the TMA weight-gradient boxes read
 // whole position tiles, and zero dz rows keep them out of the sum.
-__global__ void __launch_bounds__(kGnThreads, 2) k_rn_gn_bwd(Net a, GnB f) {
+// grid (active * P, BS), clusters of P along x (position ranges of a sample)
+__global__ void __launch_bounds__(kGnThreads, 2) k_rn_gn_bwd(Net a, GnB f, int P) {
   pb::pdl_wait();
-  const int s = blockIdx.x, i = blockIdx.y;
+  const int s = blockIdx.x / P, part = blockIdx.x - s * P, i = blockIdx.y;
   const Slot sl = a.slots[s];
-  if (i >= sl.cnt) {
+  const int pa = f.HW * part / P, pb_ = f.HW * (part + 1) / P;
+  if (i >= sl.cnt) {   // uniform over the cluster
     if (sl.cnt == 0) return;
-    const int64_t n8 = int64_t(f.HW) * f.C / 8;
+    const int64_t n8 = int64_t(pb_) * f.C / 8;
     uint4* z1 = reinterpret_cast<uint4*>(at<bf16>(a, s, f.dz) + int64_t(i) * f.HW * f.C);
     uint4* z2 = f.z2 >= 0 ? reinterpret_cast<uint4*>(at<bf16>(a, s, f.dz2) + int64_t(i) * f.HW * f.C) : nullptr;
-    for (int64_t e = threadIdx.x; e < n8; e += kGnThreads) {
+    for (int64_t e = int64_t(pa) * f.C / 8 + threadIdx.x; e < n8; e += kGnThreads) {
       z1[e] = make_uint4(0, 0, 0, 0);
       if (z2) z2[e] = make_uint4(0, 0, 0, 0);
     }
@@ -1088,10 +1137,10 @@ __global__ void __launch_bounds__(kGnThreads, 2) k_rn_gn_bwd(Net a, GnB f) {
   // the gated gradient is materialised once (fp32, in the gsc buffer or in
   // place over g0) by the first reduction pass; later passes read it
   float* G = f.gsc >= 0 ? at<float>(a, s, f.gsc) + base : at<float>(a, s, f.g0) + base;
-  gn_bwd_one<true>(a, s, i, f, G, f.z, f.stats, f.gamma, f.dz, f.pg, dsm);
+  gn_bwd_one<true>(a, s, i, f, G, f.z, f.stats, f.gamma, f.dz, f.pg, dsm, P, part, pa, pb_);
   if (f.z2 >= 0) {
     __syncthreads();
-    gn_bwd_one<false>(a, s, i, f, G, f.z2, f.stats2, f.gamma2, f.dz2, f.pg2, dsm);
+    gn_bwd_one<false>(a, s, i, f, G, f.z2, f.stats2, f.gamma2, f.dz2, f.pg2, dsm, P, part, pa, pb_);
   }
 }
 
@@ -1361,6 +1410,9 @@ Net to_net(const pb_resnet_train_args& t, const Plan& pl) {
 int conv_ntile(int n) { return n >= 256 ? 256 : n; }
 
 size_t gn_smem() { return kGnSmem; }
+// CTAs per sample of the GroupNorm kernels: by layer size only (the sums'
+// order then never depends on how many clients share a sweep)
+int gn_parts(int HW) { return HW >= 1024 ? 4 : HW >= 256 ? 2 : 1; }
 
 // TMA maps for the stride-1, 64-channel-block forward convolutions: the
 // NHWC input over every slot (5-D) and each client's bf16 weights (3-D)
@@ -1524,7 +1576,8 @@ void launch_gn_fwd(const Net& a, const ConvL& c, int64_t res, const ConvL* c2, i
   f.gamma2 = c2 ? c2->gn_gamma : -1;
   f.out = out;
   pb::prof_begin(pb::K_RN_NORM, s);
-  pb::launch_pdl(k_rn_gn_fwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
+  const int P = gn_parts(f.HW);
+  pb::launch_pdl(k_rn_gn_fwd, dim3(unsigned(active * P), a.BS), dim3(kGnThreads), gn_smem(), s, unsigned(P), a, f, P);
   pb::prof_end(pb::K_RN_NORM, s);
 }
 
@@ -1626,7 +1679,8 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
       f.z2 = cd.k.z; f.stats2 = cd.stats; f.gamma2 = cd.gn_gamma; f.dz2 = cd.k.dz; f.pg2 = cd.pg;
     }
     pb::prof_begin(pb::K_RN_NORM, s);
-    pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
+    pb::launch_pdl(k_rn_gn_bwd, dim3(unsigned(active * gn_parts(f.HW)), a.BS), dim3(kGnThreads), gn_smem(), s,
+                   unsigned(gn_parts(f.HW)), a, f, gn_parts(f.HW));
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(cb);
     launch_conv(a, cb, DGRAD, active, s);   // du (old weights)
@@ -1646,7 +1700,8 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
     m.z = ca.k.z; m.stats = ca.stats; m.gamma = ca.gn_gamma; m.dz = ca.k.dz; m.pg = ca.pg;
     m.z2 = m.stats2 = m.gamma2 = m.dz2 = m.pg2 = -1;
     pb::prof_begin(pb::K_RN_NORM, s);
-    pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, m);
+    pb::launch_pdl(k_rn_gn_bwd, dim3(unsigned(active * gn_parts(m.HW)), a.BS), dim3(kGnThreads), gn_smem(), s,
+                   unsigned(gn_parts(m.HW)), a, m, gn_parts(m.HW));
     pb::prof_end(pb::K_RN_NORM, s);
     add_gn(ca);
     launch_conv(a, ca, DGRAD, active, s);
@@ -1664,7 +1719,8 @@ int backward(const Net& a, const Plan& pl, int active, cudaStream_t s) {
   f.z = c0.k.z; f.stats = c0.stats; f.gamma = c0.gn_gamma; f.dz = c0.k.dz; f.pg = c0.pg;
   f.z2 = f.stats2 = f.gamma2 = f.dz2 = f.pg2 = -1;
   pb::prof_begin(pb::K_RN_NORM, s);
-  pb::launch_pdl(k_rn_gn_bwd, dim3(active, a.BS), dim3(kGnThreads), gn_smem(), s, 1, a, f);
+  pb::launch_pdl(k_rn_gn_bwd, dim3(unsigned(active * gn_parts(f.HW)), a.BS), dim3(kGnThreads), gn_smem(), s,
+                 unsigned(gn_parts(f.HW)), a, f, gn_parts(f.HW));
   pb::prof_end(pb::K_RN_NORM, s);
   add_gn(c0);
   wgrad_side(a, c0, active, s);   // (the side stream also serialises the shared partial buffer)
@@ -1688,6 +1744,10 @@ int setup() {
   for (const void* fn : fns) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCvSmem + 1024));
     if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_conv: ") + cudaGetErrorString(e));
+  }
+  for (const void* fn : {(const void*)k_rn_gn_fwd, (const void*)k_rn_gn_bwd}) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGnSmem));
+    if (e != cudaSuccess) return pb::fail(PB_ERR_CUDA, std::string("k_rn_gn: ") + cudaGetErrorString(e));
   }
   cudaError_t e = cudaFuncSetAttribute((const void*)k_rn_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        200 * 1024);
