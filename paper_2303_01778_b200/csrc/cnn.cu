@@ -1196,41 +1196,42 @@ __global__ void __launch_bounds__(256, 1) k_fc1_bwd(Args a) {
 // tcgen05, plus the conv2 bias gradient of this sample (per-sample partials,
 // summed in sample order by k_wgrad: deterministic).
 //
-// dgrad MMAs, column-blocked: for filter row ky ONE N = 128 MMA multiplies
-// the dz2 planes (A, K-major over co) by the four weight tiles W[ky][kx =
-// 0..3] side by side (B, MN-major: in the UMMA weight layout the 16 (kx, ci
-// block) core-matrix columns of one filter row sit 1024 B apart), and one
-// N = 32 MMA adds tap (ky, 4) into block 3 (its A one row earlier).  Block j
-// accumulates the contribution of tap (ky, j) to output row q = p - 3 + j,
-// so the epilogue sums out[q] = D3[q] + D2[q+1] + D1[q+2] + D0[q+3] (warp
-// shuffles, a 3-row halo between lane quarters).  Every MMA with N <= 64
-// costs the same ~52 cycles (tools/umma_bench2.py): 40 MMAs per sample (20 at
-// N = 128) replace 200 N = 32 ones.  M tiles: output rows [0, 125) from tile
-// rows [0, 128), rows [125, 248) from [124, 252) (row q = y*18 + x; x >= 14
-// discarded), i.e. pooled rows y 0-6 and 7-13.
+// dgrad MMAs, column-blocked: for filter row ky ONE N = 160 MMA multiplies
+// the dz2 planes (A, K-major over co, started one row early) by the five
+// weight tiles W[ky][kx = 0..4] side by side (B, MN-major: in the UMMA weight
+// layout the 20 (kx, ci block) core-matrix columns of one filter row sit
+// 1024 B apart).  Block kx accumulates the contribution of tap (ky, kx) to
+// output row q = p - 4 + kx, so the epilogue sums out[q] = sum_kx
+// D_kx[q + 4 - kx] (warp shuffles, a 4-row halo between lane quarters).  An
+// MMA with fresh operands costs ~65 cycles for N <= 128 and N/2 above
+// (tools/umma_dgrad_bench.py): 40 MMAs per sample.  M tiles: output rows
+// [0, 124) from tile rows [0, 128), rows [124, 248) from [124, 252) (row
+// q = y*18 + x; x >= 14 discarded), i.e. pooled rows y 0-6 and 7-13.
 //
 // conv1 weight gradient, per M tile (98 pooled positions p, K padded to 112):
-//   H[(d, co)][n] += sum_p G_d[p][co] * Win[p][n]
-// M = 128 = pool candidate d (TMEM lane quarter) x channel co, G_d[p][co] =
+//   H[(co, d)][n] += sum_p G_d[p][co] * Win[p][n]
+// M = 128 = channel co x pool candidate d (TMEM lane co*4 + d), G_d[p][co] =
 // bf16(relu' * dp1[p][co]) where pool1's argmax is d and 0 for the other
 // three candidates; N = 48 = the 36 cells of the 6x6 input window at
 // (2py, 2px) (bf16 image) + a ones cell (the bias) + zero pad.  Both
 // operands MN-major, no swizzle (K rows 16 B apart, core columns 1792 B
-// apart).  Then dW1[co][ky][kx] = sum_d H[(d, co)][(ky + dy)*6 + kx + dx]
-// and db1[co] = sum_d H[(d, co)][36] (smem, fixed order).  14 MMAs per sample
-// replace 157k SIMT FMAs and their 25 shared-memory loads per tap.
+// apart).  Then dW1[co][ky][kx] = sum_d H[(co, d)][(ky + dy)*6 + kx + dx]
+// and db1[co] = sum_d H[(co, d)][36]: a 4-lane shuffle reduce-scatter, fixed
+// order.  14 MMAs per sample replace 157k SIMT FMAs and their 25
+// shared-memory loads per tap.
 // Warp-specialised pipeline over the CTA's samples.  Warp 16 (one thread)
-// issues the dgrad MMAs of sample i into TMEM set i&1 as soon as its dz2
-// planes are built, bulk-copies the planes to global for k_wgrad and the
-// sample's pool1 argmaxes into smem, then the conv1-gradient MMAs of sample
-// i-1 (into columns [0, 48) of set (i-1)&1, read out by then) as each tile
-// of G lands; warps 0-15 build the planes of sample i from registers
-// prefetched during sample i-1, then -- while the MMAs run -- finish sample
-// i-1 (TMEM -> dp1 -> G and the window operand, H -> conv1 partials).
-// mbarriers: dz_full (planes built), mma_done[set], dz_free (MMAs + plane
-// store of the sample done), tmem_idle[set] (set read out), am1_full[buffer],
-// g_full (a G tile + the window operand written), g_free (tile 0's conv1
-// MMAs done: G may be rewritten), wg_done (H complete).
+// issues the dgrad MMAs of sample i (TMEM: a ring of three 160-column tile
+// buffers, tile n = 2(i - i0) + t in buffer n % 3) as soon as its dz2 planes
+// are built, bulk-copies the planes to global for k_wgrad and the sample's
+// pool1 argmaxes into smem, then the conv1-gradient MMAs of sample i-1 as
+// each tile of G lands (H(i-1) in the first 48 columns of its tile-1
+// buffer, free by then).  Warps 0-15 build the planes of sample i from
+// registers prefetched during sample i-1 (warps 12-15 first read out H of
+// sample i-2), then -- while the MMAs run -- finish sample i-1 (TMEM -> dp1
+// -> G and the window operand).  mbarriers: dz_full (planes built), dz_free
+// (MMAs + plane store of the sample done), tile_full / tile_free[buffer],
+// am1_full[buffer], g_full (a G tile + the window operand written), g_free
+// (that tile's conv1 MMAs done: G may be rewritten).
 // grid (ceil(BS/spb), active), 544 threads
 // ---------------------------------------------------------------------------
 constexpr int kBwdWork = 512;                            // warps 0-15: SIMT work
