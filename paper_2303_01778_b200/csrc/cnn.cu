@@ -127,12 +127,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
 // order, relu, bf16) with no data exchange: 6 MMAs per sample.  conv2 as
 // before: the A operand is the padded p1 image itself, one shifted descriptor
 // per filter tap.
-// Warp-specialised: warp 16 issues conv1(i) once A(i) is built and conv2(i)
-// once the p1 planes of i are written (mbarriers a_ready / p1_ready; the
-// tensor pipe runs conv1(i), conv2(i), conv1(i+1), ... in issue order, so
-// conv1(i) done => conv2(i-1) done); warps 0-15 run the conv1 epilogue of
-// i, build A(i+1), copy p1(i) out and finish conv2 of sample i-1 (two
-// 32-channel halves through smem).
+// Warp-specialised: once the p1 planes of sample k are written, warp 16
+// issues conv1(k+1) and then conv2(k), so the tensor pipe (in issue order)
+// runs conv1(k+1) before conv2(k) and the conv1 epilogue of k+1 overlaps
+// conv2(k); the p1 planes are double-buffered (k & 1) and conv1(k) done =>
+// conv2(k-2) done with its planes.  Warps 0-15: wait conv1(i), build A(i+1),
+// the conv1 epilogue of i (p1 planes, pool1 argmaxes), then finish conv2 of
+// sample i-1 (two 32-channel halves through smem).
 // ---------------------------------------------------------------------------
 constexpr int kFwdWork = 512;                // warps 0-15
 constexpr int kFwdThreads = kFwdWork + 32;   // + warp 16: MMA issue
