@@ -751,25 +751,32 @@ __global__ void __launch_bounds__(256, 1) k_lz_fold(const __grid_constant__ LzMa
   const uint32_t tmem = tmem_base;
   const int nc = c1 - c0;
   if (tid == 0 && nc > 0) {
-    // every chunk twice: the high then the low term of the weighted dH^T
+    // per chunk of 64 history rows: the high and the low term of the
+    // weighted dH^T against ONE copy of the X atoms (3 stages of 64 KB)
+    constexpr int kFoldStage = 2 * kShA + kShB;
+    static_assert(3 * kFoldStage + 1024 <= kShSmem, "k_lz_fold ring");
     auto issue = [&](int c, uint8_t* st, uint64_t* f) {
-      const int row = row_lo + (c0 + c % nc) * kAK;
-      pb::tma::expect_tx(f, kShStage);
+      const int row = row_lo + (c0 + c) * kAK;
+      pb::tma::expect_tx(f, kFoldStage);
 #pragma unroll
-      for (int h = 0; h < 2; ++h)   // weighted dH rows (high, then low term), MN-major
-        pb::tma::load_2d(st + h * 8192, c < nc ? &m.hda[1] : &m.hdl, q * 128 + h * 64, row, f);
+      for (int h = 0; h < 2; ++h) {   // weighted dH rows (high, low term), MN-major
+        pb::tma::load_2d(st + h * 8192, &m.hda[1], q * 128 + h * 64, row, f);
+        pb::tma::load_2d(st + kShA + h * 8192, &m.hdl, q * 128 + h * 64, row, f);
+      }
 #pragma unroll
       for (int h = 0; h < 4; ++h)   // X rows of the history, MN-major: four 64-feature atoms
-        pb::tma::load_2d(st + kShA + h * 8192, &m.hxa[1], k0 + h * 64, row, f);
+        pb::tma::load_2d(st + 2 * kShA + h * 8192, &m.hxa[1], k0 + h * 64, row, f);
     };
     auto mma = [&](int c, uint8_t* st) {
-      const uint32_t as = smem_u32(st), bs = smem_u32(st + kShA);
+      const uint32_t ah = smem_u32(st), al = smem_u32(st + kShA), bs = smem_u32(st + 2 * kShA);
       const uint32_t idesc = idesc_bf16(128, 256, true, true);
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_bf16(tmem, desc_mn(as + kk * 2048), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
+      for (int kk = 0; kk < 4; ++kk) {
+        mma_bf16(tmem, desc_mn(ah + kk * 2048), desc_mn(bs + kk * 2048), idesc, c > 0 || kk > 0);
+        mma_bf16(tmem, desc_mn(al + kk * 2048), desc_mn(bs + kk * 2048), idesc, true);
+      }
     };
-    tma_ring<kStages>(2 * nc, smem, kShStage, full, empty, issue, mma);
+    tma_ring<3>(nc, smem, kFoldStage, full, empty, issue, mma);
   }
   __syncthreads();
   fence_after_sync();
