@@ -67,11 +67,7 @@ using namespace pb::cnn;
 // ---------------------------------------------------------------------------
 // k_slots: one thread per active slot -> (row, batch size, row-id offset)
 // ---------------------------------------------------------------------------
-__global__ void k_slots(Args a, int active) {
-  pb::pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a.timeline && j == 0) a.timeline[a.step] = pb::globaltimer();
-  if (j >= active) return;
+__device__ Slot make_slot(const Args& a, int j) {
   const int r = a.rank[j];
   const int n = a.n[r];
   const int bs = a.bs <= 0 ? n : min(a.bs, n);
@@ -88,7 +84,18 @@ __global__ void k_slots(Args a, int active) {
   // history GEMMs that read whole 32-column chunks see exact zeros there
   // (no per-round memset of the history buffers).
   s.pad_ = a.hlen ? (a.step + 1 == a.epochs * nb ? a.hlen[r] : int64_t(a.step + 1) * a.BS) : 0;
-  a.slots[j] = s;
+  return s;
+}
+
+// Training sweeps compute their slots in k_fwd (make_slot, written back by
+// the CTAs with blockIdx.x == 0 for the later kernels of the sweep); this
+// kernel serves the low-rank switch step, which needs them before k_fwd.
+__global__ void k_slots(Args a, int active) {
+  pb::pdl_wait();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.timeline && j == 0) a.timeline[a.step] = pb::globaltimer();
+  if (j >= active) return;
+  a.slots[j] = make_slot(a, j);
 }
 
 // ---------------------------------------------------------------------------
@@ -148,9 +155,13 @@ constexpr int kSXS = 46;
 constexpr size_t kFwdSmem = kW2Bytes + 2 * kP1Bytes + 256 * kZStride * 4 + 2 * kRawImg + 32 * kSXS * 4 + kC1ABytes +
                             kC1BBytes + (32 + 64) * 4;   // 226,624 B
 
-__global__ void __maxnreg__(112) k_fwd(Args a, int spb) {
+__global__ void __maxnreg__(112) k_fwd(Args a, int spb, int mk_slots) {
   pb::pdl_wait();
-  const Slot sl = a.slots[blockIdx.y];
+  const Slot sl = mk_slots ? make_slot(a, blockIdx.y) : a.slots[blockIdx.y];
+  if (mk_slots && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.slots[blockIdx.y] = sl;   // for the later kernels of the sweep
+    if (a.timeline && blockIdx.y == 0) a.timeline[a.step] = pb::globaltimer();
+  }
   const int i0 = blockIdx.x * spb, i1 = min(sl.cnt, i0 + spb);
   if (i0 >= i1) return;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -2010,7 +2021,8 @@ static void tail_thresholds(int* head, int* wg) {
   *wg = th[1];
 }
 
-static int launch_sweep(Args& a, const ConvMaps* maps, int active, bool train, int max_spb, cudaStream_t s) {
+static int launch_sweep(Args& a, const ConvMaps* maps, int active, bool train, int max_spb, cudaStream_t s,
+                        int mk_slots = 0) {
   int head_thr, wg_thr;
   tail_thresholds(&head_thr, &wg_thr);
   // samples per CTA of the per-sample conv kernels: enough CTAs to fill the
@@ -2023,7 +2035,7 @@ static int launch_sweep(Args& a, const ConvMaps* maps, int active, bool train, i
   pb::prof_begin(pb::K_CNN_FWD, s);
   // grids put a client's CTAs next to each other (slot = blockIdx.y), so the
   // sample-split / tap-split CTAs of one client share its data through L2
-  pb::launch_pdl(k_fwd, dim3(BSpb, active), dim3(kFwdThreads), kFwdSmem, s, 1, a, spb);
+  pb::launch_pdl(k_fwd, dim3(BSpb, active), dim3(kFwdThreads), kFwdSmem, s, 1, a, spb, mk_slots);
   pb::prof_end(pb::K_CNN_FWD, s);
   if (a.hx) {
     int rc = lazy_fc1_sweep(a, active, 0, s);
@@ -2106,10 +2118,13 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
     if (active <= 0) break;
     a.step = step;
     lz.step = step;
-    pb::prof_begin(pb::K_CNN_SLOTS, s);
-    pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
-    pb::prof_end(pb::K_CNN_SLOTS, s);
-    if (sw && step == sw) {
+    const bool switch_step = sw && step == sw;
+    if (switch_step) {   // the switch reads this step's slots before k_fwd
+      pb::prof_begin(pb::K_CNN_SLOTS, s);
+      pb::launch_pdl(k_slots, dim3((active + 127) / 128), dim3(128), 0, s, 1, a, active);
+      pb::prof_end(pb::K_CNN_SLOTS, s);
+    }
+    if (switch_step) {
       // the still-active clients' fc1 after sw steps -> their w rows; from
       // here on they train on the direct kernels (p2 / dH in the workspace)
       if ((rc = lazy_fc1_switch(lz, active, s))) break;
@@ -2117,7 +2132,7 @@ extern "C" int pb_cnn_train_group(const pb_cnn_train_args* args, void* stream) {
       a.hoff = nullptr;
       a.hlen = nullptr;
     }
-    if ((rc = launch_sweep(a, &maps, active, true, spb, s))) break;
+    if ((rc = launch_sweep(a, &maps, active, true, spb, s, switch_step ? 0 : 1))) break;
     if (a.timeline && (step + 1 == t.sweeps || t.active[step + 1] <= 0))
       pb::stamp(a.timeline + step + 1, s);
   }
