@@ -18,11 +18,16 @@ for r in rows:
     unit = r["Metric Unit"]
     ms = v / 1e6 if unit == "ns" else v / 1e3 if unit == "us" else v
     seq.append((name, ms, r["Grid Size"]))
-# sweeps start at k_slots; keep the last round (the last run of consecutive sweeps)
-starts = [i for i, (n, _, _) in enumerate(seq) if n == "k_slots"]
+# sweeps start at k_fwd (k_slots before it at a low-rank switch step, and in
+# captures older than the slots-in-k_fwd change); keep the last round (the
+# last run of consecutive sweeps)
+starts = []
+for i, (n, _, _) in enumerate(seq):
+    if n == "k_slots" or (n == "k_fwd" and not (i > 0 and seq[i - 1][0] == "k_slots")):
+        starts.append(i)
 rounds, cur = [], [starts[0]]
 for a, b in zip(starts, starts[1:]):
-    gap = any(seq[j][0] not in ("k_slots",) and not seq[j][0].startswith("k_") for j in range(a, b))
+    gap = any(not seq[j][0].startswith("k_") for j in range(a, b))
     if gap:
         rounds.append(cur)
         cur = [b]
