@@ -1541,6 +1541,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd_conv(Args a, int spb) {
       if (i > i0) {
         // ---- sample j = i-1: dp1 -> G, conv1 gradients on the tensor cores ----
         const int j = i - 1, set = j & 1, u = j - i0;
+        // the last iteration has no build phase (whose barrier otherwise
+        // separates the previous epilogue's halo reads from this one's writes)
+        if (i == i1 && i - 1 > i0) work_sync();
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int e = tid + k * kBwdWork;
