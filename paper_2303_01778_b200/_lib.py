@@ -7,12 +7,14 @@ every non-zero return code becomes ``NativeError`` carrying pb_last_error().
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
-_PATH = Path(__file__).resolve().parent / "libparrot_b200.so"
+# PB_LIB: an alternative build of the same library (A/B comparisons, tools/ab_round.py)
+_PATH = Path(os.environ.get("PB_LIB") or Path(__file__).resolve().parent / "libparrot_b200.so")
 
 
 class NativeError(RuntimeError):

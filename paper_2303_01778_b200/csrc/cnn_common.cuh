@@ -92,6 +92,10 @@ struct Args {
   int64_t P;
   int32_t C, BS, bs, epochs, step;
   float lr, mu, cg, cc;
+  // lazy fc1 tail sweeps: the forward epilogue (split-K partials + b1 + zp,
+  // relu) left to k_head_tail.  Host: -1 = the head can take it; launch
+  // value: ks of the pending partials (0 = h already final)
+  int32_t epi_ks, epi_active;
 };
 
 __device__ __forceinline__ float sgd(const Args& a, int r, int64_t idx, float w, float g) {

@@ -989,7 +989,10 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       cudaEventRecord(side.join, sg);
       cudaStreamWaitEvent(s, side.join, 0);
     }
-    if (!fuse) {
+    const bool to_head = a.epi_ks < 0;   // the tail head sums the partials itself
+    a.epi_ks = !fuse && to_head ? ks : 0;
+    a.epi_active = active;
+    if (!fuse && !to_head) {
       pb::prof_begin(pb::K_CNN_LZ_FWD, s);
       pb::launch_pdl(k_lz_fwd_epi, dim3(active, kH1 * 8 / kEpiThreads), dim3(kEpiThreads), 0, s, 1, a, active, ks);
       pb::prof_end(pb::K_CNN_LZ_FWD, s);
