@@ -558,6 +558,59 @@ __device__ double block_sum_d(double v, double* scratch) {
   return t;
 }
 
+// lazy fc1 tail of the forward, done by k_head_tail (Args::epi_ks > 0): h rows
+// [4*i4, 4*i4+4) of output o = relu(split-K partials in split order + b1 +
+// the history corrections zp in tile order) -- k_lz_fwd_epi's operations in
+// its order -- into dst[q * ld] and (workspace) a.h.  The loads of an item
+// are in flight together.
+__device__ __forceinline__ void lz_epi_rows(const Args& a, int slot, int o, int i4, int cnt, float* dst, int ld,
+                                            bool to_ws) {
+  const int ks = a.epi_ks, njt = (a.step * a.BS + 127) >> 7;
+  const int64_t kzs = int64_t(a.epi_active) * kH1 * 8, jts = int64_t(kH1) * 8;   // float4 strides
+  const float4* fp = reinterpret_cast<const float4*>(a.fpart + (int64_t(slot) * kH1 + o) * 32) + i4;
+  const float4* zp = reinterpret_cast<const float4*>(a.zp + (int64_t(slot) * njt * kH1 + o) * 32) + i4;
+  float4 p[8];
+#pragma unroll
+  for (int kz = 0; kz < 8; ++kz)
+    if (kz < ks) p[kz] = fp[kz * kzs];
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+  for (int kz = 0; kz < 8; ++kz)
+    if (kz < ks) {
+      v.x += p[kz].x;
+      v.y += p[kz].y;
+      v.z += p[kz].z;
+      v.w += p[kz].w;
+    }
+  const float b = a.w[int64_t(a.slots[slot].r) * a.P + oF1B + o];
+  v.x += b;
+  v.y += b;
+  v.z += b;
+  v.w += b;
+  for (int j0 = 0; j0 < njt; j0 += 8) {
+    float4 z[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < njt) z[u] = zp[(j0 + u) * jts];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < njt) {
+        v.x += z[u].x;
+        v.y += z[u].y;
+        v.z += z[u].z;
+        v.w += z[u].w;
+      }
+  }
+  const float r[4] = {v.x, v.y, v.z, v.w};
+  float* h = a.h + (sidx(slot, 0, a.BS) + i4 * 4) * kH1 + o;   // the workspace keeps h as before
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (i4 * 4 + q < cnt) {
+      dst[q * ld] = relu_nan(r[q]);
+      if (to_ws) h[int64_t(q) * kH1] = dst[q * ld];
+    }
+}
+
 // grid (parts, active): part p owns fc1 outputs [p*512/parts, (p+1)*512/parts)
 // (tail sweeps split a client over 4 CTAs; logits and softmax are recomputed
 // by each part, the bookkeeping and the fc2 bias belong to part 0)
@@ -811,54 +864,10 @@ __global__ void __cluster_dims__(kTailParts, 1, 1) __launch_bounds__(kHeadThread
   const float* W2 = W + oF2W;
   // every global read of the kernel up front: h and fc2 column slices, fc2 bias
   if (a.epi_ks > 0) {
-    // lazy fc1 epilogue of this CTA's 64 outputs (k_lz_fwd_epi's operations
-    // in its order: split-K partials in split order, + b1, + the history
-    // corrections zp in tile order, relu); thread = (o, 4 rows), items of a
-    // thread in flight together
-    const int ks = a.epi_ks, njt = (a.step * BS + 127) >> 7;
-    const int64_t kzs = int64_t(a.epi_active) * kH1 * 32, jts = int64_t(kH1) * 32;
+    // lazy fc1 epilogue of this CTA's 64 outputs (lz_epi_rows)
     for (int e = tid; e < kTailO * 8; e += kHeadThreads) {
-      const int ol = e >> 3, i4 = e & 7, o = olo + ol;
-      if (i4 * 4 >= cnt) continue;
-      const float4* fp = reinterpret_cast<const float4*>(a.fpart + (int64_t(slot) * kH1 + o) * 32) + i4;
-      const float4* zp = reinterpret_cast<const float4*>(a.zp + (int64_t(slot) * njt * kH1 + o) * 32) + i4;
-      float4 p[8];
-#pragma unroll
-      for (int kz = 0; kz < 8; ++kz)
-        if (kz < ks) p[kz] = fp[kz * kzs / 4];
-      float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-      for (int kz = 0; kz < 8; ++kz)
-        if (kz < ks) {
-          v.x += p[kz].x;
-          v.y += p[kz].y;
-          v.z += p[kz].z;
-          v.w += p[kz].w;
-        }
-      const float b = W[oF1B + o];
-      v.x += b;
-      v.y += b;
-      v.z += b;
-      v.w += b;
-      for (int j0 = 0; j0 < njt; j0 += 8) {
-        float4 z[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j0 + u < njt) z[u] = zp[(j0 + u) * jts / 4];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (j0 + u < njt) {
-            v.x += z[u].x;
-            v.y += z[u].y;
-            v.z += z[u].z;
-            v.w += z[u].w;
-          }
-      }
-      const float r[4] = {v.x, v.y, v.z, v.w};
-      float* h = a.h + (sidx(slot, 0, BS) + i4 * 4) * kH1 + o;   // the workspace keeps h as before
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (i4 * 4 + q < cnt) h[int64_t(q) * kH1] = sH[(i4 * 4 + q) * kTailS + ol] = relu_nan(r[q]);
+      const int ol = e >> 3, i4 = e & 7;
+      if (i4 * 4 < cnt) lz_epi_rows(a, slot, olo + ol, i4, cnt, sH + i4 * 4 * kTailS + ol, kTailS, true);
     }
   } else {
     const float* hrow = a.h + sidx(slot, 0, BS) * kH1 + olo;
@@ -2093,6 +2102,8 @@ static int launch_sweep(Args& a, const ConvMaps* maps, int active, bool train, i
   pb::launch_pdl(k_fwd, dim3(BSpb, active), dim3(kFwdThreads), kFwdSmem, s, 1, a, spb, mk_slots);
   pb::prof_end(pb::K_CNN_FWD, s);
   if (a.hx) {
+    // the cluster head takes the lazy fc1 epilogue (each CTA its own outputs;
+    // measured: in the dense head it costs more than the k_lz_fwd_epi launch)
     a.epi_ks = train && active < head_thr ? -1 : 0;
     int rc = lazy_fc1_sweep(a, active, 0, s);
     if (rc) return rc;
