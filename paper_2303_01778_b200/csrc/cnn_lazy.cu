@@ -957,7 +957,17 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
       pb::prof_begin(pb::K_CNN_LZ_GRAM_FWD, sg);
       // sparse sweeps: split K over a cluster while the grid fits one wave
       const int sms = pb::sm_count();
-      const int gks = njt * active * 4 <= sms ? 4 : (njt * active * 2 <= sms ? 2 : 1);
+      static int gks_max = -1;   // cluster size cap (PB_LZ_GKS, 1..8)
+      if (gks_max < 0) {
+        const char* e = std::getenv("PB_LZ_GKS");
+        gks_max = e ? std::max(1, std::min(8, std::atoi(e))) : 4;
+      }
+      int gks = 1;
+      for (int g = gks_max; g >= 2; --g)
+        if (njt * active * g <= sms) {
+          gks = g;
+          break;
+        }
       if (njt * active * gks <= sms)   // one wave at one CTA per SM: the deep ring
         pb::launch_pdl(k_lz_gram<true, 8>, dim3(unsigned(njt * gks), unsigned(active)), dim3(128),
                        gram_smem(true, 8), sg, unsigned(gks), m, a, gks);
