@@ -932,6 +932,17 @@ static int slots_per_cta(int active) {
   return active >= th[0] ? kSh8 : active >= th[1] ? 4 : active >= th[2] ? 2 : 1;
 }
 
+// largest k_lz_bwd grid that takes the 6-stage ring at one CTA per SM
+// (PB_LZ_BWD_DEEP; default one wave) instead of 3 stages at two per SM
+static int bwd_deep_ctas() {
+  static int n = -1;
+  if (n < 0) {
+    const char* e = std::getenv("PB_LZ_BWD_DEEP");
+    n = e ? std::atoi(e) : pb::sm_count();
+  }
+  return n;
+}
+
 int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
   LzMaps& m = *maps_of(a);
   const int njt = njt_of_host(a.step, a.BS);
@@ -1027,7 +1038,7 @@ int lazy_fc1_sweep(Args& a, int active, int phase, cudaStream_t s) {
                        spc, rs);
       else if (spc == kSh8)
         pb::launch_pdl(k_lz_bwd<2, 3>, dim3((kBwKT + 1) / 2, groups), dim3(256), kShSmem, s, 1, m, a, active, spc, rs);
-      else if (kBwKT * int(groups) <= pb::sm_count())
+      else if (kBwKT * int(groups) <= bwd_deep_ctas())
         pb::launch_pdl(k_lz_bwd<1, 6>, dim3(kBwKT, groups), dim3(256), kSh1DeepSmem, s, 1, m, a, active, spc, rs);
       else
         pb::launch_pdl(k_lz_bwd<1, 3>, dim3(kBwKT, groups), dim3(256), kSh1Smem, s, 1, m, a, active, spc, rs);
